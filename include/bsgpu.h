@@ -1,0 +1,203 @@
+/*
+ * bsgpu.h — C-ABI drop-in boundary for the blocksplat (DOGS) hot path on
+ * NVIDIA B200 (sm_100a).
+ *
+ * The reference (/root/reference/proj/core) is a C++ library with no plugin
+ * registry: its operator boundary is the free-function / class API in
+ * renderer.hpp, admm.hpp, trainer.hpp and runtime.hpp. Each entry point below
+ * names the reference interface it replaces (file:line). A host adapter that
+ * keeps the reference signatures calls these (INTEGRATION.md shows it).
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types. Host arrays use the
+ *    reference's own layouts (GaussianCloud SoA, cloud.hpp:41-46; Image
+ *    row-major interleaved RGB, image.hpp:11-25) and FP64, converted at the
+ *    boundary. Device-resident state is FP32 component-major ([D][N]).
+ *  - Every call returns a status (BSG_OK = 0). On failure bsg_last_error()
+ *    returns a thread-local message; BSG_ERR_INVALID_ARGUMENT maps to the
+ *    reference's blocksplat::InvalidArgument, everything else to
+ *    std::runtime_error (errors.hpp:33-36).
+ *  - A context owns one block's state on one device (BlockTrainer is
+ *    single-owner, trainer.hpp:85-87); calls on one context must come from one
+ *    host thread at a time.
+ *  - There is no CPU fallback: creating a context without a usable sm_100
+ *    device fails with BSG_ERR_CUDA.
+ */
+#ifndef BSGPU_H
+#define BSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSG_ABI_VERSION 1
+
+enum bsg_status {
+    BSG_OK = 0,
+    BSG_ERR_INVALID_ARGUMENT = 1, /* blocksplat::InvalidArgument */
+    BSG_ERR_CUDA = 2,             /* CUDA runtime / launch failure */
+    BSG_ERR_NCCL = 3,             /* collective failure */
+    BSG_ERR_STATE = 4,            /* call out of order (e.g. step before init) */
+    BSG_ERR_CAPACITY = 5          /* device buffer capacity exceeded */
+};
+
+/* CameraView (camera.hpp:14-37): x_c = R x_w + t, pixel = (fx X/Z + cx, fy Y/Z + cy).
+ * R is the cached row-major matrix of the stored quaternion (camera.hpp:23-26). */
+typedef struct bsg_camera {
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    uint32_t width, height;
+} bsg_camera;
+
+/* RenderConfig (renderer.hpp:13-21). */
+typedef struct bsg_render_config {
+    double near_plane;         /* 0.01 */
+    double dilation;           /* 0.3 */
+    double alpha_clamp;        /* 0.99 */
+    double transmittance_stop; /* 1e-4 */
+    double sigma_extent;       /* 3.0 */
+    double background[3];      /* 0 */
+    double lambda;             /* 0.2 */
+} bsg_render_config;
+
+/* TrainerConfig device subset (trainer.hpp:13-62). Densification is not on
+ * the device path yet; the host adapter keeps it off. */
+typedef struct bsg_trainer_config {
+    uint64_t iterations;
+    double lr_position, lr_position_decay, lr_rotation, lr_log_scale, lr_features, lr_opacity;
+    double beta1, beta2, eps;
+    bsg_render_config render;
+} bsg_trainer_config;
+
+/* PropertyPenalties (admm.hpp:12-18). */
+typedef struct bsg_penalties {
+    double rho_p, rho_q, rho_s, rho_f, rho_o;
+} bsg_penalties;
+
+typedef struct bsg_ctx bsg_ctx;
+
+/* ---- lifecycle ------------------------------------------------------- */
+int bsg_abi_version(void);
+const char* bsg_last_error(void);
+/* Fills the defaults of renderer.hpp:13-21 / trainer.hpp:13-62 / admm.hpp:12-18. */
+void bsg_default_render_config(bsg_render_config* out);
+void bsg_default_trainer_config(bsg_trainer_config* out);
+void bsg_default_penalties(bsg_penalties* out);
+int bsg_create(int device, int feature_dim, bsg_ctx** out);
+int bsg_destroy(bsg_ctx* ctx);
+
+/* ---- parameters (GaussianCloud, cloud.hpp:32-102) ---------------------- */
+/* Uploads n rows (ids strictly ascending, cloud.cpp:66-74) in the reference
+ * FP64 layout: pos 3n, rot 4n (w,x,y,z), log_scale 3n, features fd*n, opacity
+ * logits n. Resets optimizer moments and densify statistics. */
+int bsg_upload_cloud(bsg_ctx* ctx, size_t n, const uint64_t* ids, const double* pos, const double* rot,
+                     const double* log_scale, const double* features, const double* opacity_logit);
+size_t bsg_cloud_size(const bsg_ctx* ctx);
+int bsg_download_cloud(bsg_ctx* ctx, uint64_t* ids, double* pos, double* rot, double* log_scale, double* features,
+                       double* opacity_logit);
+
+/* ---- rendering (renderer.hpp:71-81) ---------------------------------- */
+/* render(): out_rgb HxWx3, out_transmittance HxW, out_contributors HxW (any may be NULL). */
+int bsg_render(bsg_ctx* ctx, const bsg_camera* cam, const bsg_render_config* cfg, double* out_rgb,
+               double* out_transmittance, uint32_t* out_contributors);
+/* render_backward(): gt HxWx3. out_loss3 = {loss, l1, ssim}. Gradient arrays
+ * have the cloud layouts (culled rows are exactly 0); screen_grad_norm n,
+ * visible n. out_rendered (HxWx3) may be NULL. */
+int bsg_render_backward(bsg_ctx* ctx, const bsg_camera* cam, const double* gt_rgb, const bsg_render_config* cfg,
+                        double* out_loss3, double* g_pos, double* g_rot, double* g_log_scale, double* g_features,
+                        double* g_opacity_logit, double* screen_grad_norm, uint8_t* visible, double* out_rendered);
+
+/* ---- projection / sort introspection (parity of the integer paths) --- */
+/* Per row: visible flag, FP64 depth, footprint rect {x0,x1,y0,y1}; and the
+ * compositing order (rows of visible splats sorted by (depth, index),
+ * renderer.cpp:86-89). out_order must hold n entries; *out_visible_count is V. */
+int bsg_project(bsg_ctx* ctx, const bsg_camera* cam, const bsg_render_config* cfg, uint8_t* out_visible,
+                double* out_depth, int32_t* out_rect, uint32_t* out_order, size_t* out_visible_count);
+/* Tile lists after the tile-key sort: for the last projected camera, the
+ * (tile, row) pairs in sorted order. Pass NULL arrays to query *out_pairs. */
+int bsg_tile_pairs(bsg_ctx* ctx, uint32_t* out_tile, uint32_t* out_row, size_t capacity, size_t* out_pairs);
+
+/* ---- training (BlockTrainer, trainer.hpp:88-149) ---------------------- */
+/* Installs the training views (TrainView, trainer.hpp:80-83): cameras and
+ * ground-truth images (HxWx3 FP64 each), kept resident in HBM as FP32. */
+int bsg_set_views(bsg_ctx* ctx, size_t n_views, const bsg_camera* cams, const double* const* gt_rgb);
+int bsg_trainer_init(bsg_ctx* ctx, const bsg_trainer_config* cfg);
+/* n train_step()s (trainer.cpp:249-295) on resident views view_seq[0..n).
+ * losses (n, nullable) receives render loss + penalty per step. */
+int bsg_train_steps(bsg_ctx* ctx, size_t n, const uint32_t* view_seq, double* losses);
+/* One train_step() whose ground truth comes from host memory (HxWx3 FP32,
+ * pinned or pageable); the copy is part of the step (end-to-end path). */
+int bsg_train_step_host(bsg_ctx* ctx, const bsg_camera* cam, const float* gt_rgb_host, double* loss);
+uint64_t bsg_iteration(const bsg_ctx* ctx);
+/* Optimizer moments, [D][n] component-major FP64 (D = 11 + fd), for parity. */
+int bsg_download_moments(bsg_ctx* ctx, double* m, double* v);
+/* Densify statistics (trainer.cpp:284-289): grad_accum n, grad_seen n. */
+int bsg_download_densify_stats(bsg_ctx* ctx, double* grad_accum, uint32_t* grad_seen);
+
+/* ---- consensus (admm.hpp:47-89, trainer.cpp:161-223, runtime.cpp:482-611) */
+/* Shared rows of this block: anchor j is cloud row rows[j] (ascending ids),
+ * consensus slot slots[j] in [0, n_slots). slot_owners[s] = number of blocks
+ * owning slot s; first_owner[j] = 1 if this block is the lowest owner of
+ * slots[j] (admm.cpp:56-67 visits owners in ascending block id). */
+int bsg_set_shared(bsg_ctx* ctx, size_t n_shared, const uint32_t* rows, const uint32_t* slots,
+                   const uint8_t* first_owner, size_t n_slots, const uint32_t* slot_owners);
+/* set_anchor (trainer.cpp:161-166): z for this block's shared rows (n_shared
+ * x D, reference row layout), duals := 0, and z_prev for every slot
+ * (n_slots x D) as the master's z_prev (runtime.cpp:465). */
+int bsg_set_anchor(bsg_ctx* ctx, const double* z_rows, const double* z_prev_slots, const bsg_penalties* rho);
+int bsg_set_penalties(bsg_ctx* ctx, const bsg_penalties* rho);
+int bsg_download_duals(bsg_ctx* ctx, double* u_rows);
+int bsg_download_anchor(bsg_ctx* ctx, double* z_rows);
+/* Consensus z over all slots (n_slots x D) after the last round. */
+int bsg_download_consensus(bsg_ctx* ctx, double* z_slots);
+
+typedef struct bsg_round_args {
+    double alpha;          /* over-relaxation (admm.hpp:25) */
+    int relax;             /* enabled && alpha != 1 && !final (runtime.cpp:530) */
+    size_t n_reset;        /* extra reset slots from ownership edits (runtime.cpp:506-512) */
+    const uint32_t* reset_slots;
+    int diagnostics;       /* also compute max_disagreement and dual-mean L-inf */
+} bsg_round_args;
+
+typedef struct bsg_round_result {
+    double primal;          /* admm.cpp:147-198 */
+    double dual;
+    double max_disagreement;/* admm.cpp:219-243 (diagnostics only) */
+    double dual_mean_linf;  /* runtime.cpp:572-606 (diagnostics only) */
+    uint64_t flipped;       /* slots whose quaternion needed a sign flip */
+    double ms;              /* device time of the round on this block */
+} bsg_round_result;
+
+/* Multi-process / multi-GPU collective (one rank per block, NCCL over NVLink). */
+int bsg_nccl_unique_id(uint8_t out_id[128]);
+int bsg_comm_init(bsg_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+int bsg_consensus_round(bsg_ctx* ctx, const bsg_round_args* args, bsg_round_result* out);
+
+/* Single-process group: k contexts (any devices) reduced in ascending block
+ * order without NCCL; runs one round for all of them. */
+int bsg_group_consensus_round(bsg_ctx* const* ctxs, size_t k, const bsg_round_args* args, bsg_round_result* out);
+
+/* ---- measurement ------------------------------------------------------ */
+/* Per-stage device times of the most recent step (CUDA events on the
+ * context's stream), milliseconds, in the order of bsg_stage_name(i). */
+int bsg_enable_stage_timing(bsg_ctx* ctx, int enable);
+int bsg_stage_count(void);
+const char* bsg_stage_name(int i);
+int bsg_stage_times(bsg_ctx* ctx, double* ms);
+/* Counters of the most recent step: visible splats V, tile pairs P, kernels launched. */
+int bsg_step_counters(bsg_ctx* ctx, uint64_t* visible, uint64_t* pairs, uint64_t* launches);
+/* Kernel launches since context creation (all entry points). */
+uint64_t bsg_launch_count(const bsg_ctx* ctx);
+/* Opaque cudaStream_t of the context (for event timing by the caller). */
+void* bsg_stream(bsg_ctx* ctx);
+int bsg_synchronize(bsg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSGPU_H */

@@ -1,0 +1,426 @@
+"""ctypes binding of the C-ABI in include/bsgpu.h (libbsgpu.so).
+
+This is the Python mirror of the reference's operator surface for the hot
+path: `Block` wraps one bsg context (one BlockTrainer's device state,
+trainer.hpp:88-149) and exposes render / render_backward (renderer.hpp:71-81),
+train_step (trainer.cpp:249-295) and the consensus round (admm.hpp:47-89).
+There is no CPU fallback: if libbsgpu.so is missing or no sm_100 device is
+present, construction raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libbsgpu.so")
+
+BSG_OK = 0
+BSG_ERR_INVALID_ARGUMENT = 1
+
+
+class BsgError(RuntimeError):
+    """std::runtime_error analogue (errors.hpp)."""
+
+
+class InvalidArgument(ValueError):
+    """blocksplat::InvalidArgument (errors.hpp:33-36)."""
+
+
+class bsg_camera(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3), ("width", ctypes.c_uint32),
+                ("height", ctypes.c_uint32)]
+
+
+class bsg_render_config(ctypes.Structure):
+    _fields_ = [("near_plane", ctypes.c_double), ("dilation", ctypes.c_double), ("alpha_clamp", ctypes.c_double),
+                ("transmittance_stop", ctypes.c_double), ("sigma_extent", ctypes.c_double),
+                ("background", ctypes.c_double * 3), ("lambda_", ctypes.c_double)]
+
+
+class bsg_trainer_config(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_uint64), ("lr_position", ctypes.c_double),
+                ("lr_position_decay", ctypes.c_double), ("lr_rotation", ctypes.c_double),
+                ("lr_log_scale", ctypes.c_double), ("lr_features", ctypes.c_double), ("lr_opacity", ctypes.c_double),
+                ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("eps", ctypes.c_double),
+                ("render", bsg_render_config)]
+
+
+class bsg_penalties(ctypes.Structure):
+    _fields_ = [("rho_p", ctypes.c_double), ("rho_q", ctypes.c_double), ("rho_s", ctypes.c_double),
+                ("rho_f", ctypes.c_double), ("rho_o", ctypes.c_double)]
+
+
+class bsg_round_args(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("relax", ctypes.c_int), ("n_reset", ctypes.c_size_t),
+                ("reset_slots", ctypes.POINTER(ctypes.c_uint32)), ("diagnostics", ctypes.c_int)]
+
+
+class bsg_round_result(ctypes.Structure):
+    _fields_ = [("primal", ctypes.c_double), ("dual", ctypes.c_double), ("max_disagreement", ctypes.c_double),
+                ("dual_mean_linf", ctypes.c_double), ("flipped", ctypes.c_uint64), ("ms", ctypes.c_double)]
+
+
+# (name, restype, argtypes) for every symbol declared in include/bsgpu.h.
+_P = ctypes.c_void_p
+_DP = ctypes.POINTER(ctypes.c_double)
+_U32P = ctypes.POINTER(ctypes.c_uint32)
+_U64P = ctypes.POINTER(ctypes.c_uint64)
+_U8P = ctypes.POINTER(ctypes.c_uint8)
+_FP = ctypes.POINTER(ctypes.c_float)
+_SZ = ctypes.c_size_t
+_SZP = ctypes.POINTER(ctypes.c_size_t)
+SYMBOLS = [
+    ("bsg_abi_version", ctypes.c_int, []),
+    ("bsg_last_error", ctypes.c_char_p, []),
+    ("bsg_default_render_config", None, [ctypes.POINTER(bsg_render_config)]),
+    ("bsg_default_trainer_config", None, [ctypes.POINTER(bsg_trainer_config)]),
+    ("bsg_default_penalties", None, [ctypes.POINTER(bsg_penalties)]),
+    ("bsg_create", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    ("bsg_destroy", ctypes.c_int, [_P]),
+    ("bsg_upload_cloud", ctypes.c_int, [_P, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP]),
+    ("bsg_cloud_size", _SZ, [_P]),
+    ("bsg_download_cloud", ctypes.c_int, [_P, _U64P, _DP, _DP, _DP, _DP, _DP]),
+    ("bsg_render", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), ctypes.POINTER(bsg_render_config), _DP, _DP, _U32P]),
+    ("bsg_render_backward", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _DP, ctypes.POINTER(bsg_render_config), _DP,
+                                            _DP, _DP, _DP, _DP, _DP, _DP, _U8P, _DP]),
+    ("bsg_project", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), ctypes.POINTER(bsg_render_config), _U8P, _DP,
+                                    ctypes.POINTER(ctypes.c_int32), _U32P, _SZP]),
+    ("bsg_tile_pairs", ctypes.c_int, [_P, _U32P, _U32P, _SZ, _SZP]),
+    ("bsg_set_views", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_DP)]),
+    ("bsg_trainer_init", ctypes.c_int, [_P, ctypes.POINTER(bsg_trainer_config)]),
+    ("bsg_train_steps", ctypes.c_int, [_P, _SZ, _U32P, _DP]),
+    ("bsg_train_step_host", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _FP, _DP]),
+    ("bsg_iteration", ctypes.c_uint64, [_P]),
+    ("bsg_download_moments", ctypes.c_int, [_P, _DP, _DP]),
+    ("bsg_download_densify_stats", ctypes.c_int, [_P, _DP, _U32P]),
+    ("bsg_set_shared", ctypes.c_int, [_P, _SZ, _U32P, _U32P, _U8P, _SZ, _U32P]),
+    ("bsg_set_anchor", ctypes.c_int, [_P, _DP, _DP, ctypes.POINTER(bsg_penalties)]),
+    ("bsg_set_penalties", ctypes.c_int, [_P, ctypes.POINTER(bsg_penalties)]),
+    ("bsg_download_duals", ctypes.c_int, [_P, _DP]),
+    ("bsg_download_anchor", ctypes.c_int, [_P, _DP]),
+    ("bsg_download_consensus", ctypes.c_int, [_P, _DP]),
+    ("bsg_nccl_unique_id", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
+    ("bsg_comm_init", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int]),
+    ("bsg_consensus_round", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_round_result)]),
+    ("bsg_group_consensus_round", ctypes.c_int, [ctypes.POINTER(_P), _SZ, ctypes.POINTER(bsg_round_args),
+                                                  ctypes.POINTER(bsg_round_result)]),
+    ("bsg_enable_stage_timing", ctypes.c_int, [_P, ctypes.c_int]),
+    ("bsg_stage_count", ctypes.c_int, []),
+    ("bsg_stage_name", ctypes.c_char_p, [ctypes.c_int]),
+    ("bsg_stage_times", ctypes.c_int, [_P, _DP]),
+    ("bsg_step_counters", ctypes.c_int, [_P, _U64P, _U64P, _U64P]),
+    ("bsg_launch_count", ctypes.c_uint64, [_P]),
+    ("bsg_stream", _P, [_P]),
+    ("bsg_synchronize", ctypes.c_int, [_P]),
+]
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Loads libbsgpu.so and binds every symbol; raises if anything is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise BsgError(f"{path} not built (run __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+    for name, res, args in SYMBOLS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(status):
+    if status == BSG_OK:
+        return
+    msg = _lib.bsg_last_error().decode()
+    if status == BSG_ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    raise BsgError(f"bsg status {status}: {msg}")
+
+
+def _ptr(a, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype)) if a is not None else None
+
+
+def make_camera(fx, fy, cx, cy, R, t, width, height):
+    c = bsg_camera()
+    c.fx, c.fy, c.cx, c.cy = float(fx), float(fy), float(cx), float(cy)
+    R = np.asarray(R, dtype=np.float64).reshape(9)
+    for k in range(9):
+        c.R[k] = R[k]
+    for k in range(3):
+        c.t[k] = float(t[k])
+    c.width, c.height = int(width), int(height)
+    return c
+
+
+def render_config(**kw):
+    load_library()
+    r = bsg_render_config()
+    _lib.bsg_default_render_config(ctypes.byref(r))
+    for k, v in kw.items():
+        if k == "background":
+            for i in range(3):
+                r.background[i] = v[i]
+        elif k == "lambda_" or k == "lam":
+            r.lambda_ = v
+        else:
+            setattr(r, k, v)
+    return r
+
+
+def trainer_config(**kw):
+    load_library()
+    t = bsg_trainer_config()
+    _lib.bsg_default_trainer_config(ctypes.byref(t))
+    for k, v in kw.items():
+        setattr(t, k, v)
+    return t
+
+
+def penalties(**kw):
+    load_library()
+    p = bsg_penalties()
+    _lib.bsg_default_penalties(ctypes.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape is not None else a
+
+
+class Block:
+    """One block's device state (BlockTrainer, trainer.hpp:88-149) on one GPU."""
+
+    def __init__(self, device=0, feature_dim=3):
+        load_library()
+        self.fd = feature_dim
+        self.D = 11 + feature_dim
+        h = ctypes.c_void_p()
+        _check(_lib.bsg_create(device, feature_dim, ctypes.byref(h)))
+        self.h = h
+        self.n = 0
+        self.n_shared = 0
+        self.n_slots = 0
+
+    def close(self):
+        if self.h:
+            _lib.bsg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- parameters ----------------------------------------------------
+    def upload_cloud(self, ids, pos, rot, ls, feat, op):
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        n = len(ids)
+        pos, rot, ls = _f64(pos).reshape(n, 3), _f64(rot).reshape(n, 4), _f64(ls).reshape(n, 3)
+        feat, op = _f64(feat).reshape(n, self.fd), _f64(op).reshape(n)
+        _check(_lib.bsg_upload_cloud(self.h, n, _ptr(ids, ctypes.c_uint64), _ptr(pos, ctypes.c_double),
+                                     _ptr(rot, ctypes.c_double), _ptr(ls, ctypes.c_double),
+                                     _ptr(feat, ctypes.c_double), _ptr(op, ctypes.c_double)))
+        self.n = n
+
+    def download_cloud(self):
+        n = self.n
+        ids = np.zeros(n, np.uint64)
+        pos, rot, ls = np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3))
+        feat, op = np.zeros((n, self.fd)), np.zeros(n)
+        _check(_lib.bsg_download_cloud(self.h, _ptr(ids, ctypes.c_uint64), _ptr(pos, ctypes.c_double),
+                                       _ptr(rot, ctypes.c_double), _ptr(ls, ctypes.c_double),
+                                       _ptr(feat, ctypes.c_double), _ptr(op, ctypes.c_double)))
+        return dict(ids=ids, pos=pos, rot=rot, ls=ls, feat=feat, op=op)
+
+    # ---- rendering -----------------------------------------------------
+    def render(self, cam, cfg=None):
+        H, W = cam.height, cam.width
+        rgb, T, n = np.zeros((H, W, 3)), np.zeros((H, W)), np.zeros((H, W), np.uint32)
+        _check(_lib.bsg_render(self.h, ctypes.byref(cam), ctypes.byref(cfg) if cfg else None,
+                               _ptr(rgb, ctypes.c_double), _ptr(T, ctypes.c_double), _ptr(n, ctypes.c_uint32)))
+        return rgb, T, n
+
+    def render_backward(self, cam, gt, cfg=None):
+        H, W = cam.height, cam.width
+        gt = _f64(gt)
+        if gt.shape != (H, W, 3):
+            raise InvalidArgument("image dimension mismatch")
+        n = self.n
+        loss3 = np.zeros(3)
+        g = dict(g_pos=np.zeros((n, 3)), g_rot=np.zeros((n, 4)), g_ls=np.zeros((n, 3)), g_feat=np.zeros((n, self.fd)),
+                 g_op=np.zeros(n))
+        sgn, vis, rend = np.zeros(n), np.zeros(n, np.uint8), np.zeros((H, W, 3))
+        _check(_lib.bsg_render_backward(self.h, ctypes.byref(cam), _ptr(gt, ctypes.c_double),
+                                        ctypes.byref(cfg) if cfg else None, _ptr(loss3, ctypes.c_double),
+                                        *[_ptr(g[k], ctypes.c_double) for k in ("g_pos", "g_rot", "g_ls", "g_feat", "g_op")],
+                                        _ptr(sgn, ctypes.c_double), _ptr(vis, ctypes.c_uint8),
+                                        _ptr(rend, ctypes.c_double)))
+        g.update(loss=loss3[0], l1=loss3[1], ssim=loss3[2], screen_grad_norm=sgn, visible=vis, rendered=rend)
+        return g
+
+    def project(self, cam, cfg=None):
+        n = self.n
+        vis, depth = np.zeros(n, np.uint8), np.zeros(n)
+        rect = np.zeros((n, 4), np.int32)
+        order = np.zeros(max(n, 1), np.uint32)
+        V = ctypes.c_size_t()
+        _check(_lib.bsg_project(self.h, ctypes.byref(cam), ctypes.byref(cfg) if cfg else None,
+                                _ptr(vis, ctypes.c_uint8), _ptr(depth, ctypes.c_double),
+                                _ptr(rect, ctypes.c_int32), _ptr(order, ctypes.c_uint32), ctypes.byref(V)))
+        return dict(visible=vis, depth=depth, rect=rect, order=order[:V.value].astype(np.int64))
+
+    def tile_pairs(self):
+        P = ctypes.c_size_t()
+        _check(_lib.bsg_tile_pairs(self.h, None, None, 0, ctypes.byref(P)))
+        tile, row = np.zeros(max(P.value, 1), np.uint32), np.zeros(max(P.value, 1), np.uint32)
+        _check(_lib.bsg_tile_pairs(self.h, _ptr(tile, ctypes.c_uint32), _ptr(row, ctypes.c_uint32), len(tile),
+                                   ctypes.byref(P)))
+        return tile[:P.value], row[:P.value]
+
+    # ---- training ------------------------------------------------------
+    def set_views(self, cams, gts):
+        arr = (bsg_camera * len(cams))(*cams)
+        self._gts = [_f64(g) for g in gts]
+        ptrs = (_DP * len(cams))(*[_ptr(g, ctypes.c_double) for g in self._gts])
+        _check(_lib.bsg_set_views(self.h, len(cams), arr, ptrs))
+        self._gts = None
+
+    def trainer_init(self, cfg=None):
+        _check(_lib.bsg_trainer_init(self.h, ctypes.byref(cfg) if cfg else None))
+
+    def train_steps(self, view_seq, want_losses=True):
+        seq = np.ascontiguousarray(view_seq, dtype=np.uint32)
+        losses = np.zeros(len(seq)) if want_losses else None
+        _check(_lib.bsg_train_steps(self.h, len(seq), _ptr(seq, ctypes.c_uint32), _ptr(losses, ctypes.c_double)))
+        return losses
+
+    def train_step_host(self, cam, gt_f32):
+        loss = ctypes.c_double()
+        _check(_lib.bsg_train_step_host(self.h, ctypes.byref(cam), _ptr(gt_f32, ctypes.c_float), ctypes.byref(loss)))
+        return loss.value
+
+    def iteration(self):
+        return _lib.bsg_iteration(self.h)
+
+    def moments(self):
+        m, v = np.zeros((self.D, self.n)), np.zeros((self.D, self.n))
+        _check(_lib.bsg_download_moments(self.h, _ptr(m, ctypes.c_double), _ptr(v, ctypes.c_double)))
+        return m, v
+
+    def densify_stats(self):
+        a, s = np.zeros(self.n), np.zeros(self.n, np.uint32)
+        _check(_lib.bsg_download_densify_stats(self.h, _ptr(a, ctypes.c_double), _ptr(s, ctypes.c_uint32)))
+        return a, s
+
+    # ---- consensus -----------------------------------------------------
+    def set_shared(self, rows, slots, first_owner, slot_owners):
+        rows = np.ascontiguousarray(rows, np.uint32)
+        slots = np.ascontiguousarray(slots, np.uint32)
+        first = np.ascontiguousarray(first_owner, np.uint8)
+        owners = np.ascontiguousarray(slot_owners, np.uint32)
+        _check(_lib.bsg_set_shared(self.h, len(rows), _ptr(rows, ctypes.c_uint32), _ptr(slots, ctypes.c_uint32),
+                                   _ptr(first, ctypes.c_uint8), len(owners), _ptr(owners, ctypes.c_uint32)))
+        self.n_shared, self.n_slots = len(rows), len(owners)
+
+    def set_anchor(self, z_rows, zprev_slots, rho):
+        z = _f64(z_rows).reshape(self.n_shared, self.D)
+        zp = _f64(zprev_slots).reshape(self.n_slots, self.D) if zprev_slots is not None else None
+        _check(_lib.bsg_set_anchor(self.h, _ptr(z, ctypes.c_double), _ptr(zp, ctypes.c_double), ctypes.byref(rho)))
+
+    def set_penalties(self, rho):
+        _check(_lib.bsg_set_penalties(self.h, ctypes.byref(rho)))
+
+    def duals(self):
+        u = np.zeros((self.n_shared, self.D))
+        _check(_lib.bsg_download_duals(self.h, _ptr(u, ctypes.c_double)))
+        return u
+
+    def anchor(self):
+        z = np.zeros((self.n_shared, self.D))
+        _check(_lib.bsg_download_anchor(self.h, _ptr(z, ctypes.c_double)))
+        return z
+
+    def consensus(self):
+        z = np.zeros((self.n_slots, self.D))
+        _check(_lib.bsg_download_consensus(self.h, _ptr(z, ctypes.c_double)))
+        return z
+
+    def comm_init(self, uid, nranks, rank):
+        buf = (ctypes.c_uint8 * 128)(*uid)
+        _check(_lib.bsg_comm_init(self.h, buf, nranks, rank))
+
+    def consensus_round(self, alpha, relax, reset_slots=(), diagnostics=False):
+        a = _round_args(alpha, relax, reset_slots, diagnostics)
+        r = bsg_round_result()
+        _check(_lib.bsg_consensus_round(self.h, ctypes.byref(a), ctypes.byref(r)))
+        return _round_dict(r)
+
+    # ---- measurement ---------------------------------------------------
+    def enable_stage_timing(self, on=True):
+        _check(_lib.bsg_enable_stage_timing(self.h, 1 if on else 0))
+
+    def stage_times(self):
+        k = _lib.bsg_stage_count()
+        ms = np.zeros(k)
+        _check(_lib.bsg_stage_times(self.h, _ptr(ms, ctypes.c_double)))
+        return {_lib.bsg_stage_name(i).decode(): ms[i] for i in range(k)}
+
+    def step_counters(self):
+        v, p, l = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.bsg_step_counters(self.h, ctypes.byref(v), ctypes.byref(p), ctypes.byref(l)))
+        return dict(visible=v.value, pairs=p.value, launches=l.value)
+
+    def launch_count(self):
+        return _lib.bsg_launch_count(self.h)
+
+    def stream(self):
+        return _lib.bsg_stream(self.h)
+
+    def synchronize(self):
+        _check(_lib.bsg_synchronize(self.h))
+
+
+def _round_args(alpha, relax, reset_slots, diagnostics):
+    a = bsg_round_args()
+    a.alpha = float(alpha)
+    a.relax = 1 if relax else 0
+    rs = np.ascontiguousarray(reset_slots, np.uint32)
+    a.n_reset = len(rs)
+    a._keep = rs
+    a.reset_slots = _ptr(rs, ctypes.c_uint32) if len(rs) else None
+    a.diagnostics = 1 if diagnostics else 0
+    return a
+
+
+def _round_dict(r):
+    return dict(primal=r.primal, dual=r.dual, max_disagreement=r.max_disagreement,
+                dual_mean_linf=r.dual_mean_linf, flipped=r.flipped, ms=r.ms)
+
+
+def group_consensus_round(blocks, alpha, relax, reset_slots=(), diagnostics=False):
+    """One consensus round over blocks held by this process (ascending block id)."""
+    load_library()
+    hs = (_P * len(blocks))(*[b.h.value for b in blocks])
+    a = _round_args(alpha, relax, reset_slots, diagnostics)
+    r = bsg_round_result()
+    _check(_lib.bsg_group_consensus_round(hs, len(blocks), ctypes.byref(a), ctypes.byref(r)))
+    return _round_dict(r)
+
+
+def nccl_unique_id():
+    load_library()
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.bsg_nccl_unique_id(buf))
+    return bytes(buf)

@@ -1,0 +1,1102 @@
+// C-ABI (include/bsgpu.h): contexts, device buffers, the per-step pipeline and
+// the consensus round. Host code only; kernels live in the other .cu files.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "bsg_internal.cuh"
+
+namespace bsg {
+
+namespace {
+thread_local std::string g_err;
+
+// NCCL is resolved at run time (dlopen) so that the library never pins a
+// libnccl.so.2 of its own: inside a PyTorch process the already-loaded copy
+// (RTLD_NOLOAD) is reused, otherwise the system one is loaded on first use.
+struct NcclApi {
+    bool ready = false;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+    static NcclApi api;
+    if (api.ready) return api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw std::runtime_error(std::string("cannot load libnccl.so.2: ") + dlerror());
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy || !api.error_string)
+        throw std::runtime_error("libnccl.so.2 lacks a required symbol");
+    api.ready = true;
+    return api;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return BSG_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return BSG_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return BSG_ERR_CUDA;
+    }
+}
+
+void invalid(const std::string& m) { throw Error{BSG_ERR_INVALID_ARGUMENT, m}; }
+
+template <typename T>
+void dev_alloc(T** p, size_t count) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (count == 0) count = 1;
+    BSG_CUDA(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+}
+
+void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
+
+void free_all(Ctx* c) {
+    void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d,
+                    c->anchor_of_row, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->pkey[0],
+                    c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
+                    c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
+                    c->ssim_f, c->gt_stage, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
+                    c->in_zprev, c->slot_owners, c->pack, c->qref, c->slot_reset, c->round_scalars};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (float* p : c->view_gt)
+        if (p) cudaFree(p);
+    if (c->counters_host) cudaFreeHost(c->counters_host);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->nccl) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl));
+    if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+void check_camera(const bsg_camera* cam) {
+    if (!cam) invalid("null camera");
+    if (cam->width == 0 || cam->height == 0) invalid("camera has zero size");
+    if (cam->width > 32767 || cam->height > 32767) invalid("camera larger than 32767 px");
+}
+
+void alloc_rows(Ctx* c, size_t n) {
+    const size_t cap = std::max<size_t>(n, 1);
+    dev_alloc(&c->x, c->D * cap);
+    dev_alloc(&c->m, c->D * cap);
+    dev_alloc(&c->v, c->D * cap);
+    dev_alloc(&c->grad_accum, cap);
+    dev_alloc(&c->grad_seen, cap);
+    dev_alloc(&c->rec, 3 * cap);
+    dev_alloc(&c->depth_key, cap);
+    dev_alloc(&c->tiles, cap);
+    dev_alloc(&c->g2d, 3 * cap);
+    dev_alloc(&c->anchor_of_row, cap);
+    dev_alloc(&c->vkey[0], cap);
+    dev_alloc(&c->vkey[1], cap);
+    dev_alloc(&c->vrow[0], cap);
+    dev_alloc(&c->vrow[1], cap);
+    dev_alloc(&c->poff, cap);
+    c->cap = cap;
+}
+
+// Host FP64 reference layout -> device FP32 [D][cap].
+void upload_params(Ctx* c, const double* pos, const double* rot, const double* ls, const double* feat,
+                   const double* op) {
+    const size_t n = c->n, cap = c->cap;
+    std::vector<float> h(static_cast<size_t>(c->D) * cap, 0.f);
+    for (size_t i = 0; i < n; ++i) {
+        for (int k = 0; k < 3; ++k) h[(kPos + k) * cap + i] = static_cast<float>(pos[3 * i + k]);
+        for (int k = 0; k < 4; ++k) h[(kRot + k) * cap + i] = static_cast<float>(rot[4 * i + k]);
+        for (int k = 0; k < 3; ++k) h[(kLs + k) * cap + i] = static_cast<float>(ls[3 * i + k]);
+        for (int k = 0; k < c->fd; ++k) h[(kFeat + k) * cap + i] = static_cast<float>(feat[i * c->fd + k]);
+        h[op_comp(c->fd) * cap + i] = static_cast<float>(op[i]);
+    }
+    BSG_CUDA(cudaMemcpyAsync(c->x, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// Row-layout (reference bundle) FP64 <-> component-major FP32 for n rows.
+std::vector<float> rows_to_cm(const double* rows, size_t n, int D) {
+    std::vector<float> h(static_cast<size_t>(D) * std::max<size_t>(n, 1), 0.f);
+    for (size_t i = 0; i < n; ++i)
+        for (int c = 0; c < D; ++c) h[c * n + i] = static_cast<float>(rows[i * D + c]);
+    return h;
+}
+
+void cm_to_rows(const float* cm, size_t n, int D, double* rows) {
+    for (size_t i = 0; i < n; ++i)
+        for (int c = 0; c < D; ++c) rows[i * D + c] = cm[c * n + i];
+}
+
+// D-component row of the reference bundle order: pos3 rot4 ls3 feat fd op1 —
+// identical to the device component order, so a "row" is just D values.
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+void stage_begin(Ctx* c, int stage) {
+    if (c->stage_timing) BSG_CUDA(cudaEventRecord(c->ev[stage], c->stream));
+}
+void stage_end(Ctx* c, int stage) {
+    if (c->stage_timing) BSG_CUDA(cudaEventRecord(c->ev[stage + 1], c->stream));
+}
+
+void ensure_image_buffers(Ctx* c, int W, int H) {
+    const size_t px = static_cast<size_t>(W) * H;
+    if (px > c->img_cap) {
+        dev_alloc(&c->out_rgb, 3 * px);
+        dev_alloc(&c->out_T, px);
+        dev_alloc(&c->out_n, px);
+        dev_alloc(&c->out_last, px);
+        dev_alloc(&c->dl_dc, 3 * px);
+        dev_alloc(&c->ssim_f, 9 * px);
+        dev_alloc(&c->gt_stage, 3 * px);
+        c->img_cap = px;
+    }
+    const size_t ntiles = static_cast<size_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    if (ntiles > c->ranges_cap) {
+        dev_alloc(&c->ranges, ntiles);
+        c->ranges_cap = ntiles;
+    }
+}
+
+void ensure_pair_capacity(Ctx* c, size_t P) {
+    if (P <= c->pcap) return;
+    const size_t cap = P + P / 4 + 1024;
+    for (int k = 0; k < 2; ++k) {
+        dev_alloc(&c->pkey[k], cap);
+        dev_alloc(&c->pval[k], cap);
+    }
+    c->pcap = cap;
+}
+
+namespace {
+
+int tile_bits(const DevCam& cam) {
+    const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
+    int b = 1;
+    while ((1u << b) < ntiles) ++b;
+    return b;
+}
+
+// K1-K5: projection, compaction, depth sort, pair emission, tile sort, ranges.
+void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
+    ensure_image_buffers(c, cam.W, cam.H);
+    stage_begin(c, kStPreprocess);
+    launch_preprocess(c, cam, rc);
+    stage_end(c, kStPreprocess);
+    stage_begin(c, kStCompact);
+    compact_visible(c, static_cast<uint32_t>(c->n));
+    stage_end(c, kStCompact);
+    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(StepCounters), cudaMemcpyDeviceToHost, c->stream));
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+    const uint32_t V = c->counters_host->visible;
+    stage_begin(c, kStDepthSort);
+    // (depth, index) order: stable LSD sort of the FP64 depth bits over rows in
+    // ascending index order (renderer.cpp:86-89). Positive doubles order as u64.
+    radix_sort_u64(c, c->vkey, c->vrow, V, 0, 64, &c->depth_sorted);
+    stage_end(c, kStDepthSort);
+    stage_begin(c, kStPairs);
+    scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
+    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(StepCounters), cudaMemcpyDeviceToHost, c->stream));
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+    const uint32_t P = V ? c->counters_host->pairs : 0;
+    ensure_pair_capacity(c, P);
+    launch_pairs(c, cam, V);
+    stage_end(c, kStPairs);
+    stage_begin(c, kStTileSort);
+    radix_sort_u32(c, c->pkey, c->pval, P, 0, tile_bits(cam), &c->pairs_sorted);
+    stage_end(c, kStTileSort);
+    stage_begin(c, kStRanges);
+    launch_ranges(c, cam, P);
+    stage_end(c, kStRanges);
+    c->last_counters.visible = V;
+    c->last_counters.pairs = P;
+}
+
+float* upload_gt_f64(Ctx* c, const double* gt, size_t px) {
+    std::vector<float> h(3 * px);
+    for (size_t i = 0; i < 3 * px; ++i) h[i] = static_cast<float>(gt[i]);
+    BSG_CUDA(cudaMemcpyAsync(c->gt_stage, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+    return c->gt_stage;
+}
+
+void collect_stage_times(Ctx* c) {
+    if (!c->stage_timing) return;
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+    for (int s = 0; s < kStCount; ++s) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->ev[s], c->ev[s + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            ms = 0.f;
+        }
+        c->stage_ms[s] = ms;
+    }
+}
+
+AdamStep make_adam_step(Ctx* c) {
+    AdamStep st{};
+    const bsg_trainer_config& t = c->tcfg;
+    const uint64_t step = ++c->adam_t;  // trainer.cpp:267
+    const double progress = t.iterations > 0 ? static_cast<double>(c->iteration) / static_cast<double>(t.iterations) : 0.0;
+    const double lr_pos = t.lr_position * std::pow(t.lr_position_decay, progress);  // trainer.cpp:268-271
+    const double bc1 = 1.0 - std::pow(t.beta1, static_cast<double>(step));
+    const double bc2 = 1.0 - std::pow(t.beta2, static_cast<double>(step));
+    for (int k = 0; k < c->D; ++k) {
+        double lr = t.lr_features, rho = c->rho.rho_f;
+        if (k < kRot) { lr = lr_pos; rho = c->rho.rho_p; }
+        else if (k < kLs) { lr = t.lr_rotation; rho = c->rho.rho_q; }
+        else if (k < kFeat) { lr = t.lr_log_scale; rho = c->rho.rho_s; }
+        else if (k == op_comp(c->fd)) { lr = t.lr_opacity; rho = c->rho.rho_o; }
+        st.lr[k] = static_cast<float>(lr);
+        st.rho[k] = static_cast<float>(rho);
+    }
+    st.b1 = static_cast<float>(t.beta1);
+    st.b2 = static_cast<float>(t.beta2);
+    st.omb1 = static_cast<float>(1.0 - t.beta1);
+    st.omb2 = static_cast<float>(1.0 - t.beta2);
+    st.eps = static_cast<float>(t.eps);
+    st.inv_bc1 = static_cast<float>(1.0 / bc1);
+    st.inv_bc2 = static_cast<float>(1.0 / bc2);
+    st.has_anchor = (c->anchored && c->n_shared > 0) ? 1 : 0;
+    return st;
+}
+
+// One train_step (trainer.cpp:249-295) on a device-resident ground truth.
+void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev) {
+    c->step_launches = 0;
+    const DevCam cam = make_cam(view);
+    const DevRender rc = make_render(c->tcfg.render);
+    BSG_CUDA(cudaMemsetAsync(c->scalars, 0, sizeof(StepScalars), c->stream));
+    project_and_bin(c, cam, rc);
+    stage_begin(c, kStBlendFwd);
+    launch_blend_fwd(c, cam, rc);
+    stage_end(c, kStBlendFwd);
+    stage_begin(c, kStLoss);
+    launch_loss(c, cam, rc, gt);
+    stage_end(c, kStLoss);
+    stage_begin(c, kStBlendBwd);
+    launch_blend_bwd(c, cam, rc);
+    stage_end(c, kStBlendBwd);
+    stage_begin(c, kStAdam);
+    const AdamStep st = make_adam_step(c);
+    launch_adam(c, cam, st, loss_dev, 0);
+    stage_end(c, kStAdam);
+    launch_finalize_loss(c, cam, rc, loss_dev, st.has_anchor != 0);
+    c->iteration++;
+    c->last_counters.overflow = 0;
+}
+
+void ensure_views_buffers(Ctx* c, size_t n) {
+    if (n > c->losses_cap) {
+        dev_alloc(&c->losses_dev, 3 * n);
+        c->losses_cap = n;
+    }
+}
+
+// ---- consensus plumbing --------------------------------------------------
+void reduce_nccl(Ctx* c, void* buf, size_t count, ncclDataType_t type, ncclRedOp_t op) {
+    if (!c->nccl || c->nranks == 1) return;
+    NcclApi& n = nccl_api();
+    const ncclResult_t r = n.all_reduce(buf, buf, count, type, op, static_cast<ncclComm_t>(c->nccl), c->stream);
+    if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, std::string("ncclAllReduce: ") + n.error_string(r)};
+}
+
+__global__ void sum_into_kernel(float* __restrict__ acc, const float* __restrict__ src, size_t n) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) acc[i] += src[i];
+}
+__global__ void max_into_kernel(float* __restrict__ acc, const float* __restrict__ src, size_t n) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) acc[i] = fmaxf(acc[i], src[i]);
+}
+
+// In-order (ascending block id) reduction of one buffer across a local group.
+void reduce_group(Ctx* const* ctxs, size_t k, float* Ctx::*field, size_t count, bool max_op) {
+    if (k <= 1 || count == 0) return;
+    Ctx* c0 = ctxs[0];
+    for (size_t b = 0; b < k; ++b) BSG_CUDA(cudaStreamSynchronize(ctxs[b]->stream));
+    use_device(c0);
+    float* tmp = nullptr;
+    BSG_CUDA(cudaMalloc(&tmp, count * sizeof(float)));
+    for (size_t b = 1; b < k; ++b) {
+        BSG_CUDA(cudaMemcpyPeerAsync(tmp, c0->device, ctxs[b]->*field, ctxs[b]->device, count * sizeof(float),
+                                     c0->stream));
+        if (max_op)
+            max_into_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, c0->stream>>>(c0->*field, tmp, count);
+        else
+            sum_into_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, c0->stream>>>(c0->*field, tmp, count);
+        BSG_LAUNCHED(c0);
+    }
+    BSG_CUDA(cudaStreamSynchronize(c0->stream));
+    BSG_CUDA(cudaFree(tmp));
+    for (size_t b = 1; b < k; ++b) {
+        use_device(ctxs[b]);
+        BSG_CUDA(cudaMemcpyPeerAsync(ctxs[b]->*field, ctxs[b]->device, c0->*field, c0->device, count * sizeof(float),
+                                     ctxs[b]->stream));
+        BSG_CUDA(cudaStreamSynchronize(ctxs[b]->stream));
+    }
+}
+
+void check_round_ready(Ctx* c) {
+    if (!c->anchored) throw Error{BSG_ERR_STATE, "consensus round before set_anchor"};
+}
+
+void upload_resets(Ctx* c, const bsg_round_args* a) {
+    if (c->n_slots == 0) return;
+    BSG_CUDA(cudaMemsetAsync(c->slot_reset, 0, c->n_slots, c->stream));
+    if (a->n_reset == 0) return;
+    std::vector<uint8_t> h(c->n_slots, 0);
+    for (size_t i = 0; i < a->n_reset; ++i) {
+        if (a->reset_slots[i] >= c->n_slots) invalid("reset slot out of range");
+        h[a->reset_slots[i]] = 1;
+    }
+    BSG_CUDA(cudaMemcpyAsync(c->slot_reset, h.data(), h.size(), cudaMemcpyHostToDevice, c->stream));
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace
+
+// Exposed for consensus.cu diagnostics.
+void round_pack_duals(Ctx* c);
+void round_dual_linf(Ctx* c);
+void round_pack_minmax(Ctx* c);
+void round_spread(Ctx* c);
+
+}  // namespace bsg
+
+using namespace bsg;
+
+extern "C" {
+
+int bsg_abi_version(void) { return BSG_ABI_VERSION; }
+const char* bsg_last_error(void) { return g_err.c_str(); }
+
+void bsg_default_render_config(bsg_render_config* o) {
+    o->near_plane = 0.01;
+    o->dilation = 0.3;
+    o->alpha_clamp = 0.99;
+    o->transmittance_stop = 1e-4;
+    o->sigma_extent = 3.0;
+    o->background[0] = o->background[1] = o->background[2] = 0.0;
+    o->lambda = 0.2;
+}
+
+void bsg_default_trainer_config(bsg_trainer_config* o) {
+    o->iterations = 3000;
+    o->lr_position = 1.6e-4;
+    o->lr_position_decay = 0.01;
+    o->lr_rotation = 1e-3;
+    o->lr_log_scale = 5e-3;
+    o->lr_features = 2.5e-3;
+    o->lr_opacity = 5e-2;
+    o->beta1 = 0.9;
+    o->beta2 = 0.999;
+    o->eps = 1e-8;
+    bsg_default_render_config(&o->render);
+}
+
+void bsg_default_penalties(bsg_penalties* o) {
+    o->rho_p = 1e4;
+    o->rho_q = 1e4;
+    o->rho_s = 1e4;
+    o->rho_f = 1e3;
+    o->rho_o = 1e4;
+}
+
+int bsg_create(int device, int feature_dim, bsg_ctx** out) {
+    return guarded([&] {
+        if (!out) invalid("null output");
+        if (feature_dim != 3 && feature_dim != 12) invalid("unsupported feature width");
+        int count = 0;
+        BSG_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) invalid("no such CUDA device");
+        cudaDeviceProp prop{};
+        BSG_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) throw Error{BSG_ERR_CUDA, "libbsgpu is built for sm_100a (B200); device is sm_" +
+                                                            std::to_string(prop.major * 10 + prop.minor)};
+        auto* c = new Ctx();
+        c->device = device;
+        c->fd = feature_dim;
+        c->D = 11 + feature_dim;
+        try {
+            use_device(c);
+            BSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
+            dev_alloc(&c->counters, 1);
+            dev_alloc(&c->scalars, 1);
+            dev_alloc(&c->radix_hist, 8 * 256);
+            dev_alloc(&c->round_scalars, 8 + kMaxD);
+            dev_alloc(&c->losses_dev, 3);
+            c->losses_cap = 1;
+            for (auto& e : c->ev) BSG_CUDA(cudaEventCreate(&e));
+            bsg_default_trainer_config(&c->tcfg);
+            bsg_default_penalties(&c->rho);
+            alloc_rows(c, 1);
+        } catch (...) {
+            free_all(c);
+            delete c;
+            throw;
+        }
+        *out = reinterpret_cast<bsg_ctx*>(c);
+    });
+}
+
+int bsg_destroy(bsg_ctx* h) {
+    return guarded([&] {
+        if (!h) return;
+        auto* c = reinterpret_cast<Ctx*>(h);
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        free_all(c);
+        delete c;
+    });
+}
+
+int bsg_upload_cloud(bsg_ctx* h, size_t n, const uint64_t* ids, const double* pos, const double* rot, const double* ls,
+                     const double* feat, const double* op) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (n > 0 && (!ids || !pos || !rot || !ls || !feat || !op)) invalid("null parameter array");
+        for (size_t i = 1; i < n; ++i)
+            if (ids[i] <= ids[i - 1]) invalid("initial cloud ids not ascending");
+        if (n >= (1u << 30)) invalid("cloud larger than 2^30 rows");
+        use_device(c);
+        c->n = n;
+        c->ids.assign(ids, ids + n);
+        alloc_rows(c, n);
+        upload_params(c, pos, rot, ls, feat, op);
+        BSG_CUDA(cudaMemsetAsync(c->m, 0, c->D * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->v, 0, c->D * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->anchor_of_row, 0xff, c->cap * sizeof(int32_t), c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        c->adam_t = 0;
+        c->iteration = 0;
+        c->anchored = false;
+        c->n_shared = 0;
+        c->n_slots = 0;
+    });
+}
+
+size_t bsg_cloud_size(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->n : 0; }
+
+int bsg_download_cloud(bsg_ctx* h, uint64_t* ids, double* pos, double* rot, double* ls, double* feat, double* op) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        const size_t n = c->n, cap = c->cap;
+        std::vector<float> hx(static_cast<size_t>(c->D) * cap);
+        BSG_CUDA(cudaMemcpyAsync(hx.data(), c->x, hx.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        if (ids) std::copy(c->ids.begin(), c->ids.end(), ids);
+        for (size_t i = 0; i < n; ++i) {
+            if (pos) for (int k = 0; k < 3; ++k) pos[3 * i + k] = hx[(kPos + k) * cap + i];
+            if (rot) for (int k = 0; k < 4; ++k) rot[4 * i + k] = hx[(kRot + k) * cap + i];
+            if (ls) for (int k = 0; k < 3; ++k) ls[3 * i + k] = hx[(kLs + k) * cap + i];
+            if (feat) for (int k = 0; k < c->fd; ++k) feat[i * c->fd + k] = hx[(kFeat + k) * cap + i];
+            if (op) op[i] = hx[op_comp(c->fd) * cap + i];
+        }
+    });
+}
+
+int bsg_render(bsg_ctx* h, const bsg_camera* cam, const bsg_render_config* cfg, double* out_rgb, double* out_T,
+               uint32_t* out_n) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        check_camera(cam);
+        bsg_render_config rcfg;
+        if (cfg) rcfg = *cfg; else bsg_default_render_config(&rcfg);
+        use_device(c);
+        c->step_launches = 0;
+        const DevCam dc = make_cam(*cam);
+        const DevRender rc = make_render(rcfg);
+        project_and_bin(c, dc, rc);
+        stage_begin(c, kStBlendFwd);
+        launch_blend_fwd(c, dc, rc);
+        stage_end(c, kStBlendFwd);
+        const size_t px = static_cast<size_t>(cam->width) * cam->height;
+        std::vector<float> rgb(3 * px), T(px);
+        BSG_CUDA(cudaMemcpyAsync(rgb.data(), c->out_rgb, rgb.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(T.data(), c->out_T, T.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (out_n) BSG_CUDA(cudaMemcpyAsync(out_n, c->out_n, px * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        collect_stage_times(c);
+        if (out_rgb) for (size_t i = 0; i < 3 * px; ++i) out_rgb[i] = rgb[i];
+        if (out_T) for (size_t i = 0; i < px; ++i) out_T[i] = T[i];
+    });
+}
+
+int bsg_render_backward(bsg_ctx* h, const bsg_camera* cam, const double* gt, const bsg_render_config* cfg,
+                        double* out_loss3, double* g_pos, double* g_rot, double* g_ls, double* g_feat, double* g_op,
+                        double* sgn, uint8_t* visible, double* out_rendered) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        check_camera(cam);
+        if (!gt) invalid("image dimension mismatch");
+        bsg_render_config rcfg;
+        if (cfg) rcfg = *cfg; else bsg_default_render_config(&rcfg);
+        use_device(c);
+        c->step_launches = 0;
+        const DevCam dc = make_cam(*cam);
+        const DevRender rc = make_render(rcfg);
+        const size_t px = static_cast<size_t>(cam->width) * cam->height;
+        ensure_image_buffers(c, dc.W, dc.H);
+        const float* gtd = upload_gt_f64(c, gt, px);
+        BSG_CUDA(cudaMemsetAsync(c->scalars, 0, sizeof(StepScalars), c->stream));
+        project_and_bin(c, dc, rc);
+        stage_begin(c, kStBlendFwd);
+        launch_blend_fwd(c, dc, rc);
+        stage_end(c, kStBlendFwd);
+        stage_begin(c, kStLoss);
+        launch_loss(c, dc, rc, gtd);
+        stage_end(c, kStLoss);
+        stage_begin(c, kStBlendBwd);
+        launch_blend_bwd(c, dc, rc);
+        stage_end(c, kStBlendBwd);
+        ensure_views_buffers(c, 1);
+        launch_finalize_loss(c, dc, rc, c->losses_dev, false);
+        const size_t n = c->n;
+        double* gdev = nullptr;
+        double* sdev = nullptr;
+        uint8_t* vdev = nullptr;
+        BSG_CUDA(cudaMalloc(&gdev, std::max<size_t>(1, c->D * n) * sizeof(double)));
+        BSG_CUDA(cudaMalloc(&sdev, std::max<size_t>(1, n) * sizeof(double)));
+        BSG_CUDA(cudaMalloc(&vdev, std::max<size_t>(1, n)));
+        stage_begin(c, kStAdam);
+        launch_fold_grads(c, dc, gdev, sdev, vdev);
+        stage_end(c, kStAdam);
+        std::vector<double> g(static_cast<size_t>(c->D) * n);
+        double l3[3];
+        BSG_CUDA(cudaMemcpyAsync(g.data(), gdev, g.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(l3, c->losses_dev, sizeof(l3), cudaMemcpyDeviceToHost, c->stream));
+        if (sgn) BSG_CUDA(cudaMemcpyAsync(sgn, sdev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (visible) BSG_CUDA(cudaMemcpyAsync(visible, vdev, n, cudaMemcpyDeviceToHost, c->stream));
+        std::vector<float> rgb;
+        if (out_rendered) {
+            rgb.resize(3 * px);
+            BSG_CUDA(cudaMemcpyAsync(rgb.data(), c->out_rgb, rgb.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        }
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(gdev);
+        cudaFree(sdev);
+        cudaFree(vdev);
+        collect_stage_times(c);
+        if (out_loss3) for (int k = 0; k < 3; ++k) out_loss3[k] = l3[k];
+        for (size_t i = 0; i < n; ++i) {
+            if (g_pos) for (int k = 0; k < 3; ++k) g_pos[3 * i + k] = g[(kPos + k) * n + i];
+            if (g_rot) for (int k = 0; k < 4; ++k) g_rot[4 * i + k] = g[(kRot + k) * n + i];
+            if (g_ls) for (int k = 0; k < 3; ++k) g_ls[3 * i + k] = g[(kLs + k) * n + i];
+            if (g_feat) for (int k = 0; k < c->fd; ++k) g_feat[i * c->fd + k] = g[(kFeat + k) * n + i];
+            if (g_op) g_op[i] = g[op_comp(c->fd) * n + i];
+        }
+        if (out_rendered) for (size_t i = 0; i < 3 * px; ++i) out_rendered[i] = rgb[i];
+    });
+}
+
+int bsg_project(bsg_ctx* h, const bsg_camera* cam, const bsg_render_config* cfg, uint8_t* out_visible,
+                double* out_depth, int32_t* out_rect, uint32_t* out_order, size_t* out_V) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        check_camera(cam);
+        bsg_render_config rcfg;
+        if (cfg) rcfg = *cfg; else bsg_default_render_config(&rcfg);
+        use_device(c);
+        const DevCam dc = make_cam(*cam);
+        project_and_bin(c, dc, make_render(rcfg));
+        const size_t n = c->n;
+        const uint32_t V = c->last_counters.visible;
+        std::vector<uint32_t> tiles(n);
+        std::vector<uint64_t> keys(n);
+        std::vector<float4> rec(3 * n);
+        BSG_CUDA(cudaMemcpyAsync(tiles.data(), c->tiles, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(keys.data(), c->depth_key, n * 8, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(rec.data(), c->rec, 3 * n * sizeof(float4), cudaMemcpyDeviceToHost, c->stream));
+        if (out_order && V)
+            BSG_CUDA(cudaMemcpyAsync(out_order, c->vrow[c->depth_sorted], V * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < n; ++i) {
+            const bool vis = tiles[i] > 0;
+            if (out_visible) out_visible[i] = vis;
+            double d = 0;
+            uint32_t r01 = 0, r23 = 0;
+            if (vis) {
+                std::memcpy(&d, &keys[i], 8);
+                std::memcpy(&r01, &rec[3 * i + 2].y, 4);
+                std::memcpy(&r23, &rec[3 * i + 2].z, 4);
+            }
+            if (out_depth) out_depth[i] = d;
+            if (out_rect) {
+                out_rect[4 * i + 0] = vis ? static_cast<int32_t>(r01 & 0xffffu) : 0;
+                out_rect[4 * i + 1] = vis ? static_cast<int32_t>(r01 >> 16) : -1;
+                out_rect[4 * i + 2] = vis ? static_cast<int32_t>(r23 & 0xffffu) : 0;
+                out_rect[4 * i + 3] = vis ? static_cast<int32_t>(r23 >> 16) : -1;
+            }
+        }
+        if (out_V) *out_V = V;
+    });
+}
+
+int bsg_tile_pairs(bsg_ctx* h, uint32_t* out_tile, uint32_t* out_row, size_t capacity, size_t* out_pairs) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        const size_t P = c->last_counters.pairs;
+        if (out_pairs) *out_pairs = P;
+        if (!out_tile && !out_row) return;
+        if (capacity < P) invalid("pair buffer too small");
+        if (P == 0) return;
+        if (out_tile)
+            BSG_CUDA(cudaMemcpyAsync(out_tile, c->pkey[c->pairs_sorted], P * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (out_row)
+            BSG_CUDA(cudaMemcpyAsync(out_row, c->pval[c->pairs_sorted], P * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int bsg_set_views(bsg_ctx* h, size_t n_views, const bsg_camera* cams, const double* const* gt) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (n_views == 0) invalid("trainer needs at least one view");
+        use_device(c);
+        for (float* p : c->view_gt)
+            if (p) cudaFree(p);
+        c->view_gt.clear();
+        c->view_cams.assign(cams, cams + n_views);
+        for (size_t v = 0; v < n_views; ++v) {
+            check_camera(&cams[v]);
+            if (!gt || !gt[v]) invalid("view without ground truth");
+            const size_t px = static_cast<size_t>(cams[v].width) * cams[v].height;
+            std::vector<float> hh(3 * px);
+            for (size_t i = 0; i < 3 * px; ++i) hh[i] = static_cast<float>(gt[v][i]);
+            float* d = nullptr;
+            BSG_CUDA(cudaMalloc(&d, hh.size() * sizeof(float)));
+            BSG_CUDA(cudaMemcpy(d, hh.data(), hh.size() * sizeof(float), cudaMemcpyHostToDevice));
+            c->view_gt.push_back(d);
+            ensure_image_buffers(c, static_cast<int>(cams[v].width), static_cast<int>(cams[v].height));
+        }
+    });
+}
+
+int bsg_trainer_init(bsg_ctx* h, const bsg_trainer_config* cfg) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (cfg) c->tcfg = *cfg; else bsg_default_trainer_config(&c->tcfg);
+        use_device(c);
+        BSG_CUDA(cudaMemsetAsync(c->m, 0, c->D * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->v, 0, c->D * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        c->adam_t = 0;
+        c->iteration = 0;
+        c->trainer_ready = true;
+    });
+}
+
+int bsg_train_steps(bsg_ctx* h, size_t n, const uint32_t* view_seq, double* losses) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!c->trainer_ready) throw Error{BSG_ERR_STATE, "train step before bsg_trainer_init"};
+        if (c->view_cams.empty()) throw Error{BSG_ERR_STATE, "train step before bsg_set_views"};
+        use_device(c);
+        ensure_views_buffers(c, std::max<size_t>(n, 1));
+        for (size_t k = 0; k < n; ++k) {
+            const uint32_t vi = view_seq[k];
+            if (vi >= c->view_cams.size()) invalid("view index out of range");
+            train_one(c, c->view_cams[vi], c->view_gt[vi], c->losses_dev + 3 * k);
+        }
+        if (losses && n) {
+            std::vector<double> l(3 * n);
+            BSG_CUDA(cudaMemcpyAsync(l.data(), c->losses_dev, l.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                     c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            for (size_t k = 0; k < n; ++k) losses[k] = l[3 * k];
+        }
+        collect_stage_times(c);
+    });
+}
+
+int bsg_train_step_host(bsg_ctx* h, const bsg_camera* cam, const float* gt_host, double* loss) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!c->trainer_ready) throw Error{BSG_ERR_STATE, "train step before bsg_trainer_init"};
+        check_camera(cam);
+        if (!gt_host) invalid("null ground truth");
+        use_device(c);
+        ensure_image_buffers(c, static_cast<int>(cam->width), static_cast<int>(cam->height));
+        ensure_views_buffers(c, 1);
+        const size_t px = static_cast<size_t>(cam->width) * cam->height;
+        BSG_CUDA(cudaMemcpyAsync(c->gt_stage, gt_host, 3 * px * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        train_one(c, *cam, c->gt_stage, c->losses_dev);
+        double l3[3];
+        BSG_CUDA(cudaMemcpyAsync(l3, c->losses_dev, sizeof(l3), cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        if (loss) *loss = l3[0];
+        collect_stage_times(c);
+    });
+}
+
+uint64_t bsg_iteration(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->iteration : 0; }
+
+int bsg_download_moments(bsg_ctx* h, double* m, double* v) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        const size_t n = c->n, cap = c->cap;
+        std::vector<float> hm(c->D * cap), hv(c->D * cap);
+        BSG_CUDA(cudaMemcpyAsync(hm.data(), c->m, hm.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(hv.data(), c->v, hv.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        for (int k = 0; k < c->D; ++k)
+            for (size_t i = 0; i < n; ++i) {
+                if (m) m[k * n + i] = hm[k * cap + i];
+                if (v) v[k * n + i] = hv[k * cap + i];
+            }
+    });
+}
+
+int bsg_download_densify_stats(bsg_ctx* h, double* ga, uint32_t* gs) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        std::vector<float> a(c->n);
+        if (c->n) BSG_CUDA(cudaMemcpyAsync(a.data(), c->grad_accum, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (gs && c->n) BSG_CUDA(cudaMemcpyAsync(gs, c->grad_seen, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        if (ga) for (size_t i = 0; i < c->n; ++i) ga[i] = a[i];
+    });
+}
+
+int bsg_set_shared(bsg_ctx* h, size_t ns, const uint32_t* rows, const uint32_t* slots, const uint8_t* first,
+                   size_t n_slots, const uint32_t* owners) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        for (size_t j = 0; j < ns; ++j) {
+            if (rows[j] >= c->n) invalid("shared rows missing from cloud");
+            if (slots[j] >= n_slots) invalid("slot out of range");
+            if (j && rows[j] <= rows[j - 1]) invalid("shared rows not ascending");
+        }
+        for (size_t s = 0; s < n_slots; ++s)
+            if (owners[s] == 0) invalid("slot without owners");
+        c->n_shared = ns;
+        c->n_slots = n_slots;
+        dev_alloc(&c->sh_rows, ns);
+        dev_alloc(&c->sh_slots, ns);
+        dev_alloc(&c->sh_first, ns);
+        dev_alloc(&c->z, c->D * std::max<size_t>(ns, 1));
+        dev_alloc(&c->u, c->D * std::max<size_t>(ns, 1));
+        dev_alloc(&c->zprev, c->D * std::max<size_t>(n_slots, 1));
+        dev_alloc(&c->zslot, c->D * std::max<size_t>(n_slots, 1));
+        dev_alloc(&c->in_zprev, n_slots);
+        dev_alloc(&c->slot_owners, n_slots);
+        dev_alloc(&c->pack, 2 * c->D * std::max<size_t>(n_slots, 1) + n_slots);
+        dev_alloc(&c->qref, 4 * std::max<size_t>(n_slots, 1));
+        dev_alloc(&c->slot_reset, n_slots);
+        if (ns) {
+            BSG_CUDA(cudaMemcpy(c->sh_rows, rows, ns * 4, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpy(c->sh_slots, slots, ns * 4, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpy(c->sh_first, first, ns, cudaMemcpyHostToDevice));
+        }
+        if (n_slots) BSG_CUDA(cudaMemcpy(c->slot_owners, owners, n_slots * 4, cudaMemcpyHostToDevice));
+        std::vector<int32_t> aor(c->cap, -1);
+        for (size_t j = 0; j < ns; ++j) aor[rows[j]] = static_cast<int32_t>(j);
+        BSG_CUDA(cudaMemcpy(c->anchor_of_row, aor.data(), aor.size() * 4, cudaMemcpyHostToDevice));
+        BSG_CUDA(cudaMemset(c->in_zprev, 0, std::max<size_t>(n_slots, 1)));
+        c->anchored = false;
+    });
+}
+
+int bsg_set_anchor(bsg_ctx* h, const double* z_rows, const double* zprev_slots, const bsg_penalties* rho) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        const std::vector<float> zc = rows_to_cm(z_rows, c->n_shared, c->D);
+        if (c->n_shared) {
+            BSG_CUDA(cudaMemcpy(c->z, zc.data(), c->D * c->n_shared * 4, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemset(c->u, 0, c->D * c->n_shared * 4));
+        }
+        if (c->n_slots) {
+            if (zprev_slots) {
+                const std::vector<float> zp = rows_to_cm(zprev_slots, c->n_slots, c->D);
+                BSG_CUDA(cudaMemcpy(c->zprev, zp.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
+                BSG_CUDA(cudaMemset(c->in_zprev, 1, c->n_slots));
+            } else {
+                BSG_CUDA(cudaMemset(c->in_zprev, 0, c->n_slots));
+            }
+        }
+        if (rho) c->rho = *rho;
+        c->anchored = true;
+    });
+}
+
+int bsg_set_penalties(bsg_ctx* h, const bsg_penalties* rho) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !rho) invalid("null argument");
+        c->rho = *rho;
+    });
+}
+
+int bsg_download_duals(bsg_ctx* h, double* u_rows) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        std::vector<float> hu(c->D * std::max<size_t>(c->n_shared, 1));
+        if (c->n_shared) BSG_CUDA(cudaMemcpy(hu.data(), c->u, c->D * c->n_shared * 4, cudaMemcpyDeviceToHost));
+        cm_to_rows(hu.data(), c->n_shared, c->D, u_rows);
+    });
+}
+
+int bsg_download_anchor(bsg_ctx* h, double* z_rows) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        std::vector<float> hz(c->D * std::max<size_t>(c->n_shared, 1));
+        if (c->n_shared) BSG_CUDA(cudaMemcpy(hz.data(), c->z, c->D * c->n_shared * 4, cudaMemcpyDeviceToHost));
+        cm_to_rows(hz.data(), c->n_shared, c->D, z_rows);
+    });
+}
+
+int bsg_download_consensus(bsg_ctx* h, double* z_slots) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        std::vector<float> hz(c->D * std::max<size_t>(c->n_slots, 1));
+        if (c->n_slots) BSG_CUDA(cudaMemcpy(hz.data(), c->zslot, c->D * c->n_slots * 4, cudaMemcpyDeviceToHost));
+        cm_to_rows(hz.data(), c->n_slots, c->D, z_slots);
+    });
+}
+
+int bsg_nccl_unique_id(uint8_t out_id[128]) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId id;
+        NcclApi& n = nccl_api();
+        const ncclResult_t r = n.get_unique_id(&id);
+        if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, n.error_string(r)};
+        std::memcpy(out_id, &id, 128);
+    });
+}
+
+int bsg_comm_init(bsg_ctx* h, const uint8_t id[128], int nranks, int rank) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (nranks < 1 || rank < 0 || rank >= nranks) invalid("bad rank layout");
+        use_device(c);
+        c->nranks = nranks;
+        c->rank = rank;
+        if (nranks == 1) return;
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        ncclComm_t comm;
+        NcclApi& napi = nccl_api();
+        const ncclResult_t r = napi.comm_init_rank(&comm, nranks, uid, rank);
+        if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, std::string("ncclCommInitRank: ") + napi.error_string(r)};
+        c->nccl = comm;
+    });
+}
+
+int bsg_consensus_round(bsg_ctx* h, const bsg_round_args* a, bsg_round_result* out) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !a) invalid("null argument");
+        check_round_ready(c);
+        use_device(c);
+        upload_resets(c, a);
+        cudaEvent_t e0, e1;
+        BSG_CUDA(cudaEventCreate(&e0));
+        BSG_CUDA(cudaEventCreate(&e1));
+        BSG_CUDA(cudaEventRecord(e0, c->stream));
+        round_pack_q(c);
+        reduce_nccl(c, c->qref, 4 * c->n_slots, ncclFloat, ncclSum);
+        round_pack_main(c, a->alpha, a->relax != 0);
+        reduce_nccl(c, c->pack, (c->D + 1) * c->n_slots, ncclFloat, ncclSum);
+        round_unpack(c, a->alpha, a->relax != 0, a->n_reset ? c->slot_reset : nullptr, a->n_reset, a->diagnostics != 0);
+        reduce_nccl(c, c->round_scalars, 1, ncclFloat64, ncclSum);  // primal^2 partials
+        if (a->diagnostics) {
+            round_pack_duals(c);
+            reduce_nccl(c, c->pack, c->D * c->n_slots, ncclFloat, ncclSum);
+            round_dual_linf(c);
+            round_pack_minmax(c);
+            reduce_nccl(c, c->pack, 2 * c->D * c->n_slots, ncclFloat, ncclMax);
+            round_spread(c);
+        }
+        BSG_CUDA(cudaEventRecord(e1, c->stream));
+        double sc[8];
+        BSG_CUDA(cudaMemcpyAsync(sc, c->round_scalars, sizeof(sc), cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (out) {
+            out->primal = std::sqrt(sc[0]);
+            out->dual = std::sqrt(sc[1]);
+            out->flipped = static_cast<uint64_t>(sc[2]);
+            uint64_t b3, b4;
+            std::memcpy(&b3, &sc[3], 8);
+            std::memcpy(&b4, &sc[4], 8);
+            out->dual_mean_linf = sc[3];
+            out->max_disagreement = sc[4];
+            out->ms = ms;
+        }
+    });
+}
+
+int bsg_group_consensus_round(bsg_ctx* const* hs, size_t k, const bsg_round_args* a, bsg_round_result* out) {
+    return guarded([&] {
+        if (!hs || k == 0 || !a) invalid("no block contributions");
+        std::vector<Ctx*> cs(k);
+        for (size_t b = 0; b < k; ++b) {
+            cs[b] = reinterpret_cast<Ctx*>(hs[b]);
+            if (!cs[b]) invalid("null context");
+            check_round_ready(cs[b]);
+            if (cs[b]->n_slots != cs[0]->n_slots || cs[b]->D != cs[0]->D) invalid("slot layouts differ");
+        }
+        Ctx* const* cp = cs.data();
+        for (Ctx* c : cs) {
+            use_device(c);
+            upload_resets(c, a);
+            round_pack_q(c);
+        }
+        reduce_group(cp, k, &Ctx::qref, 4 * cs[0]->n_slots, false);
+        for (Ctx* c : cs) {
+            use_device(c);
+            round_pack_main(c, a->alpha, a->relax != 0);
+        }
+        reduce_group(cp, k, &Ctx::pack, (cs[0]->D + 1) * cs[0]->n_slots, false);
+        double primal2 = 0;
+        double sc0[8] = {};
+        for (size_t b = 0; b < k; ++b) {
+            Ctx* c = cs[b];
+            use_device(c);
+            round_unpack(c, a->alpha, a->relax != 0, a->n_reset ? c->slot_reset : nullptr, a->n_reset, false);
+            double sc[8];
+            BSG_CUDA(cudaMemcpyAsync(sc, c->round_scalars, sizeof(sc), cudaMemcpyDeviceToHost, c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            primal2 += sc[0];
+            if (b == 0) std::memcpy(sc0, sc, sizeof(sc));
+        }
+        double linf = 0, spread = 0;
+        if (a->diagnostics) {
+            for (Ctx* c : cs) {
+                use_device(c);
+                round_pack_duals(c);
+            }
+            reduce_group(cp, k, &Ctx::pack, cs[0]->D * cs[0]->n_slots, false);
+            use_device(cs[0]);
+            round_dual_linf(cs[0]);
+            for (Ctx* c : cs) {
+                use_device(c);
+                round_pack_minmax(c);
+            }
+            reduce_group(cp, k, &Ctx::pack, 2 * cs[0]->D * cs[0]->n_slots, true);
+            use_device(cs[0]);
+            round_spread(cs[0]);
+            double sc[8];
+            BSG_CUDA(cudaMemcpyAsync(sc, cs[0]->round_scalars, sizeof(sc), cudaMemcpyDeviceToHost, cs[0]->stream));
+            BSG_CUDA(cudaStreamSynchronize(cs[0]->stream));
+            linf = sc[3];
+            spread = sc[4];
+        }
+        if (out) {
+            out->primal = std::sqrt(primal2);
+            out->dual = std::sqrt(sc0[1]);
+            out->flipped = static_cast<uint64_t>(sc0[2]);
+            out->dual_mean_linf = linf;
+            out->max_disagreement = spread;
+            out->ms = 0;
+        }
+    });
+}
+
+int bsg_enable_stage_timing(bsg_ctx* h, int enable) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        c->stage_timing = enable != 0;
+    });
+}
+
+int bsg_stage_count(void) { return kStCount; }
+
+const char* bsg_stage_name(int i) {
+    static const char* names[kStCount] = {"preprocess", "compact", "depth_sort", "pairs", "tile_sort",
+                                          "ranges", "blend_fwd", "loss_ssim", "blend_bwd", "fold_adam"};
+    return (i >= 0 && i < kStCount) ? names[i] : "";
+}
+
+int bsg_stage_times(bsg_ctx* h, double* ms) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !ms) invalid("null argument");
+        for (int s = 0; s < kStCount; ++s) ms[s] = c->stage_ms[s];
+    });
+}
+
+int bsg_step_counters(bsg_ctx* h, uint64_t* visible, uint64_t* pairs, uint64_t* launches) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (visible) *visible = c->last_counters.visible;
+        if (pairs) *pairs = c->last_counters.pairs;
+        if (launches) *launches = c->step_launches;
+    });
+}
+
+uint64_t bsg_launch_count(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->launches : 0; }
+
+void* bsg_stream(bsg_ctx* h) { return h ? reinterpret_cast<Ctx*>(h)->stream : nullptr; }
+
+int bsg_synchronize(bsg_ctx* h) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        use_device(c);
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

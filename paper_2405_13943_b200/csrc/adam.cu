@@ -1,0 +1,277 @@
+// K9 + K10: fold of the image-space splat gradients to the parameters
+// (renderer.cpp:313-403) fused with the consensus penalty
+// (admm.cpp:11-45, trainer.cpp:257-265), dense Adam on every row
+// (trainer.cpp:120-131,267-281), quaternion canonicalisation (cloud.cpp:82-85)
+// and the densify statistics (trainer.cpp:284-289). One thread per row; the
+// parameter gradient is never written to memory. HBM-bound: per row it reads
+// x, m, v (3 x 4D bytes) and writes them back, plus the 48 B splat gradient
+// record for visible rows and z, u for shared rows.
+#include "bsg_internal.cuh"
+
+namespace bsg {
+namespace {
+
+// Fold of one visible row; FP64 arithmetic over FP32 inputs. g receives the
+// D parameter gradients; returns the screen-space gradient norm.
+__device__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, int fd, const DevCam& cam,
+                           const float4* __restrict__ g2d, double* g) {
+    const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
+                 gcx = g2d[3 * static_cast<size_t>(i) + 2];
+    const double gm0 = ga.x, gm1 = ga.y;
+    const double gcov[2][2] = {{ga.z, ga.w}, {ga.w, gb.x}};
+    const double gcol[3] = {gb.y, gb.z, gb.w};
+    const double gop = gcx.x;
+
+    const double pos[3] = {x[(kPos + 0) * cap + i], x[(kPos + 1) * cap + i], x[(kPos + 2) * cap + i]};
+    double pc[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) pc[r] = ((cam.R[3 * r] * pos[0] + cam.R[3 * r + 1] * pos[1]) + cam.R[3 * r + 2] * pos[2]) + cam.t[r];
+    const double z = pc[2], iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
+
+    // opacity logit (renderer.cpp:325-327)
+    const double ol = x[op_comp(fd) * cap + i];
+    const double o = 1.0 / (1.0 + exp(-ol));
+    g[op_comp(fd)] = gop * o * (1.0 - o);
+
+    // features (renderer.cpp:329-352)
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) g[kFeat + ch] = kSh0 * gcol[ch];
+    double gpd[3] = {0, 0, 0};
+    if (fd >= 12) {
+        const double u0 = pos[0] - cam.center[0], u1 = pos[1] - cam.center[1], u2 = pos[2] - cam.center[2];
+        const double un = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+        const double dir[3] = {u0 / un, u1 / un, u2 / un};
+        const double b0 = -kSh1 * dir[1], b1 = kSh1 * dir[2], b2 = -kSh1 * dir[0];
+        double gd[3] = {0, 0, 0};
+        for (int ch = 0; ch < 3; ++ch) {
+            g[kFeat + 3 + 3 * ch] = b0 * gcol[ch];
+            g[kFeat + 4 + 3 * ch] = b1 * gcol[ch];
+            g[kFeat + 5 + 3 * ch] = b2 * gcol[ch];
+            const double f3 = x[(kFeat + 3 + 3 * ch) * cap + i], f4 = x[(kFeat + 4 + 3 * ch) * cap + i],
+                         f5 = x[(kFeat + 5 + 3 * ch) * cap + i];
+            gd[0] += gcol[ch] * (f5 * -kSh1);
+            gd[1] += gcol[ch] * (f3 * -kSh1);
+            gd[2] += gcol[ch] * (f4 * kSh1);
+        }
+        const double dd = dir[0] * gd[0] + dir[1] * gd[1] + dir[2] * gd[2];
+        for (int k = 0; k < 3; ++k) gpd[k] = (gd[k] - dir[k] * dd) / un;
+    }
+
+    // screen-space norm (renderer.cpp:356-358)
+    const double sx = gm0 * cam.W * 0.5, sy = gm1 * cam.H * 0.5;
+    const double sgn = sqrt(sx * sx + sy * sy);
+
+    // mean path (renderer.cpp:360-362)
+    double gpc[3] = {gm0 * cam.fx * iz, gm1 * cam.fy * iz, -gm0 * cam.fx * pc[0] * iz2 - gm1 * cam.fy * pc[1] * iz2};
+
+    // covariance path (renderer.cpp:364-378)
+    const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * pc[0] * iz2}, {0.0, cam.fy * iz, -cam.fy * pc[1] * iz2}};
+    double A[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) A[r][k] = J[r][0] * cam.R[k] + J[r][1] * cam.R[3 + k] + J[r][2] * cam.R[6 + k];
+
+    double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
+           qz = x[(kRot + 3) * cap + i];
+    const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    double hw, hx, hy, hz;
+    if (qn == 0.0) {
+        hw = 1; hx = 0; hy = 0; hz = 0;
+    } else {
+        hw = qw / qn; hx = qx / qn; hy = qy / qn; hz = qz / qn;
+    }
+    double R[3][3];
+    R[0][0] = 1 - 2 * (hy * hy + hz * hz); R[0][1] = 2 * (hx * hy - hw * hz); R[0][2] = 2 * (hx * hz + hw * hy);
+    R[1][0] = 2 * (hx * hy + hw * hz); R[1][1] = 1 - 2 * (hx * hx + hz * hz); R[1][2] = 2 * (hy * hz - hw * hx);
+    R[2][0] = 2 * (hx * hz - hw * hy); R[2][1] = 2 * (hy * hz + hw * hx); R[2][2] = 1 - 2 * (hx * hx + hy * hy);
+    const double sc[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])), exp(static_cast<double>(x[(kLs + 1) * cap + i])),
+                          exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
+    double M[3][3], S[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) M[a][b] = R[a][b] * sc[b];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) S[a][b] = M[a][0] * M[b][0] + M[a][1] * M[b][1] + M[a][2] * M[b][2];
+
+    // g_sigma = A^T gcov A ; g_a = 2 gcov A S ; g_j = g_a W^T
+    double atg[3][2], gS[3][3], ga0[2][3], gA[2][3], gJ[2][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) atg[r][s] = A[0][r] * gcov[0][s] + A[1][r] * gcov[1][s];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gS[r][k] = atg[r][0] * A[0][k] + atg[r][1] * A[1][k];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ga0[r][k] = 2.0 * (gcov[r][0] * A[0][k] + gcov[r][1] * A[1][k]);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gA[r][k] = ga0[r][0] * S[0][k] + ga0[r][1] * S[1][k] + ga0[r][2] * S[2][k];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gJ[r][k] = gA[r][0] * cam.R[3 * k] + gA[r][1] * cam.R[3 * k + 1] + gA[r][2] * cam.R[3 * k + 2];
+    gpc[0] += gJ[0][2] * (-cam.fx * iz2);
+    gpc[1] += gJ[1][2] * (-cam.fy * iz2);
+    gpc[2] += gJ[0][0] * (-cam.fx * iz2) + gJ[1][1] * (-cam.fy * iz2) + gJ[0][2] * (2.0 * cam.fx * pc[0] * iz3) +
+              gJ[1][2] * (2.0 * cam.fy * pc[1] * iz3);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        g[kPos + k] = cam.R[k] * gpc[0] + cam.R[3 + k] * gpc[1] + cam.R[6 + k] * gpc[2] + gpd[k];
+
+    // log-scale and quaternion (renderer.cpp:383-402)
+    double gM[3][3], gR[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) gM[a][b] = 2.0 * (gS[a][0] * M[0][b] + gS[a][1] * M[1][b] + gS[a][2] * M[2][b]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) gR[a][b] = gM[a][b] * sc[b];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[kLs + k] = (R[0][k] * gM[0][k] + R[1][k] * gM[1][k] + R[2][k] * gM[2][k]) * sc[k];
+    // dR/dq_hat (renderer.cpp:198-213), contracted with gR
+    const double gq0 = 2.0 * (gR[0][1] * -hz + gR[0][2] * hy + gR[1][0] * hz + gR[1][2] * -hx + gR[2][0] * -hy + gR[2][1] * hx);
+    const double gq1 = 2.0 * (gR[0][1] * hy + gR[0][2] * hz + gR[1][0] * hy + gR[1][1] * (-2 * hx) + gR[1][2] * -hw +
+                              gR[2][0] * hz + gR[2][1] * hw + gR[2][2] * (-2 * hx));
+    const double gq2 = 2.0 * (gR[0][0] * (-2 * hy) + gR[0][1] * hx + gR[0][2] * hw + gR[1][0] * hx + gR[1][2] * hz +
+                              gR[2][0] * -hw + gR[2][1] * hz + gR[2][2] * (-2 * hy));
+    const double gq3 = 2.0 * (gR[0][0] * (-2 * hz) + gR[0][1] * -hw + gR[0][2] * hx + gR[1][0] * hw + gR[1][1] * (-2 * hz) +
+                              gR[1][2] * hy + gR[2][0] * hx + gR[2][1] * hy);
+    const double qdot = hw * gq0 + hx * gq1 + hy * gq2 + hz * gq3;
+    const double inv_qn = qn == 0.0 ? 0.0 : 1.0 / qn;
+    g[kRot + 0] = (gq0 - hw * qdot) * inv_qn;
+    g[kRot + 1] = (gq1 - hx * qdot) * inv_qn;
+    g[kRot + 2] = (gq2 - hy * qdot) * inv_qn;
+    g[kRot + 3] = (gq3 - hz * qdot) * inv_qn;
+    return sgn;
+}
+
+__global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict__ x, size_t cap, uint32_t n, int fd,
+                                                         DevCam cam, const uint32_t* __restrict__ tiles,
+                                                         const float4* __restrict__ g2d, double* __restrict__ gout,
+                                                         double* __restrict__ sgn_out, uint8_t* __restrict__ vis) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int D = 11 + fd;
+    double g[kMaxD];
+#pragma unroll
+    for (int c = 0; c < kMaxD; ++c) g[c] = 0.0;
+    double s = 0.0;
+    const bool visible = tiles[i] > 0;
+    if (visible) s = fold_row(x, cap, i, fd, cam, g2d, g);
+    for (int c = 0; c < D; ++c) gout[static_cast<size_t>(c) * n + i] = g[c];
+    sgn_out[i] = s;
+    vis[i] = visible ? 1 : 0;
+}
+
+__global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
+                                                   size_t cap, uint32_t n, int fd, DevCam cam,
+                                                   const uint32_t* __restrict__ tiles, const float4* __restrict__ g2d,
+                                                   float* __restrict__ grad_accum, uint32_t* __restrict__ grad_seen,
+                                                   const int32_t* __restrict__ anchor_of_row, const float* __restrict__ z,
+                                                   const float* __restrict__ u, size_t n_shared, AdamStep st,
+                                                   double* __restrict__ penalty) {
+    __shared__ double s_red[8];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int D = 11 + fd;
+    double pen = 0.0;
+    if (i < n) {
+        double gd[kMaxD];
+#pragma unroll
+        for (int c = 0; c < kMaxD; ++c) gd[c] = 0.0;
+        if (tiles[i] > 0) {
+            const double s = fold_row(x, cap, i, fd, cam, g2d, gd);
+            grad_accum[i] += static_cast<float>(s);
+            grad_seen[i] += 1u;
+        }
+        float xv[kMaxD], g[kMaxD];
+#pragma unroll
+        for (int c = 0; c < kMaxD; ++c) {
+            if (c < D) {
+                xv[c] = x[static_cast<size_t>(c) * cap + i];
+                g[c] = static_cast<float>(gd[c]);
+            }
+        }
+        if (st.has_anchor) {
+            const int32_t j = anchor_of_row[i];
+            if (j >= 0) {
+#pragma unroll
+                for (int c = 0; c < kMaxD; ++c) {
+                    if (c < D) {
+                        const float d = xv[c] - z[static_cast<size_t>(c) * n_shared + j] + u[static_cast<size_t>(c) * n_shared + j];
+                        pen += 0.5 * static_cast<double>(st.rho[c]) * static_cast<double>(d) * static_cast<double>(d);
+                        g[c] += st.rho[c] * d;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kMaxD; ++c) {
+            if (c < D) {
+                const size_t k = static_cast<size_t>(c) * cap + i;
+                const float mm = st.b1 * m[k] + st.omb1 * g[c];
+                const float vv = st.b2 * v[k] + st.omb2 * g[c] * g[c];
+                m[k] = mm;
+                v[k] = vv;
+                xv[c] -= st.lr[c] * (mm * st.inv_bc1) / (sqrtf(vv * st.inv_bc2) + st.eps);
+            }
+        }
+        // canonicalize_rotations (cloud.cpp:82-85; math.hpp:25-34)
+        float qw = xv[kRot], qx = xv[kRot + 1], qy = xv[kRot + 2], qz = xv[kRot + 3];
+        const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+        if (qn == 0.f) {
+            qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
+        } else {
+            qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+        }
+        if (qw < 0.f) {
+            qw = -qw; qx = -qx; qy = -qy; qz = -qz;
+        }
+        xv[kRot] = qw; xv[kRot + 1] = qx; xv[kRot + 2] = qy; xv[kRot + 3] = qz;
+#pragma unroll
+        for (int c = 0; c < kMaxD; ++c)
+            if (c < D) x[static_cast<size_t>(c) * cap + i] = xv[c];
+    }
+    if (st.has_anchor) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pen += __shfl_xor_sync(0xffffffffu, pen, o);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pen;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0;
+            for (int w = 0; w < 8; ++w) t += s_red[w];
+            if (t != 0.0) atomicAdd(penalty, t);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, uint8_t* vis) {
+    if (c->n == 0) return;
+    fold_grads_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
+        c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, c->tiles, c->g2d, g_out, sgn, vis);
+    BSG_LAUNCHED(c);
+}
+
+void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index) {
+    (void)loss_out;
+    (void)step_index;
+    if (c->n == 0) return;
+    adam_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
+        c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, c->tiles, c->g2d, c->grad_accum,
+        c->grad_seen, c->anchor_of_row, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
+    BSG_LAUNCHED(c);
+}
+
+}  // namespace bsg

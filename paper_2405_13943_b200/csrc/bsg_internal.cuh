@@ -1,0 +1,226 @@
+// Internal declarations of the B200 (sm_100a) blocksplat hot path.
+// Device state is FP32 component-major ([D][cap]); the per-Gaussian
+// projection that decides integer footprints and depth order runs in FP64
+// (see preprocess.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bsgpu.h"
+
+namespace bsg {
+
+constexpr int kTile = 16;             // 16x16 pixel tiles, one thread per pixel
+constexpr int kTileThreads = kTile * kTile;
+constexpr int kMaxFd = 12;            // SH degree 1 (cloud.hpp:16-17)
+constexpr int kMaxD = 11 + kMaxFd;    // pos3 rot4 ls3 feat fd op1
+constexpr double kSh0 = 0.28209479177387814;  // cloud.hpp:14
+constexpr double kSh1 = 0.4886025119029199;   // cloud.hpp:15
+
+// Component offsets of the [D][cap] parameter matrix.
+constexpr int kPos = 0, kRot = 3, kLs = 7, kFeat = 10;
+__host__ __device__ inline int op_comp(int fd) { return kFeat + fd; }
+
+// Camera as consumed by kernels (by value).
+struct DevCam {
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    double center[3];  // -R^T t (camera.hpp:31)
+    int W, H;
+    int tiles_x, tiles_y;
+};
+
+struct DevRender {
+    double near_plane, dilation, alpha_clamp, tstop, sigma_extent;
+    float bg[3];
+    double lambda;
+};
+
+// Per-step counters kept in device memory (read back once per step).
+struct StepCounters {
+    uint32_t visible;   // V
+    uint32_t pairs;     // P
+    uint32_t overflow;  // pairs exceeded capacity
+    uint32_t pad;
+};
+
+// Scalars reduced on the device every step.
+struct StepScalars {
+    double l1_sum;
+    double ssim_sum;
+    double penalty;
+    double pad;
+};
+
+enum Stage {
+    kStPreprocess = 0, kStCompact, kStDepthSort, kStPairs, kStTileSort, kStRanges, kStBlendFwd, kStLoss,
+    kStBlendBwd, kStAdam, kStCount
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int fd = 3, D = 14;
+    size_t n = 0, cap = 0;
+    std::vector<uint64_t> ids;
+
+    // parameters and optimizer state, [D][cap]
+    float* x = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    float* grad_accum = nullptr;   // densify statistics
+    uint32_t* grad_seen = nullptr;
+
+    // per-row scratch
+    float4* rec = nullptr;         // 3 x float4 per row: {mx,my,m00,m01},{m11,o,r,g},{b,rect01,rect23,-}
+    uint64_t* depth_key = nullptr; // FP64 depth bits
+    uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
+    float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
+    int32_t* anchor_of_row = nullptr;  // anchor index j or -1
+
+    // compaction + depth sort (ping-pong)
+    uint64_t* vkey[2] = {nullptr, nullptr};
+    uint32_t* vrow[2] = {nullptr, nullptr};
+    uint32_t* poff = nullptr;      // pair offsets (exclusive scan over sorted splats)
+    int depth_sorted = 0;          // which ping-pong buffer holds the sorted result
+
+    // tile pairs (ping-pong)
+    size_t pcap = 0;
+    uint32_t* pkey[2] = {nullptr, nullptr};
+    uint32_t* pval[2] = {nullptr, nullptr};
+    int pairs_sorted = 0;
+    uint2* ranges = nullptr;
+    size_t ranges_cap = 0;
+
+    // radix / scan scratch
+    uint32_t* scan_status = nullptr;   // decoupled look-back status words
+    size_t scan_status_cap = 0;
+    uint32_t* radix_status = nullptr;
+    size_t radix_status_cap = 0;
+    uint32_t* radix_hist = nullptr;    // [8 passes][256]
+    uint32_t* counters_dev = nullptr;  // tile-id tickets
+    StepCounters* counters = nullptr;  // device
+    StepCounters* counters_host = nullptr;  // pinned
+    StepScalars* scalars = nullptr;         // device
+    double* losses_dev = nullptr;           // per-step losses
+    size_t losses_cap = 0;
+
+    // images for the current view
+    size_t img_cap = 0;  // pixels
+    float* out_rgb = nullptr;
+    float* out_T = nullptr;
+    uint32_t* out_n = nullptr;
+    uint32_t* out_last = nullptr;
+    float* dl_dc = nullptr;
+    float* ssim_f = nullptr;   // 9 planes of the valid window grid
+    float* gt_stage = nullptr; // host ground truth staging (e2e path)
+
+    // resident training views
+    std::vector<bsg_camera> view_cams;
+    std::vector<float*> view_gt;
+
+    // training
+    bool trainer_ready = false;
+    bsg_trainer_config tcfg{};
+    uint64_t iteration = 0;
+    uint64_t adam_t = 0;
+
+    // consensus (per block)
+    size_t n_shared = 0, n_slots = 0;
+    uint32_t* sh_rows = nullptr;
+    uint32_t* sh_slots = nullptr;
+    uint8_t* sh_first = nullptr;
+    float* z = nullptr;         // anchor [D][n_shared]
+    float* u = nullptr;         // duals  [D][n_shared]
+    float* zprev = nullptr;     // [D][n_slots]
+    float* zslot = nullptr;     // consensus of the last round [D][n_slots]
+    uint8_t* in_zprev = nullptr;
+    uint32_t* slot_owners = nullptr;
+    float* pack = nullptr;      // [D+1][n_slots] (+1 = flip flag)
+    float* qref = nullptr;      // [4][n_slots]
+    uint8_t* slot_reset = nullptr;
+    double* round_scalars = nullptr;  // primal2, dual2, flips, maxdis, linf
+    bool anchored = false;
+    bsg_penalties rho{};
+    void* nccl = nullptr;       // ncclComm_t
+    int nranks = 1, rank = 0;
+
+    // measurement
+    bool stage_timing = false;
+    cudaEvent_t ev[kStCount + 1] = {};
+    float stage_ms[kStCount] = {};
+    uint64_t launches = 0;
+    uint64_t step_launches = 0;
+    StepCounters last_counters{};
+};
+
+// ---- error plumbing -----------------------------------------------------
+void set_error(const std::string& msg);
+struct Error {
+    int code;
+    std::string msg;
+};
+#define BSG_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            throw ::bsg::Error{BSG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+#define BSG_LAUNCHED(ctx)                                                                  \
+    do {                                                                                   \
+        (ctx)->launches++;                                                                 \
+        (ctx)->step_launches++;                                                            \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            throw ::bsg::Error{BSG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)}; \
+    } while (0)
+
+// ---- building blocks (scan.cu, radix.cu) -------------------------------
+// Exclusive scan of n u32 values read through a gather (in[idx ? idx[i] : i]),
+// optional predicate compaction. Result in out; total in *total_dev.
+void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,
+                        uint32_t* total_dev);
+// Stable compaction of rows with tiles[i] > 0: writes keys/rows in row order and V.
+void compact_visible(Ctx* c, uint32_t n);
+// Stable LSD radix sort (onesweep) of (u64 key, u32 val) / (u32 key, u32 val).
+// begin_bit/end_bit select the digit range; result lands in buffer *sel.
+void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel);
+void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel);
+
+// ---- rasterizer stages (preprocess.cu, raster.cu, ssim.cu, adam.cu) ----
+DevCam make_cam(const bsg_camera& c);
+DevRender make_render(const bsg_render_config& r);
+void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc);
+void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V);
+void launch_ranges(Ctx* c, const DevCam& cam, uint32_t P);
+void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc);
+void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt);
+void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc);
+void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out /*[D][n] f64*/, double* sgn, uint8_t* vis);
+struct AdamStep {
+    float lr[kMaxD];
+    float b1, b2, eps, omb1, omb2;
+    float inv_bc1, inv_bc2;
+    float rho[kMaxD];
+    int has_anchor;
+};
+void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
+void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty);
+
+// ---- consensus (consensus.cu) ------------------------------------------
+void round_pack_q(Ctx* c);
+void round_pack_main(Ctx* c, double alpha, bool relax);
+void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_dev, size_t n_reset, bool diag);
+
+// ---- the step ------------------------------------------------------------
+void ensure_image_buffers(Ctx* c, int W, int H);
+void ensure_pair_capacity(Ctx* c, size_t P);
+void stage_begin(Ctx* c, int stage);
+void stage_end(Ctx* c, int stage);
+
+}  // namespace bsg

@@ -1,0 +1,272 @@
+// K11-K14: consensus round on the shared Gaussians over a compact global
+// slot index. Replaces consensus_average / dual_update / residuals
+// (admm.cpp:71-198), the worker half of apply_broadcast (trainer.cpp:168-223)
+// and the master's gather/broadcast (runtime.cpp:482-570).
+//
+// Sum over owners is a reduction (NCCL AllReduce over NVLink, or an in-order
+// sum for a single-process group), so every block ends the round holding z
+// for every slot: there is no master hop. The quaternion sign alignment to the
+// lowest-id owner (admm.cpp:100-106) needs that owner's q first, so a 4-float
+// pre-reduction publishes it. HBM-bound element-wise kernels.
+#include <cfloat>
+
+#include "bsg_internal.cuh"
+
+namespace bsg {
+namespace {
+
+__device__ __forceinline__ float relaxed(float x, float zp, float alpha, bool blend) {
+    // admm.hpp:38-41: alpha == 1 returns x bitwise.
+    if (!blend || alpha == 1.0f) return x;
+    return alpha * x + (1.0f - alpha) * zp;
+}
+
+__global__ void pack_q_kernel(const float* __restrict__ x, size_t cap, const uint32_t* __restrict__ rows,
+                              const uint32_t* __restrict__ slots, const uint8_t* __restrict__ first, size_t ns,
+                              size_t S, float* __restrict__ qref) {
+    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (j >= ns || !first[j]) return;
+    const uint32_t r = rows[j], s = slots[j];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) qref[c * S + s] = x[(kRot + c) * cap + r];
+}
+
+__global__ void pack_main_kernel(const float* __restrict__ x, size_t cap, int D, const uint32_t* __restrict__ rows,
+                                 const uint32_t* __restrict__ slots, const uint8_t* __restrict__ first, size_t ns,
+                                 size_t S, const float* __restrict__ qref, const float* __restrict__ zprev,
+                                 const uint8_t* __restrict__ in_zprev, float alpha, int relax,
+                                 float* __restrict__ pack) {
+    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (j >= ns) return;
+    const uint32_t r = rows[j], s = slots[j];
+    float q[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) q[c] = x[(kRot + c) * cap + r];
+    float flip = 0.f;
+    if (!first[j]) {
+        const float dot = ((q[0] * qref[s] + q[1] * qref[S + s]) + q[2] * qref[2 * S + s]) + q[3] * qref[3 * S + s];
+        if (dot < 0.f) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[c] = -q[c];
+            flip = 1.f;
+        }
+    }
+    const bool blend = relax && in_zprev[s];
+    for (int c = 0; c < D; ++c) {
+        const float v = (c >= kRot && c < kRot + 4) ? q[c - kRot] : x[c * cap + r];
+        pack[c * S + s] = relaxed(v, blend ? zprev[c * S + s] : 0.f, alpha, blend);
+    }
+    pack[static_cast<size_t>(D) * S + s] = flip;
+}
+
+__device__ __forceinline__ void block_add(double v, double* dst, double* s_red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_red[w];
+        if (t != 0.0) atomicAdd(dst, t);
+    }
+}
+
+// z = sum / owners for every slot; dual residual over slots in z_prev
+// (admm.cpp:183-198); flip count; z_prev := z.
+__global__ __launch_bounds__(256) void unpack_slots_kernel(const float* __restrict__ pack, int D, size_t S,
+                                                           const uint32_t* __restrict__ owners, float* __restrict__ zslot,
+                                                           float* __restrict__ zprev, uint8_t* __restrict__ in_zprev,
+                                                           const float* __restrict__ rho, double* __restrict__ scal) {
+    __shared__ double s_red[8];
+    const size_t s = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    double d2 = 0.0, flips = 0.0;
+    if (s < S) {
+        const float inv = 1.0f / static_cast<float>(owners[s]);
+        const bool had = in_zprev[s] != 0;
+        for (int c = 0; c < D; ++c) {
+            const float zv = pack[c * S + s] * inv;
+            if (had) {
+                const double dv = static_cast<double>(rho[c]) * (static_cast<double>(zv) - zprev[c * S + s]);
+                d2 += dv * dv;
+            }
+            zslot[c * S + s] = zv;
+            zprev[c * S + s] = zv;
+        }
+        in_zprev[s] = 1;
+        flips = pack[static_cast<size_t>(D) * S + s] > 0.f ? 1.0 : 0.0;
+    }
+    block_add(d2, &scal[1], s_red);
+    __syncthreads();
+    block_add(flips, &scal[2], s_red);
+}
+
+// Worker half (trainer.cpp:186-222): x_hat = relaxed(x, anchor) WITHOUT the
+// sign flip, u += x_hat - z, reset flipped / listed slots, anchor := z; plus
+// this block's share of the primal residual (raw x, admm.cpp:151-165).
+__global__ __launch_bounds__(256) void dual_update_kernel(const float* __restrict__ x, size_t cap, int D,
+                                                          const uint32_t* __restrict__ rows,
+                                                          const uint32_t* __restrict__ slots, size_t ns, size_t S,
+                                                          const float* __restrict__ pack,
+                                                          const float* __restrict__ zslot,
+                                                          const uint8_t* __restrict__ slot_reset, float alpha,
+                                                          int relax, float* __restrict__ z, float* __restrict__ u,
+                                                          double* __restrict__ scal) {
+    __shared__ double s_red[8];
+    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    double p2 = 0.0;
+    if (j < ns) {
+        const uint32_t r = rows[j], s = slots[j];
+        const bool reset = pack[static_cast<size_t>(D) * S + s] > 0.f || (slot_reset && slot_reset[s]);
+        for (int c = 0; c < D; ++c) {
+            const float xv = x[c * cap + r];
+            const float zn = zslot[c * S + s];
+            const float xh = relaxed(xv, z[c * ns + j], alpha, relax != 0);
+            const double dr = static_cast<double>(xv) - zn;
+            p2 += dr * dr;
+            u[c * ns + j] = reset ? 0.f : u[c * ns + j] + (xh - zn);
+            z[c * ns + j] = zn;
+        }
+    }
+    block_add(p2, &scal[0], s_red);
+}
+
+// Diagnostics: duals packed by slot for the dual-mean check (runtime.cpp:572-606),
+// and +x / -x packed for max_disagreement (admm.cpp:219-243) under a MAX reduction.
+__global__ void pack_duals_kernel(const float* __restrict__ u, int D, const uint32_t* __restrict__ slots, size_t ns,
+                                  size_t S, float* __restrict__ pack) {
+    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (j >= ns) return;
+    const uint32_t s = slots[j];
+    for (int c = 0; c < D; ++c) pack[c * S + s] = u[c * ns + j];
+}
+
+__global__ void pack_minmax_kernel(const float* __restrict__ x, size_t cap, int D, const uint32_t* __restrict__ rows,
+                                   const uint32_t* __restrict__ slots, size_t ns, size_t S, float* __restrict__ pack) {
+    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (j >= ns) return;
+    const uint32_t r = rows[j], s = slots[j];
+    for (int c = 0; c < D; ++c) {
+        const float v = x[c * cap + r];
+        pack[c * S + s] = v;
+        pack[(D + c) * S + s] = -v;
+    }
+}
+
+__global__ void fill_kernel(float* p, size_t n, float v) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ __launch_bounds__(256) void dual_linf_kernel(const float* __restrict__ pack, int D, size_t S,
+                                                        const uint32_t* __restrict__ owners,
+                                                        unsigned long long* __restrict__ out_bits) {
+    const size_t s = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    double m = 0.0;
+    if (s < S) {
+        const double inv = 1.0 / owners[s];
+        for (int c = 0; c < D; ++c) m = fmax(m, fabs(pack[c * S + s] * inv));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+__global__ __launch_bounds__(256) void spread_kernel(const float* __restrict__ pack, int D, size_t S,
+                                                     const uint32_t* __restrict__ owners,
+                                                     unsigned long long* __restrict__ out_bits) {
+    const size_t s = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    double m = 0.0;
+    if (s < S && owners[s] >= 2) {
+        for (int c = 0; c < D; ++c) m = fmax(m, static_cast<double>(pack[c * S + s]) + pack[(D + c) * S + s]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+inline unsigned grid_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
+
+}  // namespace
+
+void round_pack_q(Ctx* c) {
+    BSG_CUDA(cudaMemsetAsync(c->qref, 0, 4 * c->n_slots * sizeof(float), c->stream));
+    if (c->n_shared == 0) return;
+    pack_q_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(c->x, c->cap, c->sh_rows, c->sh_slots, c->sh_first,
+                                                                 c->n_shared, c->n_slots, c->qref);
+    BSG_LAUNCHED(c);
+}
+
+void round_pack_main(Ctx* c, double alpha, bool relax) {
+    BSG_CUDA(cudaMemsetAsync(c->pack, 0, (c->D + 1) * c->n_slots * sizeof(float), c->stream));
+    if (c->n_shared == 0) return;
+    pack_main_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(
+        c->x, c->cap, c->D, c->sh_rows, c->sh_slots, c->sh_first, c->n_shared, c->n_slots, c->qref, c->zprev,
+        c->in_zprev, static_cast<float>(alpha), relax ? 1 : 0, c->pack);
+    BSG_LAUNCHED(c);
+}
+
+// After the reduction of `pack`: slots, dual update, residual partials.
+void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_dev, size_t n_reset, bool diag) {
+    (void)n_reset;
+    (void)diag;
+    BSG_CUDA(cudaMemsetAsync(c->round_scalars, 0, 8 * sizeof(double), c->stream));
+    float rho[kMaxD];
+    for (int k = 0; k < c->D; ++k) {
+        double r = c->rho.rho_f;
+        if (k < kRot) r = c->rho.rho_p;
+        else if (k < kLs) r = c->rho.rho_q;
+        else if (k < kFeat) r = c->rho.rho_s;
+        else if (k == op_comp(c->fd)) r = c->rho.rho_o;
+        rho[k] = static_cast<float>(r);
+    }
+    float* rho_dev = reinterpret_cast<float*>(c->round_scalars + 8);
+    BSG_CUDA(cudaMemcpyAsync(rho_dev, rho, sizeof(rho), cudaMemcpyHostToDevice, c->stream));
+    if (c->n_slots > 0) {
+        unpack_slots_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(c->pack, c->D, c->n_slots, c->slot_owners,
+                                                                         c->zslot, c->zprev, c->in_zprev, rho_dev,
+                                                                         c->round_scalars);
+        BSG_LAUNCHED(c);
+    }
+    if (c->n_shared > 0) {
+        dual_update_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(
+            c->x, c->cap, c->D, c->sh_rows, c->sh_slots, c->n_shared, c->n_slots, c->pack, c->zslot,
+            reset_slots_dev ? c->slot_reset : nullptr, static_cast<float>(alpha), relax ? 1 : 0, c->z, c->u,
+            c->round_scalars);
+        BSG_LAUNCHED(c);
+    }
+}
+
+void round_pack_duals(Ctx* c) {
+    BSG_CUDA(cudaMemsetAsync(c->pack, 0, c->D * c->n_slots * sizeof(float), c->stream));
+    if (c->n_shared == 0) return;
+    pack_duals_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(c->u, c->D, c->sh_slots, c->n_shared, c->n_slots,
+                                                                     c->pack);
+    BSG_LAUNCHED(c);
+}
+
+void round_dual_linf(Ctx* c) {
+    if (c->n_slots == 0) return;
+    dual_linf_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(
+        c->pack, c->D, c->n_slots, c->slot_owners, reinterpret_cast<unsigned long long*>(&c->round_scalars[3]));
+    BSG_LAUNCHED(c);
+}
+
+void round_pack_minmax(Ctx* c) {
+    const size_t n = 2 * c->D * c->n_slots;
+    if (n == 0) return;
+    fill_kernel<<<grid_for(n), 256, 0, c->stream>>>(c->pack, n, -FLT_MAX);
+    BSG_LAUNCHED(c);
+    if (c->n_shared == 0) return;
+    pack_minmax_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(c->x, c->cap, c->D, c->sh_rows, c->sh_slots,
+                                                                      c->n_shared, c->n_slots, c->pack);
+    BSG_LAUNCHED(c);
+}
+
+void round_spread(Ctx* c) {
+    if (c->n_slots == 0) return;
+    spread_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(
+        c->pack, c->D, c->n_slots, c->slot_owners, reinterpret_cast<unsigned long long*>(&c->round_scalars[4]));
+    BSG_LAUNCHED(c);
+}
+
+}  // namespace bsg

@@ -1,0 +1,174 @@
+// K1 preprocess_fwd: per-Gaussian EWA projection, SH colour, footprint rect
+// and tile count. Replaces project_gaussian / project_cloud / footprint /
+// covariance_from_params / sh_color (renderer.cpp:14-40,63-91,121-134;
+// cloud.cpp:162-193).
+//
+// The arithmetic that decides integers (culling, footprint rect, depth order)
+// is FP64 and written in the reference's evaluation order; this file is
+// compiled with --fmad=false so no multiply-add is contracted, which makes the
+// rects and depth keys bit-identical to the FP64 CPU path given the same
+// (FP32-stored) parameters. Outputs consumed by the FP32 blend are rounded
+// once at the end. Bound: HBM (56 B read + 48 B record + 12 B key/count per
+// row) with ~300 FP64 flops per row.
+#include "bsg_internal.cuh"
+
+namespace bsg {
+namespace {
+
+__device__ __forceinline__ int to_int_clamped(double v) {
+    // renderer.cpp:35-38 casts with static_cast<int>; out-of-range values are
+    // pinned to +-2^30 first (identical for every in-range value; see oracle).
+    if (v < -1073741824.0) return -1073741824;
+    if (v > 1073741824.0) return 1073741824;
+    return static_cast<int>(v);
+}
+
+__global__ __launch_bounds__(256) void preprocess_kernel(const float* __restrict__ x, size_t cap, uint32_t n, int fd,
+                                                         DevCam cam, DevRender rc, float4* __restrict__ rec,
+                                                         uint64_t* __restrict__ depth_key, uint32_t* __restrict__ tiles,
+                                                         float4* __restrict__ g2d) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double p0 = x[(kPos + 0) * cap + i], p1 = x[(kPos + 1) * cap + i], p2 = x[(kPos + 2) * cap + i];
+
+    // p_cam = R p + t (camera.hpp:28)
+    double pc[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) pc[r] = ((cam.R[3 * r] * p0 + cam.R[3 * r + 1] * p1) + cam.R[3 * r + 2] * p2) + cam.t[r];
+    uint32_t ntiles = 0;
+    if (pc[2] > rc.near_plane) {
+        // Sigma = (R S)(R S)^T, R from the normalized quaternion (cloud.cpp:162-167, math.hpp:25-44)
+        double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
+               qz = x[(kRot + 3) * cap + i];
+        const double qn = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+        if (qn == 0.0) {
+            qw = 1.0; qx = 0.0; qy = 0.0; qz = 0.0;
+        } else {
+            qw = qw / qn; qx = qx / qn; qy = qy / qn; qz = qz / qn;
+        }
+        double R[3][3];
+        R[0][0] = 1 - 2 * (qy * qy + qz * qz); R[0][1] = 2 * (qx * qy - qw * qz); R[0][2] = 2 * (qx * qz + qw * qy);
+        R[1][0] = 2 * (qx * qy + qw * qz); R[1][1] = 1 - 2 * (qx * qx + qz * qz); R[1][2] = 2 * (qy * qz - qw * qx);
+        R[2][0] = 2 * (qx * qz - qw * qy); R[2][1] = 2 * (qy * qz + qw * qx); R[2][2] = 1 - 2 * (qx * qx + qy * qy);
+        const double s[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])),
+                             exp(static_cast<double>(x[(kLs + 1) * cap + i])),
+                             exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
+        double M[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) M[a][b] = R[a][b] * s[b];
+        double S[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) S[a][b] = (M[a][0] * M[b][0] + M[a][1] * M[b][1]) + M[a][2] * M[b][2];
+
+        // mean2d (camera.hpp:34-36); J (renderer.cpp:14-20); A = J W; cov2d = A S A^T + dilation I
+        const double z = pc[2];
+        const double mx = cam.fx * pc[0] / z + cam.cx;
+        const double my = cam.fy * pc[1] / z + cam.cy;
+        const double iz = 1.0 / z, iz2 = iz * iz;
+        const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * pc[0] * iz2}, {0.0, cam.fy * iz, -cam.fy * pc[1] * iz2}};
+        double A[2][3], T[2][3], C[2][2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                A[r][k] = (J[r][0] * cam.R[k] + J[r][1] * cam.R[3 + k]) + J[r][2] * cam.R[6 + k];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) T[r][k] = (A[r][0] * S[0][k] + A[r][1] * S[1][k]) + A[r][2] * S[2][k];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const double v = (T[r][0] * A[q][0] + T[r][1] * A[q][1]) + T[r][2] * A[q][2];
+                C[r][q] = v + (r == q ? rc.dilation : rc.dilation * 0.0);
+            }
+        // max_eigenvalue_2x2 (renderer.cpp:22-26), footprint (renderer.cpp:33-40)
+        const double mid = 0.5 * (C[0][0] + C[1][1]);
+        const double det = C[0][0] * C[1][1] - C[0][1] * C[1][0];
+        const double lam = mid + sqrt(fmax(0.0, mid * mid - det));
+        const double radius = rc.sigma_extent * sqrt(lam);
+        const int x0 = max(0, to_int_clamped(ceil(mx - radius)));
+        const int x1 = min(cam.W - 1, to_int_clamped(floor(mx + radius)));
+        const int y0 = max(0, to_int_clamped(ceil(my - radius)));
+        const int y1 = min(cam.H - 1, to_int_clamped(floor(my + radius)));
+        if (x0 <= x1 && y0 <= y1) {
+            // minv (renderer.cpp:76-78), colour (cloud.cpp:180-193), opacity (cloud.hpp:55)
+            const double m00 = C[1][1] / det, m01 = -C[0][1] / det, m11 = C[0][0] / det;
+            double col[3];
+            const double* unused = nullptr;
+            (void)unused;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(x[(kFeat + ch) * cap + i]);
+            if (fd >= 12) {
+                const double u0 = p0 - cam.center[0], u1 = p1 - cam.center[1], u2 = p2 - cam.center[2];
+                const double un = sqrt((u0 * u0 + u1 * u1) + u2 * u2);
+                const double d0 = u0 / un, d1 = u1 / un, d2 = u2 / un;
+                const double b0 = -kSh1 * d1, b1 = kSh1 * d2, b2 = -kSh1 * d0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch)
+                    col[ch] += b0 * static_cast<double>(x[(kFeat + 3 + 3 * ch) * cap + i]) +
+                               b1 * static_cast<double>(x[(kFeat + 4 + 3 * ch) * cap + i]) +
+                               b2 * static_cast<double>(x[(kFeat + 5 + 3 * ch) * cap + i]);
+            }
+            const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[op_comp(fd) * cap + i])));
+            const uint32_t r01 = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
+            const uint32_t r23 = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
+            rec[3 * static_cast<size_t>(i) + 0] =
+                make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(m00), static_cast<float>(m01));
+            rec[3 * static_cast<size_t>(i) + 1] =
+                make_float4(static_cast<float>(m11), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
+            rec[3 * static_cast<size_t>(i) + 2] =
+                make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23), 0.f);
+            ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+            depth_key[i] = static_cast<uint64_t>(__double_as_longlong(z));
+            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+            g2d[3 * static_cast<size_t>(i) + 0] = zero;
+            g2d[3 * static_cast<size_t>(i) + 1] = zero;
+            g2d[3 * static_cast<size_t>(i) + 2] = zero;
+        }
+    }
+    tiles[i] = ntiles;
+}
+
+}  // namespace
+
+DevCam make_cam(const bsg_camera& c) {
+    DevCam d{};
+    d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
+    for (int k = 0; k < 9; ++k) d.R[k] = c.R[k];
+    for (int k = 0; k < 3; ++k) d.t[k] = c.t[k];
+    // center = -(R^T t), camera.hpp:31, same evaluation order as the oracle
+    for (int k = 0; k < 3; ++k) d.center[k] = -((c.R[k] * c.t[0] + c.R[3 + k] * c.t[1]) + c.R[6 + k] * c.t[2]);
+    d.W = static_cast<int>(c.width);
+    d.H = static_cast<int>(c.height);
+    d.tiles_x = (d.W + kTile - 1) / kTile;
+    d.tiles_y = (d.H + kTile - 1) / kTile;
+    return d;
+}
+
+DevRender make_render(const bsg_render_config& r) {
+    DevRender d{};
+    d.near_plane = r.near_plane;
+    d.dilation = r.dilation;
+    d.alpha_clamp = r.alpha_clamp;
+    d.tstop = r.transmittance_stop;
+    d.sigma_extent = r.sigma_extent;
+    for (int k = 0; k < 3; ++k) d.bg[k] = static_cast<float>(r.background[k]);
+    d.lambda = r.lambda;
+    return d;
+}
+
+void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
+    if (c->n == 0) return;
+    const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
+    preprocess_kernel<<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
+                                                      c->depth_key, c->tiles, c->g2d);
+    BSG_LAUNCHED(c);
+}
+
+}  // namespace bsg

@@ -1,0 +1,229 @@
+// Hand-written stable LSD radix sort, onesweep style: one histogram pass over
+// the keys for every digit, then one kernel per 8-bit digit that ranks a
+// 4096-key tile in shared memory (warp match-any multisplit, stable), resolves
+// its global digit offsets by decoupled look-back over earlier tiles, and
+// scatters through shared memory so global writes are digit-contiguous.
+// Traffic per pass: read key+value, write key+value.
+#include "bsg_internal.cuh"
+
+namespace bsg {
+namespace {
+
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsItems = 16;
+constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys
+constexpr uint32_t kStAgg = 1u << 30, kStInc = 2u << 30, kStMask = (1u << 30) - 1;
+
+template <typename K>
+__global__ __launch_bounds__(kRsThreads) void radix_hist_kernel(const K* __restrict__ keys, uint32_t n, int begin_bit,
+                                                                int passes, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[8 * 256];
+    for (int i = threadIdx.x; i < passes * 256; i += kRsThreads) sh[i] = 0;
+    __syncthreads();
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kRsThreads + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * kRsThreads) {
+        const K k = keys[i];
+        for (int p = 0; p < passes; ++p) {
+            const uint32_t d = static_cast<uint32_t>(k >> (begin_bit + 8 * p)) & 0xffu;
+            atomicAdd(&sh[p * 256 + d], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += kRsThreads)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// In-place exclusive scan of each pass's 256 bins (one block per pass).
+__global__ void radix_offsets_kernel(uint32_t* hist) {
+    __shared__ uint32_t s[256];
+    uint32_t* h = hist + blockIdx.x * 256;
+    const uint32_t v = h[threadIdx.x];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+        const uint32_t y = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+        __syncthreads();
+        s[threadIdx.x] += y;
+        __syncthreads();
+    }
+    h[threadIdx.x] = s[threadIdx.x] - v;
+}
+
+template <typename K>
+__global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                              K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                              uint32_t n, int shift,
+                                                              const uint32_t* __restrict__ pass_offsets,
+                                                              uint32_t* status, uint32_t* ticket) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K* s_keys = reinterpret_cast<K*>(smem_raw);
+    uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kRsTile);
+    __shared__ uint32_t s_whist[kRsWarps][256];
+    __shared__ uint32_t s_start[256];
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_scan[kRsWarps];
+    __shared__ uint32_t s_tile;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < kRsWarps * 256; i += kRsThreads) (&s_whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t tile_base = static_cast<uint64_t>(tile) * kRsTile;
+
+    // Warp-striped load: within a warp, item j of lane l is key w*512 + j*32 + l,
+    // so processing j in order and ranking lanes in order is the input order.
+    K k[kRsItems];
+    uint32_t val[kRsItems];
+    uint32_t rank[kRsItems];
+    uint32_t dig[kRsItems];
+#pragma unroll
+    for (int j = 0; j < kRsItems; ++j) {
+        const uint64_t i = tile_base + static_cast<uint64_t>(warp) * (32 * kRsItems) + j * 32 + lane;
+        if (i < n) {
+            k[j] = kin[i];
+            val[j] = vin[i];
+            dig[j] = static_cast<uint32_t>(k[j] >> shift) & 0xffu;
+        } else {
+            k[j] = 0;
+            val[j] = 0;
+            dig[j] = 256u;  // never matches a real digit
+        }
+    }
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kRsItems; ++j) {
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[j]);
+        uint32_t base = 0;
+        if (dig[j] < 256u) base = s_whist[warp][dig[j]];
+        rank[j] = base + __popc(peers & lt_mask);
+        __syncwarp();
+        if (dig[j] < 256u && (__ffs(peers) - 1) == lane) s_whist[warp][dig[j]] = base + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // Per digit (thread = digit): exclusive prefix over warps, tile count.
+    const int d = threadIdx.x;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) {
+        const uint32_t c = s_whist[w][d];
+        s_whist[w][d] = cnt;
+        cnt += c;
+    }
+    // Publish this tile's count, then look back for the global prefix.
+    volatile uint32_t* st = status;
+    if (tile == 0) {
+        atomicExch(&status[d], kStInc | cnt);
+    } else {
+        atomicExch(&status[static_cast<uint64_t>(tile) * 256 + d], kStAgg | cnt);
+    }
+    // Block-local exclusive scan over digits (for the shared-memory scatter).
+    {
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_scan[warp] = inc;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; ++w) wp += s_scan[w];
+        s_start[d] = wp + inc - cnt;
+    }
+    uint32_t prefix = 0;
+    if (tile > 0) {
+        int64_t p = static_cast<int64_t>(tile) - 1;
+        while (p >= 0) {
+            uint32_t s;
+            do {
+                s = st[static_cast<uint64_t>(p) * 256 + d];
+            } while ((s & ~kStMask) == 0);
+            prefix += s & kStMask;
+            if (s & kStInc) break;
+            --p;
+        }
+        atomicExch(&status[static_cast<uint64_t>(tile) * 256 + d], kStInc | (prefix + cnt));
+    }
+    s_base[d] = pass_offsets[d] + prefix;
+    __syncthreads();
+
+#pragma unroll
+    for (int j = 0; j < kRsItems; ++j) {
+        if (dig[j] < 256u) {
+            const uint32_t pos = s_start[dig[j]] + s_whist[warp][dig[j]] + rank[j];
+            s_keys[pos] = k[j];
+            s_vals[pos] = val[j];
+        }
+    }
+    __syncthreads();
+    const uint64_t rem = static_cast<uint64_t>(n) - tile_base;
+    const uint32_t valid = rem < static_cast<uint64_t>(kRsTile) ? static_cast<uint32_t>(rem) : static_cast<uint32_t>(kRsTile);
+    for (uint32_t i = threadIdx.x; i < valid; i += kRsThreads) {
+        const K key = s_keys[i];
+        const uint32_t dd = static_cast<uint32_t>(key >> shift) & 0xffu;
+        const uint32_t out = s_base[dd] + (i - s_start[dd]);
+        kout[out] = key;
+        vout[out] = s_vals[i];
+    }
+}
+
+template <typename K>
+void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel) {
+    *sel = 0;
+    if (n <= 1) return;
+    if (n >= (1u << 30)) throw Error{BSG_ERR_CAPACITY, "radix sort supports < 2^30 keys"};
+    const int passes = (end_bit - begin_bit + 7) / 8;
+    const uint32_t tiles = (n + kRsTile - 1) / kRsTile;
+    const size_t status_words = static_cast<size_t>(tiles) * 256;
+    const size_t need = (status_words + 64) * sizeof(uint32_t);
+    if (c->radix_status_cap < need) {
+        if (c->radix_status) cudaFree(c->radix_status);
+        BSG_CUDA(cudaMalloc(&c->radix_status, need * 2));
+        c->radix_status_cap = need * 2;
+    }
+    BSG_CUDA(cudaMemsetAsync(c->radix_hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
+    const int hist_blocks = static_cast<int>(std::min<uint32_t>(148u * 4u, (n + kRsThreads - 1) / kRsThreads));
+    radix_hist_kernel<K><<<hist_blocks, kRsThreads, 0, c->stream>>>(keys[0], n, begin_bit, passes, c->radix_hist);
+    BSG_LAUNCHED(c);
+    // Pass skipping needs the histogram on the host (one small copy).
+    static thread_local uint32_t h_hist[8 * 256];
+    BSG_CUDA(cudaMemcpyAsync(h_hist, c->radix_hist, passes * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    radix_offsets_kernel<<<passes, 256, 0, c->stream>>>(c->radix_hist);
+    BSG_LAUNCHED(c);
+    BSG_CUDA(cudaStreamSynchronize(c->stream));
+    const size_t smem = (sizeof(K) + sizeof(uint32_t)) * kRsTile;
+    BSG_CUDA(cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int cur = 0;
+    for (int p = 0; p < passes; ++p) {
+        bool trivial = false;
+        for (int d = 0; d < 256; ++d)
+            if (h_hist[p * 256 + d] == n) trivial = true;
+        if (trivial) continue;
+        uint32_t* ticket = c->radix_status;
+        uint32_t* status = c->radix_status + 64;
+        BSG_CUDA(cudaMemsetAsync(c->radix_status, 0, need, c->stream));
+        onesweep_kernel<K><<<tiles, kRsThreads, smem, c->stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
+                                                                   begin_bit + 8 * p, c->radix_hist + p * 256, status,
+                                                                   ticket);
+        BSG_LAUNCHED(c);
+        cur ^= 1;
+    }
+    *sel = cur;
+}
+
+}  // namespace
+
+void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel) {
+    radix_sort<uint64_t>(c, keys, vals, n, begin_bit, end_bit, sel);
+}
+
+void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel) {
+    radix_sort<uint32_t>(c, keys, vals, n, begin_bit, end_bit, sel);
+}
+
+}  // namespace bsg

@@ -1,0 +1,186 @@
+// Single-pass exclusive scan with decoupled look-back, and the stable
+// compaction of visible splats built on it. Both are HBM-bound streaming
+// passes: one read of the input, one write of the output.
+#include "bsg_internal.cuh"
+
+namespace bsg {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr uint32_t kFlagAgg = 1u, kFlagInc = 2u;
+
+__device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_t v) {
+    return (static_cast<unsigned long long>(flag) << 32) | v;
+}
+
+__device__ __forceinline__ void publish(unsigned long long* st, uint32_t flag, uint32_t v) {
+    atomicExch(st, pack_status(flag, v));
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+        if (lane == kScanThreads / 32 - 1) *total = wi;
+    }
+    __syncthreads();
+    return s_warp[warp] + inc - v;
+}
+
+// Warp 0 walks predecessors 32 at a time until it meets an inclusive prefix.
+__device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32_t tile) {
+    const int lane = threadIdx.x & 31;
+    uint32_t prefix = 0;
+    int64_t window = static_cast<int64_t>(tile) - 1;
+    while (window >= 0) {
+        const int64_t p = window - lane;
+        unsigned long long st = 0;
+        uint32_t flag = kFlagInc;  // lanes past tile 0 act as an empty inclusive prefix
+        if (p >= 0) {
+            do {
+                st = *reinterpret_cast<volatile unsigned long long*>(&status[p]);
+                flag = static_cast<uint32_t>(st >> 32);
+            } while (flag == 0);
+        }
+        const uint32_t inc_mask = __ballot_sync(0xffffffffu, flag == kFlagInc);
+        const int stop = __ffs(inc_mask) - 1;  // nearest predecessor with an inclusive prefix
+        uint32_t val = (p >= 0 && (inc_mask == 0 || lane <= stop)) ? static_cast<uint32_t>(st) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (inc_mask != 0) break;
+        window -= 32;
+    }
+    return prefix;
+}
+
+// MODE 0: plain exclusive scan of in[gather ? gather[i] : i].
+// MODE 1: compaction of rows with tiles[i] > 0 (in = tiles), emits keys/rows.
+template <int MODE>
+__global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __restrict__ in,
+                                                            const uint32_t* __restrict__ gather,
+                                                            uint32_t* __restrict__ out, uint32_t n,
+                                                            unsigned long long* status, uint32_t* ticket,
+                                                            uint32_t* total_out, const uint64_t* __restrict__ keys,
+                                                            uint64_t* __restrict__ out_keys,
+                                                            uint32_t* __restrict__ out_rows) {
+    __shared__ uint32_t s_tile, s_prefix, s_total;
+    __shared__ uint32_t s_warp[kScanThreads / 32];
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t base = static_cast<uint64_t>(tile) * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint64_t i = base + k;
+        uint32_t x = 0;
+        if (i < n) {
+            if (MODE == 1) {
+                x = in[i] > 0 ? 1u : 0u;
+            } else {
+                x = in[gather ? gather[i] : i];
+            }
+        }
+        v[k] = x;
+        sum += x;
+    }
+    const uint32_t tprefix = block_exclusive(sum, s_warp, &s_total);
+    if (threadIdx.x < 32) {
+        const uint32_t total = s_total;
+        if (tile == 0) {
+            if (threadIdx.x == 0) {
+                publish(&status[0], kFlagInc, total);
+                s_prefix = 0;
+            }
+        } else {
+            if (threadIdx.x == 0) publish(&status[tile], kFlagAgg, total);
+            const uint32_t prefix = look_back(status, tile);
+            if (threadIdx.x == 0) {
+                publish(&status[tile], kFlagInc, prefix + total);
+                s_prefix = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (static_cast<uint64_t>(tile) + 1) * kScanTile >= n && total_out) *total_out = s_prefix + s_total;
+    uint32_t run = s_prefix + tprefix;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const uint64_t i = base + k;
+        if (i < n) {
+            if (MODE == 1) {
+                if (v[k]) {
+                    out_keys[run] = keys[i];
+                    out_rows[run] = static_cast<uint32_t>(i);
+                }
+            } else {
+                out[i] = run;
+            }
+        }
+        run += v[k];
+    }
+}
+
+void prepare_status(Ctx* c, uint32_t tiles) {
+    const size_t need = (static_cast<size_t>(tiles) + 2) * sizeof(unsigned long long);
+    if (c->scan_status_cap < need) {
+        if (c->scan_status) cudaFree(c->scan_status);
+        BSG_CUDA(cudaMalloc(&c->scan_status, need * 2));
+        c->scan_status_cap = need * 2;
+    }
+    BSG_CUDA(cudaMemsetAsync(c->scan_status, 0, need, c->stream));
+}
+
+}  // namespace
+
+void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,
+                        uint32_t* total_dev) {
+    if (n == 0) {
+        BSG_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), c->stream));
+        return;
+    }
+    const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
+    prepare_status(c, tiles);
+    auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
+    auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
+    scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
+                                                          nullptr, nullptr);
+    BSG_LAUNCHED(c);
+}
+
+void compact_visible(Ctx* c, uint32_t n) {
+    if (n == 0) {
+        BSG_CUDA(cudaMemsetAsync(&c->counters->visible, 0, sizeof(uint32_t), c->stream));
+        return;
+    }
+    const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
+    prepare_status(c, tiles);
+    auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
+    auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
+    scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, nullptr, n, status, ticket,
+                                                          &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0]);
+    BSG_LAUNCHED(c);
+}
+
+}  // namespace bsg

