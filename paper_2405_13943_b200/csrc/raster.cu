@@ -59,7 +59,8 @@ __global__ __launch_bounds__(256) void ranges_kernel(const uint32_t* __restrict_
 __global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __restrict__ ranges,
                                                                  const uint32_t* __restrict__ pval,
                                                                  const float4* __restrict__ rec, int W, int H,
-                                                                 int tiles_x, float tstop, float aclamp, float bg0,
+                                                                 int tiles_x, double tstop, float aclamp,
+                                                                 double aclamp_d, float bg0,
                                                                  float bg1, float bg2, float* __restrict__ out_rgb,
                                                                  float* __restrict__ out_T,
                                                                  uint32_t* __restrict__ out_n,
@@ -70,7 +71,13 @@ __global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __
     const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
+    // The stop decision tracks T in FP64 like the reference: stacked clamped
+    // splats give T = (1 - 0.99)^k exactly at the 1e-4 threshold (renderer
+    // KAT test_renderer.cpp:272-282), which FP32 would cross one splat early.
+    // Colour accumulation stays FP32.
     float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    double Td = 1.0;
+    const double oma_clamp = 1.0 - static_cast<double>(aclamp_d);
     uint32_t n = 0, last = 0;
     bool done = !inside;
     const float fx = static_cast<float>(px), fy = static_cast<float>(py);
@@ -90,7 +97,7 @@ __global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __
             int x0, x1, y0, y1;
             unpack_rect(c, x0, x1, y0, y1);
             if (px < x0 || px > x1 || py < y0 || py > y1) continue;
-            if (T < tstop) {
+            if (Td < tstop) {
                 done = true;
                 break;
             }
@@ -98,12 +105,16 @@ __global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __
             const float dx = fx - a.x, dy = fy - a.y;
             const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
             const float g = __expf(-0.5f * q);
-            const float alpha = fminf(b.y * g, aclamp);
+            const float og = b.y * g;
+            // no float lies in [0.99, float(0.99)), so this is the FP64 clamp test
+            const bool clamped = og >= aclamp;
+            const float alpha = clamped ? aclamp : og;
             const float w = alpha * T;
             c0 += b.z * w;
             c1 += b.w * w;
             c2 += c.x * w;
             T *= 1.f - alpha;
+            Td *= clamped ? oma_clamp : static_cast<double>(1.f - og);  // 1 - og exact for og >= 0.5
             ++n;
             last = start - range.x + j + 1;
         }
@@ -113,7 +124,7 @@ __global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __
         out_rgb[3 * p + 0] = c0 + T * bg0;
         out_rgb[3 * p + 1] = c1 + T * bg1;
         out_rgb[3 * p + 2] = c2 + T * bg2;
-        out_T[p] = T;
+        out_T[p] = static_cast<float>(Td);
         out_n[p] = n;
         out_last[p] = last;
     }
@@ -260,8 +271,9 @@ void launch_ranges(Ctx* c, const DevCam& cam, uint32_t P) {
 void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
     blend_fwd_kernel<<<ntiles, kTileThreads, 0, c->stream>>>(
-        c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.tstop),
-        static_cast<float>(rc.alpha_clamp), rc.bg[0], rc.bg[1], rc.bg[2], c->out_rgb, c->out_T, c->out_n, c->out_last);
+        c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, rc.tstop,
+        static_cast<float>(rc.alpha_clamp), rc.alpha_clamp, rc.bg[0], rc.bg[1], rc.bg[2], c->out_rgb, c->out_T,
+        c->out_n, c->out_last);
     BSG_LAUNCHED(c);
 }
 

@@ -1,0 +1,159 @@
+"""GPU parity of the training step (fused fold + ADMM penalty + Adam,
+trainer.cpp:249-295) and of the consensus round (admm.cpp:71-198,
+trainer.cpp:168-223) against the oracle, through the C-ABI."""
+import numpy as np
+import pytest
+
+import _oracle as orc
+from gpu_helpers import dev_cam, gpu, new_block
+from paper_2405_13943_b200 import api
+from refcases import HostCloud, random_bundle
+
+pytestmark = gpu
+
+
+def toy_scene(seed=3, gaussians=40, cameras=6, size=32, extent=4.0):
+    sc = orc.SynthConfig()
+    sc.seed, sc.gaussians, sc.cameras, sc.image_size, sc.extent = seed, gaussians, cameras, size, extent
+    s = orc.generate_scene(sc)
+    p, c = s.points()
+    init = HostCloud.from_oracle(orc.init_cloud_from_points(p, c, 0, 0.1)).narrowed()
+    return s, init
+
+
+def oracle_cfg(iters, seed=1):
+    tc = orc.TrainerConfig()
+    tc.iterations, tc.seed = iters, seed
+    tc.densify_enabled = False
+    return tc
+
+
+def device_trainer(init, s):
+    b = new_block(init)
+    b.set_views([dev_cam(v) for v in s.views], s.images())
+    b.trainer_init(api.trainer_config(iterations=20))
+    return b
+
+
+def rows_of(hc):
+    return np.concatenate([hc.pos, hc.rot, hc.ls, hc.feat, hc.op[:, None]], 1)
+
+
+def test_view_order_matches_trainer():
+    """S20: the host view sequence equals BlockTrainer's Fisher-Yates draw."""
+    s, init = toy_scene()
+    t = orc.BlockTrainer(0, init.oracle(), s.views, s.images(), [], init.n, oracle_cfg(20))
+    seq = orc.view_sequence(1, 0, len(s.views), 9)
+    for k in range(9):
+        t.train_step()
+        assert t.last_view() == seq[k]
+
+
+@pytest.mark.parametrize("steps", [1, 10])
+def test_train_steps_track_oracle(steps):
+    s, init = toy_scene()
+    tc = oracle_cfg(20)
+    t = orc.BlockTrainer(0, init.oracle(), s.views, s.images(), [], init.n, tc)
+    seq = orc.view_sequence(1, 0, len(s.views), steps)
+    b = device_trainer(init, s)
+    losses = b.train_steps(seq)
+    want_losses = [t.train_step() for _ in range(steps)]
+    np.testing.assert_allclose(losses, want_losses, rtol=2e-4)
+    got = b.download_cloud()
+    want = HostCloud.from_oracle(t.cloud())
+    g = np.concatenate([got["pos"], got["rot"], got["ls"], got["feat"], got["op"][:, None]], 1)
+    w = rows_of(want)
+    err = np.abs(g - w)
+    # Adam moves every coordinate by ~lr per step; FP32 vs FP64 differences are
+    # ~1e-6 except where a near-zero gradient flips sign (bounded by 2 lr).
+    frac_close = np.mean(err <= 1e-5 + 1e-5 * np.abs(w))
+    assert frac_close >= 0.98, frac_close
+    assert err.max() <= 2 * 5e-2 * steps + 1e-5
+    m, v = b.moments()
+    assert np.all(np.isfinite(m)) and np.all(v >= 0)
+    ga, gs = b.densify_stats()
+    assert np.array_equal(gs, np.array(t.grad_seen(), dtype=np.uint32))
+    np.testing.assert_allclose(ga, t.grad_accum(), rtol=5e-3, atol=1e-9)
+
+
+def test_penalty_pulls_invisible_gaussian_on_device():
+    """test_trainer.cpp:308-338 through the fused kernel."""
+    c = HostCloud(np.array([0], np.uint64), [[0, 0, -10]], [[1.0, 0, 0, 0]], [[-1, -1, -1]], [[1, 1, 1]], [2.0])
+    cam = orc.look_at([0, 0, 20], [0, 0, 25], [0, 1, 0], 10, 10, 4, 4, 8, 8)
+    b = new_block(c)
+    b.set_views([dev_cam(cam)], [np.zeros((8, 8, 3))])
+    b.trainer_init(api.trainer_config(iterations=100))
+    b.set_shared([0], [0], [1], [1])
+    z = np.concatenate([c.pos, c.rot, c.ls, c.feat, c.op[:, None]], 1).copy()
+    z[0, 13] = -1.0
+    z[0, 0] = 1.0
+    b.set_anchor(z, z, api.penalties())
+    b.train_steps([0] * 10)
+    got = b.download_cloud()
+    assert abs(got["op"][0] - (-1.0)) < 3.0
+    assert abs(got["pos"][0, 0] - 1.0) < 1.0
+    t = orc.BlockTrainer(0, c.oracle(), [cam], [np.zeros((8, 8, 3))], [0], 1, oracle_cfg(100))
+    zc = c.copy(); zc.op[0] = -1.0; zc.pos[0, 0] = 1.0
+    t.set_anchor(zc.oracle(), orc.Penalties())
+    t.run_iterations(10)
+    want = t.cloud().dict()
+    np.testing.assert_allclose(got["op"], want["op"], atol=1e-4)
+    np.testing.assert_allclose(got["pos"], want["pos"], atol=1e-4)
+
+
+def make_blocks_for_consensus(flip_ids=(3,)):
+    """Two blocks sharing ids {2..7} (block 0 owns 0..7, block 1 owns 2..11)."""
+    a = random_bundle(list(range(0, 8)), 40).narrowed()
+    b = random_bundle(list(range(2, 12)), 41).narrowed()
+    # shared rows of block 1 close to block 0's, with one antipodal quaternion
+    for gid in range(2, 8):
+        ia, ib = gid, gid - 2
+        b.pos[ib] = a.pos[ia] + 0.01 * (gid % 3)
+        b.rot[ib] = a.rot[ia] * (-1.0 if gid in flip_ids else 1.0)
+    b = b.narrowed()
+    shared = list(range(2, 8))
+    zprev = random_bundle(shared, 42).narrowed()
+    return a, b, shared, zprev
+
+
+def setup_device_block(hc, shared, block_id, zprev, rho):
+    dev = new_block(hc)
+    rows = [int(np.searchsorted(hc.ids, g)) for g in shared]
+    slots = list(range(len(shared)))
+    first = [1 if block_id == 0 else 0] * len(shared)
+    dev.set_shared(rows, slots, first, [2] * len(shared))
+    zp = rows_of(zprev)
+    dev.set_anchor(zp, zp, rho)
+    return dev
+
+
+@pytest.mark.parametrize("relax", [False, True])
+def test_consensus_round_matches_oracle(relax):
+    a, b, shared, zprev = make_blocks_for_consensus()
+    rho = api.penalties()
+    da = setup_device_block(a, shared, 0, zprev, rho)
+    db = setup_device_block(b, shared, 1, zprev, rho)
+    alpha = 1.6
+    res = api.group_consensus_round([da, db], alpha, relax, diagnostics=True)
+    sa = orc.slice_by_ids(a.oracle(), shared)
+    sb = orc.slice_by_ids(b.oracle(), shared)
+    z, flipped = orc.consensus_average([(0, sa), (1, sb)], relax, zprev.oracle(), alpha)
+    zr = rows_of(HostCloud.from_oracle(z))
+    np.testing.assert_allclose(da.consensus(), zr, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(db.consensus(), zr, rtol=1e-6, atol=1e-6)
+    assert res["flipped"] == len(flipped) == 1
+    p, d = orc.residuals([(0, sa), (1, sb)], z, zprev.oracle(), orc.Penalties())
+    assert res["primal"] == pytest.approx(p, rel=1e-5)
+    assert res["dual"] == pytest.approx(d, rel=1e-4)
+    # duals: u = 0 + x_hat - z (x_hat relaxed against the anchor, no flip), flipped ids reset
+    for dev, hc in ((da, a), (db, b)):
+        x = rows_of(HostCloud.from_oracle(orc.slice_by_ids(hc.oracle(), shared)))
+        xh = alpha * x + (1 - alpha) * rows_of(zprev) if relax else x
+        want_u = xh - zr
+        for k, gid in enumerate(shared):
+            if gid in flipped:
+                want_u[k] = 0
+        np.testing.assert_allclose(dev.duals(), want_u, rtol=1e-5, atol=2e-6)
+        np.testing.assert_allclose(dev.anchor(), zr, rtol=1e-6, atol=1e-6)
+    # dual-mean diagnostic (runtime.cpp:572-606) and disagreement (admm.cpp:219-243)
+    assert res["max_disagreement"] == pytest.approx(orc.max_disagreement([(0, sa), (1, sb)]), rel=1e-5)
