@@ -1,0 +1,408 @@
+"""Benchmark of the DOGS block-training hot path on B200.
+
+Workload (BASELINE.json configs[1], SURVEY §8(d) cfg 2): synthetic
+Mill-19-like scene, 2M Gaussians in a 100 x 20 x 100 box, 64 views at
+1024x768 on an aerial grid, K = N blocks (one per GPU, recursive longer-axis
+split with expansion s = 1.4, consensus every `interval` iterations over NCCL).
+A step is one training iteration of every block (render fwd, L1+SSIM loss,
+render bwd, fused fold + ADMM penalty + Adam) plus the amortised consensus
+round. Ground truth is rendered once by the device forward from the
+generating cloud; training starts from a perturbed copy.
+
+`--impl reference` times the reference's CPU algorithm (the oracle port,
+oracle/_oracle: single-threaded FP64 BlockTrainer::train_step, as the
+reference runs one thread per block) on the same block, on rank 0.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+CFG = dict(n=2_000_000, width=1024, height=768, views=64, extent=100.0, scale=1.4, seed=42)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--interval", type=int, default=25, help="consensus interval (iterations)")
+    p.add_argument("--n", type=int, default=CFG["n"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--views", type=int, default=CFG["views"], help="fewer views for profiling runs only")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_block(rank, world, n, device, n_views=CFG["views"]):
+    """Scene -> plan -> this rank's block on the device, GT rendered on device."""
+    from paper_2405_13943_b200 import api
+    from paper_2405_13943_b200.scene import aerial_scene, perturbed_init
+
+    cloud, cams = aerial_scene(n, CFG["width"], CFG["height"], CFG["views"], CFG["extent"], CFG["seed"])
+    cams = cams[:n_views]
+    init = perturbed_init(cloud, CFG["seed"])
+    centers = np.array([c.center() for c in cams])
+    plan = api.Plan(cloud["ids"], cloud["pos"], centers, world, CFG["scale"])
+    ids, views = plan.block(rank)
+    sel = ids.astype(np.int64)  # ids are 0..n-1 = row indices of the global cloud
+    # ground truth of this block's views: the generating cloud rendered on device
+    gt_block = api.Block(device, 3)
+    gt_block.upload_cloud(cloud["ids"], cloud["pos"], cloud["rot"], cloud["ls"], cloud["feat"], cloud["op"])
+    view_cams = [cams[v].device() for v in views]
+    gts = [gt_block.render(c)[0] for c in view_cams]
+    gt_block.close()
+    blk = api.Block(device, 3)
+    blk.upload_cloud(init["ids"][sel], init["pos"][sel], init["rot"][sel], init["ls"][sel], init["feat"][sel],
+                     init["op"][sel])
+    blk.set_views(view_cams, gts)
+    blk.trainer_init(api.trainer_config(iterations=30000))
+    sids, cnt, _ = plan.shared()
+    rows, slots, first = plan.block_shared(rank)
+    if world > 1:
+        blk.set_shared(rows, slots, first, cnt)
+        D = 14
+        init_rows = np.concatenate([init["pos"], init["rot"], init["ls"], init["feat"], init["op"][:, None]], 1)
+        zprev = init_rows[sids.astype(np.int64)]
+        blk.set_anchor(zprev[slots], zprev, api.penalties())
+    return blk, view_cams, gts, dict(block_gaussians=len(ids), block_views=len(views), shared_ids=len(sids),
+                                     block_shared=len(rows))
+
+
+def algorithmic_bytes(stage, n, V, P, HW, shared):
+    """SURVEY §8(d) fused-minimum byte accounting per launch of the stage's kernel."""
+    if stage == "fold_adam":
+        return 340 * n + 64 * V + 112 * shared       # x,m,v read+write (14 f32 each), tiles, g2d, densify stats, z,u
+    if stage == "preprocess":
+        return 60 * n + 104 * V                     # params read, tiles write; record + key + zeroed grads
+    if stage == "blend_fwd":
+        return 52 * P + 24 * HW                     # pair index + 48 B record per pair; rgb,T,n,last per pixel
+    if stage == "blend_bwd":
+        return 52 * P + 20 * HW + 48 * V            # records, per-pixel T,last,dL/dC, one gradient record per splat
+    if stage == "loss_ssim":
+        return 24 * HW + 36 * HW + 36 * HW + 24 * HW + 12 * HW
+    if stage == "depth_sort":
+        return 8 * V + 7 * 24 * V                   # histogram read + passes (key u64 + row u32, read+write)
+    if stage == "tile_sort":
+        return 4 * P + 2 * 16 * P
+    return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2405_13943_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    blk, view_cams, gts, info = build_block(rank, world, args.n, local_rank, args.views)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        blk.comm_init(uid[0], world, rank)
+    nv = len(view_cams)
+    rng = np.random.default_rng(1000 + rank)
+    order = []
+
+    def next_view():
+        nonlocal order
+        if not order:
+            order = list(rng.permutation(nv))
+        return int(order.pop())
+
+    stream = torch.cuda.ExternalStream(blk.stream())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def consensus(it):
+        if world > 1 and it % args.interval == 0:
+            return blk.consensus_round(1.6, True)
+        return None
+
+    # warm-up
+    it = 0
+    for _ in range(args.warmup):
+        blk.train_steps([next_view()], want_losses=False)
+        it += 1
+        consensus(it)
+    blk.enable_stage_timing(True)
+    stage_sum = {}
+    counters_sum = dict(visible=0, pairs=0)
+    round_ms = []
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = blk.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    e0.record(stream)
+    for s in range(args.steps):
+        blk.train_steps([next_view()], want_losses=False)
+        it += 1
+        for k, v in blk.stage_times().items():
+            stage_sum[k] = stage_sum.get(k, 0.0) + v
+        c = blk.step_counters()
+        counters_sum["visible"] += c["visible"]
+        counters_sum["pairs"] += c["pairs"]
+        r = consensus(it)
+        if r is not None:
+            round_ms.append(r["ms"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = blk.launch_count() - launches0
+    elapsed = e0.elapsed_time(e1)
+    t = torch.tensor([elapsed], device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    blk.enable_stage_timing(False)
+
+    # end-to-end: ground truth copied from pinned host memory every step, loss read back
+    pinned = [torch.from_numpy(g.astype(np.float32)).pin_memory() for g in gts]
+    e2e_steps = max(5, args.steps // 2)
+    barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for s in range(e2e_steps):
+        v = next_view()
+        blk.train_step_host(view_cams[v], pinned[v].numpy())
+        it += 1
+        consensus(it)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t2 = torch.tensor([f0.elapsed_time(f1)], device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_ms_step = float(t2.item()) / e2e_steps
+    h2d = 3 * CFG["width"] * CFG["height"] * 4
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    stage_ms = {k: v / args.steps for k, v in stage_sum.items()}
+    dominant = max(stage_ms, key=stage_ms.get)
+    # roofline of the dominant single-kernel stage with a byte model
+    candidates = [k for k in ("fold_adam", "blend_fwd", "blend_bwd", "preprocess", "loss_ssim") if k in stage_ms]
+    roof_stage = max(candidates, key=lambda k: stage_ms[k])
+    V = counters_sum["visible"] / args.steps
+    P = counters_sum["pairs"] / args.steps
+    HW = CFG["width"] * CFG["height"]
+    nb = info["block_gaussians"]
+    bytes_ = algorithmic_bytes(roof_stage, nb, V, P, HW, info["block_shared"])
+    peak, peak_kind = peaks()
+    achieved = bytes_ / (stage_ms[roof_stage] * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(roof_stage)
+        except Exception:
+            traffic = None
+    out = {
+        "metric": "training iters/sec (K=N blocks, 1 block per GPU)",
+        "value": 1000.0 / ms_step,
+        "unit": "iters/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 (FP64 projection)",
+        "data": "synthetic (Mill-19-like aerial scene, GT rendered on device from the generating cloud)",
+        "config": {"workload": "cfg2: 2M Gaussians, 64 views 1024x768, K=N blocks, s=1.4" if args.n == CFG["n"]
+                   else f"cfg2-shape with {args.n} Gaussians", "gaussians": args.n, "width": CFG["width"],
+                   "height": CFG["height"], "views": CFG["views"], "blocks": world, "expand_scale": CFG["scale"],
+                   "consensus_interval": args.interval, "block0_gaussians": nb, "block0_views": info["block_views"],
+                   "shared_ids": info["shared_ids"], "l2": "inputs > L2 (Adam state 2M x 168 B)",
+                   "parallelism": f"blocks{world}"},
+        "e2e": {"value": 1000.0 / e2e_ms_step, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8},
+        "gpu_launches": int(launches),
+        "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "dominant_stage": dominant,
+        "visible_per_step": V,
+        "pairs_per_step": P,
+        "consensus_ms_per_round": float(np.mean(round_ms)) if round_ms else 0.0,
+        "consensus_ms_per_iter": (float(np.mean(round_ms)) / args.interval) if round_ms else 0.0,
+        "roofline": {"kernel": roof_stage, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": bytes_,
+                     "peak_source": peak_kind},
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.cpu_steps, args.n)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def oracle_block(n):
+    """The reference algorithm on the same block (K=1 at N=1): FP64 CPU trainer."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import _oracle as orc
+
+    from paper_2405_13943_b200.scene import aerial_scene, perturbed_init
+
+    cloud, cams = aerial_scene(n, CFG["width"], CFG["height"], CFG["views"], CFG["extent"], CFG["seed"])
+    init = perturbed_init(cloud, CFG["seed"])
+    oc = orc.Cloud(init["ids"], init["pos"], init["rot"], init["ls"], init["feat"], init["op"])
+
+    def ocam(c):
+        o = orc.Camera()
+        o.fx, o.fy, o.cx, o.cy = c.fx, c.fy, c.cx, c.cy
+        o.set_rotation_quat(list(c.q))
+        o.t = list(c.t)
+        o.width, o.height = c.width, c.height
+        return o
+
+    cs = [ocam(c) for c in cams]
+    gt = [np.full((CFG["height"], CFG["width"], 3), 0.5) for _ in cs]
+    tc = orc.TrainerConfig()
+    tc.iterations = 30000
+    tc.densify_enabled = False
+    return orc.BlockTrainer(0, oc, cs, gt, [], n, tc)
+
+
+def cpu_baseline(steps, n):
+    tr = oracle_block(n)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        tr.train_step()
+    dt = time.perf_counter() - t0
+    return {"value": steps / dt, "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": f"{steps} FP64 train_step()s of the full cfg2 block ({n} Gaussians, 1024x768, constant-0.5 GT) "
+                      f"by the oracle port, single thread as the reference runs one thread per block; {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    tr = oracle_block(args.n)
+    for _ in range(min(args.warmup, 1)):
+        tr.train_step()
+    t0 = time.perf_counter()
+    done = 0
+    budget = 150.0
+    for _ in range(args.steps):
+        tr.train_step()
+        done += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    dt = time.perf_counter() - t0
+    v = done / dt
+    out = {"metric": "training iters/sec (K=N blocks, 1 block per GPU)", "value": v, "unit": "iters/s",
+           "n_gpus": world, "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": 1000.0 * dt / done,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+           "data": "synthetic (same scene; constant-0.5 GT: the arithmetic per step does not depend on GT content)",
+           "config": {"workload": "cfg2 block 0 (K=1): 2M Gaussians, 1024x768" if args.n == CFG["n"]
+                      else f"cfg2-shape with {args.n} Gaussians", "gaussians": args.n, "blocks": 1},
+           "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "port",
+                            "sample": f"{done} train_step()s (time-capped at {budget:.0f} s), oracle port of the "
+                                      f"reference BlockTrainer, one thread"},
+           "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

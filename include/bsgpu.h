@@ -181,6 +181,25 @@ int bsg_consensus_round(bsg_ctx* ctx, const bsg_round_args* args, bsg_round_resu
  * order without NCCL; runs one round for all of them. */
 int bsg_group_consensus_round(bsg_ctx* const* ctxs, size_t k, const bsg_round_args* args, bsg_round_result* out);
 
+/* ---- block planner (host, splitter.cpp:48-201; runtime.cpp:265-305) ---
+ * Recursive median bipartition along the longer ground axis into k cells,
+ * expansion by `scale` about each cell centre on the ground axes (vertical
+ * axis spans everything), closed-box assignment with nearest-box fallback.
+ * The points are the Gaussian positions (plan_cluster). Shared ids (two or
+ * more owners) get consensus slots in ascending id order. Host-only: no GPU. */
+typedef struct bsg_plan bsg_plan;
+const char* bsg_plan_last_error(void);
+int bsg_plan_create(size_t n, const uint64_t* ids, const double* pos, size_t n_views, const double* view_centers,
+                    uint32_t k, double scale, int vertical_axis, int midpoint_plane, bsg_plan** out);
+void bsg_plan_destroy(bsg_plan* plan);
+int bsg_plan_block_sizes(const bsg_plan* plan, uint32_t block, size_t* n_gaussians, size_t* n_views);
+int bsg_plan_block(const bsg_plan* plan, uint32_t block, uint64_t* ids, uint32_t* views);
+int bsg_plan_boxes(const bsg_plan* plan, double* core_min, double* core_max, double* exp_min, double* exp_max);
+size_t bsg_plan_shared_count(const bsg_plan* plan);
+int bsg_plan_shared(const bsg_plan* plan, uint64_t* ids, uint32_t* owner_count, uint32_t* first_owner);
+int bsg_plan_block_shared(const bsg_plan* plan, uint32_t block, size_t* n_out, uint32_t* rows, uint32_t* slots,
+                          uint8_t* first_owner);
+
 /* ---- measurement ------------------------------------------------------ */
 /* Per-stage device times of the most recent step (CUDA events on the
  * context's stream), milliseconds, in the order of bsg_stage_name(i). */

@@ -106,6 +106,16 @@ SYMBOLS = [
     ("bsg_consensus_round", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_round_result)]),
     ("bsg_group_consensus_round", ctypes.c_int, [ctypes.POINTER(_P), _SZ, ctypes.POINTER(bsg_round_args),
                                                   ctypes.POINTER(bsg_round_result)]),
+    ("bsg_plan_last_error", ctypes.c_char_p, []),
+    ("bsg_plan_create", ctypes.c_int, [_SZ, _U64P, _DP, _SZ, _DP, ctypes.c_uint32, ctypes.c_double, ctypes.c_int,
+                                        ctypes.c_int, ctypes.POINTER(_P)]),
+    ("bsg_plan_destroy", None, [_P]),
+    ("bsg_plan_block_sizes", ctypes.c_int, [_P, ctypes.c_uint32, _SZP, _SZP]),
+    ("bsg_plan_block", ctypes.c_int, [_P, ctypes.c_uint32, _U64P, _U32P]),
+    ("bsg_plan_boxes", ctypes.c_int, [_P, _DP, _DP, _DP, _DP]),
+    ("bsg_plan_shared_count", _SZ, [_P]),
+    ("bsg_plan_shared", ctypes.c_int, [_P, _U64P, _U32P, _U32P]),
+    ("bsg_plan_block_shared", ctypes.c_int, [_P, ctypes.c_uint32, _SZP, _U32P, _U32P, _U8P]),
     ("bsg_enable_stage_timing", ctypes.c_int, [_P, ctypes.c_int]),
     ("bsg_stage_count", ctypes.c_int, []),
     ("bsg_stage_name", ctypes.c_char_p, [ctypes.c_int]),
@@ -424,3 +434,56 @@ def nccl_unique_id():
     buf = (ctypes.c_uint8 * 128)()
     _check(_lib.bsg_nccl_unique_id(buf))
     return bytes(buf)
+
+
+class Plan:
+    """Block partition + consensus slots (splitter.cpp:48-201, runtime.cpp:265-305),
+    computed by the native host planner in libbsgpu.so."""
+
+    def __init__(self, ids, pos, view_centers, k, scale, vertical_axis=1, midpoint_plane=False):
+        load_library()
+        ids = np.ascontiguousarray(ids, np.uint64)
+        pos = _f64(pos).reshape(len(ids), 3)
+        vc = _f64(view_centers).reshape(-1, 3) if len(view_centers) else np.zeros((0, 3))
+        h = ctypes.c_void_p()
+        st = _lib.bsg_plan_create(len(ids), _ptr(ids, ctypes.c_uint64), _ptr(pos, ctypes.c_double), len(vc),
+                                  _ptr(vc, ctypes.c_double), k, float(scale), vertical_axis,
+                                  1 if midpoint_plane else 0, ctypes.byref(h))
+        if st != BSG_OK:
+            msg = _lib.bsg_plan_last_error().decode()
+            raise InvalidArgument(msg) if st == BSG_ERR_INVALID_ARGUMENT else BsgError(msg)
+        self.h = h
+        self.k = k
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.bsg_plan_destroy(self.h)
+            self.h = None
+
+    def block(self, b):
+        ng, nv = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.bsg_plan_block_sizes(self.h, b, ctypes.byref(ng), ctypes.byref(nv))
+        ids, views = np.zeros(max(ng.value, 1), np.uint64), np.zeros(max(nv.value, 1), np.uint32)
+        _lib.bsg_plan_block(self.h, b, _ptr(ids, ctypes.c_uint64), _ptr(views, ctypes.c_uint32))
+        return ids[:ng.value], views[:nv.value]
+
+    def boxes(self):
+        k = self.k
+        out = [np.zeros((k, 3)) for _ in range(4)]
+        _lib.bsg_plan_boxes(self.h, *[_ptr(o, ctypes.c_double) for o in out])
+        return dict(core_min=out[0], core_max=out[1], exp_min=out[2], exp_max=out[3])
+
+    def shared(self):
+        s = _lib.bsg_plan_shared_count(self.h)
+        ids, cnt, first = np.zeros(max(s, 1), np.uint64), np.zeros(max(s, 1), np.uint32), np.zeros(max(s, 1), np.uint32)
+        _lib.bsg_plan_shared(self.h, _ptr(ids, ctypes.c_uint64), _ptr(cnt, ctypes.c_uint32), _ptr(first, ctypes.c_uint32))
+        return ids[:s], cnt[:s], first[:s]
+
+    def block_shared(self, b):
+        ids, _ = self.block(b)
+        n = ctypes.c_size_t()
+        rows, slots, first = (np.zeros(max(len(ids), 1), np.uint32), np.zeros(max(len(ids), 1), np.uint32),
+                              np.zeros(max(len(ids), 1), np.uint8))
+        _lib.bsg_plan_block_shared(self.h, b, ctypes.byref(n), _ptr(rows, ctypes.c_uint32), _ptr(slots, ctypes.c_uint32),
+                                   _ptr(first, ctypes.c_uint8))
+        return rows[:n.value], slots[:n.value], first[:n.value]

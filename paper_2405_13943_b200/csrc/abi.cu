@@ -75,7 +75,7 @@ void dev_alloc(T** p, size_t count) {
 void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
-    void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d,
+    void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->gbuf,
                     c->anchor_of_row, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
@@ -109,6 +109,7 @@ void alloc_rows(Ctx* c, size_t n) {
     dev_alloc(&c->depth_key, cap);
     dev_alloc(&c->tiles, cap);
     dev_alloc(&c->g2d, 3 * cap);
+    dev_alloc(&c->gbuf, c->D * cap);
     dev_alloc(&c->anchor_of_row, cap);
     dev_alloc(&c->vkey[0], cap);
     dev_alloc(&c->vkey[1], cap);
@@ -299,6 +300,9 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     stage_begin(c, kStBlendBwd);
     launch_blend_bwd(c, cam, rc);
     stage_end(c, kStBlendBwd);
+    stage_begin(c, kStFold);
+    launch_fold_visible(c, cam, c->last_counters.visible);
+    stage_end(c, kStFold);
     stage_begin(c, kStAdam);
     const AdamStep st = make_adam_step(c);
     launch_adam(c, cam, st, loss_dev, 0);
@@ -589,9 +593,9 @@ int bsg_render_backward(bsg_ctx* h, const bsg_camera* cam, const double* gt, con
         BSG_CUDA(cudaMalloc(&gdev, std::max<size_t>(1, c->D * n) * sizeof(double)));
         BSG_CUDA(cudaMalloc(&sdev, std::max<size_t>(1, n) * sizeof(double)));
         BSG_CUDA(cudaMalloc(&vdev, std::max<size_t>(1, n)));
-        stage_begin(c, kStAdam);
+        stage_begin(c, kStFold);
         launch_fold_grads(c, dc, gdev, sdev, vdev);
-        stage_end(c, kStAdam);
+        stage_end(c, kStFold);
         std::vector<double> g(static_cast<size_t>(c->D) * n);
         double l3[3];
         BSG_CUDA(cudaMemcpyAsync(g.data(), gdev, g.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1064,7 +1068,7 @@ int bsg_stage_count(void) { return kStCount; }
 
 const char* bsg_stage_name(int i) {
     static const char* names[kStCount] = {"preprocess", "compact", "depth_sort", "pairs", "tile_sort",
-                                          "ranges", "blend_fwd", "loss_ssim", "blend_bwd", "fold_adam"};
+                                          "ranges", "blend_fwd", "loss_ssim", "blend_bwd", "fold", "adam"};
     return (i >= 0 && i < kStCount) ? names[i] : "";
 }
 

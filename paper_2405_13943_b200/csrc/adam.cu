@@ -1,11 +1,12 @@
-// K9 + K10: fold of the image-space splat gradients to the parameters
-// (renderer.cpp:313-403) fused with the consensus penalty
-// (admm.cpp:11-45, trainer.cpp:257-265), dense Adam on every row
-// (trainer.cpp:120-131,267-281), quaternion canonicalisation (cloud.cpp:82-85)
-// and the densify statistics (trainer.cpp:284-289). One thread per row; the
-// parameter gradient is never written to memory. HBM-bound: per row it reads
-// x, m, v (3 x 4D bytes) and writes them back, plus the 48 B splat gradient
-// record for visible rows and z, u for shared rows.
+// K9 fold + K10 Adam. The fold of the image-space splat gradients to the
+// parameters (renderer.cpp:313-403) runs once per VISIBLE splat over the
+// compacted list (FP64 arithmetic, ~1.5k flops) and writes the parameter
+// gradient rows it touched; the dense Adam (trainer.cpp:120-131,267-281) with
+// the consensus penalty (admm.cpp:11-45, trainer.cpp:257-265) and quaternion
+// canonicalisation (cloud.cpp:82-85) then streams every row once. Keeping the
+// FP64 fold out of the dense kernel keeps the dense kernel a pure HBM stream:
+// per row it reads x, m, v (3 x 4D bytes) and the visible flag, and writes
+// x, m, v back; visible rows add a 4D-byte gradient read, shared rows z and u.
 #include "bsg_internal.cuh"
 
 namespace bsg {
@@ -174,57 +175,69 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
     vis[i] = visible ? 1 : 0;
 }
 
+// Fold over the compacted visible list (V threads): parameter gradient of
+// each visible row into gbuf[D][cap] (FP32), densify statistics.
+__global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, int fd, DevCam cam,
+                                                           const uint32_t* __restrict__ vis_rows, uint32_t V,
+                                                           const float4* __restrict__ g2d, float* __restrict__ gbuf,
+                                                           float* __restrict__ grad_accum,
+                                                           uint32_t* __restrict__ grad_seen) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= V) return;
+    const uint32_t i = vis_rows[p];
+    const int D = 11 + fd;
+    double g[kMaxD];
+#pragma unroll
+    for (int c = 0; c < kMaxD; ++c) g[c] = 0.0;
+    const double s = fold_row(x, cap, i, fd, cam, g2d, g);
+#pragma unroll
+    for (int c = 0; c < kMaxD; ++c)
+        if (c < D) gbuf[static_cast<size_t>(c) * cap + i] = static_cast<float>(g[c]);
+    grad_accum[i] += static_cast<float>(s);
+    grad_seen[i] += 1u;
+}
+
+// Dense Adam over every row (trainer.cpp:267-281): streaming x, m, v in
+// [D][cap] layout (every component access is coalesced); rows not visible
+// this step have a zero render gradient; shared rows add rho (x - z + u).
+template <int D>
 __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
-                                                   size_t cap, uint32_t n, int fd, DevCam cam,
-                                                   const uint32_t* __restrict__ tiles, const float4* __restrict__ g2d,
-                                                   float* __restrict__ grad_accum, uint32_t* __restrict__ grad_seen,
+                                                   size_t cap, uint32_t n, const uint32_t* __restrict__ tiles,
+                                                   const float* __restrict__ gbuf,
                                                    const int32_t* __restrict__ anchor_of_row, const float* __restrict__ z,
                                                    const float* __restrict__ u, size_t n_shared, AdamStep st,
                                                    double* __restrict__ penalty) {
     __shared__ double s_red[8];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int D = 11 + fd;
     double pen = 0.0;
     if (i < n) {
-        double gd[kMaxD];
+        const bool visible = tiles[i] > 0;
+        float xv[D], g[D];
 #pragma unroll
-        for (int c = 0; c < kMaxD; ++c) gd[c] = 0.0;
-        if (tiles[i] > 0) {
-            const double s = fold_row(x, cap, i, fd, cam, g2d, gd);
-            grad_accum[i] += static_cast<float>(s);
-            grad_seen[i] += 1u;
-        }
-        float xv[kMaxD], g[kMaxD];
-#pragma unroll
-        for (int c = 0; c < kMaxD; ++c) {
-            if (c < D) {
-                xv[c] = x[static_cast<size_t>(c) * cap + i];
-                g[c] = static_cast<float>(gd[c]);
-            }
+        for (int c = 0; c < D; ++c) {
+            xv[c] = x[static_cast<size_t>(c) * cap + i];
+            g[c] = visible ? gbuf[static_cast<size_t>(c) * cap + i] : 0.f;
         }
         if (st.has_anchor) {
             const int32_t j = anchor_of_row[i];
             if (j >= 0) {
 #pragma unroll
-                for (int c = 0; c < kMaxD; ++c) {
-                    if (c < D) {
-                        const float d = xv[c] - z[static_cast<size_t>(c) * n_shared + j] + u[static_cast<size_t>(c) * n_shared + j];
-                        pen += 0.5 * static_cast<double>(st.rho[c]) * static_cast<double>(d) * static_cast<double>(d);
-                        g[c] += st.rho[c] * d;
-                    }
+                for (int c = 0; c < D; ++c) {
+                    // penalty_loss_and_grad (admm.cpp:24-28) at the pre-step x
+                    const float d = xv[c] - z[static_cast<size_t>(c) * n_shared + j] + u[static_cast<size_t>(c) * n_shared + j];
+                    pen += 0.5 * static_cast<double>(st.rho[c]) * static_cast<double>(d) * static_cast<double>(d);
+                    g[c] += st.rho[c] * d;
                 }
             }
         }
 #pragma unroll
-        for (int c = 0; c < kMaxD; ++c) {
-            if (c < D) {
-                const size_t k = static_cast<size_t>(c) * cap + i;
-                const float mm = st.b1 * m[k] + st.omb1 * g[c];
-                const float vv = st.b2 * v[k] + st.omb2 * g[c] * g[c];
-                m[k] = mm;
-                v[k] = vv;
-                xv[c] -= st.lr[c] * (mm * st.inv_bc1) / (sqrtf(vv * st.inv_bc2) + st.eps);
-            }
+        for (int c = 0; c < D; ++c) {
+            const size_t k = static_cast<size_t>(c) * cap + i;
+            const float mm = st.b1 * m[k] + st.omb1 * g[c];
+            const float vv = st.b2 * v[k] + st.omb2 * g[c] * g[c];
+            m[k] = mm;
+            v[k] = vv;
+            xv[c] -= st.lr[c] * (mm * st.inv_bc1) / (sqrtf(vv * st.inv_bc2) + st.eps);
         }
         // canonicalize_rotations (cloud.cpp:82-85; math.hpp:25-34)
         float qw = xv[kRot], qx = xv[kRot + 1], qy = xv[kRot + 2], qz = xv[kRot + 3];
@@ -239,8 +252,7 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
         }
         xv[kRot] = qw; xv[kRot + 1] = qx; xv[kRot + 2] = qy; xv[kRot + 3] = qz;
 #pragma unroll
-        for (int c = 0; c < kMaxD; ++c)
-            if (c < D) x[static_cast<size_t>(c) * cap + i] = xv[c];
+        for (int c = 0; c < D; ++c) x[static_cast<size_t>(c) * cap + i] = xv[c];
     }
     if (st.has_anchor) {
 #pragma unroll
@@ -264,13 +276,27 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
     BSG_LAUNCHED(c);
 }
 
+void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
+    if (V == 0) return;
+    fold_visible_kernel<<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, c->fd, cam, c->vrow[c->depth_sorted], V,
+                                                                 c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
+    BSG_LAUNCHED(c);
+}
+
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index) {
+    (void)cam;
     (void)loss_out;
     (void)step_index;
     if (c->n == 0) return;
-    adam_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
-        c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, c->tiles, c->g2d, c->grad_accum,
-        c->grad_seen, c->anchor_of_row, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
+    const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
+    if (c->fd == 3)
+        adam_kernel<14><<<blocks, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->tiles,
+                                                       c->gbuf, c->anchor_of_row, c->z, c->u, c->n_shared, st,
+                                                       &c->scalars->penalty);
+    else
+        adam_kernel<23><<<blocks, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->tiles,
+                                                       c->gbuf, c->anchor_of_row, c->z, c->u, c->n_shared, st,
+                                                       &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }
 

@@ -59,7 +59,7 @@ struct StepScalars {
 
 enum Stage {
     kStPreprocess = 0, kStCompact, kStDepthSort, kStPairs, kStTileSort, kStRanges, kStBlendFwd, kStLoss,
-    kStBlendBwd, kStAdam, kStCount
+    kStBlendBwd, kStFold, kStAdam, kStCount
 };
 
 struct Ctx {
@@ -81,6 +81,7 @@ struct Ctx {
     uint64_t* depth_key = nullptr; // FP64 depth bits
     uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
     float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
+    float* gbuf = nullptr;         // parameter gradient of visible rows, [D][cap]
     int32_t* anchor_of_row = nullptr;  // anchor index j or -1
 
     // compaction + depth sort (ping-pong)
@@ -209,6 +210,7 @@ struct AdamStep {
     float rho[kMaxD];
     int has_anchor;
 };
+void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
 void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty);
 

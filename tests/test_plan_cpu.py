@@ -1,0 +1,67 @@
+"""The native host planner (libbsgpu.so, host/plan.cpp) against the oracle's
+split_recursive + expand_and_assign (splitter.cpp:48-201): block membership,
+shared sets, view assignment and boxes must be bit-exact (north star). CPU only."""
+import numpy as np
+import pytest
+
+import _oracle as orc
+from paper_2405_13943_b200 import api
+from paper_2405_13943_b200.scene import aerial_scene, look_at
+from refcases import HostCloud
+
+
+def oracle_partition(cloud, cams, k, scale):
+    return orc.split_and_assign(cloud.pos, k, cams, cloud.oracle(), scale, 1, False)
+
+
+def to_oracle_cam(c):
+    oc = orc.look_at([0, 5, 0], [0, 0, 1], [0, 1, 0], 1, 1, 0, 0, 2, 2)  # placeholder, overwritten below
+    oc.fx, oc.fy, oc.cx, oc.cy = c.fx, c.fy, c.cx, c.cy
+    oc.set_rotation_quat(list(c.q))
+    oc.t = list(c.t)
+    oc.width, oc.height = c.width, c.height
+    return oc
+
+
+@pytest.mark.parametrize("n,k,scale", [(1000, 2, 1.4), (5000, 4, 1.4), (20000, 8, 1.4), (20000, 8, 2.0), (3000, 3, 1.0)])
+def test_planner_bit_exact(n, k, scale):
+    cloud, cams = aerial_scene(n, 64, 48, 16, 100.0, seed=n + k)
+    hc = HostCloud(cloud["ids"], cloud["pos"], cloud["rot"], cloud["ls"], cloud["feat"], cloud["op"])
+    ocams = [to_oracle_cam(c) for c in cams]
+    centers = np.array([c.center() for c in cams])
+    np.testing.assert_array_equal(centers, np.array([oc.center() for oc in ocams]))
+    plan = api.Plan(hc.ids, hc.pos, centers, k, scale)
+    want = oracle_partition(hc, ocams, k, scale)
+    boxes = plan.boxes()
+    for key in ("core_min", "core_max", "exp_min", "exp_max"):
+        np.testing.assert_array_equal(boxes[key], want[key])
+    for b in range(k):
+        ids, views = plan.block(b)
+        assert list(ids) == list(want["block_gaussians"][b])
+        assert list(views) == list(want["block_views"][b])
+    sids, cnt, first = plan.shared()
+    assert list(sids) == sorted(want["shared"].keys())
+    for s, gid in enumerate(sids):
+        owners = want["shared"][int(gid)]
+        assert cnt[s] == len(owners) and first[s] == owners[0]
+    # per-block slot tables
+    for b in range(k):
+        ids, _ = plan.block(b)
+        rows, slots, fo = plan.block_shared(b)
+        assert np.all(sids[slots] == ids[rows])
+        assert np.all(fo == (first[slots] == b))
+
+
+def test_planner_rejects_bad_input():
+    with pytest.raises(api.InvalidArgument):
+        api.Plan(np.arange(3, dtype=np.uint64), np.zeros((3, 3)), np.zeros((0, 3)), 4, 1.4)
+    with pytest.raises(api.InvalidArgument):
+        api.Plan(np.arange(3, dtype=np.uint64), np.zeros((3, 3)), np.zeros((0, 3)), 2, 0.5)
+
+
+def test_look_at_matches_oracle():
+    c = look_at([3.0, 30.0, -2.0], [5.0, 0.0, 1.0], [0, 1, 0], 800, 800, 512, 384, 1024, 768)
+    o = orc.look_at([3.0, 30.0, -2.0], [5.0, 0.0, 1.0], [0, 1, 0], 800, 800, 512, 384, 1024, 768)
+    assert list(c.q) == list(o.q)
+    np.testing.assert_array_equal(c.R, o.R)
+    np.testing.assert_array_equal(c.t, np.array(o.t))
