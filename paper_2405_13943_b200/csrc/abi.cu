@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <stdexcept>
 
@@ -203,30 +204,36 @@ int tile_bits(const DevCam& cam) {
 // K1-K5: projection, compaction, depth sort, pair emission, tile sort, ranges.
 void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     ensure_image_buffers(c, cam.W, cam.H);
+    BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
     stage_begin(c, kStPreprocess);
     launch_preprocess(c, cam, rc);
     stage_end(c, kStPreprocess);
     stage_begin(c, kStCompact);
-    compact_visible(c, static_cast<uint32_t>(c->n));
+    compact_visible(c, static_cast<uint32_t>(c->n));  // + digit histograms of the depth keys
     stage_end(c, kStCompact);
-    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(StepCounters), cudaMemcpyDeviceToHost, c->stream));
+    // One readback: V and the depth-key histograms (pass skipping).
+    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist), cudaMemcpyDeviceToHost,
+                             c->stream));
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     const uint32_t V = c->counters_host->visible;
     stage_begin(c, kStDepthSort);
     // (depth, index) order: stable LSD sort of the FP64 depth bits over rows in
     // ascending index order (renderer.cpp:86-89). Positive doubles order as u64.
-    radix_sort_u64(c, c->vkey, c->vrow, V, 0, 64, &c->depth_sorted);
+    radix_sort_u64(c, c->vkey, c->vrow, V, 8, &c->counters->depth_hist[0][0], &c->counters_host->depth_hist[0][0],
+                   &c->depth_sorted);
     stage_end(c, kStDepthSort);
     stage_begin(c, kStPairs);
     scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
-    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, sizeof(StepCounters), cudaMemcpyDeviceToHost, c->stream));
+    BSG_CUDA(cudaMemcpyAsync(&c->counters_host->pairs, &c->counters->pairs, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                             c->stream));
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     const uint32_t P = V ? c->counters_host->pairs : 0;
     ensure_pair_capacity(c, P);
-    launch_pairs(c, cam, V);
+    launch_pairs(c, cam, V);  // + digit histograms of the tile keys
     stage_end(c, kStPairs);
     stage_begin(c, kStTileSort);
-    radix_sort_u32(c, c->pkey, c->pval, P, 0, tile_bits(cam), &c->pairs_sorted);
+    const int passes = (tile_bits(cam) + 7) / 8;
+    radix_sort_u32(c, c->pkey, c->pval, P, passes, &c->counters->tile_hist[0][0], nullptr, &c->pairs_sorted);
     stage_end(c, kStTileSort);
     stage_begin(c, kStRanges);
     launch_ranges(c, cam, P);
@@ -450,7 +457,7 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
             dev_alloc(&c->counters, 1);
             dev_alloc(&c->scalars, 1);
-            dev_alloc(&c->radix_hist, 8 * 256);
+            dev_alloc(&c->radix_hist, 1);
             dev_alloc(&c->round_scalars, 8 + kMaxD);
             dev_alloc(&c->losses_dev, 3);
             c->losses_cap = 1;

@@ -14,8 +14,9 @@ namespace {
 
 // Fold of one visible row; FP64 arithmetic over FP32 inputs. g receives the
 // D parameter gradients; returns the screen-space gradient norm.
-__device__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, int fd, const DevCam& cam,
-                           const float4* __restrict__ g2d, double* g) {
+template <int fd>
+__device__ __forceinline__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, const DevCam& cam,
+                                           const float4* __restrict__ g2d, double* g) {
     const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
                  gcx = g2d[3 * static_cast<size_t>(i) + 2];
     const double gm0 = ga.x, gm1 = ga.y;
@@ -38,12 +39,13 @@ __device__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, 
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) g[kFeat + ch] = kSh0 * gcol[ch];
     double gpd[3] = {0, 0, 0};
-    if (fd >= 12) {
+    if constexpr (fd >= 12) {
         const double u0 = pos[0] - cam.center[0], u1 = pos[1] - cam.center[1], u2 = pos[2] - cam.center[2];
         const double un = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
         const double dir[3] = {u0 / un, u1 / un, u2 / un};
         const double b0 = -kSh1 * dir[1], b1 = kSh1 * dir[2], b2 = -kSh1 * dir[0];
         double gd[3] = {0, 0, 0};
+#pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             g[kFeat + 3 + 3 * ch] = b0 * gcol[ch];
             g[kFeat + 4 + 3 * ch] = b1 * gcol[ch];
@@ -55,6 +57,7 @@ __device__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, 
             gd[2] += gcol[ch] * (f4 * kSh1);
         }
         const double dd = dir[0] * gd[0] + dir[1] * gd[1] + dir[2] * gd[2];
+#pragma unroll
         for (int k = 0; k < 3; ++k) gpd[k] = (gd[k] - dir[k] * dd) / un;
     }
 
@@ -157,19 +160,21 @@ __device__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, 
     return sgn;
 }
 
-__global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict__ x, size_t cap, uint32_t n, int fd,
+template <int fd>
+__global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
                                                          DevCam cam, const uint32_t* __restrict__ tiles,
                                                          const float4* __restrict__ g2d, double* __restrict__ gout,
                                                          double* __restrict__ sgn_out, uint8_t* __restrict__ vis) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int D = 11 + fd;
-    double g[kMaxD];
+    constexpr int D = 11 + fd;
+    double g[D];
 #pragma unroll
-    for (int c = 0; c < kMaxD; ++c) g[c] = 0.0;
+    for (int c = 0; c < D; ++c) g[c] = 0.0;
     double s = 0.0;
     const bool visible = tiles[i] > 0;
-    if (visible) s = fold_row(x, cap, i, fd, cam, g2d, g);
+    if (visible) s = fold_row<fd>(x, cap, i, cam, g2d, g);
+#pragma unroll
     for (int c = 0; c < D; ++c) gout[static_cast<size_t>(c) * n + i] = g[c];
     sgn_out[i] = s;
     vis[i] = visible ? 1 : 0;
@@ -177,7 +182,8 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
 
 // Fold over the compacted visible list (V threads): parameter gradient of
 // each visible row into gbuf[D][cap] (FP32), densify statistics.
-__global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, int fd, DevCam cam,
+template <int fd>
+__global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, DevCam cam,
                                                            const uint32_t* __restrict__ vis_rows, uint32_t V,
                                                            const float4* __restrict__ g2d, float* __restrict__ gbuf,
                                                            float* __restrict__ grad_accum,
@@ -185,14 +191,13 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= V) return;
     const uint32_t i = vis_rows[p];
-    const int D = 11 + fd;
-    double g[kMaxD];
+    constexpr int D = 11 + fd;
+    double g[D];
 #pragma unroll
-    for (int c = 0; c < kMaxD; ++c) g[c] = 0.0;
-    const double s = fold_row(x, cap, i, fd, cam, g2d, g);
+    for (int c = 0; c < D; ++c) g[c] = 0.0;
+    const double s = fold_row<fd>(x, cap, i, cam, g2d, g);
 #pragma unroll
-    for (int c = 0; c < kMaxD; ++c)
-        if (c < D) gbuf[static_cast<size_t>(c) * cap + i] = static_cast<float>(g[c]);
+    for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + i] = static_cast<float>(g[c]);
     grad_accum[i] += static_cast<float>(s);
     grad_seen[i] += 1u;
 }
@@ -271,15 +276,24 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
 
 void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, uint8_t* vis) {
     if (c->n == 0) return;
-    fold_grads_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
-        c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, c->tiles, c->g2d, g_out, sgn, vis);
+    const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
+    if (c->fd == 3)
+        fold_grads_kernel<3><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
+                                                            c->g2d, g_out, sgn, vis);
+    else
+        fold_grads_kernel<12><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
+                                                             c->g2d, g_out, sgn, vis);
     BSG_LAUNCHED(c);
 }
 
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
-    fold_visible_kernel<<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, c->fd, cam, c->vrow[c->depth_sorted], V,
-                                                                 c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
+    if (c->fd == 3)
+        fold_visible_kernel<3><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vrow[c->depth_sorted], V,
+                                                                        c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
+    else
+        fold_visible_kernel<12><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vrow[c->depth_sorted], V,
+                                                                         c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
     BSG_LAUNCHED(c);
 }
 

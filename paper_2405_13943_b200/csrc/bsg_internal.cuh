@@ -47,6 +47,8 @@ struct StepCounters {
     uint32_t pairs;     // P
     uint32_t overflow;  // pairs exceeded capacity
     uint32_t pad;
+    uint32_t depth_hist[8][256];  // digit histograms of the visible depth keys (filled by the compaction)
+    uint32_t tile_hist[2][256];   // digit histograms of the tile keys (filled by the pair emission)
 };
 
 // Scalars reduced on the device every step.
@@ -188,10 +190,15 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
                         uint32_t* total_dev);
 // Stable compaction of rows with tiles[i] > 0: writes keys/rows in row order and V.
 void compact_visible(Ctx* c, uint32_t n);
-// Stable LSD radix sort (onesweep) of (u64 key, u32 val) / (u32 key, u32 val).
-// begin_bit/end_bit select the digit range; result lands in buffer *sel.
-void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel);
-void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel);
+// Stable LSD radix sort (onesweep) of (u64 key, u32 val) / (u32 key, u32 val)
+// over `passes` 8-bit digits from bit 0. d_hist holds the per-pass digit
+// counts (produced by the kernel that wrote the keys) and is turned into
+// offsets in place; h_hist (nullable) is a host copy used to skip passes
+// whose digit is constant. Result lands in buffer *sel.
+void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                    const uint32_t* h_hist, int* sel);
+void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                    const uint32_t* h_hist, int* sel);
 
 // ---- rasterizer stages (preprocess.cu, raster.cu, ssim.cu, adam.cu) ----
 DevCam make_cam(const bsg_camera& c);

@@ -36,7 +36,28 @@ __global__ __launch_bounds__(256) void preprocess_kernel(const float* __restrict
 #pragma unroll
     for (int r = 0; r < 3; ++r) pc[r] = ((cam.R[3 * r] * p0 + cam.R[3 * r + 1] * p1) + cam.R[3 * r + 2] * p2) + cam.t[r];
     uint32_t ntiles = 0;
-    if (pc[2] > rc.near_plane) {
+    bool maybe_visible = pc[2] > rc.near_plane;
+    if (maybe_visible) {
+        // Conservative reject before the FP64 covariance: lambda_max(cov2d) <=
+        // |J|_F^2 max(s)^2 + dilation (A = J W with W orthonormal, |Sigma|_2 =
+        // max(s)^2), so a centre farther outside the image than 3 sqrt(bound)
+        // (+1% and 2 px of slack for FP32 rounding) can only have an empty rect.
+        // Anything not rejected takes the exact path below, so the visible set
+        // and every rect are unchanged.
+        const float z = static_cast<float>(pc[2]), iz = 1.0f / z;
+        const float fxz = static_cast<float>(cam.fx) * iz, fyz = static_cast<float>(cam.fy) * iz;
+        const float jx = fxz * static_cast<float>(pc[0]) * iz, jy = fyz * static_cast<float>(pc[1]) * iz;
+        const float jf2 = fxz * fxz + fyz * fyz + jx * jx + jy * jy;
+        const float lmax = fmaxf(fmaxf(x[(kLs + 0) * cap + i], x[(kLs + 1) * cap + i]), x[(kLs + 2) * cap + i]);
+        const float smax = expf(lmax) * 1.01f;
+        const float rb = static_cast<float>(rc.sigma_extent) * sqrtf(jf2 * smax * smax + static_cast<float>(rc.dilation)) * 1.01f + 2.0f;
+        const float mxf = fxz * static_cast<float>(pc[0]) + static_cast<float>(cam.cx);
+        const float myf = fyz * static_cast<float>(pc[1]) + static_cast<float>(cam.cy);
+        if (mxf + rb < 0.f || mxf - rb > static_cast<float>(cam.W - 1) || myf + rb < 0.f ||
+            myf - rb > static_cast<float>(cam.H - 1))
+            maybe_visible = false;
+    }
+    if (maybe_visible) {
         // Sigma = (R S)(R S)^T, R from the normalized quaternion (cloud.cpp:162-167, math.hpp:25-44)
         double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
                qz = x[(kRot + 3) * cap + i];
@@ -100,8 +121,6 @@ __global__ __launch_bounds__(256) void preprocess_kernel(const float* __restrict
             // minv (renderer.cpp:76-78), colour (cloud.cpp:180-193), opacity (cloud.hpp:55)
             const double m00 = C[1][1] / det, m01 = -C[0][1] / det, m11 = C[0][0] / det;
             double col[3];
-            const double* unused = nullptr;
-            (void)unused;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(x[(kFeat + ch) * cap + i]);
             if (fd >= 12) {

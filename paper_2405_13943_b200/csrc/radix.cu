@@ -1,6 +1,7 @@
-// Hand-written stable LSD radix sort, onesweep style: one histogram pass over
-// the keys for every digit, then one kernel per 8-bit digit that ranks a
-// 4096-key tile in shared memory (warp match-any multisplit, stable), resolves
+// Hand-written stable LSD radix sort, onesweep style: the kernel that
+// produces the keys also builds every digit's histogram, then one kernel per
+// 8-bit digit ranks a 1024-4096-key tile in shared memory (warp match-any
+// multisplit, stable), resolves
 // its global digit offsets by decoupled look-back over earlier tiles, and
 // scatters through shared memory so global writes are digit-contiguous.
 // Traffic per pass: read key+value, write key+value.
@@ -11,28 +12,7 @@ namespace {
 
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsItems = 16;
-constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys
 constexpr uint32_t kStAgg = 1u << 30, kStInc = 2u << 30, kStMask = (1u << 30) - 1;
-
-template <typename K>
-__global__ __launch_bounds__(kRsThreads) void radix_hist_kernel(const K* __restrict__ keys, uint32_t n, int begin_bit,
-                                                                int passes, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t sh[8 * 256];
-    for (int i = threadIdx.x; i < passes * 256; i += kRsThreads) sh[i] = 0;
-    __syncthreads();
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kRsThreads + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * kRsThreads) {
-        const K k = keys[i];
-        for (int p = 0; p < passes; ++p) {
-            const uint32_t d = static_cast<uint32_t>(k >> (begin_bit + 8 * p)) & 0xffu;
-            atomicAdd(&sh[p * 256 + d], 1u);
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < passes * 256; i += kRsThreads)
-        if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
 
 // In-place exclusive scan of each pass's 256 bins (one block per pass).
 __global__ void radix_offsets_kernel(uint32_t* hist) {
@@ -50,12 +30,13 @@ __global__ void radix_offsets_kernel(uint32_t* hist) {
     h[threadIdx.x] = s[threadIdx.x] - v;
 }
 
-template <typename K>
+template <typename K, int kRsItems>
 __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                               K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                               uint32_t n, int shift,
                                                               const uint32_t* __restrict__ pass_offsets,
                                                               uint32_t* status, uint32_t* ticket) {
+    constexpr int kRsTile = kRsThreads * kRsItems;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s_keys = reinterpret_cast<K*>(smem_raw);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kRsTile);
@@ -171,59 +152,65 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
     }
 }
 
-template <typename K>
-void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel) {
-    *sel = 0;
-    if (n <= 1) return;
-    if (n >= (1u << 30)) throw Error{BSG_ERR_CAPACITY, "radix sort supports < 2^30 keys"};
-    const int passes = (end_bit - begin_bit + 7) / 8;
-    const uint32_t tiles = (n + kRsTile - 1) / kRsTile;
-    const size_t status_words = static_cast<size_t>(tiles) * 256;
-    const size_t need = (status_words + 64) * sizeof(uint32_t);
+template <typename K, int ITEMS>
+void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                   const uint32_t* h_hist, int* sel) {
+    constexpr int kTileKeys = kRsThreads * ITEMS;
+    const uint32_t tiles = (n + kTileKeys - 1) / kTileKeys;
+    const size_t need = (static_cast<size_t>(tiles) * 256 + 64) * sizeof(uint32_t);
     if (c->radix_status_cap < need) {
         if (c->radix_status) cudaFree(c->radix_status);
         BSG_CUDA(cudaMalloc(&c->radix_status, need * 2));
         c->radix_status_cap = need * 2;
     }
-    BSG_CUDA(cudaMemsetAsync(c->radix_hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
-    const int hist_blocks = static_cast<int>(std::min<uint32_t>(148u * 4u, (n + kRsThreads - 1) / kRsThreads));
-    radix_hist_kernel<K><<<hist_blocks, kRsThreads, 0, c->stream>>>(keys[0], n, begin_bit, passes, c->radix_hist);
-    BSG_LAUNCHED(c);
-    // Pass skipping needs the histogram on the host (one small copy).
-    static thread_local uint32_t h_hist[8 * 256];
-    BSG_CUDA(cudaMemcpyAsync(h_hist, c->radix_hist, passes * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-    radix_offsets_kernel<<<passes, 256, 0, c->stream>>>(c->radix_hist);
-    BSG_LAUNCHED(c);
-    BSG_CUDA(cudaStreamSynchronize(c->stream));
-    const size_t smem = (sizeof(K) + sizeof(uint32_t)) * kRsTile;
-    BSG_CUDA(cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = (sizeof(K) + sizeof(uint32_t)) * kTileKeys;
+    BSG_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int cur = 0;
     for (int p = 0; p < passes; ++p) {
-        bool trivial = false;
-        for (int d = 0; d < 256; ++d)
-            if (h_hist[p * 256 + d] == n) trivial = true;
-        if (trivial) continue;
-        uint32_t* ticket = c->radix_status;
-        uint32_t* status = c->radix_status + 64;
+        if (h_hist) {
+            bool trivial = false;
+            for (int d = 0; d < 256; ++d)
+                if (h_hist[p * 256 + d] == n) trivial = true;
+            if (trivial) continue;
+        }
         BSG_CUDA(cudaMemsetAsync(c->radix_status, 0, need, c->stream));
-        onesweep_kernel<K><<<tiles, kRsThreads, smem, c->stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
-                                                                   begin_bit + 8 * p, c->radix_hist + p * 256, status,
-                                                                   ticket);
+        onesweep_kernel<K, ITEMS><<<tiles, kRsThreads, smem, c->stream>>>(
+            keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, d_hist + p * 256, c->radix_status + 64,
+            c->radix_status);
         BSG_LAUNCHED(c);
         cur ^= 1;
     }
     *sel = cur;
 }
 
-}  // namespace
-
-void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel) {
-    radix_sort<uint64_t>(c, keys, vals, n, begin_bit, end_bit, sel);
+template <typename K>
+void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                const uint32_t* h_hist, int* sel) {
+    *sel = 0;
+    if (n <= 1) return;
+    if (n >= (1u << 30)) throw Error{BSG_ERR_CAPACITY, "radix sort supports < 2^30 keys"};
+    radix_offsets_kernel<<<passes, 256, 0, c->stream>>>(d_hist);
+    BSG_LAUNCHED(c);
+    // Small inputs get small tiles so the grid still covers the 148 SMs.
+    if (n < (1u << 19))
+        launch_passes<K, 4>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+    else if (n < (1u << 21))
+        launch_passes<K, 8>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+    else
+        launch_passes<K, 16>(c, keys, vals, n, passes, d_hist, h_hist, sel);
 }
 
-void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int begin_bit, int end_bit, int* sel) {
-    radix_sort<uint32_t>(c, keys, vals, n, begin_bit, end_bit, sel);
+}  // namespace
+
+void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                    const uint32_t* h_hist, int* sel) {
+    radix_sort<uint64_t>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+}
+
+void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                    const uint32_t* h_hist, int* sel) {
+    radix_sort<uint32_t>(c, keys, vals, n, passes, d_hist, h_hist, sel);
 }
 
 }  // namespace bsg

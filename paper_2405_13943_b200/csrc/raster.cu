@@ -26,21 +26,31 @@ __global__ __launch_bounds__(256) void emit_pairs_kernel(const uint32_t* __restr
                                                          const uint32_t* __restrict__ offsets,
                                                          const float4* __restrict__ rec, uint32_t V, int tiles_x,
                                                          uint32_t* __restrict__ pkey, uint32_t* __restrict__ pval,
-                                                         uint32_t pcap) {
+                                                         uint32_t pcap, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_hist[2 * 256];
+    for (int k = threadIdx.x; k < 512; k += blockDim.x) s_hist[k] = 0;
+    __syncthreads();
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= V) return;
-    const uint32_t row = sorted_rows[p];
-    int x0, x1, y0, y1;
-    unpack_rect(rec[3 * static_cast<size_t>(row) + 2], x0, x1, y0, y1);
-    uint32_t o = offsets[p];
-    for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-        for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
-            if (o < pcap) {
-                pkey[o] = static_cast<uint32_t>(ty * tiles_x + tx);
-                pval[o] = row;
+    if (p < V) {
+        const uint32_t row = sorted_rows[p];
+        int x0, x1, y0, y1;
+        unpack_rect(rec[3 * static_cast<size_t>(row) + 2], x0, x1, y0, y1);
+        uint32_t o = offsets[p];
+        for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+            for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
+                const uint32_t key = static_cast<uint32_t>(ty * tiles_x + tx);
+                if (o < pcap) {
+                    pkey[o] = key;
+                    pval[o] = row;
+                }
+                atomicAdd(&s_hist[key & 0xffu], 1u);
+                atomicAdd(&s_hist[256 + ((key >> 8) & 0xffu)], 1u);
+                ++o;
             }
-            ++o;
-        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 512; k += blockDim.x)
+        if (s_hist[k]) atomicAdd(&hist[k], s_hist[k]);
 }
 
 __global__ __launch_bounds__(256) void ranges_kernel(const uint32_t* __restrict__ pkey, uint32_t P,
@@ -130,10 +140,45 @@ __global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __
     }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Transpose-reduce of 16 per-lane values across a warp in 8+4+2+1+1 = 16
+// shuffles (instead of 16 x 5): at each halving step a lane keeps one half
+// of its values and receives the partner's copy of that half. On return,
+// lane l holds the full warp sum of value index ((l >> 1) & 15) bit-reversed
+// per the step order; `reduced_index` gives the mapping.
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+    const bool h16 = lane & 16;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+    for (int k = 0; k < 8; ++k) {
+        const float send = h16 ? v[k] : v[k + 8];
+        const float keep = h16 ? v[k + 8] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    const bool h8 = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float send = h8 ? v[k] : v[k + 4];
+        const float keep = h8 ? v[k + 4] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const bool h4 = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float send = h4 ? v[k] : v[k + 2];
+        const float keep = h4 ? v[k + 2] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    const bool h2 = lane & 2;
+    {
+        const float send = h2 ? v[0] : v[1];
+        const float keep = h2 ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// Value index owned by `lane` after transpose_reduce16.
+__device__ __forceinline__ int reduced_index(int lane) {
+    return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
 }
 
 // K8: reverse traversal (renderer.cpp:274-311). Each pixel rewinds exactly
@@ -232,20 +277,19 @@ __global__ __launch_bounds__(kTileThreads) void blend_bwd_kernel(const uint2* __
             }
             const unsigned mask = __ballot_sync(0xffffffffu, contrib);
             if (mask == 0) continue;
-            if (__popc(mask) > 1) {
-                gmx = warp_sum(gmx); gmy = warp_sum(gmy); gc00 = warp_sum(gc00); gc01 = warp_sum(gc01);
-                gc11 = warp_sum(gc11); gr = warp_sum(gr); gg = warp_sum(gg); gb = warp_sum(gb); go = warp_sum(go);
-                if (lane == 0) {
-                    float4* dst = g2d + 3 * static_cast<size_t>(s_row[sj]);
-                    atomicAdd(dst, make_float4(gmx, gmy, gc00, gc01));
-                    atomicAdd(dst + 1, make_float4(gc11, gr, gg, gb));
-                    atomicAdd(reinterpret_cast<float*>(dst + 2), go);
+            float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(s_row[sj]));
+            if (__popc(mask) <= 2) {
+                // one or two contributing pixels: direct atomics are cheaper than a reduction
+                if (contrib) {
+                    atomicAdd(reinterpret_cast<float4*>(dst), make_float4(gmx, gmy, gc00, gc01));
+                    atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(gc11, gr, gg, gb));
+                    atomicAdd(dst + 8, go);
                 }
-            } else if (contrib) {
-                float4* dst = g2d + 3 * static_cast<size_t>(s_row[sj]);
-                atomicAdd(dst, make_float4(gmx, gmy, gc00, gc01));
-                atomicAdd(dst + 1, make_float4(gc11, gr, gg, gb));
-                atomicAdd(reinterpret_cast<float*>(dst + 2), go);
+            } else {
+                float vals[16] = {gmx, gmy, gc00, gc01, gc11, gr, gg, gb, go, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                const float r = transpose_reduce16(vals, lane);
+                const int idx = reduced_index(lane);
+                if ((lane & 1) == 0 && idx < 9) atomicAdd(dst + idx, r);
             }
         }
     }
@@ -256,7 +300,8 @@ __global__ __launch_bounds__(kTileThreads) void blend_bwd_kernel(const uint2* __
 void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     emit_pairs_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(c->vrow[c->depth_sorted], c->poff, c->rec, V, cam.tiles_x,
-                                                              c->pkey[0], c->pval[0], static_cast<uint32_t>(c->pcap));
+                                                              c->pkey[0], c->pval[0], static_cast<uint32_t>(c->pcap),
+                                                              &c->counters->tile_hist[0][0]);
     BSG_LAUNCHED(c);
 }
 

@@ -82,10 +82,14 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                                                             unsigned long long* status, uint32_t* ticket,
                                                             uint32_t* total_out, const uint64_t* __restrict__ keys,
                                                             uint64_t* __restrict__ out_keys,
-                                                            uint32_t* __restrict__ out_rows) {
+                                                            uint32_t* __restrict__ out_rows,
+                                                            uint32_t* __restrict__ hist_out) {
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
+    __shared__ uint32_t s_hist[MODE == 1 ? 8 * 256 : 1];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    if (MODE == 1)
+        for (int k = threadIdx.x; k < 8 * 256; k += kScanThreads) s_hist[k] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint64_t base = static_cast<uint64_t>(tile) * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
@@ -131,14 +135,22 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         if (i < n) {
             if (MODE == 1) {
                 if (v[k]) {
-                    out_keys[run] = keys[i];
+                    const uint64_t key = keys[i];
+                    out_keys[run] = key;
                     out_rows[run] = static_cast<uint32_t>(i);
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) atomicAdd(&s_hist[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
                 }
             } else {
                 out[i] = run;
             }
         }
         run += v[k];
+    }
+    if (MODE == 1) {
+        __syncthreads();
+        for (int k = threadIdx.x; k < 8 * 256; k += kScanThreads)
+            if (s_hist[k]) atomicAdd(&hist_out[k], s_hist[k]);
     }
 }
 
@@ -165,7 +177,7 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
-                                                          nullptr, nullptr);
+                                                          nullptr, nullptr, nullptr);
     BSG_LAUNCHED(c);
 }
 
@@ -179,7 +191,8 @@ void compact_visible(Ctx* c, uint32_t n) {
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, nullptr, n, status, ticket,
-                                                          &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0]);
+                                                          &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0],
+                                                          &c->counters->depth_hist[0][0]);
     BSG_LAUNCHED(c);
 }
 
