@@ -77,7 +77,7 @@ void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
     void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->gbuf,
-                    c->anchor_of_row, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->pkey[0],
+                    c->anchor_of_row, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
                     c->ssim_f, c->gt_stage, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
@@ -100,7 +100,7 @@ void check_camera(const bsg_camera* cam) {
 }
 
 void alloc_rows(Ctx* c, size_t n) {
-    const size_t cap = std::max<size_t>(n, 1);
+    const size_t cap = (std::max<size_t>(n, 1) + 31) / 32 * 32;  // float4-aligned component rows
     dev_alloc(&c->x, c->D * cap);
     dev_alloc(&c->m, c->D * cap);
     dev_alloc(&c->v, c->D * cap);
@@ -117,6 +117,7 @@ void alloc_rows(Ctx* c, size_t n) {
     dev_alloc(&c->vrow[0], cap);
     dev_alloc(&c->vrow[1], cap);
     dev_alloc(&c->poff, cap);
+    dev_alloc(&c->vis_rows, cap);
     c->cap = cap;
 }
 

@@ -202,62 +202,101 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
     grad_seen[i] += 1u;
 }
 
-// Dense Adam over every row (trainer.cpp:267-281): streaming x, m, v in
-// [D][cap] layout (every component access is coalesced); rows not visible
-// this step have a zero render gradient; shared rows add rho (x - z + u).
-template <int D>
+// Dense Adam over every row (trainer.cpp:267-281), element-wise: thread =
+// 4 consecutive rows of one component (float4 loads/stores of x, m, v), so the
+// kernel is a pure coalesced stream. blockIdx.y selects the component; y == 3
+// is the quaternion group, whose 4 components per row are updated together
+// and then canonicalised (cloud.cpp:82-85, math.hpp:25-34). Rows not visible
+// this step have a zero render gradient; shared rows add rho (x - z + u)
+// evaluated at the pre-step x (admm.cpp:24-28, trainer.cpp:257-265).
+__device__ __forceinline__ float adam_update(float x, float g, float& m, float& v, float lr, const AdamStep& st) {
+    m = st.b1 * m + st.omb1 * g;
+    v = st.b2 * v + st.omb2 * g * g;
+    return x - lr * (m * st.inv_bc1) / (sqrtf(v * st.inv_bc2) + st.eps);
+}
+
 __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
                                                    size_t cap, uint32_t n, const uint32_t* __restrict__ tiles,
                                                    const float* __restrict__ gbuf,
                                                    const int32_t* __restrict__ anchor_of_row, const float* __restrict__ z,
-                                                   const float* __restrict__ u, size_t n_shared, AdamStep st,
+                                                   const float* __restrict__ u, size_t ns, AdamStep st,
                                                    double* __restrict__ penalty) {
     __shared__ double s_red[8];
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t r0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    const int y = blockIdx.y;
+    const bool rot = y == 3;
+    const int c0 = rot ? kRot : (y < 3 ? y : y + 3);
+    const int nc = rot ? 4 : 1;
     double pen = 0.0;
-    if (i < n) {
-        const bool visible = tiles[i] > 0;
-        float xv[D], g[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            xv[c] = x[static_cast<size_t>(c) * cap + i];
-            g[c] = visible ? gbuf[static_cast<size_t>(c) * cap + i] : 0.f;
-        }
+    if (r0 < n) {
+        const int nr = n - r0 >= 4 ? 4 : static_cast<int>(n - r0);
+        const uint4 t4 = *reinterpret_cast<const uint4*>(tiles + r0);
+        const uint32_t tv[4] = {t4.x, t4.y, t4.z, t4.w};
+        int aj[4] = {-1, -1, -1, -1};
         if (st.has_anchor) {
-            const int32_t j = anchor_of_row[i];
-            if (j >= 0) {
+            const int4 a4 = *reinterpret_cast<const int4*>(anchor_of_row + r0);
+            aj[0] = a4.x; aj[1] = a4.y; aj[2] = a4.z; aj[3] = a4.w;
+        }
+        float xs[4][4];  // [component][row]
 #pragma unroll
-                for (int c = 0; c < D; ++c) {
-                    // penalty_loss_and_grad (admm.cpp:24-28) at the pre-step x
-                    const float d = xv[c] - z[static_cast<size_t>(c) * n_shared + j] + u[static_cast<size_t>(c) * n_shared + j];
-                    pen += 0.5 * static_cast<double>(st.rho[c]) * static_cast<double>(d) * static_cast<double>(d);
-                    g[c] += st.rho[c] * d;
+        for (int k = 0; k < 4; ++k) {
+            if (k < nc) {
+                const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
+                const float4 x4 = *reinterpret_cast<const float4*>(x + off);
+                float4 m4 = *reinterpret_cast<const float4*>(m + off);
+                float4 v4 = *reinterpret_cast<const float4*>(v + off);
+                const float xr[4] = {x4.x, x4.y, x4.z, x4.w};
+                float mr[4] = {m4.x, m4.y, m4.z, m4.w}, vr[4] = {v4.x, v4.y, v4.z, v4.w};
+                const float lr = st.lr[c0 + k], rho = st.rho[c0 + k];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    float g = tv[r] > 0 ? gbuf[off + r] : 0.f;
+                    if (aj[r] >= 0) {
+                        const float d = xr[r] - z[static_cast<size_t>(c0 + k) * ns + aj[r]] +
+                                        u[static_cast<size_t>(c0 + k) * ns + aj[r]];
+                        if (r < nr) pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
+                        g += rho * d;
+                    }
+                    xs[k][r] = adam_update(xr[r], g, mr[r], vr[r], lr, st);
+                }
+                if (nr == 4) {
+                    *reinterpret_cast<float4*>(m + off) = make_float4(mr[0], mr[1], mr[2], mr[3]);
+                    *reinterpret_cast<float4*>(v + off) = make_float4(vr[0], vr[1], vr[2], vr[3]);
+                } else {
+                    for (int r = 0; r < nr; ++r) {
+                        m[off + r] = mr[r];
+                        v[off + r] = vr[r];
+                    }
                 }
             }
         }
+        if (rot) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            const size_t k = static_cast<size_t>(c) * cap + i;
-            const float mm = st.b1 * m[k] + st.omb1 * g[c];
-            const float vv = st.b2 * v[k] + st.omb2 * g[c] * g[c];
-            m[k] = mm;
-            v[k] = vv;
-            xv[c] -= st.lr[c] * (mm * st.inv_bc1) / (sqrtf(vv * st.inv_bc2) + st.eps);
+            for (int r = 0; r < 4; ++r) {
+                float qw = xs[0][r], qx = xs[1][r], qy = xs[2][r], qz = xs[3][r];
+                const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+                if (qn == 0.f) {
+                    qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
+                } else {
+                    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+                }
+                if (qw < 0.f) {
+                    qw = -qw; qx = -qx; qy = -qy; qz = -qz;
+                }
+                xs[0][r] = qw; xs[1][r] = qx; xs[2][r] = qy; xs[3][r] = qz;
+            }
         }
-        // canonicalize_rotations (cloud.cpp:82-85; math.hpp:25-34)
-        float qw = xv[kRot], qx = xv[kRot + 1], qy = xv[kRot + 2], qz = xv[kRot + 3];
-        const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-        if (qn == 0.f) {
-            qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
-        } else {
-            qw /= qn; qx /= qn; qy /= qn; qz /= qn;
-        }
-        if (qw < 0.f) {
-            qw = -qw; qx = -qx; qy = -qy; qz = -qz;
-        }
-        xv[kRot] = qw; xv[kRot + 1] = qx; xv[kRot + 2] = qy; xv[kRot + 3] = qz;
 #pragma unroll
-        for (int c = 0; c < D; ++c) x[static_cast<size_t>(c) * cap + i] = xv[c];
+        for (int k = 0; k < 4; ++k) {
+            if (k < nc) {
+                const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
+                if (nr == 4) {
+                    *reinterpret_cast<float4*>(x + off) = make_float4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
+                } else {
+                    for (int r = 0; r < nr; ++r) x[off + r] = xs[k][r];
+                }
+            }
+        }
     }
     if (st.has_anchor) {
 #pragma unroll
@@ -289,10 +328,10 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     if (c->fd == 3)
-        fold_visible_kernel<3><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vrow[c->depth_sorted], V,
+        fold_visible_kernel<3><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
                                                                         c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
     else
-        fold_visible_kernel<12><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vrow[c->depth_sorted], V,
+        fold_visible_kernel<12><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
                                                                          c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
     BSG_LAUNCHED(c);
 }
@@ -302,15 +341,9 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     (void)loss_out;
     (void)step_index;
     if (c->n == 0) return;
-    const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
-    if (c->fd == 3)
-        adam_kernel<14><<<blocks, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->tiles,
-                                                       c->gbuf, c->anchor_of_row, c->z, c->u, c->n_shared, st,
-                                                       &c->scalars->penalty);
-    else
-        adam_kernel<23><<<blocks, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->tiles,
-                                                       c->gbuf, c->anchor_of_row, c->z, c->u, c->n_shared, st,
-                                                       &c->scalars->penalty);
+    const dim3 grid(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(c->D - 3));
+    adam_kernel<<<grid, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->tiles, c->gbuf,
+                                             c->anchor_of_row, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }
 

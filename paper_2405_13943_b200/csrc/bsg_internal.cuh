@@ -90,6 +90,7 @@ struct Ctx {
     uint64_t* vkey[2] = {nullptr, nullptr};
     uint32_t* vrow[2] = {nullptr, nullptr};
     uint32_t* poff = nullptr;      // pair offsets (exclusive scan over sorted splats)
+    uint32_t* vis_rows = nullptr;  // visible rows in ascending row order (compaction output)
     int depth_sorted = 0;          // which ping-pong buffer holds the sorted result
 
     // tile pairs (ping-pong)

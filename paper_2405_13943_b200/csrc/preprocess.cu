@@ -23,135 +23,172 @@ __device__ __forceinline__ int to_int_clamped(double v) {
     return static_cast<int>(v);
 }
 
-__global__ __launch_bounds__(256) void preprocess_kernel(const float* __restrict__ x, size_t cap, uint32_t n, int fd,
-                                                         DevCam cam, DevRender rc, float4* __restrict__ rec,
-                                                         uint64_t* __restrict__ depth_key, uint32_t* __restrict__ tiles,
-                                                         float4* __restrict__ g2d) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double p0 = x[(kPos + 0) * cap + i], p1 = x[(kPos + 1) * cap + i], p2 = x[(kPos + 2) * cap + i];
+constexpr int kPreThreads = 256;
+constexpr int kPreRowsPerThread = 8;
+constexpr int kPreChunk = kPreThreads * kPreRowsPerThread;
 
-    // p_cam = R p + t (camera.hpp:28)
-    double pc[3];
+// Two phases per CTA over a chunk of 2048 rows. Phase 1 (FP32, every row):
+// a conservative reject -- lambda_max(cov2d) <= |J|_F^2 max(s)^2 + dilation
+// (A = J W with W orthonormal, |Sigma|_2 = max(s)^2), so a centre farther
+// outside the image than sigma_extent sqrt(bound) (+1% and 2 px slack for
+// FP32 rounding) or behind the near plane (with slack) can only be culled.
+// Survivors are queued in shared memory. Phase 2 runs the exact FP64 path on
+// the queue with every lane busy (rows are in id order, i.e. spatially random,
+// so doing this per thread would leave most lanes of a warp idle). The
+// visible set and every rect are exactly those of the exact path.
+__global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
+                                                                 int fd, DevCam cam, DevRender rc,
+                                                                 float4* __restrict__ rec,
+                                                                 uint64_t* __restrict__ depth_key,
+                                                                 uint32_t* __restrict__ tiles,
+                                                                 float4* __restrict__ g2d) {
+    __shared__ uint32_t s_rows[kPreChunk];
+    __shared__ uint32_t s_count;
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    const uint32_t chunk0 = blockIdx.x * kPreChunk;
+    const float fxf = static_cast<float>(cam.fx), fyf = static_cast<float>(cam.fy);
+    const float cxf = static_cast<float>(cam.cx), cyf = static_cast<float>(cam.cy);
+    float Rf[9], tf[3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) pc[r] = ((cam.R[3 * r] * p0 + cam.R[3 * r + 1] * p1) + cam.R[3 * r + 2] * p2) + cam.t[r];
-    uint32_t ntiles = 0;
-    bool maybe_visible = pc[2] > rc.near_plane;
-    if (maybe_visible) {
-        // Conservative reject before the FP64 covariance: lambda_max(cov2d) <=
-        // |J|_F^2 max(s)^2 + dilation (A = J W with W orthonormal, |Sigma|_2 =
-        // max(s)^2), so a centre farther outside the image than 3 sqrt(bound)
-        // (+1% and 2 px of slack for FP32 rounding) can only have an empty rect.
-        // Anything not rejected takes the exact path below, so the visible set
-        // and every rect are unchanged.
-        const float z = static_cast<float>(pc[2]), iz = 1.0f / z;
-        const float fxz = static_cast<float>(cam.fx) * iz, fyz = static_cast<float>(cam.fy) * iz;
-        const float jx = fxz * static_cast<float>(pc[0]) * iz, jy = fyz * static_cast<float>(pc[1]) * iz;
-        const float jf2 = fxz * fxz + fyz * fyz + jx * jx + jy * jy;
-        const float lmax = fmaxf(fmaxf(x[(kLs + 0) * cap + i], x[(kLs + 1) * cap + i]), x[(kLs + 2) * cap + i]);
-        const float smax = expf(lmax) * 1.01f;
-        const float rb = static_cast<float>(rc.sigma_extent) * sqrtf(jf2 * smax * smax + static_cast<float>(rc.dilation)) * 1.01f + 2.0f;
-        const float mxf = fxz * static_cast<float>(pc[0]) + static_cast<float>(cam.cx);
-        const float myf = fyz * static_cast<float>(pc[1]) + static_cast<float>(cam.cy);
-        if (mxf + rb < 0.f || mxf - rb > static_cast<float>(cam.W - 1) || myf + rb < 0.f ||
-            myf - rb > static_cast<float>(cam.H - 1))
-            maybe_visible = false;
-    }
-    if (maybe_visible) {
-        // Sigma = (R S)(R S)^T, R from the normalized quaternion (cloud.cpp:162-167, math.hpp:25-44)
-        double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
-               qz = x[(kRot + 3) * cap + i];
-        const double qn = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
-        if (qn == 0.0) {
-            qw = 1.0; qx = 0.0; qy = 0.0; qz = 0.0;
+    for (int k = 0; k < 9; ++k) Rf[k] = static_cast<float>(cam.R[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tf[k] = static_cast<float>(cam.t[k]);
+    const float nearf = static_cast<float>(rc.near_plane);
+    for (int k = 0; k < kPreRowsPerThread; ++k) {
+        const uint32_t i = chunk0 + k * kPreThreads + threadIdx.x;
+        if (i >= n) break;
+        const float p0 = x[(kPos + 0) * cap + i], p1 = x[(kPos + 1) * cap + i], p2 = x[(kPos + 2) * cap + i];
+        const float z = (Rf[6] * p0 + Rf[7] * p1) + Rf[8] * p2 + tf[2];
+        const float px = (Rf[0] * p0 + Rf[1] * p1) + Rf[2] * p2 + tf[0];
+        const float py = (Rf[3] * p0 + Rf[4] * p1) + Rf[5] * p2 + tf[1];
+        // FP32 z may differ from FP64 z by ~1e-6 |p|: keep anything that could be past the near plane
+        bool cand = z > nearf - 1e-3f * (1.0f + fabsf(p0) + fabsf(p1) + fabsf(p2));
+        if (cand && z > 0.5f * nearf) {
+            const float iz = 1.0f / z;
+            const float fxz = fxf * iz, fyz = fyf * iz;
+            const float jx = fxz * px * iz, jy = fyz * py * iz;
+            const float jf2 = fxz * fxz + fyz * fyz + jx * jx + jy * jy;
+            const float lmax = fmaxf(fmaxf(x[(kLs + 0) * cap + i], x[(kLs + 1) * cap + i]), x[(kLs + 2) * cap + i]);
+            const float smax = expf(lmax) * 1.01f;
+            const float rb = static_cast<float>(rc.sigma_extent) * sqrtf(jf2 * smax * smax + static_cast<float>(rc.dilation)) * 1.01f + 2.0f;
+            const float mxf = fxz * px + cxf, myf = fyz * py + cyf;
+            if (mxf + rb < 0.f || mxf - rb > static_cast<float>(cam.W - 1) || myf + rb < 0.f ||
+                myf - rb > static_cast<float>(cam.H - 1))
+                cand = false;
+        }
+        if (cand) {
+            s_rows[atomicAdd(&s_count, 1u)] = i;
         } else {
-            qw = qw / qn; qx = qx / qn; qy = qy / qn; qz = qz / qn;
-        }
-        double R[3][3];
-        R[0][0] = 1 - 2 * (qy * qy + qz * qz); R[0][1] = 2 * (qx * qy - qw * qz); R[0][2] = 2 * (qx * qz + qw * qy);
-        R[1][0] = 2 * (qx * qy + qw * qz); R[1][1] = 1 - 2 * (qx * qx + qz * qz); R[1][2] = 2 * (qy * qz - qw * qx);
-        R[2][0] = 2 * (qx * qz - qw * qy); R[2][1] = 2 * (qy * qz + qw * qx); R[2][2] = 1 - 2 * (qx * qx + qy * qy);
-        const double s[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])),
-                             exp(static_cast<double>(x[(kLs + 1) * cap + i])),
-                             exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
-        double M[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) M[a][b] = R[a][b] * s[b];
-        double S[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) S[a][b] = (M[a][0] * M[b][0] + M[a][1] * M[b][1]) + M[a][2] * M[b][2];
-
-        // mean2d (camera.hpp:34-36); J (renderer.cpp:14-20); A = J W; cov2d = A S A^T + dilation I
-        const double z = pc[2];
-        const double mx = cam.fx * pc[0] / z + cam.cx;
-        const double my = cam.fy * pc[1] / z + cam.cy;
-        const double iz = 1.0 / z, iz2 = iz * iz;
-        const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * pc[0] * iz2}, {0.0, cam.fy * iz, -cam.fy * pc[1] * iz2}};
-        double A[2][3], T[2][3], C[2][2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                A[r][k] = (J[r][0] * cam.R[k] + J[r][1] * cam.R[3 + k]) + J[r][2] * cam.R[6 + k];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) T[r][k] = (A[r][0] * S[0][k] + A[r][1] * S[1][k]) + A[r][2] * S[2][k];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const double v = (T[r][0] * A[q][0] + T[r][1] * A[q][1]) + T[r][2] * A[q][2];
-                C[r][q] = v + (r == q ? rc.dilation : rc.dilation * 0.0);
-            }
-        // max_eigenvalue_2x2 (renderer.cpp:22-26), footprint (renderer.cpp:33-40)
-        const double mid = 0.5 * (C[0][0] + C[1][1]);
-        const double det = C[0][0] * C[1][1] - C[0][1] * C[1][0];
-        const double lam = mid + sqrt(fmax(0.0, mid * mid - det));
-        const double radius = rc.sigma_extent * sqrt(lam);
-        const int x0 = max(0, to_int_clamped(ceil(mx - radius)));
-        const int x1 = min(cam.W - 1, to_int_clamped(floor(mx + radius)));
-        const int y0 = max(0, to_int_clamped(ceil(my - radius)));
-        const int y1 = min(cam.H - 1, to_int_clamped(floor(my + radius)));
-        if (x0 <= x1 && y0 <= y1) {
-            // minv (renderer.cpp:76-78), colour (cloud.cpp:180-193), opacity (cloud.hpp:55)
-            const double m00 = C[1][1] / det, m01 = -C[0][1] / det, m11 = C[0][0] / det;
-            double col[3];
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(x[(kFeat + ch) * cap + i]);
-            if (fd >= 12) {
-                const double u0 = p0 - cam.center[0], u1 = p1 - cam.center[1], u2 = p2 - cam.center[2];
-                const double un = sqrt((u0 * u0 + u1 * u1) + u2 * u2);
-                const double d0 = u0 / un, d1 = u1 / un, d2 = u2 / un;
-                const double b0 = -kSh1 * d1, b1 = kSh1 * d2, b2 = -kSh1 * d0;
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch)
-                    col[ch] += b0 * static_cast<double>(x[(kFeat + 3 + 3 * ch) * cap + i]) +
-                               b1 * static_cast<double>(x[(kFeat + 4 + 3 * ch) * cap + i]) +
-                               b2 * static_cast<double>(x[(kFeat + 5 + 3 * ch) * cap + i]);
-            }
-            const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[op_comp(fd) * cap + i])));
-            const uint32_t r01 = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
-            const uint32_t r23 = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
-            rec[3 * static_cast<size_t>(i) + 0] =
-                make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(m00), static_cast<float>(m01));
-            rec[3 * static_cast<size_t>(i) + 1] =
-                make_float4(static_cast<float>(m11), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
-            rec[3 * static_cast<size_t>(i) + 2] =
-                make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23), 0.f);
-            ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-            depth_key[i] = static_cast<uint64_t>(__double_as_longlong(z));
-            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-            g2d[3 * static_cast<size_t>(i) + 0] = zero;
-            g2d[3 * static_cast<size_t>(i) + 1] = zero;
-            g2d[3 * static_cast<size_t>(i) + 2] = zero;
+            tiles[i] = 0;
         }
     }
-    tiles[i] = ntiles;
+    __syncthreads();
+    const uint32_t count = s_count;
+    for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
+        const uint32_t i = s_rows[q];
+        const double p0 = x[(kPos + 0) * cap + i], p1 = x[(kPos + 1) * cap + i], p2 = x[(kPos + 2) * cap + i];
+        // p_cam = R p + t (camera.hpp:28)
+        double pc[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) pc[r] = ((cam.R[3 * r] * p0 + cam.R[3 * r + 1] * p1) + cam.R[3 * r + 2] * p2) + cam.t[r];
+        uint32_t ntiles = 0;
+        if (pc[2] > rc.near_plane) {
+            // Sigma = (R S)(R S)^T, R from the normalized quaternion (cloud.cpp:162-167, math.hpp:25-44)
+            double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
+                   qz = x[(kRot + 3) * cap + i];
+            const double qn = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+            if (qn == 0.0) {
+                qw = 1.0; qx = 0.0; qy = 0.0; qz = 0.0;
+            } else {
+                qw = qw / qn; qx = qx / qn; qy = qy / qn; qz = qz / qn;
+            }
+            double R[3][3];
+            R[0][0] = 1 - 2 * (qy * qy + qz * qz); R[0][1] = 2 * (qx * qy - qw * qz); R[0][2] = 2 * (qx * qz + qw * qy);
+            R[1][0] = 2 * (qx * qy + qw * qz); R[1][1] = 1 - 2 * (qx * qx + qz * qz); R[1][2] = 2 * (qy * qz - qw * qx);
+            R[2][0] = 2 * (qx * qz - qw * qy); R[2][1] = 2 * (qy * qz + qw * qx); R[2][2] = 1 - 2 * (qx * qx + qy * qy);
+            const double s[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])),
+                                 exp(static_cast<double>(x[(kLs + 1) * cap + i])),
+                                 exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
+            double M[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) M[a][b] = R[a][b] * s[b];
+            double S[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) S[a][b] = (M[a][0] * M[b][0] + M[a][1] * M[b][1]) + M[a][2] * M[b][2];
+
+            // mean2d (camera.hpp:34-36); J (renderer.cpp:14-20); A = J W; cov2d = A S A^T + dilation I
+            const double z = pc[2];
+            const double mx = cam.fx * pc[0] / z + cam.cx;
+            const double my = cam.fy * pc[1] / z + cam.cy;
+            const double iz = 1.0 / z, iz2 = iz * iz;
+            const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * pc[0] * iz2}, {0.0, cam.fy * iz, -cam.fy * pc[1] * iz2}};
+            double A[2][3], T[2][3], C[2][2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    A[r][k] = (J[r][0] * cam.R[k] + J[r][1] * cam.R[3 + k]) + J[r][2] * cam.R[6 + k];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) T[r][k] = (A[r][0] * S[0][k] + A[r][1] * S[1][k]) + A[r][2] * S[2][k];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double v = (T[r][0] * A[q][0] + T[r][1] * A[q][1]) + T[r][2] * A[q][2];
+                    C[r][q] = v + (r == q ? rc.dilation : rc.dilation * 0.0);
+                }
+            // max_eigenvalue_2x2 (renderer.cpp:22-26), footprint (renderer.cpp:33-40)
+            const double mid = 0.5 * (C[0][0] + C[1][1]);
+            const double det = C[0][0] * C[1][1] - C[0][1] * C[1][0];
+            const double lam = mid + sqrt(fmax(0.0, mid * mid - det));
+            const double radius = rc.sigma_extent * sqrt(lam);
+            const int x0 = max(0, to_int_clamped(ceil(mx - radius)));
+            const int x1 = min(cam.W - 1, to_int_clamped(floor(mx + radius)));
+            const int y0 = max(0, to_int_clamped(ceil(my - radius)));
+            const int y1 = min(cam.H - 1, to_int_clamped(floor(my + radius)));
+            if (x0 <= x1 && y0 <= y1) {
+                // minv (renderer.cpp:76-78), colour (cloud.cpp:180-193), opacity (cloud.hpp:55)
+                const double m00 = C[1][1] / det, m01 = -C[0][1] / det, m11 = C[0][0] / det;
+                double col[3];
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(x[(kFeat + ch) * cap + i]);
+                if (fd >= 12) {
+                    const double u0 = p0 - cam.center[0], u1 = p1 - cam.center[1], u2 = p2 - cam.center[2];
+                    const double un = sqrt((u0 * u0 + u1 * u1) + u2 * u2);
+                    const double d0 = u0 / un, d1 = u1 / un, d2 = u2 / un;
+                    const double b0 = -kSh1 * d1, b1 = kSh1 * d2, b2 = -kSh1 * d0;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch)
+                        col[ch] += b0 * static_cast<double>(x[(kFeat + 3 + 3 * ch) * cap + i]) +
+                                   b1 * static_cast<double>(x[(kFeat + 4 + 3 * ch) * cap + i]) +
+                                   b2 * static_cast<double>(x[(kFeat + 5 + 3 * ch) * cap + i]);
+                }
+                const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[op_comp(fd) * cap + i])));
+                const uint32_t r01 = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
+                const uint32_t r23 = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
+                rec[3 * static_cast<size_t>(i) + 0] =
+                    make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(m00), static_cast<float>(m01));
+                rec[3 * static_cast<size_t>(i) + 1] =
+                    make_float4(static_cast<float>(m11), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
+                rec[3 * static_cast<size_t>(i) + 2] =
+                    make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23), 0.f);
+                ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+                depth_key[i] = static_cast<uint64_t>(__double_as_longlong(z));
+                const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+                g2d[3 * static_cast<size_t>(i) + 0] = zero;
+                g2d[3 * static_cast<size_t>(i) + 1] = zero;
+                g2d[3 * static_cast<size_t>(i) + 2] = zero;
+            }
+        }
+        tiles[i] = ntiles;
+    }
 }
 
 }  // namespace
@@ -184,8 +221,8 @@ DevRender make_render(const bsg_render_config& r) {
 
 void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     if (c->n == 0) return;
-    const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
-    preprocess_kernel<<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
+    const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
+    preprocess_kernel<<<blocks, kPreThreads, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
                                                       c->depth_key, c->tiles, c->g2d);
     BSG_LAUNCHED(c);
 }

@@ -138,6 +138,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                     const uint64_t key = keys[i];
                     out_keys[run] = key;
                     out_rows[run] = static_cast<uint32_t>(i);
+                    out[run] = static_cast<uint32_t>(i);
 #pragma unroll
                     for (int p = 0; p < 8; ++p) atomicAdd(&s_hist[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
                 }
@@ -190,7 +191,7 @@ void compact_visible(Ctx* c, uint32_t n) {
     prepare_status(c, tiles);
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
-    scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, nullptr, n, status, ticket,
+    scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
                                                           &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0],
                                                           &c->counters->depth_hist[0][0]);
     BSG_LAUNCHED(c);
