@@ -152,6 +152,14 @@ int bsg_set_anchor(bsg_ctx* ctx, const double* z_rows, const double* z_prev_slot
 int bsg_set_penalties(bsg_ctx* ctx, const bsg_penalties* rho);
 int bsg_download_duals(bsg_ctx* ctx, double* u_rows);
 int bsg_download_anchor(bsg_ctx* ctx, double* z_rows);
+/* Restores duals (n_shared x D rows), e.g. after the shared set shrinks. */
+int bsg_upload_duals(bsg_ctx* ctx, const double* u_rows);
+/* apply_broadcast (trainer.cpp:168-223) with a z computed elsewhere (e.g. a
+ * master process, runtime.cpp:567-570): z_slots is n_slots x D rows; the
+ * relaxed local x_hat uses the current anchor, u += x_hat - z, listed slots are
+ * reset, anchor := z. */
+int bsg_apply_broadcast(bsg_ctx* ctx, const double* z_slots, size_t n_reset, const uint32_t* reset_slots, double alpha,
+                        int relax);
 /* Consensus z over all slots (n_slots x D) after the last round. */
 int bsg_download_consensus(bsg_ctx* ctx, double* z_slots);
 
@@ -199,6 +207,39 @@ size_t bsg_plan_shared_count(const bsg_plan* plan);
 int bsg_plan_shared(const bsg_plan* plan, uint64_t* ids, uint32_t* owner_count, uint32_t* first_owner);
 int bsg_plan_block_shared(const bsg_plan* plan, uint32_t block, size_t* n_out, uint32_t* rows, uint32_t* slots,
                           uint8_t* first_owner);
+
+/* ---- K-block driver (run_simulated, runtime.cpp:623-671) --------------- */
+/* plan_cluster + BlockTrainers + consensus rounds, implemented by the C++
+ * host layer (include/blocksplat_gpu.hpp) in this library. */
+typedef struct bsg_session_options {
+    uint64_t total_iterations;  /* SessionOptions::total_iterations */
+    uint32_t interval;          /* ConsensusConfig (admm.hpp:20-29) */
+    double alpha, mu, tau_inc, tau_dec;
+    uint64_t freeze_iteration;
+    int adaptive, enabled;
+    bsg_penalties rho;
+    uint64_t seed;              /* TrainerConfig::seed */
+    uint32_t blocks;            /* plan_cluster arguments (runtime.hpp:101-103) */
+    double expand_scale;
+    uint32_t holdout;
+} bsg_session_options;
+
+typedef struct bsg_round_diag {  /* RoundDiagnostics (runtime.hpp:61-71) */
+    uint64_t iteration;
+    double primal, dual;
+    bsg_penalties rho;
+    double max_disagreement, dual_mean_linf, mean_loss;
+    uint64_t shared_count, global_count;
+    double consensus_ms;
+} bsg_round_diag;
+
+const char* bsg_driver_last_error(void);
+int bsg_run_simulated(int feature_dim, size_t n, const uint64_t* ids, const double* pos, const double* rot,
+                      const double* log_scale, const double* features, const double* opacity_logit, size_t n_views,
+                      const bsg_camera* cams, const double* const* gt_rgb, const bsg_trainer_config* trainer,
+                      const bsg_session_options* session, size_t n_devices, const int* devices, double* out_pos,
+                      double* out_rot, double* out_log_scale, double* out_features, double* out_opacity_logit,
+                      bsg_round_diag* rounds, size_t max_rounds, size_t* n_rounds, double* wall_seconds);
 
 /* ---- measurement ------------------------------------------------------ */
 /* Per-stage device times of the most recent step (CUDA events on the

@@ -62,6 +62,21 @@ class bsg_round_result(ctypes.Structure):
                 ("dual_mean_linf", ctypes.c_double), ("flipped", ctypes.c_uint64), ("ms", ctypes.c_double)]
 
 
+class bsg_session_options(ctypes.Structure):
+    _fields_ = [("total_iterations", ctypes.c_uint64), ("interval", ctypes.c_uint32), ("alpha", ctypes.c_double),
+                ("mu", ctypes.c_double), ("tau_inc", ctypes.c_double), ("tau_dec", ctypes.c_double),
+                ("freeze_iteration", ctypes.c_uint64), ("adaptive", ctypes.c_int), ("enabled", ctypes.c_int),
+                ("rho", bsg_penalties), ("seed", ctypes.c_uint64), ("blocks", ctypes.c_uint32),
+                ("expand_scale", ctypes.c_double), ("holdout", ctypes.c_uint32)]
+
+
+class bsg_round_diag(ctypes.Structure):
+    _fields_ = [("iteration", ctypes.c_uint64), ("primal", ctypes.c_double), ("dual", ctypes.c_double),
+                ("rho", bsg_penalties), ("max_disagreement", ctypes.c_double), ("dual_mean_linf", ctypes.c_double),
+                ("mean_loss", ctypes.c_double), ("shared_count", ctypes.c_uint64), ("global_count", ctypes.c_uint64),
+                ("consensus_ms", ctypes.c_double)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/bsgpu.h.
 _P = ctypes.c_void_p
 _DP = ctypes.POINTER(ctypes.c_double)
@@ -100,7 +115,9 @@ SYMBOLS = [
     ("bsg_set_penalties", ctypes.c_int, [_P, ctypes.POINTER(bsg_penalties)]),
     ("bsg_download_duals", ctypes.c_int, [_P, _DP]),
     ("bsg_download_anchor", ctypes.c_int, [_P, _DP]),
+    ("bsg_upload_duals", ctypes.c_int, [_P, _DP]),
     ("bsg_download_consensus", ctypes.c_int, [_P, _DP]),
+    ("bsg_apply_broadcast", ctypes.c_int, [_P, _DP, _SZ, _U32P, ctypes.c_double, ctypes.c_int]),
     ("bsg_nccl_unique_id", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
     ("bsg_comm_init", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int]),
     ("bsg_consensus_round", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_round_result)]),
@@ -116,6 +133,12 @@ SYMBOLS = [
     ("bsg_plan_shared_count", _SZ, [_P]),
     ("bsg_plan_shared", ctypes.c_int, [_P, _U64P, _U32P, _U32P]),
     ("bsg_plan_block_shared", ctypes.c_int, [_P, ctypes.c_uint32, _SZP, _U32P, _U32P, _U8P]),
+    ("bsg_driver_last_error", ctypes.c_char_p, []),
+    ("bsg_run_simulated", ctypes.c_int, [ctypes.c_int, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZ,
+                                          ctypes.POINTER(bsg_camera), ctypes.POINTER(_DP),
+                                          ctypes.POINTER(bsg_trainer_config), ctypes.POINTER(bsg_session_options), _SZ,
+                                          ctypes.POINTER(ctypes.c_int), _DP, _DP, _DP, _DP, _DP,
+                                          ctypes.POINTER(bsg_round_diag), _SZ, _SZP, _DP]),
     ("bsg_enable_stage_timing", ctypes.c_int, [_P, ctypes.c_int]),
     ("bsg_stage_count", ctypes.c_int, []),
     ("bsg_stage_name", ctypes.c_char_p, [ctypes.c_int]),
@@ -367,6 +390,12 @@ class Block:
         _check(_lib.bsg_download_consensus(self.h, _ptr(z, ctypes.c_double)))
         return z
 
+    def apply_broadcast(self, z_slots, reset_slots, alpha, relax):
+        z = _f64(z_slots).reshape(self.n_slots, self.D)
+        rs = np.ascontiguousarray(reset_slots, np.uint32)
+        _check(_lib.bsg_apply_broadcast(self.h, _ptr(z, ctypes.c_double), len(rs), _ptr(rs, ctypes.c_uint32) if len(rs) else None,
+                                        float(alpha), 1 if relax else 0))
+
     def comm_init(self, uid, nranks, rank):
         buf = (ctypes.c_uint8 * 128)(*uid)
         _check(_lib.bsg_comm_init(self.h, buf, nranks, rank))
@@ -487,3 +516,49 @@ class Plan:
         _lib.bsg_plan_block_shared(self.h, b, ctypes.byref(n), _ptr(rows, ctypes.c_uint32), _ptr(slots, ctypes.c_uint32),
                                    _ptr(first, ctypes.c_uint8))
         return rows[:n.value], slots[:n.value], first[:n.value]
+
+
+def session_options(total_iterations, interval=100, alpha=1.6, blocks=1, expand_scale=1.4, holdout=8, seed=0,
+                    enabled=True, adaptive=True, rho=None):
+    """SessionOptions + ConsensusConfig (runtime.hpp:109-115, admm.hpp:20-29) + plan arguments."""
+    s = bsg_session_options()
+    s.total_iterations, s.interval, s.alpha = total_iterations, interval, alpha
+    s.mu, s.tau_inc, s.tau_dec, s.freeze_iteration = 10.0, 2.0, 2.0, 2000
+    s.adaptive, s.enabled = int(adaptive), int(enabled)
+    s.rho = rho if rho is not None else penalties()
+    s.seed, s.blocks, s.expand_scale, s.holdout = seed, blocks, expand_scale, holdout
+    return s
+
+
+def run_simulated(cloud, cams, gts, trainer_cfg, session, devices=(0,)):
+    """run_simulated (runtime.cpp:623-671) of the native host layer: plan_cluster
+    + K device BlockTrainers + device consensus rounds. Returns (model, rounds, wall_s)."""
+    load_library()
+    ids = np.ascontiguousarray(cloud["ids"], np.uint64)
+    n = len(ids)
+    fd = np.asarray(cloud["feat"]).reshape(n, -1).shape[1]
+    arrs = [_f64(cloud[k]) for k in ("pos", "rot", "ls", "feat", "op")]
+    cam_arr = (bsg_camera * len(cams))(*cams)
+    gts = [_f64(g) for g in gts]
+    gptr = (_DP * len(gts))(*[_ptr(g, ctypes.c_double) for g in gts])
+    outs = [np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros((n, fd)), np.zeros(n)]
+    max_rounds = int(session.total_iterations // max(session.interval, 1)) + 2
+    rounds = (bsg_round_diag * max_rounds)()
+    nr, wall = ctypes.c_size_t(), ctypes.c_double()
+    dev = (ctypes.c_int * len(devices))(*devices)
+    st = _lib.bsg_run_simulated(fd, n, _ptr(ids, ctypes.c_uint64), *[_ptr(a, ctypes.c_double) for a in arrs],
+                                len(cams), cam_arr, gptr, ctypes.byref(trainer_cfg), ctypes.byref(session),
+                                len(devices), dev, *[_ptr(o, ctypes.c_double) for o in outs], rounds, max_rounds,
+                                ctypes.byref(nr), ctypes.byref(wall))
+    if st != BSG_OK:
+        msg = _lib.bsg_driver_last_error().decode()
+        raise InvalidArgument(msg) if st == BSG_ERR_INVALID_ARGUMENT else BsgError(msg)
+    model = dict(ids=ids, pos=outs[0], rot=outs[1], ls=outs[2], feat=outs[3], op=outs[4])
+    rl = []
+    for j in range(min(nr.value, max_rounds)):
+        r = rounds[j]
+        rl.append(dict(iteration=r.iteration, primal=r.primal, dual=r.dual,
+                       rho=(r.rho.rho_p, r.rho.rho_q, r.rho.rho_s, r.rho.rho_f, r.rho.rho_o),
+                       max_disagreement=r.max_disagreement, dual_mean_linf=r.dual_mean_linf, mean_loss=r.mean_loss,
+                       shared_count=r.shared_count, global_count=r.global_count, consensus_ms=r.consensus_ms))
+    return model, rl, wall.value

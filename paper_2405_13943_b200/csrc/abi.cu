@@ -898,6 +898,17 @@ int bsg_download_duals(bsg_ctx* h, double* u_rows) {
     });
 }
 
+int bsg_upload_duals(bsg_ctx* h, const double* u_rows) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!c->anchored) throw Error{BSG_ERR_STATE, "duals before set_anchor"};
+        use_device(c);
+        const std::vector<float> uc = rows_to_cm(u_rows, c->n_shared, c->D);
+        if (c->n_shared) BSG_CUDA(cudaMemcpy(c->u, uc.data(), c->D * c->n_shared * 4, cudaMemcpyHostToDevice));
+    });
+}
+
 int bsg_download_anchor(bsg_ctx* h, double* z_rows) {
     return guarded([&] {
         auto* c = reinterpret_cast<Ctx*>(h);
@@ -917,6 +928,28 @@ int bsg_download_consensus(bsg_ctx* h, double* z_slots) {
         std::vector<float> hz(c->D * std::max<size_t>(c->n_slots, 1));
         if (c->n_slots) BSG_CUDA(cudaMemcpy(hz.data(), c->zslot, c->D * c->n_slots * 4, cudaMemcpyDeviceToHost));
         cm_to_rows(hz.data(), c->n_slots, c->D, z_slots);
+    });
+}
+
+int bsg_apply_broadcast(bsg_ctx* h, const double* z_slots, size_t n_reset, const uint32_t* reset_slots, double alpha,
+                        int relax) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        check_round_ready(c);
+        use_device(c);
+        if (c->n_slots) {
+            const std::vector<float> zc = rows_to_cm(z_slots, c->n_slots, c->D);
+            BSG_CUDA(cudaMemcpy(c->zslot, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpy(c->zprev, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemset(c->in_zprev, 1, c->n_slots));
+        }
+        bsg_round_args args{};
+        args.n_reset = n_reset;
+        args.reset_slots = reset_slots;
+        upload_resets(c, &args);
+        round_apply_broadcast(c, alpha, relax != 0, n_reset > 0);
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 

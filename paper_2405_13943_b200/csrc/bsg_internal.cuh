@@ -226,6 +226,7 @@ void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double
 void round_pack_q(Ctx* c);
 void round_pack_main(Ctx* c, double alpha, bool relax);
 void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_dev, size_t n_reset, bool diag);
+void round_apply_broadcast(Ctx* c, double alpha, bool relax, bool has_resets);
 
 // ---- the step ------------------------------------------------------------
 void ensure_image_buffers(Ctx* c, int W, int H);

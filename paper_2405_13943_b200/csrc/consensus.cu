@@ -236,6 +236,18 @@ void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_d
     }
 }
 
+// apply_broadcast with a host-provided z (trainer.cpp:168-223): zslot holds
+// z for every slot; no flips, resets from slot_reset.
+void round_apply_broadcast(Ctx* c, double alpha, bool relax, bool has_resets) {
+    BSG_CUDA(cudaMemsetAsync(c->round_scalars, 0, 8 * sizeof(double), c->stream));
+    BSG_CUDA(cudaMemsetAsync(c->pack + static_cast<size_t>(c->D) * c->n_slots, 0, c->n_slots * sizeof(float), c->stream));
+    if (c->n_shared == 0) return;
+    dual_update_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(
+        c->x, c->cap, c->D, c->sh_rows, c->sh_slots, c->n_shared, c->n_slots, c->pack, c->zslot,
+        has_resets ? c->slot_reset : nullptr, static_cast<float>(alpha), relax ? 1 : 0, c->z, c->u, c->round_scalars);
+    BSG_LAUNCHED(c);
+}
+
 void round_pack_duals(Ctx* c) {
     BSG_CUDA(cudaMemsetAsync(c->pack, 0, c->D * c->n_slots * sizeof(float), c->stream));
     if (c->n_shared == 0) return;

@@ -1,0 +1,113 @@
+// C++ self-test of the reference-shaped host API (include/blocksplat_gpu.hpp),
+// mirroring a few of the reference's own unit tests (test_renderer.cpp,
+// test_trainer.cpp) so that a reference call site is shown to compile and run
+// unchanged against the device implementation. Exit code = failures.
+#include <cmath>
+#include <cstdio>
+
+#include "../../include/blocksplat_gpu.hpp"
+
+using namespace blocksplat;
+
+static int failures = 0;
+#define CHECK(cond)                                                         \
+    do {                                                                    \
+        if (!(cond)) {                                                      \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);     \
+            ++failures;                                                     \
+        }                                                                   \
+    } while (0)
+
+static double logit(double p) { return std::log(p / (1.0 - p)); }
+
+static CameraView axis_camera(double f, double c, uint32_t size) {  // test_renderer.cpp:18-24
+    CameraView cam;
+    cam.fx = cam.fy = f;
+    cam.cx = cam.cy = c;
+    cam.width = cam.height = size;
+    return cam;
+}
+
+static void push(GaussianCloud& c, uint64_t id, Vec3 pos, Vec3 rgb, double opacity, double ls = -1.0) {
+    c.ids.push_back(id);
+    c.positions.insert(c.positions.end(), pos.begin(), pos.end());
+    c.rotations.insert(c.rotations.end(), {1, 0, 0, 0});
+    c.log_scales.insert(c.log_scales.end(), {ls, ls, ls});
+    for (double v : rgb) c.features.push_back(v / kSh0);
+    c.opacity_logits.push_back(logit(opacity));
+}
+
+int main() {
+    {  // test_renderer.cpp:204-216 single centred splat
+        GaussianCloud c(kFeatureDimDeg0);
+        push(c, 1, {0, 0, 5}, {0.9, 0.5, 0.25}, 0.8);
+        RenderOutput out = render(c, axis_camera(100, 8, 17));
+        const size_t px = 8 * 17 + 8;
+        CHECK(std::abs(out.color.data[3 * px] - 0.72) < 1e-6);
+        CHECK(std::abs(out.transmittance[px] - 0.2) < 1e-6);
+        CHECK(out.contributors[px] >= 1);
+    }
+    {  // test_renderer.cpp:272-282 early stop
+        GaussianCloud c(kFeatureDimDeg0);
+        for (int i = 0; i < 10; ++i) push(c, i + 1, {0, 0, 4 + 0.2 * i}, {0.5, 0.5, 0.5}, 0.9999);
+        RenderOutput out = render(c, axis_camera(100, 8, 17));
+        CHECK(out.contributors[8 * 17 + 8] == 3);
+    }
+    {  // test_renderer.cpp:373-387 culled rows
+        GaussianCloud c(kFeatureDimDeg0);
+        push(c, 1, {0, 0, 5}, {0.5, 0.5, 0.5}, 0.7);
+        push(c, 2, {0, 0, -5}, {0.5, 0.5, 0.5}, 0.7);
+        BackwardOutput bw = render_backward(c, axis_camera(100, 8, 17), Image(17, 17, 0.9));
+        CHECK(bw.visible[0] == 1 && bw.visible[1] == 0);
+        CHECK(bw.grads.opacity_logits[1] == 0.0 && bw.grads.opacity_logits[0] != 0.0);
+        bool threw = false;
+        try {
+            render_backward(c, axis_camera(100, 8, 17), Image(16, 17, 0.9));
+        } catch (const InvalidArgument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {  // test_trainer.cpp:275-306 anchor + broadcast bookkeeping
+        GaussianCloud c(kFeatureDimDeg0);
+        for (int i = 0; i < 3; ++i) push(c, i, {i * 5.0 - 5.0, 0, 5}, {0.5, 0.3, 0.2}, 0.5, -2.0);
+        Image img(8, 8, 0.0);
+        CameraView cam = look_at({0, 0, -5}, {0, 0, 5}, {0, 1, 0}, 10, 10, 4, 4, 8, 8);
+        TrainerConfig cfg;
+        cfg.iterations = 100;
+        BlockTrainer t(0, c, {TrainView{cam, &img}}, {0, 1}, 3, cfg);
+        PropertyPenalties rho;
+        GaussianCloud z0 = slice_by_ids(c, {0, 1});
+        for (double& v : z0.opacity_logits) v += 0.25;
+        t.set_anchor(z0, rho);
+        CHECK(t.anchor().ids == (std::vector<uint64_t>{0, 1}));
+        for (double v : t.duals().opacity_logits) CHECK(v == 0.0);
+        GaussianCloud z1 = slice_by_ids(c, {0});
+        for (double& v : z1.opacity_logits) v -= 0.5;
+        t.apply_broadcast(z1, {}, {1}, rho, 1.0, false);
+        CHECK(t.shared_ids() == (std::vector<uint64_t>{0}));
+        CHECK(std::abs(t.duals().opacity_logits[0] - 0.5) < 1e-6);
+        t.apply_broadcast(z1, {0}, {}, rho, 1.0, false);
+        CHECK(t.duals().opacity_logits[0] == 0.0);
+        const double l0 = t.train_step();
+        t.run_iterations(9);
+        CHECK(t.iteration() == 10);
+        CHECK(std::isfinite(l0) && std::isfinite(t.last_loss()));
+    }
+    {  // densification is rejected loudly, not silently ignored
+        GaussianCloud c(kFeatureDimDeg0);
+        push(c, 0, {0, 0, 5}, {0.5, 0.5, 0.5}, 0.5);
+        Image img(8, 8, 0.0);
+        TrainerConfig cfg;
+        cfg.densify.enabled = true;
+        bool threw = false;
+        try {
+            BlockTrainer t(0, c, {TrainView{axis_camera(10, 4, 8), &img}}, {}, 1, cfg);
+        } catch (const InvalidArgument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+    return failures;
+}

@@ -65,3 +65,30 @@ def test_look_at_matches_oracle():
     assert list(c.q) == list(o.q)
     np.testing.assert_array_equal(c.R, o.R)
     np.testing.assert_array_equal(c.t, np.array(o.t))
+
+
+def desk_scene():
+    from refcases import HostCloud as HC
+    sc = orc.SynthConfig()
+    sc.seed, sc.gaussians, sc.cameras, sc.image_size, sc.extent = 42, 200, 24, 96, 10.0
+    s = orc.generate_scene(sc)
+    p, c = s.points()
+    init = HC.from_oracle(orc.init_cloud_from_points(p, c, 0, 0.1)).narrowed()
+    s.has_checkpoint = True
+    s.checkpoint = init.oracle()
+    return s, init
+
+
+def test_planner_matches_oracle_plan():
+    s, init = desk_scene()
+    tc = orc.TrainerConfig()
+    plan = orc.plan_cluster(s, 4, 1.4, 8, tc)
+    centers = np.array([v.center() for v in s.views])
+    p = api.Plan(init.ids, init.pos, centers, 4, 1.4)
+    for b in range(4):
+        ids, views = p.block(b)
+        assert list(ids) == plan.shard_ids(b)
+        assert [v for v in views if v % 8 != 0] == plan.shard_views(b)
+        rows, slots, first = p.block_shared(b)
+        sids, _, _ = p.shared()
+        assert list(sids[slots]) == plan.shard_shared(b)
