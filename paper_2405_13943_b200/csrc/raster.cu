@@ -62,89 +62,140 @@ __global__ __launch_bounds__(256) void ranges_kernel(const uint32_t* __restrict_
     if (i == P - 1 || pkey[i + 1] != k) ranges[k].y = i + 1;
 }
 
-// K6: one CTA per 16x16 tile, one thread per pixel; splat records staged in
-// shared memory 256 at a time. renderer.cpp:160-181 semantics: per pixel,
-// contributors are the splats whose rect contains it, in (depth, index) order;
-// break before compositing once T < stop; alpha = min(o g, clamp); no 1/255 skip.
-__global__ __launch_bounds__(kTileThreads) void blend_fwd_kernel(const uint2* __restrict__ ranges,
-                                                                 const uint32_t* __restrict__ pval,
-                                                                 const float4* __restrict__ rec, int W, int H,
-                                                                 int tiles_x, double tstop, float aclamp,
-                                                                 double aclamp_d, float bg0,
-                                                                 float bg1, float bg2, float* __restrict__ out_rgb,
-                                                                 float* __restrict__ out_T,
-                                                                 uint32_t* __restrict__ out_n,
-                                                                 uint32_t* __restrict__ out_last) {
-    __shared__ float4 s_a[kTileThreads], s_b[kTileThreads], s_c[kTileThreads];
+// K7 blend forward: one CTA of 128 threads per 16x16 tile. Warp w owns the
+// 8x8 sub-tile (w & 1, w >> 1); each lane owns two pixels of it (rows ly and
+// ly + 4), so every shared-memory record load and rect unpack serves two
+// pixels. Splat records are staged 256 at a time with a 4-bit mask of the
+// sub-tiles their rect overlaps; a warp skips entries outside its sub-tile
+// with one uniform test. Semantics (renderer.cpp:160-181): per pixel, the
+// contributors are the splats whose rect contains it, in (depth, index)
+// order; break before compositing once T < stop; alpha = min(o g, clamp); no
+// 1/255 skip. The stop decision uses T in FP64 (stacked clamped splats give
+// T = (1 - 0.99)^k exactly at the 1e-4 threshold, test_renderer.cpp:272-282).
+constexpr int kBlendThreads = 128;
+constexpr int kBatch = 256;
+
+__device__ __forceinline__ uint32_t subtile_mask(int x0, int x1, int y0, int y1, int tx0, int ty0) {
+    // rect (tile-local) vs the four 8x8 sub-tiles
+    const int lx0 = x0 - tx0, lx1 = x1 - tx0, ly0 = y0 - ty0, ly1 = y1 - ty0;
+    const bool left = lx0 <= 7 && lx1 >= 0, right = lx1 >= 8 && lx0 <= 15;
+    const bool top = ly0 <= 7 && ly1 >= 0, bottom = ly1 >= 8 && ly0 <= 15;
+    return (left && top ? 1u : 0u) | (right && top ? 2u : 0u) | (left && bottom ? 4u : 0u) |
+           (right && bottom ? 8u : 0u);
+}
+
+__global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* __restrict__ ranges,
+                                                                  const uint32_t* __restrict__ pval,
+                                                                  const float4* __restrict__ rec, int W, int H,
+                                                                  int tiles_x, double tstop, float aclamp,
+                                                                  double aclamp_d, float bg0, float bg1, float bg2,
+                                                                  float* __restrict__ out_rgb,
+                                                                  float* __restrict__ out_T,
+                                                                  uint32_t* __restrict__ out_n,
+                                                                  uint32_t* __restrict__ out_last) {
+    __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
+    __shared__ uint8_t s_m[kBatch];
     const int tile = blockIdx.x;
-    const int px = (tile % tiles_x) * kTile + (threadIdx.x % kTile);
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
-    const bool inside = px < W && py < H;
+    const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx0 + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty0 + (warp >> 1) * 8 + (lane >> 3);
+    const int py1 = py0 + 4;
+    const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const uint2 range = ranges[tile];
-    // The stop decision tracks T in FP64 like the reference: stacked clamped
-    // splats give T = (1 - 0.99)^k exactly at the 1e-4 threshold (renderer
-    // KAT test_renderer.cpp:272-282), which FP32 would cross one splat early.
-    // Colour accumulation stays FP32.
-    float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    double Td = 1.0;
-    const double oma_clamp = 1.0 - static_cast<double>(aclamp_d);
-    uint32_t n = 0, last = 0;
-    bool done = !inside;
-    const float fx = static_cast<float>(px), fy = static_cast<float>(py);
-    for (uint32_t start = range.x; start < range.y; start += kTileThreads) {
-        if (__syncthreads_count(done) == kTileThreads) break;
-        const uint32_t idx = start + threadIdx.x;
-        if (idx < range.y) {
-            const size_t r = 3 * static_cast<size_t>(pval[idx]);
-            s_a[threadIdx.x] = rec[r];
-            s_b[threadIdx.x] = rec[r + 1];
-            s_c[threadIdx.x] = rec[r + 2];
+    const double oma_clamp = 1.0 - aclamp_d;
+    float T0 = 1.f, T1 = 1.f, r0 = 0.f, g0 = 0.f, b0 = 0.f, r1 = 0.f, g1 = 0.f, b1 = 0.f;
+    double Td0 = 1.0, Td1 = 1.0;
+    uint32_t n0 = 0, n1 = 0, last0 = 0, last1 = 0;
+    bool done0 = !in0, done1 = !in1;
+    const uint32_t wbit = 1u << warp;
+    const float fx = static_cast<float>(px), fy0 = static_cast<float>(py0), fy1 = static_cast<float>(py1);
+    for (uint32_t start = range.x; start < range.y; start += kBatch) {
+        if (__syncthreads_count(done0 && done1) == kBlendThreads) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t idx = start + threadIdx.x + h * kBlendThreads;
+            if (idx < range.y) {
+                const size_t r = 3 * static_cast<size_t>(pval[idx]);
+                const float4 c = rec[r + 2];
+                int x0, x1, y0, y1;
+                unpack_rect(c, x0, x1, y0, y1);
+                s_a[threadIdx.x + h * kBlendThreads] = rec[r];
+                s_b[threadIdx.x + h * kBlendThreads] = rec[r + 1];
+                s_c[threadIdx.x + h * kBlendThreads] = c;
+                s_m[threadIdx.x + h * kBlendThreads] = static_cast<uint8_t>(subtile_mask(x0, x1, y0, y1, tx0, ty0));
+            }
         }
         __syncthreads();
-        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kTileThreads), range.y - start));
-        for (int j = 0; !done && j < cnt; ++j) {
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBatch), range.y - start));
+        for (int j = 0; j < cnt && !(done0 && done1); ++j) {
+            if (!(s_m[j] & wbit)) continue;  // warp-uniform
             const float4 c = s_c[j];
             int x0, x1, y0, y1;
             unpack_rect(c, x0, x1, y0, y1);
-            if (px < x0 || px > x1 || py < y0 || py > y1) continue;
-            if (Td < tstop) {
-                done = true;
-                break;
-            }
+            const bool inx = px >= x0 && px <= x1;
+            const bool hit0 = !done0 && inx && py0 >= y0 && py0 <= y1;
+            const bool hit1 = !done1 && inx && py1 >= y0 && py1 <= y1;
+            if (!(hit0 || hit1)) continue;
             const float4 a = s_a[j], b = s_b[j];
-            const float dx = fx - a.x, dy = fy - a.y;
-            const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
-            const float g = __expf(-0.5f * q);
-            const float og = b.y * g;
-            // no float lies in [0.99, float(0.99)), so this is the FP64 clamp test
-            const bool clamped = og >= aclamp;
-            const float alpha = clamped ? aclamp : og;
-            const float w = alpha * T;
-            c0 += b.z * w;
-            c1 += b.w * w;
-            c2 += c.x * w;
-            T *= 1.f - alpha;
-            Td *= clamped ? oma_clamp : static_cast<double>(1.f - og);  // 1 - og exact for og >= 0.5
-            ++n;
-            last = start - range.x + j + 1;
+            const float dx = fx - a.x;
+            const uint32_t pos = start - range.x + j + 1;
+            if (hit0) {
+                if (Td0 < tstop) {
+                    done0 = true;
+                } else {
+                    const float dy = fy0 - a.y;
+                    const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
+                    const float og = b.y * __expf(-0.5f * q);
+                    const bool clamped = og >= aclamp;  // no float lies in [0.99, float(0.99))
+                    const float alpha = clamped ? aclamp : og;
+                    const float w = alpha * T0;
+                    r0 += b.z * w; g0 += b.w * w; b0 += c.x * w;
+                    T0 *= 1.f - alpha;
+                    Td0 *= clamped ? oma_clamp : static_cast<double>(1.f - og);  // 1 - og exact for og >= 0.5
+                    ++n0;
+                    last0 = pos;
+                }
+            }
+            if (hit1) {
+                if (Td1 < tstop) {
+                    done1 = true;
+                } else {
+                    const float dy = fy1 - a.y;
+                    const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
+                    const float og = b.y * __expf(-0.5f * q);
+                    const bool clamped = og >= aclamp;
+                    const float alpha = clamped ? aclamp : og;
+                    const float w = alpha * T1;
+                    r1 += b.z * w; g1 += b.w * w; b1 += c.x * w;
+                    T1 *= 1.f - alpha;
+                    Td1 *= clamped ? oma_clamp : static_cast<double>(1.f - og);
+                    ++n1;
+                    last1 = pos;
+                }
+            }
         }
     }
-    if (inside) {
-        const size_t p = static_cast<size_t>(py) * W + px;
-        out_rgb[3 * p + 0] = c0 + T * bg0;
-        out_rgb[3 * p + 1] = c1 + T * bg1;
-        out_rgb[3 * p + 2] = c2 + T * bg2;
-        out_T[p] = static_cast<float>(Td);
-        out_n[p] = n;
-        out_last[p] = last;
+    if (in0) {
+        const size_t p = static_cast<size_t>(py0) * W + px;
+        out_rgb[3 * p + 0] = r0 + T0 * bg0;
+        out_rgb[3 * p + 1] = g0 + T0 * bg1;
+        out_rgb[3 * p + 2] = b0 + T0 * bg2;
+        out_T[p] = static_cast<float>(Td0);
+        out_n[p] = n0;
+        out_last[p] = last0;
+    }
+    if (in1) {
+        const size_t p = static_cast<size_t>(py1) * W + px;
+        out_rgb[3 * p + 0] = r1 + T1 * bg0;
+        out_rgb[3 * p + 1] = g1 + T1 * bg1;
+        out_rgb[3 * p + 2] = b1 + T1 * bg2;
+        out_T[p] = static_cast<float>(Td1);
+        out_n[p] = n1;
+        out_last[p] = last1;
     }
 }
 
-// Transpose-reduce of 16 per-lane values across a warp in 8+4+2+1+1 = 16
-// shuffles (instead of 16 x 5): at each halving step a lane keeps one half
-// of its values and receives the partner's copy of that half. On return,
-// lane l holds the full warp sum of value index ((l >> 1) & 15) bit-reversed
-// per the step order; `reduced_index` gives the mapping.
 __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
     const bool h16 = lane & 16;
 #pragma unroll
@@ -181,112 +232,141 @@ __device__ __forceinline__ int reduced_index(int lane) {
     return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
 }
 
-// K8: reverse traversal (renderer.cpp:274-311). Each pixel rewinds exactly
-// the contributors it composited (T recovered by division, 1-alpha >= 0.01);
-// the per-splat image-space gradients of the 32 pixels of a warp are reduced
-// with shuffles before one set of global vector atomics per warp.
-__global__ __launch_bounds__(kTileThreads) void blend_bwd_kernel(const uint2* __restrict__ ranges,
-                                                                 const uint32_t* __restrict__ pval,
-                                                                 const float4* __restrict__ rec, int W, int H,
-                                                                 int tiles_x, float aclamp, float bg0, float bg1,
-                                                                 float bg2, const float* __restrict__ in_T,
-                                                                 const uint32_t* __restrict__ in_last,
-                                                                 const float* __restrict__ dl_dc,
-                                                                 float4* __restrict__ g2d) {
-    __shared__ float4 s_a[kTileThreads], s_b[kTileThreads], s_c[kTileThreads];
-    __shared__ uint32_t s_row[kTileThreads];
+// Per-pixel reverse recurrence (renderer.cpp:288-308) for one contributor;
+// accumulates this pixel's share of the splat's 9 image-space gradients.
+struct BwdPix {
+    float T, d0, d1, d2, s0, s1, s2;
+};
+
+__device__ __forceinline__ void bwd_step(BwdPix& P, float dx, float dy, const float4& a, const float4& b,
+                                         const float4& c, float aclamp, float (&acc)[9]) {
+    const float mdx = a.z * dx + a.w * dy, mdy = a.w * dx + b.x * dy;
+    const float q = dx * mdx + dy * mdy;
+    const float g = __expf(-0.5f * q);
+    const float og = b.y * g;
+    const float alpha = fminf(og, aclamp);
+    const float inv = __frcp_rn(1.f - alpha);  // 1 - alpha >= 0.01
+    const float Tb = P.T * inv;
+    const float at = alpha * Tb;
+    acc[5] += P.d0 * at;
+    acc[6] += P.d1 * at;
+    acc[7] += P.d2 * at;
+    const float dlda = (P.d0 * (b.z * Tb - P.s0 * inv) + P.d1 * (b.w * Tb - P.s1 * inv)) + P.d2 * (c.x * Tb - P.s2 * inv);
+    if (og < aclamp) {
+        const float k = dlda * b.y * g;
+        acc[0] += k * mdx;
+        acc[1] += k * mdy;
+        const float h = 0.5f * k;
+        acc[2] += h * (mdx * mdx);
+        acc[3] += h * (mdx * mdy);
+        acc[4] += h * (mdy * mdy);
+        acc[8] += dlda * g;
+    }
+    P.s0 += b.z * at;
+    P.s1 += b.w * at;
+    P.s2 += c.x * at;
+    P.T = Tb;
+}
+
+// K9 blend backward: reverse traversal of each pixel's composited list
+// (T recovered by division, 1 - alpha >= 0.01), same CTA layout as K7 (two
+// pixels per lane, per-warp sub-tile skip). The 9 per-splat gradients of the
+// warp's 64 pixels are summed in registers, transpose-reduced across the warp
+// in 16 shuffles and added with 9 scalar atomics; one or two contributing
+// lanes add directly.
+__global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2* __restrict__ ranges,
+                                                                  const uint32_t* __restrict__ pval,
+                                                                  const float4* __restrict__ rec, int W, int H,
+                                                                  int tiles_x, float aclamp, float bg0, float bg1,
+                                                                  float bg2, const float* __restrict__ in_T,
+                                                                  const uint32_t* __restrict__ in_last,
+                                                                  const float* __restrict__ dl_dc,
+                                                                  float4* __restrict__ g2d) {
+    __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
+    __shared__ uint32_t s_row[kBatch];
+    __shared__ uint8_t s_m[kBatch];
     __shared__ uint32_t s_max;
     const int tile = blockIdx.x;
-    const int px = (tile % tiles_x) * kTile + (threadIdx.x % kTile);
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
-    const bool inside = px < W && py < H;
+    const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx0 + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty0 + (warp >> 1) * 8 + (lane >> 3);
+    const int py1 = py0 + 4;
+    const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const uint2 range = ranges[tile];
-    const int lane = threadIdx.x & 31;
-    uint32_t my_last = 0;
-    float T = 1.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
-    if (inside) {
-        const size_t p = static_cast<size_t>(py) * W + px;
-        my_last = in_last[p];
-        T = in_T[p];
-        d0 = dl_dc[3 * p];
-        d1 = dl_dc[3 * p + 1];
-        d2 = dl_dc[3 * p + 2];
+    BwdPix P0{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, P1{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint32_t last0 = 0, last1 = 0;
+    if (in0) {
+        const size_t p = static_cast<size_t>(py0) * W + px;
+        last0 = in_last[p];
+        P0.T = in_T[p];
+        P0.d0 = dl_dc[3 * p]; P0.d1 = dl_dc[3 * p + 1]; P0.d2 = dl_dc[3 * p + 2];
     }
-    float s0 = T * bg0, s1 = T * bg1, s2 = T * bg2;  // suffix: contributions behind
+    if (in1) {
+        const size_t p = static_cast<size_t>(py1) * W + px;
+        last1 = in_last[p];
+        P1.T = in_T[p];
+        P1.d0 = dl_dc[3 * p]; P1.d1 = dl_dc[3 * p + 1]; P1.d2 = dl_dc[3 * p + 2];
+    }
+    P0.s0 = P0.T * bg0; P0.s1 = P0.T * bg1; P0.s2 = P0.T * bg2;  // suffix: contributions behind
+    P1.s0 = P1.T * bg0; P1.s1 = P1.T * bg1; P1.s2 = P1.T * bg2;
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
-    // warp max then one shared atomic per warp
-    uint32_t wm = my_last;
+    uint32_t wm = max(last0, last1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
     if (lane == 0) atomicMax(&s_max, wm);
     __syncthreads();
     const uint32_t max_last = s_max;
-    const float fx = static_cast<float>(px), fy = static_cast<float>(py);
-    for (int64_t end = max_last; end > 0; end -= kTileThreads) {
-        const int64_t start = end - kTileThreads > 0 ? end - kTileThreads : 0;
+    const uint32_t wbit = 1u << warp;
+    const float fx = static_cast<float>(px), fy0 = static_cast<float>(py0), fy1 = static_cast<float>(py1);
+    for (int64_t end = max_last; end > 0; end -= kBatch) {
+        const int64_t start = end - kBatch > 0 ? end - kBatch : 0;
         __syncthreads();
-        const int64_t li = start + threadIdx.x;
-        if (li < end) {
-            const uint32_t row = pval[range.x + li];
-            const size_t r = 3 * static_cast<size_t>(row);
-            s_a[threadIdx.x] = rec[r];
-            s_b[threadIdx.x] = rec[r + 1];
-            s_c[threadIdx.x] = rec[r + 2];
-            s_row[threadIdx.x] = row;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = threadIdx.x + h * kBlendThreads;
+            const int64_t li = start + t;
+            if (li < end) {
+                const uint32_t row = pval[range.x + li];
+                const size_t r = 3 * static_cast<size_t>(row);
+                const float4 c = rec[r + 2];
+                int x0, x1, y0, y1;
+                unpack_rect(c, x0, x1, y0, y1);
+                s_a[t] = rec[r];
+                s_b[t] = rec[r + 1];
+                s_c[t] = c;
+                s_row[t] = row;
+                s_m[t] = static_cast<uint8_t>(subtile_mask(x0, x1, y0, y1, tx0, ty0));
+            }
         }
         __syncthreads();
         for (int64_t j = end - 1; j >= start; --j) {
             const int sj = static_cast<int>(j - start);
+            if (!(s_m[sj] & wbit)) continue;  // warp-uniform
             const float4 c = s_c[sj];
             int x0, x1, y0, y1;
             unpack_rect(c, x0, x1, y0, y1);
-            const bool contrib = static_cast<uint32_t>(j) < my_last && px >= x0 && px <= x1 && py >= y0 && py <= y1;
-            float gmx = 0.f, gmy = 0.f, gc00 = 0.f, gc01 = 0.f, gc11 = 0.f, gr = 0.f, gg = 0.f, gb = 0.f, go = 0.f;
-            if (contrib) {
-                const float4 a = s_a[sj], b = s_b[sj];
-                const float dx = fx - a.x, dy = fy - a.y;
-                const float mdx = a.z * dx + a.w * dy, mdy = a.w * dx + b.x * dy;
-                const float q = dx * mdx + dy * mdy;
-                const float g = __expf(-0.5f * q);
-                const float og = b.y * g;
-                const float alpha = fminf(og, aclamp);
-                const float oma = 1.f - alpha;
-                const float inv = 1.f / oma;
-                const float Tb = T * inv;
-                const float at = alpha * Tb;
-                gr = d0 * at;
-                gg = d1 * at;
-                gb = d2 * at;
-                const float dlda = (d0 * (b.z * Tb - s0 * inv) + d1 * (b.w * Tb - s1 * inv)) + d2 * (c.x * Tb - s2 * inv);
-                if (og < aclamp) {
-                    const float dl_dg = dlda * b.y;
-                    const float k = dl_dg * g;
-                    gmx = k * mdx;
-                    gmy = k * mdy;
-                    const float h = 0.5f * k;
-                    gc00 = h * (mdx * mdx);
-                    gc01 = h * (mdx * mdy);
-                    gc11 = h * (mdy * mdy);
-                    go = dlda * g;
-                }
-                s0 += b.z * at;
-                s1 += b.w * at;
-                s2 += c.x * at;
-                T = Tb;
-            }
-            const unsigned mask = __ballot_sync(0xffffffffu, contrib);
+            const bool inx = px >= x0 && px <= x1;
+            const bool hit0 = static_cast<uint32_t>(j) < last0 && inx && py0 >= y0 && py0 <= y1;
+            const bool hit1 = static_cast<uint32_t>(j) < last1 && inx && py1 >= y0 && py1 <= y1;
+            const unsigned mask = __ballot_sync(0xffffffffu, hit0 || hit1);
             if (mask == 0) continue;
+            float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const float4 a = s_a[sj], b = s_b[sj];
+            const float dx = fx - a.x;
+            if (hit0) bwd_step(P0, dx, fy0 - a.y, a, b, c, aclamp, acc);
+            if (hit1) bwd_step(P1, dx, fy1 - a.y, a, b, c, aclamp, acc);
             float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(s_row[sj]));
             if (__popc(mask) <= 2) {
-                // one or two contributing pixels: direct atomics are cheaper than a reduction
-                if (contrib) {
-                    atomicAdd(reinterpret_cast<float4*>(dst), make_float4(gmx, gmy, gc00, gc01));
-                    atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(gc11, gr, gg, gb));
-                    atomicAdd(dst + 8, go);
+                if (hit0 || hit1) {
+                    atomicAdd(reinterpret_cast<float4*>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
+                    atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+                    atomicAdd(dst + 8, acc[8]);
                 }
             } else {
-                float vals[16] = {gmx, gmy, gc00, gc01, gc11, gr, gg, gb, go, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                float vals[16] = {acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8],
+                                  0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 const float r = transpose_reduce16(vals, lane);
                 const int idx = reduced_index(lane);
                 if ((lane & 1) == 0 && idx < 9) atomicAdd(dst + idx, r);
@@ -315,7 +395,7 @@ void launch_ranges(Ctx* c, const DevCam& cam, uint32_t P) {
 
 void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
-    blend_fwd_kernel<<<ntiles, kTileThreads, 0, c->stream>>>(
+    blend_fwd_kernel<<<ntiles, kBlendThreads, 0, c->stream>>>(
         c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, rc.tstop,
         static_cast<float>(rc.alpha_clamp), rc.alpha_clamp, rc.bg[0], rc.bg[1], rc.bg[2], c->out_rgb, c->out_T,
         c->out_n, c->out_last);
@@ -324,7 +404,7 @@ void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
 
 void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
-    blend_bwd_kernel<<<ntiles, kTileThreads, 0, c->stream>>>(
+    blend_bwd_kernel<<<ntiles, kBlendThreads, 0, c->stream>>>(
         c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.alpha_clamp),
         rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d);
     BSG_LAUNCHED(c);
