@@ -42,6 +42,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--views", type=int, default=CFG["views"], help="fewer views for profiling runs only")
+    p.add_argument("--profile", action="store_true",
+                   help="ncu mode: constant ground truth (no GT renders), no e2e/CPU legs")
     return p.parse_args()
 
 
@@ -109,7 +111,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_block(rank, world, n, device, n_views=CFG["views"]):
+def build_block(rank, world, n, device, n_views=CFG["views"], constant_gt=False):
     """Scene -> plan -> this rank's block on the device, GT rendered on device."""
     from paper_2405_13943_b200 import api
     from paper_2405_13943_b200.scene import aerial_scene, perturbed_init
@@ -122,11 +124,14 @@ def build_block(rank, world, n, device, n_views=CFG["views"]):
     ids, views = plan.block(rank)
     sel = ids.astype(np.int64)  # ids are 0..n-1 = row indices of the global cloud
     # ground truth of this block's views: the generating cloud rendered on device
-    gt_block = api.Block(device, 3)
-    gt_block.upload_cloud(cloud["ids"], cloud["pos"], cloud["rot"], cloud["ls"], cloud["feat"], cloud["op"])
     view_cams = [cams[v].device() for v in views]
-    gts = [gt_block.render(c)[0] for c in view_cams]
-    gt_block.close()
+    if constant_gt:
+        gts = [np.full((CFG["height"], CFG["width"], 3), 0.5) for _ in view_cams]
+    else:
+        gt_block = api.Block(device, 3)
+        gt_block.upload_cloud(cloud["ids"], cloud["pos"], cloud["rot"], cloud["ls"], cloud["feat"], cloud["op"])
+        gts = [gt_block.render(c)[0] for c in view_cams]
+        gt_block.close()
     blk = api.Block(device, 3)
     blk.upload_cloud(init["ids"][sel], init["pos"][sel], init["rot"][sel], init["ls"][sel], init["feat"][sel],
                      init["op"][sel])
@@ -172,7 +177,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    blk, view_cams, gts, info = build_block(rank, world, args.n, local_rank, args.views)
+    blk, view_cams, gts, info = build_block(rank, world, args.n, local_rank, args.views, args.profile)
     if world > 1:
         import torch.distributed as dist
         uid = [api.nccl_unique_id() if rank == 0 else None]
@@ -242,6 +247,10 @@ def run_ours(args, rank, world, local_rank):
     ms_step = ms_total / args.steps
     blk.enable_stage_timing(False)
 
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "ms_per_step": ms_step}), flush=True)
+        return
     # end-to-end: ground truth copied from pinned host memory every step, loss read back
     pinned = [torch.from_numpy(g.astype(np.float32)).pin_memory() for g in gts]
     e2e_steps = max(5, args.steps // 2)

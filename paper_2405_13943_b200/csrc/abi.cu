@@ -218,23 +218,38 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     const uint32_t V = c->counters_host->visible;
     stage_begin(c, kStDepthSort);
-    // (depth, index) order: stable LSD sort of the FP64 depth bits over rows in
-    // ascending index order (renderer.cpp:86-89). Positive doubles order as u64.
-    radix_sort_u64(c, c->vkey, c->vrow, V, 8, &c->counters->depth_hist[0][0], &c->counters_host->depth_hist[0][0],
+    // (depth, index) order (renderer.cpp:86-89): stable LSD sort of the upper
+    // 32 bits of the FP64 depth (positive doubles order as u64) over rows in
+    // ascending index order, then runs of equal upper bits sorted by the lower
+    // 32 bits. A run longer than 64 falls back to all 8 digit passes.
+    radix_sort_u64(c, c->vkey, c->vrow, V, 4, 8, &c->counters->depth_hist[0][0], &c->counters_host->depth_hist[0][0],
                    &c->depth_sorted);
+    depth_tie_fixup(c, c->vkey[c->depth_sorted], c->vrow[c->depth_sorted], V, &c->counters->overflow);
     stage_end(c, kStDepthSort);
     stage_begin(c, kStPairs);
     scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
-    BSG_CUDA(cudaMemcpyAsync(&c->counters_host->pairs, &c->counters->pairs, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                             c->stream));
+    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, 16, cudaMemcpyDeviceToHost, c->stream));
     BSG_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->counters_host->overflow) {
+        // rare: a long run of equal upper depth bits -> full 64-bit sort
+        BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
+        compact_visible(c, static_cast<uint32_t>(c->n));
+        BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist),
+                                 cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        radix_sort_u64(c, c->vkey, c->vrow, V, 0, 8, &c->counters->depth_hist[0][0],
+                       &c->counters_host->depth_hist[0][0], &c->depth_sorted);
+        scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
+        BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, 16, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+    }
     const uint32_t P = V ? c->counters_host->pairs : 0;
     ensure_pair_capacity(c, P);
     launch_pairs(c, cam, V);  // + digit histograms of the tile keys
     stage_end(c, kStPairs);
     stage_begin(c, kStTileSort);
     const int passes = (tile_bits(cam) + 7) / 8;
-    radix_sort_u32(c, c->pkey, c->pval, P, passes, &c->counters->tile_hist[0][0], nullptr, &c->pairs_sorted);
+    radix_sort_u32(c, c->pkey, c->pval, P, 0, passes, &c->counters->tile_hist[0][0], nullptr, &c->pairs_sorted);
     stage_end(c, kStTileSort);
     stage_begin(c, kStRanges);
     launch_ranges(c, cam, P);

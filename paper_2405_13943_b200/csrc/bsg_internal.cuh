@@ -196,10 +196,13 @@ void compact_visible(Ctx* c, uint32_t n);
 // counts (produced by the kernel that wrote the keys) and is turned into
 // offsets in place; h_hist (nullable) is a host copy used to skip passes
 // whose digit is constant. Result lands in buffer *sel.
-void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
-                    const uint32_t* h_hist, int* sel);
-void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
-                    const uint32_t* h_hist, int* sel);
+void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
+                    uint32_t* d_hist, const uint32_t* h_hist, int* sel);
+void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
+                    uint32_t* d_hist, const uint32_t* h_hist, int* sel);
+// Sorts runs of equal upper-32-bit depth keys by their lower 32 bits (stable);
+// sets *long_run if a run exceeds 64 (caller redoes the full sort).
+void depth_tie_fixup(Ctx* c, uint64_t* keys, uint32_t* rows, uint32_t V, uint32_t* long_run);
 
 // ---- rasterizer stages (preprocess.cu, raster.cu, ssim.cu, adam.cu) ----
 DevCam make_cam(const bsg_camera& c);

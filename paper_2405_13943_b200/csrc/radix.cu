@@ -153,7 +153,7 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
 }
 
 template <typename K, int ITEMS>
-void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes, uint32_t* d_hist,
                    const uint32_t* h_hist, int* sel) {
     constexpr int kTileKeys = kRsThreads * ITEMS;
     const uint32_t tiles = (n + kTileKeys - 1) / kTileKeys;
@@ -167,7 +167,7 @@ void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int passes
     BSG_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int cur = 0;
-    for (int p = 0; p < passes; ++p) {
+    for (int p = first_pass; p < passes; ++p) {
         if (h_hist) {
             bool trivial = false;
             for (int d = 0; d < 256; ++d)
@@ -185,32 +185,70 @@ void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int passes
 }
 
 template <typename K>
-void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes, uint32_t* d_hist,
                 const uint32_t* h_hist, int* sel) {
     *sel = 0;
     if (n <= 1) return;
     if (n >= (1u << 30)) throw Error{BSG_ERR_CAPACITY, "radix sort supports < 2^30 keys"};
-    radix_offsets_kernel<<<passes, 256, 0, c->stream>>>(d_hist);
+    radix_offsets_kernel<<<passes - first_pass, 256, 0, c->stream>>>(d_hist + 256 * first_pass);
     BSG_LAUNCHED(c);
     // Small inputs get small tiles so the grid still covers the 148 SMs.
     if (n < (1u << 19))
-        launch_passes<K, 4>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+        launch_passes<K, 4>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
     else if (n < (1u << 21))
-        launch_passes<K, 8>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+        launch_passes<K, 8>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
     else
-        launch_passes<K, 16>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+        launch_passes<K, 16>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
+}
+
+// After a stable sort on the upper 32 bits of the FP64 depth, splats whose
+// depths share those bits (|dz|/z < 2^-20) are still in row order; sort each
+// such run by the low 32 bits, stably, so the result is the full (depth,
+// index) order of renderer.cpp:86-89. Runs longer than 64 are flagged and the
+// caller falls back to the full 64-bit sort.
+__global__ void depth_tie_fixup_kernel(uint64_t* __restrict__ keys, uint32_t* __restrict__ rows, uint32_t V,
+                                       uint32_t* __restrict__ long_run) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= V) return;
+    const uint32_t hi = static_cast<uint32_t>(keys[i] >> 32);
+    if (i > 0 && static_cast<uint32_t>(keys[i - 1] >> 32) == hi) return;  // not a run start
+    if (i + 1 >= V || static_cast<uint32_t>(keys[i + 1] >> 32) != hi) return;  // singleton
+    uint32_t e = i + 2;
+    while (e < V && static_cast<uint32_t>(keys[e] >> 32) == hi && e - i <= 64) ++e;
+    if (e - i > 64) {
+        atomicOr(long_run, 1u);
+        return;
+    }
+    for (uint32_t a = i + 1; a < e; ++a) {
+        const uint64_t k = keys[a];
+        const uint32_t r = rows[a];
+        uint32_t b = a;
+        while (b > i && keys[b - 1] > k) {
+            keys[b] = keys[b - 1];
+            rows[b] = rows[b - 1];
+            --b;
+        }
+        keys[b] = k;
+        rows[b] = r;
+    }
 }
 
 }  // namespace
 
-void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
-                    const uint32_t* h_hist, int* sel) {
-    radix_sort<uint64_t>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
+                    uint32_t* d_hist, const uint32_t* h_hist, int* sel) {
+    radix_sort<uint64_t>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
 }
 
-void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
-                    const uint32_t* h_hist, int* sel) {
-    radix_sort<uint32_t>(c, keys, vals, n, passes, d_hist, h_hist, sel);
+void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
+                    uint32_t* d_hist, const uint32_t* h_hist, int* sel) {
+    radix_sort<uint32_t>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
+}
+
+void depth_tie_fixup(Ctx* c, uint64_t* keys, uint32_t* rows, uint32_t V, uint32_t* long_run) {
+    if (V < 2) return;
+    depth_tie_fixup_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(keys, rows, V, long_run);
+    BSG_LAUNCHED(c);
 }
 
 }  // namespace bsg

@@ -219,3 +219,22 @@ def test_fd_gradients_through_device():
                 checked += 1
                 failed += not ok
     assert failed <= 0.01 * checked, (failed, checked)
+
+
+def test_equal_depth_runs_keep_index_order():
+    """Many splats with bit-identical FP64 depth (a fronto-parallel plane seen
+    by an axis camera): the upper-32-bit depth sort + tie fix-up must give
+    (depth, index) order; a run longer than 64 takes the full 64-bit path."""
+    g = np.random.default_rng(7)
+    for n_plane, n_other in ((40, 60), (300, 100)):
+        rows = []
+        for i in range(n_plane):
+            splat_at(rows, i, [g.uniform(-0.5, 0.5), g.uniform(-0.5, 0.5), 5.0], (0.5, 0.2, 0.1), 0.5, -3.0)
+        for i in range(n_other):
+            splat_at(rows, n_plane + i, [g.uniform(-0.5, 0.5), g.uniform(-0.5, 0.5), g.uniform(4.0, 6.0)],
+                     (0.1, 0.2, 0.5), 0.5, -3.0)
+        c = cloud_from_rows(rows).narrowed()
+        cam = axis_camera(100, 32, 64)
+        got = new_block(c).project(dev_cam(cam))
+        want = orc.project(c.oracle(), cam, orc.RenderConfig())
+        assert np.array_equal(got["order"], want["order"])
