@@ -210,7 +210,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     launch_preprocess(c, cam, rc);
     stage_end(c, kStPreprocess);
     stage_begin(c, kStCompact);
-    compact_visible(c, static_cast<uint32_t>(c->n));  // + digit histograms of the depth keys
+    compact_visible(c, static_cast<uint32_t>(c->n), 4);  // + digit histograms of the upper depth bytes
     stage_end(c, kStCompact);
     // One readback: V and the depth-key histograms (pass skipping).
     BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist), cudaMemcpyDeviceToHost,
@@ -233,7 +233,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     if (c->counters_host->overflow) {
         // rare: a long run of equal upper depth bits -> full 64-bit sort
         BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
-        compact_visible(c, static_cast<uint32_t>(c->n));
+        compact_visible(c, static_cast<uint32_t>(c->n), 0);
         BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist),
                                  cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));

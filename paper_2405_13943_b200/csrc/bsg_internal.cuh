@@ -190,7 +190,8 @@ struct Error {
 void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,
                         uint32_t* total_dev);
 // Stable compaction of rows with tiles[i] > 0: writes keys/rows in row order and V.
-void compact_visible(Ctx* c, uint32_t n);
+// hist_first: lowest depth-key byte whose digit histogram is built.
+void compact_visible(Ctx* c, uint32_t n, int hist_first);
 // Stable LSD radix sort (onesweep) of (u64 key, u32 val) / (u32 key, u32 val)
 // over `passes` 8-bit digits from bit 0. d_hist holds the per-pass digit
 // counts (produced by the kernel that wrote the keys) and is turned into

@@ -95,6 +95,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   uint32_t* __restrict__ out_last) {
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint8_t s_m[kBatch];
+    __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
     const int tile = blockIdx.x;
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -128,8 +129,18 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
         }
         __syncthreads();
         const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBatch), range.y - start));
-        for (int j = 0; j < cnt && !(done0 && done1); ++j) {
-            if (!(s_m[j] & wbit)) continue;  // warp-uniform
+        // this warp's entries (rect overlaps its sub-tile), in list order
+        int nl = 0;
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
+            const int e = c0 + lane;
+            const bool mine = e < cnt && (s_m[e] & wbit);
+            const unsigned bal = __ballot_sync(0xffffffffu, mine);
+            if (mine) s_list[warp][nl + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
+            nl += __popc(bal);
+        }
+        __syncwarp();
+        for (int k = 0; k < nl && !(done0 && done1); ++k) {
+            const int j = s_list[warp][k];
             const float4 c = s_c[j];
             int x0, x1, y0, y1;
             unpack_rect(c, x0, x1, y0, y1);
@@ -139,7 +150,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
             if (!(hit0 || hit1)) continue;
             const float4 a = s_a[j], b = s_b[j];
             const float dx = fx - a.x;
-            const uint32_t pos = start - range.x + j + 1;
+            const uint32_t pos = start - range.x + static_cast<uint32_t>(j) + 1;
             if (hit0) {
                 if (Td0 < tstop) {
                     done0 = true;
@@ -285,6 +296,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint32_t s_row[kBatch];
     __shared__ uint8_t s_m[kBatch];
+    __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
     __shared__ uint32_t s_max;
     const int tile = blockIdx.x;
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
@@ -320,13 +332,13 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
     const uint32_t max_last = s_max;
     const uint32_t wbit = 1u << warp;
     const float fx = static_cast<float>(px), fy0 = static_cast<float>(py0), fy1 = static_cast<float>(py1);
-    for (int64_t end = max_last; end > 0; end -= kBatch) {
-        const int64_t start = end - kBatch > 0 ? end - kBatch : 0;
+    for (int end = static_cast<int>(max_last); end > 0; end -= kBatch) {
+        const int start = end - kBatch > 0 ? end - kBatch : 0;
         __syncthreads();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int t = threadIdx.x + h * kBlendThreads;
-            const int64_t li = start + t;
+            const int li = start + t;
             if (li < end) {
                 const uint32_t row = pval[range.x + li];
                 const size_t r = 3 * static_cast<size_t>(row);
@@ -341,9 +353,20 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             }
         }
         __syncthreads();
-        for (int64_t j = end - 1; j >= start; --j) {
-            const int sj = static_cast<int>(j - start);
-            if (!(s_m[sj] & wbit)) continue;  // warp-uniform
+        // this warp's entries (rect overlaps its sub-tile), ascending
+        const int cnt = end - start;
+        int nl = 0;
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
+            const int e = c0 + lane;
+            const bool mine = e < cnt && (s_m[e] & wbit);
+            const unsigned bal = __ballot_sync(0xffffffffu, mine);
+            if (mine) s_list[warp][nl + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
+            nl += __popc(bal);
+        }
+        __syncwarp();
+        for (int k = nl - 1; k >= 0; --k) {
+            const int sj = s_list[warp][k];
+            const int j = start + sj;
             const float4 c = s_c[sj];
             int x0, x1, y0, y1;
             unpack_rect(c, x0, x1, y0, y1);

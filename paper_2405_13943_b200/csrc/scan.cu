@@ -83,7 +83,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                                                             uint32_t* total_out, const uint64_t* __restrict__ keys,
                                                             uint64_t* __restrict__ out_keys,
                                                             uint32_t* __restrict__ out_rows,
-                                                            uint32_t* __restrict__ hist_out) {
+                                                            uint32_t* __restrict__ hist_out, int hist_first) {
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_hist[MODE == 1 ? 8 * 256 : 1];
@@ -140,7 +140,8 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                     out_rows[run] = static_cast<uint32_t>(i);
                     out[run] = static_cast<uint32_t>(i);
 #pragma unroll
-                    for (int p = 0; p < 8; ++p) atomicAdd(&s_hist[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
+                    for (int p = 0; p < 8; ++p)
+                        if (p >= hist_first) atomicAdd(&s_hist[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
                 }
             } else {
                 out[i] = run;
@@ -178,11 +179,11 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
-                                                          nullptr, nullptr, nullptr);
+                                                          nullptr, nullptr, nullptr, 0);
     BSG_LAUNCHED(c);
 }
 
-void compact_visible(Ctx* c, uint32_t n) {
+void compact_visible(Ctx* c, uint32_t n, int hist_first) {
     if (n == 0) {
         BSG_CUDA(cudaMemsetAsync(&c->counters->visible, 0, sizeof(uint32_t), c->stream));
         return;
@@ -193,7 +194,7 @@ void compact_visible(Ctx* c, uint32_t n) {
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
                                                           &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0],
-                                                          &c->counters->depth_hist[0][0]);
+                                                          &c->counters->depth_hist[0][0], hist_first);
     BSG_LAUNCHED(c);
 }
 
