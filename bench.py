@@ -34,8 +34,8 @@ CFG = dict(n=2_000_000, width=1024, height=768, views=64, extent=100.0, scale=1.
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=400)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--interval", type=int, default=25, help="consensus interval (iterations)")
     p.add_argument("--n", type=int, default=CFG["n"])
@@ -61,7 +61,8 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons, sampled every 20 ms from before
+    the warm-up; stop(t0, t1) keeps the samples taken inside [t0, t1]."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -74,7 +75,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                          "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -83,11 +84,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def stop(self):
+    def wait_first(self, timeout=5.0):
+        t = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def stop(self, t0=None, t1=None):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -95,7 +102,8 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        window = [ln for ts, ln in self.lines if t0 is None or (t0 <= ts <= t1)]
+        for ln in window:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -150,22 +158,27 @@ def build_block(rank, world, n, device, n_views=CFG["views"], constant_gt=False)
 
 
 def algorithmic_bytes(stage, n, V, P, HW, shared):
-    """SURVEY §8(d) fused-minimum byte accounting per launch of the stage's kernel."""
-    if stage == "fold_adam":
-        return 340 * n + 64 * V + 112 * shared       # x,m,v read+write (14 f32 each), tiles, g2d, densify stats, z,u
-    if stage == "preprocess":
-        return 60 * n + 104 * V                     # params read, tiles write; record + key + zeroed grads
-    if stage == "blend_fwd":
-        return 52 * P + 24 * HW                     # pair index + 48 B record per pair; rgb,T,n,last per pixel
-    if stage == "blend_bwd":
-        return 52 * P + 20 * HW + 48 * V            # records, per-pixel T,last,dL/dC, one gradient record per splat
-    if stage == "loss_ssim":
-        return 24 * HW + 36 * HW + 36 * HW + 24 * HW + 12 * HW
-    if stage == "depth_sort":
-        return 8 * V + 7 * 24 * V                   # histogram read + passes (key u64 + row u32, read+write)
-    if stage == "tile_sort":
-        return 4 * P + 2 * 16 * P
-    return None
+    """SURVEY §8(d) fused-minimum byte accounting per launch of each stage
+    (n rows, V visible splats, P tile pairs, HW pixels, D = 14 FP32 components
+    per row at SH degree 0). DESIGN.md §3 lists the same figures."""
+    D4 = 56
+    model = {
+        # x, m, v read + written for every row; visibility flag; gradient of visible rows; z, u of shared rows
+        "adam": 6 * D4 * n + 4 * n + D4 * V + 2 * D4 * shared,
+        # visible row's parameters + 2D gradient record read; parameter gradient + densify stats written
+        "fold": (D4 + 48 + 4) * V + (D4 + 8) * V,
+        # pos + log-scale of every row, tiles-touched written; rest of the row, splat record, depth key,
+        # zeroed gradient record for visible rows
+        "preprocess": 28 * n + (32 + 48 + 8 + 48) * V,
+        "compact": 4 * n + 16 * V,
+        "depth_sort": 4 * 24 * V,                   # 4 LSD passes over (u64 key, u32 row), read + write
+        "pairs": 12 * V + 8 * P,
+        "tile_sort": 2 * 16 * P,                    # ceil(12 tile bits / 8) passes over (u32 key, u32 row)
+        "blend_fwd": 52 * P + 24 * HW,              # pair row + 48 B record per pair; rgb, T, n, last per pixel
+        "loss_ssim": 36 * HW,                       # rendered + GT read, dL/dC written (fused minimum)
+        "blend_bwd": 52 * P + 20 * HW + 48 * V,     # records; T, last, dL/dC per pixel; one gradient record per splat
+    }
+    return model.get(stage)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -205,38 +218,33 @@ def run_ours(args, rank, world, local_rank):
             return blk.consensus_round(1.6, True)
         return None
 
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    clocks.wait_first()
     # warm-up
     it = 0
     for _ in range(args.warmup):
         blk.train_steps([next_view()], want_losses=False)
         it += 1
         consensus(it)
-    blk.enable_stage_timing(True)
-    stage_sum = {}
-    counters_sum = dict(visible=0, pairs=0)
+    # timed region: steps back to back, no per-stage events or host reads
     round_ms = []
-    clocks = ClockSampler(local_rank)
     barrier()
     torch.cuda.synchronize()
     launches0 = blk.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks.start()
+    tc0 = time.perf_counter()
     e0.record(stream)
     for s in range(args.steps):
         blk.train_steps([next_view()], want_losses=False)
         it += 1
-        for k, v in blk.stage_times().items():
-            stage_sum[k] = stage_sum.get(k, 0.0) + v
-        c = blk.step_counters()
-        counters_sum["visible"] += c["visible"]
-        counters_sum["pairs"] += c["pairs"]
         r = consensus(it)
         if r is not None:
             round_ms.append(r["ms"])
     e1.record(stream)
     torch.cuda.synchronize()
+    tc1 = time.perf_counter()
     barrier()
-    clk = clocks.stop()
     launches = blk.launch_count() - launches0
     elapsed = e0.elapsed_time(e1)
     t = torch.tensor([elapsed], device="cuda")
@@ -245,6 +253,22 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
+    clk = clocks.stop(tc0, tc1)
+
+    # per-stage breakdown: a separate pass with CUDA events between the stages
+    blk.enable_stage_timing(True)
+    stage_steps = min(args.steps, 100)
+    stage_sum = {}
+    counters_sum = dict(visible=0, pairs=0)
+    for s in range(stage_steps):
+        blk.train_steps([next_view()], want_losses=False)
+        it += 1
+        consensus(it)
+        for k, v in blk.stage_times().items():
+            stage_sum[k] = stage_sum.get(k, 0.0) + v
+        c = blk.step_counters()
+        counters_sum["visible"] += c["visible"]
+        counters_sum["pairs"] += c["pairs"]
     blk.enable_stage_timing(False)
 
     if args.profile:
@@ -278,25 +302,34 @@ def run_ours(args, rank, world, local_rank):
             import torch.distributed as dist
             dist.destroy_process_group()
         return
-    stage_ms = {k: v / args.steps for k, v in stage_sum.items()}
+    stage_ms = {k: v / stage_steps for k, v in stage_sum.items()}
     dominant = max(stage_ms, key=stage_ms.get)
-    # roofline of the dominant single-kernel stage with a byte model
-    candidates = [k for k in ("fold_adam", "blend_fwd", "blend_bwd", "preprocess", "loss_ssim") if k in stage_ms]
-    roof_stage = max(candidates, key=lambda k: stage_ms[k])
-    V = counters_sum["visible"] / args.steps
-    P = counters_sum["pairs"] / args.steps
+    V = counters_sum["visible"] / stage_steps
+    P = counters_sum["pairs"] / stage_steps
     HW = CFG["width"] * CFG["height"]
     nb = info["block_gaussians"]
-    bytes_ = algorithmic_bytes(roof_stage, nb, V, P, HW, info["block_shared"])
     peak, peak_kind = peaks()
-    achieved = bytes_ / (stage_ms[roof_stage] * 1e-3) / 1e9
-    traffic = None
+    traffic_all = {}
     prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(roof_stage)
+            traffic_all = json.load(open(prof))
         except Exception:
-            traffic = None
+            traffic_all = {}
+
+    def roof(stage):
+        b = algorithmic_bytes(stage, nb, V, P, HW, info["block_shared"])
+        if b is None or stage_ms.get(stage, 0) <= 0:
+            return None
+        a = b / (stage_ms[stage] * 1e-3) / 1e9
+        tr = traffic_all.get(stage)
+        return {"kernel": stage, "bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+                "traffic": float(sum(tr.values())) if tr else None, "algorithmic_bytes_per_launch": b,
+                "peak_source": peak_kind}
+
+    stage_roofs = {k: roof(k) for k in stage_ms if roof(k) is not None}
+    roof_stage = max(stage_roofs, key=lambda k: stage_ms[k])
+    roofline = stage_roofs[roof_stage]
     out = {
         "metric": "training iters/sec (K=N blocks, 1 block per GPU)",
         "value": 1000.0 / ms_step,
@@ -319,14 +352,16 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": 1000.0 / e2e_ms_step, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "stage_ms_note": f"separate {stage_steps}-step pass with CUDA events between stages (adds one host sync per step)",
         "dominant_stage": dominant,
         "visible_per_step": V,
         "pairs_per_step": P,
         "consensus_ms_per_round": float(np.mean(round_ms)) if round_ms else 0.0,
         "consensus_ms_per_iter": (float(np.mean(round_ms)) / args.interval) if round_ms else 0.0,
-        "roofline": {"kernel": roof_stage, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": bytes_,
-                     "peak_source": peak_kind},
+        "roofline": roofline,
+        "stage_rooflines": {k: {"achieved": round(v["achieved"], 1), "frac": round(v["frac"], 4),
+                                "algorithmic_bytes": round(v["algorithmic_bytes_per_launch"]),
+                                "traffic": v["traffic"]} for k, v in stage_roofs.items()},
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:

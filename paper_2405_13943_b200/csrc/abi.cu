@@ -77,7 +77,7 @@ void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
     void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->gbuf,
-                    c->anchor_of_row, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
+                    c->vis_mask, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
                     c->ssim_f, c->gt_stage, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
@@ -111,7 +111,9 @@ void alloc_rows(Ctx* c, size_t n) {
     dev_alloc(&c->tiles, cap);
     dev_alloc(&c->g2d, 3 * cap);
     dev_alloc(&c->gbuf, c->D * cap);
-    dev_alloc(&c->anchor_of_row, cap);
+    dev_alloc(&c->vis_mask, cap / 32);
+    dev_alloc(&c->sh_mask, cap / 32);
+    dev_alloc(&c->sh_prefix, cap / 32);
     dev_alloc(&c->vkey[0], cap);
     dev_alloc(&c->vkey[1], cap);
     dev_alloc(&c->vrow[0], cap);
@@ -519,7 +521,9 @@ int bsg_upload_cloud(bsg_ctx* h, size_t n, const uint64_t* ids, const double* po
         BSG_CUDA(cudaMemsetAsync(c->v, 0, c->D * c->cap * sizeof(float), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->anchor_of_row, 0xff, c->cap * sizeof(int32_t), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->vis_mask, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->sh_mask, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->sh_prefix, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->adam_t = 0;
         c->iteration = 0;
@@ -862,9 +866,16 @@ int bsg_set_shared(bsg_ctx* h, size_t ns, const uint32_t* rows, const uint32_t* 
             BSG_CUDA(cudaMemcpy(c->sh_first, first, ns, cudaMemcpyHostToDevice));
         }
         if (n_slots) BSG_CUDA(cudaMemcpy(c->slot_owners, owners, n_slots * 4, cudaMemcpyHostToDevice));
-        std::vector<int32_t> aor(c->cap, -1);
-        for (size_t j = 0; j < ns; ++j) aor[rows[j]] = static_cast<int32_t>(j);
-        BSG_CUDA(cudaMemcpy(c->anchor_of_row, aor.data(), aor.size() * 4, cudaMemcpyHostToDevice));
+        // anchor index of a row = its rank among the (ascending) shared rows
+        std::vector<uint32_t> mask(c->cap / 32, 0), prefix(c->cap / 32, 0);
+        for (size_t j = 0; j < ns; ++j) mask[rows[j] / 32] |= 1u << (rows[j] % 32);
+        uint32_t run = 0;
+        for (size_t w = 0; w < mask.size(); ++w) {
+            prefix[w] = run;
+            run += static_cast<uint32_t>(__builtin_popcount(mask[w]));
+        }
+        BSG_CUDA(cudaMemcpy(c->sh_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice));
+        BSG_CUDA(cudaMemcpy(c->sh_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice));
         BSG_CUDA(cudaMemset(c->in_zprev, 0, std::max<size_t>(n_slots, 1)));
         c->anchored = false;
     });

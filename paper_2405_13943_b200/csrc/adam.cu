@@ -15,7 +15,13 @@ namespace {
 // Fold of one visible row; FP64 arithmetic over FP32 inputs. g receives the
 // D parameter gradients; returns the screen-space gradient norm.
 template <int fd>
-__device__ __forceinline__ double fold_row(const float* __restrict__ x, size_t cap, uint32_t i, const DevCam& cam,
+__device__ __forceinline__ void load_row(const float* __restrict__ x, size_t cap, uint32_t i, float (&prm)[11 + fd]) {
+#pragma unroll
+    for (int k = 0; k < 11 + fd; ++k) prm[k] = x[k * cap + i];
+}
+
+template <int fd>
+__device__ __forceinline__ double fold_row(const float (&prm)[11 + fd], uint32_t i, const DevCam& cam,
                                            const float4* __restrict__ g2d, double* g) {
     const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
                  gcx = g2d[3 * static_cast<size_t>(i) + 2];
@@ -24,14 +30,14 @@ __device__ __forceinline__ double fold_row(const float* __restrict__ x, size_t c
     const double gcol[3] = {gb.y, gb.z, gb.w};
     const double gop = gcx.x;
 
-    const double pos[3] = {x[(kPos + 0) * cap + i], x[(kPos + 1) * cap + i], x[(kPos + 2) * cap + i]};
+    const double pos[3] = {prm[kPos + 0], prm[kPos + 1], prm[kPos + 2]};
     double pc[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) pc[r] = ((cam.R[3 * r] * pos[0] + cam.R[3 * r + 1] * pos[1]) + cam.R[3 * r + 2] * pos[2]) + cam.t[r];
     const double z = pc[2], iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
 
     // opacity logit (renderer.cpp:325-327)
-    const double ol = x[op_comp(fd) * cap + i];
+    const double ol = prm[kFeat + fd];  // op_comp(fd)
     const double o = 1.0 / (1.0 + exp(-ol));
     g[op_comp(fd)] = gop * o * (1.0 - o);
 
@@ -50,8 +56,7 @@ __device__ __forceinline__ double fold_row(const float* __restrict__ x, size_t c
             g[kFeat + 3 + 3 * ch] = b0 * gcol[ch];
             g[kFeat + 4 + 3 * ch] = b1 * gcol[ch];
             g[kFeat + 5 + 3 * ch] = b2 * gcol[ch];
-            const double f3 = x[(kFeat + 3 + 3 * ch) * cap + i], f4 = x[(kFeat + 4 + 3 * ch) * cap + i],
-                         f5 = x[(kFeat + 5 + 3 * ch) * cap + i];
+            const double f3 = prm[kFeat + 3 + 3 * ch], f4 = prm[kFeat + 4 + 3 * ch], f5 = prm[kFeat + 5 + 3 * ch];
             gd[0] += gcol[ch] * (f5 * -kSh1);
             gd[1] += gcol[ch] * (f3 * -kSh1);
             gd[2] += gcol[ch] * (f4 * kSh1);
@@ -76,8 +81,7 @@ __device__ __forceinline__ double fold_row(const float* __restrict__ x, size_t c
 #pragma unroll
         for (int k = 0; k < 3; ++k) A[r][k] = J[r][0] * cam.R[k] + J[r][1] * cam.R[3 + k] + J[r][2] * cam.R[6 + k];
 
-    double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
-           qz = x[(kRot + 3) * cap + i];
+    double qw = prm[kRot + 0], qx = prm[kRot + 1], qy = prm[kRot + 2], qz = prm[kRot + 3];
     const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
     double hw, hx, hy, hz;
     if (qn == 0.0) {
@@ -89,8 +93,8 @@ __device__ __forceinline__ double fold_row(const float* __restrict__ x, size_t c
     R[0][0] = 1 - 2 * (hy * hy + hz * hz); R[0][1] = 2 * (hx * hy - hw * hz); R[0][2] = 2 * (hx * hz + hw * hy);
     R[1][0] = 2 * (hx * hy + hw * hz); R[1][1] = 1 - 2 * (hx * hx + hz * hz); R[1][2] = 2 * (hy * hz - hw * hx);
     R[2][0] = 2 * (hx * hz - hw * hy); R[2][1] = 2 * (hy * hz + hw * hx); R[2][2] = 1 - 2 * (hx * hx + hy * hy);
-    const double sc[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])), exp(static_cast<double>(x[(kLs + 1) * cap + i])),
-                          exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
+    const double sc[3] = {exp(static_cast<double>(prm[kLs + 0])), exp(static_cast<double>(prm[kLs + 1])),
+                          exp(static_cast<double>(prm[kLs + 2]))};
     double M[3][3], S[3][3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -173,7 +177,11 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
     for (int c = 0; c < D; ++c) g[c] = 0.0;
     double s = 0.0;
     const bool visible = tiles[i] > 0;
-    if (visible) s = fold_row<fd>(x, cap, i, cam, g2d, g);
+    if (visible) {
+        float prm[11 + fd];
+        load_row<fd>(x, cap, i, prm);
+        s = fold_row<fd>(prm, i, cam, g2d, g);
+    }
 #pragma unroll
     for (int c = 0; c < D; ++c) gout[static_cast<size_t>(c) * n + i] = g[c];
     sgn_out[i] = s;
@@ -195,82 +203,97 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
     double g[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) g[c] = 0.0;
-    const double s = fold_row<fd>(x, cap, i, cam, g2d, g);
+    float prm[11 + fd];
+    load_row<fd>(x, cap, i, prm);
+    const double s = fold_row<fd>(prm, i, cam, g2d, g);
 #pragma unroll
     for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + i] = static_cast<float>(g[c]);
     grad_accum[i] += static_cast<float>(s);
     grad_seen[i] += 1u;
 }
 
-// Dense Adam over every row (trainer.cpp:267-281), element-wise: thread =
-// 4 consecutive rows of one component (float4 loads/stores of x, m, v), so the
-// kernel is a pure coalesced stream. blockIdx.y selects the component; y == 3
-// is the quaternion group, whose 4 components per row are updated together
-// and then canonicalised (cloud.cpp:82-85, math.hpp:25-34). Rows not visible
-// this step have a zero render gradient; shared rows add rho (x - z + u)
-// evaluated at the pre-step x (admm.cpp:24-28, trainer.cpp:257-265).
+// Dense Adam over every row (trainer.cpp:267-281), element-wise: a thread
+// owns Q quads of 4 consecutive rows of one component (float4 loads/stores of
+// x, m, v), so the kernel is a pure coalesced stream. Launch 1 covers the 10
+// scalar components (blockIdx.y, Q = 2); launch 2 the quaternion group, whose
+// 4 components per row are updated together and then canonicalised
+// (cloud.cpp:82-85, math.hpp:25-34). Visibility comes from the 1-bit-per-row
+// mask built by the compaction, shared-row anchors from a bit mask + per-word
+// prefix (anchor index = rank of the row among the shared rows), so no
+// per-row side array is re-read per component. Rows not visible this step
+// have a zero render gradient; shared rows add rho (x - z + u) evaluated at
+// the pre-step x (admm.cpp:24-28, trainer.cpp:257-265).
 __device__ __forceinline__ float adam_update(float x, float g, float& m, float& v, float lr, const AdamStep& st) {
     m = st.b1 * m + st.omb1 * g;
     v = st.b2 * v + st.omb2 * g * g;
     return x - lr * (m * st.inv_bc1) / (sqrtf(v * st.inv_bc2) + st.eps);
 }
 
+__device__ __forceinline__ int comp_of_group(int y) { return y < 3 ? y : y + 4; }  // pos 0-2, ls/feat/op 7..
+
+template <bool ROT, int Q>
 __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
-                                                   size_t cap, uint32_t n, const uint32_t* __restrict__ tiles,
+                                                   size_t cap, uint32_t n, const uint32_t* __restrict__ vis_mask,
                                                    const float* __restrict__ gbuf,
-                                                   const int32_t* __restrict__ anchor_of_row, const float* __restrict__ z,
+                                                   const uint32_t* __restrict__ sh_mask,
+                                                   const uint32_t* __restrict__ sh_prefix, const float* __restrict__ z,
                                                    const float* __restrict__ u, size_t ns, AdamStep st,
                                                    double* __restrict__ penalty) {
     __shared__ double s_red[8];
-    const uint32_t r0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-    const int y = blockIdx.y;
-    const bool rot = y == 3;
-    const int c0 = rot ? kRot : (y < 3 ? y : y + 3);
-    const int nc = rot ? 4 : 1;
+    constexpr int NC = ROT ? 4 : 1;
+    const int c0 = ROT ? kRot : comp_of_group(blockIdx.y);
     double pen = 0.0;
-    if (r0 < n) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t r0 = 4 * ((blockIdx.x * blockDim.x + threadIdx.x) * Q + q);
+        if (r0 >= n) break;
         const int nr = n - r0 >= 4 ? 4 : static_cast<int>(n - r0);
-        const uint4 t4 = *reinterpret_cast<const uint4*>(tiles + r0);
-        const uint32_t tv[4] = {t4.x, t4.y, t4.z, t4.w};
+        const uint32_t word = r0 >> 5, bit0 = r0 & 31u;
+        const uint32_t vis = (vis_mask[word] >> bit0) & 0xfu;
         int aj[4] = {-1, -1, -1, -1};
         if (st.has_anchor) {
-            const int4 a4 = *reinterpret_cast<const int4*>(anchor_of_row + r0);
-            aj[0] = a4.x; aj[1] = a4.y; aj[2] = a4.z; aj[3] = a4.w;
-        }
-        float xs[4][4];  // [component][row]
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (k < nc) {
-                const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
-                const float4 x4 = *reinterpret_cast<const float4*>(x + off);
-                float4 m4 = *reinterpret_cast<const float4*>(m + off);
-                float4 v4 = *reinterpret_cast<const float4*>(v + off);
-                const float xr[4] = {x4.x, x4.y, x4.z, x4.w};
-                float mr[4] = {m4.x, m4.y, m4.z, m4.w}, vr[4] = {v4.x, v4.y, v4.z, v4.w};
-                const float lr = st.lr[c0 + k], rho = st.rho[c0 + k];
+            const uint32_t sm = sh_mask[word];
+            if ((sm >> bit0) & 0xfu) {
+                const uint32_t pre = sh_prefix[word];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    float g = tv[r] > 0 ? gbuf[off + r] : 0.f;
-                    if (aj[r] >= 0) {
-                        const float d = xr[r] - z[static_cast<size_t>(c0 + k) * ns + aj[r]] +
-                                        u[static_cast<size_t>(c0 + k) * ns + aj[r]];
-                        if (r < nr) pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
-                        g += rho * d;
-                    }
-                    xs[k][r] = adam_update(xr[r], g, mr[r], vr[r], lr, st);
-                }
-                if (nr == 4) {
-                    *reinterpret_cast<float4*>(m + off) = make_float4(mr[0], mr[1], mr[2], mr[3]);
-                    *reinterpret_cast<float4*>(v + off) = make_float4(vr[0], vr[1], vr[2], vr[3]);
-                } else {
-                    for (int r = 0; r < nr; ++r) {
-                        m[off + r] = mr[r];
-                        v[off + r] = vr[r];
-                    }
+                    const uint32_t b = bit0 + r;
+                    if ((sm >> b) & 1u) aj[r] = static_cast<int>(pre + __popc(sm & ((1u << b) - 1u)));
                 }
             }
         }
-        if (rot) {
+        float xs[NC][4];  // [component][row]
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
+            const float4 x4 = *reinterpret_cast<const float4*>(x + off);
+            const float4 m4 = *reinterpret_cast<const float4*>(m + off);
+            const float4 v4 = *reinterpret_cast<const float4*>(v + off);
+            const float xr[4] = {x4.x, x4.y, x4.z, x4.w};
+            float mr[4] = {m4.x, m4.y, m4.z, m4.w}, vr[4] = {v4.x, v4.y, v4.z, v4.w};
+            const float lr = st.lr[c0 + k], rho = st.rho[c0 + k];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                float g = ((vis >> r) & 1u) ? gbuf[off + r] : 0.f;
+                if (aj[r] >= 0) {
+                    const float d = xr[r] - z[static_cast<size_t>(c0 + k) * ns + aj[r]] +
+                                    u[static_cast<size_t>(c0 + k) * ns + aj[r]];
+                    if (r < nr) pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
+                    g += rho * d;
+                }
+                xs[k][r] = adam_update(xr[r], g, mr[r], vr[r], lr, st);
+            }
+            if (nr == 4) {
+                *reinterpret_cast<float4*>(m + off) = make_float4(mr[0], mr[1], mr[2], mr[3]);
+                *reinterpret_cast<float4*>(v + off) = make_float4(vr[0], vr[1], vr[2], vr[3]);
+            } else {
+                for (int r = 0; r < nr; ++r) {
+                    m[off + r] = mr[r];
+                    v[off + r] = vr[r];
+                }
+            }
+        }
+        if constexpr (ROT) {
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 float qw = xs[0][r], qx = xs[1][r], qy = xs[2][r], qz = xs[3][r];
@@ -287,14 +310,12 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (k < nc) {
-                const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
-                if (nr == 4) {
-                    *reinterpret_cast<float4*>(x + off) = make_float4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
-                } else {
-                    for (int r = 0; r < nr; ++r) x[off + r] = xs[k][r];
-                }
+        for (int k = 0; k < NC; ++k) {
+            const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
+            if (nr == 4) {
+                *reinterpret_cast<float4*>(x + off) = make_float4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
+            } else {
+                for (int r = 0; r < nr; ++r) x[off + r] = xs[k][r];
             }
         }
     }
@@ -341,9 +362,15 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     (void)loss_out;
     (void)step_index;
     if (c->n == 0) return;
-    const dim3 grid(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(c->D - 3));
-    adam_kernel<<<grid, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, static_cast<uint32_t>(c->n), c->tiles, c->gbuf,
-                                             c->anchor_of_row, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
+    const uint32_t n = static_cast<uint32_t>(c->n);
+    const int scalar_groups = c->D - 4;  // every component but the quaternion
+    const dim3 g1(static_cast<uint32_t>((c->n + 2047) / 2048), static_cast<uint32_t>(scalar_groups));
+    adam_kernel<false, 2><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
+                                                     c->sh_prefix, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
+    BSG_LAUNCHED(c);
+    const dim3 g2(static_cast<uint32_t>((c->n + 1023) / 1024), 1);
+    adam_kernel<true, 1><<<g2, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
+                                                    c->sh_prefix, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }
 

@@ -84,7 +84,9 @@ struct Ctx {
     uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
     float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
     float* gbuf = nullptr;         // parameter gradient of visible rows, [D][cap]
-    int32_t* anchor_of_row = nullptr;  // anchor index j or -1
+    uint32_t* vis_mask = nullptr;  // 1 bit per row: visible this step (written by the compaction)
+    uint32_t* sh_mask = nullptr;   // 1 bit per row: shared (has an anchor)
+    uint32_t* sh_prefix = nullptr; // shared rows before each 32-row word (anchor index = prefix + rank in word)
 
     // compaction + depth sort (ping-pong)
     uint64_t* vkey[2] = {nullptr, nullptr};

@@ -24,10 +24,10 @@ __device__ __forceinline__ int to_int_clamped(double v) {
 }
 
 constexpr int kPreThreads = 256;
-constexpr int kPreRowsPerThread = 8;
+constexpr int kPreRowsPerThread = 4;
 constexpr int kPreChunk = kPreThreads * kPreRowsPerThread;
 
-// Two phases per CTA over a chunk of 2048 rows. Phase 1 (FP32, every row):
+// Two phases per CTA over a chunk of 1024 rows. Phase 1 (FP32, every row):
 // a conservative reject -- lambda_max(cov2d) <= |J|_F^2 max(s)^2 + dilation
 // (A = J W with W orthonormal, |Sigma|_2 = max(s)^2), so a centre farther
 // outside the image than sigma_extent sqrt(bound) (+1% and 2 px slack for
@@ -36,7 +36,7 @@ constexpr int kPreChunk = kPreThreads * kPreRowsPerThread;
 // the queue with every lane busy (rows are in id order, i.e. spatially random,
 // so doing this per thread would leave most lanes of a warp idle). The
 // visible set and every rect are exactly those of the exact path.
-__global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
+__global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
                                                                  int fd, DevCam cam, DevRender rc,
                                                                  float4* __restrict__ rec,
                                                                  uint64_t* __restrict__ depth_key,
@@ -55,10 +55,23 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
 #pragma unroll
     for (int k = 0; k < 3; ++k) tf[k] = static_cast<float>(cam.t[k]);
     const float nearf = static_cast<float>(rc.near_plane);
+    // all loads of the thread's rows first (one DRAM round trip), then the tests
+    float pp[kPreRowsPerThread][3], ll[kPreRowsPerThread][3];
+#pragma unroll
+    for (int k = 0; k < kPreRowsPerThread; ++k) {
+        const uint32_t i = chunk0 + k * kPreThreads + threadIdx.x;
+        const uint32_t j = i < n ? i : 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            pp[k][a] = x[(kPos + a) * cap + j];
+            ll[k][a] = x[(kLs + a) * cap + j];
+        }
+    }
+#pragma unroll
     for (int k = 0; k < kPreRowsPerThread; ++k) {
         const uint32_t i = chunk0 + k * kPreThreads + threadIdx.x;
         if (i >= n) break;
-        const float p0 = x[(kPos + 0) * cap + i], p1 = x[(kPos + 1) * cap + i], p2 = x[(kPos + 2) * cap + i];
+        const float p0 = pp[k][0], p1 = pp[k][1], p2 = pp[k][2];
         const float z = (Rf[6] * p0 + Rf[7] * p1) + Rf[8] * p2 + tf[2];
         const float px = (Rf[0] * p0 + Rf[1] * p1) + Rf[2] * p2 + tf[0];
         const float py = (Rf[3] * p0 + Rf[4] * p1) + Rf[5] * p2 + tf[1];
@@ -69,7 +82,7 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
             const float fxz = fxf * iz, fyz = fyf * iz;
             const float jx = fxz * px * iz, jy = fyz * py * iz;
             const float jf2 = fxz * fxz + fyz * fyz + jx * jx + jy * jy;
-            const float lmax = fmaxf(fmaxf(x[(kLs + 0) * cap + i], x[(kLs + 1) * cap + i]), x[(kLs + 2) * cap + i]);
+            const float lmax = fmaxf(fmaxf(ll[k][0], ll[k][1]), ll[k][2]);
             const float smax = expf(lmax) * 1.01f;
             const float rb = static_cast<float>(rc.sigma_extent) * sqrtf(jf2 * smax * smax + static_cast<float>(rc.dilation)) * 1.01f + 2.0f;
             const float mxf = fxz * px + cxf, myf = fyz * py + cyf;
@@ -87,7 +100,14 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
     const uint32_t count = s_count;
     for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
         const uint32_t i = s_rows[q];
-        const double p0 = x[(kPos + 0) * cap + i], p1 = x[(kPos + 1) * cap + i], p2 = x[(kPos + 2) * cap + i];
+        // every parameter of the row up front: one dependent DRAM round trip
+        float prm[kMaxD];
+#pragma unroll
+        for (int k = 0; k < 11 + 3; ++k) prm[k] = x[k * cap + i];
+        if (fd >= 12)
+#pragma unroll
+            for (int k = 14; k < 11 + kMaxFd; ++k) prm[k] = x[k * cap + i];
+        const double p0 = prm[kPos + 0], p1 = prm[kPos + 1], p2 = prm[kPos + 2];
         // p_cam = R p + t (camera.hpp:28)
         double pc[3];
 #pragma unroll
@@ -95,8 +115,7 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
         uint32_t ntiles = 0;
         if (pc[2] > rc.near_plane) {
             // Sigma = (R S)(R S)^T, R from the normalized quaternion (cloud.cpp:162-167, math.hpp:25-44)
-            double qw = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
-                   qz = x[(kRot + 3) * cap + i];
+            double qw = prm[kRot + 0], qx = prm[kRot + 1], qy = prm[kRot + 2], qz = prm[kRot + 3];
             const double qn = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
             if (qn == 0.0) {
                 qw = 1.0; qx = 0.0; qy = 0.0; qz = 0.0;
@@ -107,9 +126,8 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
             R[0][0] = 1 - 2 * (qy * qy + qz * qz); R[0][1] = 2 * (qx * qy - qw * qz); R[0][2] = 2 * (qx * qz + qw * qy);
             R[1][0] = 2 * (qx * qy + qw * qz); R[1][1] = 1 - 2 * (qx * qx + qz * qz); R[1][2] = 2 * (qy * qz - qw * qx);
             R[2][0] = 2 * (qx * qz - qw * qy); R[2][1] = 2 * (qy * qz + qw * qx); R[2][2] = 1 - 2 * (qx * qx + qy * qy);
-            const double s[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])),
-                                 exp(static_cast<double>(x[(kLs + 1) * cap + i])),
-                                 exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
+            const double s[3] = {exp(static_cast<double>(prm[kLs + 0])), exp(static_cast<double>(prm[kLs + 1])),
+                                 exp(static_cast<double>(prm[kLs + 2]))};
             double M[3][3];
 #pragma unroll
             for (int a = 0; a < 3; ++a)
@@ -158,7 +176,7 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
                 const double m00 = C[1][1] / det, m01 = -C[0][1] / det, m11 = C[0][0] / det;
                 double col[3];
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(x[(kFeat + ch) * cap + i]);
+                for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(prm[kFeat + ch]);
                 if (fd >= 12) {
                     const double u0 = p0 - cam.center[0], u1 = p1 - cam.center[1], u2 = p2 - cam.center[2];
                     const double un = sqrt((u0 * u0 + u1 * u1) + u2 * u2);
@@ -166,11 +184,11 @@ __global__ __launch_bounds__(kPreThreads) void preprocess_kernel(const float* __
                     const double b0 = -kSh1 * d1, b1 = kSh1 * d2, b2 = -kSh1 * d0;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch)
-                        col[ch] += b0 * static_cast<double>(x[(kFeat + 3 + 3 * ch) * cap + i]) +
-                                   b1 * static_cast<double>(x[(kFeat + 4 + 3 * ch) * cap + i]) +
-                                   b2 * static_cast<double>(x[(kFeat + 5 + 3 * ch) * cap + i]);
+                        col[ch] += b0 * static_cast<double>(prm[kFeat + 3 + 3 * ch]) +
+                                   b1 * static_cast<double>(prm[kFeat + 4 + 3 * ch]) +
+                                   b2 * static_cast<double>(prm[kFeat + 5 + 3 * ch]);
                 }
-                const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[op_comp(fd) * cap + i])));
+                const double o = 1.0 / (1.0 + exp(-static_cast<double>(fd >= 12 ? prm[kFeat + kMaxFd] : prm[kFeat + 3])));  // op_comp(fd)
                 const uint32_t r01 = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
                 const uint32_t r23 = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
                 rec[3 * static_cast<size_t>(i) + 0] =

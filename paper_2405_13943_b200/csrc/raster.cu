@@ -13,6 +13,21 @@
 namespace bsg {
 namespace {
 
+// exp(-q/2) as one MUFU.EX2 (ex2.approx.ftz: ~2 ulp; results below 2^-126
+// flush to 0, i.e. alpha < 1e-38) and a 1-MUFU reciprocal, shared by the
+// forward and backward blends so both see bit-identical alphas.
+constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 * log2(e)
+__device__ __forceinline__ float gauss_weight(float q) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(q * kNegHalfLog2e));
+    return y;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ void unpack_rect(const float4& c, int& x0, int& x1, int& y0, int& y1) {
     const uint32_t r01 = __float_as_uint(c.y), r23 = __float_as_uint(c.z);
     x0 = static_cast<int>(r01 & 0xffffu);
@@ -157,7 +172,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                 } else {
                     const float dy = fy0 - a.y;
                     const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
-                    const float og = b.y * __expf(-0.5f * q);
+                    const float og = b.y * gauss_weight(q);
                     const bool clamped = og >= aclamp;  // no float lies in [0.99, float(0.99))
                     const float alpha = clamped ? aclamp : og;
                     const float w = alpha * T0;
@@ -174,7 +189,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                 } else {
                     const float dy = fy1 - a.y;
                     const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
-                    const float og = b.y * __expf(-0.5f * q);
+                    const float og = b.y * gauss_weight(q);
                     const bool clamped = og >= aclamp;
                     const float alpha = clamped ? aclamp : og;
                     const float w = alpha * T1;
@@ -207,40 +222,36 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
     }
 }
 
-__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
-    const bool h16 = lane & 16;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const float send = h16 ? v[k] : v[k + 8];
-        const float keep = h16 ? v[k + 8] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    const bool h8 = lane & 8;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float send = h8 ? v[k] : v[k + 4];
-        const float keep = h8 ? v[k + 4] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    const bool h4 = lane & 4;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const float send = h4 ? v[k] : v[k + 2];
-        const float keep = h4 ? v[k + 2] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    const bool h2 = lane & 2;
-    {
-        const float send = h2 ? v[0] : v[1];
-        const float keep = h2 ? v[1] : v[0];
-        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+// Warp sum of 9 per-lane values as a transposition: at each xor stage a
+// lane keeps one half of its (zero-padded) array and adds the partner's copy
+// of the same half, so 5 + 3 + 2 + 1 + 1 = 12 shuffles give every lane the
+// full sum of value index reduced9_index(lane) (valid when < 9; lanes that
+// differ only in bit 0 hold the same value).
+__device__ __forceinline__ float pair_stage(float keep_lo, float keep_hi, bool hi, int mask) {
+    const float send = hi ? keep_lo : keep_hi;
+    const float keep = hi ? keep_hi : keep_lo;
+    return keep + __shfl_xor_sync(0xffffffffu, send, mask);
 }
 
-// Value index owned by `lane` after transpose_reduce16.
-__device__ __forceinline__ int reduced_index(int lane) {
-    return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
+__device__ __forceinline__ float warp_reduce9(const float (&v)[9], int lane) {
+    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
+    float a1[5];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a1[j] = pair_stage(v[2 * j], v[2 * j + 1], b16, 16);
+    a1[4] = pair_stage(v[8], 0.f, b16, 16);
+    float a2[3];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) a2[j] = pair_stage(a1[2 * j], a1[2 * j + 1], b8, 8);
+    a2[2] = pair_stage(a1[4], 0.f, b8, 8);
+    const float a30 = pair_stage(a2[0], a2[1], b4, 4);
+    const float a31 = pair_stage(a2[2], 0.f, b4, 4);
+    const float a4 = pair_stage(a30, a31, b2, 2);
+    return a4 + __shfl_xor_sync(0xffffffffu, a4, 1);
+}
+
+// Value index owned by `lane` after warp_reduce9.
+__device__ __forceinline__ int reduced9_index(int lane) {
+    return ((lane & 2) ? 8 : 0) + ((lane & 4) ? 4 : 0) + ((lane & 8) ? 2 : 0) + ((lane & 16) ? 1 : 0);
 }
 
 // Per-pixel reverse recurrence (renderer.cpp:288-308) for one contributor;
@@ -253,10 +264,10 @@ __device__ __forceinline__ void bwd_step(BwdPix& P, float dx, float dy, const fl
                                          const float4& c, float aclamp, float (&acc)[9]) {
     const float mdx = a.z * dx + a.w * dy, mdy = a.w * dx + b.x * dy;
     const float q = dx * mdx + dy * mdy;
-    const float g = __expf(-0.5f * q);
+    const float g = gauss_weight(q);
     const float og = b.y * g;
     const float alpha = fminf(og, aclamp);
-    const float inv = __frcp_rn(1.f - alpha);  // 1 - alpha >= 0.01
+    const float inv = fast_rcp(1.f - alpha);  // 1 - alpha >= 0.01
     const float Tb = P.T * inv;
     const float at = alpha * Tb;
     acc[5] += P.d0 * at;
@@ -283,7 +294,7 @@ __device__ __forceinline__ void bwd_step(BwdPix& P, float dx, float dy, const fl
 // (T recovered by division, 1 - alpha >= 0.01), same CTA layout as K7 (two
 // pixels per lane, per-warp sub-tile skip). The 9 per-splat gradients of the
 // warp's 64 pixels are summed in registers, transpose-reduced across the warp
-// in 16 shuffles and added with 9 scalar atomics; one or two contributing
+// in 12 shuffles and added with 9 scalar atomics; one or two contributing
 // lanes add directly.
 __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2* __restrict__ ranges,
                                                                   const uint32_t* __restrict__ pval,
@@ -388,10 +399,8 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                     atomicAdd(dst + 8, acc[8]);
                 }
             } else {
-                float vals[16] = {acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8],
-                                  0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                const float r = transpose_reduce16(vals, lane);
-                const int idx = reduced_index(lane);
+                const float r = warp_reduce9(acc, lane);
+                const int idx = reduced9_index(lane);
                 if ((lane & 1) == 0 && idx < 9) atomicAdd(dst + idx, r);
             }
         }

@@ -83,7 +83,8 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                                                             uint32_t* total_out, const uint64_t* __restrict__ keys,
                                                             uint64_t* __restrict__ out_keys,
                                                             uint32_t* __restrict__ out_rows,
-                                                            uint32_t* __restrict__ hist_out, int hist_first) {
+                                                            uint32_t* __restrict__ hist_out, int hist_first,
+                                                            uint32_t* __restrict__ mask_out, uint32_t mask_words) {
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
     __shared__ uint32_t s_hist[MODE == 1 ? 8 * 256 : 1];
@@ -108,6 +109,16 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         }
         v[k] = x;
         sum += x;
+    }
+    if (MODE == 1) {
+        // 1 bit per row: this thread's 8 rows form one byte, 4 lanes one word
+        uint32_t byte = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) byte |= v[k] << k;
+        const uint32_t b1 = __shfl_down_sync(0xffffffffu, byte, 1), b2 = __shfl_down_sync(0xffffffffu, byte, 2),
+                       b3 = __shfl_down_sync(0xffffffffu, byte, 3);
+        const uint64_t word = base / 32;
+        if ((threadIdx.x & 3) == 0 && word < mask_words) mask_out[word] = byte | (b1 << 8) | (b2 << 16) | (b3 << 24);
     }
     const uint32_t tprefix = block_exclusive(sum, s_warp, &s_total);
     if (threadIdx.x < 32) {
@@ -179,7 +190,7 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
-                                                          nullptr, nullptr, nullptr, 0);
+                                                          nullptr, nullptr, nullptr, 0, nullptr, 0);
     BSG_LAUNCHED(c);
 }
 
@@ -194,7 +205,8 @@ void compact_visible(Ctx* c, uint32_t n, int hist_first) {
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
                                                           &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0],
-                                                          &c->counters->depth_hist[0][0], hist_first);
+                                                          &c->counters->depth_hist[0][0], hist_first, c->vis_mask,
+                                                          static_cast<uint32_t>(c->cap / 32));
     BSG_LAUNCHED(c);
 }
 

@@ -58,6 +58,9 @@ def test_run_simulated_matches_oracle(blocks, alpha):
     s, init = desk_scene()
     plan, want, model, rounds = run_both(s, init, blocks, 60, 20, alpha)
     assert len(rounds) == len(want.rounds) == 3
+    trace = [(g["iteration"], g["mean_loss"], w.mean_loss, g["primal"], w.primal_residual, g["rho"][0], w.rho.rho_p)
+             for g, w in zip(rounds, want.rounds)]
+    print("rounds (it, loss gpu/ref, primal gpu/ref, rho_p gpu/ref):", trace)
     for g, w in zip(rounds, want.rounds):
         assert g["iteration"] == w.iteration
         assert g["shared_count"] == w.shared_count and g["global_count"] == w.global_count
