@@ -214,10 +214,10 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
 
 // Dense Adam over every row (trainer.cpp:267-281), element-wise: a thread
 // owns Q quads of 4 consecutive rows of one component (float4 loads/stores of
-// x, m, v), so the kernel is a pure coalesced stream. Launch 1 covers the 10
-// scalar components (blockIdx.y, Q = 2); launch 2 the quaternion group, whose
-// 4 components per row are updated together and then canonicalised
-// (cloud.cpp:82-85, math.hpp:25-34). Visibility comes from the 1-bit-per-row
+// x, m, v), so the kernel is a pure coalesced stream. Launch 1 covers the
+// scalar components (blockIdx.y, Q = 1); launch 2 (adam_rot_kernel) the
+// quaternion group, whose 4 components per row are updated together and then
+// canonicalised (cloud.cpp:82-85, math.hpp:25-34). Visibility comes from the 1-bit-per-row
 // mask built by the compaction, shared-row anchors from a bit mask + per-word
 // prefix (anchor index = rank of the row among the shared rows), so no
 // per-row side array is re-read per component. Rows not visible this step
@@ -231,7 +231,7 @@ __device__ __forceinline__ float adam_update(float x, float g, float& m, float& 
 
 __device__ __forceinline__ int comp_of_group(int y) { return y < 3 ? y : y + 4; }  // pos 0-2, ls/feat/op 7..
 
-template <bool ROT, int Q>
+template <int Q>
 __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
                                                    size_t cap, uint32_t n, const uint32_t* __restrict__ vis_mask,
                                                    const float* __restrict__ gbuf,
@@ -240,14 +240,26 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
                                                    const float* __restrict__ u, size_t ns, AdamStep st,
                                                    double* __restrict__ penalty) {
     __shared__ double s_red[8];
-    constexpr int NC = ROT ? 4 : 1;
-    const int c0 = ROT ? kRot : comp_of_group(blockIdx.y);
+    constexpr int NC = 1;
+    const int c0 = comp_of_group(blockIdx.y);
     double pen = 0.0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const uint32_t r0 = 4 * ((blockIdx.x * blockDim.x + threadIdx.x) * Q + q);
         if (r0 >= n) break;
         const int nr = n - r0 >= 4 ? 4 : static_cast<int>(n - r0);
+        // the streamed x, m, v quads first; everything they do not depend on after
+        float xs[NC][4], ms[NC][4], vs[NC][4];  // [component][row]
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
+            const float4 x4 = *reinterpret_cast<const float4*>(x + off);
+            const float4 m4 = *reinterpret_cast<const float4*>(m + off);
+            const float4 v4 = *reinterpret_cast<const float4*>(v + off);
+            xs[k][0] = x4.x; xs[k][1] = x4.y; xs[k][2] = x4.z; xs[k][3] = x4.w;
+            ms[k][0] = m4.x; ms[k][1] = m4.y; ms[k][2] = m4.z; ms[k][3] = m4.w;
+            vs[k][0] = v4.x; vs[k][1] = v4.y; vs[k][2] = v4.z; vs[k][3] = v4.w;
+        }
         const uint32_t word = r0 >> 5, bit0 = r0 & 31u;
         const uint32_t vis = (vis_mask[word] >> bit0) & 0xfu;
         int aj[4] = {-1, -1, -1, -1};
@@ -262,51 +274,30 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
                 }
             }
         }
-        float xs[NC][4];  // [component][row]
+        // gradient and anchor loads of every row before any arithmetic: one round trip
+        float g[NC][4], zr[NC][4], ur[NC][4];
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
             const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
-            const float4 x4 = *reinterpret_cast<const float4*>(x + off);
-            const float4 m4 = *reinterpret_cast<const float4*>(m + off);
-            const float4 v4 = *reinterpret_cast<const float4*>(v + off);
-            const float xr[4] = {x4.x, x4.y, x4.z, x4.w};
-            float mr[4] = {m4.x, m4.y, m4.z, m4.w}, vr[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                g[k][r] = ((vis >> r) & 1u) ? gbuf[off + r] : 0.f;
+                zr[k][r] = aj[r] >= 0 ? z[static_cast<size_t>(c0 + k) * ns + aj[r]] : 0.f;
+                ur[k][r] = aj[r] >= 0 ? u[static_cast<size_t>(c0 + k) * ns + aj[r]] : 0.f;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
             const float lr = st.lr[c0 + k], rho = st.rho[c0 + k];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                float g = ((vis >> r) & 1u) ? gbuf[off + r] : 0.f;
+                float gr = g[k][r];
                 if (aj[r] >= 0) {
-                    const float d = xr[r] - z[static_cast<size_t>(c0 + k) * ns + aj[r]] +
-                                    u[static_cast<size_t>(c0 + k) * ns + aj[r]];
+                    const float d = xs[k][r] - zr[k][r] + ur[k][r];
                     if (r < nr) pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
-                    g += rho * d;
+                    gr += rho * d;
                 }
-                xs[k][r] = adam_update(xr[r], g, mr[r], vr[r], lr, st);
-            }
-            if (nr == 4) {
-                *reinterpret_cast<float4*>(m + off) = make_float4(mr[0], mr[1], mr[2], mr[3]);
-                *reinterpret_cast<float4*>(v + off) = make_float4(vr[0], vr[1], vr[2], vr[3]);
-            } else {
-                for (int r = 0; r < nr; ++r) {
-                    m[off + r] = mr[r];
-                    v[off + r] = vr[r];
-                }
-            }
-        }
-        if constexpr (ROT) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                float qw = xs[0][r], qx = xs[1][r], qy = xs[2][r], qz = xs[3][r];
-                const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-                if (qn == 0.f) {
-                    qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
-                } else {
-                    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
-                }
-                if (qw < 0.f) {
-                    qw = -qw; qx = -qx; qy = -qy; qz = -qz;
-                }
-                xs[0][r] = qw; xs[1][r] = qx; xs[2][r] = qy; xs[3][r] = qz;
+                xs[k][r] = adam_update(xs[k][r], gr, ms[k][r], vs[k][r], lr, st);
             }
         }
 #pragma unroll
@@ -314,9 +305,91 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
             const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
             if (nr == 4) {
                 *reinterpret_cast<float4*>(x + off) = make_float4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
+                *reinterpret_cast<float4*>(m + off) = make_float4(ms[k][0], ms[k][1], ms[k][2], ms[k][3]);
+                *reinterpret_cast<float4*>(v + off) = make_float4(vs[k][0], vs[k][1], vs[k][2], vs[k][3]);
             } else {
-                for (int r = 0; r < nr; ++r) x[off + r] = xs[k][r];
+                for (int r = 0; r < nr; ++r) {
+                    x[off + r] = xs[k][r];
+                    m[off + r] = ms[k][r];
+                    v[off + r] = vs[k][r];
+                }
             }
+        }
+    }
+    if (st.has_anchor) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pen += __shfl_xor_sync(0xffffffffu, pen, o);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pen;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0;
+            for (int w = 0; w < 8; ++w) t += s_red[w];
+            if (t != 0.0) atomicAdd(penalty, t);
+        }
+    }
+}
+
+// Quaternion group, one row per thread: the 4 components are read as 4
+// coalesced scalar streams (x, m, v each), updated, canonicalised and written
+// back. One row per thread keeps the register count low enough for the
+// occupancy a 12-stream kernel needs.
+__global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, float* __restrict__ m,
+                                                       float* __restrict__ v, size_t cap, uint32_t n,
+                                                       const uint32_t* __restrict__ vis_mask,
+                                                       const float* __restrict__ gbuf,
+                                                       const uint32_t* __restrict__ sh_mask,
+                                                       const uint32_t* __restrict__ sh_prefix,
+                                                       const float* __restrict__ z, const float* __restrict__ u,
+                                                       size_t ns, AdamStep st, double* __restrict__ penalty) {
+    __shared__ double s_red[8];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    double pen = 0.0;
+    if (i < n) {
+        float xs[4], ms[4], vs[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const size_t off = static_cast<size_t>(kRot + k) * cap + i;
+            xs[k] = x[off];
+            ms[k] = m[off];
+            vs[k] = v[off];
+        }
+        const uint32_t word = i >> 5, bit = i & 31u;
+        const bool visible = (vis_mask[word] >> bit) & 1u;
+        int aj = -1;
+        if (st.has_anchor) {
+            const uint32_t sm = sh_mask[word];
+            if ((sm >> bit) & 1u) aj = static_cast<int>(sh_prefix[word] + __popc(sm & ((1u << bit) - 1u)));
+        }
+        float g[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g[k] = visible ? gbuf[static_cast<size_t>(kRot + k) * cap + i] : 0.f;
+        if (aj >= 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float rho = st.rho[kRot + k];
+                const float d = xs[k] - z[static_cast<size_t>(kRot + k) * ns + aj] + u[static_cast<size_t>(kRot + k) * ns + aj];
+                pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
+                g[k] += rho * d;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xs[k] = adam_update(xs[k], g[k], ms[k], vs[k], st.lr[kRot + k], st);
+        // canonicalise (cloud.cpp:82-85): one reciprocal per row, sign flip folded into the scale
+        float qw = xs[0], qx = xs[1], qy = xs[2], qz = xs[3];
+        const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+        if (qn == 0.f) {
+            qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
+        } else {
+            const float inv = (qw < 0.f ? -1.f : 1.f) / qn;
+            qw *= inv; qx *= inv; qy *= inv; qz *= inv;
+        }
+        xs[0] = qw; xs[1] = qx; xs[2] = qy; xs[3] = qz;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const size_t off = static_cast<size_t>(kRot + k) * cap + i;
+            x[off] = xs[k];
+            m[off] = ms[k];
+            v[off] = vs[k];
         }
     }
     if (st.has_anchor) {
@@ -364,13 +437,13 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     if (c->n == 0) return;
     const uint32_t n = static_cast<uint32_t>(c->n);
     const int scalar_groups = c->D - 4;  // every component but the quaternion
-    const dim3 g1(static_cast<uint32_t>((c->n + 2047) / 2048), static_cast<uint32_t>(scalar_groups));
-    adam_kernel<false, 2><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
+    const dim3 g1(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(scalar_groups));
+    adam_kernel<1><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
                                                      c->sh_prefix, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);
-    const dim3 g2(static_cast<uint32_t>((c->n + 1023) / 1024), 1);
-    adam_kernel<true, 1><<<g2, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
-                                                    c->sh_prefix, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
+    adam_rot_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
+        c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, st,
+        &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }
 

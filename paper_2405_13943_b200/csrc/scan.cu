@@ -140,23 +140,37 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
     __syncthreads();
     if (threadIdx.x == 0 && (static_cast<uint64_t>(tile) + 1) * kScanTile >= n && total_out) *total_out = s_prefix + s_total;
     uint32_t run = s_prefix + tprefix;
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = base + k;
-        if (i < n) {
-            if (MODE == 1) {
-                if (v[k]) {
-                    const uint64_t key = keys[i];
-                    out_keys[run] = key;
-                    out_rows[run] = static_cast<uint32_t>(i);
-                    out[run] = static_cast<uint32_t>(i);
-#pragma unroll
-                    for (int p = 0; p < 8; ++p)
-                        if (p >= hist_first) atomicAdd(&s_hist[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
-                }
-            } else {
-                out[i] = run;
+        if (MODE == 1) {
+            const bool vis = v[k] != 0;  // v[k] = 0 past n
+            uint64_t key = 0;
+            if (vis) {
+                key = keys[i];
+                out_keys[run] = key;
+                out_rows[run] = static_cast<uint32_t>(i);
+                out[run] = static_cast<uint32_t>(i);
             }
+            // digit histograms: the upper depth bytes are nearly constant, so
+            // lanes whose digit equals the first active lane's are counted
+            // with one atomic (ballot), the rest add individually
+            const unsigned act = __ballot_sync(0xffffffffu, vis);
+            if (act) {
+                const int src = __ffs(act) - 1;
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    if (p < hist_first) continue;
+                    const uint32_t d = static_cast<uint32_t>((key >> (8 * p)) & 0xffu);
+                    const uint32_t d0 = __shfl_sync(0xffffffffu, d, src);
+                    const unsigned same = __ballot_sync(0xffffffffu, vis && d == d0);
+                    if (lane == src) atomicAdd(&s_hist[p * 256 + d0], __popc(same));
+                    else if (vis && d != d0) atomicAdd(&s_hist[p * 256 + d], 1u);
+                }
+            }
+        } else if (i < n) {
+            out[i] = run;
         }
         run += v[k];
     }
