@@ -212,7 +212,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     launch_preprocess(c, cam, rc);
     stage_end(c, kStPreprocess);
     stage_begin(c, kStCompact);
-    compact_visible(c, static_cast<uint32_t>(c->n), 4);  // + digit histograms of the upper depth bytes
+    compact_visible(c, static_cast<uint32_t>(c->n), true);  // + digit histograms of the 32-bit depth keys
     stage_end(c, kStCompact);
     // One readback: V and the depth-key histograms (pass skipping).
     BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist), cudaMemcpyDeviceToHost,
@@ -220,22 +220,23 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     const uint32_t V = c->counters_host->visible;
     stage_begin(c, kStDepthSort);
-    // (depth, index) order (renderer.cpp:86-89): stable LSD sort of the upper
-    // 32 bits of the FP64 depth (positive doubles order as u64) over rows in
-    // ascending index order, then runs of equal upper bits sorted by the lower
-    // 32 bits. A run longer than 64 falls back to all 8 digit passes.
-    radix_sort_u64(c, c->vkey, c->vrow, V, 4, 8, &c->counters->depth_hist[0][0], &c->counters_host->depth_hist[0][0],
-                   &c->depth_sorted);
-    depth_tie_fixup(c, c->vkey[c->depth_sorted], c->vrow[c->depth_sorted], V, &c->counters->overflow);
+    // (depth, index) order (renderer.cpp:86-89): stable LSD sort of the 32-bit
+    // range-normalised depth key over rows in ascending index order, then runs
+    // of equal keys sorted by the full FP64 depth. A run longer than 64 that is
+    // out of order falls back to all 8 digit passes of the FP64 bits.
+    uint32_t* k32[2] = {reinterpret_cast<uint32_t*>(c->vkey[0]), reinterpret_cast<uint32_t*>(c->vkey[1])};
+    radix_sort_u32(c, k32, c->vrow, V, 0, depth_key_bits(V) / 8, &c->counters->depth_hist[0][0],
+                   &c->counters_host->depth_hist[0][0], &c->depth_sorted);
+    depth_tie_fixup(c, k32[c->depth_sorted], c->vrow[c->depth_sorted], c->depth_key, V, &c->counters->overflow);
     stage_end(c, kStDepthSort);
     stage_begin(c, kStPairs);
     scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
     BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, 16, cudaMemcpyDeviceToHost, c->stream));
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     if (c->counters_host->overflow) {
-        // rare: a long run of equal upper depth bits -> full 64-bit sort
+        // rare: a long out-of-order run of equal 32-bit keys -> full 64-bit sort
         BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
-        compact_visible(c, static_cast<uint32_t>(c->n), 0);
+        compact_visible(c, static_cast<uint32_t>(c->n), false);
         BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist),
                                  cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));

@@ -45,8 +45,10 @@ struct DevRender {
 struct StepCounters {
     uint32_t visible;   // V
     uint32_t pairs;     // P
-    uint32_t overflow;  // pairs exceeded capacity
-    uint32_t pad;
+    uint32_t overflow;  // a run of equal 32-bit depth keys too long for the fix-up
+    uint32_t visible_pre;  // visible count as seen by the preprocess (sizes the depth key)
+    unsigned long long zmin_inv;  // ~bits of the smallest visible FP64 depth (atomicMax of the complement)
+    unsigned long long zmax;      // bits of the largest visible FP64 depth
     uint32_t depth_hist[8][256];  // digit histograms of the visible depth keys (filled by the compaction)
     uint32_t tile_hist[2][256];   // digit histograms of the tile keys (filled by the pair emission)
 };
@@ -186,14 +188,26 @@ struct Error {
             throw ::bsg::Error{BSG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)}; \
     } while (0)
 
+// Width of the range-normalised depth key for V visible splats: ~6 bits more
+// than log2(V), so equal keys (distinct depths in one bucket) stay rare,
+// rounded up to whole 8-bit radix digits.
+__host__ __device__ inline int depth_key_bits(uint32_t V) {
+    int lg = 0;
+    while (lg < 32 && (1ull << lg) < V) ++lg;
+    const int b = ((lg + 6 + 7) / 8) * 8;
+    return b < 16 ? 16 : (b > 32 ? 32 : b);
+}
+
 // ---- building blocks (scan.cu, radix.cu) -------------------------------
 // Exclusive scan of n u32 values read through a gather (in[idx ? idx[i] : i]),
 // optional predicate compaction. Result in out; total in *total_dev.
 void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,
                         uint32_t* total_dev);
 // Stable compaction of rows with tiles[i] > 0: writes keys/rows in row order and V.
-// hist_first: lowest depth-key byte whose digit histogram is built.
-void compact_visible(Ctx* c, uint32_t n, int hist_first);
+// key32: the 32-bit range-normalised depth key (bits(z) - bits(zmin)) >> shift
+// into vkey (as u32) with its 4 digit histograms; otherwise the full FP64 bits
+// with all 8 digit histograms.
+void compact_visible(Ctx* c, uint32_t n, bool key32);
 // Stable LSD radix sort (onesweep) of (u64 key, u32 val) / (u32 key, u32 val)
 // over `passes` 8-bit digits from bit 0. d_hist holds the per-pass digit
 // counts (produced by the kernel that wrote the keys) and is turned into
@@ -203,9 +217,10 @@ void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, in
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel);
 void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel);
-// Sorts runs of equal upper-32-bit depth keys by their lower 32 bits (stable);
-// sets *long_run if a run exceeds 64 (caller redoes the full sort).
-void depth_tie_fixup(Ctx* c, uint64_t* keys, uint32_t* rows, uint32_t V, uint32_t* long_run);
+// Sorts runs of equal 32-bit depth keys by the full FP64 depth bits of their
+// rows (stable); sets *long_run if a run exceeds 64 (caller redoes the full sort).
+void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,
+                     uint32_t* long_run);
 
 // ---- rasterizer stages (preprocess.cu, raster.cu, ssim.cu, adam.cu) ----
 DevCam make_cam(const bsg_camera& c);

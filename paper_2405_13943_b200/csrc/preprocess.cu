@@ -41,10 +41,18 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  float4* __restrict__ rec,
                                                                  uint64_t* __restrict__ depth_key,
                                                                  uint32_t* __restrict__ tiles,
-                                                                 float4* __restrict__ g2d) {
+                                                                 float4* __restrict__ g2d,
+                                                                 StepCounters* __restrict__ counters) {
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint32_t s_count;
-    if (threadIdx.x == 0) s_count = 0;
+    __shared__ unsigned long long s_zmin_inv, s_zmax;
+    __shared__ uint32_t s_visible;
+    if (threadIdx.x == 0) {
+        s_count = 0;
+        s_visible = 0;
+        s_zmin_inv = 0;
+        s_zmax = 0;
+    }
     __syncthreads();
     const uint32_t chunk0 = blockIdx.x * kPreChunk;
     const float fxf = static_cast<float>(cam.fx), fyf = static_cast<float>(cam.fy);
@@ -98,6 +106,8 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
     }
     __syncthreads();
     const uint32_t count = s_count;
+    unsigned long long zmin_inv = 0, zmax = 0;  // depth range of this thread's visible splats
+    uint32_t nvis = 0;
     for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
         const uint32_t i = s_rows[q];
         // every parameter of the row up front: one dependent DRAM round trip
@@ -198,7 +208,11 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                 rec[3 * static_cast<size_t>(i) + 2] =
                     make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23), 0.f);
                 ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
-                depth_key[i] = static_cast<uint64_t>(__double_as_longlong(z));
+                const unsigned long long zb = static_cast<unsigned long long>(__double_as_longlong(z));
+                depth_key[i] = zb;
+                zmin_inv = max(zmin_inv, ~zb);
+                zmax = max(zmax, zb);
+                ++nvis;
                 const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
                 g2d[3 * static_cast<size_t>(i) + 0] = zero;
                 g2d[3 * static_cast<size_t>(i) + 1] = zero;
@@ -206,6 +220,25 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
             }
         }
         tiles[i] = ntiles;
+    }
+    // visible depth range (keys the 32-bit depth sort); one atomic pair per CTA
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        zmin_inv = max(zmin_inv, __shfl_xor_sync(0xffffffffu, zmin_inv, o));
+        zmax = max(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nvis += __shfl_xor_sync(0xffffffffu, nvis, o);
+    if ((threadIdx.x & 31) == 0 && zmax) {
+        atomicMax(&s_zmin_inv, zmin_inv);
+        atomicMax(&s_zmax, zmax);
+        atomicAdd(&s_visible, nvis);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_zmax) {
+        atomicMax(&counters->zmin_inv, s_zmin_inv);
+        atomicMax(&counters->zmax, s_zmax);
+        atomicAdd(&counters->visible_pre, s_visible);
     }
 }
 
@@ -241,7 +274,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     if (c->n == 0) return;
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     preprocess_kernel<<<blocks, kPreThreads, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
-                                                      c->depth_key, c->tiles, c->g2d);
+                                                      c->depth_key, c->tiles, c->g2d, c->counters);
     BSG_LAUNCHED(c);
 }
 

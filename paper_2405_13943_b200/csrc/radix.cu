@@ -201,34 +201,59 @@ void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pas
         launch_passes<K, 16>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
 }
 
-// After a stable sort on the upper 32 bits of the FP64 depth, splats whose
-// depths share those bits (|dz|/z < 2^-20) are still in row order; sort each
-// such run by the low 32 bits, stably, so the result is the full (depth,
-// index) order of renderer.cpp:86-89. Runs longer than 64 are flagged and the
-// caller falls back to the full 64-bit sort.
-__global__ void depth_tie_fixup_kernel(uint64_t* __restrict__ keys, uint32_t* __restrict__ rows, uint32_t V,
+// After a stable sort on the 32-bit range-normalised depth key (bits(z) -
+// bits(zmin)) >> shift, splats whose depths fall in one key bucket (within
+// 2^shift ulps) are still in row order; sort each such run by the full FP64
+// depth bits, stably, so the result is the (depth, index) order of
+// renderer.cpp:86-89. Runs longer than 64 (many equal keys that are not all
+// equal depths) are flagged and the caller falls back to the full 64-bit sort.
+__global__ void depth_tie_fixup_kernel(uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
+                                       const uint64_t* __restrict__ depth_bits, uint32_t V,
                                        uint32_t* __restrict__ long_run) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= V) return;
-    const uint32_t hi = static_cast<uint32_t>(keys[i] >> 32);
-    if (i > 0 && static_cast<uint32_t>(keys[i - 1] >> 32) == hi) return;  // not a run start
-    if (i + 1 >= V || static_cast<uint32_t>(keys[i + 1] >> 32) != hi) return;  // singleton
+    const uint32_t k = keys[i];
+    if (i > 0 && keys[i - 1] == k) return;       // not a run start
+    if (i + 1 >= V || keys[i + 1] != k) return;  // singleton
     uint32_t e = i + 2;
-    while (e < V && static_cast<uint32_t>(keys[e] >> 32) == hi && e - i <= 64) ++e;
+    while (e < V && keys[e] == k && e - i <= 64) ++e;
+    // insertion sort by full depth; already-ordered runs (equal depths, index
+    // order) cost one comparison per element, whatever their length
+    uint64_t prev = depth_bits[rows[i]];
+    bool sorted = true;
+    for (uint32_t a = i + 1; a < e; ++a) {
+        const uint64_t d = depth_bits[rows[a]];
+        if (d < prev) sorted = false;
+        prev = d;
+    }
+    if (sorted) {
+        // a long run of equal keys that is already in order needs no fall-back
+        if (e - i > 64) {
+            uint32_t f = e;
+            while (f < V && keys[f] == k) {
+                const uint64_t d = depth_bits[rows[f]];
+                if (d < prev) {
+                    atomicOr(long_run, 1u);
+                    return;
+                }
+                prev = d;
+                ++f;
+            }
+        }
+        return;
+    }
     if (e - i > 64) {
         atomicOr(long_run, 1u);
         return;
     }
     for (uint32_t a = i + 1; a < e; ++a) {
-        const uint64_t k = keys[a];
         const uint32_t r = rows[a];
+        const uint64_t d = depth_bits[r];
         uint32_t b = a;
-        while (b > i && keys[b - 1] > k) {
-            keys[b] = keys[b - 1];
+        while (b > i && depth_bits[rows[b - 1]] > d) {
             rows[b] = rows[b - 1];
             --b;
         }
-        keys[b] = k;
         rows[b] = r;
     }
 }
@@ -245,9 +270,10 @@ void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, in
     radix_sort<uint32_t>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
 }
 
-void depth_tie_fixup(Ctx* c, uint64_t* keys, uint32_t* rows, uint32_t V, uint32_t* long_run) {
+void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,
+                     uint32_t* long_run) {
     if (V < 2) return;
-    depth_tie_fixup_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(keys, rows, V, long_run);
+    depth_tie_fixup_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(keys, rows, depth_bits, V, long_run);
     BSG_LAUNCHED(c);
 }
 

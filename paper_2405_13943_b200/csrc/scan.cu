@@ -74,23 +74,37 @@ __device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32
 }
 
 // MODE 0: plain exclusive scan of in[gather ? gather[i] : i].
-// MODE 1: compaction of rows with tiles[i] > 0 (in = tiles), emits keys/rows.
+// MODE 1: compaction of rows with tiles[i] > 0 (in = tiles), emits the FP64
+//         depth bits as u64 keys + rows, 8 digit histograms.
+// MODE 2: as 1 with the 32-bit range-normalised key (bits - zmin) >> shift,
+//         4 digit histograms (the key has depth_key_bits(V) <= 32 bits).
 template <int MODE>
 __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __restrict__ in,
                                                             const uint32_t* __restrict__ gather,
                                                             uint32_t* __restrict__ out, uint32_t n,
                                                             unsigned long long* status, uint32_t* ticket,
                                                             uint32_t* total_out, const uint64_t* __restrict__ keys,
-                                                            uint64_t* __restrict__ out_keys,
+                                                            void* __restrict__ out_keys_v,
+                                                            const StepCounters* __restrict__ range,
                                                             uint32_t* __restrict__ out_rows,
                                                             uint32_t* __restrict__ hist_out, int hist_first,
                                                             uint32_t* __restrict__ mask_out, uint32_t mask_words) {
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
-    __shared__ uint32_t s_hist[MODE == 1 ? 8 * 256 : 1];
+    constexpr int kDigits = MODE == 2 ? 4 : 8;
+    __shared__ uint32_t s_hist[MODE != 0 ? kDigits * 256 : 1];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    if (MODE == 1)
-        for (int k = threadIdx.x; k < 8 * 256; k += kScanThreads) s_hist[k] = 0;
+    if (MODE != 0)
+        for (int k = threadIdx.x; k < kDigits * 256; k += kScanThreads) s_hist[k] = 0;
+    unsigned long long zmin = 0;
+    int shift = 0;
+    if (MODE == 2) {
+        zmin = ~range->zmin_inv;
+        const unsigned long long span = range->zmax - zmin;  // 0 when nothing (or one depth) is visible
+        const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+        const int kb = depth_key_bits(range->visible_pre);
+        shift = bits > kb ? bits - kb : 0;
+    }
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint64_t base = static_cast<uint64_t>(tile) * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
@@ -101,7 +115,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         const uint64_t i = base + k;
         uint32_t x = 0;
         if (i < n) {
-            if (MODE == 1) {
+            if (MODE != 0) {
                 x = in[i] > 0 ? 1u : 0u;
             } else {
                 x = in[gather ? gather[i] : i];
@@ -110,7 +124,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         v[k] = x;
         sum += x;
     }
-    if (MODE == 1) {
+    if (MODE != 0) {
         // 1 bit per row: this thread's 8 rows form one byte, 4 lanes one word
         uint32_t byte = 0;
 #pragma unroll
@@ -144,23 +158,29 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = base + k;
-        if (MODE == 1) {
+        if (MODE != 0) {
             const bool vis = v[k] != 0;  // v[k] = 0 past n
             uint64_t key = 0;
             if (vis) {
-                key = keys[i];
-                out_keys[run] = key;
+                const uint64_t zb = keys[i];
+                if (MODE == 2) {
+                    key = (zb - zmin) >> shift;
+                    static_cast<uint32_t*>(out_keys_v)[run] = static_cast<uint32_t>(key);
+                } else {
+                    key = zb;
+                    static_cast<uint64_t*>(out_keys_v)[run] = key;
+                }
                 out_rows[run] = static_cast<uint32_t>(i);
                 out[run] = static_cast<uint32_t>(i);
             }
-            // digit histograms: the upper depth bytes are nearly constant, so
-            // lanes whose digit equals the first active lane's are counted
-            // with one atomic (ballot), the rest add individually
+            // digit histograms: the upper digits are nearly constant, so lanes
+            // whose digit equals the first active lane's are counted with one
+            // atomic (ballot), the rest add individually
             const unsigned act = __ballot_sync(0xffffffffu, vis);
             if (act) {
                 const int src = __ffs(act) - 1;
 #pragma unroll
-                for (int p = 0; p < 8; ++p) {
+                for (int p = 0; p < kDigits; ++p) {
                     if (p < hist_first) continue;
                     const uint32_t d = static_cast<uint32_t>((key >> (8 * p)) & 0xffu);
                     const uint32_t d0 = __shfl_sync(0xffffffffu, d, src);
@@ -174,9 +194,9 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         }
         run += v[k];
     }
-    if (MODE == 1) {
+    if (MODE != 0) {
         __syncthreads();
-        for (int k = threadIdx.x; k < 8 * 256; k += kScanThreads)
+        for (int k = threadIdx.x; k < kDigits * 256; k += kScanThreads)
             if (s_hist[k]) atomicAdd(&hist_out[k], s_hist[k]);
     }
 }
@@ -204,11 +224,11 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
-                                                          nullptr, nullptr, nullptr, 0, nullptr, 0);
+                                                          nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0);
     BSG_LAUNCHED(c);
 }
 
-void compact_visible(Ctx* c, uint32_t n, int hist_first) {
+void compact_visible(Ctx* c, uint32_t n, bool key32) {
     if (n == 0) {
         BSG_CUDA(cudaMemsetAsync(&c->counters->visible, 0, sizeof(uint32_t), c->stream));
         return;
@@ -217,10 +237,16 @@ void compact_visible(Ctx* c, uint32_t n, int hist_first) {
     prepare_status(c, tiles);
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
-    scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
-                                                          &c->counters->visible, c->depth_key, c->vkey[0], c->vrow[0],
-                                                          &c->counters->depth_hist[0][0], hist_first, c->vis_mask,
-                                                          static_cast<uint32_t>(c->cap / 32));
+    if (key32)
+        scan_kernel<2><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
+                                                              &c->counters->visible, c->depth_key, c->vkey[0],
+                                                              c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
+                                                              c->vis_mask, static_cast<uint32_t>(c->cap / 32));
+    else
+        scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
+                                                              &c->counters->visible, c->depth_key, c->vkey[0],
+                                                              c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
+                                                              c->vis_mask, static_cast<uint32_t>(c->cap / 32));
     BSG_LAUNCHED(c);
 }
 

@@ -238,3 +238,36 @@ def test_equal_depth_runs_keep_index_order():
         got = new_block(c).project(dev_cam(cam))
         want = orc.project(c.oracle(), cam, orc.RenderConfig())
         assert np.array_equal(got["order"], want["order"])
+
+
+def plane_cluster_cloud(n, half_width, depth_spread, seed):
+    """n splats on a plane facing the tilted reference camera, at depth 5 +-
+    depth_spread (then rounded to f32 world positions), plus one far splat at
+    depth ~5000 that stretches the depth span, so the 32-bit range-normalised
+    depth key (~2^23 double ulps per bucket) merges many distinct FP64 depths."""
+    cam = ref_camera(256)
+    Rm = np.array(cam.R).reshape(3, 3)
+    g = np.random.default_rng(seed)
+    t = np.array(cam.t)
+    pc = np.stack([g.uniform(-half_width, half_width, n), g.uniform(-half_width, half_width, n),
+                   5.0 + g.uniform(-depth_spread, depth_spread, n)], 1)
+    pc = np.vstack([pc, [[0.0, 0.0, 5000.0]]])
+    pw = (pc - t) @ Rm
+    rows = []
+    for i, p in enumerate(pw):
+        splat_at(rows, i, p, (0.5, 0.4, 0.3), 0.5, -4.0 if i < n else 1.0)
+    return cloud_from_rows(rows).narrowed(), cam
+
+
+@pytest.mark.parametrize("n,spread", [(20000, 2e-2), (6000, 1e-7)], ids=["short-runs", "long-runs"])
+def test_depth_key_collisions_match_reference_order(n, spread):
+    """Depth buckets holding several distinct FP64 depths: runs <= 64 go
+    through the tie fix-up, longer out-of-order runs through the full 64-bit
+    fall-back; both must reproduce renderer.cpp:86-89 bit-exactly."""
+    cloud, cam = plane_cluster_cloud(n, 1.5, spread, 3)
+    got = new_block(cloud).project(dev_cam(cam))
+    want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
+    vis = want["visible"].astype(bool)
+    assert vis.sum() > 0.9 * n
+    assert np.array_equal(got["visible"], want["visible"])
+    assert np.array_equal(got["order"], want["order"])
