@@ -90,6 +90,8 @@ void free_all(Ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->nccl) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl));
+    if (c->gt_ready) cudaEventDestroy(c->gt_ready);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -311,7 +313,9 @@ AdamStep make_adam_step(Ctx* c) {
 }
 
 // One train_step (trainer.cpp:249-295) on a device-resident ground truth.
-void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev) {
+// gt_ready (nullable): event the loss waits on (ground truth still in flight
+// on the copy stream while projection, sorting and the forward blend run).
+void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev, cudaEvent_t gt_ready = nullptr) {
     c->step_launches = 0;
     const DevCam cam = make_cam(view);
     const DevRender rc = make_render(c->tcfg.render);
@@ -321,6 +325,7 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     launch_blend_fwd(c, cam, rc);
     stage_end(c, kStBlendFwd);
     stage_begin(c, kStLoss);
+    if (gt_ready) BSG_CUDA(cudaStreamWaitEvent(c->stream, gt_ready, 0));
     launch_loss(c, cam, rc, gt);
     stage_end(c, kStLoss);
     stage_begin(c, kStBlendBwd);
@@ -473,6 +478,8 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
         try {
             use_device(c);
             BSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            BSG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+            BSG_CUDA(cudaEventCreateWithFlags(&c->gt_ready, cudaEventDisableTiming));
             BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
             dev_alloc(&c->counters, 1);
             dev_alloc(&c->scalars, 1);
@@ -791,8 +798,11 @@ int bsg_train_step_host(bsg_ctx* h, const bsg_camera* cam, const float* gt_host,
         ensure_image_buffers(c, static_cast<int>(cam->width), static_cast<int>(cam->height));
         ensure_views_buffers(c, 1);
         const size_t px = static_cast<size_t>(cam->width) * cam->height;
-        BSG_CUDA(cudaMemcpyAsync(c->gt_stage, gt_host, 3 * px * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-        train_one(c, *cam, c->gt_stage, c->losses_dev);
+        // the ground-truth upload overlaps the step's projection/sort/forward blend
+        BSG_CUDA(cudaMemcpyAsync(c->gt_stage, gt_host, 3 * px * sizeof(float), cudaMemcpyHostToDevice,
+                                 c->copy_stream));
+        BSG_CUDA(cudaEventRecord(c->gt_ready, c->copy_stream));
+        train_one(c, *cam, c->gt_stage, c->losses_dev, c->gt_ready);
         double l3[3];
         BSG_CUDA(cudaMemcpyAsync(l3, c->losses_dev, sizeof(l3), cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));

@@ -69,6 +69,8 @@ enum Stage {
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host ground-truth uploads (e2e path)
+    cudaEvent_t gt_ready = nullptr;
     int fd = 3, D = 14;
     size_t n = 0, cap = 0;
     std::vector<uint64_t> ids;

@@ -24,7 +24,17 @@ constexpr int kPX = kTX + 2 * kHalf;              // 74 patch columns
 constexpr int kPY = kTY + 2 * kHalf;              // 26 patch rows
 constexpr int kPS = 76;                           // padded row stride (16 B aligned)
 constexpr int kThreads = 256;
-__constant__ float c_win[kW];
+// ssim_window_1d (ssim.cpp:112-122): exp(-d^2 / (2 1.5^2)) normalised in FP64,
+// rounded to FP32. Compile-time immediates so every tap is an FFMA with an
+// immediate operand (half the FMA-pipe occupancy of a register/constant
+// operand); launch_loss re-derives them on the host and refuses to run on a
+// mismatch.
+__device__ constexpr float kWin[kW] = {0x1.0d956cp-10f, 0x1.f1fe02p-8f, 0x1.26eb18p-5f, 0x1.bff0fep-4f,
+                                       0x1.b43c40p-3f,  0x1.106560p-2f, 0x1.b43c40p-3f, 0x1.bff0fep-4f,
+                                       0x1.26eb18p-5f,  0x1.f1fe02p-8f, 0x1.0d956cp-10f};
+constexpr float kWinHost[kW] = {0x1.0d956cp-10f, 0x1.f1fe02p-8f, 0x1.26eb18p-5f, 0x1.bff0fep-4f,
+                                0x1.b43c40p-3f,  0x1.106560p-2f, 0x1.b43c40p-3f, 0x1.bff0fep-4f,
+                                0x1.26eb18p-5f,  0x1.f1fe02p-8f, 0x1.0d956cp-10f};
 
 __device__ __forceinline__ double block_sum_d(double v, double* s_red) {
 #pragma unroll
@@ -54,7 +64,7 @@ __device__ __forceinline__ void corr4(const float (&v)[16], float (&o)[4]) {
     for (int j = 0; j < 4; ++j) {
         float s = 0.f;
 #pragma unroll
-        for (int t = 0; t < kW; ++t) s += c_win[t] * v[j + t];
+        for (int t = 0; t < kW; ++t) s += kWin[t] * v[j + t];
         o[j] = s;
     }
 }
@@ -242,16 +252,17 @@ bool g_ready[64] = {};
 
 void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt) {
     if (!g_ready[c->device]) {
-        // ssim_window_1d (ssim.cpp:112-122), computed in FP64 then rounded.
-        float w[kW];
+        // ssim_window_1d (ssim.cpp:112-122), computed in FP64 then rounded: must
+        // equal the compiled-in taps.
         double k[kW], sum = 0;
         for (int i = 0; i < kW; ++i) {
             const double d = i - kHalf;
             k[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
             sum += k[i];
         }
-        for (int i = 0; i < kW; ++i) w[i] = static_cast<float>(k[i] / sum);
-        BSG_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof(w)));
+        for (int i = 0; i < kW; ++i)
+            if (static_cast<float>(k[i] / sum) != kWinHost[i])
+                throw Error{BSG_ERR_CUDA, "SSIM window taps differ from ssim_window_1d"};
         BSG_CUDA(cudaFuncSetAttribute(ssim_windows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sizeof(WinSmem))));
         BSG_CUDA(cudaFuncSetAttribute(ssim_pixels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
