@@ -157,6 +157,10 @@ def build_block(rank, world, n, device, n_views=CFG["views"], constant_gt=False)
                                      block_shared=len(rows))
 
 
+STAGE_KERNEL = {"blend_bwd": "blend_bwd_kernel", "blend_fwd": "blend_fwd_kernel", "adam": "adam_kernel",
+                "preprocess": "preprocess_kernel", "fold": "fold_visible_kernel", "loss_ssim": "ssim_windows_kernel"}
+
+
 def algorithmic_bytes(stage, n, V, P, HW, shared):
     """SURVEY §8(d) fused-minimum byte accounting per launch of each stage
     (n rows, V visible splats, P tile pairs, HW pixels, D = 14 FP32 components
@@ -330,6 +334,18 @@ def run_ours(args, rank, world, local_rank):
     stage_roofs = {k: roof(k) for k in stage_ms if roof(k) is not None}
     roof_stage = max(stage_roofs, key=lambda k: stage_ms[k])
     roofline = stage_roofs[roof_stage]
+    # the blend kernels are instruction-issue bound, not HBM bound: attach the
+    # ncu issue / pipe utilisation of the dominant stage's kernel (profiles/)
+    kmet_path = os.path.join(ROOT, "profiles", "kernel_metrics.json")
+    if os.path.exists(kmet_path):
+        try:
+            km = json.load(open(kmet_path)).get(STAGE_KERNEL.get(roof_stage, ""), None)
+        except Exception:
+            km = None
+        if km:
+            roofline["compute"] = {"bound": "sm_issue", "issue_slots_busy_pct": round(km["issue_pct"], 1),
+                                   "fma_pipe_pct": round(km["fma_pct"], 1), "alu_pipe_pct": round(km["alu_pct"], 1),
+                                   "xu_pipe_pct": round(km["xu_pct"], 1), "source": km["capture"]}
     out = {
         "metric": "training iters/sec (K=N blocks, 1 block per GPU)",
         "value": 1000.0 / ms_step,

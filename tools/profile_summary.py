@@ -115,6 +115,8 @@ def main():
     tp = os.path.join(prof, "dram_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp))
+    kp = os.path.join(prof, "kernel_metrics.json")
+    kmet = json.load(open(kp)) if os.path.exists(kp) else {}
     lines = [f"# ncu --set full captures `{tag}` (one launch each, inside `bench.py --profile`)", "",
              "| kernel | " + " | ".join(k for k, _, _ in METRICS) + " | top stalls (warps per issue) |",
              "|---" * (len(METRICS) + 2) + "|"]
@@ -132,8 +134,11 @@ def main():
         rd, wr = num(m.get("dram__bytes_read.sum", "")), num(m.get("dram__bytes_write.sum", ""))
         if st and rd is not None and wr is not None:
             traffic.setdefault(st, {})[base(name)] = rd + wr
+        kmet[base(name)] = {k: (num(m.get(key, "")) or 0.0) * sc for k, key, sc in METRICS}
+        kmet[base(name)]["capture"] = f"profiles/ncu_{tag}.md"
     open(os.path.join(prof, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(tp, "w"), indent=1, sort_keys=True)
+    json.dump(kmet, open(kp, "w"), indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
