@@ -185,6 +185,29 @@ int bsg_nccl_unique_id(uint8_t out_id[128]);
 int bsg_comm_init(bsg_ctx* ctx, const uint8_t id[128], int nranks, int rank);
 int bsg_consensus_round(bsg_ctx* ctx, const bsg_round_args* args, bsg_round_result* out);
 
+/* Penalty adaptation (adapt_penalties, admm.cpp:200-217) applied on the device
+ * at the end of an asynchronous round: `iteration` is the round's iteration t. */
+typedef struct bsg_adapt_args {
+    double mu, tau_inc, tau_dec;   /* ConsensusConfig (admm.hpp:20-29) */
+    uint64_t freeze_iteration;
+    int adaptive;
+    uint64_t iteration;
+} bsg_adapt_args;
+
+/* Asynchronous round (the overlap of SURVEY §8(e)): enqueued on the block's
+ * communication stream behind the last parameter update, returns at once.
+ * The next bsg_train_steps runs projection, sorting, both blends and the fold
+ * while the round's reductions are in flight; only its penalty + Adam waits
+ * for the round, and reads the (possibly adapted) rho from device memory, so
+ * the exact iteration order of Alg. 2 is kept with no host round trip.
+ * adapt (nullable): adapt rho on the device from the reduced residuals (every
+ * rank decides on identical reduced values). Collective: all ranks call it in
+ * the same order. bsg_consensus_wait blocks for the pending round and returns
+ * its result and the rho now in force (rho_out nullable). The pending round
+ * must be waited for before the next one is started. */
+int bsg_consensus_round_async(bsg_ctx* ctx, const bsg_round_args* args, const bsg_adapt_args* adapt);
+int bsg_consensus_wait(bsg_ctx* ctx, bsg_round_result* out, bsg_penalties* rho_out);
+
 /* Single-process group: k contexts (any devices) reduced in ascending block
  * order without NCCL; runs one round for all of them. */
 int bsg_group_consensus_round(bsg_ctx* const* ctxs, size_t k, const bsg_round_args* args, bsg_round_result* out);

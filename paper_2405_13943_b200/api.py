@@ -62,6 +62,11 @@ class bsg_round_result(ctypes.Structure):
                 ("dual_mean_linf", ctypes.c_double), ("flipped", ctypes.c_uint64), ("ms", ctypes.c_double)]
 
 
+class bsg_adapt_args(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_double), ("tau_inc", ctypes.c_double), ("tau_dec", ctypes.c_double),
+                ("freeze_iteration", ctypes.c_uint64), ("adaptive", ctypes.c_int), ("iteration", ctypes.c_uint64)]
+
+
 class bsg_session_options(ctypes.Structure):
     _fields_ = [("total_iterations", ctypes.c_uint64), ("interval", ctypes.c_uint32), ("alpha", ctypes.c_double),
                 ("mu", ctypes.c_double), ("tau_inc", ctypes.c_double), ("tau_dec", ctypes.c_double),
@@ -121,6 +126,8 @@ SYMBOLS = [
     ("bsg_nccl_unique_id", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
     ("bsg_comm_init", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int]),
     ("bsg_consensus_round", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_round_result)]),
+    ("bsg_consensus_round_async", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_adapt_args)]),
+    ("bsg_consensus_wait", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_result), ctypes.POINTER(bsg_penalties)]),
     ("bsg_group_consensus_round", ctypes.c_int, [ctypes.POINTER(_P), _SZ, ctypes.POINTER(bsg_round_args),
                                                   ctypes.POINTER(bsg_round_result)]),
     ("bsg_plan_last_error", ctypes.c_char_p, []),
@@ -405,6 +412,24 @@ class Block:
         r = bsg_round_result()
         _check(_lib.bsg_consensus_round(self.h, ctypes.byref(a), ctypes.byref(r)))
         return _round_dict(r)
+
+    def consensus_round_async(self, alpha, relax, iteration=None, reset_slots=(), diagnostics=False, mu=10.0,
+                              tau_inc=2.0, tau_dec=2.0, freeze_iteration=2000, adaptive=True):
+        """Enqueue a round that overlaps the next train step (only its Adam
+        waits). iteration=None: no penalty adaptation on the device."""
+        self._round_args = _round_args(alpha, relax, reset_slots, diagnostics)  # keep alive until the call returns
+        ad = None
+        if iteration is not None:
+            ad = bsg_adapt_args(mu, tau_inc, tau_dec, freeze_iteration, 1 if adaptive else 0, int(iteration))
+        _check(_lib.bsg_consensus_round_async(self.h, ctypes.byref(self._round_args),
+                                              ctypes.byref(ad) if ad is not None else None))
+
+    def consensus_wait(self):
+        r, rho = bsg_round_result(), bsg_penalties()
+        _check(_lib.bsg_consensus_wait(self.h, ctypes.byref(r), ctypes.byref(rho)))
+        d = _round_dict(r)
+        d["rho"] = (rho.rho_p, rho.rho_q, rho.rho_s, rho.rho_f, rho.rho_o)
+        return d
 
     # ---- measurement ---------------------------------------------------
     def enable_stage_timing(self, on=True):

@@ -91,6 +91,12 @@ void free_all(Ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->nccl) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl));
     if (c->gt_ready) cudaEventDestroy(c->gt_ready);
+    for (cudaEvent_t e : {c->x_ready, c->round_done, c->round_t0, c->round_t1})
+        if (e) cudaEventDestroy(e);
+    if (c->round_host) cudaFreeHost(c->round_host);
+    if (c->rho_dev) cudaFree(c->rho_dev);
+    if (c->rho_state) cudaFree(c->rho_state);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -293,13 +299,12 @@ AdamStep make_adam_step(Ctx* c) {
     const double bc1 = 1.0 - std::pow(t.beta1, static_cast<double>(step));
     const double bc2 = 1.0 - std::pow(t.beta2, static_cast<double>(step));
     for (int k = 0; k < c->D; ++k) {
-        double lr = t.lr_features, rho = c->rho.rho_f;
-        if (k < kRot) { lr = lr_pos; rho = c->rho.rho_p; }
-        else if (k < kLs) { lr = t.lr_rotation; rho = c->rho.rho_q; }
-        else if (k < kFeat) { lr = t.lr_log_scale; rho = c->rho.rho_s; }
-        else if (k == op_comp(c->fd)) { lr = t.lr_opacity; rho = c->rho.rho_o; }
+        double lr = t.lr_features;
+        if (k < kRot) lr = lr_pos;
+        else if (k < kLs) lr = t.lr_rotation;
+        else if (k < kFeat) lr = t.lr_log_scale;
+        else if (k == op_comp(c->fd)) lr = t.lr_opacity;
         st.lr[k] = static_cast<float>(lr);
-        st.rho[k] = static_cast<float>(rho);
     }
     st.b1 = static_cast<float>(t.beta1);
     st.b2 = static_cast<float>(t.beta2);
@@ -335,6 +340,8 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     launch_fold_visible(c, cam, c->last_counters.visible);
     stage_end(c, kStFold);
     stage_begin(c, kStAdam);
+    // penalty + Adam need the round's anchor, duals and rho
+    if (c->round_pending) BSG_CUDA(cudaStreamWaitEvent(c->stream, c->round_done, 0));
     const AdamStep st = make_adam_step(c);
     launch_adam(c, cam, st, loss_dev, 0);
     stage_end(c, kStAdam);
@@ -480,6 +487,14 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             BSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             BSG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
             BSG_CUDA(cudaEventCreateWithFlags(&c->gt_ready, cudaEventDisableTiming));
+            BSG_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+            BSG_CUDA(cudaEventCreateWithFlags(&c->x_ready, cudaEventDisableTiming));
+            BSG_CUDA(cudaEventCreateWithFlags(&c->round_done, cudaEventDisableTiming));
+            BSG_CUDA(cudaEventCreate(&c->round_t0));
+            BSG_CUDA(cudaEventCreate(&c->round_t1));
+            BSG_CUDA(cudaMallocHost(&c->round_host, 8 * sizeof(double)));
+            dev_alloc(&c->rho_dev, kMaxD);
+            dev_alloc(&c->rho_state, 5);
             BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
             dev_alloc(&c->counters, 1);
             dev_alloc(&c->scalars, 1);
@@ -490,6 +505,7 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             for (auto& e : c->ev) BSG_CUDA(cudaEventCreate(&e));
             bsg_default_trainer_config(&c->tcfg);
             bsg_default_penalties(&c->rho);
+            upload_rho(c);
             alloc_rows(c, 1);
         } catch (...) {
             free_all(c);
@@ -911,7 +927,10 @@ int bsg_set_anchor(bsg_ctx* h, const double* z_rows, const double* zprev_slots, 
                 BSG_CUDA(cudaMemset(c->in_zprev, 0, c->n_slots));
             }
         }
-        if (rho) c->rho = *rho;
+        if (rho) {
+            c->rho = *rho;
+            upload_rho(c);
+        }
         c->anchored = true;
     });
 }
@@ -920,7 +939,10 @@ int bsg_set_penalties(bsg_ctx* h, const bsg_penalties* rho) {
     return guarded([&] {
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c || !rho) invalid("null argument");
+        if (c->round_pending) throw Error{BSG_ERR_STATE, "set_penalties while a consensus round is pending"};
+        use_device(c);
         c->rho = *rho;
+        upload_rho(c);
     });
 }
 
@@ -1020,23 +1042,39 @@ int bsg_comm_init(bsg_ctx* h, const uint8_t id[128], int nranks, int rank) {
     });
 }
 
-int bsg_consensus_round(bsg_ctx* h, const bsg_round_args* a, bsg_round_result* out) {
+// The round on the communication stream (c->stream is swapped for the
+// duration of the enqueue so the round_* helpers launch there).
+struct CommScope {
+    Ctx* c;
+    cudaStream_t main;
+    explicit CommScope(Ctx* ctx) : c(ctx), main(ctx->stream) { c->stream = c->comm_stream; }
+    ~CommScope() { c->stream = main; }
+};
+
+int bsg_consensus_round_async(bsg_ctx* h, const bsg_round_args* a, const bsg_adapt_args* adapt) {
     return guarded([&] {
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c || !a) invalid("null argument");
         check_round_ready(c);
+        if (c->round_pending) throw Error{BSG_ERR_STATE, "consensus round started before the previous one was waited for"};
         use_device(c);
+        BSG_CUDA(cudaEventRecord(c->x_ready, c->stream));  // behind the last parameter update
+        CommScope scope(c);
         upload_resets(c, a);
-        cudaEvent_t e0, e1;
-        BSG_CUDA(cudaEventCreate(&e0));
-        BSG_CUDA(cudaEventCreate(&e1));
-        BSG_CUDA(cudaEventRecord(e0, c->stream));
+        BSG_CUDA(cudaStreamWaitEvent(c->stream, c->x_ready, 0));
+        BSG_CUDA(cudaEventRecord(c->round_t0, c->stream));
         round_pack_q(c);
         reduce_nccl(c, c->qref, 4 * c->n_slots, ncclFloat, ncclSum);
         round_pack_main(c, a->alpha, a->relax != 0);
         reduce_nccl(c, c->pack, (c->D + 1) * c->n_slots, ncclFloat, ncclSum);
         round_unpack(c, a->alpha, a->relax != 0, a->n_reset ? c->slot_reset : nullptr, a->n_reset, a->diagnostics != 0);
-        reduce_nccl(c, c->round_scalars, 1, ncclFloat64, ncclSum);  // primal^2 partials
+        // primal^2 partials sum over ranks; dual^2 and the flip count are computed
+        // identically everywhere, so only rank 0 contributes them and every rank
+        // adapts rho on bit-identical inputs
+        if (c->nccl && c->nranks > 1 && c->rank != 0)
+            BSG_CUDA(cudaMemsetAsync(c->round_scalars + 1, 0, 2 * sizeof(double), c->stream));
+        reduce_nccl(c, c->round_scalars, 3, ncclFloat64, ncclSum);
+        if (adapt) round_adapt(c, *adapt);
         if (a->diagnostics) {
             round_pack_duals(c);
             reduce_nccl(c, c->pack, c->D * c->n_slots, ncclFloat, ncclSum);
@@ -1045,26 +1083,45 @@ int bsg_consensus_round(bsg_ctx* h, const bsg_round_args* a, bsg_round_result* o
             reduce_nccl(c, c->pack, 2 * c->D * c->n_slots, ncclFloat, ncclMax);
             round_spread(c);
         }
-        BSG_CUDA(cudaEventRecord(e1, c->stream));
-        double sc[8];
-        BSG_CUDA(cudaMemcpyAsync(sc, c->round_scalars, sizeof(sc), cudaMemcpyDeviceToHost, c->stream));
-        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        BSG_CUDA(cudaEventRecord(c->round_t1, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(c->round_host, c->round_scalars, 8 * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+        BSG_CUDA(cudaEventRecord(c->round_done, c->stream));
+        c->round_pending = true;
+        c->round_diag = a->diagnostics != 0;
+    });
+}
+
+int bsg_consensus_wait(bsg_ctx* h, bsg_round_result* out, bsg_penalties* rho_out) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!c->round_pending) throw Error{BSG_ERR_STATE, "no consensus round pending"};
+        use_device(c);
+        BSG_CUDA(cudaEventSynchronize(c->round_done));
+        c->round_pending = false;
+        double rs[5];
+        BSG_CUDA(cudaMemcpy(rs, c->rho_state, sizeof(rs), cudaMemcpyDeviceToHost));
+        c->rho = bsg_penalties{rs[0], rs[1], rs[2], rs[3], rs[4]};
+        if (rho_out) *rho_out = c->rho;
         float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        cudaEventElapsedTime(&ms, c->round_t0, c->round_t1);
+        const double* sc = c->round_host;
         if (out) {
             out->primal = std::sqrt(sc[0]);
             out->dual = std::sqrt(sc[1]);
             out->flipped = static_cast<uint64_t>(sc[2]);
-            uint64_t b3, b4;
-            std::memcpy(&b3, &sc[3], 8);
-            std::memcpy(&b4, &sc[4], 8);
-            out->dual_mean_linf = sc[3];
-            out->max_disagreement = sc[4];
+            out->dual_mean_linf = c->round_diag ? sc[3] : 0.0;
+            out->max_disagreement = c->round_diag ? sc[4] : 0.0;
             out->ms = ms;
         }
     });
+}
+
+int bsg_consensus_round(bsg_ctx* h, const bsg_round_args* a, bsg_round_result* out) {
+    const int st = bsg_consensus_round_async(h, a, nullptr);
+    if (st != BSG_OK) return st;
+    return bsg_consensus_wait(h, out, nullptr);
 }
 
 int bsg_group_consensus_round(bsg_ctx* const* hs, size_t k, const bsg_round_args* a, bsg_round_result* out) {

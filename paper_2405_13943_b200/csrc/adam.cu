@@ -237,7 +237,8 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
                                                    const float* __restrict__ gbuf,
                                                    const uint32_t* __restrict__ sh_mask,
                                                    const uint32_t* __restrict__ sh_prefix, const float* __restrict__ z,
-                                                   const float* __restrict__ u, size_t ns, AdamStep st,
+                                                   const float* __restrict__ u, size_t ns,
+                                                   const float* __restrict__ rho_dev, AdamStep st,
                                                    double* __restrict__ penalty) {
     __shared__ double s_red[8];
     constexpr int NC = 1;
@@ -288,7 +289,7 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
         }
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            const float lr = st.lr[c0 + k], rho = st.rho[c0 + k];
+            const float lr = st.lr[c0 + k], rho = st.has_anchor ? rho_dev[c0 + k] : 0.f;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 float gr = g[k][r];
@@ -340,7 +341,8 @@ __global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, fl
                                                        const uint32_t* __restrict__ sh_mask,
                                                        const uint32_t* __restrict__ sh_prefix,
                                                        const float* __restrict__ z, const float* __restrict__ u,
-                                                       size_t ns, AdamStep st, double* __restrict__ penalty) {
+                                                       size_t ns, const float* __restrict__ rho_dev, AdamStep st,
+                                                       double* __restrict__ penalty) {
     __shared__ double s_red[8];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     double pen = 0.0;
@@ -366,7 +368,7 @@ __global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, fl
         if (aj >= 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float rho = st.rho[kRot + k];
+                const float rho = rho_dev[kRot + k];
                 const float d = xs[k] - z[static_cast<size_t>(kRot + k) * ns + aj] + u[static_cast<size_t>(kRot + k) * ns + aj];
                 pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
                 g[k] += rho * d;
@@ -439,11 +441,12 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     const int scalar_groups = c->D - 4;  // every component but the quaternion
     const dim3 g1(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(scalar_groups));
     adam_kernel<1><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
-                                                     c->sh_prefix, c->z, c->u, c->n_shared, st, &c->scalars->penalty);
+                                              c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
+                                              &c->scalars->penalty);
     BSG_LAUNCHED(c);
     adam_rot_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
-        c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, st,
-        &c->scalars->penalty);
+        c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
+        c->rho_dev, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }
 

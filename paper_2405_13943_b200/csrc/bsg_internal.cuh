@@ -71,6 +71,11 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host ground-truth uploads (e2e path)
     cudaEvent_t gt_ready = nullptr;
+    cudaStream_t comm_stream = nullptr;  // consensus rounds (overlap with the next step)
+    cudaEvent_t x_ready = nullptr, round_done = nullptr, round_t0 = nullptr, round_t1 = nullptr;
+    bool round_pending = false;
+    bool round_diag = false;
+    double* round_host = nullptr;        // pinned copy of round_scalars
     int fd = 3, D = 14;
     size_t n = 0, cap = 0;
     std::vector<uint64_t> ids;
@@ -156,7 +161,9 @@ struct Ctx {
     uint8_t* slot_reset = nullptr;
     double* round_scalars = nullptr;  // primal2, dual2, flips, maxdis, linf
     bool anchored = false;
-    bsg_penalties rho{};
+    bsg_penalties rho{};           // host copy; the device copy below is authoritative for Adam
+    float* rho_dev = nullptr;      // per-component rho [kMaxD] read by the penalty + Adam
+    double* rho_state = nullptr;   // rho_p, rho_q, rho_s, rho_f, rho_o (adapted on the device)
     void* nccl = nullptr;       // ncclComm_t
     int nranks = 1, rank = 0;
 
@@ -238,7 +245,6 @@ struct AdamStep {
     float lr[kMaxD];
     float b1, b2, eps, omb1, omb2;
     float inv_bc1, inv_bc2;
-    float rho[kMaxD];
     int has_anchor;
 };
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
@@ -250,6 +256,10 @@ void round_pack_q(Ctx* c);
 void round_pack_main(Ctx* c, double alpha, bool relax);
 void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_dev, size_t n_reset, bool diag);
 void round_apply_broadcast(Ctx* c, double alpha, bool relax, bool has_resets);
+// adapt_penalties (admm.cpp:200-217) on the device from round_scalars; writes rho_state and rho_dev.
+void round_adapt(Ctx* c, const bsg_adapt_args& a);
+// rho_state / rho_dev from the host copy c->rho (stream-ordered on c->stream).
+void upload_rho(Ctx* c);
 
 // ---- the step ------------------------------------------------------------
 void ensure_image_buffers(Ctx* c, int W, int H);

@@ -186,6 +186,40 @@ __global__ __launch_bounds__(256) void spread_kernel(const float* __restrict__ p
 
 inline unsigned grid_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
+__device__ __forceinline__ void rho_to_components(const double* rs, int fd, float* rho_dev) {
+    const int D = 11 + fd;
+    for (int k = 0; k < D; ++k) {
+        double r = rs[3];                       // features
+        if (k < kRot) r = rs[0];
+        else if (k < kLs) r = rs[1];
+        else if (k < kFeat) r = rs[2];
+        else if (k == kFeat + fd) r = rs[4];    // opacity
+        rho_dev[k] = static_cast<float>(r);
+    }
+}
+
+// adapt_penalties (admm.cpp:200-217) from the reduced residuals: primal^2 in
+// scal[0], dual^2 in scal[1] (identical on every rank after the reduction).
+__global__ void adapt_kernel(const double* __restrict__ scal, double* __restrict__ rs, int fd,
+                             float* __restrict__ rho_dev, bsg_adapt_args a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (a.adaptive && a.iteration <= a.freeze_iteration) {
+        const double primal = sqrt(scal[0]), dual = sqrt(scal[1]);
+        double f = 1.0;
+        if (primal > a.mu * dual)
+            f = a.tau_inc;
+        else if (dual > a.mu * primal)
+            f = 1.0 / a.tau_dec;
+        if (f != 1.0)
+            for (int k = 0; k < 5; ++k) rs[k] *= f;
+    }
+    rho_to_components(rs, fd, rho_dev);
+}
+
+__global__ void rho_components_kernel(const double* __restrict__ rs, int fd, float* __restrict__ rho_dev) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) rho_to_components(rs, fd, rho_dev);
+}
+
 }  // namespace
 
 void round_pack_q(Ctx* c) {
@@ -210,17 +244,7 @@ void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_d
     (void)n_reset;
     (void)diag;
     BSG_CUDA(cudaMemsetAsync(c->round_scalars, 0, 8 * sizeof(double), c->stream));
-    float rho[kMaxD];
-    for (int k = 0; k < c->D; ++k) {
-        double r = c->rho.rho_f;
-        if (k < kRot) r = c->rho.rho_p;
-        else if (k < kLs) r = c->rho.rho_q;
-        else if (k < kFeat) r = c->rho.rho_s;
-        else if (k == op_comp(c->fd)) r = c->rho.rho_o;
-        rho[k] = static_cast<float>(r);
-    }
-    float* rho_dev = reinterpret_cast<float*>(c->round_scalars + 8);
-    BSG_CUDA(cudaMemcpyAsync(rho_dev, rho, sizeof(rho), cudaMemcpyHostToDevice, c->stream));
+    const float* rho_dev = c->rho_dev;  // rho in force this round (the dual residual weights)
     if (c->n_slots > 0) {
         unpack_slots_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(c->pack, c->D, c->n_slots, c->slot_owners,
                                                                          c->zslot, c->zprev, c->in_zprev, rho_dev,
@@ -279,6 +303,19 @@ void round_spread(Ctx* c) {
     spread_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(
         c->pack, c->D, c->n_slots, c->slot_owners, reinterpret_cast<unsigned long long*>(&c->round_scalars[4]));
     BSG_LAUNCHED(c);
+}
+
+void round_adapt(Ctx* c, const bsg_adapt_args& a) {
+    adapt_kernel<<<1, 32, 0, c->stream>>>(c->round_scalars, c->rho_state, c->fd, c->rho_dev, a);
+    BSG_LAUNCHED(c);
+}
+
+void upload_rho(Ctx* c) {
+    const double h[5] = {c->rho.rho_p, c->rho.rho_q, c->rho.rho_s, c->rho.rho_f, c->rho.rho_o};
+    BSG_CUDA(cudaMemcpyAsync(c->rho_state, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    rho_components_kernel<<<1, 32, 0, c->stream>>>(c->rho_state, c->fd, c->rho_dev);
+    BSG_LAUNCHED(c);
+    BSG_CUDA(cudaStreamSynchronize(c->stream));  // h lives on this stack frame
 }
 
 }  // namespace bsg

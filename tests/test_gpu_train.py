@@ -157,3 +157,54 @@ def test_consensus_round_matches_oracle(relax):
         np.testing.assert_allclose(dev.anchor(), zr, rtol=1e-6, atol=1e-6)
     # dual-mean diagnostic (runtime.cpp:572-606) and disagreement (admm.cpp:219-243)
     assert res["max_disagreement"] == pytest.approx(orc.max_disagreement([(0, sa), (1, sb)]), rel=1e-5)
+
+
+def _anchored_trainer(init, s, shared_rows, zprev_rows, rho):
+    b = device_trainer(init, s)
+    n = len(shared_rows)
+    b.set_shared(shared_rows, list(range(n)), [1] * n, [1] * n)
+    b.set_anchor(zprev_rows, zprev_rows, rho)
+    return b
+
+
+def test_async_round_overlaps_next_step_exactly():
+    """an asynchronous round (comm stream, device-side penalty
+    adaptation) followed immediately by train steps -- whose Adam waits for the
+    round -- equals a synchronous round, host-side adapt_penalties
+    (admm.cpp:200-217) and the same steps."""
+    s, init = toy_scene()
+    shared_rows = list(range(0, init.n, 3))
+    g = np.random.default_rng(5)
+    x0 = rows_of(init)[shared_rows]
+    zprev = (x0 + 0.05 * g.standard_normal(x0.shape)).astype(np.float32).astype(np.float64)
+    rho = api.penalties()
+    seq = orc.view_sequence(1, 0, len(s.views), 12)
+    # synchronous reference
+    a = _anchored_trainer(init, s, shared_rows, zprev, rho)
+    a.train_steps(seq[:4])
+    ra = a.consensus_round(1.6, True)
+    mu, tau_inc, tau_dec = 10.0, 2.0, 2.0
+    f = 1.0
+    if ra["primal"] > mu * ra["dual"]:
+        f = tau_inc
+    elif ra["dual"] > mu * ra["primal"]:
+        f = 1.0 / tau_dec
+    rho_a = api.penalties(**{k: getattr(rho, k) * f for k in ("rho_p", "rho_q", "rho_s", "rho_f", "rho_o")})
+    a.set_penalties(rho_a)
+    la = a.train_steps(seq[4:12])
+    # asynchronous: the round is in flight while the next steps project/sort/blend
+    b = _anchored_trainer(init, s, shared_rows, zprev, rho)
+    b.train_steps(seq[:4])
+    b.consensus_round_async(1.6, True, iteration=4, mu=mu, tau_inc=tau_inc, tau_dec=tau_dec)
+    lb = b.train_steps(seq[4:12])
+    rb = b.consensus_wait()
+    assert f != 1.0  # the case exercises the adaptation
+    assert rb["rho"] == pytest.approx((rho_a.rho_p, rho_a.rho_q, rho_a.rho_s, rho_a.rho_f, rho_a.rho_o), rel=1e-12)
+    assert rb["primal"] == pytest.approx(ra["primal"], rel=1e-6)
+    assert rb["dual"] == pytest.approx(ra["dual"], rel=1e-6)
+    np.testing.assert_allclose(lb, la, rtol=1e-4)
+    np.testing.assert_allclose(b.duals(), a.duals(), rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(b.anchor(), a.anchor(), rtol=1e-5, atol=1e-6)
+    ga, gb = a.download_cloud(), b.download_cloud()
+    for k in ("pos", "rot", "ls", "feat", "op"):
+        np.testing.assert_allclose(gb[k], ga[k], rtol=1e-4, atol=1e-5)

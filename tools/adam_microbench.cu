@@ -243,7 +243,8 @@ int main() {
         CK(cudaMemset(X, 0, DD * cap * 4)); CK(cudaMemset(M, 0, DD * cap * 4)); CK(cudaMemset(Vv, 0, DD * cap * 4));
         CK(cudaMemset(G, 0, DD * cap * 4));
         bsg::AdamStep st{};
-        for (int k = 0; k < 23; ++k) { st.lr[k] = 1e-3f; st.rho[k] = 1.f; }
+        for (int k = 0; k < 23; ++k) st.lr[k] = 1e-3f;
+        float* rho_d; CK(cudaMalloc(&rho_d, 23 * 4)); CK(cudaMemset(rho_d, 0, 23 * 4));
         st.b1 = 0.9f; st.b2 = 0.999f; st.omb1 = 0.1f; st.omb2 = 0.001f; st.eps = 1e-8f; st.inv_bc1 = 10.f; st.inv_bc2 = 1000.f;
         st.has_anchor = 0;
         double* pen; CK(cudaMalloc(&pen, 8));
@@ -260,15 +261,15 @@ int main() {
         };
         runp("prod scalar (10 comps)", b10, [&] {
             bsg::adam_kernel<1><<<dim3((n + 1023) / 1024, 10), 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
-                                                                            nullptr, nullptr, 0, st, pen); });
+                                                                            nullptr, nullptr, 0, rho_d, st, pen); });
         runp("prod rot (4 comps)", b4, [&] {
             bsg::adam_rot_kernel<<<(n + 255) / 256, 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
-                                                                          nullptr, nullptr, 0, st, pen); });
+                                                                          nullptr, nullptr, 0, rho_d, st, pen); });
         runp("prod both", b10 + b4, [&] {
             bsg::adam_kernel<1><<<dim3((n + 1023) / 1024, 10), 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
-                                                                            nullptr, nullptr, 0, st, pen);
+                                                                            nullptr, nullptr, 0, rho_d, st, pen);
             bsg::adam_rot_kernel<<<(n + 255) / 256, 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
-                                                                          nullptr, nullptr, 0, st, pen); });
+                                                                          nullptr, nullptr, 0, rho_d, st, pen); });
     }
     CK(cudaDeviceSynchronize());
     return 0;
