@@ -217,10 +217,20 @@ def run_ours(args, rank, world, local_rank):
             import torch.distributed as dist
             dist.barrier()
 
-    def consensus(it):
-        if world > 1 and it % args.interval == 0:
-            return blk.consensus_round(1.6, True)
-        return None
+    pending = [False]
+
+    def consensus(it, flush=False):
+        """Every `interval` iterations an asynchronous round: it
+        overlaps the next step's projection/sort/blends/fold, only that step's
+        Adam waits; its result is collected after the next step is enqueued."""
+        r = None
+        if pending[0]:
+            r = blk.consensus_wait()
+            pending[0] = False
+        if world > 1 and not flush and it % args.interval == 0:
+            blk.consensus_round_async(1.6, True, iteration=it)
+            pending[0] = True
+        return r
 
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -231,6 +241,7 @@ def run_ours(args, rank, world, local_rank):
         blk.train_steps([next_view()], want_losses=False)
         it += 1
         consensus(it)
+    consensus(it, flush=True)
     # timed region: steps back to back, no per-stage events or host reads
     round_ms = []
     barrier()
@@ -245,6 +256,9 @@ def run_ours(args, rank, world, local_rank):
         r = consensus(it)
         if r is not None:
             round_ms.append(r["ms"])
+    r = consensus(it, flush=True)
+    if r is not None:
+        round_ms.append(r["ms"])
     e1.record(stream)
     torch.cuda.synchronize()
     tc1 = time.perf_counter()
@@ -273,6 +287,7 @@ def run_ours(args, rank, world, local_rank):
         c = blk.step_counters()
         counters_sum["visible"] += c["visible"]
         counters_sum["pairs"] += c["pairs"]
+    consensus(it, flush=True)
     blk.enable_stage_timing(False)
 
     if args.profile:
@@ -291,6 +306,7 @@ def run_ours(args, rank, world, local_rank):
         blk.train_step_host(view_cams[v], pinned[v].numpy())
         it += 1
         consensus(it)
+    consensus(it, flush=True)
     f1.record(stream)
     torch.cuda.synchronize()
     barrier()

@@ -76,7 +76,7 @@ void dev_alloc(T** p, size_t count) {
 void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
-    void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->gbuf,
+    void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->gbuf,
                     c->vis_mask, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
@@ -495,6 +495,7 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             BSG_CUDA(cudaMallocHost(&c->round_host, 8 * sizeof(double)));
             dev_alloc(&c->rho_dev, kMaxD);
             dev_alloc(&c->rho_state, 5);
+            dev_alloc(&c->g2d_wide, 9 * static_cast<size_t>(kWideCap));
             BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
             dev_alloc(&c->counters, 1);
             dev_alloc(&c->scalars, 1);
@@ -984,6 +985,9 @@ int bsg_download_consensus(bsg_ctx* h, double* z_slots) {
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c) invalid("null context");
         use_device(c);
+        if (c->round_pending) throw Error{BSG_ERR_STATE, "consensus download while a round is pending"};
+        round_slots_from_sums(c);
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         std::vector<float> hz(c->D * std::max<size_t>(c->n_slots, 1));
         if (c->n_slots) BSG_CUDA(cudaMemcpy(hz.data(), c->zslot, c->D * c->n_slots * 4, cudaMemcpyDeviceToHost));
         cm_to_rows(hz.data(), c->n_slots, c->D, z_slots);
@@ -1000,6 +1004,7 @@ int bsg_apply_broadcast(bsg_ctx* h, const double* z_slots, size_t n_reset, const
         if (c->n_slots) {
             const std::vector<float> zc = rows_to_cm(z_slots, c->n_slots, c->D);
             BSG_CUDA(cudaMemcpy(c->zslot, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
+            c->zslot_from_pack = false;
             BSG_CUDA(cudaMemcpy(c->zprev, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
             BSG_CUDA(cudaMemset(c->in_zprev, 1, c->n_slots));
         }
@@ -1068,11 +1073,8 @@ int bsg_consensus_round_async(bsg_ctx* h, const bsg_round_args* a, const bsg_ada
         round_pack_main(c, a->alpha, a->relax != 0);
         reduce_nccl(c, c->pack, (c->D + 1) * c->n_slots, ncclFloat, ncclSum);
         round_unpack(c, a->alpha, a->relax != 0, a->n_reset ? c->slot_reset : nullptr, a->n_reset, a->diagnostics != 0);
-        // primal^2 partials sum over ranks; dual^2 and the flip count are computed
-        // identically everywhere, so only rank 0 contributes them and every rank
-        // adapts rho on bit-identical inputs
-        if (c->nccl && c->nranks > 1 && c->rank != 0)
-            BSG_CUDA(cudaMemsetAsync(c->round_scalars + 1, 0, 2 * sizeof(double), c->stream));
+        // primal^2, dual^2 (each slot by its lowest owner) and flip-count partials
+        // summed over ranks: every rank adapts rho on bit-identical inputs
         reduce_nccl(c, c->round_scalars, 3, ncclFloat64, ncclSum);
         if (adapt) round_adapt(c, *adapt);
         if (a->diagnostics) {
@@ -1146,17 +1148,18 @@ int bsg_group_consensus_round(bsg_ctx* const* hs, size_t k, const bsg_round_args
             round_pack_main(c, a->alpha, a->relax != 0);
         }
         reduce_group(cp, k, &Ctx::pack, (cs[0]->D + 1) * cs[0]->n_slots, false);
-        double primal2 = 0;
-        double sc0[8] = {};
+        double primal2 = 0, dual2 = 0, flips = 0;  // per-block partials, summed in block order
         for (size_t b = 0; b < k; ++b) {
             Ctx* c = cs[b];
             use_device(c);
-            round_unpack(c, a->alpha, a->relax != 0, a->n_reset ? c->slot_reset : nullptr, a->n_reset, false);
+            round_unpack(c, a->alpha, a->relax != 0, a->n_reset ? c->slot_reset : nullptr, a->n_reset,
+                         a->diagnostics != 0);
             double sc[8];
             BSG_CUDA(cudaMemcpyAsync(sc, c->round_scalars, sizeof(sc), cudaMemcpyDeviceToHost, c->stream));
             BSG_CUDA(cudaStreamSynchronize(c->stream));
             primal2 += sc[0];
-            if (b == 0) std::memcpy(sc0, sc, sizeof(sc));
+            dual2 += sc[1];
+            flips += sc[2];
         }
         double linf = 0, spread = 0;
         if (a->diagnostics) {
@@ -1182,8 +1185,8 @@ int bsg_group_consensus_round(bsg_ctx* const* hs, size_t k, const bsg_round_args
         }
         if (out) {
             out->primal = std::sqrt(primal2);
-            out->dual = std::sqrt(sc0[1]);
-            out->flipped = static_cast<uint64_t>(sc0[2]);
+            out->dual = std::sqrt(dual2);
+            out->flipped = static_cast<uint64_t>(flips);
             out->dual_mean_linf = linf;
             out->max_disagreement = spread;
             out->ms = 0;

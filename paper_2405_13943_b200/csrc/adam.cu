@@ -20,15 +20,34 @@ __device__ __forceinline__ void load_row(const float* __restrict__ x, size_t cap
     for (int k = 0; k < 11 + fd; ++k) prm[k] = x[k * cap + i];
 }
 
+// The 9 image-space gradients of row i: FP32 record, or the FP64 slot of a
+// wide splat (slot index in rec[3i+2].w, see kWideArea).
+struct Grad2D {
+    double v[9];
+};
+__device__ __forceinline__ Grad2D load_g2d(uint32_t i, const float4* __restrict__ rec,
+                                           const float4* __restrict__ g2d, const double* __restrict__ g2d_wide) {
+    Grad2D g;
+    const uint32_t wslot = __float_as_uint(rec[3 * static_cast<size_t>(i) + 2].w);
+    if (wslot != kNoWide) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) g.v[k] = g2d_wide[9 * static_cast<size_t>(wslot) + k];
+    } else {
+        const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
+                     gc = g2d[3 * static_cast<size_t>(i) + 2];
+        g.v[0] = ga.x; g.v[1] = ga.y; g.v[2] = ga.z; g.v[3] = ga.w;
+        g.v[4] = gb.x; g.v[5] = gb.y; g.v[6] = gb.z; g.v[7] = gb.w; g.v[8] = gc.x;
+    }
+    return g;
+}
+
 template <int fd>
-__device__ __forceinline__ double fold_row(const float (&prm)[11 + fd], uint32_t i, const DevCam& cam,
-                                           const float4* __restrict__ g2d, double* g) {
-    const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
-                 gcx = g2d[3 * static_cast<size_t>(i) + 2];
-    const double gm0 = ga.x, gm1 = ga.y;
-    const double gcov[2][2] = {{ga.z, ga.w}, {ga.w, gb.x}};
-    const double gcol[3] = {gb.y, gb.z, gb.w};
-    const double gop = gcx.x;
+__device__ __forceinline__ double fold_row(const float (&prm)[11 + fd], const Grad2D& g2, const DevCam& cam,
+                                           double* g) {
+    const double gm0 = g2.v[0], gm1 = g2.v[1];
+    const double gcov[2][2] = {{g2.v[2], g2.v[3]}, {g2.v[3], g2.v[4]}};
+    const double gcol[3] = {g2.v[5], g2.v[6], g2.v[7]};
+    const double gop = g2.v[8];
 
     const double pos[3] = {prm[kPos + 0], prm[kPos + 1], prm[kPos + 2]};
     double pc[3];
@@ -167,7 +186,9 @@ __device__ __forceinline__ double fold_row(const float (&prm)[11 + fd], uint32_t
 template <int fd>
 __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
                                                          DevCam cam, const uint32_t* __restrict__ tiles,
-                                                         const float4* __restrict__ g2d, double* __restrict__ gout,
+                                                         const float4* __restrict__ rec,
+                                                         const float4* __restrict__ g2d,
+                                                         const double* __restrict__ g2d_wide, double* __restrict__ gout,
                                                          double* __restrict__ sgn_out, uint8_t* __restrict__ vis) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -180,7 +201,7 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
     if (visible) {
         float prm[11 + fd];
         load_row<fd>(x, cap, i, prm);
-        s = fold_row<fd>(prm, i, cam, g2d, g);
+        s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
     }
 #pragma unroll
     for (int c = 0; c < D; ++c) gout[static_cast<size_t>(c) * n + i] = g[c];
@@ -193,7 +214,9 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
 template <int fd>
 __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, DevCam cam,
                                                            const uint32_t* __restrict__ vis_rows, uint32_t V,
-                                                           const float4* __restrict__ g2d, float* __restrict__ gbuf,
+                                                           const float4* __restrict__ rec,
+                                                           const float4* __restrict__ g2d,
+                                                           const double* __restrict__ g2d_wide, float* __restrict__ gbuf,
                                                            float* __restrict__ grad_accum,
                                                            uint32_t* __restrict__ grad_seen) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -205,7 +228,7 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
     for (int c = 0; c < D; ++c) g[c] = 0.0;
     float prm[11 + fd];
     load_row<fd>(x, cap, i, prm);
-    const double s = fold_row<fd>(prm, i, cam, g2d, g);
+    const double s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
 #pragma unroll
     for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + i] = static_cast<float>(g[c]);
     grad_accum[i] += static_cast<float>(s);
@@ -414,10 +437,10 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
     const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
     if (c->fd == 3)
         fold_grads_kernel<3><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
-                                                            c->g2d, g_out, sgn, vis);
+                                                            c->rec, c->g2d, c->g2d_wide, g_out, sgn, vis);
     else
         fold_grads_kernel<12><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
-                                                             c->g2d, g_out, sgn, vis);
+                                                             c->rec, c->g2d, c->g2d_wide, g_out, sgn, vis);
     BSG_LAUNCHED(c);
 }
 
@@ -425,10 +448,12 @@ void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     if (c->fd == 3)
         fold_visible_kernel<3><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
-                                                                        c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
+                                                                        c->rec, c->g2d, c->g2d_wide, c->gbuf,
+                                                                        c->grad_accum, c->grad_seen);
     else
         fold_visible_kernel<12><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
-                                                                         c->g2d, c->gbuf, c->grad_accum, c->grad_seen);
+                                                                         c->rec, c->g2d, c->g2d_wide, c->gbuf,
+                                                                        c->grad_accum, c->grad_seen);
     BSG_LAUNCHED(c);
 }
 

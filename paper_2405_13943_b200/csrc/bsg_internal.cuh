@@ -15,6 +15,13 @@
 namespace bsg {
 
 constexpr int kTile = 16;             // 16x16 pixel tiles, one thread per pixel
+// Splats whose footprint rect covers at least kWideArea pixels (near-plane
+// grazers spanning most of the image) accumulate their image-space gradient
+// in FP64 (compact slot per splat): their fold cancels to ~1e-5 of the sum, so
+// FP32 atomics in arbitrary order would leave O(10%) run-to-run noise.
+constexpr uint32_t kWideArea = 4096;
+constexpr uint32_t kWideCap = 65536;  // wide splats per step with an FP64 slot (others stay FP32)
+constexpr uint32_t kNoWide = 0xffffffffu;
 constexpr int kTileThreads = kTile * kTile;
 constexpr int kMaxFd = 12;            // SH degree 1 (cloud.hpp:16-17)
 constexpr int kMaxD = 11 + kMaxFd;    // pos3 rot4 ls3 feat fd op1
@@ -47,6 +54,8 @@ struct StepCounters {
     uint32_t pairs;     // P
     uint32_t overflow;  // a run of equal 32-bit depth keys too long for the fix-up
     uint32_t visible_pre;  // visible count as seen by the preprocess (sizes the depth key)
+    uint32_t wide;         // wide splats given an FP64 gradient slot this step
+    uint32_t pad2;
     unsigned long long zmin_inv;  // ~bits of the smallest visible FP64 depth (atomicMax of the complement)
     unsigned long long zmax;      // bits of the largest visible FP64 depth
     uint32_t depth_hist[8][256];  // digit histograms of the visible depth keys (filled by the compaction)
@@ -92,6 +101,7 @@ struct Ctx {
     uint64_t* depth_key = nullptr; // FP64 depth bits
     uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
     float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
+    double* g2d_wide = nullptr;    // [kWideCap][9] FP64 gradients of wide splats (slot in rec[3i+2].w)
     float* gbuf = nullptr;         // parameter gradient of visible rows, [D][cap]
     uint32_t* vis_mask = nullptr;  // 1 bit per row: visible this step (written by the compaction)
     uint32_t* sh_mask = nullptr;   // 1 bit per row: shared (has an anchor)
@@ -153,7 +163,8 @@ struct Ctx {
     float* z = nullptr;         // anchor [D][n_shared]
     float* u = nullptr;         // duals  [D][n_shared]
     float* zprev = nullptr;     // [D][n_slots]
-    float* zslot = nullptr;     // consensus of the last round [D][n_slots]
+    float* zslot = nullptr;     // consensus of the last round [D][n_slots] (materialised on demand)
+    bool zslot_from_pack = false;  // zslot is stale; `pack` holds the reduced sums
     uint8_t* in_zprev = nullptr;
     uint32_t* slot_owners = nullptr;
     float* pack = nullptr;      // [D+1][n_slots] (+1 = flip flag)
@@ -255,6 +266,7 @@ void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double
 void round_pack_q(Ctx* c);
 void round_pack_main(Ctx* c, double alpha, bool relax);
 void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_dev, size_t n_reset, bool diag);
+void round_slots_from_sums(Ctx* c);
 void round_apply_broadcast(Ctx* c, double alpha, bool relax, bool has_resets);
 // adapt_penalties (admm.cpp:200-217) on the device from round_scalars; writes rho_state and rho_dev.
 void round_adapt(Ctx* c, const bsg_adapt_args& a);

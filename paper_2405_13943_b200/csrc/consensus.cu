@@ -31,31 +31,37 @@ __global__ void pack_q_kernel(const float* __restrict__ x, size_t cap, const uin
     for (int c = 0; c < 4; ++c) qref[c * S + s] = x[(kRot + c) * cap + r];
 }
 
-__global__ void pack_main_kernel(const float* __restrict__ x, size_t cap, int D, const uint32_t* __restrict__ rows,
-                                 const uint32_t* __restrict__ slots, const uint8_t* __restrict__ first, size_t ns,
-                                 size_t S, const float* __restrict__ qref, const float* __restrict__ zprev,
-                                 const uint8_t* __restrict__ in_zprev, float alpha, int relax,
-                                 float* __restrict__ pack) {
+template <int D>
+__global__ __launch_bounds__(256) void pack_main_kernel(const float* __restrict__ x, size_t cap,
+                                                        const uint32_t* __restrict__ rows,
+                                                        const uint32_t* __restrict__ slots,
+                                                        const uint8_t* __restrict__ first, size_t ns, size_t S,
+                                                        const float* __restrict__ qref,
+                                                        const float* __restrict__ zprev,
+                                                        const uint8_t* __restrict__ in_zprev, float alpha, int relax,
+                                                        float* __restrict__ pack) {
     const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (j >= ns) return;
     const uint32_t r = rows[j], s = slots[j];
-    float q[4];
+    const bool blend = relax && in_zprev[s];
+    float v[D], zp[D];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) q[c] = x[(kRot + c) * cap + r];
+    for (int c = 0; c < D; ++c) {
+        v[c] = x[c * cap + r];
+        zp[c] = blend ? zprev[c * S + s] : 0.f;
+    }
     float flip = 0.f;
     if (!first[j]) {
-        const float dot = ((q[0] * qref[s] + q[1] * qref[S + s]) + q[2] * qref[2 * S + s]) + q[3] * qref[3 * S + s];
+        const float dot = ((v[kRot] * qref[s] + v[kRot + 1] * qref[S + s]) + v[kRot + 2] * qref[2 * S + s]) +
+                          v[kRot + 3] * qref[3 * S + s];
         if (dot < 0.f) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) q[c] = -q[c];
+            for (int c = kRot; c < kRot + 4; ++c) v[c] = -v[c];
             flip = 1.f;
         }
     }
-    const bool blend = relax && in_zprev[s];
-    for (int c = 0; c < D; ++c) {
-        const float v = (c >= kRot && c < kRot + 4) ? q[c - kRot] : x[c * cap + r];
-        pack[c * S + s] = relaxed(v, blend ? zprev[c * S + s] : 0.f, alpha, blend);
-    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) pack[c * S + s] = relaxed(v[c], zp[c], alpha, blend);
     pack[static_cast<size_t>(D) * S + s] = flip;
 }
 
@@ -69,35 +75,6 @@ __device__ __forceinline__ void block_add(double v, double* dst, double* s_red) 
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_red[w];
         if (t != 0.0) atomicAdd(dst, t);
     }
-}
-
-// z = sum / owners for every slot; dual residual over slots in z_prev
-// (admm.cpp:183-198); flip count; z_prev := z.
-__global__ __launch_bounds__(256) void unpack_slots_kernel(const float* __restrict__ pack, int D, size_t S,
-                                                           const uint32_t* __restrict__ owners, float* __restrict__ zslot,
-                                                           float* __restrict__ zprev, uint8_t* __restrict__ in_zprev,
-                                                           const float* __restrict__ rho, double* __restrict__ scal) {
-    __shared__ double s_red[8];
-    const size_t s = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    double d2 = 0.0, flips = 0.0;
-    if (s < S) {
-        const float inv = 1.0f / static_cast<float>(owners[s]);
-        const bool had = in_zprev[s] != 0;
-        for (int c = 0; c < D; ++c) {
-            const float zv = pack[c * S + s] * inv;
-            if (had) {
-                const double dv = static_cast<double>(rho[c]) * (static_cast<double>(zv) - zprev[c * S + s]);
-                d2 += dv * dv;
-            }
-            zslot[c * S + s] = zv;
-            zprev[c * S + s] = zv;
-        }
-        in_zprev[s] = 1;
-        flips = pack[static_cast<size_t>(D) * S + s] > 0.f ? 1.0 : 0.0;
-    }
-    block_add(d2, &scal[1], s_red);
-    __syncthreads();
-    block_add(flips, &scal[2], s_red);
 }
 
 // Worker half (trainer.cpp:186-222): x_hat = relaxed(x, anchor) WITHOUT the
@@ -128,6 +105,85 @@ __global__ __launch_bounds__(256) void dual_update_kernel(const float* __restric
         }
     }
     block_add(p2, &scal[0], s_red);
+}
+
+// One pass over this block's shared rows after the reduction of `pack`
+// (replaces a pass over every global slot): z = sum / owners for the block's
+// own slots, this block's share of the dual residual (admm.cpp:183-198; each
+// slot counted by its lowest owner only, summed across ranks with the primal
+// partials) and of the flip count, z_prev := z, and the worker half of
+// apply_broadcast (trainer.cpp:186-222): x_hat = relaxed(x, anchor) WITHOUT the
+// sign flip, u += x_hat - z, reset flipped / listed slots, anchor := z, plus
+// the primal residual partial on the raw x (admm.cpp:151-165).
+template <int D>
+__global__ __launch_bounds__(256, 2) void unpack_own_kernel(const float* __restrict__ x, size_t cap,
+                                                         const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ slots,
+                                                         const uint8_t* __restrict__ first, size_t ns, size_t S,
+                                                         const float* __restrict__ pack,
+                                                         const uint32_t* __restrict__ owners,
+                                                         float* __restrict__ zprev, uint8_t* __restrict__ in_zprev,
+                                                         const float* __restrict__ rho,
+                                                         const uint8_t* __restrict__ slot_reset, float alpha, int relax,
+                                                         float* __restrict__ z, float* __restrict__ u,
+                                                         double* __restrict__ scal) {
+    __shared__ double s_red[8];
+    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    double p2 = 0.0, d2 = 0.0, flips = 0.0;
+    if (j < ns) {
+        const uint32_t r = rows[j], s = slots[j];
+        // every load of the row first (one round trip; the loop below then has no
+        // load-after-store ordering to respect)
+        float pk[D], zp[D], xv[D], za[D], uv[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            pk[c] = pack[c * S + s];
+            zp[c] = zprev[c * S + s];
+            xv[c] = x[c * cap + r];
+            za[c] = z[c * ns + j];
+            uv[c] = u[c * ns + j];
+        }
+        const bool lead = first[j] != 0;
+        const float inv = 1.0f / static_cast<float>(owners[s]);
+        const bool had = in_zprev[s] != 0;
+        const bool flipped = pack[static_cast<size_t>(D) * S + s] > 0.f;
+        const bool reset = flipped || (slot_reset && slot_reset[s]);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const float zv = pk[c] * inv;
+            if (lead && had) {
+                const double dv = static_cast<double>(rho[c]) * (static_cast<double>(zv) - zp[c]);
+                d2 += dv * dv;
+            }
+            const float xh = relaxed(xv[c], za[c], alpha, relax != 0);
+            const double dr = static_cast<double>(xv[c]) - zv;
+            p2 += dr * dr;
+            uv[c] = reset ? 0.f : uv[c] + (xh - zv);
+            zp[c] = zv;
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            zprev[c * S + s] = zp[c];
+            z[c * ns + j] = zp[c];
+            u[c * ns + j] = uv[c];
+        }
+        in_zprev[s] = 1;
+        flips = lead && flipped ? 1.0 : 0.0;
+    }
+    block_add(p2, &scal[0], s_red);
+    __syncthreads();
+    block_add(d2, &scal[1], s_red);
+    __syncthreads();
+    block_add(flips, &scal[2], s_red);
+}
+
+// z for every slot from the reduced sums (consensus download, diagnostics).
+__global__ void slots_from_sums_kernel(const float* __restrict__ pack, int D, size_t S,
+                                       const uint32_t* __restrict__ owners, float* __restrict__ zslot) {
+    const size_t s = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (s >= S) return;
+    const float inv = 1.0f / static_cast<float>(owners[s]);
+    for (int c = 0; c < D; ++c) zslot[c * S + s] = pack[c * S + s] * inv;
 }
 
 // Diagnostics: duals packed by slot for the dual-mean check (runtime.cpp:572-606),
@@ -233,31 +289,38 @@ void round_pack_q(Ctx* c) {
 void round_pack_main(Ctx* c, double alpha, bool relax) {
     BSG_CUDA(cudaMemsetAsync(c->pack, 0, (c->D + 1) * c->n_slots * sizeof(float), c->stream));
     if (c->n_shared == 0) return;
-    pack_main_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(
-        c->x, c->cap, c->D, c->sh_rows, c->sh_slots, c->sh_first, c->n_shared, c->n_slots, c->qref, c->zprev,
-        c->in_zprev, static_cast<float>(alpha), relax ? 1 : 0, c->pack);
+    auto kern = c->fd == 3 ? pack_main_kernel<14> : pack_main_kernel<23>;
+    kern<<<grid_for(c->n_shared), 256, 0, c->stream>>>(c->x, c->cap, c->sh_rows, c->sh_slots, c->sh_first,
+                                                       c->n_shared, c->n_slots, c->qref, c->zprev, c->in_zprev,
+                                                       static_cast<float>(alpha), relax ? 1 : 0, c->pack);
     BSG_LAUNCHED(c);
 }
 
-// After the reduction of `pack`: slots, dual update, residual partials.
+// After the reduction of `pack`: z of the own slots, dual update, residual partials.
 void round_unpack(Ctx* c, double alpha, bool relax, const uint8_t* reset_slots_dev, size_t n_reset, bool diag) {
     (void)n_reset;
-    (void)diag;
     BSG_CUDA(cudaMemsetAsync(c->round_scalars, 0, 8 * sizeof(double), c->stream));
-    const float* rho_dev = c->rho_dev;  // rho in force this round (the dual residual weights)
-    if (c->n_slots > 0) {
-        unpack_slots_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(c->pack, c->D, c->n_slots, c->slot_owners,
-                                                                         c->zslot, c->zprev, c->in_zprev, rho_dev,
-                                                                         c->round_scalars);
-        BSG_LAUNCHED(c);
-    }
     if (c->n_shared > 0) {
-        dual_update_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(
-            c->x, c->cap, c->D, c->sh_rows, c->sh_slots, c->n_shared, c->n_slots, c->pack, c->zslot,
-            reset_slots_dev ? c->slot_reset : nullptr, static_cast<float>(alpha), relax ? 1 : 0, c->z, c->u,
-            c->round_scalars);
+        auto kern = c->fd == 3 ? unpack_own_kernel<14> : unpack_own_kernel<23>;
+        kern<<<grid_for(c->n_shared), 256, 0, c->stream>>>(
+            c->x, c->cap, c->sh_rows, c->sh_slots, c->sh_first, c->n_shared, c->n_slots, c->pack, c->slot_owners,
+            c->zprev, c->in_zprev, c->rho_dev, reset_slots_dev ? c->slot_reset : nullptr, static_cast<float>(alpha),
+            relax ? 1 : 0, c->z, c->u, c->round_scalars);
         BSG_LAUNCHED(c);
     }
+    c->zslot_from_pack = true;
+    if (diag) round_slots_from_sums(c);  // diagnostics reuse `pack`
+}
+
+// zslot (z of every slot) from the reduced sums still held in `pack`.
+void round_slots_from_sums(Ctx* c) {
+    if (!c->zslot_from_pack) return;
+    if (c->n_slots > 0) {
+        slots_from_sums_kernel<<<grid_for(c->n_slots), 256, 0, c->stream>>>(c->pack, c->D, c->n_slots, c->slot_owners,
+                                                                            c->zslot);
+        BSG_LAUNCHED(c);
+    }
+    c->zslot_from_pack = false;
 }
 
 // apply_broadcast with a host-provided z (trainer.cpp:168-223): zslot holds

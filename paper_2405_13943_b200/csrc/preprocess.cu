@@ -42,6 +42,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  uint64_t* __restrict__ depth_key,
                                                                  uint32_t* __restrict__ tiles,
                                                                  float4* __restrict__ g2d,
+                                                                 double* __restrict__ g2d_wide,
                                                                  StepCounters* __restrict__ counters) {
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint32_t s_count;
@@ -205,8 +206,19 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                     make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(m00), static_cast<float>(m01));
                 rec[3 * static_cast<size_t>(i) + 1] =
                     make_float4(static_cast<float>(m11), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
+                // wide footprint: FP64 gradient slot (see kWideArea)
+                uint32_t wslot = kNoWide;
+                if (static_cast<uint32_t>(x1 - x0 + 1) * static_cast<uint32_t>(y1 - y0 + 1) >= kWideArea) {
+                    const uint32_t w = atomicAdd(&counters->wide, 1u);
+                    if (w < kWideCap) {
+                        wslot = w;
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) g2d_wide[9 * static_cast<size_t>(w) + k] = 0.0;
+                    }
+                }
                 rec[3 * static_cast<size_t>(i) + 2] =
-                    make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23), 0.f);
+                    make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23),
+                                __uint_as_float(wslot));
                 ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
                 const unsigned long long zb = static_cast<unsigned long long>(__double_as_longlong(z));
                 depth_key[i] = zb;
@@ -274,7 +286,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     if (c->n == 0) return;
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     preprocess_kernel<<<blocks, kPreThreads, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
-                                                      c->depth_key, c->tiles, c->g2d, c->counters);
+                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->counters);
     BSG_LAUNCHED(c);
 }
 

@@ -14,14 +14,15 @@ namespace bsg {
 namespace {
 
 // exp(-q/2) as one MUFU.EX2 (ex2.approx.ftz: ~2 ulp; results below 2^-126
-// flush to 0, i.e. alpha < 1e-38) and a 1-MUFU reciprocal, shared by the
-// forward and backward blends so both see bit-identical alphas.
+// flush to 0, i.e. alpha < 1e-38), shared by the forward and backward blends
+// so both see bit-identical alphas.
 constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 * log2(e)
 __device__ __forceinline__ float gauss_weight(float q) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(q * kNegHalfLog2e));
     return y;
 }
+
 __device__ __forceinline__ float fast_rcp(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -303,7 +304,8 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   float bg2, const float* __restrict__ in_T,
                                                                   const uint32_t* __restrict__ in_last,
                                                                   const float* __restrict__ dl_dc,
-                                                                  float4* __restrict__ g2d) {
+                                                                  float4* __restrict__ g2d,
+                                                                  double* __restrict__ g2d_wide) {
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint32_t s_row[kBatch];
     __shared__ uint8_t s_m[kBatch];
@@ -391,8 +393,9 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             const float dx = fx - a.x;
             if (hit0) bwd_step(P0, dx, fy0 - a.y, a, b, c, aclamp, acc);
             if (hit1) bwd_step(P1, dx, fy1 - a.y, a, b, c, aclamp, acc);
+            const uint32_t wslot = __float_as_uint(c.w);  // FP64 slot of a wide splat (kWideArea)
             float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(s_row[sj]));
-            if (__popc(mask) <= 2) {
+            if (__popc(mask) <= 2 && wslot == kNoWide) {
                 if (hit0 || hit1) {
                     atomicAdd(reinterpret_cast<float4*>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
                     atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
@@ -401,7 +404,12 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             } else {
                 const float r = warp_reduce9(acc, lane);
                 const int idx = reduced9_index(lane);
-                if ((lane & 1) == 0 && idx < 9) atomicAdd(dst + idx, r);
+                if ((lane & 1) == 0 && idx < 9) {
+                    if (wslot == kNoWide)
+                        atomicAdd(dst + idx, r);
+                    else
+                        atomicAdd(g2d_wide + 9 * static_cast<size_t>(wslot) + idx, static_cast<double>(r));
+                }
             }
         }
     }
@@ -438,7 +446,7 @@ void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
     blend_bwd_kernel<<<ntiles, kBlendThreads, 0, c->stream>>>(
         c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.alpha_clamp),
-        rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d);
+        rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d, c->g2d_wide);
     BSG_LAUNCHED(c);
 }
 

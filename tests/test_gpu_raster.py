@@ -138,9 +138,11 @@ def test_render_backward_matches_oracle(name, cloud, cam):
     # Splats grazing the near plane (z ~ 0.01, only in the 30-degree aerial
     # cases; the reference has no frustum guard band) fold their image-space
     # gradient through 1/z^2 and 1/z^3 Jacobian terms that cancel to ~1e-5 of
-    # their size, so FP32 accumulation leaves O(1e-2) relative error on their
-    # position/rotation/scale gradients. They are held to 10%; all others to
-    # the 2e-3 norm-wise bar.
+    # their size. Their footprints are wide (>= kWideArea px), so the device
+    # accumulates their image-space gradients in FP64 (deterministic; FP32
+    # atomics gave 2-12% run-to-run); what remains is the FP32 per-pixel
+    # arithmetic, ~4% on their position gradients. They are held to 6%; all
+    # others to the 2e-3 norm-wise bar.
     proj = orc.project(cloud.oracle(), cam, orc.RenderConfig())
     grazing = proj["visible"].astype(bool) & (proj["depth"] < 1.0)
     errs = grad_close({k: (v[~grazing] if k.startswith("g_") else v) for k, v in got.items()},
@@ -151,7 +153,7 @@ def test_render_backward_matches_oracle(name, cloud, cam):
         errs = grad_close({k: (v[grazing] if k.startswith("g_") else v) for k, v in got.items()},
                           {k: (v[grazing] if k.startswith("g_") else v) for k, v in want.items()}, 1e-3)
         for k, e in errs.items():
-            assert e <= 0.1, (k, e)
+            assert e <= 0.06, (k, e)
     # element-wise on the entries that carry the signal (non-grazing rows)
     for k in ("g_pos", "g_rot", "g_ls", "g_feat", "g_op"):
         gk, wk = got[k][~grazing], want[k][~grazing]
