@@ -109,6 +109,25 @@ RenderOutput render(const GaussianCloud& cloud, const CameraView& cam, const Ren
 BackwardOutput render_backward(const GaussianCloud& cloud, const CameraView& cam, const Image& gt,
                                const RenderConfig& cfg = {}, int device = 0);
 
+// metrics.hpp:15-36. psnr is the reference's host formula; evaluate renders
+// and scores on the device (bsg_evaluate). The reference takes a LoadedScene;
+// here its views and images are passed directly (same holdout rule).
+double psnr(const Image& a, const Image& b);
+struct ViewMetrics {
+    uint64_t view_id = 0;
+    double psnr = 0;
+    double ssim = 0;
+};
+struct MetricsReport {
+    std::vector<ViewMetrics> per_view;
+    double mean_psnr = 0;
+    double mean_ssim = 0;
+    size_t gaussian_count = 0;
+};
+MetricsReport evaluate(const GaussianCloud& model, const std::vector<CameraView>& views,
+                       const std::vector<Image>& images, uint32_t holdout_modulus, const RenderConfig& rc = {},
+                       int device = 0);
+
 // trainer.hpp:13-62
 struct LearningRates {
     double position = 1.6e-4, position_decay = 0.01, rotation = 1e-3, log_scale = 5e-3, features = 2.5e-3,

@@ -138,6 +138,16 @@ int bsg_download_moments(bsg_ctx* ctx, double* m, double* v);
 /* Densify statistics (trainer.cpp:284-289): grad_accum n, grad_seen n. */
 int bsg_download_densify_stats(bsg_ctx* ctx, double* grad_accum, uint32_t* grad_seen);
 
+/* evaluate (metrics.cpp:28-51) of the uploaded cloud: renders every view with
+ * index % holdout_modulus == 0 (0: every view) and scores it against gt[i]
+ * (HxWx3 FP64, reference Image layout): PSNR = min(99, 10 log10(1 / mse))
+ * over all channels from an FP64 squared error (metrics.cpp:14-26), and mean
+ * SSIM (ssim.cpp). per_view_* (nullable, capacity n_views) receive the scored
+ * views in order; BSG_ERR_INVALID_ARGUMENT "empty holdout" when none qualifies. */
+int bsg_evaluate(bsg_ctx* ctx, size_t n_views, const bsg_camera* cams, const double* const* gt,
+                 uint32_t holdout_modulus, const bsg_render_config* cfg, double* per_view_psnr, double* per_view_ssim,
+                 size_t* n_scored, double* mean_psnr, double* mean_ssim);
+
 /* ---- consensus (admm.hpp:47-89, trainer.cpp:161-223, runtime.cpp:482-611) */
 /* Shared rows of this block: anchor j is cloud row rows[j] (ascending ids),
  * consensus slot slots[j] in [0, n_slots). slot_owners[s] = number of blocks

@@ -103,6 +103,8 @@ SYMBOLS = [
     ("bsg_cloud_size", _SZ, [_P]),
     ("bsg_download_cloud", ctypes.c_int, [_P, _U64P, _DP, _DP, _DP, _DP, _DP]),
     ("bsg_render", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), ctypes.POINTER(bsg_render_config), _DP, _DP, _U32P]),
+    ("bsg_evaluate", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_DP), ctypes.c_uint32,
+                                    ctypes.POINTER(bsg_render_config), _DP, _DP, _SZP, _DP, _DP]),
     ("bsg_render_backward", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _DP, ctypes.POINTER(bsg_render_config), _DP,
                                             _DP, _DP, _DP, _DP, _DP, _DP, _U8P, _DP]),
     ("bsg_project", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), ctypes.POINTER(bsg_render_config), _U8P, _DP,
@@ -291,6 +293,19 @@ class Block:
         _check(_lib.bsg_render(self.h, ctypes.byref(cam), ctypes.byref(cfg) if cfg else None,
                                _ptr(rgb, ctypes.c_double), _ptr(T, ctypes.c_double), _ptr(n, ctypes.c_uint32)))
         return rgb, T, n
+
+    def evaluate(self, cams, gts, holdout_modulus=8, cfg=None):
+        """evaluate (metrics.cpp:28-51) on the device: per-view PSNR / SSIM of
+        the views with index % holdout_modulus == 0, and their means."""
+        arr = (bsg_camera * len(cams))(*cams)
+        keep = [_f64(g) for g in gts]
+        ptrs = (_DP * len(cams))(*[_ptr(g, ctypes.c_double) for g in keep])
+        p, q = np.zeros(max(len(cams), 1)), np.zeros(max(len(cams), 1))
+        k, mp, ms = ctypes.c_size_t(), ctypes.c_double(), ctypes.c_double()
+        _check(_lib.bsg_evaluate(self.h, len(cams), arr, ptrs, int(holdout_modulus), ctypes.byref(cfg) if cfg else None,
+                                 _ptr(p, ctypes.c_double), _ptr(q, ctypes.c_double), ctypes.byref(k), ctypes.byref(mp),
+                                 ctypes.byref(ms)))
+        return dict(psnr=p[:k.value], ssim=q[:k.value], mean_psnr=mp.value, mean_ssim=ms.value)
 
     def render_backward(self, cam, gt, cfg=None):
         H, W = cam.height, cam.width

@@ -269,6 +269,12 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     c->last_counters.pairs = P;
 }
 
+}  // namespace
+
+void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc) { project_and_bin(c, cam, rc); }
+
+namespace {
+
 float* upload_gt_f64(Ctx* c, const double* gt, size_t px) {
     std::vector<float> h(3 * px);
     for (size_t i = 0; i < 3 * px; ++i) h[i] = static_cast<float>(gt[i]);
@@ -605,6 +611,59 @@ int bsg_render(bsg_ctx* h, const bsg_camera* cam, const bsg_render_config* cfg, 
         collect_stage_times(c);
         if (out_rgb) for (size_t i = 0; i < 3 * px; ++i) out_rgb[i] = rgb[i];
         if (out_T) for (size_t i = 0; i < px; ++i) out_T[i] = T[i];
+    });
+}
+
+int bsg_evaluate(bsg_ctx* h, size_t n_views, const bsg_camera* cams, const double* const* gt, uint32_t holdout_modulus,
+                 const bsg_render_config* cfg, double* per_view_psnr, double* per_view_ssim, size_t* n_scored,
+                 double* mean_psnr, double* mean_ssim) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (n_views && (!cams || !gt)) invalid("null views");
+        bsg_render_config rcfg;
+        if (cfg) rcfg = *cfg; else bsg_default_render_config(&rcfg);
+        use_device(c);
+        const DevRender rc = make_render(rcfg);
+        double* gt_dev = nullptr;
+        double* scratch = nullptr;
+        size_t gt_cap = 0;
+        size_t k = 0;
+        double sp = 0, ss = 0;
+        try {
+            BSG_CUDA(cudaMalloc(&scratch, sizeof(double)));
+            for (size_t i = 0; i < n_views; ++i) {
+                if (holdout_modulus != 0 && i % holdout_modulus != 0) continue;  // metrics.cpp:34
+                check_camera(&cams[i]);
+                if (!gt[i]) invalid("null ground truth");
+                const DevCam dc = make_cam(cams[i]);
+                ensure_image_buffers(c, dc.W, dc.H);
+                const size_t n = 3 * static_cast<size_t>(dc.W) * dc.H;
+                if (n > gt_cap) {
+                    if (gt_dev) cudaFree(gt_dev);
+                    BSG_CUDA(cudaMalloc(&gt_dev, n * sizeof(double)));
+                    gt_cap = n;
+                }
+                BSG_CUDA(cudaMemcpyAsync(gt_dev, gt[i], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                double r[2];
+                eval_view(c, dc, rc, gt_dev, scratch, r);
+                if (per_view_psnr) per_view_psnr[k] = r[0];
+                if (per_view_ssim) per_view_ssim[k] = r[1];
+                sp += r[0];
+                ss += r[1];
+                ++k;
+            }
+        } catch (...) {
+            if (gt_dev) cudaFree(gt_dev);
+            if (scratch) cudaFree(scratch);
+            throw;
+        }
+        if (gt_dev) cudaFree(gt_dev);
+        if (scratch) cudaFree(scratch);
+        if (k == 0) invalid("empty holdout");  // metrics.cpp:44
+        if (n_scored) *n_scored = k;
+        if (mean_psnr) *mean_psnr = sp / static_cast<double>(k);
+        if (mean_ssim) *mean_ssim = ss / static_cast<double>(k);
     });
 }
 

@@ -261,6 +261,10 @@ struct AdamStep {
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
 void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty);
+bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt);
+// K1-K5 for one view (abi.cu), and the evaluation of one holdout view (eval.cu).
+void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc);
+void eval_view(Ctx* c, const DevCam& cam, const DevRender& rc, const double* gt_dev, double* scratch, double out[2]);
 
 // ---- consensus (consensus.cu) ------------------------------------------
 void round_pack_q(Ctx* c);

@@ -250,7 +250,7 @@ bool g_ready[64] = {};
 
 }  // namespace
 
-void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt) {
+void ensure_ssim_ready(Ctx* c) {
     if (!g_ready[c->device]) {
         // ssim_window_1d (ssim.cpp:112-122), computed in FP64 then rounded: must
         // equal the compiled-in taps.
@@ -269,6 +269,10 @@ void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt
                                       static_cast<int>(sizeof(PixSmem))));
         g_ready[c->device] = true;
     }
+}
+
+void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt) {
+    ensure_ssim_ready(c);
     const int W = cam.W, H = cam.H;
     const bool has_ssim = W >= kW && H >= kW;
     const int Wv = W - 2 * kHalf, Hv = H - 2 * kHalf;
@@ -284,6 +288,20 @@ void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt
         c->out_rgb, gt, W, H, c->ssim_f, has_ssim ? 1 : 0, static_cast<float>(rc.lambda / count),
         static_cast<float>(1.0 / (3.0 * W * H)), c->dl_dc, &c->scalars->l1_sum);
     BSG_LAUNCHED(c);
+}
+
+// Windows pass only (mean SSIM into scalars->ssim_sum); false when the image
+// is smaller than the window (ssim.cpp:12-14: SSIM = 1).
+bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt) {
+    const int W = cam.W, H = cam.H;
+    if (W < kW || H < kW) return false;
+    ensure_ssim_ready(c);
+    const int Wv = W - 2 * kHalf, Hv = H - 2 * kHalf;
+    dim3 grid((Wv + kTX - 1) / kTX, (Hv + kTY - 1) / kTY);
+    ssim_windows_kernel<<<grid, kThreads, sizeof(WinSmem), c->stream>>>(c->out_rgb, gt, W, H, c->ssim_f,
+                                                                       &c->scalars->ssim_sum);
+    BSG_LAUNCHED(c);
+    return true;
 }
 
 void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty) {

@@ -254,6 +254,49 @@ RenderOutput render(const GaussianCloud& cloud, const CameraView& cam, const Ren
     return out;
 }
 
+double psnr(const Image& a, const Image& b) {  // metrics.cpp:14-26
+    if (a.width != b.width || a.height != b.height) throw InvalidArgument("image dimensions differ");
+    if (a.data.empty()) throw InvalidArgument("empty image");
+    double acc = 0;
+    for (size_t i = 0; i < a.data.size(); ++i) {
+        const double d = a.data[i] - b.data[i];
+        acc += d * d;
+    }
+    const double mse = acc / static_cast<double>(a.data.size());
+    if (mse <= 0) return 99.0;
+    return std::min(99.0, 10.0 * std::log10(1.0 / mse));
+}
+
+MetricsReport evaluate(const GaussianCloud& model, const std::vector<CameraView>& views,
+                       const std::vector<Image>& images, uint32_t holdout_modulus, const RenderConfig& rc,
+                       int device) {  // metrics.cpp:28-51
+    if (views.size() != images.size()) throw InvalidArgument("image dimension mismatch");
+    bsg_ctx* ctx = t_ctx.get(device, model.feature_dim());
+    upload(ctx, model);
+    std::vector<bsg_camera> cams(views.size());
+    std::vector<const double*> gts(views.size());
+    for (size_t i = 0; i < views.size(); ++i) {
+        if (images[i].width != views[i].width || images[i].height != views[i].height)
+            throw InvalidArgument("image dimension mismatch");
+        cams[i] = to_dev(views[i]);
+        gts[i] = images[i].data.data();
+    }
+    const bsg_render_config dc = to_dev(rc);
+    std::vector<double> p(views.size() + 1), q(views.size() + 1);
+    size_t k = 0;
+    MetricsReport report;
+    check(bsg_evaluate(ctx, views.size(), cams.data(), gts.data(), holdout_modulus, &dc, p.data(), q.data(), &k,
+                       &report.mean_psnr, &report.mean_ssim));
+    size_t j = 0;
+    for (size_t i = 0; i < views.size(); ++i) {
+        if (holdout_modulus != 0 && i % holdout_modulus != 0) continue;
+        report.per_view.push_back(ViewMetrics{views[i].view_id, p[j], q[j]});
+        ++j;
+    }
+    report.gaussian_count = model.size();
+    return report;
+}
+
 BackwardOutput render_backward(const GaussianCloud& cloud, const CameraView& cam, const Image& gt,
                                const RenderConfig& cfg, int device) {
     if (gt.width != cam.width || gt.height != cam.height) throw InvalidArgument("image dimension mismatch");

@@ -53,6 +53,21 @@ int main() {
         RenderOutput out = render(c, axis_camera(100, 8, 17));
         CHECK(out.contributors[8 * 17 + 8] == 3);
     }
+    {  // test_metrics.cpp shape: psnr identities and evaluate's holdout rule on the device
+        GaussianCloud c(kFeatureDimDeg0);
+        push(c, 1, {0, 0, 5}, {0.9, 0.5, 0.25}, 0.8);
+        const CameraView cam = axis_camera(100, 8, 17);
+        const Image rendered = render(c, cam).color;
+        CHECK(psnr(rendered, rendered) == 99.0);
+        Image off = rendered;
+        for (double& v : off.data) v += 0.1;
+        CHECK(std::abs(psnr(rendered, off) - 20.0) < 1e-9);
+        const MetricsReport m = evaluate(c, {cam, cam, cam}, {rendered, off, rendered}, 2);
+        CHECK(m.per_view.size() == 2);  // views 0 and 2
+        CHECK(m.per_view[0].psnr == 99.0 && m.per_view[1].psnr == 99.0);
+        const MetricsReport all = evaluate(c, {cam, cam}, {rendered, off}, 0);
+        CHECK(all.per_view.size() == 2 && std::abs(all.per_view[1].psnr - 20.0) < 1e-3);
+    }
     {  // test_renderer.cpp:373-387 culled rows
         GaussianCloud c(kFeatureDimDeg0);
         push(c, 1, {0, 0, 5}, {0.5, 0.5, 0.5}, 0.7);

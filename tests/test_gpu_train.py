@@ -208,3 +208,28 @@ def test_async_round_overlaps_next_step_exactly():
     ga, gb = a.download_cloud(), b.download_cloud()
     for k in ("pos", "rot", "ls", "feat", "op"):
         np.testing.assert_allclose(gb[k], ga[k], rtol=1e-4, atol=1e-5)
+
+
+def test_evaluate_matches_reference_metrics():
+    """evaluate (metrics.cpp:28-51) on the device: holdout rule, PSNR
+    (metrics.cpp:14-26) and SSIM (ssim.cpp) vs the FP64 oracle rendering."""
+    s, init = toy_scene(size=40)
+    ims = s.images()
+    b = new_block(init)
+    for holdout in (3, 0):
+        got = b.evaluate([dev_cam(v) for v in s.views], ims, holdout_modulus=holdout)
+        idx = [i for i in range(len(s.views)) if holdout == 0 or i % holdout == 0]
+        assert len(got["psnr"]) == len(idx)
+        for k, i in enumerate(idx):
+            r = orc.render(init.oracle(), s.views[i], orc.RenderConfig())[0]
+            assert got["psnr"][k] == pytest.approx(orc.psnr(r, ims[i]), abs=1e-4)
+            assert got["ssim"][k] == pytest.approx(orc.ssim(r, ims[i]), abs=1e-5)
+        assert got["mean_psnr"] == pytest.approx(np.mean(got["psnr"]), rel=1e-12)
+    # identical images are capped at 99 dB
+    r0 = orc.render(init.oracle(), s.views[0], orc.RenderConfig())[0]
+    capped = b.evaluate([dev_cam(s.views[0])], [b.render(dev_cam(s.views[0]))[0]], holdout_modulus=0)
+    assert capped["psnr"][0] == 99.0 and capped["ssim"][0] == pytest.approx(1.0, abs=1e-6)
+    assert np.abs(b.render(dev_cam(s.views[0]))[0] - r0).max() < 1e-4
+    assert len(b.evaluate([dev_cam(s.views[1])], [ims[1]], holdout_modulus=2)["psnr"]) == 1  # index 0 qualifies
+    with pytest.raises(api.InvalidArgument):
+        b.evaluate([], [], holdout_modulus=1)  # metrics.cpp:44 "empty holdout"
