@@ -144,7 +144,7 @@ def build_block(rank, world, n, device, n_views=CFG["views"], constant_gt=False)
     blk.upload_cloud(init["ids"][sel], init["pos"][sel], init["rot"][sel], init["ls"][sel], init["feat"][sel],
                      init["op"][sel])
     blk.set_views(view_cams, gts)
-    blk.trainer_init(api.trainer_config(iterations=30000))
+    blk.trainer_init(api.trainer_config(iterations=30000, densify={"enabled": 0}))
     sids, cnt, _ = plan.shared()
     rows, slots, first = plan.block_shared(rank)
     if world > 1:

@@ -8,7 +8,9 @@
 //    is a row-major std::array<double, 9>.
 //  - BlockTrainer owns a device context; cloud()/duals()/anchor() download.
 //  - Densification (trainer.cpp:301-385) is not on the device path yet
-//    (SURVEY §8(f)1): a TrainerConfig with densify.enabled is rejected.
+//    (SURVEY §8(f)1): densification runs on the device; run_simulated with
+//    K > 1 rejects a schedule that would densify (the master's id bookkeeping,
+//    runtime.cpp:490-518, is SURVEY §8(f)2).
 //  - FP32 device state: results match the FP64 reference within the
 //    tolerances stated in tests/ (integer paths bit-exact).
 #pragma once
@@ -137,7 +139,7 @@ struct AdamParams {
     double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
 };
 struct DensifyConfig {
-    bool enabled = false;  // reference default is true; not on the device path yet
+    bool enabled = true;  // on the device (csrc/densify.cu); run_simulated with K > 1 rejects a run that densifies
     uint32_t interval = 200;
     uint64_t stop_iteration = 0;
     double grad_threshold = 2e-4, prune_opacity = 0.005, split_scale_fraction = 0.01, split_shrink = 1.6;
@@ -192,6 +194,10 @@ public:
     GaussianCloud duals() const;
     GaussianCloud anchor() const;
     const std::vector<uint64_t>& shared_ids() const { return shared_ids_; }
+    // trainer.hpp:137-140: ids removed by densification since the last call, and
+    // the rows it added that are still in the cloud (ascending ids).
+    std::vector<uint64_t> take_removed_ids();
+    GaussianCloud take_new_rows();
     uint64_t iteration() const;
     double last_loss() const { return last_loss_; }
     uint32_t block_id() const { return block_id_; }
@@ -203,6 +209,7 @@ public:
 
 private:
     void install_shared();
+    void refresh_ids();
     uint32_t block_id_;
     TrainerConfig cfg_;
     bsg_ctx* ctx_ = nullptr;

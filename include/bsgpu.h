@@ -64,13 +64,30 @@ typedef struct bsg_render_config {
     double lambda;             /* 0.2 */
 } bsg_render_config;
 
-/* TrainerConfig device subset (trainer.hpp:13-62). Densification is not on
- * the device path yet; the host adapter keeps it off. */
+/* DensifyConfig (trainer.hpp:43-51) plus the BlockTrainer inputs densification
+ * needs: the block id and global initial count of its IdAllocator
+ * (trainer.cpp:55-66; block k hands out [k 2^48, (k+1) 2^48), block 0 starting
+ * past the initial ids). The scene extent (trainer.cpp:153-154) is taken from
+ * the cloud at bsg_trainer_init. */
+typedef struct bsg_densify_config {
+    int enabled;                  /* 1 */
+    uint32_t interval;            /* 200 */
+    uint64_t stop_iteration;      /* 0 resolves to 60% of iterations */
+    double grad_threshold;        /* 2e-4, mean screen-space gradient norm */
+    double prune_opacity;         /* 0.005 */
+    double split_scale_fraction;  /* 0.01 of the scene extent: clone below, split above */
+    double split_shrink;          /* 1.6 */
+    uint32_t block_id;            /* 0 */
+    uint64_t global_initial_count;/* 0: the uploaded cloud's size */
+} bsg_densify_config;
+
+/* TrainerConfig device subset (trainer.hpp:13-62). */
 typedef struct bsg_trainer_config {
     uint64_t iterations;
     double lr_position, lr_position_decay, lr_rotation, lr_log_scale, lr_features, lr_opacity;
     double beta1, beta2, eps;
     bsg_render_config render;
+    bsg_densify_config densify;
 } bsg_trainer_config;
 
 /* PropertyPenalties (admm.hpp:12-18). */
@@ -137,6 +154,14 @@ uint64_t bsg_iteration(const bsg_ctx* ctx);
 int bsg_download_moments(bsg_ctx* ctx, double* m, double* v);
 /* Densify statistics (trainer.cpp:284-289): grad_accum n, grad_seen n. */
 int bsg_download_densify_stats(bsg_ctx* ctx, double* grad_accum, uint32_t* grad_seen);
+/* take_removed_ids / take_new_rows (trainer.hpp:137-140): ids removed by
+ * densification since the last call (pruned rows and split parents, in
+ * removal order), and ids of rows it added that are still in the cloud
+ * (ascending); both lists are cleared. Query sizes with a null output. */
+int bsg_take_removed_ids(bsg_ctx* ctx, uint64_t* out, size_t capacity, size_t* n);
+int bsg_take_new_ids(bsg_ctx* ctx, uint64_t* out, size_t capacity, size_t* n);
+/* Shared ids of this block after densification pruned some (ascending). */
+int bsg_shared_ids(bsg_ctx* ctx, uint64_t* out, size_t capacity, size_t* n);
 
 /* evaluate (metrics.cpp:28-51) of the uploaded cloud: renders every view with
  * index % holdout_modulus == 0 (0: every view) and scores it against gt[i]

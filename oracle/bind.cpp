@@ -253,6 +253,16 @@ PYBIND11_MODULE(_oracle, m) {
                       [](TrainerConfig& c, bool v) { c.densify.enabled = v; })
         .def_property("densify_interval", [](const TrainerConfig& c) { return c.densify.interval; },
                       [](TrainerConfig& c, uint32_t v) { c.densify.interval = v; })
+        .def_property("densify_stop_iteration", [](const TrainerConfig& c) { return c.densify.stop_iteration; },
+                      [](TrainerConfig& c, uint64_t v) { c.densify.stop_iteration = v; })
+        .def_property("densify_grad_threshold", [](const TrainerConfig& c) { return c.densify.grad_threshold; },
+                      [](TrainerConfig& c, double v) { c.densify.grad_threshold = v; })
+        .def_property("densify_prune_opacity", [](const TrainerConfig& c) { return c.densify.prune_opacity; },
+                      [](TrainerConfig& c, double v) { c.densify.prune_opacity = v; })
+        .def_property("densify_split_scale_fraction", [](const TrainerConfig& c) { return c.densify.split_scale_fraction; },
+                      [](TrainerConfig& c, double v) { c.densify.split_scale_fraction = v; })
+        .def_property("densify_split_shrink", [](const TrainerConfig& c) { return c.densify.split_shrink; },
+                      [](TrainerConfig& c, double v) { c.densify.split_shrink = v; })
         .def_property("lr", [](const TrainerConfig& c) {
             return std::array<double, 6>{c.lr.position, c.lr.position_decay, c.lr.rotation, c.lr.log_scale, c.lr.features, c.lr.opacity}; },
                       [](TrainerConfig& c, std::array<double, 6> v) {
@@ -292,7 +302,9 @@ PYBIND11_MODULE(_oracle, m) {
         .def("grad_accum", [](PyTrainer& p) { return p.t->grad_accum(); })
         .def("grad_seen", [](PyTrainer& p) { return p.t->grad_seen(); })
         .def("moments", [](PyTrainer& p, int which) { return p.t->moments(which); })
-        .def("adam_steps", [](PyTrainer& p) { return p.t->adam_steps(); });
+        .def("adam_steps", [](PyTrainer& p) { return p.t->adam_steps(); })
+        .def("take_removed_ids", [](PyTrainer& p) { return p.t->take_removed_ids(); })
+        .def("take_new_rows", [](PyTrainer& p) { return p.t->take_new_rows(); });
 
     // View order exactly as BlockTrainer draws it (trainer.cpp:250-252).
     m.def("view_sequence", [](uint64_t seed, uint32_t block_id, size_t n_views, size_t n_steps) {

@@ -39,12 +39,19 @@ class bsg_render_config(ctypes.Structure):
                 ("background", ctypes.c_double * 3), ("lambda_", ctypes.c_double)]
 
 
+class bsg_densify_config(ctypes.Structure):
+    _fields_ = [("enabled", ctypes.c_int), ("interval", ctypes.c_uint32), ("stop_iteration", ctypes.c_uint64),
+                ("grad_threshold", ctypes.c_double), ("prune_opacity", ctypes.c_double),
+                ("split_scale_fraction", ctypes.c_double), ("split_shrink", ctypes.c_double),
+                ("block_id", ctypes.c_uint32), ("global_initial_count", ctypes.c_uint64)]
+
+
 class bsg_trainer_config(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_uint64), ("lr_position", ctypes.c_double),
                 ("lr_position_decay", ctypes.c_double), ("lr_rotation", ctypes.c_double),
                 ("lr_log_scale", ctypes.c_double), ("lr_features", ctypes.c_double), ("lr_opacity", ctypes.c_double),
                 ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("eps", ctypes.c_double),
-                ("render", bsg_render_config)]
+                ("render", bsg_render_config), ("densify", bsg_densify_config)]
 
 
 class bsg_penalties(ctypes.Structure):
@@ -116,6 +123,9 @@ SYMBOLS = [
     ("bsg_train_step_host", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _FP, _DP]),
     ("bsg_iteration", ctypes.c_uint64, [_P]),
     ("bsg_download_moments", ctypes.c_int, [_P, _DP, _DP]),
+    ("bsg_take_removed_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
+    ("bsg_take_new_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
+    ("bsg_shared_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
     ("bsg_download_densify_stats", ctypes.c_int, [_P, _DP, _U32P]),
     ("bsg_set_shared", ctypes.c_int, [_P, _SZ, _U32P, _U32P, _U8P, _SZ, _U32P]),
     ("bsg_set_anchor", ctypes.c_int, [_P, _DP, _DP, ctypes.POINTER(bsg_penalties)]),
@@ -217,12 +227,16 @@ def render_config(**kw):
     return r
 
 
-def trainer_config(**kw):
+def trainer_config(densify=None, **kw):
+    """TrainerConfig defaults (trainer.hpp:13-62); densify: dict of
+    DensifyConfig fields (e.g. {"enabled": 0})."""
     load_library()
     t = bsg_trainer_config()
     _lib.bsg_default_trainer_config(ctypes.byref(t))
     for k, v in kw.items():
         setattr(t, k, v)
+    for k, v in (densify or {}).items():
+        setattr(t.densify, k, v)
     return t
 
 
@@ -250,9 +264,14 @@ class Block:
         h = ctypes.c_void_p()
         _check(_lib.bsg_create(device, feature_dim, ctypes.byref(h)))
         self.h = h
-        self.n = 0
+        self._n = 0
         self.n_shared = 0
         self.n_slots = 0
+
+    @property
+    def n(self):
+        """Rows in the device cloud (changes when densification runs)."""
+        return int(_lib.bsg_cloud_size(self.h)) if self.h else self._n
 
     def close(self):
         if self.h:
@@ -274,7 +293,7 @@ class Block:
         _check(_lib.bsg_upload_cloud(self.h, n, _ptr(ids, ctypes.c_uint64), _ptr(pos, ctypes.c_double),
                                      _ptr(rot, ctypes.c_double), _ptr(ls, ctypes.c_double),
                                      _ptr(feat, ctypes.c_double), _ptr(op, ctypes.c_double)))
-        self.n = n
+        self._n = n
 
     def download_cloud(self):
         n = self.n
@@ -373,6 +392,22 @@ class Block:
         m, v = np.zeros((self.D, self.n)), np.zeros((self.D, self.n))
         _check(_lib.bsg_download_moments(self.h, _ptr(m, ctypes.c_double), _ptr(v, ctypes.c_double)))
         return m, v
+
+    def _id_list(self, fn):
+        n = ctypes.c_size_t()
+        _check(fn(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint64)
+        _check(fn(self.h, _ptr(out, ctypes.c_uint64), len(out), ctypes.byref(n)))
+        return out[:n.value]
+
+    def take_removed_ids(self):
+        return self._id_list(_lib.bsg_take_removed_ids)
+
+    def take_new_ids(self):
+        return self._id_list(_lib.bsg_take_new_ids)
+
+    def shared_ids(self):
+        return self._id_list(_lib.bsg_shared_ids)
 
     def densify_stats(self):
         a, s = np.zeros(self.n), np.zeros(self.n, np.uint32)

@@ -112,23 +112,7 @@ void alloc_rows(Ctx* c, size_t n) {
     dev_alloc(&c->x, c->D * cap);
     dev_alloc(&c->m, c->D * cap);
     dev_alloc(&c->v, c->D * cap);
-    dev_alloc(&c->grad_accum, cap);
-    dev_alloc(&c->grad_seen, cap);
-    dev_alloc(&c->rec, 3 * cap);
-    dev_alloc(&c->depth_key, cap);
-    dev_alloc(&c->tiles, cap);
-    dev_alloc(&c->g2d, 3 * cap);
-    dev_alloc(&c->gbuf, c->D * cap);
-    dev_alloc(&c->vis_mask, cap / 32);
-    dev_alloc(&c->sh_mask, cap / 32);
-    dev_alloc(&c->sh_prefix, cap / 32);
-    dev_alloc(&c->vkey[0], cap);
-    dev_alloc(&c->vkey[1], cap);
-    dev_alloc(&c->vrow[0], cap);
-    dev_alloc(&c->vrow[1], cap);
-    dev_alloc(&c->poff, cap);
-    dev_alloc(&c->vis_rows, cap);
-    c->cap = cap;
+    alloc_row_scratch(c, cap);
 }
 
 // Host FP64 reference layout -> device FP32 [D][cap].
@@ -144,6 +128,19 @@ void upload_params(Ctx* c, const double* pos, const double* rot, const double* l
         h[op_comp(c->fd) * cap + i] = static_cast<float>(op[i]);
     }
     BSG_CUDA(cudaMemcpyAsync(c->x, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    // scene extent of the (FP32-stored) positions: |tight_aabb extent| (trainer.cpp:153-154)
+    if (c->n) {
+        double lo[3], hi[3];
+        for (int k = 0; k < 3; ++k) lo[k] = hi[k] = h[(kPos + k) * cap];
+        for (size_t i = 0; i < c->n; ++i)
+            for (int k = 0; k < 3; ++k) {
+                const double v = h[(kPos + k) * cap + i];
+                lo[k] = std::min(lo[k], v);
+                hi[k] = std::max(hi[k], v);
+            }
+        const double e0 = hi[0] - lo[0], e1 = hi[1] - lo[1], e2 = hi[2] - lo[2];
+        c->scene_extent = std::max(std::sqrt((e0 * e0 + e1 * e1) + e2 * e2), 1e-9);
+    }
     BSG_CUDA(cudaStreamSynchronize(c->stream));
 }
 
@@ -272,6 +269,40 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
 }  // namespace
 
 void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc) { project_and_bin(c, cam, rc); }
+
+void alloc_row_scratch(Ctx* c, size_t cap) {
+    dev_alloc(&c->grad_accum, cap);
+    dev_alloc(&c->grad_seen, cap);
+    dev_alloc(&c->rec, 3 * cap);
+    dev_alloc(&c->depth_key, cap);
+    dev_alloc(&c->tiles, cap);
+    dev_alloc(&c->g2d, 3 * cap);
+    dev_alloc(&c->gbuf, c->D * cap);
+    dev_alloc(&c->vis_mask, cap / 32);
+    dev_alloc(&c->sh_mask, cap / 32);
+    dev_alloc(&c->sh_prefix, cap / 32);
+    dev_alloc(&c->vkey[0], cap);
+    dev_alloc(&c->vkey[1], cap);
+    dev_alloc(&c->vrow[0], cap);
+    dev_alloc(&c->vrow[1], cap);
+    dev_alloc(&c->poff, cap);
+    dev_alloc(&c->vis_rows, cap);
+    c->cap = cap;
+}
+
+// Anchor index of a row = its rank among the (ascending) shared rows: 1 bit per
+// row + shared rows before each 32-row word (read by the Adam kernels).
+void install_shared_masks(Ctx* c) {
+    std::vector<uint32_t> mask(c->cap / 32, 0), prefix(c->cap / 32, 0);
+    for (uint32_t r : c->sh_rows_host) mask[r / 32] |= 1u << (r % 32);
+    uint32_t run = 0;
+    for (size_t w = 0; w < mask.size(); ++w) {
+        prefix[w] = run;
+        run += static_cast<uint32_t>(__builtin_popcount(mask[w]));
+    }
+    BSG_CUDA(cudaMemcpy(c->sh_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice));
+    BSG_CUDA(cudaMemcpy(c->sh_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice));
+}
 
 namespace {
 
@@ -463,6 +494,15 @@ void bsg_default_trainer_config(bsg_trainer_config* o) {
     o->beta2 = 0.999;
     o->eps = 1e-8;
     bsg_default_render_config(&o->render);
+    o->densify.enabled = 1;  // trainer.hpp:43-51
+    o->densify.interval = 200;
+    o->densify.stop_iteration = 0;
+    o->densify.grad_threshold = 2e-4;
+    o->densify.prune_opacity = 0.005;
+    o->densify.split_scale_fraction = 0.01;
+    o->densify.split_shrink = 1.6;
+    o->densify.block_id = 0;
+    o->densify.global_initial_count = 0;
 }
 
 void bsg_default_penalties(bsg_penalties* o) {
@@ -572,6 +612,8 @@ int bsg_download_cloud(bsg_ctx* h, uint64_t* ids, double* pos, double* rot, doub
         if (!c) invalid("null context");
         use_device(c);
         const size_t n = c->n, cap = c->cap;
+        if (ids) std::copy(c->ids.begin(), c->ids.end(), ids);
+        if (!pos && !rot && !ls && !feat && !op) return;  // ids only
         std::vector<float> hx(static_cast<size_t>(c->D) * cap);
         BSG_CUDA(cudaMemcpyAsync(hx.data(), c->x, hx.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
@@ -835,6 +877,14 @@ int bsg_trainer_init(bsg_ctx* h, const bsg_trainer_config* cfg) {
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->adam_t = 0;
         c->iteration = 0;
+        bsg_densify_config& d = c->tcfg.densify;
+        if (d.stop_iteration == 0) d.stop_iteration = (c->tcfg.iterations * 6) / 10;  // trainer.cpp:148-149
+        if (d.enabled && d.interval == 0) invalid("densify interval 0");
+        const uint64_t initial = d.global_initial_count ? d.global_initial_count : c->n;
+        c->alloc_next = (static_cast<uint64_t>(d.block_id) << 48) + (d.block_id == 0 ? initial : 0);  // trainer.cpp:55-61
+        c->alloc_end = (static_cast<uint64_t>(d.block_id) + 1) << 48;
+        c->removed_ids.clear();
+        c->new_ids.clear();
         c->trainer_ready = true;
     });
 }
@@ -851,6 +901,7 @@ int bsg_train_steps(bsg_ctx* h, size_t n, const uint32_t* view_seq, double* loss
             const uint32_t vi = view_seq[k];
             if (vi >= c->view_cams.size()) invalid("view index out of range");
             train_one(c, c->view_cams[vi], c->view_gt[vi], c->losses_dev + 3 * k);
+            maybe_densify(c);
         }
         if (losses && n) {
             std::vector<double> l(3 * n);
@@ -879,6 +930,7 @@ int bsg_train_step_host(bsg_ctx* h, const bsg_camera* cam, const float* gt_host,
                                  c->copy_stream));
         BSG_CUDA(cudaEventRecord(c->gt_ready, c->copy_stream));
         train_one(c, *cam, c->gt_stage, c->losses_dev, c->gt_ready);
+        maybe_densify(c);
         double l3[3];
         BSG_CUDA(cudaMemcpyAsync(l3, c->losses_dev, sizeof(l3), cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
@@ -920,6 +972,47 @@ int bsg_download_densify_stats(bsg_ctx* h, double* ga, uint32_t* gs) {
     });
 }
 
+int bsg_take_removed_ids(bsg_ctx* h, uint64_t* out, size_t capacity, size_t* n) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !n) invalid("null argument");
+        *n = c->removed_ids.size();
+        if (!out) return;
+        if (capacity < *n) invalid("capacity too small");
+        std::copy(c->removed_ids.begin(), c->removed_ids.end(), out);
+        c->removed_ids.clear();
+    });
+}
+
+int bsg_take_new_ids(bsg_ctx* h, uint64_t* out, size_t capacity, size_t* n) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !n) invalid("null argument");
+        // trainer.cpp take_new_rows: the added ids still in the cloud, ascending
+        std::vector<uint64_t> live;
+        std::vector<uint64_t> sorted = c->new_ids;
+        std::sort(sorted.begin(), sorted.end());
+        for (uint64_t id : sorted)
+            if (std::binary_search(c->ids.begin(), c->ids.end(), id)) live.push_back(id);
+        *n = live.size();
+        if (!out) return;
+        if (capacity < *n) invalid("capacity too small");
+        std::copy(live.begin(), live.end(), out);
+        c->new_ids.clear();
+    });
+}
+
+int bsg_shared_ids(bsg_ctx* h, uint64_t* out, size_t capacity, size_t* n) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !n) invalid("null argument");
+        *n = c->sh_rows_host.size();
+        if (!out) return;
+        if (capacity < *n) invalid("capacity too small");
+        for (size_t j = 0; j < *n; ++j) out[j] = c->ids[c->sh_rows_host[j]];
+    });
+}
+
 int bsg_set_shared(bsg_ctx* h, size_t ns, const uint32_t* rows, const uint32_t* slots, const uint8_t* first,
                    size_t n_slots, const uint32_t* owners) {
     return guarded([&] {
@@ -953,16 +1046,10 @@ int bsg_set_shared(bsg_ctx* h, size_t ns, const uint32_t* rows, const uint32_t* 
             BSG_CUDA(cudaMemcpy(c->sh_first, first, ns, cudaMemcpyHostToDevice));
         }
         if (n_slots) BSG_CUDA(cudaMemcpy(c->slot_owners, owners, n_slots * 4, cudaMemcpyHostToDevice));
-        // anchor index of a row = its rank among the (ascending) shared rows
-        std::vector<uint32_t> mask(c->cap / 32, 0), prefix(c->cap / 32, 0);
-        for (size_t j = 0; j < ns; ++j) mask[rows[j] / 32] |= 1u << (rows[j] % 32);
-        uint32_t run = 0;
-        for (size_t w = 0; w < mask.size(); ++w) {
-            prefix[w] = run;
-            run += static_cast<uint32_t>(__builtin_popcount(mask[w]));
-        }
-        BSG_CUDA(cudaMemcpy(c->sh_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice));
-        BSG_CUDA(cudaMemcpy(c->sh_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice));
+        c->sh_rows_host.assign(rows, rows + ns);
+        c->sh_slots_host.assign(slots, slots + ns);
+        c->sh_first_host.assign(first, first + ns);
+        install_shared_masks(c);
         BSG_CUDA(cudaMemset(c->in_zprev, 0, std::max<size_t>(n_slots, 1)));
         c->anchored = false;
     });

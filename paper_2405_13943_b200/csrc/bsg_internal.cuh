@@ -55,7 +55,9 @@ struct StepCounters {
     uint32_t overflow;  // a run of equal 32-bit depth keys too long for the fix-up
     uint32_t visible_pre;  // visible count as seen by the preprocess (sizes the depth key)
     uint32_t wide;         // wide splats given an FP64 gradient slot this step
-    uint32_t pad2;
+    uint32_t dens_keep;    // densify: surviving rows
+    uint32_t dens_children;// densify: added rows
+    uint32_t pad3;
     unsigned long long zmin_inv;  // ~bits of the smallest visible FP64 depth (atomicMax of the complement)
     unsigned long long zmax;      // bits of the largest visible FP64 depth
     uint32_t depth_hist[8][256];  // digit histograms of the visible depth keys (filled by the compaction)
@@ -154,6 +156,12 @@ struct Ctx {
     bsg_trainer_config tcfg{};
     uint64_t iteration = 0;
     uint64_t adam_t = 0;
+    // densification (trainer.cpp:301-385)
+    double scene_extent = 1e-9;
+    uint64_t alloc_next = 0, alloc_end = 0;  // IdAllocator
+    std::vector<uint64_t> removed_ids, new_ids;
+    std::vector<uint32_t> sh_rows_host, sh_slots_host;  // host copies of the shared bookkeeping
+    std::vector<uint8_t> sh_first_host;
 
     // consensus (per block)
     size_t n_shared = 0, n_slots = 0;
@@ -265,6 +273,13 @@ bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt);
 // K1-K5 for one view (abi.cu), and the evaluation of one holdout view (eval.cu).
 void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc);
 void eval_view(Ctx* c, const DevCam& cam, const DevRender& rc, const double* gt_dev, double* scratch, double out[2]);
+
+// ---- densification (densify.cu) ----------------------------------------
+// maybe_densify (trainer.cpp:301-385) after the step that made c->iteration.
+void maybe_densify(Ctx* c);
+// (Re)allocation of the per-row arrays for `cap` rows (x, m, v untouched).
+void alloc_row_scratch(Ctx* c, size_t cap);
+void install_shared_masks(Ctx* c);
 
 // ---- consensus (consensus.cu) ------------------------------------------
 void round_pack_q(Ctx* c);

@@ -60,6 +60,13 @@ bsg_trainer_config to_dev(const TrainerConfig& t) {
     d.beta2 = t.adam.beta2;
     d.eps = t.adam.eps;
     d.render = to_dev(t.render);
+    d.densify.enabled = t.densify.enabled ? 1 : 0;  // trainer.hpp:43-51
+    d.densify.interval = t.densify.interval;
+    d.densify.stop_iteration = t.densify.stop_iteration;
+    d.densify.grad_threshold = t.densify.grad_threshold;
+    d.densify.prune_opacity = t.densify.prune_opacity;
+    d.densify.split_scale_fraction = t.densify.split_scale_fraction;
+    d.densify.split_shrink = t.densify.split_shrink;
     return d;
 }
 
@@ -344,11 +351,8 @@ BlockTrainer::BlockTrainer(uint32_t block_id, GaussianCloud initial, std::vector
                            int device)
     : block_id_(block_id), cfg_(cfg), fd_(initial.feature_dim()), views_(std::move(views)),
       shared_ids_(std::move(shared_ids)) {
-    (void)global_initial_count;  // id allocation belongs to densification (trainer.cpp:55-66)
     if (views_.empty()) throw InvalidArgument("trainer needs at least one view");
     if (!initial.check_invariants()) throw InvalidArgument("initial cloud ids not ascending");
-    if (cfg_.densify.enabled)
-        throw InvalidArgument("densification is not on the device path yet (SURVEY 8(f)1); set densify.enabled = false");
     check(bsg_create(device, fd_, &ctx_));
     ids_ = initial.ids;
     upload(ctx_, initial);
@@ -362,7 +366,9 @@ BlockTrainer::BlockTrainer(uint32_t block_id, GaussianCloud initial, std::vector
         gts.push_back(v.image->data.data());
     }
     check(bsg_set_views(ctx_, cams.size(), cams.data(), gts.data()));
-    const bsg_trainer_config tc = to_dev(cfg_);
+    bsg_trainer_config tc = to_dev(cfg_);
+    tc.densify.block_id = block_id;  // IdAllocator::for_block (trainer.cpp:55-61)
+    tc.densify.global_initial_count = global_initial_count;
     check(bsg_trainer_init(ctx_, &tc));
     // trainer.cpp:116-118,135-159
     rng_ = new std::mt19937_64(cfg_.seed ^ (0x9e3779b97f4a7c15ull * (static_cast<uint64_t>(block_id) + 1)));
@@ -370,6 +376,9 @@ BlockTrainer::BlockTrainer(uint32_t block_id, GaussianCloud initial, std::vector
     for (size_t i = 0; i < view_order_.size(); ++i) view_order_[i] = i;
     for (uint64_t id : shared_ids_)
         if (std::find(ids_.begin(), ids_.end(), id) == ids_.end()) throw InvalidArgument("shared rows missing from cloud");
+    // the device needs the shared set before any anchor: densification buds
+    // shared rows instead of splitting them (trainer.cpp:333-340)
+    if (!shared_ids_.empty()) install_shared();
 }
 
 BlockTrainer::BlockTrainer(BlockTrainer&& o) noexcept
@@ -402,9 +411,43 @@ void BlockTrainer::run_iterations(uint64_t n) {
         seq[s] = static_cast<uint32_t>(view_order_[view_cursor_]);
         view_cursor_ = (view_cursor_ + 1) % view_order_.size();
     }
+    const uint64_t it0 = bsg_iteration(ctx_);
     std::vector<double> losses(n);
     check(bsg_train_steps(ctx_, n, seq.data(), losses.data()));
     last_loss_ = losses.back();
+    // densification points (trainer.cpp:303-304) crossed by this batch
+    const uint64_t stop = cfg_.densify.stop_iteration ? cfg_.densify.stop_iteration : (cfg_.iterations * 6) / 10;
+    const uint64_t it1 = std::min<uint64_t>(it0 + n, stop), iv = cfg_.densify.interval;
+    if (cfg_.densify.enabled && iv && it1 / iv > it0 / iv) refresh_ids();
+}
+
+// Densification on the device changes rows and ids (trainer.cpp:301-385):
+// re-read the id column and the shared ids that survived.
+void BlockTrainer::refresh_ids() {
+    const size_t n = bsg_cloud_size(ctx_);
+    ids_.resize(n);
+    check(bsg_download_cloud(ctx_, ids_.data(), nullptr, nullptr, nullptr, nullptr, nullptr));
+    size_t ns = 0;
+    check(bsg_shared_ids(ctx_, nullptr, 0, &ns));
+    shared_ids_.resize(ns);
+    check(bsg_shared_ids(ctx_, shared_ids_.data(), ns, &ns));
+    if (slots_.size() != shared_ids_.size()) slots_.clear();
+}
+
+std::vector<uint64_t> BlockTrainer::take_removed_ids() {  // trainer.cpp take_removed_ids
+    size_t n = 0;
+    check(bsg_take_removed_ids(ctx_, nullptr, 0, &n));
+    std::vector<uint64_t> out(n);
+    check(bsg_take_removed_ids(ctx_, out.data(), n, &n));
+    return out;
+}
+
+GaussianCloud BlockTrainer::take_new_rows() {  // trainer.cpp take_new_rows
+    size_t n = 0;
+    check(bsg_take_new_ids(ctx_, nullptr, 0, &n));
+    std::vector<uint64_t> ids(n);
+    check(bsg_take_new_ids(ctx_, ids.data(), n, &n));
+    return slice_by_ids(cloud(), ids);
 }
 
 void BlockTrainer::install_shared() {
@@ -566,6 +609,14 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
     const auto K = static_cast<uint32_t>(plan.shards.size());
     if (K == 0) throw InvalidArgument("plan has no shards");
     if (devices.empty()) throw InvalidArgument("no devices");
+    {
+        // the master's bookkeeping of removed / new ids (runtime.cpp:490-518) is
+        // not on this path yet: refuse a K > 1 schedule that densifies
+        const DensifyConfig& d = trainer.densify;
+        const uint64_t stop = d.stop_iteration ? d.stop_iteration : (trainer.iterations * 6) / 10;
+        if (K > 1 && d.enabled && d.interval && d.interval <= stop)
+            throw InvalidArgument("run_simulated with K > 1 and densification is not supported on the device path");
+    }
     const int fd = plan.init_cloud.feature_dim(), D = 11 + fd;
     std::vector<BlockTrainer> tr;
     tr.reserve(K);

@@ -54,6 +54,13 @@ int bsg_run_simulated(int fd, size_t n, const uint64_t* ids, const double* pos, 
         t.render.sigma_extent = tc->render.sigma_extent;
         for (int k = 0; k < 3; ++k) t.render.background[k] = tc->render.background[k];
         t.render.lambda = tc->render.lambda;
+        t.densify.enabled = tc->densify.enabled != 0;
+        t.densify.interval = tc->densify.interval;
+        t.densify.stop_iteration = tc->densify.stop_iteration;
+        t.densify.grad_threshold = tc->densify.grad_threshold;
+        t.densify.prune_opacity = tc->densify.prune_opacity;
+        t.densify.split_scale_fraction = tc->densify.split_scale_fraction;
+        t.densify.split_shrink = tc->densify.split_shrink;
         SessionOptions opt;
         opt.total_iterations = so->total_iterations;
         opt.consensus.interval = so->interval;

@@ -37,6 +37,29 @@ static void push(GaussianCloud& c, uint64_t id, Vec3 pos, Vec3 rgb, double opaci
     c.opacity_logits.push_back(logit(opacity));
 }
 
+// test_trainer.cpp:45-70 fixtures
+static GaussianCloud spread_cloud(int n, double log_scale, double opacity0 = 0.5) {
+    GaussianCloud c(kFeatureDimDeg0);
+    for (int i = 0; i < n; ++i) {
+        c.ids.push_back(static_cast<uint64_t>(i));
+        c.positions.insert(c.positions.end(), {i * 5.0 - 2.5 * (n - 1), 0, 5});
+        c.rotations.insert(c.rotations.end(), {1, 0, 0, 0});
+        c.log_scales.insert(c.log_scales.end(), {log_scale, log_scale, log_scale});
+        c.features.insert(c.features.end(), {1.5, 1.0, 0.5});
+        c.opacity_logits.push_back(logit(i == 0 ? opacity0 : 0.5));
+    }
+    return c;
+}
+
+struct ViewHolder {
+    Image img;
+    std::vector<TrainView> views;
+    ViewHolder(uint32_t size, double fill, double f, const Vec3& from) : img(size, size, fill) {
+        const CameraView cam = look_at(from, {0, 0, 5}, {0, 1, 0}, f, f, size / 2.0, size / 2.0, size, size);
+        views.push_back({cam, &img});
+    }
+};
+
 int main() {
     {  // test_renderer.cpp:204-216 single centred splat
         GaussianCloud c(kFeatureDimDeg0);
@@ -109,19 +132,84 @@ int main() {
         CHECK(t.iteration() == 10);
         CHECK(std::isfinite(l0) && std::isfinite(t.last_loss()));
     }
-    {  // densification is rejected loudly, not silently ignored
-        GaussianCloud c(kFeatureDimDeg0);
-        push(c, 0, {0, 0, 5}, {0.5, 0.5, 0.5}, 0.5);
-        Image img(8, 8, 0.0);
+    // test_trainer.cpp:185-273: the reference's densification unit tests
+    // through the device path (csrc/densify.cu)
+    {  // densify prunes transparent gaussians
+        GaussianCloud c = spread_cloud(2, -3.0, 0.001);
+        ViewHolder vh(16, 0.0, 14, {0, 0, -4});
         TrainerConfig cfg;
-        cfg.densify.enabled = true;
-        bool threw = false;
-        try {
-            BlockTrainer t(0, c, {TrainView{axis_camera(10, 4, 8), &img}}, {}, 1, cfg);
-        } catch (const InvalidArgument&) {
-            threw = true;
-        }
-        CHECK(threw);
+        cfg.iterations = 100;
+        cfg.densify.interval = 5;
+        cfg.densify.grad_threshold = 1e9;  // isolate pruning
+        BlockTrainer t(0, c, vh.views, {}, 2, cfg);
+        t.run_iterations(5);
+        CHECK(t.cloud().size() == 1);
+        CHECK(t.cloud().ids == std::vector<uint64_t>{1});
+        CHECK(t.take_removed_ids() == std::vector<uint64_t>{0});
+        CHECK(t.take_new_rows().empty());
+    }
+    {  // densify clones small high-gradient gaussians
+        GaussianCloud c = spread_cloud(2, -6.0);
+        ViewHolder vh(16, 0.9, 14, {0, 0, -4});
+        TrainerConfig cfg;
+        cfg.iterations = 100;
+        cfg.densify.interval = 4;
+        cfg.densify.grad_threshold = 0.0;
+        BlockTrainer t(0, c, vh.views, {}, 2, cfg);
+        t.run_iterations(4);
+        CHECK(t.cloud().size() == 4);
+        CHECK(t.take_removed_ids().empty());
+        CHECK(t.take_new_rows().ids == (std::vector<uint64_t>{2, 3}));
+        CHECK(t.cloud().find(0) != GaussianCloud::npos && t.cloud().find(1) != GaussianCloud::npos);
+    }
+    {  // densify splits large gaussians and replaces the parent
+        GaussianCloud c = spread_cloud(2, 0.0);
+        ViewHolder vh(16, 0.9, 14, {0, 0, -4});
+        TrainerConfig cfg;
+        cfg.iterations = 100;
+        cfg.lr.log_scale = 0.0;  // freeze scales so the shrink factor is exact
+        cfg.densify.interval = 4;
+        cfg.densify.grad_threshold = 0.0;
+        BlockTrainer t(0, c, vh.views, {}, 2, cfg);
+        t.run_iterations(4);
+        CHECK(t.cloud().size() == 4);
+        CHECK(t.take_removed_ids() == (std::vector<uint64_t>{0, 1}));
+        CHECK(t.take_new_rows().ids == (std::vector<uint64_t>{2, 3, 4, 5}));
+        const GaussianCloud m = t.cloud();
+        for (size_t i = 0; i < m.size(); ++i)
+            CHECK(std::abs(m.log_scales[3 * i] - (0.0 - std::log(1.6))) < 1e-6);  // FP32 storage
+    }
+    {  // shared gaussians bud a child and keep their id
+        GaussianCloud c = spread_cloud(2, 0.0);
+        ViewHolder vh(16, 0.9, 14, {0, 0, -4});
+        TrainerConfig cfg;
+        cfg.iterations = 100;
+        cfg.densify.interval = 4;
+        cfg.densify.grad_threshold = 0.0;
+        BlockTrainer t(0, c, vh.views, {0}, 2, cfg);
+        t.run_iterations(4);
+        CHECK(t.cloud().size() == 4);
+        CHECK(t.cloud().find(0) != GaussianCloud::npos);
+        CHECK(t.cloud().find(1) == GaussianCloud::npos);
+        CHECK(t.take_removed_ids() == std::vector<uint64_t>{1});
+        CHECK(t.take_new_rows().size() == 3);
+        CHECK(t.shared_ids() == std::vector<uint64_t>{0});
+    }
+    {  // pruning a shared gaussian also drops its consensus rows
+        GaussianCloud c = spread_cloud(2, -3.0, 0.001);
+        ViewHolder vh(16, 0.0, 14, {0, 0, -4});
+        TrainerConfig cfg;
+        cfg.iterations = 100;
+        cfg.densify.interval = 5;
+        cfg.densify.grad_threshold = 1e9;
+        BlockTrainer t(0, c, vh.views, {0, 1}, 2, cfg);
+        PropertyPenalties rho;
+        t.set_anchor(slice_by_ids(c, {0, 1}), rho);
+        CHECK(t.anchor().size() == 2);
+        t.run_iterations(5);
+        CHECK(t.shared_ids() == std::vector<uint64_t>{1});
+        CHECK(t.anchor().ids == std::vector<uint64_t>{1});
+        CHECK(t.duals().ids == std::vector<uint64_t>{1});
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures;

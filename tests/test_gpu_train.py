@@ -233,3 +233,81 @@ def test_evaluate_matches_reference_metrics():
     assert len(b.evaluate([dev_cam(s.views[1])], [ims[1]], holdout_modulus=2)["psnr"]) == 1  # index 0 qualifies
     with pytest.raises(api.InvalidArgument):
         b.evaluate([], [], holdout_modulus=1)  # metrics.cpp:44 "empty holdout"
+
+
+def _midpoint_threshold(values, q):
+    """A threshold between two neighbouring sorted values near quantile q, so
+    FP32-vs-FP64 differences cannot flip a decision."""
+    v = np.sort(np.asarray(values, np.float64))
+    k = int(np.clip(round(q * (len(v) - 1)), 1, len(v) - 1))
+    gaps = np.diff(v)
+    lo = max(1, k - 3)
+    j = lo + int(np.argmax(gaps[lo - 1:k + 3]))  # widest gap near the quantile
+    return 0.5 * (v[j - 1] + v[j])
+
+
+@pytest.mark.parametrize("shared_every", [0, 4])
+def test_densify_matches_oracle(shared_every):
+    """maybe_densify (trainer.cpp:301-385) on the device: prune / clone / split
+    (non-shared) / bud (shared) decisions, block-disjoint ids, optimizer state
+    compaction and the shared-set shrink, against the oracle trainer."""
+    s, init = toy_scene(gaussians=120, cameras=6, size=40)
+    steps = 6
+    shared = [int(i) for i in init.ids[::shared_every]] if shared_every else []
+    rows = [int(np.searchsorted(init.ids, g)) for g in shared]
+    anchor = HostCloud(init.ids[rows], init.pos[rows], init.rot[rows], init.ls[rows], init.feat[rows], init.op[rows])
+
+    def oracle_trainer(tc):
+        t = orc.BlockTrainer(0, init.oracle(), s.views, s.images(), shared, init.n, tc)
+        if shared:
+            t.set_anchor(anchor.oracle(), orc.Penalties())
+        return t
+
+    # probe the state at the densification point to place every threshold in a gap
+    probe = oracle_trainer(oracle_cfg(30))
+    for _ in range(steps):
+        probe.train_step()
+    ga, gs = np.array(probe.grad_accum()), np.array(probe.grad_seen())
+    pc = HostCloud.from_oracle(probe.cloud())
+    grad_thr = _midpoint_threshold(ga[gs > 0] / gs[gs > 0], 0.5)
+    prune = _midpoint_threshold(1 / (1 + np.exp(-pc.op)), 0.2)
+    lo, hi = init.pos.min(0), init.pos.max(0)
+    extent = np.sqrt(((hi - lo) ** 2).sum())
+    frac = _midpoint_threshold(np.exp(pc.ls).max(1) / extent, 0.5)
+    dens = dict(enabled=1, interval=steps, stop_iteration=steps, grad_threshold=grad_thr, prune_opacity=prune,
+                split_scale_fraction=frac, split_shrink=1.6)
+    tc = oracle_cfg(30)
+    tc.densify_enabled, tc.densify_interval, tc.densify_stop_iteration = True, steps, steps
+    tc.densify_grad_threshold, tc.densify_prune_opacity, tc.densify_split_scale_fraction = grad_thr, prune, frac
+    t = oracle_trainer(tc)
+    n_steps = steps + 3
+    want_losses = [t.train_step() for _ in range(n_steps)]
+    b = new_block(init)
+    b.set_views([dev_cam(v) for v in s.views], s.images())
+    b.trainer_init(api.trainer_config(iterations=30, densify=dens))
+    if shared:
+        b.set_shared(rows, list(range(len(rows))), [1] * len(rows), [1] * len(rows))
+        z = rows_of(anchor)
+        b.set_anchor(z, z, api.penalties())
+    seq = orc.view_sequence(1, 0, len(s.views), n_steps)
+    losses = b.train_steps(seq)
+    want = HostCloud.from_oracle(t.cloud())
+    got = b.download_cloud()
+    # the decisions are integer: same ids in the same rows
+    removed, new = list(t.take_removed_ids()), HostCloud.from_oracle(t.take_new_rows()).ids
+    assert len(removed) > 0 and len(new) > 0
+    assert np.array_equal(got["ids"], want.ids)
+    assert list(b.take_removed_ids()) == removed
+    assert np.array_equal(b.take_new_ids(), new)
+    assert all(int(i) >= init.n for i in new)  # block 0 allocates past the initial ids
+    if shared:
+        assert list(b.shared_ids()) == list(t.shared_ids())
+    # before the densification the trajectories agree to FP32 rounding; after it
+    # the children start from FP32 vs FP64 parents (one view's small loss moved 0.7%)
+    np.testing.assert_allclose(losses[:steps], want_losses[:steps], rtol=5e-4)
+    np.testing.assert_allclose(losses[steps:], want_losses[steps:], rtol=1e-2)
+    g = np.concatenate([got["pos"], got["rot"], got["ls"], got["feat"], got["op"][:, None]], 1)
+    err = np.abs(g - rows_of(want))
+    assert np.mean(err <= 1e-4 + 1e-4 * np.abs(rows_of(want))) >= 0.98
+    m, v = b.moments()
+    assert m.shape[1] == len(want.ids) and np.all(v >= 0)

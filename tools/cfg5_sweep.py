@@ -42,7 +42,7 @@ def run(n, warmup, steps, stage_steps):
     blk.upload_cloud(cloud["ids"], cloud["pos"], cloud["rot"], cloud["ls"], cloud["feat"], cloud["op"])
     del cloud
     blk.set_views([cam], [np.full((H, W, 3), 0.5)])
-    blk.trainer_init(api.trainer_config(iterations=30000))
+    blk.trainer_init(api.trainer_config(iterations=30000, densify={"enabled": 0}))
     stream = torch.cuda.ExternalStream(blk.stream())
     for _ in range(warmup):
         blk.train_steps([0], want_losses=False)

@@ -60,7 +60,7 @@ def main():
                      init["op"][sel])
     vcams = [cams[v].device() for v in views]
     blk.set_views(vcams, [np.full((cfg["height"], cfg["width"], 3), 0.5) for _ in vcams])
-    blk.trainer_init(api.trainer_config(iterations=30000))
+    blk.trainer_init(api.trainer_config(iterations=30000, densify={"enabled": 0}))
     # one rank holds only its own contributions: with the plan's owner counts
     # z = (own contribution) / owners would drag the anchors away and change the
     # training cost, so every slot counts one owner here (same kernels, same sizes)
