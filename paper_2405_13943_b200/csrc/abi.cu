@@ -396,7 +396,7 @@ void ensure_views_buffers(Ctx* c, size_t n) {
 
 // ---- consensus plumbing --------------------------------------------------
 void reduce_nccl(Ctx* c, void* buf, size_t count, ncclDataType_t type, ncclRedOp_t op) {
-    if (!c->nccl || c->nranks == 1) return;
+    if (!c->nccl) return;
     NcclApi& n = nccl_api();
     const ncclResult_t r = n.all_reduce(buf, buf, count, type, op, static_cast<ncclComm_t>(c->nccl), c->stream);
     if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, std::string("ncclAllReduce: ") + n.error_string(r)};
@@ -1182,7 +1182,8 @@ int bsg_comm_init(bsg_ctx* h, const uint8_t id[128], int nranks, int rank) {
         use_device(c);
         c->nranks = nranks;
         c->rank = rank;
-        if (nranks == 1) return;
+        // a one-rank communicator is created too: its AllReduces are local
+        // copies, and the NCCL path runs (and is tested) on a single GPU
         ncclUniqueId uid;
         std::memcpy(&uid, id, 128);
         ncclComm_t comm;

@@ -311,3 +311,30 @@ def test_densify_matches_oracle(shared_every):
     assert np.mean(err <= 1e-4 + 1e-4 * np.abs(rows_of(want))) >= 0.98
     m, v = b.moments()
     assert m.shape[1] == len(want.ids) and np.all(v >= 0)
+
+
+def test_nccl_round_path_single_rank():
+    """The NCCL code path of the round (dlopen'd libnccl, AllReduces on the
+    communication stream) with a one-rank communicator: same result as the
+    communicator-less round."""
+    s, init = toy_scene()
+    shared_rows = list(range(0, init.n, 2))
+    x0 = rows_of(init)[shared_rows]
+    zprev = (x0 + 0.02).astype(np.float32).astype(np.float64)
+    seq = orc.view_sequence(1, 0, len(s.views), 6)
+    out = []
+    for use_nccl in (False, True):
+        b = _anchored_trainer(init, s, shared_rows, zprev, api.penalties())
+        if use_nccl:
+            b.comm_init(api.nccl_unique_id(), 1, 0)
+        b.train_steps(seq[:3])
+        b.consensus_round_async(1.6, True, iteration=3)
+        b.train_steps(seq[3:])
+        r = b.consensus_wait()
+        out.append((r, b.anchor(), b.duals()))
+    (ra, za, ua), (rb, zb, ub) = out
+    assert rb["primal"] == pytest.approx(ra["primal"], rel=1e-6)
+    assert rb["dual"] == pytest.approx(ra["dual"], rel=1e-6)
+    assert rb["rho"] == ra["rho"]
+    np.testing.assert_allclose(zb, za, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(ub, ua, rtol=1e-5, atol=1e-6)
