@@ -206,6 +206,12 @@ public:
     // shared ids in the group-wide slot table.
     void bind_slots(const std::vector<uint32_t>& slots, const std::vector<uint8_t>& first_owner,
                     const std::vector<uint32_t>& slot_owners);
+    // The group's shared set changed (densification, runtime.cpp:490-518): keep
+    // only `keep_ids` (ascending) on new slots, carrying their anchor and duals;
+    // zprev_slots = the master's z_prev for the new slot table (rows x D).
+    void rebind_slots(const std::vector<uint64_t>& keep_ids, const std::vector<uint32_t>& slots,
+                      const std::vector<uint8_t>& first_owner, const std::vector<uint32_t>& slot_owners,
+                      const std::vector<double>& zprev_slots, const PropertyPenalties& rho);
 
 private:
     void install_shared();

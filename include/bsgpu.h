@@ -295,9 +295,13 @@ const char* bsg_driver_last_error(void);
 int bsg_run_simulated(int feature_dim, size_t n, const uint64_t* ids, const double* pos, const double* rot,
                       const double* log_scale, const double* features, const double* opacity_logit, size_t n_views,
                       const bsg_camera* cams, const double* const* gt_rgb, const bsg_trainer_config* trainer,
-                      const bsg_session_options* session, size_t n_devices, const int* devices, double* out_pos,
-                      double* out_rot, double* out_log_scale, double* out_features, double* out_opacity_logit,
+                      const bsg_session_options* session, size_t n_devices, const int* devices,
+                      size_t model_capacity, uint64_t* out_ids, double* out_pos, double* out_rot,
+                      double* out_log_scale, double* out_features, double* out_opacity_logit, size_t* out_n,
                       bsg_round_diag* rounds, size_t max_rounds, size_t* n_rounds, double* wall_seconds);
+/* The out_* arrays hold up to model_capacity rows of the assembled model
+ * (densification changes its size; *out_n receives it, BSG_ERR_CAPACITY when
+ * it exceeds the capacity). */
 
 /* ---- measurement ------------------------------------------------------ */
 /* Per-stage device times of the most recent step (CUDA events on the

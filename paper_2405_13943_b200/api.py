@@ -156,7 +156,7 @@ SYMBOLS = [
     ("bsg_run_simulated", ctypes.c_int, [ctypes.c_int, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZ,
                                           ctypes.POINTER(bsg_camera), ctypes.POINTER(_DP),
                                           ctypes.POINTER(bsg_trainer_config), ctypes.POINTER(bsg_session_options), _SZ,
-                                          ctypes.POINTER(ctypes.c_int), _DP, _DP, _DP, _DP, _DP,
+                                          ctypes.POINTER(ctypes.c_int), _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZP,
                                           ctypes.POINTER(bsg_round_diag), _SZ, _SZP, _DP]),
     ("bsg_enable_stage_timing", ctypes.c_int, [_P, ctypes.c_int]),
     ("bsg_stage_count", ctypes.c_int, []),
@@ -616,19 +616,24 @@ def run_simulated(cloud, cams, gts, trainer_cfg, session, devices=(0,)):
     cam_arr = (bsg_camera * len(cams))(*cams)
     gts = [_f64(g) for g in gts]
     gptr = (_DP * len(gts))(*[_ptr(g, ctypes.c_double) for g in gts])
-    outs = [np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros((n, fd)), np.zeros(n)]
+    cap = 16 * n + 1024  # densification grows the model
+    out_ids = np.zeros(cap, np.uint64)
+    outs = [np.zeros((cap, 3)), np.zeros((cap, 4)), np.zeros((cap, 3)), np.zeros((cap, fd)), np.zeros(cap)]
+    n_out = ctypes.c_size_t()
     max_rounds = int(session.total_iterations // max(session.interval, 1)) + 2
     rounds = (bsg_round_diag * max_rounds)()
     nr, wall = ctypes.c_size_t(), ctypes.c_double()
     dev = (ctypes.c_int * len(devices))(*devices)
     st = _lib.bsg_run_simulated(fd, n, _ptr(ids, ctypes.c_uint64), *[_ptr(a, ctypes.c_double) for a in arrs],
                                 len(cams), cam_arr, gptr, ctypes.byref(trainer_cfg), ctypes.byref(session),
-                                len(devices), dev, *[_ptr(o, ctypes.c_double) for o in outs], rounds, max_rounds,
+                                len(devices), dev, cap, _ptr(out_ids, ctypes.c_uint64),
+                                *[_ptr(o, ctypes.c_double) for o in outs], ctypes.byref(n_out), rounds, max_rounds,
                                 ctypes.byref(nr), ctypes.byref(wall))
     if st != BSG_OK:
         msg = _lib.bsg_driver_last_error().decode()
         raise InvalidArgument(msg) if st == BSG_ERR_INVALID_ARGUMENT else BsgError(msg)
-    model = dict(ids=ids, pos=outs[0], rot=outs[1], ls=outs[2], feat=outs[3], op=outs[4])
+    m = n_out.value
+    model = dict(ids=out_ids[:m], pos=outs[0][:m], rot=outs[1][:m], ls=outs[2][:m], feat=outs[3][:m], op=outs[4][:m])
     rl = []
     for j in range(min(nr.value, max_rounds)):
         r = rounds[j]

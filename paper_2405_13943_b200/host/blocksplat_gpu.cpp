@@ -10,6 +10,7 @@
 #include <exception>
 #include <memory>
 #include <random>
+#include <set>
 #include <thread>
 
 namespace blocksplat {
@@ -475,6 +476,20 @@ void BlockTrainer::bind_slots(const std::vector<uint32_t>& slots, const std::vec
     install_shared();
 }
 
+void BlockTrainer::rebind_slots(const std::vector<uint64_t>& keep_ids, const std::vector<uint32_t>& slots,
+                                const std::vector<uint8_t>& first_owner, const std::vector<uint32_t>& slot_owners,
+                                const std::vector<double>& zprev_slots, const PropertyPenalties& rho) {
+    const GaussianCloud a_old = anchor(), u_old = duals();
+    const std::vector<double> ar = rows_of(a_old, find_all(a_old, keep_ids, "anchor misses kept ids")),
+                              ur = rows_of(u_old, find_all(u_old, keep_ids, "duals miss kept ids"));
+    shared_ids_ = keep_ids;
+    bind_slots(slots, first_owner, slot_owners);
+    const bsg_penalties p = to_dev(rho);
+    check(bsg_set_anchor(ctx_, ar.data(), zprev_slots.empty() ? nullptr : zprev_slots.data(), &p));
+    check(bsg_upload_duals(ctx_, ur.data()));
+    have_anchor_ = true;
+}
+
 void BlockTrainer::set_anchor(const GaussianCloud& z, const PropertyPenalties& rho) {  // trainer.cpp:161-166
     if (slots_.size() != shared_ids_.size()) install_shared();
     const std::vector<double> zr = rows_of(z, find_all(z, shared_ids_, "broadcast misses shared ids"));
@@ -609,14 +624,6 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
     const auto K = static_cast<uint32_t>(plan.shards.size());
     if (K == 0) throw InvalidArgument("plan has no shards");
     if (devices.empty()) throw InvalidArgument("no devices");
-    {
-        // the master's bookkeeping of removed / new ids (runtime.cpp:490-518) is
-        // not on this path yet: refuse a K > 1 schedule that densifies
-        const DensifyConfig& d = trainer.densify;
-        const uint64_t stop = d.stop_iteration ? d.stop_iteration : (trainer.iterations * 6) / 10;
-        if (K > 1 && d.enabled && d.interval && d.interval <= stop)
-            throw InvalidArgument("run_simulated with K > 1 and densification is not supported on the device path");
-    }
     const int fd = plan.init_cloud.feature_dim(), D = 11 + fd;
     std::vector<BlockTrainer> tr;
     tr.reserve(K);
@@ -626,7 +633,9 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
                         devices[b % devices.size()]);
     }
     // Global slots and the round-0 anchor (runtime.cpp:465-477, trainer.cpp:161-166).
-    const std::vector<uint64_t>& S = plan.shared_ids;
+    std::vector<uint64_t> S = plan.shared_ids;  // the current consensus slot table (ascending ids)
+    std::map<uint64_t, std::vector<uint32_t>> owners = plan.owners;
+    std::set<uint64_t> global_ids(plan.init_cloud.ids.begin(), plan.init_cloud.ids.end());
     const GaussianCloud z0 = slice_by_ids(plan.init_cloud, S);
     const std::vector<double> z0_rows = rows_of(z0, find_all(z0, S, "initial cloud ill-formed"));
     PropertyPenalties rho = opt.rho;
@@ -669,11 +678,79 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
         done = t;
+        // ownership changes from densification (runtime.cpp:490-518)
+        std::map<uint64_t, size_t> prev_owner_count;
+        for (uint32_t b = 0; b < K; ++b)
+            for (uint64_t id : tr[b].take_removed_ids()) {
+                auto it = owners.find(id);
+                if (it == owners.end()) continue;
+                prev_owner_count.emplace(id, it->second.size());
+                auto& list = it->second;
+                list.erase(std::remove(list.begin(), list.end(), b), list.end());
+            }
+        std::vector<uint64_t> reset_ids, dead_ids;
+        for (const auto& [id, prev] : prev_owner_count) {
+            const auto& list = owners.at(id);
+            if (list.empty())
+                dead_ids.push_back(id);
+            else if (prev >= 2 && list.size() >= 2)
+                reset_ids.push_back(id);  // (prev >= 2, now 1 owner: unshared, leaves the slot table)
+        }
+        for (uint64_t id : dead_ids) {
+            owners.erase(id);
+            global_ids.erase(id);
+        }
+        for (uint32_t b = 0; b < K; ++b)
+            for (uint64_t id : tr[b].take_new_rows().ids) {
+                owners[id] = {b};
+                global_ids.insert(id);
+            }
+        std::vector<uint64_t> shared_now;
+        for (const auto& [id, list] : owners)
+            if (list.size() >= 2) shared_now.push_back(id);
+        if (shared_now != S) {
+            // new slot table; every block keeps its anchor / duals for the ids
+            // that stay shared, z_prev comes from the last consensus (all of
+            // shared_now was shared before: new rows start single-owner)
+            std::vector<double> zp_old(S.size() * D), zp_new(shared_now.size() * D);
+            if (!S.empty()) check(bsg_download_consensus(ctxs[0], zp_old.data()));
+            if (done == schedule.front()) std::copy(z0_rows.begin(), z0_rows.end(), zp_old.begin());
+            std::vector<uint32_t> cnt(shared_now.size()), first_owner(shared_now.size());
+            for (size_t k = 0; k < shared_now.size(); ++k) {
+                const size_t old = std::lower_bound(S.begin(), S.end(), shared_now[k]) - S.begin();
+                std::copy(&zp_old[old * D], &zp_old[old * D] + D, &zp_new[k * D]);
+                const auto& list = owners.at(shared_now[k]);
+                cnt[k] = static_cast<uint32_t>(list.size());
+                first_owner[k] = *std::min_element(list.begin(), list.end());
+            }
+            for (uint32_t b = 0; b < K; ++b) {
+                std::vector<uint64_t> keep;
+                std::vector<uint32_t> slots;
+                std::vector<uint8_t> first;
+                for (uint64_t id : tr[b].shared_ids()) {
+                    auto it = std::lower_bound(shared_now.begin(), shared_now.end(), id);
+                    if (it == shared_now.end() || *it != id) continue;
+                    keep.push_back(id);
+                    slots.push_back(static_cast<uint32_t>(it - shared_now.begin()));
+                    first.push_back(first_owner[slots.back()] == b ? 1 : 0);
+                }
+                tr[b].rebind_slots(keep, slots, first, cnt, zp_new, opt.consensus.enabled ? rho : zero_rho);
+                ctxs[b] = tr[b].context();
+            }
+            S = shared_now;
+        }
+        std::vector<uint32_t> reset_slots;
+        for (uint64_t id : reset_ids) {
+            auto it = std::lower_bound(S.begin(), S.end(), id);
+            if (it != S.end() && *it == id) reset_slots.push_back(static_cast<uint32_t>(it - S.begin()));
+        }
         // consensus round on the device (runtime.cpp:529-548, trainer.cpp:168-223)
         bsg_round_args args{};
         args.alpha = opt.consensus.alpha;
         args.relax = opt.consensus.enabled && opt.consensus.alpha != 1.0 && !final_round;
         args.diagnostics = 1;
+        args.n_reset = reset_slots.size();
+        args.reset_slots = reset_slots.empty() ? nullptr : reset_slots.data();
         bsg_round_result r{};
         const auto r0 = std::chrono::steady_clock::now();
         check(bsg_group_consensus_round(ctxs.data(), K, &args, &r));
@@ -693,14 +770,20 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
         for (auto& x : tr) d.mean_loss += x.last_loss();
         d.mean_loss /= K;
         d.shared_count = S.size();
-        d.global_count = plan.init_cloud.size();
+        d.global_count = global_ids.size();
         d.consensus_ms = round_ms;
         result.rounds.push_back(d);
         if (observer) observer(d);
     }
     // Global model (runtime.cpp:550-565): shared rows = normalised z, the rest
     // from their single owner's final cloud.
-    GaussianCloud model = plan.init_cloud;
+    GaussianCloud model(fd);
+    model.ids.assign(global_ids.begin(), global_ids.end());
+    model.positions.resize(3 * model.size());
+    model.rotations.resize(4 * model.size());
+    model.log_scales.resize(3 * model.size());
+    model.features.resize(static_cast<size_t>(fd) * model.size());
+    model.opacity_logits.resize(model.size());
     std::vector<double> zs(S.size() * D);
     if (!S.empty()) check(bsg_download_consensus(ctxs[0], zs.data()));
     std::vector<GaussianCloud> finals;
@@ -719,7 +802,7 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
                 for (int k = 3; k < 7; ++k) row[k] /= qn;
             }
         } else {
-            const uint32_t owner = plan.owners.at(id).front();
+            const uint32_t owner = owners.at(id).front();
             const GaussianCloud& c = finals[owner];
             const std::vector<double> r = rows_of(c, {c.find(id)});
             std::copy(r.begin(), r.end(), row);

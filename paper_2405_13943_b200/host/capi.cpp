@@ -16,8 +16,9 @@ const char* bsg_driver_last_error(void) { return g_drv_err.c_str(); }
 int bsg_run_simulated(int fd, size_t n, const uint64_t* ids, const double* pos, const double* rot, const double* ls,
                       const double* feat, const double* op, size_t n_views, const bsg_camera* cams,
                       const double* const* gts, const bsg_trainer_config* tc, const bsg_session_options* so,
-                      size_t n_devices, const int* devices, double* out_pos, double* out_rot, double* out_ls,
-                      double* out_feat, double* out_op, bsg_round_diag* rounds, size_t max_rounds, size_t* n_rounds,
+                      size_t n_devices, const int* devices, size_t model_capacity, uint64_t* out_ids,
+                      double* out_pos, double* out_rot, double* out_ls, double* out_feat, double* out_op,
+                      size_t* out_n, bsg_round_diag* rounds, size_t max_rounds, size_t* n_rounds,
                       double* wall_seconds) {
     using namespace blocksplat;
     try {
@@ -76,7 +77,14 @@ int bsg_run_simulated(int fd, size_t n, const uint64_t* ids, const double* pos, 
         std::vector<int> devs(devices, devices + n_devices);
         if (devs.empty()) devs.push_back(0);
         const RunResult r = run_simulated(plan, t, opt, {}, devs);
-        for (size_t i = 0; i < n; ++i) {
+        const size_t nm = r.model.size();
+        if (out_n) *out_n = nm;
+        if (nm > model_capacity) {
+            g_drv_err = "model larger than the output capacity";
+            return BSG_ERR_CAPACITY;
+        }
+        if (out_ids) std::copy(r.model.ids.begin(), r.model.ids.end(), out_ids);
+        for (size_t i = 0; i < nm; ++i) {
             for (int k = 0; k < 3; ++k) out_pos[3 * i + k] = r.model.positions[3 * i + k];
             for (int k = 0; k < 4; ++k) out_rot[4 * i + k] = r.model.rotations[4 * i + k];
             for (int k = 0; k < 3; ++k) out_ls[3 * i + k] = r.model.log_scales[3 * i + k];

@@ -24,17 +24,20 @@ def desk_scene(seed=42, gaussians=200, cameras=24, size=96, extent=10.0):
     return s, init
 
 
-def run_both(s, init, blocks, iters, interval, alpha):
+def run_both(s, init, blocks, iters, interval, alpha, densify_interval=0):
     tc = orc.TrainerConfig()
     tc.iterations, tc.seed = iters, 7
-    tc.densify_enabled = False
+    tc.densify_enabled = densify_interval > 0
+    if densify_interval:
+        tc.densify_interval = densify_interval
     plan = orc.plan_cluster(s, blocks, 1.4, 8, tc)
     so = orc.SessionOptions()
     so.total_iterations = iters
     so.consensus.interval = interval
     so.consensus.alpha = alpha
     want = orc.run_simulated(plan, tc, so)
-    gcfg = api.trainer_config(iterations=iters)
+    gcfg = api.trainer_config(iterations=iters, densify=dict(enabled=1 if densify_interval else 0,
+                                                             interval=densify_interval or 200))
     sess = api.session_options(iters, interval=interval, alpha=alpha, blocks=blocks, expand_scale=1.4, holdout=8,
                                seed=7)
     cloud = dict(ids=init.ids, pos=init.pos, rot=init.rot, ls=init.ls, feat=init.feat, op=init.op)
@@ -95,3 +98,23 @@ def test_cpp_host_api_selftest():
     exe = os.path.join(os.path.dirname(api.LIB_PATH), "blocksplat_gpu_selftest")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_run_simulated_with_densification():
+    """K = 2 run whose blocks densify (trainer.cpp:301-385 on the device) with
+    the master's ownership bookkeeping (runtime.cpp:490-518: dead / unshared /
+    reset ids, new rows, a shrinking slot table) on the host. The density
+    decisions are FP thresholds evaluated in FP32 (device) vs FP64 (oracle),
+    so counts are held to 2% and the holdout PSNR to 0.15 dB."""
+    s, init = desk_scene(gaussians=400)
+    plan, want, model, rounds = run_both(s, init, 2, 60, 20, 1.6, densify_interval=10)
+    assert len(rounds) == len(want.rounds) == 3
+    for g, w in zip(rounds, want.rounds):
+        assert g["iteration"] == w.iteration
+        assert abs(g["global_count"] - w.global_count) <= 0.02 * w.global_count
+        assert abs(g["shared_count"] - w.shared_count) <= 0.02 * max(w.shared_count, 1) + 1
+    assert want.rounds[-1].global_count != init.n  # the run really densified
+    mc = HostCloud(model["ids"], model["pos"], model["rot"], model["ls"], model["feat"], model["op"])
+    p_gpu = holdout_psnr(mc.oracle(), s)
+    p_ref = holdout_psnr(want.model, s)
+    assert abs(p_gpu - p_ref) <= 0.15, (p_gpu, p_ref)
