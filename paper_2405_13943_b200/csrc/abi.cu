@@ -219,8 +219,8 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     stage_begin(c, kStCompact);
     compact_visible(c, static_cast<uint32_t>(c->n), true);  // + digit histograms of the 32-bit depth keys
     stage_end(c, kStCompact);
-    // One readback: V and the depth-key histograms (pass skipping).
-    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist), cudaMemcpyDeviceToHost,
+    // One readback: V (sizes the depth key and the sort).
+    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, depth_hist), cudaMemcpyDeviceToHost,
                              c->stream));
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     const uint32_t V = c->counters_host->visible;
@@ -230,8 +230,8 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     // of equal keys sorted by the full FP64 depth. A run longer than 64 that is
     // out of order falls back to all 8 digit passes of the FP64 bits.
     uint32_t* k32[2] = {reinterpret_cast<uint32_t*>(c->vkey[0]), reinterpret_cast<uint32_t*>(c->vkey[1])};
-    radix_sort_u32(c, k32, c->vrow, V, 0, depth_key_bits(V) / 8, &c->counters->depth_hist[0][0],
-                   &c->counters_host->depth_hist[0][0], &c->depth_sorted);
+    radix_sort_u32_hist(c, k32, c->vrow, V, depth_key_bits(V) / 8, &c->counters->depth_hist[0][0],
+                        &c->depth_sorted);
     depth_tie_fixup(c, k32[c->depth_sorted], c->vrow[c->depth_sorted], c->depth_key, V, &c->counters->overflow);
     stage_end(c, kStDepthSort);
     stage_begin(c, kStPairs);

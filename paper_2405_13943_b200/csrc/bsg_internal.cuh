@@ -245,6 +245,10 @@ void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, in
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel);
 void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel);
+// As radix_sort_u32 over `passes` digits from bit 0, building the digit
+// histograms itself from keys[0] (no pass skipping).
+void radix_sort_u32_hist(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                         int* sel);
 // Sorts runs of equal 32-bit depth keys by the full FP64 depth bits of their
 // rows (stable); sets *long_run if a run exceeds 64 (caller redoes the full sort).
 void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,

@@ -7,6 +7,8 @@
 // Traffic per pass: read key+value, write key+value.
 #include "bsg_internal.cuh"
 
+#include <algorithm>
+
 namespace bsg {
 namespace {
 
@@ -152,6 +154,24 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
     }
 }
 
+// Digit histograms of `passes` 8-bit digits over n keys (for keys whose
+// producer did not build them): shared-memory counts per CTA, one global
+// atomic per non-empty bin.
+template <typename K>
+__global__ __launch_bounds__(256) void digit_hist_kernel(const K* __restrict__ keys, uint32_t n, int passes,
+                                                         uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_h[4 * 256];
+    for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) s_h[k] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const K key = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < passes * 256; k += blockDim.x)
+        if (s_h[k]) atomicAdd(&hist[k], s_h[k]);
+}
+
 template <typename K, int ITEMS>
 void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes, uint32_t* d_hist,
                    const uint32_t* h_hist, int* sel) {
@@ -268,6 +288,18 @@ void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, in
 void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel) {
     radix_sort<uint32_t>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
+}
+
+void radix_sort_u32_hist(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
+                         int* sel) {
+    *sel = 0;
+    if (n <= 1) return;
+    if (passes > 4) throw Error{BSG_ERR_INVALID_ARGUMENT, "at most 4 digit passes"};
+    BSG_CUDA(cudaMemsetAsync(d_hist, 0, passes * 256 * sizeof(uint32_t), c->stream));
+    const unsigned grid = std::min<unsigned>((n + 4095) / 4096, 148);  // few CTAs: one global atomic per bin each
+    digit_hist_kernel<uint32_t><<<grid, 256, 0, c->stream>>>(keys[0], n, passes, d_hist);
+    BSG_LAUNCHED(c);
+    radix_sort<uint32_t>(c, keys, vals, n, 0, passes, d_hist, nullptr, sel);
 }
 
 void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,

@@ -76,8 +76,8 @@ __device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32
 // MODE 0: plain exclusive scan of in[gather ? gather[i] : i].
 // MODE 1: compaction of rows with tiles[i] > 0 (in = tiles), emits the FP64
 //         depth bits as u64 keys + rows, 8 digit histograms.
-// MODE 2: as 1 with the 32-bit range-normalised key (bits - zmin) >> shift,
-//         4 digit histograms (the key has depth_key_bits(V) <= 32 bits).
+// MODE 2: as 1 with the 32-bit range-normalised key (bits - zmin) >> shift
+//         (depth_key_bits(V) <= 32 bits), no histograms.
 template <int MODE>
 __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __restrict__ in,
                                                             const uint32_t* __restrict__ gather,
@@ -91,10 +91,10 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                                                             uint32_t* __restrict__ mask_out, uint32_t mask_words) {
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
-    constexpr int kDigits = MODE == 2 ? 4 : 8;
-    __shared__ uint32_t s_hist[MODE != 0 ? kDigits * 256 : 1];
+    constexpr int kDigits = 8;
+    __shared__ uint32_t s_hist[MODE == 1 ? kDigits * 256 : 1];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    if (MODE != 0)
+    if (MODE == 1)
         for (int k = threadIdx.x; k < kDigits * 256; k += kScanThreads) s_hist[k] = 0;
     unsigned long long zmin = 0;
     int shift = 0;
@@ -173,10 +173,12 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                 out_rows[run] = static_cast<uint32_t>(i);
                 out[run] = static_cast<uint32_t>(i);
             }
-            // digit histograms: the upper digits are nearly constant, so lanes
-            // whose digit equals the first active lane's are counted with one
-            // atomic (ballot), the rest add individually
-            const unsigned act = __ballot_sync(0xffffffffu, vis);
+            // digit histograms (the FP64-bits fall-back only; the 32-bit keys get
+            // theirs from a pass over the V compacted keys, radix.cu): the upper
+            // digits are nearly constant, so lanes whose digit equals the first
+            // active lane's are counted with one atomic (ballot), the rest add
+            // individually
+            const unsigned act = MODE == 1 ? __ballot_sync(0xffffffffu, vis) : 0u;
             if (act) {
                 const int src = __ffs(act) - 1;
 #pragma unroll
@@ -194,7 +196,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         }
         run += v[k];
     }
-    if (MODE != 0) {
+    if (MODE == 1) {
         __syncthreads();
         for (int k = threadIdx.x; k < kDigits * 256; k += kScanThreads)
             if (s_hist[k]) atomicAdd(&hist_out[k], s_hist[k]);
