@@ -1,10 +1,12 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): every rank derives the
 same block plan with the native planner, the per-rank slot tables cover the
 global slot table with the right owner counts and one first owner per slot,
-and the two-reduction consensus protocol the device runs over NCCL
-(q-reference pre-reduction, then sum of relaxed sign-aligned contributions +
-flip flags) reproduces the reference's consensus_average / dual_update /
-residuals when the sums are done by torch.distributed. The pack/unpack here
+and the consensus protocol the device runs over NCCL (q-reference
+pre-reduction, sum of relaxed sign-aligned contributions + flip flags, then a
+3-double reduction of the residual / flip partials, each slot's dual residual
+counted by its lowest owner) reproduces the reference's consensus_average /
+dual_update / residuals when the sums are done by torch.distributed, with
+identical residuals and penalty decisions on every rank. The pack/unpack here
 is a numpy restatement of csrc/consensus.cu for the protocol check only."""
 import os
 import socket
@@ -87,11 +89,23 @@ def worker(rank, world, port, out_q):
     xh = ALPHA * x + (1 - ALPHA) * zprev[slots]
     u = xh - z[slots]
     u[np.isin(slots, flipped)] = 0
-    # primal residual partial -> scalar all-reduce
-    p2 = torch.tensor([float(((x.astype(np.float64) - z[slots]) ** 2).sum())], dtype=torch.float64)
-    dist.all_reduce(p2)
+    # residual partials -> one 3-double all-reduce (csrc/consensus.cu unpack_own_kernel):
+    # primal^2 over own rows; dual^2 and flips over the slots this rank leads
+    rho = api.penalties()
+    rho_c = np.array([rho.rho_p] * 3 + [rho.rho_q] * 4 + [rho.rho_s] * 3 + [rho.rho_f] * 3 + [rho.rho_o], np.float64)
+    lead = first == 1
+    zf = z[slots].astype(np.float64)
+    p2 = float(((x.astype(np.float64) - zf) ** 2).sum())
+    d2 = float(((rho_c * (zf[lead] - zprev[slots][lead].astype(np.float64))) ** 2).sum())
+    fl = float((pack[slots, D] > 0)[lead].sum())
+    scal = torch.tensor([p2, d2, fl], dtype=torch.float64)
+    dist.all_reduce(scal)
+    primal, dual = float(np.sqrt(scal[0].item())), float(np.sqrt(scal[1].item()))
+    # adapt_penalties (admm.cpp:200-217) on the reduced, rank-identical values
+    f = 2.0 if primal > 10.0 * dual else (0.5 if dual > 10.0 * primal else 1.0)
     out_q.put((rank, dict(ids=ids, slots=slots, first=first, sids=sids, owners=owners, z=z, flipped=flipped,
-                          u=u, primal=float(np.sqrt(p2.item())), x=rows(mine), zprev=zprev)))
+                          u=u, primal=primal, dual=dual, flips=int(scal[2].item()), rho_factor=f, x=rows(mine),
+                          zprev=zprev)))
     dist.destroy_process_group()
 
 
@@ -133,8 +147,13 @@ def test_two_rank_consensus_protocol_matches_reference():
     np.testing.assert_allclose(r0["z"], zr, rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(r1["z"], zr, rtol=1e-5, atol=1e-5)
     assert sorted(r0["sids"][r0["flipped"]].tolist()) == sorted(flipped)
-    primal, _ = orc.residuals(locs, z, zp.oracle(), orc.Penalties())
+    primal, dual = orc.residuals(locs, z, zp.oracle(), orc.Penalties())
     assert r0["primal"] == pytest.approx(primal, rel=1e-4)
+    assert r0["dual"] == pytest.approx(dual, rel=1e-4)
+    # every rank holds bit-identical residuals, flip count and penalty decision
+    assert (r0["primal"], r0["dual"], r0["flips"], r0["rho_factor"]) == (r1["primal"], r1["dual"], r1["flips"],
+                                                                         r1["rho_factor"])
+    assert r0["flips"] == len(flipped)
     for b, r in ((0, r0), (1, r1)):
         xs = rows(HostCloud.from_oracle(orc.slice_by_ids(locs[b][1], list(r0["sids"][r["slots"]]))))
         u = orc.dual_update(orc.zero_bundle(list(r0["sids"][r["slots"]]), 3),
