@@ -14,10 +14,19 @@ namespace {
 
 // Fold of one visible row; FP64 arithmetic over FP32 inputs. g receives the
 // D parameter gradients; returns the screen-space gradient norm.
+// The row's parameters from the preprocess's row-contiguous cache (visible
+// rows only; same values as x[.][i] this step).
 template <int fd>
-__device__ __forceinline__ void load_row(const float* __restrict__ x, size_t cap, uint32_t i, float (&prm)[11 + fd]) {
+__device__ __forceinline__ void load_row(const float4* __restrict__ pcache, uint32_t i, float (&prm)[11 + fd]) {
+    constexpr int D = 11 + fd, NV = (D + 3) / 4;
+    float v[4 * NV];
 #pragma unroll
-    for (int k = 0; k < 11 + fd; ++k) prm[k] = x[k * cap + i];
+    for (int k = 0; k < NV; ++k) {
+        const float4 q = pcache[static_cast<size_t>(kParamVec) * i + k];
+        v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) prm[k] = v[k];
 }
 
 // The 9 image-space gradients of row i: FP32 record, or the FP64 slot of a
@@ -187,6 +196,7 @@ template <int fd>
 __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
                                                          DevCam cam, const uint32_t* __restrict__ tiles,
                                                          const float4* __restrict__ rec,
+                                                         const float4* __restrict__ pcache,
                                                          const float4* __restrict__ g2d,
                                                          const double* __restrict__ g2d_wide, double* __restrict__ gout,
                                                          double* __restrict__ sgn_out, uint8_t* __restrict__ vis) {
@@ -200,7 +210,7 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
     const bool visible = tiles[i] > 0;
     if (visible) {
         float prm[11 + fd];
-        load_row<fd>(x, cap, i, prm);
+        load_row<fd>(pcache, i, prm);
         s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
     }
 #pragma unroll
@@ -210,11 +220,13 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
 }
 
 // Fold over the compacted visible list (V threads): parameter gradient of
-// each visible row into gbuf[D][cap] (FP32), densify statistics.
+// each visible row into gbuf[D][.] at its visible position (coalesced; Adam
+// finds it through the visibility mask + per-word prefix), densify statistics.
 template <int fd>
 __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, DevCam cam,
                                                            const uint32_t* __restrict__ vis_rows, uint32_t V,
                                                            const float4* __restrict__ rec,
+                                                           const float4* __restrict__ pcache,
                                                            const float4* __restrict__ g2d,
                                                            const double* __restrict__ g2d_wide, float* __restrict__ gbuf,
                                                            float* __restrict__ grad_accum,
@@ -227,10 +239,10 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
 #pragma unroll
     for (int c = 0; c < D; ++c) g[c] = 0.0;
     float prm[11 + fd];
-    load_row<fd>(x, cap, i, prm);
+    load_row<fd>(pcache, i, prm);
     const double s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
 #pragma unroll
-    for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + i] = static_cast<float>(g[c]);
+    for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + p] = static_cast<float>(g[c]);  // coalesced
     grad_accum[i] += static_cast<float>(s);
     grad_seen[i] += 1u;
 }
@@ -257,6 +269,7 @@ __device__ __forceinline__ int comp_of_group(int y) { return y < 3 ? y : y + 4; 
 template <int Q>
 __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
                                                    size_t cap, uint32_t n, const uint32_t* __restrict__ vis_mask,
+                                                   const uint32_t* __restrict__ vis_prefix,
                                                    const float* __restrict__ gbuf,
                                                    const uint32_t* __restrict__ sh_mask,
                                                    const uint32_t* __restrict__ sh_prefix, const float* __restrict__ z,
@@ -285,7 +298,10 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
             vs[k][0] = v4.x; vs[k][1] = v4.y; vs[k][2] = v4.z; vs[k][3] = v4.w;
         }
         const uint32_t word = r0 >> 5, bit0 = r0 & 31u;
-        const uint32_t vis = (vis_mask[word] >> bit0) & 0xfu;
+        const uint32_t vword = vis_mask[word];
+        const uint32_t vis = (vword >> bit0) & 0xfu;
+        // visible position of the quad's first row (gbuf is by visible position)
+        const uint32_t vpos = vis ? vis_prefix[word] + __popc(vword & ((1u << bit0) - 1u)) : 0u;
         int aj[4] = {-1, -1, -1, -1};
         if (st.has_anchor) {
             const uint32_t sm = sh_mask[word];
@@ -305,7 +321,9 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
             const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                g[k][r] = ((vis >> r) & 1u) ? gbuf[off + r] : 0.f;
+                g[k][r] = ((vis >> r) & 1u)
+                              ? gbuf[static_cast<size_t>(c0 + k) * cap + vpos + __popc(vis & ((1u << r) - 1u))]
+                              : 0.f;
                 zr[k][r] = aj[r] >= 0 ? z[static_cast<size_t>(c0 + k) * ns + aj[r]] : 0.f;
                 ur[k][r] = aj[r] >= 0 ? u[static_cast<size_t>(c0 + k) * ns + aj[r]] : 0.f;
             }
@@ -360,6 +378,7 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
 __global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, float* __restrict__ m,
                                                        float* __restrict__ v, size_t cap, uint32_t n,
                                                        const uint32_t* __restrict__ vis_mask,
+                                                       const uint32_t* __restrict__ vis_prefix,
                                                        const float* __restrict__ gbuf,
                                                        const uint32_t* __restrict__ sh_mask,
                                                        const uint32_t* __restrict__ sh_prefix,
@@ -379,7 +398,9 @@ __global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, fl
             vs[k] = v[off];
         }
         const uint32_t word = i >> 5, bit = i & 31u;
-        const bool visible = (vis_mask[word] >> bit) & 1u;
+        const uint32_t vword = vis_mask[word];
+        const bool visible = (vword >> bit) & 1u;
+        const uint32_t vpos = visible ? vis_prefix[word] + __popc(vword & ((1u << bit) - 1u)) : 0u;
         int aj = -1;
         if (st.has_anchor) {
             const uint32_t sm = sh_mask[word];
@@ -387,7 +408,7 @@ __global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, fl
         }
         float g[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) g[k] = visible ? gbuf[static_cast<size_t>(kRot + k) * cap + i] : 0.f;
+        for (int k = 0; k < 4; ++k) g[k] = visible ? gbuf[static_cast<size_t>(kRot + k) * cap + vpos] : 0.f;
         if (aj >= 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -437,10 +458,10 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
     const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
     if (c->fd == 3)
         fold_grads_kernel<3><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
-                                                            c->rec, c->g2d, c->g2d_wide, g_out, sgn, vis);
+                                                            c->rec, c->pcache, c->g2d, c->g2d_wide, g_out, sgn, vis);
     else
         fold_grads_kernel<12><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
-                                                             c->rec, c->g2d, c->g2d_wide, g_out, sgn, vis);
+                                                             c->rec, c->pcache, c->g2d, c->g2d_wide, g_out, sgn, vis);
     BSG_LAUNCHED(c);
 }
 
@@ -448,11 +469,11 @@ void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     if (c->fd == 3)
         fold_visible_kernel<3><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
-                                                                        c->rec, c->g2d, c->g2d_wide, c->gbuf,
+                                                                        c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
                                                                         c->grad_accum, c->grad_seen);
     else
         fold_visible_kernel<12><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
-                                                                         c->rec, c->g2d, c->g2d_wide, c->gbuf,
+                                                                         c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
                                                                         c->grad_accum, c->grad_seen);
     BSG_LAUNCHED(c);
 }
@@ -465,12 +486,14 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     const uint32_t n = static_cast<uint32_t>(c->n);
     const int scalar_groups = c->D - 4;  // every component but the quaternion
     const dim3 g1(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(scalar_groups));
-    adam_kernel<1><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask,
+    adam_kernel<1><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf,
+                                              c->sh_mask,
                                               c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
                                               &c->scalars->penalty);
     BSG_LAUNCHED(c);
     adam_rot_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
-        c->x, c->m, c->v, c->cap, n, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
+        c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u,
+        c->n_shared,
         c->rho_dev, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }

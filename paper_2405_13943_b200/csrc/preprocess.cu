@@ -43,6 +43,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  uint32_t* __restrict__ tiles,
                                                                  float4* __restrict__ g2d,
                                                                  double* __restrict__ g2d_wide,
+                                                                 float4* __restrict__ pcache,
                                                                  StepCounters* __restrict__ counters) {
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint32_t s_count;
@@ -118,6 +119,14 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
         if (fd >= 12)
 #pragma unroll
             for (int k = 14; k < 11 + kMaxFd; ++k) prm[k] = x[k * cap + i];
+        // the row's parameters, row-contiguous, for the fold's gather (64 / 96 B;
+        // written for every FP32-test survivor, read only for visible rows)
+#pragma unroll
+        for (int v = 0; v < kParamVec; ++v)
+            if (4 * v < 11 + (fd >= 12 ? kMaxFd : 3))
+                pcache[static_cast<size_t>(kParamVec) * i + v] =
+                    make_float4(prm[4 * v], 4 * v + 1 < kMaxD ? prm[4 * v + 1] : 0.f,
+                                4 * v + 2 < kMaxD ? prm[4 * v + 2] : 0.f, 4 * v + 3 < kMaxD ? prm[4 * v + 3] : 0.f);
         const double p0 = prm[kPos + 0], p1 = prm[kPos + 1], p2 = prm[kPos + 2];
         // p_cam = R p + t (camera.hpp:28)
         double pc[3];
@@ -286,7 +295,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     if (c->n == 0) return;
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     preprocess_kernel<<<blocks, kPreThreads, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
-                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->counters);
+                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters);
     BSG_LAUNCHED(c);
 }
 

@@ -88,7 +88,8 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                                                             const StepCounters* __restrict__ range,
                                                             uint32_t* __restrict__ out_rows,
                                                             uint32_t* __restrict__ hist_out, int hist_first,
-                                                            uint32_t* __restrict__ mask_out, uint32_t mask_words) {
+                                                            uint32_t* __restrict__ mask_out, uint32_t mask_words,
+                                                            uint32_t* __restrict__ prefix_out) {
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
     constexpr int kDigits = 8;
@@ -155,6 +156,8 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
     if (threadIdx.x == 0 && (static_cast<uint64_t>(tile) + 1) * kScanTile >= n && total_out) *total_out = s_prefix + s_total;
     uint32_t run = s_prefix + tprefix;
     const int lane = threadIdx.x & 31;
+    if (MODE != 0 && (threadIdx.x & 3) == 0 && base / 32 < mask_words)
+        prefix_out[base / 32] = run;  // visible rows before this 32-row word
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const uint64_t i = base + k;
@@ -226,7 +229,7 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
     auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
     auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
     scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
-                                                          nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0);
+                                                          nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr);
     BSG_LAUNCHED(c);
 }
 
@@ -243,12 +246,14 @@ void compact_visible(Ctx* c, uint32_t n, bool key32) {
         scan_kernel<2><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
                                                               &c->counters->visible, c->depth_key, c->vkey[0],
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
-                                                              c->vis_mask, static_cast<uint32_t>(c->cap / 32));
+                                                              c->vis_mask, static_cast<uint32_t>(c->cap / 32),
+                                                              c->vis_prefix);
     else
         scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
                                                               &c->counters->visible, c->depth_key, c->vkey[0],
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
-                                                              c->vis_mask, static_cast<uint32_t>(c->cap / 32));
+                                                              c->vis_mask, static_cast<uint32_t>(c->cap / 32),
+                                                              c->vis_prefix);
     BSG_LAUNCHED(c);
 }
 

@@ -12,7 +12,8 @@ import pytest
 
 import _oracle as orc
 from gpu_helpers import dev_cam, expected_pairs, gpu, new_block, rcfg, rel_err
-from refcases import (aerial_scene, axis_camera, cloud_from_rows, empty_cloud, random_cloud, ref_camera, splat_at)
+from refcases import (HostCloud, aerial_scene, axis_camera, cloud_from_rows, empty_cloud, random_cloud, ref_camera,
+                      splat_at)
 
 pytestmark = gpu
 
@@ -273,3 +274,60 @@ def test_depth_key_collisions_match_reference_order(n, spread):
     assert vis.sum() > 0.9 * n
     assert np.array_equal(got["visible"], want["visible"])
     assert np.array_equal(got["order"], want["order"])
+
+
+def with_sh1(hc, seed, amp=0.5):
+    """SH degree 1 copy (cloud.hpp:16-17): the band-0 colour plus random
+    band-1 coefficients (channel-major, cloud.cpp:180-193)."""
+    g = np.random.default_rng(seed)
+    feat = np.concatenate([hc.feat[:, :3], amp * g.standard_normal((hc.n, 9))], 1)
+    return HostCloud(hc.ids, hc.pos, hc.rot, hc.ls, feat, hc.op).narrowed()
+
+
+def _bench_scene_sh1(n, w, h, seed):
+    """The bench's aerial generator (5 degree tilt, no near-plane grazers: their
+    FP32 conic cancellation is covered by the degree-0 30-degree cases) with
+    band-1 features."""
+    from paper_2405_13943_b200.scene import aerial_scene as bench_scene
+    cl, cams = bench_scene(n, w, h, 4, 20.0, seed)
+    hc = HostCloud(cl["ids"], cl["pos"], cl["rot"], cl["ls"], cl["feat"], cl["op"])
+    c = cams[0]
+    cam = orc.Camera()
+    cam.fx, cam.fy, cam.cx, cam.cy = c.fx, c.fy, c.cx, c.cy
+    cam.set_rotation_quat(list(c.q))
+    cam.t = list(c.t)
+    cam.width, cam.height = c.width, c.height
+    return with_sh1(hc, 2), cam
+
+
+SH1_CASES = [("random90-sh1", with_sh1(random_cloud(400, 90), 1), ref_camera(64)),
+             ("aerial-sh1", *_bench_scene_sh1(20000, 160, 120, 5))]
+
+
+@pytest.mark.parametrize("name,cloud,cam", SH1_CASES, ids=[c[0] for c in SH1_CASES])
+def test_sh1_render_and_gradients(name, cloud, cam):
+    """SH degree 1 through every device stage: view-dependent colour in the
+    projection (bit-exact integer paths), the image, and the band-1 feature and
+    view-direction position gradients of the fold."""
+    assert cloud.fd == 12
+    b = new_block(cloud)
+    got = b.project(dev_cam(cam))
+    want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
+    assert np.array_equal(got["visible"], want["visible"])
+    assert np.array_equal(got["order"], want["order"])
+    rgb, T, n = b.render(dev_cam(cam))
+    wrgb, wT, wn = orc.render(cloud.oracle(), cam, orc.RenderConfig())
+    flips = n != wn
+    assert flips.mean() <= 1e-3
+    assert np.abs(rgb - wrgb)[~flips].max() <= 1e-4
+    gt = np.random.default_rng(4).uniform(0, 1, (cam.height, cam.width, 3))
+    g = b.render_backward(dev_cam(cam), gt)
+    w = orc.render_backward(cloud.oracle(), cam, gt, orc.RenderConfig())
+    assert g["loss"] == pytest.approx(w["loss"], rel=2e-5)
+    proj = want
+    grazing = proj["visible"].astype(bool) & (proj["depth"] < 1.0)
+    errs = grad_close({k: (v[~grazing] if k.startswith("g_") else v) for k, v in g.items()},
+                      {k: (v[~grazing] if k.startswith("g_") else v) for k, v in w.items()}, 1e-3)
+    for k, e in errs.items():
+        assert e <= 2e-3, (k, e)
+    assert g["g_feat"].shape[1] == 12 and np.abs(w["g_feat"][:, 3:]).max() > 0

@@ -101,10 +101,19 @@ def test_penalty_pulls_invisible_gaussian_on_device():
     np.testing.assert_allclose(got["pos"], want["pos"], atol=1e-4)
 
 
-def make_blocks_for_consensus(flip_ids=(3,)):
+def _sh1(hc, seed):
+    g = np.random.default_rng(seed)
+    feat = np.concatenate([hc.feat[:, :3], 0.3 * g.standard_normal((hc.n, 9))], 1)
+    return HostCloud(hc.ids, hc.pos, hc.rot, hc.ls, feat, hc.op)
+
+
+def make_blocks_for_consensus(flip_ids=(3,), fd=3):
     """Two blocks sharing ids {2..7} (block 0 owns 0..7, block 1 owns 2..11)."""
-    a = random_bundle(list(range(0, 8)), 40).narrowed()
-    b = random_bundle(list(range(2, 12)), 41).narrowed()
+    a = random_bundle(list(range(0, 8)), 40)
+    b = random_bundle(list(range(2, 12)), 41)
+    if fd == 12:
+        a, b = _sh1(a, 1), _sh1(b, 2)
+    a, b = a.narrowed(), b.narrowed()
     # shared rows of block 1 close to block 0's, with one antipodal quaternion
     for gid in range(2, 8):
         ia, ib = gid, gid - 2
@@ -112,7 +121,8 @@ def make_blocks_for_consensus(flip_ids=(3,)):
         b.rot[ib] = a.rot[ia] * (-1.0 if gid in flip_ids else 1.0)
     b = b.narrowed()
     shared = list(range(2, 8))
-    zprev = random_bundle(shared, 42).narrowed()
+    zprev = random_bundle(shared, 42)
+    zprev = (_sh1(zprev, 3) if fd == 12 else zprev).narrowed()
     return a, b, shared, zprev
 
 
@@ -127,9 +137,9 @@ def setup_device_block(hc, shared, block_id, zprev, rho):
     return dev
 
 
-@pytest.mark.parametrize("relax", [False, True])
-def test_consensus_round_matches_oracle(relax):
-    a, b, shared, zprev = make_blocks_for_consensus()
+@pytest.mark.parametrize("relax,fd", [(False, 3), (True, 3), (True, 12)])
+def test_consensus_round_matches_oracle(relax, fd):
+    a, b, shared, zprev = make_blocks_for_consensus(fd=fd)
     rho = api.penalties()
     da = setup_device_block(a, shared, 0, zprev, rho)
     db = setup_device_block(b, shared, 1, zprev, rho)
@@ -338,3 +348,23 @@ def test_nccl_round_path_single_rank():
     assert rb["rho"] == ra["rho"]
     np.testing.assert_allclose(zb, za, rtol=1e-6, atol=1e-7)
     np.testing.assert_allclose(ub, ua, rtol=1e-5, atol=1e-6)
+
+
+def test_sh1_train_steps_track_oracle():
+    """Adam and the fold over D = 23 components (SH degree 1)."""
+    s, init = toy_scene()
+    g = np.random.default_rng(7)
+    feat = np.concatenate([init.feat[:, :3], 0.3 * g.standard_normal((init.n, 9))], 1)
+    init = HostCloud(init.ids, init.pos, init.rot, init.ls, feat, init.op).narrowed()
+    tc = oracle_cfg(20)
+    t = orc.BlockTrainer(0, init.oracle(), s.views, s.images(), [], init.n, tc)
+    seq = orc.view_sequence(1, 0, len(s.views), 6)
+    b = device_trainer(init, s)
+    losses = b.train_steps(seq)
+    want_losses = [t.train_step() for _ in range(6)]
+    np.testing.assert_allclose(losses, want_losses, rtol=2e-4)
+    got = b.download_cloud()
+    want = HostCloud.from_oracle(t.cloud())
+    gr = np.concatenate([got["pos"], got["rot"], got["ls"], got["feat"], got["op"][:, None]], 1)
+    err = np.abs(gr - rows_of(want))
+    assert np.mean(err <= 1e-5 + 1e-5 * np.abs(rows_of(want))) >= 0.98

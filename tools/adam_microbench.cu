@@ -260,15 +260,15 @@ int main() {
             printf("%-28s best %7.1f us  %6.0f GB/s\n", name, best * 1e3, bytes / (best * 1e-3) / 1e9);
         };
         runp("prod scalar (10 comps)", b10, [&] {
-            bsg::adam_kernel<1><<<dim3((n + 1023) / 1024, 10), 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
+            bsg::adam_kernel<1><<<dim3((n + 1023) / 1024, 10), 256>>>(X, M, Vv, cap, n, vis, vis, G, nullptr, nullptr,
                                                                             nullptr, nullptr, 0, rho_d, st, pen); });
         runp("prod rot (4 comps)", b4, [&] {
-            bsg::adam_rot_kernel<<<(n + 255) / 256, 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
+            bsg::adam_rot_kernel<<<(n + 255) / 256, 256>>>(X, M, Vv, cap, n, vis, vis, G, nullptr, nullptr,
                                                                           nullptr, nullptr, 0, rho_d, st, pen); });
         runp("prod both", b10 + b4, [&] {
-            bsg::adam_kernel<1><<<dim3((n + 1023) / 1024, 10), 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
+            bsg::adam_kernel<1><<<dim3((n + 1023) / 1024, 10), 256>>>(X, M, Vv, cap, n, vis, vis, G, nullptr, nullptr,
                                                                             nullptr, nullptr, 0, rho_d, st, pen);
-            bsg::adam_rot_kernel<<<(n + 255) / 256, 256>>>(X, M, Vv, cap, n, vis, G, nullptr, nullptr,
+            bsg::adam_rot_kernel<<<(n + 255) / 256, 256>>>(X, M, Vv, cap, n, vis, vis, G, nullptr, nullptr,
                                                                           nullptr, nullptr, 0, rho_d, st, pen); });
     }
     CK(cudaDeviceSynchronize());
