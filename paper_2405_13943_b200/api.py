@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbsgpu.so")
+# BSG_LIB: developer override (A/B builds of the library); the default is the in-tree build.
+LIB_PATH = os.environ.get("BSG_LIB") or os.path.join(_HERE, "lib", "libbsgpu.so")
 
 BSG_OK = 0
 BSG_ERR_INVALID_ARGUMENT = 1
