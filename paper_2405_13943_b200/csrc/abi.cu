@@ -190,9 +190,13 @@ void ensure_image_buffers(Ctx* c, int W, int H) {
     }
 }
 
+// Tile-pair buffers grow geometrically (x2, at least the row count): a
+// reallocation frees and allocates device memory under a device-wide sync
+// (tens of ms for large buffers), so views with more pairs than seen so far
+// must not trigger one each time.
 void ensure_pair_capacity(Ctx* c, size_t P) {
     if (P <= c->pcap) return;
-    const size_t cap = P + P / 4 + 1024;
+    const size_t cap = std::max({2 * P, 2 * c->pcap, c->cap, static_cast<size_t>(1) << 20});
     for (int k = 0; k < 2; ++k) {
         dev_alloc(&c->pkey[k], cap);
         dev_alloc(&c->pval[k], cap);
