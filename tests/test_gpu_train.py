@@ -368,3 +368,36 @@ def test_sh1_train_steps_track_oracle():
     gr = np.concatenate([got["pos"], got["rot"], got["ls"], got["feat"], got["op"][:, None]], 1)
     err = np.abs(gr - rows_of(want))
     assert np.mean(err <= 1e-5 + 1e-5 * np.abs(rows_of(want))) >= 0.98
+
+
+@pytest.mark.parametrize("case", ["nothing-visible", "tiny-image", "empty-cloud"])
+def test_train_step_edge_cases_track_oracle(case):
+    """Steps where the raster has nothing to do (every splat culled; V = P = 0),
+    an image smaller than the SSIM window (ssim.cpp:12-14: SSIM = 1, zero
+    gradient), and an empty cloud: loss and the dense Adam (moments decay,
+    invisible rows move, trainer.cpp:267-281) still match the oracle."""
+    s, init = toy_scene()
+    views, imgs = list(s.views), s.images()
+    if case == "nothing-visible":
+        cam = orc.look_at([0.0, 0.0, 50.0], [0.0, 0.0, 100.0], [0.0, 1.0, 0.0], 30, 30, 16, 16, 32, 32)
+        views, imgs = [cam], [np.full((32, 32, 3), 0.25)]
+    elif case == "tiny-image":
+        cam = orc.look_at([0.0, 0.5, -6.0], [0.0, 0.0, 0.0], [0.0, 1.0, 0.0], 8, 8, 4, 4, 8, 8)
+        views, imgs = [cam], [np.full((8, 8, 3), 0.4)]
+    else:
+        init = HostCloud(np.zeros(0, np.uint64), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)),
+                         np.zeros((0, 3)), np.zeros(0))
+        views, imgs = views[:2], imgs[:2]
+    t = orc.BlockTrainer(0, init.oracle(), views, imgs, [], max(init.n, 1), oracle_cfg(20))
+    b = new_block(init)
+    b.set_views([dev_cam(v) for v in views], imgs)
+    b.trainer_init(api.trainer_config(iterations=20))
+    seq = orc.view_sequence(1, 0, len(views), 4)
+    losses = b.train_steps(seq)
+    want = [t.train_step() for _ in range(4)]
+    np.testing.assert_allclose(losses, want, rtol=2e-4, atol=1e-9)
+    if init.n:
+        got = b.download_cloud()
+        w = HostCloud.from_oracle(t.cloud())
+        g = np.concatenate([got["pos"], got["rot"], got["ls"], got["feat"], got["op"][:, None]], 1)
+        assert np.mean(np.abs(g - rows_of(w)) <= 1e-5 + 1e-5 * np.abs(rows_of(w))) >= 0.98
