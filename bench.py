@@ -382,6 +382,9 @@ def run_ours(args, rank, world, local_rank):
                    "shared_ids": info["shared_ids"], "l2": "inputs > L2 (Adam state 2M x 168 B)",
                    "parallelism": f"blocks{world}"},
         "e2e": {"value": 1000.0 / e2e_ms_step, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8},
+        # one global iteration = one local step of every block (Alg. 2); each GPU renders one full view per
+        # iteration whatever K is, so the job's view throughput is K x value
+        "block_steps_per_s": world * 1000.0 / ms_step,
         "gpu_launches": int(launches),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "stage_ms_note": f"separate {stage_steps}-step pass with CUDA events between stages (adds one host sync per step)",
