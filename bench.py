@@ -277,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
     blk.enable_stage_timing(True)
     stage_steps = min(args.steps, 100)
     stage_sum = {}
-    counters_sum = dict(visible=0, pairs=0)
+    counters_sum = dict(visible=0, pairs=0, blend_evals=0)
     for s in range(stage_steps):
         blk.train_steps([next_view()], want_losses=False)
         it += 1
@@ -287,6 +287,7 @@ def run_ours(args, rank, world, local_rank):
         c = blk.step_counters()
         counters_sum["visible"] += c["visible"]
         counters_sum["pairs"] += c["pairs"]
+        counters_sum["blend_evals"] += c["blend_evals"]
     consensus(it, flush=True)
     blk.enable_stage_timing(False)
 
@@ -362,6 +363,24 @@ def run_ours(args, rank, world, local_rank):
             roofline["compute"] = {"bound": "sm_issue", "issue_slots_busy_pct": round(km["issue_pct"], 1),
                                    "fma_pipe_pct": round(km["fma_pct"], 1), "alu_pipe_pct": round(km["alu_pct"], 1),
                                    "xu_pipe_pct": round(km["xu_pct"], 1), "source": km["capture"]}
+    # useful FP32 work of the blends: per composited (pixel, contributor)
+    # pair ~15 FLOP + 1 exp forward, ~40 FLOP + 1 exp + 1 reciprocal backward
+    evals = counters_sum["blend_evals"] / stage_steps
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12      # TFLOP/s at the sampled clock
+    mufu_peak = 148 * 16 * sm_mhz * 1e6 / 1e12           # T ops/s (16 MUFU lanes / SM)
+    blend_work = {}
+    for st, flop, mufu in (("blend_fwd", 15, 1), ("blend_bwd", 40, 2)):
+        if stage_ms.get(st):
+            t = stage_ms[st] * 1e-3
+            blend_work[st] = {"evaluations": evals, "tflops": evals * flop / t / 1e12,
+                              "fp32_frac": evals * flop / t / 1e12 / fp32_peak,
+                              "mufu_frac": evals * mufu / t / 1e12 / mufu_peak}
+    if roof_stage in blend_work:
+        roofline.setdefault("compute", {}).update({"fp32_tflops": round(blend_work[roof_stage]["tflops"], 3),
+                                                   "fp32_peak_tflops": round(fp32_peak, 1),
+                                                   "fp32_frac": round(blend_work[roof_stage]["fp32_frac"], 4),
+                                                   "mufu_frac": round(blend_work[roof_stage]["mufu_frac"], 4)})
     out = {
         "metric": "training iters/sec (K=N blocks, 1 block per GPU)",
         "value": 1000.0 / ms_step,
@@ -390,6 +409,8 @@ def run_ours(args, rank, world, local_rank):
         "stage_ms_note": f"separate {stage_steps}-step pass with CUDA events between stages (adds one host sync per step)",
         "dominant_stage": dominant,
         "visible_per_step": V,
+        "blend_evaluations_per_step": evals,
+        "blend_work": blend_work,
         "pairs_per_step": P,
         "consensus_ms_per_round": float(np.mean(round_ms)) if round_ms else 0.0,
         "consensus_ms_per_iter": (float(np.mean(round_ms)) / args.interval) if round_ms else 0.0,

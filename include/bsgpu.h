@@ -312,6 +312,10 @@ const char* bsg_stage_name(int i);
 int bsg_stage_times(bsg_ctx* ctx, double* ms);
 /* Counters of the most recent step: visible splats V, tile pairs P, kernels launched. */
 int bsg_step_counters(bsg_ctx* ctx, uint64_t* visible, uint64_t* pairs, uint64_t* launches);
+/* (pixel, contributor) pairs the forward blend composited in the last step
+ * (read only while stage timing is enabled; the FP32 work measure of the
+ * blend rooflines). */
+uint64_t bsg_step_blend_evals(const bsg_ctx* ctx);
 /* Kernel launches since context creation (all entry points). */
 uint64_t bsg_launch_count(const bsg_ctx* ctx);
 /* Opaque cudaStream_t of the context (for event timing by the caller). */

@@ -322,7 +322,10 @@ float* upload_gt_f64(Ctx* c, const double* gt, size_t px) {
 
 void collect_stage_times(Ctx* c) {
     if (!c->stage_timing) return;
+    BSG_CUDA(cudaMemcpyAsync(&c->counters_host->evals, &c->counters->evals, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c->stream));
     BSG_CUDA(cudaStreamSynchronize(c->stream));
+    c->last_evals = c->counters_host->evals;
     for (int s = 0; s < kStCount; ++s) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, c->ev[s], c->ev[s + 1]) != cudaSuccess) {
@@ -1380,6 +1383,8 @@ int bsg_step_counters(bsg_ctx* h, uint64_t* visible, uint64_t* pairs, uint64_t* 
         if (launches) *launches = c->step_launches;
     });
 }
+
+uint64_t bsg_step_blend_evals(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->last_evals : 0; }
 
 uint64_t bsg_launch_count(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->launches : 0; }
 

@@ -59,6 +59,7 @@ struct StepCounters {
     uint32_t dens_keep;    // densify: surviving rows
     uint32_t dens_children;// densify: added rows
     uint32_t pad3;
+    unsigned long long evals;  // (pixel, contributor) alpha evaluations composited by the forward blend
     unsigned long long zmin_inv;  // ~bits of the smallest visible FP64 depth (atomicMax of the complement)
     unsigned long long zmax;      // bits of the largest visible FP64 depth
     uint32_t depth_hist[8][256];  // digit histograms of the visible depth keys (filled by the compaction)
@@ -196,6 +197,7 @@ struct Ctx {
     float stage_ms[kStCount] = {};
     uint64_t launches = 0;
     uint64_t step_launches = 0;
+    uint64_t last_evals = 0;  // forward-blend evaluations of the last step (read when stage timing is on)
     StepCounters last_counters{};
 };
 

@@ -108,7 +108,8 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   float* __restrict__ out_rgb,
                                                                   float* __restrict__ out_T,
                                                                   uint32_t* __restrict__ out_n,
-                                                                  uint32_t* __restrict__ out_last) {
+                                                                  uint32_t* __restrict__ out_last,
+                                                                  unsigned long long* __restrict__ evals) {
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint8_t s_m[kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
@@ -203,6 +204,11 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
             }
         }
     }
+    // work counter for the FP32 roofline: composited (pixel, contributor) pairs
+    uint32_t ev = n0 + n1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    if (lane == 0 && ev) atomicAdd(evals, static_cast<unsigned long long>(ev));
     if (in0) {
         const size_t p = static_cast<size_t>(py0) * W + px;
         out_rgb[3 * p + 0] = r0 + T0 * bg0;
@@ -438,7 +444,7 @@ void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     blend_fwd_kernel<<<ntiles, kBlendThreads, 0, c->stream>>>(
         c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, rc.tstop,
         static_cast<float>(rc.alpha_clamp), rc.alpha_clamp, rc.bg[0], rc.bg[1], rc.bg[2], c->out_rgb, c->out_T,
-        c->out_n, c->out_last);
+        c->out_n, c->out_last, &c->counters->evals);
     BSG_LAUNCHED(c);
 }
 
