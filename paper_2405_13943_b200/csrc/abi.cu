@@ -87,6 +87,8 @@ void free_all(Ctx* c) {
     for (float* p : c->view_gt)
         if (p) cudaFree(p);
     if (c->counters_host) cudaFreeHost(c->counters_host);
+    if (c->mbox) cudaFreeHost(c->mbox);
+    if (c->lb_ticket) cudaFree(c->lb_ticket);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->nccl) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl));
@@ -214,6 +216,10 @@ int tile_bits(const DevCam& cam) {
 }
 
 // K1-K5: projection, compaction, depth sort, pair emission, tile sort, ranges.
+// No stream synchronisation on the common path: the compaction and the
+// pair-offset scan publish V and P to the host-mapped mailbox, and the host
+// polls for each while the kernel enqueued behind it (depth histograms, pair
+// emission into the current capacity) keeps the GPU busy.
 void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     ensure_image_buffers(c, cam.W, cam.H);
     BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
@@ -221,50 +227,80 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     launch_preprocess(c, cam, rc);
     stage_end(c, kStPreprocess);
     stage_begin(c, kStCompact);
-    compact_visible(c, static_cast<uint32_t>(c->n), true);  // + digit histograms of the 32-bit depth keys
+    uint32_t V = 0, kbits = 16;
+    uint32_t* k32[2] = {reinterpret_cast<uint32_t*>(c->vkey[0]), reinterpret_cast<uint32_t*>(c->vkey[1])};
+    if (c->n) {
+        Publish pv;
+        pv.val = &c->mbox->V;
+        pv.seq_word = &c->mbox->seq_v;
+        pv.seq = ++c->mbox_seq;
+        pv.extra_src = &c->counters->visible_pre;
+        pv.extra_dst = &c->mbox->visible_pre;
+        compact_visible(c, static_cast<uint32_t>(c->n), true, pv);
+        launch_depth_hist(c, k32[0]);  // digit histograms of the 32-bit depth keys
+        wait_mailbox(c, &c->mbox->seq_v, pv.seq);
+        V = c->mbox->V;
+        kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
+    } else {
+        compact_visible(c, 0, true);
+    }
     stage_end(c, kStCompact);
-    // One readback: V (sizes the depth key and the sort).
-    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, depth_hist), cudaMemcpyDeviceToHost,
-                             c->stream));
-    BSG_CUDA(cudaStreamSynchronize(c->stream));
-    const uint32_t V = c->counters_host->visible;
     stage_begin(c, kStDepthSort);
     // (depth, index) order (renderer.cpp:86-89): stable LSD sort of the 32-bit
     // range-normalised depth key over rows in ascending index order, then runs
     // of equal keys sorted by the full FP64 depth. A run longer than 64 that is
     // out of order falls back to all 8 digit passes of the FP64 bits.
-    uint32_t* k32[2] = {reinterpret_cast<uint32_t*>(c->vkey[0]), reinterpret_cast<uint32_t*>(c->vkey[1])};
-    radix_sort_u32_hist(c, k32, c->vrow, V, depth_key_bits(V) / 8, &c->counters->depth_hist[0][0],
-                        &c->depth_sorted);
+    c->depth_sorted = 0;
+    if (V > 1)
+        radix_sort_u32(c, k32, c->vrow, V, 0, static_cast<int>(kbits / 8), &c->counters->depth_hist[0][0], nullptr,
+                       &c->depth_sorted);
     depth_tie_fixup(c, k32[c->depth_sorted], c->vrow[c->depth_sorted], c->depth_key, V, &c->counters->overflow);
     stage_end(c, kStDepthSort);
     stage_begin(c, kStPairs);
-    scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
-    BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, 16, cudaMemcpyDeviceToHost, c->stream));
-    BSG_CUDA(cudaStreamSynchronize(c->stream));
-    if (c->counters_host->overflow) {
-        // rare: a long out-of-order run of equal 32-bit keys -> full 64-bit sort
-        BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
-        compact_visible(c, static_cast<uint32_t>(c->n), false);
-        BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist),
-                                 cudaMemcpyDeviceToHost, c->stream));
-        BSG_CUDA(cudaStreamSynchronize(c->stream));
-        radix_sort_u64(c, c->vkey, c->vrow, V, 0, 8, &c->counters->depth_hist[0][0],
-                       &c->counters_host->depth_hist[0][0], &c->depth_sorted);
-        scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
-        BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, 16, cudaMemcpyDeviceToHost, c->stream));
-        BSG_CUDA(cudaStreamSynchronize(c->stream));
+    uint32_t P = 0;
+    if (V) {
+        Publish pp;
+        pp.val = &c->mbox->P;
+        pp.seq_word = &c->mbox->seq_p;
+        pp.seq = ++c->mbox_seq;
+        pp.extra_src = &c->counters->overflow;
+        pp.extra_dst = &c->mbox->overflow;
+        scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs, pp);
+        launch_pairs(c, cam, V);  // into the current capacity; + digit histograms of the tile keys
+        wait_mailbox(c, &c->mbox->seq_p, pp.seq);
+        P = c->mbox->P;
+        bool redo = false;
+        if (c->mbox->overflow) {
+            // rare: a long out-of-order run of equal 32-bit keys -> full 64-bit sort
+            BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
+            compact_visible(c, static_cast<uint32_t>(c->n), false);
+            BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, offsetof(StepCounters, tile_hist),
+                                     cudaMemcpyDeviceToHost, c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            radix_sort_u64(c, c->vkey, c->vrow, V, 0, 8, &c->counters->depth_hist[0][0],
+                           &c->counters_host->depth_hist[0][0], &c->depth_sorted);
+            scan_exclusive_u32(c, c->tiles, c->vrow[c->depth_sorted], c->poff, V, &c->counters->pairs);
+            BSG_CUDA(cudaMemcpyAsync(c->counters_host, c->counters, 16, cudaMemcpyDeviceToHost, c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            P = c->counters_host->pairs;
+            redo = true;
+        }
+        if (P > c->pcap) {
+            ensure_pair_capacity(c, P);
+            redo = true;
+        }
+        if (redo) {  // the emission ran against the old order or capacity
+            BSG_CUDA(cudaMemsetAsync(&c->counters->tile_hist[0][0], 0, sizeof(c->counters->tile_hist), c->stream));
+            launch_pairs(c, cam, V);
+        }
     }
-    const uint32_t P = V ? c->counters_host->pairs : 0;
-    ensure_pair_capacity(c, P);
-    launch_pairs(c, cam, V);  // + digit histograms of the tile keys
     stage_end(c, kStPairs);
     stage_begin(c, kStTileSort);
     const int passes = (tile_bits(cam) + 7) / 8;
     radix_sort_u32(c, c->pkey, c->pval, P, 0, passes, &c->counters->tile_hist[0][0], nullptr, &c->pairs_sorted);
     stage_end(c, kStTileSort);
     stage_begin(c, kStRanges);
-    launch_ranges(c, cam, P);
+    launch_ranges(c, cam, V, P);
     stage_end(c, kStRanges);
     c->last_counters.visible = V;
     c->last_counters.pairs = P;
@@ -370,8 +406,7 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     c->step_launches = 0;
     const DevCam cam = make_cam(view);
     const DevRender rc = make_render(c->tcfg.render);
-    BSG_CUDA(cudaMemsetAsync(c->scalars, 0, sizeof(StepScalars), c->stream));
-    project_and_bin(c, cam, rc);
+    project_and_bin(c, cam, rc);  // (the preprocess zeroes the step scalars)
     stage_begin(c, kStBlendFwd);
     launch_blend_fwd(c, cam, rc);
     stage_end(c, kStBlendFwd);
@@ -552,6 +587,8 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             dev_alloc(&c->rho_state, 5);
             dev_alloc(&c->g2d_wide, 9 * static_cast<size_t>(kWideCap));
             BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
+            BSG_CUDA(cudaHostAlloc(&c->mbox, sizeof(Mailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+            std::memset(c->mbox, 0, sizeof(Mailbox));
             dev_alloc(&c->counters, 1);
             dev_alloc(&c->scalars, 1);
             dev_alloc(&c->radix_hist, 1);

@@ -66,6 +66,32 @@ struct StepCounters {
     uint32_t tile_hist[2][256];   // digit histograms of the tile keys (filled by the pair emission)
 };
 
+// Host-mapped pinned mailbox: the compaction and the pair-offset scan write
+// their totals here (value, then __threadfence_system, then the sequence
+// word), so the host learns V and P by polling instead of a copy + stream
+// sync, while the kernel enqueued behind them keeps the GPU busy.
+struct Mailbox {
+    uint32_t seq_v, V, visible_pre, pad0;
+    uint32_t seq_p, P, overflow, pad1;
+};
+
+// Where a scan's final CTA publishes its total (all null: nowhere).
+struct Publish {
+    uint32_t* val = nullptr;
+    uint32_t* seq_word = nullptr;
+    uint32_t seq = 0;
+    const uint32_t* extra_src = nullptr;  // copied to extra_dst before the sequence word
+    uint32_t* extra_dst = nullptr;
+};
+
+// One decoupled look-back launch: status words carry the launch's epoch (no
+// zeroing between launches), tile ids come from a monotonic 64-bit ticket.
+struct Lookback {
+    unsigned long long* ticket;
+    unsigned long long base;
+    uint32_t epoch;
+};
+
 // Scalars reduced on the device every step.
 struct StepScalars {
     double l1_sum;
@@ -130,10 +156,15 @@ struct Ctx {
     size_t ranges_cap = 0;
 
     // radix / scan scratch
-    uint32_t* scan_status = nullptr;   // decoupled look-back status words
+    unsigned long long* scan_status = nullptr;   // decoupled look-back status words (epoch-tagged)
     size_t scan_status_cap = 0;
-    uint32_t* radix_status = nullptr;
+    unsigned long long* radix_status = nullptr;
     size_t radix_status_cap = 0;
+    unsigned long long* lb_ticket = nullptr;  // [2] monotonic tile tickets (scan, radix)
+    unsigned long long lb_next[2] = {0, 0};   // host mirror of the tickets handed out
+    uint32_t lb_epoch = 0;
+    Mailbox* mbox = nullptr;                  // host-mapped pinned
+    uint32_t mbox_seq = 0;
     uint32_t* radix_hist = nullptr;    // [8 passes][256]
     uint32_t* counters_dev = nullptr;  // tile-id tickets
     StepCounters* counters = nullptr;  // device
@@ -236,12 +267,16 @@ __host__ __device__ inline int depth_key_bits(uint32_t V) {
 // Exclusive scan of n u32 values read through a gather (in[idx ? idx[i] : i]),
 // optional predicate compaction. Result in out; total in *total_dev.
 void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,
-                        uint32_t* total_dev);
+                        uint32_t* total_dev, const Publish& pub = Publish{});
+// Look-back bookkeeping for one launch of `grid` CTAs (which: 0 scan, 1 radix).
+Lookback next_lookback(Ctx* c, int which, uint32_t grid);
+// Polls the mailbox until *seq_word == seq (checks the stream for errors while waiting).
+void wait_mailbox(Ctx* c, const volatile uint32_t* seq_word, uint32_t seq);
 // Stable compaction of rows with tiles[i] > 0: writes keys/rows in row order and V.
 // key32: the 32-bit range-normalised depth key (bits(z) - bits(zmin)) >> shift
 // into vkey (as u32) with its 4 digit histograms; otherwise the full FP64 bits
 // with all 8 digit histograms.
-void compact_visible(Ctx* c, uint32_t n, bool key32);
+void compact_visible(Ctx* c, uint32_t n, bool key32, const Publish& pub = Publish{});
 // Stable LSD radix sort (onesweep) of (u64 key, u32 val) / (u32 key, u32 val)
 // over `passes` 8-bit digits from bit 0. d_hist holds the per-pass digit
 // counts (produced by the kernel that wrote the keys) and is turned into
@@ -251,10 +286,11 @@ void radix_sort_u64(Ctx* c, uint64_t* keys[2], uint32_t* vals[2], uint32_t n, in
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel);
 void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int first_pass, int passes,
                     uint32_t* d_hist, const uint32_t* h_hist, int* sel);
-// As radix_sort_u32 over `passes` digits from bit 0, building the digit
-// histograms itself from keys[0] (no pass skipping).
-void radix_sort_u32_hist(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
-                         int* sel);
+// Digit histograms of the compacted 32-bit depth keys into counters->depth_hist
+// (zeroed by the step's counter reset); n and the digit count come from the
+// device counters (visible, depth_key_bits(visible_pre)), so it is enqueued
+// before the host knows V.
+void launch_depth_hist(Ctx* c, const uint32_t* keys);
 // Sorts runs of equal 32-bit depth keys by the full FP64 depth bits of their
 // rows (stable); sets *long_run if a run exceeds 64 (caller redoes the full sort).
 void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,
@@ -265,7 +301,7 @@ DevCam make_cam(const bsg_camera& c);
 DevRender make_render(const bsg_render_config& r);
 void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V);
-void launch_ranges(Ctx* c, const DevCam& cam, uint32_t P);
+void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P);
 void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt);
 void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc);

@@ -44,7 +44,8 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  float4* __restrict__ g2d,
                                                                  double* __restrict__ g2d_wide,
                                                                  float4* __restrict__ pcache,
-                                                                 StepCounters* __restrict__ counters) {
+                                                                 StepCounters* __restrict__ counters,
+                                                                 StepScalars* __restrict__ scalars) {
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint32_t s_count;
     __shared__ unsigned long long s_zmin_inv, s_zmax;
@@ -55,6 +56,9 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
         s_zmin_inv = 0;
         s_zmax = 0;
     }
+    // the step's loss / penalty sums start from zero (accumulated by later kernels)
+    if (blockIdx.x == 0 && threadIdx.x < sizeof(StepScalars) / sizeof(double))
+        reinterpret_cast<double*>(scalars)[threadIdx.x] = 0.0;
     __syncthreads();
     const uint32_t chunk0 = blockIdx.x * kPreChunk;
     const float fxf = static_cast<float>(cam.fx), fyf = static_cast<float>(cam.fy);
@@ -292,10 +296,14 @@ DevRender make_render(const bsg_render_config& r) {
 }
 
 void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
-    if (c->n == 0) return;
+    if (c->n == 0) {
+        BSG_CUDA(cudaMemsetAsync(c->scalars, 0, sizeof(StepScalars), c->stream));
+        return;
+    }
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     preprocess_kernel<<<blocks, kPreThreads, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
-                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters);
+                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters,
+                                                      c->scalars);
     BSG_LAUNCHED(c);
 }
 

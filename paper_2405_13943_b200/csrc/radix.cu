@@ -16,28 +16,12 @@ constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr uint32_t kStAgg = 1u << 30, kStInc = 2u << 30, kStMask = (1u << 30) - 1;
 
-// In-place exclusive scan of each pass's 256 bins (one block per pass).
-__global__ void radix_offsets_kernel(uint32_t* hist) {
-    __shared__ uint32_t s[256];
-    uint32_t* h = hist + blockIdx.x * 256;
-    const uint32_t v = h[threadIdx.x];
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {
-        const uint32_t y = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
-        __syncthreads();
-        s[threadIdx.x] += y;
-        __syncthreads();
-    }
-    h[threadIdx.x] = s[threadIdx.x] - v;
-}
-
 template <typename K, int kRsItems>
 __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                               K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                               uint32_t n, int shift,
-                                                              const uint32_t* __restrict__ pass_offsets,
-                                                              uint32_t* status, uint32_t* ticket) {
+                                                              const uint32_t* __restrict__ pass_hist,
+                                                              unsigned long long* status, Lookback lb) {
     constexpr int kRsTile = kRsThreads * kRsItems;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s_keys = reinterpret_cast<K*>(smem_raw);
@@ -46,10 +30,11 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
     __shared__ uint32_t s_start[256];
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_scan[kRsWarps];
+    __shared__ uint32_t s_gscan[kRsWarps];
     __shared__ uint32_t s_tile;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    if (threadIdx.x == 0) s_tile = static_cast<uint32_t>(atomicAdd(lb.ticket, 1ull) - lb.base);
     for (int i = threadIdx.x; i < kRsWarps * 256; i += kRsThreads) (&s_whist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -96,42 +81,57 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
         s_whist[w][d] = cnt;
         cnt += c;
     }
-    // Publish this tile's count, then look back for the global prefix.
-    volatile uint32_t* st = status;
+    // Publish this tile's count, then look back for the global prefix. Status
+    // word: [epoch 32 | flag 2 | count 30]; other launches' words read as unset.
+    const unsigned long long tag = static_cast<unsigned long long>(lb.epoch) << 32;
+    volatile unsigned long long* st = status;
     if (tile == 0) {
-        atomicExch(&status[d], kStInc | cnt);
+        atomicExch(&status[d], tag | kStInc | cnt);
     } else {
-        atomicExch(&status[static_cast<uint64_t>(tile) * 256 + d], kStAgg | cnt);
+        atomicExch(&status[static_cast<uint64_t>(tile) * 256 + d], tag | kStAgg | cnt);
     }
-    // Block-local exclusive scan over digits (for the shared-memory scatter).
+    // Block-local exclusive scans over digits: this tile's counts (for the
+    // shared-memory scatter) and the pass histogram (global digit offsets).
+    const uint32_t hcnt = pass_hist[d];
     {
-        uint32_t inc = cnt;
+        uint32_t inc = cnt, ginc = hcnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+            const uint32_t gy = __shfl_up_sync(0xffffffffu, ginc, o);
+            if (lane >= o) {
+                inc += y;
+                ginc += gy;
+            }
         }
-        if (lane == 31) s_scan[warp] = inc;
+        if (lane == 31) {
+            s_scan[warp] = inc;
+            s_gscan[warp] = ginc;
+        }
         __syncthreads();
-        uint32_t wp = 0;
-        for (int w = 0; w < warp; ++w) wp += s_scan[w];
+        uint32_t wp = 0, gwp = 0;
+        for (int w = 0; w < warp; ++w) {
+            wp += s_scan[w];
+            gwp += s_gscan[w];
+        }
         s_start[d] = wp + inc - cnt;
+        s_base[d] = gwp + ginc - hcnt;
     }
     uint32_t prefix = 0;
     if (tile > 0) {
         int64_t p = static_cast<int64_t>(tile) - 1;
         while (p >= 0) {
-            uint32_t s;
+            unsigned long long s;
             do {
                 s = st[static_cast<uint64_t>(p) * 256 + d];
-            } while ((s & ~kStMask) == 0);
-            prefix += s & kStMask;
+            } while ((s >> 32) != lb.epoch || (s & ~static_cast<unsigned long long>(kStMask) & 0xffffffffull) == 0);
+            prefix += static_cast<uint32_t>(s) & kStMask;
             if (s & kStInc) break;
             --p;
         }
-        atomicExch(&status[static_cast<uint64_t>(tile) * 256 + d], kStInc | (prefix + cnt));
+        atomicExch(&status[static_cast<uint64_t>(tile) * 256 + d], tag | kStInc | (prefix + cnt));
     }
-    s_base[d] = pass_offsets[d] + prefix;
+    s_base[d] += prefix;
     __syncthreads();
 
 #pragma unroll
@@ -154,17 +154,19 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
     }
 }
 
-// Digit histograms of `passes` 8-bit digits over n keys (for keys whose
-// producer did not build them): shared-memory counts per CTA, one global
-// atomic per non-empty bin.
-template <typename K>
-__global__ __launch_bounds__(256) void digit_hist_kernel(const K* __restrict__ keys, uint32_t n, int passes,
-                                                         uint32_t* __restrict__ hist) {
+// Digit histograms of the 8-bit digits of the V compacted 32-bit depth keys
+// (V and the key width read from the step counters): shared-memory counts
+// per CTA, one global atomic per non-empty bin.
+__global__ __launch_bounds__(256) void depth_hist_kernel(const uint32_t* __restrict__ keys,
+                                                         StepCounters* __restrict__ cnt) {
     __shared__ uint32_t s_h[4 * 256];
+    const uint32_t n = cnt->visible;
+    const int passes = depth_key_bits(cnt->visible_pre) / 8;
+    uint32_t* hist = &cnt->depth_hist[0][0];
     for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) s_h[k] = 0;
     __syncthreads();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const K key = keys[i];
+        const uint32_t key = keys[i];
         for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * 256 + ((key >> (8 * p)) & 0xffu)], 1u);
     }
     __syncthreads();
@@ -177,11 +179,12 @@ void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_
                    const uint32_t* h_hist, int* sel) {
     constexpr int kTileKeys = kRsThreads * ITEMS;
     const uint32_t tiles = (n + kTileKeys - 1) / kTileKeys;
-    const size_t need = (static_cast<size_t>(tiles) * 256 + 64) * sizeof(uint32_t);
+    const size_t need = static_cast<size_t>(tiles) * 256;
     if (c->radix_status_cap < need) {
         if (c->radix_status) cudaFree(c->radix_status);
-        BSG_CUDA(cudaMalloc(&c->radix_status, need * 2));
-        c->radix_status_cap = need * 2;
+        BSG_CUDA(cudaMalloc(&c->radix_status, 2 * need * sizeof(unsigned long long)));
+        BSG_CUDA(cudaMemset(c->radix_status, 0, 2 * need * sizeof(unsigned long long)));  // epoch 0 is never used
+        c->radix_status_cap = 2 * need;
     }
     const size_t smem = (sizeof(K) + sizeof(uint32_t)) * kTileKeys;
     BSG_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -194,10 +197,9 @@ void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_
                 if (h_hist[p * 256 + d] == n) trivial = true;
             if (trivial) continue;
         }
-        BSG_CUDA(cudaMemsetAsync(c->radix_status, 0, need, c->stream));
+        const Lookback lb = next_lookback(c, 1, tiles);
         onesweep_kernel<K, ITEMS><<<tiles, kRsThreads, smem, c->stream>>>(
-            keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, d_hist + p * 256, c->radix_status + 64,
-            c->radix_status);
+            keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, d_hist + p * 256, c->radix_status, lb);
         BSG_LAUNCHED(c);
         cur ^= 1;
     }
@@ -210,8 +212,6 @@ void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pas
     *sel = 0;
     if (n <= 1) return;
     if (n >= (1u << 30)) throw Error{BSG_ERR_CAPACITY, "radix sort supports < 2^30 keys"};
-    radix_offsets_kernel<<<passes - first_pass, 256, 0, c->stream>>>(d_hist + 256 * first_pass);
-    BSG_LAUNCHED(c);
     // Tile size: the passes are look-back-latency bound at the sizes of a step
     // (V ~ 2e5 keys, P ~ 4e5 pairs); 2k-key tiles measured best there (cfg 2:
     // depth sort 79 -> 71 us, tile sort 52 -> 43 us vs 1k-key tiles); only tiny
@@ -293,16 +293,10 @@ void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, in
     radix_sort<uint32_t>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
 }
 
-void radix_sort_u32_hist(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, int passes, uint32_t* d_hist,
-                         int* sel) {
-    *sel = 0;
-    if (n <= 1) return;
-    if (passes > 4) throw Error{BSG_ERR_INVALID_ARGUMENT, "at most 4 digit passes"};
-    BSG_CUDA(cudaMemsetAsync(d_hist, 0, passes * 256 * sizeof(uint32_t), c->stream));
-    const unsigned grid = std::min<unsigned>((n + 4095) / 4096, 148);  // few CTAs: one global atomic per bin each
-    digit_hist_kernel<uint32_t><<<grid, 256, 0, c->stream>>>(keys[0], n, passes, d_hist);
+void launch_depth_hist(Ctx* c, const uint32_t* keys) {
+    const unsigned grid = std::min<unsigned>(static_cast<unsigned>((c->n + 4095) / 4096), 148);  // upper bound V <= n
+    depth_hist_kernel<<<std::max(grid, 1u), 256, 0, c->stream>>>(keys, c->counters);
     BSG_LAUNCHED(c);
-    radix_sort<uint32_t>(c, keys, vals, n, 0, passes, d_hist, nullptr, sel);
 }
 
 void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,

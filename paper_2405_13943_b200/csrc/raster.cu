@@ -42,9 +42,13 @@ __global__ __launch_bounds__(256) void emit_pairs_kernel(const uint32_t* __restr
                                                          const uint32_t* __restrict__ offsets,
                                                          const float4* __restrict__ rec, uint32_t V, int tiles_x,
                                                          uint32_t* __restrict__ pkey, uint32_t* __restrict__ pval,
-                                                         uint32_t pcap, uint32_t* __restrict__ hist) {
+                                                         uint32_t pcap, uint32_t* __restrict__ hist,
+                                                         uint2* __restrict__ ranges, uint32_t ntiles) {
     __shared__ uint32_t s_hist[2 * 256];
     for (int k = threadIdx.x; k < 512; k += blockDim.x) s_hist[k] = 0;
+    // tiles without pairs keep the empty range (ranges_kernel writes the rest)
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
+        ranges[t] = make_uint2(0u, 0u);
     __syncthreads();
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p < V) {
@@ -425,15 +429,17 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
 
 void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
+    const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
     emit_pairs_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(c->vrow[c->depth_sorted], c->poff, c->rec, V, cam.tiles_x,
                                                               c->pkey[0], c->pval[0], static_cast<uint32_t>(c->pcap),
-                                                              &c->counters->tile_hist[0][0]);
+                                                              &c->counters->tile_hist[0][0], c->ranges, ntiles);
     BSG_LAUNCHED(c);
 }
 
-void launch_ranges(Ctx* c, const DevCam& cam, uint32_t P) {
+// V > 0: the pair emission already cleared the tile ranges.
+void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P) {
     const size_t ntiles = static_cast<size_t>(cam.tiles_x) * cam.tiles_y;
-    BSG_CUDA(cudaMemsetAsync(c->ranges, 0, ntiles * sizeof(uint2), c->stream));
+    if (V == 0) BSG_CUDA(cudaMemsetAsync(c->ranges, 0, ntiles * sizeof(uint2), c->stream));
     if (P == 0) return;
     ranges_kernel<<<(P + 255) / 256, 256, 0, c->stream>>>(c->pkey[c->pairs_sorted], P, c->ranges);
     BSG_LAUNCHED(c);

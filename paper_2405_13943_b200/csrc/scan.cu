@@ -3,6 +3,8 @@
 // passes: one read of the input, one write of the output.
 #include "bsg_internal.cuh"
 
+#include <atomic>
+
 namespace bsg {
 namespace {
 
@@ -11,12 +13,14 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr uint32_t kFlagAgg = 1u, kFlagInc = 2u;
 
-__device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_t v) {
-    return (static_cast<unsigned long long>(flag) << 32) | v;
+// Status word: [epoch 30 | flag 2 | value 32]. A word from another launch
+// (other epoch) reads as "not yet published", so the buffer is never cleared.
+__device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32_t flag, uint32_t v) {
+    return (static_cast<unsigned long long>(epoch) << 34) | (static_cast<unsigned long long>(flag) << 32) | v;
 }
 
-__device__ __forceinline__ void publish(unsigned long long* st, uint32_t flag, uint32_t v) {
-    atomicExch(st, pack_status(flag, v));
+__device__ __forceinline__ void publish(unsigned long long* st, uint32_t epoch, uint32_t flag, uint32_t v) {
+    atomicExch(st, pack_status(epoch, flag, v));
 }
 
 // Block-wide exclusive scan of one value per thread; returns the exclusive
@@ -47,7 +51,7 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_warp
 }
 
 // Warp 0 walks predecessors 32 at a time until it meets an inclusive prefix.
-__device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32_t tile) {
+__device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32_t tile, uint32_t epoch) {
     const int lane = threadIdx.x & 31;
     uint32_t prefix = 0;
     int64_t window = static_cast<int64_t>(tile) - 1;
@@ -58,7 +62,7 @@ __device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32
         if (p >= 0) {
             do {
                 st = *reinterpret_cast<volatile unsigned long long*>(&status[p]);
-                flag = static_cast<uint32_t>(st >> 32);
+                flag = static_cast<uint32_t>(st >> 34) == epoch ? static_cast<uint32_t>(st >> 32) & 3u : 0u;
             } while (flag == 0);
         }
         const uint32_t inc_mask = __ballot_sync(0xffffffffu, flag == kFlagInc);
@@ -82,7 +86,7 @@ template <int MODE>
 __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __restrict__ in,
                                                             const uint32_t* __restrict__ gather,
                                                             uint32_t* __restrict__ out, uint32_t n,
-                                                            unsigned long long* status, uint32_t* ticket,
+                                                            unsigned long long* status, Lookback lb, Publish pub,
                                                             uint32_t* total_out, const uint64_t* __restrict__ keys,
                                                             void* __restrict__ out_keys_v,
                                                             const StepCounters* __restrict__ range,
@@ -94,7 +98,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
     __shared__ uint32_t s_warp[kScanThreads / 32];
     constexpr int kDigits = 8;
     __shared__ uint32_t s_hist[MODE == 1 ? kDigits * 256 : 1];
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    if (threadIdx.x == 0) s_tile = static_cast<uint32_t>(atomicAdd(lb.ticket, 1ull) - lb.base);
     if (MODE == 1)
         for (int k = threadIdx.x; k < kDigits * 256; k += kScanThreads) s_hist[k] = 0;
     unsigned long long zmin = 0;
@@ -140,20 +144,29 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         const uint32_t total = s_total;
         if (tile == 0) {
             if (threadIdx.x == 0) {
-                publish(&status[0], kFlagInc, total);
+                publish(&status[0], lb.epoch, kFlagInc, total);
                 s_prefix = 0;
             }
         } else {
-            if (threadIdx.x == 0) publish(&status[tile], kFlagAgg, total);
-            const uint32_t prefix = look_back(status, tile);
+            if (threadIdx.x == 0) publish(&status[tile], lb.epoch, kFlagAgg, total);
+            const uint32_t prefix = look_back(status, tile, lb.epoch);
             if (threadIdx.x == 0) {
-                publish(&status[tile], kFlagInc, prefix + total);
+                publish(&status[tile], lb.epoch, kFlagInc, prefix + total);
                 s_prefix = prefix;
             }
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && (static_cast<uint64_t>(tile) + 1) * kScanTile >= n && total_out) *total_out = s_prefix + s_total;
+    if (threadIdx.x == 0 && (static_cast<uint64_t>(tile) + 1) * kScanTile >= n) {
+        const uint32_t grand = s_prefix + s_total;
+        if (total_out) *total_out = grand;
+        if (pub.seq_word) {  // host-mapped mailbox: value(s), system fence, sequence word
+            *reinterpret_cast<volatile uint32_t*>(pub.val) = grand;
+            if (pub.extra_dst) *reinterpret_cast<volatile uint32_t*>(pub.extra_dst) = *pub.extra_src;
+            __threadfence_system();
+            *reinterpret_cast<volatile uint32_t*>(pub.seq_word) = pub.seq;
+        }
+    }
     uint32_t run = s_prefix + tprefix;
     const int lane = threadIdx.x & 31;
     if (MODE != 0 && (threadIdx.x & 3) == 0 && base / 32 < mask_words)
@@ -207,49 +220,88 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
 }
 
 void prepare_status(Ctx* c, uint32_t tiles) {
-    const size_t need = (static_cast<size_t>(tiles) + 2) * sizeof(unsigned long long);
+    const size_t need = static_cast<size_t>(tiles) + 1;
     if (c->scan_status_cap < need) {
         if (c->scan_status) cudaFree(c->scan_status);
-        BSG_CUDA(cudaMalloc(&c->scan_status, need * 2));
-        c->scan_status_cap = need * 2;
+        BSG_CUDA(cudaMalloc(&c->scan_status, 2 * need * sizeof(unsigned long long)));
+        BSG_CUDA(cudaMemset(c->scan_status, 0, 2 * need * sizeof(unsigned long long)));  // epoch 0 is never used
+        c->scan_status_cap = 2 * need;
     }
-    BSG_CUDA(cudaMemsetAsync(c->scan_status, 0, need, c->stream));
 }
 
 }  // namespace
 
+Lookback next_lookback(Ctx* c, int which, uint32_t grid) {
+    if (!c->lb_ticket) {
+        BSG_CUDA(cudaMalloc(&c->lb_ticket, 2 * sizeof(unsigned long long)));
+        BSG_CUDA(cudaMemset(c->lb_ticket, 0, 2 * sizeof(unsigned long long)));
+        c->lb_next[0] = c->lb_next[1] = 0;
+    }
+    c->lb_epoch = (c->lb_epoch + 1) & 0x3fffffffu;
+    if (c->lb_epoch == 0) c->lb_epoch = 1;
+    Lookback lb{c->lb_ticket + which, c->lb_next[which], c->lb_epoch};
+    c->lb_next[which] += grid;
+    return lb;
+}
+
+void wait_mailbox(Ctx* c, const volatile uint32_t* seq_word, uint32_t seq) {
+    for (uint32_t it = 1;; ++it) {
+        if (*seq_word == seq) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            return;
+        }
+        if ((it & 255u) == 0) {  // a failed or finished stream never writes it
+            const cudaError_t e = cudaStreamQuery(c->stream);
+            if (e == cudaSuccess) {
+                if (*seq_word == seq) {
+                    std::atomic_thread_fence(std::memory_order_acquire);
+                    return;
+                }
+                throw Error{BSG_ERR_CUDA, "stream completed without writing the mailbox"};
+            }
+            if (e != cudaErrorNotReady) BSG_CUDA(e);
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#elif defined(__aarch64__)
+        asm volatile("yield");
+#endif
+    }
+}
+
 void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,
-                        uint32_t* total_dev) {
+                        uint32_t* total_dev, const Publish& pub) {
     if (n == 0) {
         BSG_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), c->stream));
+        if (pub.seq_word) throw Error{BSG_ERR_STATE, "empty scan cannot publish"};
         return;
     }
     const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
     prepare_status(c, tiles);
-    auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
-    auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
-    scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, status, ticket, total_dev, nullptr,
-                                                          nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr);
+    const Lookback lb = next_lookback(c, 0, tiles);
+    scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, c->scan_status, lb, pub, total_dev,
+                                                          nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0,
+                                                          nullptr);
     BSG_LAUNCHED(c);
 }
 
-void compact_visible(Ctx* c, uint32_t n, bool key32) {
+void compact_visible(Ctx* c, uint32_t n, bool key32, const Publish& pub) {
     if (n == 0) {
         BSG_CUDA(cudaMemsetAsync(&c->counters->visible, 0, sizeof(uint32_t), c->stream));
+        if (pub.seq_word) throw Error{BSG_ERR_STATE, "empty compaction cannot publish"};
         return;
     }
     const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
     prepare_status(c, tiles);
-    auto* status = reinterpret_cast<unsigned long long*>(c->scan_status) + 1;
-    auto* ticket = reinterpret_cast<uint32_t*>(c->scan_status);
+    const Lookback lb = next_lookback(c, 0, tiles);
     if (key32)
-        scan_kernel<2><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
+        scan_kernel<2><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, c->scan_status, lb, pub,
                                                               &c->counters->visible, c->depth_key, c->vkey[0],
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
                                                               c->vis_mask, static_cast<uint32_t>(c->cap / 32),
                                                               c->vis_prefix);
     else
-        scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, status, ticket,
+        scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, c->scan_status, lb, pub,
                                                               &c->counters->visible, c->depth_key, c->vkey[0],
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
                                                               c->vis_mask, static_cast<uint32_t>(c->cap / 32),

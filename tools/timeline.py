@@ -1,0 +1,96 @@
+"""Kernel timeline of the bench workload (cfg 2, one block) from CUPTI via
+torch.profiler: per-kernel warm durations, GPU idle gaps between consecutive
+kernels of one step, and the busy fraction of the step. Answers "how much of
+the step is launch / host-sync gap rather than kernel time".
+
+usage: python tools/timeline.py [--steps 50] [--out profiles/timeline.json]
+"""
+import argparse
+import json
+import os
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    import bench
+    torch.cuda.set_device(0)
+    blk, cams, _, _ = bench.build_block(0, 1, bench.CFG["n"], 0, constant_gt=False)
+    g = np.random.default_rng(3)
+    seq = [int(v) for v in g.integers(0, len(cams), args.warmup + args.steps)]
+    for v in seq[:args.warmup]:
+        blk.train_steps([v], want_losses=False)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        for v in seq[args.warmup:]:
+            blk.train_steps([v], want_losses=False)
+        torch.cuda.synchronize()
+    ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    kern = sorted([(e.time_range.start, e.time_range.end, e.name) for e in ev], key=lambda t: t[0])
+    if not kern:
+        print(json.dumps({"error": "no CUDA activity captured"}))
+        return
+    t0, t1 = kern[0][0], kern[-1][1]
+    span = t1 - t0
+    busy = 0.0
+    gaps = []
+    cur_end = kern[0][0]
+    per = defaultdict(lambda: [0, 0.0])
+    prev_name = None
+    for s, e, n in kern:
+        if s > cur_end:
+            gaps.append((s - cur_end, prev_name, n))
+        busy += max(0.0, e - max(s, cur_end))
+        cur_end = max(cur_end, e)
+        per[n][0] += 1
+        per[n][1] += e - s
+        prev_name = n
+    gap_by = defaultdict(lambda: [0, 0.0])
+    for d, a, b in gaps:
+        k = f"{a[:40]} -> {b[:40]}"
+        gap_by[k][0] += 1
+        gap_by[k][1] += d
+    top_gaps = sorted(gap_by.items(), key=lambda kv: -kv[1][1])[:12]
+    # one step in order (from the 10th preprocess launch to the next)
+    starts = [i for i, k in enumerate(kern) if "preprocess_kernel" in k[2]]
+    seq_one = []
+    if len(starts) > 11:
+        prev_end = kern[starts[10] - 1][1]
+        for s, e, n in kern[starts[10]:starts[11]]:
+            short = n.split("(")[0].replace("bsg::(anonymous namespace)::", "").replace("void ", "")
+            seq_one.append({"kernel": short, "gap_us": round(s - prev_end, 2), "us": round(e - s, 2)})
+            prev_end = e
+    out = {
+        "steps": args.steps,
+        "one_step": seq_one,
+        "span_us_per_step": span / args.steps,
+        "busy_us_per_step": busy / args.steps,
+        "idle_us_per_step": (span - busy) / args.steps,
+        "kernels_per_step": len(kern) / args.steps,
+        "kernels": {n: {"per_step": c / args.steps, "us_per_step": t / args.steps}
+                    for n, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1])},
+        "top_gaps": [{"between": k, "per_step": c / args.steps, "us_per_step": t / args.steps}
+                     for k, (c, t) in top_gaps],
+        "gpu": torch.cuda.get_device_name(0),
+    }
+    print(json.dumps(out, indent=1))
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(out, f, indent=1)
+    blk.close()
+
+
+if __name__ == "__main__":
+    main()
