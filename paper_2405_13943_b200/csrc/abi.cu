@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -166,6 +167,11 @@ void cm_to_rows(const float* cm, size_t n, int D, double* rows) {
 
 void set_error(const std::string& msg) { g_err = msg; }
 
+bool pdl_enabled() {
+    static const bool on = std::getenv("BSG_NO_PDL") == nullptr;
+    return on;
+}
+
 void stage_begin(Ctx* c, int stage) {
     if (c->stage_timing) BSG_CUDA(cudaEventRecord(c->ev[stage], c->stream));
 }
@@ -215,6 +221,12 @@ int tile_bits(const DevCam& cam) {
     return b;
 }
 
+__global__ __launch_bounds__(512) void zero_counters_kernel(StepCounters* __restrict__ cnt) {
+    pdl_prologue();
+    uint32_t* w = reinterpret_cast<uint32_t*>(cnt);
+    for (uint32_t i = threadIdx.x; i < sizeof(StepCounters) / 4; i += blockDim.x) w[i] = 0;
+}
+
 // K1-K5: projection, compaction, depth sort, pair emission, tile sort, ranges.
 // No stream synchronisation on the common path: the compaction and the
 // pair-offset scan publish V and P to the host-mapped mailbox, and the host
@@ -222,7 +234,8 @@ int tile_bits(const DevCam& cam) {
 // emission into the current capacity) keeps the GPU busy.
 void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     ensure_image_buffers(c, cam.W, cam.H);
-    BSG_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), c->stream));
+    launch_pdl(c->stream, 1, 512, 0, zero_counters_kernel, c->counters);
+    BSG_LAUNCHED(c);
     stage_begin(c, kStPreprocess);
     launch_preprocess(c, cam, rc);
     stage_end(c, kStPreprocess);

@@ -200,6 +200,7 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
                                                          const float4* __restrict__ g2d,
                                                          const double* __restrict__ g2d_wide, double* __restrict__ gout,
                                                          double* __restrict__ sgn_out, uint8_t* __restrict__ vis) {
+    pdl_prologue();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     constexpr int D = 11 + fd;
@@ -231,6 +232,7 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
                                                            const double* __restrict__ g2d_wide, float* __restrict__ gbuf,
                                                            float* __restrict__ grad_accum,
                                                            uint32_t* __restrict__ grad_seen) {
+    pdl_prologue();
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= V) return;
     const uint32_t i = vis_rows[p];
@@ -276,6 +278,7 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
                                                    const float* __restrict__ u, size_t ns,
                                                    const float* __restrict__ rho_dev, AdamStep st,
                                                    double* __restrict__ penalty) {
+    pdl_prologue();
     __shared__ double s_red[8];
     constexpr int NC = 1;
     const int c0 = comp_of_group(blockIdx.y);
@@ -385,6 +388,7 @@ __global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, fl
                                                        const float* __restrict__ z, const float* __restrict__ u,
                                                        size_t ns, const float* __restrict__ rho_dev, AdamStep st,
                                                        double* __restrict__ penalty) {
+    pdl_prologue();
     __shared__ double s_red[8];
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     double pen = 0.0;
@@ -457,10 +461,10 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
     if (c->n == 0) return;
     const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
     if (c->fd == 3)
-        fold_grads_kernel<3><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
+        launch_pdl(c->stream, blocks, 256, 0, fold_grads_kernel<3>, c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
                                                             c->rec, c->pcache, c->g2d, c->g2d_wide, g_out, sgn, vis);
     else
-        fold_grads_kernel<12><<<blocks, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
+        launch_pdl(c->stream, blocks, 256, 0, fold_grads_kernel<12>, c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
                                                              c->rec, c->pcache, c->g2d, c->g2d_wide, g_out, sgn, vis);
     BSG_LAUNCHED(c);
 }
@@ -468,11 +472,11 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     if (c->fd == 3)
-        fold_visible_kernel<3><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
+        launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<3>, c->x, c->cap, cam, c->vis_rows, V,
                                                                         c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
                                                                         c->grad_accum, c->grad_seen);
     else
-        fold_visible_kernel<12><<<(V + 127) / 128, 128, 0, c->stream>>>(c->x, c->cap, cam, c->vis_rows, V,
+        launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<12>, c->x, c->cap, cam, c->vis_rows, V,
                                                                          c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
                                                                         c->grad_accum, c->grad_seen);
     BSG_LAUNCHED(c);
@@ -486,13 +490,12 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     const uint32_t n = static_cast<uint32_t>(c->n);
     const int scalar_groups = c->D - 4;  // every component but the quaternion
     const dim3 g1(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(scalar_groups));
-    adam_kernel<1><<<g1, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf,
+    launch_pdl(c->stream, g1, 256, 0, adam_kernel<1>, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf,
                                               c->sh_mask,
                                               c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
                                               &c->scalars->penalty);
     BSG_LAUNCHED(c);
-    adam_rot_kernel<<<static_cast<uint32_t>((c->n + 255) / 256), 256, 0, c->stream>>>(
-        c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u,
+    launch_pdl(c->stream, static_cast<uint32_t>((c->n + 255) / 256), 256, 0, adam_rot_kernel, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u,
         c->n_shared,
         c->rho_dev, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);

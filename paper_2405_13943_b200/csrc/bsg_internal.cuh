@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/bsgpu.h"
@@ -252,6 +253,33 @@ struct Error {
         if (e_ != cudaSuccess)                                                             \
             throw ::bsg::Error{BSG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)}; \
     } while (0)
+
+// Programmatic dependent launch (PDL) for the kernels of a step: each one is
+// launched with programmatic stream serialisation, so its CTAs are scheduled
+// while the previous kernel drains, and starts with pdl_prologue(): wait until
+// the previous grid has completed and flushed its writes, then allow the next
+// kernel to be scheduled. (Without the launch attribute both are no-ops.)
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // false when BSG_NO_PDL is set (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(cudaStream_t stream, dim3 grid, dim3 block, size_t smem, void (*kernel)(KArgs...), Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    BSG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // Width of the range-normalised depth key for V visible splats: ~6 bits more
 // than log2(V), so equal keys (distinct depths in one bucket) stay rare,

@@ -46,6 +46,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  float4* __restrict__ pcache,
                                                                  StepCounters* __restrict__ counters,
                                                                  StepScalars* __restrict__ scalars) {
+    pdl_prologue();
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint32_t s_count;
     __shared__ unsigned long long s_zmin_inv, s_zmax;
@@ -301,7 +302,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
         return;
     }
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
-    preprocess_kernel<<<blocks, kPreThreads, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
+    launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
                                                       c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters,
                                                       c->scalars);
     BSG_LAUNCHED(c);

@@ -22,6 +22,7 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
                                                               uint32_t n, int shift,
                                                               const uint32_t* __restrict__ pass_hist,
                                                               unsigned long long* status, Lookback lb) {
+    pdl_prologue();
     constexpr int kRsTile = kRsThreads * kRsItems;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s_keys = reinterpret_cast<K*>(smem_raw);
@@ -159,6 +160,7 @@ __global__ __launch_bounds__(kRsThreads) void onesweep_kernel(const K* __restric
 // per CTA, one global atomic per non-empty bin.
 __global__ __launch_bounds__(256) void depth_hist_kernel(const uint32_t* __restrict__ keys,
                                                          StepCounters* __restrict__ cnt) {
+    pdl_prologue();
     __shared__ uint32_t s_h[4 * 256];
     const uint32_t n = cnt->visible;
     const int passes = depth_key_bits(cnt->visible_pre) / 8;
@@ -198,8 +200,7 @@ void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_
             if (trivial) continue;
         }
         const Lookback lb = next_lookback(c, 1, tiles);
-        onesweep_kernel<K, ITEMS><<<tiles, kRsThreads, smem, c->stream>>>(
-            keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, d_hist + p * 256, c->radix_status, lb);
+        launch_pdl(c->stream, tiles, kRsThreads, smem, onesweep_kernel<K, ITEMS>, keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, d_hist + p * 256, c->radix_status, lb);
         BSG_LAUNCHED(c);
         cur ^= 1;
     }
@@ -233,6 +234,7 @@ void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pas
 __global__ void depth_tie_fixup_kernel(uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
                                        const uint64_t* __restrict__ depth_bits, uint32_t V,
                                        uint32_t* __restrict__ long_run) {
+    pdl_prologue();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= V) return;
     const uint32_t k = keys[i];
@@ -295,14 +297,14 @@ void radix_sort_u32(Ctx* c, uint32_t* keys[2], uint32_t* vals[2], uint32_t n, in
 
 void launch_depth_hist(Ctx* c, const uint32_t* keys) {
     const unsigned grid = std::min<unsigned>(static_cast<unsigned>((c->n + 4095) / 4096), 148);  // upper bound V <= n
-    depth_hist_kernel<<<std::max(grid, 1u), 256, 0, c->stream>>>(keys, c->counters);
+    launch_pdl(c->stream, std::max(grid, 1u), 256, 0, depth_hist_kernel, keys, c->counters);
     BSG_LAUNCHED(c);
 }
 
 void depth_tie_fixup(Ctx* c, uint32_t* keys, uint32_t* rows, const uint64_t* depth_bits, uint32_t V,
                      uint32_t* long_run) {
     if (V < 2) return;
-    depth_tie_fixup_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(keys, rows, depth_bits, V, long_run);
+    launch_pdl(c->stream, (V + 255) / 256, 256, 0, depth_tie_fixup_kernel, keys, rows, depth_bits, V, long_run);
     BSG_LAUNCHED(c);
 }
 

@@ -44,6 +44,7 @@ __global__ __launch_bounds__(256) void emit_pairs_kernel(const uint32_t* __restr
                                                          uint32_t* __restrict__ pkey, uint32_t* __restrict__ pval,
                                                          uint32_t pcap, uint32_t* __restrict__ hist,
                                                          uint2* __restrict__ ranges, uint32_t ntiles) {
+    pdl_prologue();
     __shared__ uint32_t s_hist[2 * 256];
     for (int k = threadIdx.x; k < 512; k += blockDim.x) s_hist[k] = 0;
     // tiles without pairs keep the empty range (ranges_kernel writes the rest)
@@ -75,6 +76,7 @@ __global__ __launch_bounds__(256) void emit_pairs_kernel(const uint32_t* __restr
 
 __global__ __launch_bounds__(256) void ranges_kernel(const uint32_t* __restrict__ pkey, uint32_t P,
                                                      uint2* __restrict__ ranges) {
+    pdl_prologue();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
     const uint32_t k = pkey[i];
@@ -114,6 +116,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   uint32_t* __restrict__ out_n,
                                                                   uint32_t* __restrict__ out_last,
                                                                   unsigned long long* __restrict__ evals) {
+    pdl_prologue();
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint8_t s_m[kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
@@ -316,6 +319,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   const float* __restrict__ dl_dc,
                                                                   float4* __restrict__ g2d,
                                                                   double* __restrict__ g2d_wide) {
+    pdl_prologue();
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint32_t s_row[kBatch];
     __shared__ uint8_t s_m[kBatch];
@@ -430,7 +434,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
 void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
-    emit_pairs_kernel<<<(V + 255) / 256, 256, 0, c->stream>>>(c->vrow[c->depth_sorted], c->poff, c->rec, V, cam.tiles_x,
+    launch_pdl(c->stream, (V + 255) / 256, 256, 0, emit_pairs_kernel, c->vrow[c->depth_sorted], c->poff, c->rec, V, cam.tiles_x,
                                                               c->pkey[0], c->pval[0], static_cast<uint32_t>(c->pcap),
                                                               &c->counters->tile_hist[0][0], c->ranges, ntiles);
     BSG_LAUNCHED(c);
@@ -441,14 +445,13 @@ void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P) {
     const size_t ntiles = static_cast<size_t>(cam.tiles_x) * cam.tiles_y;
     if (V == 0) BSG_CUDA(cudaMemsetAsync(c->ranges, 0, ntiles * sizeof(uint2), c->stream));
     if (P == 0) return;
-    ranges_kernel<<<(P + 255) / 256, 256, 0, c->stream>>>(c->pkey[c->pairs_sorted], P, c->ranges);
+    launch_pdl(c->stream, (P + 255) / 256, 256, 0, ranges_kernel, c->pkey[c->pairs_sorted], P, c->ranges);
     BSG_LAUNCHED(c);
 }
 
 void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
-    blend_fwd_kernel<<<ntiles, kBlendThreads, 0, c->stream>>>(
-        c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, rc.tstop,
+    launch_pdl(c->stream, ntiles, kBlendThreads, 0, blend_fwd_kernel, c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, rc.tstop,
         static_cast<float>(rc.alpha_clamp), rc.alpha_clamp, rc.bg[0], rc.bg[1], rc.bg[2], c->out_rgb, c->out_T,
         c->out_n, c->out_last, &c->counters->evals);
     BSG_LAUNCHED(c);
@@ -456,8 +459,7 @@ void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
 
 void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
-    blend_bwd_kernel<<<ntiles, kBlendThreads, 0, c->stream>>>(
-        c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.alpha_clamp),
+    launch_pdl(c->stream, ntiles, kBlendThreads, 0, blend_bwd_kernel, c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.alpha_clamp),
         rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d, c->g2d_wide);
     BSG_LAUNCHED(c);
 }

@@ -94,6 +94,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
                                                             uint32_t* __restrict__ hist_out, int hist_first,
                                                             uint32_t* __restrict__ mask_out, uint32_t mask_words,
                                                             uint32_t* __restrict__ prefix_out) {
+    pdl_prologue();
     __shared__ uint32_t s_tile, s_prefix, s_total;
     __shared__ uint32_t s_warp[kScanThreads / 32];
     constexpr int kDigits = 8;
@@ -279,7 +280,7 @@ void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, 
     const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
     prepare_status(c, tiles);
     const Lookback lb = next_lookback(c, 0, tiles);
-    scan_kernel<0><<<tiles, kScanThreads, 0, c->stream>>>(in, gather_idx, out, n, c->scan_status, lb, pub, total_dev,
+    launch_pdl(c->stream, tiles, kScanThreads, 0, scan_kernel<0>, in, gather_idx, out, n, c->scan_status, lb, pub, total_dev,
                                                           nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0,
                                                           nullptr);
     BSG_LAUNCHED(c);
@@ -295,13 +296,13 @@ void compact_visible(Ctx* c, uint32_t n, bool key32, const Publish& pub) {
     prepare_status(c, tiles);
     const Lookback lb = next_lookback(c, 0, tiles);
     if (key32)
-        scan_kernel<2><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, c->scan_status, lb, pub,
+        launch_pdl(c->stream, tiles, kScanThreads, 0, scan_kernel<2>, c->tiles, nullptr, c->vis_rows, n, c->scan_status, lb, pub,
                                                               &c->counters->visible, c->depth_key, c->vkey[0],
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
                                                               c->vis_mask, static_cast<uint32_t>(c->cap / 32),
                                                               c->vis_prefix);
     else
-        scan_kernel<1><<<tiles, kScanThreads, 0, c->stream>>>(c->tiles, nullptr, c->vis_rows, n, c->scan_status, lb, pub,
+        launch_pdl(c->stream, tiles, kScanThreads, 0, scan_kernel<1>, c->tiles, nullptr, c->vis_rows, n, c->scan_status, lb, pub,
                                                               &c->counters->visible, c->depth_key, c->vkey[0],
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
                                                               c->vis_mask, static_cast<uint32_t>(c->cap / 32),

@@ -78,6 +78,7 @@ struct WinSmem {
 __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __restrict__ x,
                                                                 const float* __restrict__ y, int W, int H,
                                                                 float* __restrict__ f, double* __restrict__ ssim_sum) {
+    pdl_prologue();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WinSmem& S = *reinterpret_cast<WinSmem*>(smem_raw);
     __shared__ double s_red[kThreads / 32];
@@ -175,6 +176,7 @@ __global__ __launch_bounds__(kThreads) void ssim_pixels_kernel(const float* __re
                                                                int W, int H, const float* __restrict__ f, int has_ssim,
                                                                float lam_over_count, float inv_count3,
                                                                float* __restrict__ dl_dc, double* __restrict__ l1_sum) {
+    pdl_prologue();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PixSmem& S = *reinterpret_cast<PixSmem*>(smem_raw);
     __shared__ double s_red[kThreads / 32];
@@ -237,6 +239,7 @@ __global__ __launch_bounds__(kThreads) void ssim_pixels_kernel(const float* __re
 
 __global__ void finalize_kernel(const StepScalars* s, double inv_count3, double inv_count, int has_ssim, double lambda,
                                 int add_penalty, double* out) {
+    pdl_prologue();
     const double l1 = s->l1_sum * inv_count3;
     const double ss = has_ssim ? s->ssim_sum * inv_count : 1.0;
     double loss = l1 + lambda * (1.0 - ss);
@@ -279,13 +282,12 @@ void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt
     const double count = has_ssim ? 3.0 * Wv * Hv : 1.0;
     if (has_ssim) {
         dim3 grid((Wv + kTX - 1) / kTX, (Hv + kTY - 1) / kTY);
-        ssim_windows_kernel<<<grid, kThreads, sizeof(WinSmem), c->stream>>>(c->out_rgb, gt, W, H, c->ssim_f,
+        launch_pdl(c->stream, grid, kThreads, sizeof(WinSmem), ssim_windows_kernel, c->out_rgb, gt, W, H, c->ssim_f,
                                                                            &c->scalars->ssim_sum);
         BSG_LAUNCHED(c);
     }
     dim3 grid2((W + kTX - 1) / kTX, (H + kTY - 1) / kTY);
-    ssim_pixels_kernel<<<grid2, kThreads, sizeof(PixSmem), c->stream>>>(
-        c->out_rgb, gt, W, H, c->ssim_f, has_ssim ? 1 : 0, static_cast<float>(rc.lambda / count),
+    launch_pdl(c->stream, grid2, kThreads, sizeof(PixSmem), ssim_pixels_kernel, c->out_rgb, gt, W, H, c->ssim_f, has_ssim ? 1 : 0, static_cast<float>(rc.lambda / count),
         static_cast<float>(1.0 / (3.0 * W * H)), c->dl_dc, &c->scalars->l1_sum);
     BSG_LAUNCHED(c);
 }
@@ -298,7 +300,7 @@ bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt) {
     ensure_ssim_ready(c);
     const int Wv = W - 2 * kHalf, Hv = H - 2 * kHalf;
     dim3 grid((Wv + kTX - 1) / kTX, (Hv + kTY - 1) / kTY);
-    ssim_windows_kernel<<<grid, kThreads, sizeof(WinSmem), c->stream>>>(c->out_rgb, gt, W, H, c->ssim_f,
+    launch_pdl(c->stream, grid, kThreads, sizeof(WinSmem), ssim_windows_kernel, c->out_rgb, gt, W, H, c->ssim_f,
                                                                        &c->scalars->ssim_sum);
     BSG_LAUNCHED(c);
     return true;
@@ -308,7 +310,7 @@ void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double
     const int W = cam.W, H = cam.H;
     const bool has_ssim = W >= kW && H >= kW;
     const double count = has_ssim ? 3.0 * (W - 2 * kHalf) * (H - 2 * kHalf) : 1.0;
-    finalize_kernel<<<1, 1, 0, c->stream>>>(c->scalars, 1.0 / (3.0 * W * H), 1.0 / count, has_ssim ? 1 : 0, rc.lambda,
+    launch_pdl(c->stream, 1, 1, 0, finalize_kernel, c->scalars, 1.0 / (3.0 * W * H), 1.0 / count, has_ssim ? 1 : 0, rc.lambda,
                                             add_penalty ? 1 : 0, out);
     BSG_LAUNCHED(c);
 }

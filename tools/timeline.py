@@ -37,6 +37,35 @@ def main():
         for v in seq[args.warmup:]:
             blk.train_steps([v], want_losses=False)
         torch.cuda.synchronize()
+    # host launch -> device start latency per kernel (chrome trace: correlation ids)
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".json", delete=False) as tf:
+        trace_path = tf.name
+    prof.export_chrome_trace(trace_path)
+    with open(trace_path) as f:
+        tr = json.load(f)
+    os.unlink(trace_path)
+    launches, kernels = {}, {}
+    for e in tr.get("traceEvents", []):
+        cat = e.get("cat", "")
+        corr = (e.get("args") or {}).get("correlation")
+        if corr is None or e.get("ph") != "X":
+            continue
+        if cat == "cuda_runtime" or cat == "cuda_driver":
+            launches[corr] = (e["ts"], e["ts"] + e.get("dur", 0), e.get("name", ""))
+        elif cat in ("kernel", "gpu_memset", "gpu_memcpy"):
+            kernels[corr] = (e["ts"], e["ts"] + e.get("dur", 0), e.get("name", ""))
+    slack = defaultdict(list)
+    rows = sorted((ks, kn, ks - launches[corr][1]) for corr, (ks, ke, kn) in kernels.items() if corr in launches)
+    pos = 0
+    for ks, kn, sl in rows:
+        short = kn.replace("bsg::(anonymous namespace)::", "").replace("void ", "").split("(")[0]
+        if short.startswith("zero_counters"):
+            pos = 0
+        slack[f"{pos:02d} {short}"].append(sl)  # > 0: the kernel was queued before it could start
+        pos += 1
+    host_slack = {k: {"median_us": float(np.median(v)), "min_us": float(np.min(v)), "n": len(v)}
+                  for k, v in slack.items()}
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     kern = sorted([(e.time_range.start, e.time_range.end, e.name) for e in ev], key=lambda t: t[0])
     if not kern:
@@ -69,12 +98,13 @@ def main():
     if len(starts) > 11:
         prev_end = kern[starts[10] - 1][1]
         for s, e, n in kern[starts[10]:starts[11]]:
-            short = n.split("(")[0].replace("bsg::(anonymous namespace)::", "").replace("void ", "")
+            short = n.replace("bsg::(anonymous namespace)::", "").replace("void ", "").split("(")[0]
             seq_one.append({"kernel": short, "gap_us": round(s - prev_end, 2), "us": round(e - s, 2)})
             prev_end = e
     out = {
         "steps": args.steps,
         "one_step": seq_one,
+        "launch_to_start_us": host_slack,
         "span_us_per_step": span / args.steps,
         "busy_us_per_step": busy / args.steps,
         "idle_us_per_step": (span - busy) / args.steps,
