@@ -260,10 +260,15 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
 // per-row side array is re-read per component. Rows not visible this step
 // have a zero render gradient; shared rows add rho (x - z + u) evaluated at
 // the pre-step x (admm.cpp:24-28, trainer.cpp:257-265).
+// The step's sqrt and division are the approximate MUFU forms (sqrt.approx,
+// rcp-based division, ~2 ulp each on the update term, far below the FP32
+// rounding of x itself); the IEEE sequences made the kernel issue-bound.
 __device__ __forceinline__ float adam_update(float x, float g, float& m, float& v, float lr, const AdamStep& st) {
     m = st.b1 * m + st.omb1 * g;
     v = st.b2 * v + st.omb2 * g * g;
-    return x - lr * (m * st.inv_bc1) / (sqrtf(v * st.inv_bc2) + st.eps);
+    float sq;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * st.inv_bc2));
+    return x - lr * __fdividef(m * st.inv_bc1, sq + st.eps);
 }
 
 __device__ __forceinline__ int comp_of_group(int y) { return y < 3 ? y : y + 4; }  // pos 0-2, ls/feat/op 7..
