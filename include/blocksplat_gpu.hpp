@@ -7,10 +7,8 @@
 //  - No Eigen: small vectors are std::array (Vec3/Vec4), CameraView::rotation
 //    is a row-major std::array<double, 9>.
 //  - BlockTrainer owns a device context; cloud()/duals()/anchor() download.
-//  - Densification (trainer.cpp:301-385) is not on the device path yet
-//    (SURVEY §8(f)1): densification runs on the device; run_simulated with
-//    K > 1 rejects a schedule that would densify (the master's id bookkeeping,
-//    runtime.cpp:490-518, is SURVEY §8(f)2).
+//  - Densification (trainer.cpp:301-385) runs on the device; run_simulated
+//    keeps the master's id / owner bookkeeping (runtime.cpp:490-518) on the host.
 //  - FP32 device state: results match the FP64 reference within the
 //    tolerances stated in tests/ (integer paths bit-exact).
 #pragma once
@@ -68,11 +66,32 @@ struct CameraView {
     Mat3 rotation{1, 0, 0, 0, 1, 0, 0, 0, 1};
     Vec3 translation{0, 0, 0};
     uint32_t width = 0, height = 0;
+    std::string image_path;
     void set_rotation_quat(const Vec4& q);
     Vec3 center() const;
 };
 CameraView look_at(const Vec3& position, const Vec3& target, const Vec3& world_up, double fx, double fy, double cx,
                    double cy, uint32_t width, uint32_t height);
+
+// errors.hpp:10-31: container / wire decode errors, matched on the code.
+enum class FormatErrorCode {
+    BadMagic,
+    UnsupportedVersion,
+    TruncatedSection,
+    UnknownSection,
+    TruncatedBuffer,
+    CountOverflow,
+    NonMonotoneIds,
+    BadHeader,
+};
+class FormatError : public std::runtime_error {
+public:
+    FormatError(FormatErrorCode code, const std::string& message) : std::runtime_error(message), code_(code) {}
+    FormatErrorCode code() const noexcept { return code_; }
+
+private:
+    FormatErrorCode code_;
+};
 
 struct Image {  // image.hpp:11-25
     uint32_t width = 0, height = 0;
@@ -281,5 +300,32 @@ struct SessionOptions {  // runtime.hpp:109-115
 RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, const SessionOptions& opt,
                         const std::function<void(const RoundDiagnostics&)>& observer = {},
                         const std::vector<int>& devices = {0});
+
+// scene.hpp:15-50 / scene_io.cpp: the DOGS container (little-endian, magic
+// "DOGS", version u32, tagged sections CAMS / PNTS / GSPL, each a 4-byte tag,
+// a u64 length and the payload). GSPL is the f32 Gaussian checkpoint; the
+// trained model is written as a container holding only it (main.cpp:353-357).
+struct ScenePoint {
+    std::array<float, 3> position{0, 0, 0};
+    std::array<uint8_t, 3> rgb{0, 0, 0};
+};
+struct SceneDataset {
+    std::vector<ScenePoint> points;
+    std::vector<CameraView> views;
+    bool has_checkpoint = false;
+    GaussianCloud checkpoint;
+};
+inline constexpr uint32_t kSceneFormatVersion = 1;
+std::vector<uint8_t> encode_scene(const SceneDataset& scene);
+SceneDataset decode_scene(const uint8_t* data, size_t size);
+void save_scene(const std::string& path, const SceneDataset& scene);
+SceneDataset load_scene(const std::string& path);
+GaussianCloud narrow_to_f32(const GaussianCloud& cloud);
+// The GSPL payload of a block's device cloud, encoded on the device
+// (bsg_encode_gspl): byte-identical to the GSPL section encode_scene writes
+// for that cloud (the device parameters are already f32).
+std::vector<uint8_t> encode_gspl_device(bsg_ctx* ctx);
+// model.dogs (main.cpp:353-357): a container holding only the narrowed model.
+void save_model(const std::string& path, const GaussianCloud& model);
 
 }  // namespace blocksplat

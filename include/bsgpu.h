@@ -41,7 +41,8 @@ enum bsg_status {
     BSG_ERR_CUDA = 2,             /* CUDA runtime / launch failure */
     BSG_ERR_NCCL = 3,             /* collective failure */
     BSG_ERR_STATE = 4,            /* call out of order (e.g. step before init) */
-    BSG_ERR_CAPACITY = 5          /* device buffer capacity exceeded */
+    BSG_ERR_CAPACITY = 5,         /* device buffer capacity exceeded */
+    BSG_ERR_FORMAT = 6            /* blocksplat::FormatError (container decode); see format_code */
 };
 
 /* CameraView (camera.hpp:14-37): x_c = R x_w + t, pixel = (fx X/Z + cx, fy Y/Z + cy).
@@ -116,6 +117,13 @@ int bsg_upload_cloud(bsg_ctx* ctx, size_t n, const uint64_t* ids, const double* 
 size_t bsg_cloud_size(const bsg_ctx* ctx);
 int bsg_download_cloud(bsg_ctx* ctx, uint64_t* ids, double* pos, double* rot, double* log_scale, double* features,
                        double* opacity_logit);
+/* GSPL checkpoint payload of the context's cloud (scene_io.cpp:48-59): u64
+ * count, u32 feature width, u64 ids, then f32 positions 3n, rotations 4n,
+ * log-scales 3n, features fd*n, opacity logits n, little-endian. Encoded on
+ * the device from the FP32 parameters (narrow_to_f32, scene_io.cpp:230-241,
+ * is the identity on them). out == NULL: *out_len receives the byte size;
+ * otherwise out_cap must be at least that (BSG_ERR_CAPACITY). */
+int bsg_encode_gspl(bsg_ctx* ctx, uint8_t* out, size_t out_cap, size_t* out_len);
 
 /* ---- rendering (renderer.hpp:71-81) ---------------------------------- */
 /* render(): out_rgb HxWx3, out_transmittance HxW, out_contributors HxW (any may be NULL). */
@@ -302,6 +310,24 @@ int bsg_run_simulated(int feature_dim, size_t n, const uint64_t* ids, const doub
 /* The out_* arrays hold up to model_capacity rows of the assembled model
  * (densification changes its size; *out_n receives it, BSG_ERR_CAPACITY when
  * it exceeds the capacity). */
+
+/* ---- checkpoint files (DOGS container, scene_io.cpp) ------------------- */
+/* model.dogs (main.cpp:353-357): a DOGS v1 container with empty CAMS / PNTS
+ * sections and the GSPL section of the f32-narrowed model. */
+int bsg_save_model(const char* path, int feature_dim, size_t n, const uint64_t* ids, const double* pos,
+                   const double* rot, const double* log_scale, const double* features, const double* opacity_logit);
+/* The GSPL checkpoint of a DOGS container file (the plan_cluster checkpoint
+ * path, runtime.cpp:273-275). ids == NULL: only *out_n and *out_fd. On a
+ * decode error returns BSG_ERR_FORMAT with *format_code = the
+ * FormatErrorCode (errors.hpp:10-19, 0 = BadMagic ... 7 = BadHeader);
+ * a container without a checkpoint gives BSG_ERR_INVALID_ARGUMENT. */
+int bsg_load_checkpoint(const char* path, size_t capacity, uint64_t* ids, double* pos, double* rot,
+                        double* log_scale, double* features, double* opacity_logit, size_t* out_n, int* out_fd,
+                        int* format_code);
+/* Same, from bytes in memory (decode_scene, scene_io.cpp:134-176). */
+int bsg_decode_checkpoint(const uint8_t* data, size_t size, size_t capacity, uint64_t* ids, double* pos,
+                          double* rot, double* log_scale, double* features, double* opacity_logit, size_t* out_n,
+                          int* out_fd, int* format_code);
 
 /* ---- measurement ------------------------------------------------------ */
 /* Per-stage device times of the most recent step (CUDA events on the

@@ -18,6 +18,8 @@ LIB_PATH = os.environ.get("BSG_LIB") or os.path.join(_HERE, "lib", "libbsgpu.so"
 
 BSG_OK = 0
 BSG_ERR_INVALID_ARGUMENT = 1
+BSG_ERR_CAPACITY = 5
+BSG_ERR_FORMAT = 6
 
 
 class BsgError(RuntimeError):
@@ -110,6 +112,12 @@ SYMBOLS = [
     ("bsg_upload_cloud", ctypes.c_int, [_P, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP]),
     ("bsg_cloud_size", _SZ, [_P]),
     ("bsg_download_cloud", ctypes.c_int, [_P, _U64P, _DP, _DP, _DP, _DP, _DP]),
+    ("bsg_encode_gspl", ctypes.c_int, [_P, _U8P, _SZ, _SZP]),
+    ("bsg_save_model", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP]),
+    ("bsg_load_checkpoint", ctypes.c_int, [ctypes.c_char_p, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZP,
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    ("bsg_decode_checkpoint", ctypes.c_int, [_U8P, _SZ, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZP,
+                                              ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("bsg_render", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), ctypes.POINTER(bsg_render_config), _DP, _DP, _U32P]),
     ("bsg_evaluate", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_DP), ctypes.c_uint32,
                                     ctypes.POINTER(bsg_render_config), _DP, _DP, _SZP, _DP, _DP]),
@@ -306,6 +314,14 @@ class Block:
                                        _ptr(rot, ctypes.c_double), _ptr(ls, ctypes.c_double),
                                        _ptr(feat, ctypes.c_double), _ptr(op, ctypes.c_double)))
         return dict(ids=ids, pos=pos, rot=rot, ls=ls, feat=feat, op=op)
+
+    def encode_gspl(self):
+        """GSPL checkpoint payload of the device cloud (scene_io.cpp:48-59), encoded on the device."""
+        ln = ctypes.c_size_t()
+        _check(_lib.bsg_encode_gspl(self.h, None, 0, ctypes.byref(ln)))
+        out = np.zeros(ln.value, np.uint8)
+        _check(_lib.bsg_encode_gspl(self.h, _ptr(out, ctypes.c_uint8), ln.value, ctypes.byref(ln)))
+        return out.tobytes()
 
     # ---- rendering -----------------------------------------------------
     def render(self, cam, cfg=None):
@@ -644,3 +660,62 @@ def run_simulated(cloud, cams, gts, trainer_cfg, session, devices=(0,)):
                        max_disagreement=r.max_disagreement, dual_mean_linf=r.dual_mean_linf, mean_loss=r.mean_loss,
                        shared_count=r.shared_count, global_count=r.global_count, consensus_ms=r.consensus_ms))
     return model, rl, wall.value
+
+
+class FormatError(RuntimeError):
+    """blocksplat::FormatError (errors.hpp:10-31); .code is the FormatErrorCode name."""
+
+    CODES = ("BadMagic", "UnsupportedVersion", "TruncatedSection", "UnknownSection", "TruncatedBuffer",
+             "CountOverflow", "NonMonotoneIds", "BadHeader")
+
+    def __init__(self, code, msg):
+        super().__init__(f"{self.CODES[code]}: {msg}")
+        self.code = self.CODES[code]
+
+
+def _driver_check(status, fcode=None):
+    if status == BSG_OK:
+        return
+    msg = _lib.bsg_driver_last_error().decode()
+    if status == BSG_ERR_FORMAT:
+        raise FormatError(fcode.value, msg)
+    if status == BSG_ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    raise BsgError(f"bsg status {status}: {msg}")
+
+
+def save_model(path, cloud):
+    """model.dogs (main.cpp:353-357): DOGS container with the f32-narrowed model as its GSPL section."""
+    load_library()
+    ids = np.ascontiguousarray(cloud["ids"], np.uint64)
+    n = len(ids)
+    fd = np.asarray(cloud["feat"]).reshape(n, -1).shape[1] if n else int(cloud.get("fd", 3))
+    arrs = [_f64(cloud[k]) for k in ("pos", "rot", "ls", "feat", "op")]
+    _driver_check(_lib.bsg_save_model(os.fsencode(path), fd, n, _ptr(ids, ctypes.c_uint64),
+                                      *[_ptr(a, ctypes.c_double) for a in arrs]))
+
+
+def _checkpoint(call):
+    n, fd, fc = ctypes.c_size_t(), ctypes.c_int(), ctypes.c_int(-1)
+    _driver_check(call(0, None, None, None, None, None, None, ctypes.byref(n), ctypes.byref(fd), ctypes.byref(fc)), fc)
+    m, f = n.value, fd.value
+    ids = np.zeros(max(m, 1), np.uint64)
+    outs = [np.zeros((max(m, 1), w)) for w in (3, 4, 3, f)] + [np.zeros(max(m, 1))]
+    _driver_check(call(m, _ptr(ids, ctypes.c_uint64), *[_ptr(o, ctypes.c_double) for o in outs], ctypes.byref(n),
+                       ctypes.byref(fd), ctypes.byref(fc)), fc)
+    return dict(ids=ids[:m], pos=outs[0][:m], rot=outs[1][:m], ls=outs[2][:m], feat=outs[3][:m], op=outs[4][:m])
+
+
+def load_checkpoint(path):
+    """GSPL checkpoint of a DOGS container file (runtime.cpp:273-275), as FP64 arrays."""
+    load_library()
+    p = os.fsencode(path)
+    return _checkpoint(lambda cap, *a: _lib.bsg_load_checkpoint(p, cap, *a))
+
+
+def decode_checkpoint(data):
+    """GSPL checkpoint of DOGS container bytes (decode_scene, scene_io.cpp:134-176)."""
+    load_library()
+    buf = np.frombuffer(bytes(data), np.uint8).copy()
+    ptr = _ptr(buf, ctypes.c_uint8) if len(buf) else None
+    return _checkpoint(lambda cap, *a: _lib.bsg_decode_checkpoint(ptr, len(buf), cap, *a))

@@ -687,6 +687,31 @@ int bsg_download_cloud(bsg_ctx* h, uint64_t* ids, double* pos, double* rot, doub
     });
 }
 
+int bsg_encode_gspl(bsg_ctx* h, uint8_t* out, size_t out_cap, size_t* out_len) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!out_len) invalid("null out_len");
+        const size_t n = c->n;
+        const size_t floats = static_cast<size_t>(11 + c->fd) * n;
+        const size_t len = 8 + 4 + 8 * n + 4 * floats;
+        *out_len = len;
+        if (!out) return;
+        if (out_cap < len) throw Error{BSG_ERR_CAPACITY, "GSPL buffer smaller than the payload"};
+        use_device(c);
+        const uint64_t count = n;
+        const uint32_t fd = static_cast<uint32_t>(c->fd);
+        std::memcpy(out, &count, 8);
+        std::memcpy(out + 8, &fd, 4);
+        if (n) std::memcpy(out + 12, c->ids.data(), 8 * n);
+        if (!floats) return;
+        // gbuf ([D][cap] f32 step scratch) holds the transposed arrays
+        launch_gspl_floats(c, c->gbuf);
+        BSG_CUDA(cudaMemcpyAsync(out + 12 + 8 * n, c->gbuf, 4 * floats, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 int bsg_render(bsg_ctx* h, const bsg_camera* cam, const bsg_render_config* cfg, double* out_rgb, double* out_T,
                uint32_t* out_n) {
     return guarded([&] {

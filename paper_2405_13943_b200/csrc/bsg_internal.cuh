@@ -329,6 +329,8 @@ DevCam make_cam(const bsg_camera& c);
 DevRender make_render(const bsg_render_config& r);
 void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V);
+// The f32 arrays of the GSPL checkpoint section ((11 + fd) n floats, section order) into out.
+void launch_gspl_floats(Ctx* c, float* out);
 void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P);
 void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt);

@@ -1,5 +1,6 @@
 // C entry point of the K-block driver (run_simulated over the C++ host
 // layer), for hosts that bind C (Python ctypes, the bench, tests).
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -8,6 +9,46 @@
 namespace {
 thread_local std::string g_drv_err;
 }
+
+namespace {
+
+template <typename Decode>
+int checkpoint_out(Decode&& decode, size_t cap, uint64_t* ids, double* pos, double* rot, double* ls, double* feat,
+                   double* op, size_t* out_n, int* out_fd, int* format_code) {
+    using namespace blocksplat;
+    try {
+        const SceneDataset d = decode();
+        if (!d.has_checkpoint) throw InvalidArgument("container has no GSPL checkpoint");
+        const GaussianCloud& c = d.checkpoint;
+        const size_t n = c.size();
+        const int fd = c.feature_dim();
+        if (out_n) *out_n = n;
+        if (out_fd) *out_fd = fd;
+        if (!ids) return BSG_OK;
+        if (n > cap) {
+            g_drv_err = "checkpoint has more rows than the capacity";
+            return BSG_ERR_CAPACITY;
+        }
+        std::copy(c.ids.begin(), c.ids.end(), ids);
+        if (pos) std::copy(c.positions.begin(), c.positions.end(), pos);
+        if (rot) std::copy(c.rotations.begin(), c.rotations.end(), rot);
+        if (ls) std::copy(c.log_scales.begin(), c.log_scales.end(), ls);
+        if (feat) std::copy(c.features.begin(), c.features.end(), feat);
+        if (op) std::copy(c.opacity_logits.begin(), c.opacity_logits.end(), op);
+        return BSG_OK;
+    } catch (const FormatError& e) {
+        g_drv_err = e.what();
+        if (format_code) *format_code = static_cast<int>(e.code());
+        return BSG_ERR_FORMAT;
+    } catch (const InvalidArgument& e) {
+        g_drv_err = e.what();
+        return BSG_ERR_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_drv_err = e.what();
+        return BSG_ERR_STATE;
+    }
+}
+}  // namespace
 
 extern "C" {
 
@@ -115,6 +156,54 @@ int bsg_run_simulated(int fd, size_t n, const uint64_t* ids, const double* pos, 
         g_drv_err = e.what();
         return BSG_ERR_STATE;
     }
+}
+
+int bsg_save_model(const char* path, int fd, size_t n, const uint64_t* ids, const double* pos, const double* rot,
+                   const double* ls, const double* feat, const double* op) {
+    using namespace blocksplat;
+    try {
+        if (!path) throw InvalidArgument("null path");
+        if (fd != kFeatureDimDeg0 && fd != kFeatureDimDeg1) throw InvalidArgument("feature width must be 3 or 12");
+        if (n && (!ids || !pos || !rot || !ls || !feat || !op)) throw InvalidArgument("null model array");
+        GaussianCloud m(fd);
+        if (n) {
+            m.ids.assign(ids, ids + n);
+            m.positions.assign(pos, pos + 3 * n);
+            m.rotations.assign(rot, rot + 4 * n);
+            m.log_scales.assign(ls, ls + 3 * n);
+            m.features.assign(feat, feat + n * fd);
+            m.opacity_logits.assign(op, op + n);
+        }
+        save_model(path, m);
+        return BSG_OK;
+    } catch (const InvalidArgument& e) {
+        g_drv_err = e.what();
+        return BSG_ERR_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_drv_err = e.what();
+        return BSG_ERR_STATE;
+    }
+}
+
+
+int bsg_load_checkpoint(const char* path, size_t cap, uint64_t* ids, double* pos, double* rot, double* ls,
+                        double* feat, double* op, size_t* out_n, int* out_fd, int* format_code) {
+    if (!path) {
+        g_drv_err = "null path";
+        return BSG_ERR_INVALID_ARGUMENT;
+    }
+    return checkpoint_out([&] { return blocksplat::load_scene(path); }, cap, ids, pos, rot, ls, feat, op, out_n,
+                          out_fd, format_code);
+}
+
+int bsg_decode_checkpoint(const uint8_t* data, size_t size, size_t cap, uint64_t* ids, double* pos, double* rot,
+                          double* ls, double* feat, double* op, size_t* out_n, int* out_fd, int* format_code) {
+    if (!data && size) {
+        g_drv_err = "null data";
+        return BSG_ERR_INVALID_ARGUMENT;
+    }
+    return checkpoint_out([&] { return blocksplat::decode_scene(data, size); }, cap, ids, pos, rot, ls, feat, op,
+                          out_n, out_fd, format_code);
 }
 
 }  // extern "C"
