@@ -705,10 +705,22 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
                 owners[id] = {b};
                 global_ids.insert(id);
             }
+        // The shared set only shrinks (new rows have one owner; removals drop
+        // owners), so it is S minus the ids that fell below two owners: a
+        // merge over S and the (sorted) changed ids instead of a scan of the
+        // whole owner map every round.
+        std::vector<uint64_t> lost;
+        for (const auto& [id, prev] : prev_owner_count) {
+            (void)prev;
+            auto it = owners.find(id);
+            if (it == owners.end() || it->second.size() < 2) lost.push_back(id);
+        }
         std::vector<uint64_t> shared_now;
-        for (const auto& [id, list] : owners)
-            if (list.size() >= 2) shared_now.push_back(id);
-        if (shared_now != S) {
+        if (!lost.empty()) {
+            shared_now.reserve(S.size());
+            std::set_difference(S.begin(), S.end(), lost.begin(), lost.end(), std::back_inserter(shared_now));
+        }
+        if (!lost.empty() && shared_now.size() != S.size()) {
             // new slot table; every block keeps its anchor / duals for the ids
             // that stay shared, z_prev comes from the last consensus (all of
             // shared_now was shared before: new rows start single-owner)
@@ -786,32 +798,44 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
     model.opacity_logits.resize(model.size());
     std::vector<double> zs(S.size() * D);
     if (!S.empty()) check(bsg_download_consensus(ctxs[0], zs.data()));
-    std::vector<GaussianCloud> finals;
-    for (auto& x : tr) finals.push_back(x.cloud());
-    for (size_t i = 0; i < model.size(); ++i) {
-        const uint64_t id = model.ids[i];
-        auto sit = std::lower_bound(S.begin(), S.end(), id);
-        double row[11 + kFeatureDimDeg1];
-        if (sit != S.end() && *sit == id) {
-            const double* z = &zs[(sit - S.begin()) * D];
-            std::copy(z, z + D, row);
-            const double qn = std::sqrt(((row[3] * row[3] + row[4] * row[4]) + row[5] * row[5]) + row[6] * row[6]);
-            if (qn == 0.0) {
-                row[3] = 1; row[4] = 0; row[5] = 0; row[6] = 0;
-            } else {
-                for (int k = 3; k < 7; ++k) row[k] /= qn;
-            }
-        } else {
-            const uint32_t owner = owners.at(id).front();
-            const GaussianCloud& c = finals[owner];
-            const std::vector<double> r = rows_of(c, {c.find(id)});
-            std::copy(r.begin(), r.end(), row);
-        }
+    auto row_of = [&](uint64_t id) {
+        return static_cast<size_t>(std::lower_bound(model.ids.begin(), model.ids.end(), id) - model.ids.begin());
+    };
+    auto put = [&](size_t i, const double* row) {
         for (int k = 0; k < 3; ++k) model.positions[3 * i + k] = row[k];
         for (int k = 0; k < 4; ++k) model.rotations[4 * i + k] = row[3 + k];
         for (int k = 0; k < 3; ++k) model.log_scales[3 * i + k] = row[7 + k];
         for (int k = 0; k < fd; ++k) model.features[i * fd + k] = row[10 + k];
         model.opacity_logits[i] = row[10 + fd];
+    };
+    // shared rows: the consensus z with unit quaternions (runtime.cpp:578-581)
+    for (size_t k = 0; k < S.size(); ++k) {
+        double row[11 + kFeatureDimDeg1];
+        std::copy(&zs[k * D], &zs[k * D] + D, row);
+        const double qn = std::sqrt(((row[3] * row[3] + row[4] * row[4]) + row[5] * row[5]) + row[6] * row[6]);
+        if (qn == 0.0) {
+            row[3] = 1; row[4] = 0; row[5] = 0; row[6] = 0;
+        } else {
+            for (int q = 3; q < 7; ++q) row[q] /= qn;
+        }
+        put(row_of(S[k]), row);
+    }
+    // every other row from its single owner's final cloud, one pass per block
+    for (uint32_t b = 0; b < K; ++b) {
+        const GaussianCloud c = tr[b].cloud();
+        for (size_t j = 0; j < c.size(); ++j) {
+            const uint64_t id = c.ids[j];
+            if (std::binary_search(S.begin(), S.end(), id)) continue;
+            auto it = owners.find(id);
+            if (it == owners.end() || it->second.front() != b) continue;
+            double row[11 + kFeatureDimDeg1];
+            for (int k = 0; k < 3; ++k) row[k] = c.positions[3 * j + k];
+            for (int k = 0; k < 4; ++k) row[3 + k] = c.rotations[4 * j + k];
+            for (int k = 0; k < 3; ++k) row[7 + k] = c.log_scales[3 * j + k];
+            for (int k = 0; k < fd; ++k) row[10 + k] = c.features[j * fd + k];
+            row[10 + fd] = c.opacity_logits[j];
+            put(row_of(id), row);
+        }
     }
     result.model = std::move(model);
     result.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
