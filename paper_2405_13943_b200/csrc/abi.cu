@@ -355,8 +355,8 @@ void install_shared_masks(Ctx* c) {
         prefix[w] = run;
         run += static_cast<uint32_t>(__builtin_popcount(mask[w]));
     }
-    BSG_CUDA(cudaMemcpy(c->sh_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice));
-    BSG_CUDA(cudaMemcpy(c->sh_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice));
+    BSG_CUDA(cudaMemcpyAsync(c->sh_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    BSG_CUDA(cudaMemcpyAsync(c->sh_prefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, c->stream));
 }
 
 namespace {
@@ -941,7 +941,7 @@ int bsg_set_views(bsg_ctx* h, size_t n_views, const bsg_camera* cams, const doub
             for (size_t i = 0; i < 3 * px; ++i) hh[i] = static_cast<float>(gt[v][i]);
             float* d = nullptr;
             BSG_CUDA(cudaMalloc(&d, hh.size() * sizeof(float)));
-            BSG_CUDA(cudaMemcpy(d, hh.data(), hh.size() * sizeof(float), cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpyAsync(d, hh.data(), hh.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
             c->view_gt.push_back(d);
             ensure_image_buffers(c, static_cast<int>(cams[v].width), static_cast<int>(cams[v].height));
         }
@@ -1125,16 +1125,16 @@ int bsg_set_shared(bsg_ctx* h, size_t ns, const uint32_t* rows, const uint32_t* 
         dev_alloc(&c->qref, 4 * std::max<size_t>(n_slots, 1));
         dev_alloc(&c->slot_reset, n_slots);
         if (ns) {
-            BSG_CUDA(cudaMemcpy(c->sh_rows, rows, ns * 4, cudaMemcpyHostToDevice));
-            BSG_CUDA(cudaMemcpy(c->sh_slots, slots, ns * 4, cudaMemcpyHostToDevice));
-            BSG_CUDA(cudaMemcpy(c->sh_first, first, ns, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpyAsync(c->sh_rows, rows, ns * 4, cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemcpyAsync(c->sh_slots, slots, ns * 4, cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemcpyAsync(c->sh_first, first, ns, cudaMemcpyHostToDevice, c->stream));
         }
-        if (n_slots) BSG_CUDA(cudaMemcpy(c->slot_owners, owners, n_slots * 4, cudaMemcpyHostToDevice));
+        if (n_slots) BSG_CUDA(cudaMemcpyAsync(c->slot_owners, owners, n_slots * 4, cudaMemcpyHostToDevice, c->stream));
         c->sh_rows_host.assign(rows, rows + ns);
         c->sh_slots_host.assign(slots, slots + ns);
         c->sh_first_host.assign(first, first + ns);
         install_shared_masks(c);
-        BSG_CUDA(cudaMemset(c->in_zprev, 0, std::max<size_t>(n_slots, 1)));
+        BSG_CUDA(cudaMemsetAsync(c->in_zprev, 0, std::max<size_t>(n_slots, 1), c->stream));
         c->anchored = false;
     });
 }
@@ -1146,16 +1146,16 @@ int bsg_set_anchor(bsg_ctx* h, const double* z_rows, const double* zprev_slots, 
         use_device(c);
         const std::vector<float> zc = rows_to_cm(z_rows, c->n_shared, c->D);
         if (c->n_shared) {
-            BSG_CUDA(cudaMemcpy(c->z, zc.data(), c->D * c->n_shared * 4, cudaMemcpyHostToDevice));
-            BSG_CUDA(cudaMemset(c->u, 0, c->D * c->n_shared * 4));
+            BSG_CUDA(cudaMemcpyAsync(c->z, zc.data(), c->D * c->n_shared * 4, cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemsetAsync(c->u, 0, c->D * c->n_shared * 4, c->stream));
         }
         if (c->n_slots) {
             if (zprev_slots) {
                 const std::vector<float> zp = rows_to_cm(zprev_slots, c->n_slots, c->D);
-                BSG_CUDA(cudaMemcpy(c->zprev, zp.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
-                BSG_CUDA(cudaMemset(c->in_zprev, 1, c->n_slots));
+                BSG_CUDA(cudaMemcpyAsync(c->zprev, zp.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice, c->stream));
+                BSG_CUDA(cudaMemsetAsync(c->in_zprev, 1, c->n_slots, c->stream));
             } else {
-                BSG_CUDA(cudaMemset(c->in_zprev, 0, c->n_slots));
+                BSG_CUDA(cudaMemsetAsync(c->in_zprev, 0, c->n_slots, c->stream));
             }
         }
         if (rho) {
@@ -1183,7 +1183,8 @@ int bsg_download_duals(bsg_ctx* h, double* u_rows) {
         if (!c) invalid("null context");
         use_device(c);
         std::vector<float> hu(c->D * std::max<size_t>(c->n_shared, 1));
-        if (c->n_shared) BSG_CUDA(cudaMemcpy(hu.data(), c->u, c->D * c->n_shared * 4, cudaMemcpyDeviceToHost));
+        if (c->n_shared) BSG_CUDA(cudaMemcpyAsync(hu.data(), c->u, c->D * c->n_shared * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         cm_to_rows(hu.data(), c->n_shared, c->D, u_rows);
     });
 }
@@ -1195,7 +1196,7 @@ int bsg_upload_duals(bsg_ctx* h, const double* u_rows) {
         if (!c->anchored) throw Error{BSG_ERR_STATE, "duals before set_anchor"};
         use_device(c);
         const std::vector<float> uc = rows_to_cm(u_rows, c->n_shared, c->D);
-        if (c->n_shared) BSG_CUDA(cudaMemcpy(c->u, uc.data(), c->D * c->n_shared * 4, cudaMemcpyHostToDevice));
+        if (c->n_shared) BSG_CUDA(cudaMemcpyAsync(c->u, uc.data(), c->D * c->n_shared * 4, cudaMemcpyHostToDevice, c->stream));
     });
 }
 
@@ -1205,7 +1206,8 @@ int bsg_download_anchor(bsg_ctx* h, double* z_rows) {
         if (!c) invalid("null context");
         use_device(c);
         std::vector<float> hz(c->D * std::max<size_t>(c->n_shared, 1));
-        if (c->n_shared) BSG_CUDA(cudaMemcpy(hz.data(), c->z, c->D * c->n_shared * 4, cudaMemcpyDeviceToHost));
+        if (c->n_shared) BSG_CUDA(cudaMemcpyAsync(hz.data(), c->z, c->D * c->n_shared * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         cm_to_rows(hz.data(), c->n_shared, c->D, z_rows);
     });
 }
@@ -1219,7 +1221,8 @@ int bsg_download_consensus(bsg_ctx* h, double* z_slots) {
         round_slots_from_sums(c);
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         std::vector<float> hz(c->D * std::max<size_t>(c->n_slots, 1));
-        if (c->n_slots) BSG_CUDA(cudaMemcpy(hz.data(), c->zslot, c->D * c->n_slots * 4, cudaMemcpyDeviceToHost));
+        if (c->n_slots) BSG_CUDA(cudaMemcpyAsync(hz.data(), c->zslot, c->D * c->n_slots * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         cm_to_rows(hz.data(), c->n_slots, c->D, z_slots);
     });
 }
@@ -1233,10 +1236,10 @@ int bsg_apply_broadcast(bsg_ctx* h, const double* z_slots, size_t n_reset, const
         use_device(c);
         if (c->n_slots) {
             const std::vector<float> zc = rows_to_cm(z_slots, c->n_slots, c->D);
-            BSG_CUDA(cudaMemcpy(c->zslot, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpyAsync(c->zslot, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice, c->stream));
             c->zslot_from_pack = false;
-            BSG_CUDA(cudaMemcpy(c->zprev, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice));
-            BSG_CUDA(cudaMemset(c->in_zprev, 1, c->n_slots));
+            BSG_CUDA(cudaMemcpyAsync(c->zprev, zc.data(), c->D * c->n_slots * 4, cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemsetAsync(c->in_zprev, 1, c->n_slots, c->stream));
         }
         bsg_round_args args{};
         args.n_reset = n_reset;
@@ -1334,7 +1337,7 @@ int bsg_consensus_wait(bsg_ctx* h, bsg_round_result* out, bsg_penalties* rho_out
         BSG_CUDA(cudaEventSynchronize(c->round_done));
         c->round_pending = false;
         double rs[5];
-        BSG_CUDA(cudaMemcpy(rs, c->rho_state, sizeof(rs), cudaMemcpyDeviceToHost));
+        BSG_CUDA(cudaMemcpyAsync(rs, c->rho_state, sizeof(rs), cudaMemcpyDeviceToHost, c->stream));
         c->rho = bsg_penalties{rs[0], rs[1], rs[2], rs[3], rs[4]};
         if (rho_out) *rho_out = c->rho;
         float ms = 0;

@@ -245,7 +245,7 @@ void maybe_densify(Ctx* c) {
             BSG_CUDA(cudaMalloc(&nz, c->D * std::max<size_t>(ns, 1) * sizeof(float)));
             BSG_CUDA(cudaMalloc(&nu, c->D * std::max<size_t>(ns, 1) * sizeof(float)));
             if (ns) {
-                BSG_CUDA(cudaMemcpy(src_dev, src.data(), ns * 4, cudaMemcpyHostToDevice));
+                BSG_CUDA(cudaMemcpyAsync(src_dev, src.data(), ns * 4, cudaMemcpyHostToDevice, c->stream));
                 gather_cols_kernel<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, c->stream>>>(c->z, c->n_shared,
                                                                                               src_dev, ns, c->D, nz);
                 BSG_LAUNCHED(c);
@@ -264,9 +264,9 @@ void maybe_densify(Ctx* c) {
         realloc_dev(&c->sh_slots, ns);
         realloc_dev(&c->sh_first, ns);
         if (ns) {
-            BSG_CUDA(cudaMemcpy(c->sh_rows, rows.data(), ns * 4, cudaMemcpyHostToDevice));
-            BSG_CUDA(cudaMemcpy(c->sh_slots, slots.data(), ns * 4, cudaMemcpyHostToDevice));
-            BSG_CUDA(cudaMemcpy(c->sh_first, first.data(), ns, cudaMemcpyHostToDevice));
+            BSG_CUDA(cudaMemcpyAsync(c->sh_rows, rows.data(), ns * 4, cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemcpyAsync(c->sh_slots, slots.data(), ns * 4, cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemcpyAsync(c->sh_first, first.data(), ns, cudaMemcpyHostToDevice, c->stream));
         }
         c->n_shared = ns;
         c->sh_rows_host = std::move(rows);

@@ -185,7 +185,7 @@ void launch_passes(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_
     if (c->radix_status_cap < need) {
         if (c->radix_status) cudaFree(c->radix_status);
         BSG_CUDA(cudaMalloc(&c->radix_status, 2 * need * sizeof(unsigned long long)));
-        BSG_CUDA(cudaMemset(c->radix_status, 0, 2 * need * sizeof(unsigned long long)));  // epoch 0 is never used
+        BSG_CUDA(cudaMemsetAsync(c->radix_status, 0, 2 * need * sizeof(unsigned long long), c->stream));  // epoch 0 is never used
         c->radix_status_cap = 2 * need;
     }
     const size_t smem = (sizeof(K) + sizeof(uint32_t)) * kTileKeys;

@@ -225,7 +225,7 @@ void prepare_status(Ctx* c, uint32_t tiles) {
     if (c->scan_status_cap < need) {
         if (c->scan_status) cudaFree(c->scan_status);
         BSG_CUDA(cudaMalloc(&c->scan_status, 2 * need * sizeof(unsigned long long)));
-        BSG_CUDA(cudaMemset(c->scan_status, 0, 2 * need * sizeof(unsigned long long)));  // epoch 0 is never used
+        BSG_CUDA(cudaMemsetAsync(c->scan_status, 0, 2 * need * sizeof(unsigned long long), c->stream));  // epoch 0 is never used
         c->scan_status_cap = 2 * need;
     }
 }
@@ -235,7 +235,7 @@ void prepare_status(Ctx* c, uint32_t tiles) {
 Lookback next_lookback(Ctx* c, int which, uint32_t grid) {
     if (!c->lb_ticket) {
         BSG_CUDA(cudaMalloc(&c->lb_ticket, 2 * sizeof(unsigned long long)));
-        BSG_CUDA(cudaMemset(c->lb_ticket, 0, 2 * sizeof(unsigned long long)));
+        BSG_CUDA(cudaMemsetAsync(c->lb_ticket, 0, 2 * sizeof(unsigned long long), c->stream));
         c->lb_next[0] = c->lb_next[1] = 0;
     }
     c->lb_epoch = (c->lb_epoch + 1) & 0x3fffffffu;

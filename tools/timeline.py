@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--e2e", action="store_true", help="steps through bsg_train_step_host (pinned host GT)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -30,12 +31,21 @@ def main():
     blk, cams, _, _ = bench.build_block(0, 1, bench.CFG["n"], 0, constant_gt=False)
     g = np.random.default_rng(3)
     seq = [int(v) for v in g.integers(0, len(cams), args.warmup + args.steps)]
+    if args.e2e:
+        _, _, gts, _ = bench.build_block(0, 1, 1000, 0, constant_gt=True)  # shapes only
+        pinned = [torch.full((bench.CFG["height"], bench.CFG["width"], 3), 0.5).pin_memory() for _ in range(4)]
+
+        def step(v):
+            blk.train_step_host(cams[v], pinned[v % 4].numpy())
+    else:
+        def step(v):
+            blk.train_steps([v], want_losses=False)
     for v in seq[:args.warmup]:
-        blk.train_steps([v], want_losses=False)
+        step(v)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for v in seq[args.warmup:]:
-            blk.train_steps([v], want_losses=False)
+            step(v)
         torch.cuda.synchronize()
     # host launch -> device start latency per kernel (chrome trace: correlation ids)
     import tempfile
