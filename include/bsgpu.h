@@ -157,6 +157,14 @@ int bsg_train_steps(bsg_ctx* ctx, size_t n, const uint32_t* view_seq, double* lo
 /* One train_step() whose ground truth comes from host memory (HxWx3 FP32,
  * pinned or pageable); the copy is part of the step (end-to-end path). */
 int bsg_train_step_host(bsg_ctx* ctx, const bsg_camera* cam, const float* gt_rgb_host, double* loss);
+/* n steps on host ground-truth images (BlockTrainer::run_iterations over
+ * host-resident views, trainer.hpp:100-104): step k trains on cams[k] against
+ * gts_host[k] (HxWx3 FP32, pinned for full overlap). Each image is copied on
+ * a copy stream into one of two device buffers while the previous step
+ * computes; losses[k] (nullable) receives step k's loss (one read-back of all
+ * n at the end of the call). */
+int bsg_train_steps_host(bsg_ctx* ctx, size_t n, const bsg_camera* cams, const float* const* gts_host,
+                         double* losses);
 uint64_t bsg_iteration(const bsg_ctx* ctx);
 /* Optimizer moments, [D][n] component-major FP64 (D = 11 + fd), for parity. */
 int bsg_download_moments(bsg_ctx* ctx, double* m, double* v);

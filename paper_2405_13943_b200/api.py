@@ -130,6 +130,7 @@ SYMBOLS = [
     ("bsg_trainer_init", ctypes.c_int, [_P, ctypes.POINTER(bsg_trainer_config)]),
     ("bsg_train_steps", ctypes.c_int, [_P, _SZ, _U32P, _DP]),
     ("bsg_train_step_host", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _FP, _DP]),
+    ("bsg_train_steps_host", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_FP), _DP]),
     ("bsg_iteration", ctypes.c_uint64, [_P]),
     ("bsg_download_moments", ctypes.c_int, [_P, _DP, _DP]),
     ("bsg_take_removed_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
@@ -402,6 +403,16 @@ class Block:
         loss = ctypes.c_double()
         _check(_lib.bsg_train_step_host(self.h, ctypes.byref(cam), _ptr(gt_f32, ctypes.c_float), ctypes.byref(loss)))
         return loss.value
+
+    def train_steps_host(self, cams, gts_f32):
+        """n steps on host images (float32 HxWx3, pinned for overlap); returns the n losses."""
+        n = len(cams)
+        cam_arr = (bsg_camera * n)(*cams)
+        keep = [np.ascontiguousarray(g, dtype=np.float32) for g in gts_f32]
+        ptrs = (_FP * n)(*[_ptr(g, ctypes.c_float) for g in keep])
+        out = np.zeros(n)
+        _check(_lib.bsg_train_steps_host(self.h, n, cam_arr, ptrs, _ptr(out, ctypes.c_double)))
+        return out
 
     def iteration(self):
         return _lib.bsg_iteration(self.h)

@@ -81,7 +81,7 @@ void free_all(Ctx* c) {
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
-                    c->ssim_f, c->gt_stage, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
+                    c->ssim_f, c->gt_stage, c->gt_stage_b, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
                     c->in_zprev, c->slot_owners, c->pack, c->qref, c->slot_reset, c->round_scalars};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -93,7 +93,8 @@ void free_all(Ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->nccl) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl));
-    if (c->gt_ready) cudaEventDestroy(c->gt_ready);
+    for (cudaEvent_t e : {c->gt_ready, c->gt_ready_b, c->gt_free[0], c->gt_free[1]})
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->x_ready, c->round_done, c->round_t0, c->round_t1})
         if (e) cudaEventDestroy(e);
     if (c->round_host) cudaFreeHost(c->round_host);
@@ -189,6 +190,7 @@ void ensure_image_buffers(Ctx* c, int W, int H) {
         dev_alloc(&c->dl_dc, 3 * px);
         dev_alloc(&c->ssim_f, 9 * px);
         dev_alloc(&c->gt_stage, 3 * px);
+        dev_alloc(&c->gt_stage_b, 3 * px);
         c->img_cap = px;
     }
     const size_t ntiles = static_cast<size_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
@@ -590,6 +592,8 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             BSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             BSG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
             BSG_CUDA(cudaEventCreateWithFlags(&c->gt_ready, cudaEventDisableTiming));
+            BSG_CUDA(cudaEventCreateWithFlags(&c->gt_ready_b, cudaEventDisableTiming));
+            for (auto& e : c->gt_free) BSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             BSG_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
             BSG_CUDA(cudaEventCreateWithFlags(&c->x_ready, cudaEventDisableTiming));
             BSG_CUDA(cudaEventCreateWithFlags(&c->round_done, cudaEventDisableTiming));
@@ -993,6 +997,46 @@ int bsg_train_steps(bsg_ctx* h, size_t n, const uint32_t* view_seq, double* loss
                                      c->stream));
             BSG_CUDA(cudaStreamSynchronize(c->stream));
             for (size_t k = 0; k < n; ++k) losses[k] = l[3 * k];
+        }
+        collect_stage_times(c);
+    });
+}
+
+int bsg_train_steps_host(bsg_ctx* h, size_t n, const bsg_camera* cams, const float* const* gts_host,
+                         double* losses) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!c->trainer_ready) throw Error{BSG_ERR_STATE, "train step before bsg_trainer_init"};
+        if (n && (!cams || !gts_host)) invalid("null views");
+        for (size_t k = 0; k < n; ++k) {
+            check_camera(&cams[k]);
+            if (!gts_host[k]) invalid("null ground truth");
+        }
+        use_device(c);
+        ensure_views_buffers(c, std::max<size_t>(n, 1));
+        for (size_t k = 0; k < n; ++k) {
+            const bsg_camera& cam = cams[k];
+            ensure_image_buffers(c, static_cast<int>(cam.width), static_cast<int>(cam.height));
+            const int b = static_cast<int>(k & 1);
+            float* buf = b ? c->gt_stage_b : c->gt_stage;
+            cudaEvent_t ready = b ? c->gt_ready_b : c->gt_ready;
+            // step k-2 read this buffer: its loss must be done before the overwrite
+            if (k >= 2) BSG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->gt_free[b], 0));
+            const size_t px = static_cast<size_t>(cam.width) * cam.height;
+            BSG_CUDA(cudaMemcpyAsync(buf, gts_host[k], 3 * px * sizeof(float), cudaMemcpyHostToDevice, c->copy_stream));
+            BSG_CUDA(cudaEventRecord(ready, c->copy_stream));
+            train_one(c, cam, buf, c->losses_dev + 3 * k, ready);
+            BSG_CUDA(cudaEventRecord(c->gt_free[b], c->stream));
+            maybe_densify(c);
+        }
+        if (n) {
+            std::vector<double> l(3 * n);
+            BSG_CUDA(cudaMemcpyAsync(l.data(), c->losses_dev, l.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                     c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            if (losses)
+                for (size_t k = 0; k < n; ++k) losses[k] = l[3 * k];
         }
         collect_stage_times(c);
     });

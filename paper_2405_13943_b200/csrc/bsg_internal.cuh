@@ -111,6 +111,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host ground-truth uploads (e2e path)
     cudaEvent_t gt_ready = nullptr;
+    cudaEvent_t gt_ready_b = nullptr, gt_free[2] = {nullptr, nullptr};  // double-buffered host ground truth
     cudaStream_t comm_stream = nullptr;  // consensus rounds (overlap with the next step)
     cudaEvent_t x_ready = nullptr, round_done = nullptr, round_t0 = nullptr, round_t1 = nullptr;
     bool round_pending = false;
@@ -183,6 +184,7 @@ struct Ctx {
     float* dl_dc = nullptr;
     float* ssim_f = nullptr;   // 9 planes of the valid window grid
     float* gt_stage = nullptr; // host ground truth staging (e2e path)
+    float* gt_stage_b = nullptr;  // second staging buffer (bsg_train_steps_host)
 
     // resident training views
     std::vector<bsg_camera> view_cams;

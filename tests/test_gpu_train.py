@@ -401,3 +401,20 @@ def test_train_step_edge_cases_track_oracle(case):
         w = HostCloud.from_oracle(t.cloud())
         g = np.concatenate([got["pos"], got["rot"], got["ls"], got["feat"], got["op"][:, None]], 1)
         assert np.mean(np.abs(g - rows_of(w)) <= 1e-5 + 1e-5 * np.abs(rows_of(w))) >= 0.98
+
+
+def test_train_steps_host_matches_resident_views():
+    """bsg_train_steps_host (host images, double-buffered uploads) trains like
+    bsg_train_steps on the same views resident on the device."""
+    s, init = toy_scene(seed=5)
+    seq = orc.view_sequence(1, 0, len(s.views), 9)
+    a = device_trainer(init, s)
+    la = a.train_steps(seq)
+    b = device_trainer(init, s)
+    ims = s.images()
+    cams = [dev_cam(s.views[v]) for v in seq]
+    lb = b.train_steps_host(cams, [np.ascontiguousarray(ims[v], dtype=np.float32) for v in seq])
+    np.testing.assert_allclose(lb, la, rtol=1e-5)
+    ca, cb = a.download_cloud(), b.download_cloud()
+    for k in ("pos", "rot", "ls", "feat", "op"):
+        np.testing.assert_allclose(cb[k], ca[k], rtol=1e-4, atol=1e-6)
