@@ -106,6 +106,22 @@ __device__ __forceinline__ uint32_t subtile_mask(int x0, int x1, int y0, int y1,
            (right && bottom ? 8u : 0u);
 }
 
+// Forward blend: hit mask of a splat rect over warp w's 8x8 sub-tile: low
+// byte = the sub-tile columns inside [x0, x1], high byte = the rows inside
+// [y0, y1]; 0 when they do not overlap. Built once per staged entry, so the
+// per-entry hit test of a lane is two shifts and an AND (measured: -3% fwd;
+// in the backward the extra staging work outweighed it, +2%).
+__device__ __forceinline__ uint32_t span_bits(int lo, int hi) {  // bits [lo, hi] of 0..7, clamped
+    lo = max(lo, 0);
+    hi = min(hi, 7);
+    return lo <= hi ? ((0xffu >> (7 - hi)) & (0xffu << lo)) : 0u;
+}
+
+__device__ __forceinline__ uint16_t region_hits(int x0, int x1, int y0, int y1, int sx, int sy) {
+    const uint32_t cm = span_bits(x0 - sx, x1 - sx), rm = span_bits(y0 - sy, y1 - sy);
+    return static_cast<uint16_t>(cm && rm ? (cm | (rm << 8)) : 0u);
+}
+
 __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* __restrict__ ranges,
                                                                   const uint32_t* __restrict__ pval,
                                                                   const float4* __restrict__ rec, int W, int H,
@@ -118,7 +134,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   unsigned long long* __restrict__ evals) {
     pdl_prologue();
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
-    __shared__ uint8_t s_m[kBatch];
+    __shared__ uint16_t s_hm[kBlendThreads / 32][kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
     const int tile = blockIdx.x;
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
@@ -127,13 +143,13 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
     const int py0 = ty0 + (warp >> 1) * 8 + (lane >> 3);
     const int py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+    const int hb = lane & 7, hr = 8 + (lane >> 3);  // this lane's column bit, first row bit
     const uint2 range = ranges[tile];
     const double oma_clamp = 1.0 - aclamp_d;
     float T0 = 1.f, T1 = 1.f, r0 = 0.f, g0 = 0.f, b0 = 0.f, r1 = 0.f, g1 = 0.f, b1 = 0.f;
     double Td0 = 1.0, Td1 = 1.0;
     uint32_t n0 = 0, n1 = 0, last0 = 0, last1 = 0;
     bool done0 = !in0, done1 = !in1;
-    const uint32_t wbit = 1u << warp;
     const float fx = static_cast<float>(px), fy0 = static_cast<float>(py0), fy1 = static_cast<float>(py1);
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
         if (__syncthreads_count(done0 && done1) == kBlendThreads) break;
@@ -145,10 +161,13 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                 const float4 c = rec[r + 2];
                 int x0, x1, y0, y1;
                 unpack_rect(c, x0, x1, y0, y1);
-                s_a[threadIdx.x + h * kBlendThreads] = rec[r];
-                s_b[threadIdx.x + h * kBlendThreads] = rec[r + 1];
-                s_c[threadIdx.x + h * kBlendThreads] = c;
-                s_m[threadIdx.x + h * kBlendThreads] = static_cast<uint8_t>(subtile_mask(x0, x1, y0, y1, tx0, ty0));
+                const int t = threadIdx.x + h * kBlendThreads;
+                s_a[t] = rec[r];
+                s_b[t] = rec[r + 1];
+                s_c[t] = c;
+#pragma unroll
+                for (int w = 0; w < kBlendThreads / 32; ++w)
+                    s_hm[w][t] = region_hits(x0, x1, y0, y1, tx0 + (w & 1) * 8, ty0 + (w >> 1) * 8);
             }
         }
         __syncthreads();
@@ -157,7 +176,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
         int nl = 0;
         for (int c0 = 0; c0 < cnt; c0 += 32) {
             const int e = c0 + lane;
-            const bool mine = e < cnt && (s_m[e] & wbit);
+            const bool mine = e < cnt && s_hm[warp][e] != 0;
             const unsigned bal = __ballot_sync(0xffffffffu, mine);
             if (mine) s_list[warp][nl + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
             nl += __popc(bal);
@@ -165,14 +184,12 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
         __syncwarp();
         for (int k = 0; k < nl && !(done0 && done1); ++k) {
             const int j = s_list[warp][k];
-            const float4 c = s_c[j];
-            int x0, x1, y0, y1;
-            unpack_rect(c, x0, x1, y0, y1);
-            const bool inx = px >= x0 && px <= x1;
-            const bool hit0 = !done0 && inx && py0 >= y0 && py0 <= y1;
-            const bool hit1 = !done1 && inx && py1 >= y0 && py1 <= y1;
+            const uint32_t hm = s_hm[warp][j];
+            const uint32_t cb = hm >> hb;
+            const bool hit0 = !done0 && (cb & (hm >> hr) & 1u);
+            const bool hit1 = !done1 && (cb & (hm >> (hr + 4)) & 1u);
             if (!(hit0 || hit1)) continue;
-            const float4 a = s_a[j], b = s_b[j];
+            const float4 a = s_a[j], b = s_b[j], c = s_c[j];
             const float dx = fx - a.x;
             const uint32_t pos = start - range.x + static_cast<uint32_t>(j) + 1;
             if (hit0) {
