@@ -214,12 +214,13 @@ void radix_sort(Ctx* c, K* keys[2], uint32_t* vals[2], uint32_t n, int first_pas
     if (n <= 1) return;
     if (n >= (1u << 30)) throw Error{BSG_ERR_CAPACITY, "radix sort supports < 2^30 keys"};
     // Tile size: the passes are look-back-latency bound at the sizes of a step
-    // (V ~ 2e5 keys, P ~ 4e5 pairs); 2k-key tiles measured best there (cfg 2:
-    // depth sort 79 -> 71 us, tile sort 52 -> 43 us vs 1k-key tiles); only tiny
-    // inputs keep 1k-key tiles for SM coverage.
+    // (V ~ 2e5 keys, P ~ 4e5 pairs). Measured at cfg 2: 2k-key tiles beat 1k
+    // (depth sort 79 -> 71 us, tile sort 52 -> 43 us); 4k beat 2k from ~4e5
+    // keys on (tile sort 34.5 -> 32.3 us) but not at 2e5 (depth 42 -> 46 us);
+    // tiny inputs keep 1k-key tiles for SM coverage.
     if (n < (1u << 16))
         launch_passes<K, 4>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
-    else if (n < (1u << 22))
+    else if (n < (1u << 18))
         launch_passes<K, 8>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);
     else
         launch_passes<K, 16>(c, keys, vals, n, first_pass, passes, d_hist, h_hist, sel);

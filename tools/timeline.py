@@ -37,6 +37,9 @@ def main():
 
         def step(v):
             blk.train_step_host(cams[v], pinned[v % 4].numpy())
+
+        def chunk(vs):  # the bench's e2e path: one host-image call per consensus interval
+            blk.train_steps_host([cams[v] for v in vs], [pinned[v % 4].numpy() for v in vs])
     else:
         def step(v):
             blk.train_steps([v], want_losses=False)
@@ -44,8 +47,13 @@ def main():
         step(v)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        for v in seq[args.warmup:]:
-            step(v)
+        if args.e2e:
+            rest = seq[args.warmup:]
+            for i in range(0, len(rest), 25):
+                chunk(rest[i:i + 25])
+        else:
+            for v in seq[args.warmup:]:
+                step(v)
         torch.cuda.synchronize()
     # host launch -> device start latency per kernel (chrome trace: correlation ids)
     import tempfile
