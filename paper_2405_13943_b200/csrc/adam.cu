@@ -273,8 +273,11 @@ __device__ __forceinline__ float adam_update(float x, float g, float& m, float& 
 
 __device__ __forceinline__ int comp_of_group(int y) { return y < 3 ? y : y + 4; }  // pos 0-2, ls/feat/op 7..
 
+// Occupancy: 5 (scalar groups, 48 registers) and 6 (quaternion group, 39)
+// resident CTAs per SM keep more loads in flight than the unbounded 52 / 64
+// registers (cfg 2: 134.4 -> 131.4 us for the two launches).
 template <int Q>
-__global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
+__global__ __launch_bounds__(256, 5) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
                                                    size_t cap, uint32_t n, const uint32_t* __restrict__ vis_mask,
                                                    const uint32_t* __restrict__ vis_prefix,
                                                    const float* __restrict__ gbuf,
@@ -383,7 +386,7 @@ __global__ __launch_bounds__(256) void adam_kernel(float* __restrict__ x, float*
 // coalesced scalar streams (x, m, v each), updated, canonicalised and written
 // back. One row per thread keeps the register count low enough for the
 // occupancy a 12-stream kernel needs.
-__global__ __launch_bounds__(256) void adam_rot_kernel(float* __restrict__ x, float* __restrict__ m,
+__global__ __launch_bounds__(256, 6) void adam_rot_kernel(float* __restrict__ x, float* __restrict__ m,
                                                        float* __restrict__ v, size_t cap, uint32_t n,
                                                        const uint32_t* __restrict__ vis_mask,
                                                        const uint32_t* __restrict__ vis_prefix,
