@@ -79,7 +79,7 @@ void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 void free_all(Ctx* c) {
     void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
-                    c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->scan_status, c->radix_status, c->radix_hist,
+                    c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
                     c->ssim_f, c->gt_stage, c->gt_stage_b, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
                     c->in_zprev, c->slot_owners, c->pack, c->qref, c->slot_reset, c->round_scalars};
@@ -196,6 +196,7 @@ void ensure_image_buffers(Ctx* c, int W, int H) {
     const size_t ntiles = static_cast<size_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
     if (ntiles > c->ranges_cap) {
         dev_alloc(&c->ranges, ntiles);
+        dev_alloc(&c->tile_order, ntiles);
         c->ranges_cap = ntiles;
     }
 }

@@ -155,6 +155,7 @@ struct Ctx {
     uint32_t* pval[2] = {nullptr, nullptr};
     int pairs_sorted = 0;
     uint2* ranges = nullptr;
+    uint32_t* tile_order = nullptr;  // blend launch order: tiles by descending pair count
     size_t ranges_cap = 0;
 
     // radix / scan scratch

@@ -84,6 +84,55 @@ __global__ __launch_bounds__(256) void ranges_kernel(const uint32_t* __restrict_
     if (i == P - 1 || pkey[i + 1] != k) ranges[k].y = i + 1;
 }
 
+// Blend launch order: tiles sorted by descending pair count (longest
+// processing time first), so the heaviest tiles start in the first wave and
+// the light ones fill the tail of the ~2.5 waves. One CTA, counting sort on
+// min(count, 1023); the order inside a bucket is free (tiles are
+// independent, every output is per tile). List-scheduling model on the cfg 2
+// views' tile counts: 7-19% shorter makespan than row-major order.
+__global__ __launch_bounds__(1024) void tile_order_kernel(const uint2* __restrict__ ranges, uint32_t ntiles,
+                                                          uint32_t* __restrict__ order) {
+    pdl_prologue();
+    __shared__ uint32_t s_cnt[1024];
+    __shared__ uint32_t s_warp[32];
+    const uint32_t t = threadIdx.x;
+    s_cnt[t] = 0;
+    __syncthreads();
+    for (uint32_t i = t; i < ntiles; i += 1024) {
+        const uint2 r = ranges[i];
+        atomicAdd(&s_cnt[1023u - min(r.y - r.x, 1023u)], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 1024 bucket counts
+    const uint32_t v = s_cnt[t];
+    uint32_t inc = v;
+    const int lane = t & 31, warp = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    s_cnt[t] = s_warp[warp] + inc - v;
+    __syncthreads();
+    for (uint32_t i = t; i < ntiles; i += 1024) {
+        const uint2 r = ranges[i];
+        order[atomicAdd(&s_cnt[1023u - min(r.y - r.x, 1023u)], 1u)] = i;
+    }
+}
+
 // K7 blend forward: one CTA of 128 threads per 16x16 tile. Warp w owns the
 // 8x8 sub-tile (w & 1, w >> 1); each lane owns two pixels of it (rows ly and
 // ly + 4), so every shared-memory record load and rect unpack serves two
@@ -131,12 +180,13 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   float* __restrict__ out_T,
                                                                   uint32_t* __restrict__ out_n,
                                                                   uint32_t* __restrict__ out_last,
-                                                                  unsigned long long* __restrict__ evals) {
+                                                                  unsigned long long* __restrict__ evals,
+                                                                  const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint16_t s_hm[kBlendThreads / 32][kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
-    const int tile = blockIdx.x;
+    const int tile = static_cast<int>(tile_order[blockIdx.x]);
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx0 + (warp & 1) * 8 + (lane & 7);
@@ -335,14 +385,15 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   const uint32_t* __restrict__ in_last,
                                                                   const float* __restrict__ dl_dc,
                                                                   float4* __restrict__ g2d,
-                                                                  double* __restrict__ g2d_wide) {
+                                                                  double* __restrict__ g2d_wide,
+                                                                  const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
     __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
     __shared__ uint32_t s_row[kBatch];
     __shared__ uint8_t s_m[kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
     __shared__ uint32_t s_max;
-    const int tile = blockIdx.x;
+    const int tile = static_cast<int>(tile_order[blockIdx.x]);
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx0 + (warp & 1) * 8 + (lane & 7);
@@ -461,8 +512,14 @@ void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V) {
 void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P) {
     const size_t ntiles = static_cast<size_t>(cam.tiles_x) * cam.tiles_y;
     if (V == 0) BSG_CUDA(cudaMemsetAsync(c->ranges, 0, ntiles * sizeof(uint2), c->stream));
-    if (P == 0) return;
+    if (P == 0) {
+        launch_pdl(c->stream, 1, 1024, 0, tile_order_kernel, c->ranges, static_cast<uint32_t>(ntiles), c->tile_order);
+        BSG_LAUNCHED(c);
+        return;
+    }
     launch_pdl(c->stream, (P + 255) / 256, 256, 0, ranges_kernel, c->pkey[c->pairs_sorted], P, c->ranges);
+    BSG_LAUNCHED(c);
+    launch_pdl(c->stream, 1, 1024, 0, tile_order_kernel, c->ranges, static_cast<uint32_t>(ntiles), c->tile_order);
     BSG_LAUNCHED(c);
 }
 
@@ -470,14 +527,14 @@ void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
     launch_pdl(c->stream, ntiles, kBlendThreads, 0, blend_fwd_kernel, c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, rc.tstop,
         static_cast<float>(rc.alpha_clamp), rc.alpha_clamp, rc.bg[0], rc.bg[1], rc.bg[2], c->out_rgb, c->out_T,
-        c->out_n, c->out_last, &c->counters->evals);
+        c->out_n, c->out_last, &c->counters->evals, c->tile_order);
     BSG_LAUNCHED(c);
 }
 
 void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
     launch_pdl(c->stream, ntiles, kBlendThreads, 0, blend_bwd_kernel, c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.alpha_clamp),
-        rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d, c->g2d_wide);
+        rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d, c->g2d_wide, c->tile_order);
     BSG_LAUNCHED(c);
 }
 
