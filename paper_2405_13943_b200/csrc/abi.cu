@@ -79,7 +79,7 @@ void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 void free_all(Ctx* c) {
     void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
-                    c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->scan_status, c->radix_status, c->radix_hist,
+                    c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->tile_cnt, c->tile_cur, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
                     c->ssim_f, c->gt_stage, c->gt_stage_b, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
                     c->in_zprev, c->slot_owners, c->pack, c->qref, c->slot_reset, c->round_scalars};
@@ -197,6 +197,8 @@ void ensure_image_buffers(Ctx* c, int W, int H) {
     if (ntiles > c->ranges_cap) {
         dev_alloc(&c->ranges, ntiles);
         dev_alloc(&c->tile_order, ntiles);
+        dev_alloc(&c->tile_cnt, ntiles);
+        dev_alloc(&c->tile_cur, ntiles);
         c->ranges_cap = ntiles;
     }
 }
@@ -224,10 +226,12 @@ int tile_bits(const DevCam& cam) {
     return b;
 }
 
-__global__ __launch_bounds__(512) void zero_counters_kernel(StepCounters* __restrict__ cnt) {
+__global__ __launch_bounds__(512) void zero_counters_kernel(StepCounters* __restrict__ cnt,
+                                                           uint32_t* __restrict__ tile_cnt, uint32_t ntiles) {
     pdl_prologue();
     uint32_t* w = reinterpret_cast<uint32_t*>(cnt);
     for (uint32_t i = threadIdx.x; i < sizeof(StepCounters) / 4; i += blockDim.x) w[i] = 0;
+    for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) tile_cnt[i] = 0;
 }
 
 // K1-K5: projection, compaction, depth sort, pair emission, tile sort, ranges.
@@ -235,41 +239,22 @@ __global__ __launch_bounds__(512) void zero_counters_kernel(StepCounters* __rest
 // pair-offset scan publish V and P to the host-mapped mailbox, and the host
 // polls for each while the kernel enqueued behind it (depth histograms, pair
 // emission into the current capacity) keeps the GPU busy.
-void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
-    ensure_image_buffers(c, cam.W, cam.H);
-    launch_pdl(c->stream, 1, 512, 0, zero_counters_kernel, c->counters);
-    BSG_LAUNCHED(c);
-    stage_begin(c, kStPreprocess);
-    launch_preprocess(c, cam, rc);
-    stage_end(c, kStPreprocess);
-    stage_begin(c, kStCompact);
-    uint32_t V = 0, kbits = 16;
+// Global binning (the fallback, and bsg_project's path): stable LSD sort of
+// the 32-bit range-normalised depth key + exact FP64 tie fix-up, pair
+// emission in depth order, stable tile-key sort, ranges, launch order.
+uint32_t bin_global(Ctx* c, const DevCam& cam, uint32_t V, uint32_t kbits) {
     uint32_t* k32[2] = {reinterpret_cast<uint32_t*>(c->vkey[0]), reinterpret_cast<uint32_t*>(c->vkey[1])};
-    if (c->n) {
-        Publish pv;
-        pv.val = &c->mbox->V;
-        pv.seq_word = &c->mbox->seq_v;
-        pv.seq = ++c->mbox_seq;
-        pv.extra_src = &c->counters->visible_pre;
-        pv.extra_dst = &c->mbox->visible_pre;
-        compact_visible(c, static_cast<uint32_t>(c->n), true, pv);
-        launch_depth_hist(c, k32[0]);  // digit histograms of the 32-bit depth keys
-        wait_mailbox(c, &c->mbox->seq_v, pv.seq);
-        V = c->mbox->V;
-        kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
-    } else {
-        compact_visible(c, 0, true);
-    }
-    stage_end(c, kStCompact);
     stage_begin(c, kStDepthSort);
     // (depth, index) order (renderer.cpp:86-89): stable LSD sort of the 32-bit
     // range-normalised depth key over rows in ascending index order, then runs
     // of equal keys sorted by the full FP64 depth. A run longer than 64 that is
     // out of order falls back to all 8 digit passes of the FP64 bits.
     c->depth_sorted = 0;
-    if (V > 1)
+    if (V > 1) {
+        launch_depth_hist(c, k32[0]);  // digit histograms of the 32-bit depth keys
         radix_sort_u32(c, k32, c->vrow, V, 0, static_cast<int>(kbits / 8), &c->counters->depth_hist[0][0], nullptr,
                        &c->depth_sorted);
+    }
     depth_tie_fixup(c, k32[c->depth_sorted], c->vrow[c->depth_sorted], c->depth_key, V, &c->counters->overflow);
     stage_end(c, kStDepthSort);
     stage_begin(c, kStPairs);
@@ -318,8 +303,81 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     stage_begin(c, kStRanges);
     launch_ranges(c, cam, V, P);
     stage_end(c, kStRanges);
+    c->last_binning = 1;
+    return P;
+}
+
+// K1-K5: projection, compaction, binning into tiles, per-tile depth order,
+// ranges. No stream synchronisation on the common path: the compaction and
+// the tile scan publish V and P to the host-mapped mailbox, and the host
+// polls for them while the kernel enqueued behind (the speculative pair
+// emission into the current capacity) keeps the GPU busy.
+void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
+    ensure_image_buffers(c, cam.W, cam.H);
+    const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
+    launch_pdl(c->stream, 1, 512, 0, zero_counters_kernel, c->counters, c->tile_cnt, ntiles);
+    BSG_LAUNCHED(c);
+    stage_begin(c, kStPreprocess);
+    launch_preprocess(c, cam, rc);  // + pairs per tile
+    stage_end(c, kStPreprocess);
+    stage_begin(c, kStCompact);
+    uint32_t V = 0, kbits = 16, P = 0;
+    if (c->n == 0) {
+        compact_visible(c, 0, true);
+        stage_end(c, kStCompact);
+        launch_ranges(c, cam, 0, 0);  // empty ranges + launch order
+        c->last_binning = 1;
+        c->last_counters.visible = 0;
+        c->last_counters.pairs = 0;
+        return;
+    }
+    Publish pv;
+    pv.val = &c->mbox->V;
+    pv.seq_word = &c->mbox->seq_v;
+    pv.seq = ++c->mbox_seq;
+    pv.extra_src = &c->counters->visible_pre;
+    pv.extra_dst = &c->mbox->visible_pre;
+    compact_visible(c, static_cast<uint32_t>(c->n), true, pv);
+    stage_end(c, kStCompact);
+    if (c->global_order) {
+        wait_mailbox(c, &c->mbox->seq_v, pv.seq);
+        V = c->mbox->V;
+        kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
+        P = bin_global(c, cam, V, kbits);
+    } else {
+        stage_begin(c, kStDepthSort);
+        uint32_t seq = ++c->mbox_seq;
+        launch_tile_scan(c, cam, seq);
+        stage_end(c, kStDepthSort);
+        stage_begin(c, kStPairs);
+        launch_emit_tiles(c, cam);  // speculative: into the current capacity
+        wait_mailbox(c, &c->mbox->seq_v, pv.seq);
+        V = c->mbox->V;
+        kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
+        wait_mailbox(c, &c->mbox->seq_p, seq);
+        P = c->mbox->P;
+        const uint32_t max_tile = c->mbox->max_tile;
+        stage_end(c, kStPairs);
+        if (max_tile > kTileSortCap) {
+            P = bin_global(c, cam, V, kbits);  // a tile too long for the shared-memory sort
+        } else {
+            if (P > c->pcap) {  // the emission ran out of capacity: grow, reset the cursors, emit again
+                ensure_pair_capacity(c, P);
+                launch_tile_scan(c, cam, ++c->mbox_seq);
+                launch_emit_tiles(c, cam);
+            }
+            stage_begin(c, kStTileSort);
+            if (P) launch_tile_sort(c, cam, max_tile);
+            stage_end(c, kStTileSort);
+            stage_begin(c, kStRanges);  // (ranges and the launch order came from the tile scan)
+            stage_end(c, kStRanges);
+            c->pairs_sorted = 0;
+            c->last_binning = 0;
+        }
+    }
     c->last_counters.visible = V;
     c->last_counters.pairs = P;
+    c->last_ntiles = ntiles;
 }
 
 }  // namespace
@@ -876,7 +934,14 @@ int bsg_project(bsg_ctx* h, const bsg_camera* cam, const bsg_render_config* cfg,
         if (cfg) rcfg = *cfg; else bsg_default_render_config(&rcfg);
         use_device(c);
         const DevCam dc = make_cam(*cam);
-        project_and_bin(c, dc, make_render(rcfg));
+        c->global_order = true;  // the depth order of the visible splats is an output here
+        try {
+            project_and_bin(c, dc, make_render(rcfg));
+        } catch (...) {
+            c->global_order = false;
+            throw;
+        }
+        c->global_order = false;
         const size_t n = c->n;
         const uint32_t V = c->last_counters.visible;
         std::vector<uint32_t> tiles(n);
@@ -920,8 +985,17 @@ int bsg_tile_pairs(bsg_ctx* h, uint32_t* out_tile, uint32_t* out_row, size_t cap
         if (!out_tile && !out_row) return;
         if (capacity < P) invalid("pair buffer too small");
         if (P == 0) return;
-        if (out_tile)
+        if (out_tile && c->last_binning == 1)
             BSG_CUDA(cudaMemcpyAsync(out_tile, c->pkey[c->pairs_sorted], P * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (out_tile && c->last_binning == 0) {
+            // per-tile binning keeps no tile keys: the ranges give them
+            const size_t nt = c->last_ntiles;
+            std::vector<uint2> rg(nt);
+            BSG_CUDA(cudaMemcpyAsync(rg.data(), c->ranges, nt * sizeof(uint2), cudaMemcpyDeviceToHost, c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            for (size_t t = 0; t < nt; ++t)
+                for (uint32_t q = rg[t].x; q < rg[t].y && q < P; ++q) out_tile[q] = static_cast<uint32_t>(t);
+        }
         if (out_row)
             BSG_CUDA(cudaMemcpyAsync(out_row, c->pval[c->pairs_sorted], P * 4, cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));

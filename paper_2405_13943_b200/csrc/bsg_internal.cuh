@@ -73,8 +73,13 @@ struct StepCounters {
 // sync, while the kernel enqueued behind them keeps the GPU busy.
 struct Mailbox {
     uint32_t seq_v, V, visible_pre, pad0;
-    uint32_t seq_p, P, overflow, pad1;
+    uint32_t seq_p, P, overflow, max_tile;  // max_tile: largest per-tile pair count (per-tile binning)
 };
+
+// Per-tile binning sorts a tile's pairs by (FP64 depth bits, row) in shared
+// memory; a view with a tile holding more pairs falls back to the global
+// depth sort + stable tile sort.
+constexpr uint32_t kTileSortCap = 4096;
 
 // Where a scan's final CTA publishes its total (all null: nowhere).
 struct Publish {
@@ -156,7 +161,12 @@ struct Ctx {
     int pairs_sorted = 0;
     uint2* ranges = nullptr;
     uint32_t* tile_order = nullptr;  // blend launch order: tiles by descending pair count
+    uint32_t* tile_cnt = nullptr;    // pairs per tile (counted by the preprocess)
+    uint32_t* tile_cur = nullptr;    // per-tile write cursors of the pair emission
     size_t ranges_cap = 0;
+    bool global_order = false;       // bsg_project: global depth sort path (exposes the depth order)
+    int last_binning = 0;            // 0: per-tile sort, 1: global sorts (what the pair buffers hold)
+    size_t last_ntiles = 0;
 
     // radix / scan scratch
     unsigned long long* scan_status = nullptr;   // decoupled look-back status words (epoch-tagged)
@@ -336,6 +346,12 @@ DevCam make_cam(const bsg_camera& c);
 DevRender make_render(const bsg_render_config& r);
 void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V);
+// Per-tile binning: tile ranges / cursors / launch order from the preprocess's
+// tile counts (P and the largest count to the mailbox under `seq`), the rows
+// placed into their tiles (pval[1]), each tile sorted by (depth, row) into pval[0].
+void launch_tile_scan(Ctx* c, const DevCam& cam, uint32_t seq);
+void launch_emit_tiles(Ctx* c, const DevCam& cam);
+void launch_tile_sort(Ctx* c, const DevCam& cam, uint32_t max_tile);
 // The f32 arrays of the GSPL checkpoint section ((11 + fd) n floats, section order) into out.
 void launch_gspl_floats(Ctx* c, float* out);
 void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P);

@@ -45,7 +45,8 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  double* __restrict__ g2d_wide,
                                                                  float4* __restrict__ pcache,
                                                                  StepCounters* __restrict__ counters,
-                                                                 StepScalars* __restrict__ scalars) {
+                                                                 StepScalars* __restrict__ scalars,
+                                                                 uint32_t* __restrict__ tile_cnt) {
     pdl_prologue();
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint32_t s_count;
@@ -234,6 +235,9 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                     make_float4(static_cast<float>(col[2]), __uint_as_float(r01), __uint_as_float(r23),
                                 __uint_as_float(wslot));
                 ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+                // pairs per tile for the per-tile binning
+                for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) atomicAdd(&tile_cnt[ty * cam.tiles_x + tx], 1u);
                 const unsigned long long zb = static_cast<unsigned long long>(__double_as_longlong(z));
                 depth_key[i] = zb;
                 zmin_inv = max(zmin_inv, ~zb);
@@ -304,7 +308,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
                                                       c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters,
-                                                      c->scalars);
+                                                      c->scalars, c->tile_cnt);
     BSG_LAUNCHED(c);
 }
 

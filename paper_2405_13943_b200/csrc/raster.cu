@@ -10,6 +10,8 @@
 // order. Blending is FP32 (exp through MUFU).
 #include "bsg_internal.cuh"
 
+#include <algorithm>
+
 namespace bsg {
 namespace {
 
@@ -82,6 +84,180 @@ __global__ __launch_bounds__(256) void ranges_kernel(const uint32_t* __restrict_
     const uint32_t k = pkey[i];
     if (i == 0 || pkey[i - 1] != k) ranges[k].x = i;
     if (i == P - 1 || pkey[i + 1] != k) ranges[k].y = i + 1;
+}
+
+// ---- per-tile binning (the default path) --------------------------------
+// The preprocess counts each visible splat into every tile its rect overlaps.
+// K4a scans the counts into tile ranges and emission cursors (one CTA), and
+// publishes P and the largest tile count; K4b places every visible splat's row
+// into each of its tiles at an atomically claimed slot (order inside a tile is
+// arbitrary); K5 sorts each tile's rows in shared memory by (FP64 depth bits,
+// row) -- exactly the reference's stable (depth, index) order restricted to
+// the tile (renderer.cpp:86-89) -- replacing the global depth sort, its tie
+// fix-up and the stable tile-key sort.
+
+// One CTA: exclusive scan of the tile counts -> ranges and cursors, the blend
+// launch order (descending count), and P / max count to the mailbox.
+__global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restrict__ cnt, uint32_t ntiles,
+                                                         uint2* __restrict__ ranges, uint32_t* __restrict__ cur,
+                                                         uint32_t* __restrict__ order, Mailbox* mb, uint32_t seq,
+                                                         uint32_t* __restrict__ pairs_dev) {
+    pdl_prologue();
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_bucket[1024];
+    __shared__ uint32_t s_max;
+    const uint32_t t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const uint32_t per = (ntiles + 1023) / 1024;  // consecutive tiles per thread
+    const uint32_t b0 = t * per, b1 = min(b0 + per, ntiles);
+    uint32_t sum = 0, mx = 0;
+    for (uint32_t i = b0; i < b1; ++i) {
+        const uint32_t v = cnt[i];
+        sum += v;
+        mx = max(mx, v);
+    }
+    s_bucket[t] = 0;
+    if (t == 0) s_max = 0;
+    // block exclusive scan of the per-thread sums
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (lane == 0) atomicMax(&s_max, mx);
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi;  // inclusive
+    }
+    __syncthreads();
+    uint32_t run = (warp ? s_warp[warp - 1] : 0u) + inc - sum;
+    for (uint32_t i = b0; i < b1; ++i) {
+        const uint32_t v = cnt[i];
+        ranges[i] = make_uint2(run, run + v);
+        cur[i] = run;
+        run += v;
+        atomicAdd(&s_bucket[1023u - min(v, 1023u)], 1u);
+    }
+    __syncthreads();
+    // launch order: counting sort of the tiles by descending count
+    {
+        const uint32_t v = s_bucket[t];
+        uint32_t bi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, bi, o);
+            if (lane >= o) bi += y;
+        }
+        __syncthreads();
+        if (lane == 31) s_warp[warp] = bi;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t w = s_warp[lane];
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            s_warp[lane] = wi - w;
+        }
+        __syncthreads();
+        s_bucket[t] = s_warp[warp] + bi - v;
+        __syncthreads();
+    }
+    for (uint32_t i = b0; i < b1; ++i) order[atomicAdd(&s_bucket[1023u - min(cnt[i], 1023u)], 1u)] = i;
+    if (t == 1023) {  // the last thread's running sum is P
+        *pairs_dev = run;
+        *reinterpret_cast<volatile uint32_t*>(&mb->P) = run;
+        *reinterpret_cast<volatile uint32_t*>(&mb->max_tile) = s_max;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&mb->seq_p) = seq;
+    }
+}
+
+// One thread per visible splat (grid-stride; V from the step counters): its
+// row into every tile it overlaps, at a slot claimed from the tile's cursor.
+__global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restrict__ vis_rows,
+                                                         const StepCounters* __restrict__ counters,
+                                                         const float4* __restrict__ rec, int tiles_x,
+                                                         uint32_t* __restrict__ cur, uint32_t* __restrict__ out_rows,
+                                                         uint32_t pcap) {
+    pdl_prologue();
+    const uint32_t V = counters->visible;
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < V; p += gridDim.x * blockDim.x) {
+        const uint32_t row = vis_rows[p];
+        int x0, x1, y0, y1;
+        unpack_rect(rec[3 * static_cast<size_t>(row) + 2], x0, x1, y0, y1);
+        for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+            for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
+                const uint32_t slot = atomicAdd(&cur[ty * tiles_x + tx], 1u);
+                if (slot < pcap) out_rows[slot] = row;
+            }
+    }
+}
+
+// One CTA per tile: the tile's rows sorted by (FP64 depth bits, row) with a
+// bitonic network in shared memory (size: the next power of two of the
+// tile's count, at most kTileSortCap; dynamic shared memory sized for the
+// view's largest tile).
+__global__ __launch_bounds__(512) void tile_sort_kernel(const uint2* __restrict__ ranges,
+                                                        const uint32_t* __restrict__ rows_in,
+                                                        const uint64_t* __restrict__ depth_key,
+                                                        uint32_t* __restrict__ rows_out) {
+    pdl_prologue();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint2 r = ranges[blockIdx.x];
+    const uint32_t n = r.y - r.x;
+    if (n == 0) return;
+    if (n == 1) {
+        if (threadIdx.x == 0) rows_out[r.x] = rows_in[r.x];
+        return;
+    }
+    uint32_t N = 2;
+    while (N < n) N <<= 1;
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint64_t) * N);
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        if (i < n) {
+            const uint32_t row = rows_in[r.x + i];
+            sk[i] = depth_key[row];
+            sv[i] = row;
+        } else {
+            sk[i] = ~0ull;  // padding sorts last
+            sv[i] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= N; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                // i-th compare-exchange pair of this stage: a has bit j clear
+                const uint32_t a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+                const uint32_t b = a | j;
+                const bool up = (a & k) == 0;
+                const uint64_t ka = sk[a], kb = sk[b];
+                const uint32_t va = sv[a], vb = sv[b];
+                const bool gt = ka > kb || (ka == kb && va > vb);
+                if (gt == up) {
+                    sk[a] = kb; sk[b] = ka;
+                    sv[a] = vb; sv[b] = va;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rows_out[r.x + i] = sv[i];
 }
 
 // Blend launch order: tiles sorted by descending pair count (longest
@@ -520,6 +696,35 @@ void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P) {
     launch_pdl(c->stream, (P + 255) / 256, 256, 0, ranges_kernel, c->pkey[c->pairs_sorted], P, c->ranges);
     BSG_LAUNCHED(c);
     launch_pdl(c->stream, 1, 1024, 0, tile_order_kernel, c->ranges, static_cast<uint32_t>(ntiles), c->tile_order);
+    BSG_LAUNCHED(c);
+}
+
+void launch_tile_scan(Ctx* c, const DevCam& cam, uint32_t seq) {
+    const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
+    launch_pdl(c->stream, 1, 1024, 0, tile_scan_kernel, c->tile_cnt, ntiles, c->ranges, c->tile_cur, c->tile_order,
+               c->mbox, seq, &c->counters->pairs);
+    BSG_LAUNCHED(c);
+}
+
+void launch_emit_tiles(Ctx* c, const DevCam& cam) {
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(static_cast<uint32_t>((c->n + 255) / 256), 148 * 8));
+    launch_pdl(c->stream, grid, 256, 0, emit_tiles_kernel, c->vis_rows, c->counters, c->rec, cam.tiles_x, c->tile_cur,
+               c->pval[1], static_cast<uint32_t>(c->pcap));
+    BSG_LAUNCHED(c);
+}
+
+void launch_tile_sort(Ctx* c, const DevCam& cam, uint32_t max_tile) {
+    const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
+    uint32_t N = 2;
+    while (N < max_tile) N <<= 1;
+    const size_t smem = N * (sizeof(uint64_t) + sizeof(uint32_t));
+    static bool attr_set[64] = {};
+    if (!attr_set[c->device]) {
+        BSG_CUDA(cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kTileSortCap * (sizeof(uint64_t) + sizeof(uint32_t)))));
+        attr_set[c->device] = true;
+    }
+    launch_pdl(c->stream, ntiles, 512, smem, tile_sort_kernel, c->ranges, c->pval[1], c->depth_key, c->pval[0]);
     BSG_LAUNCHED(c);
 }
 

@@ -46,13 +46,41 @@ def test_projection_integer_paths_bit_exact(name, cloud, cam):
 
 @pytest.mark.parametrize("name,cloud,cam", CASES, ids=[c[0] for c in CASES])
 def test_tile_keys_and_order_bit_exact(name, cloud, cam):
-    b = new_block(cloud)
-    b.project(dev_cam(cam))
-    tile, row = b.tile_pairs()
     want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
     ek, er = expected_pairs(want, cam.width, cam.height)
+    b = new_block(cloud)
+    # global path (bsg_project): depth sort + tie fix-up + stable tile sort
+    b.project(dev_cam(cam))
+    tile, row = b.tile_pairs()
     assert np.array_equal(tile.astype(np.int64), ek)
     assert np.array_equal(row.astype(np.int64), er)
+    # per-tile path (every render / training step): counts, atomic placement,
+    # shared-memory (depth, row) sort per tile
+    b.render(dev_cam(cam))
+    tile, row = b.tile_pairs()
+    assert np.array_equal(tile.astype(np.int64), ek)
+    assert np.array_equal(row.astype(np.int64), er)
+
+
+def test_per_tile_binning_falls_back_for_a_crowded_tile():
+    """More pairs in one tile than the shared-memory sort holds (kTileSortCap
+    = 4096): the step takes the global sort path; order and image still match."""
+    g = np.random.default_rng(11)
+    n = 6000
+    cam = axis_camera(50, 8, 16)  # one 16x16 tile, principal point at its centre
+    pos = np.column_stack([g.uniform(-0.4, 0.4, n), g.uniform(-0.4, 0.4, n), g.uniform(4.0, 6.0, n)])
+    q = g.normal(size=(n, 4))
+    cloud = HostCloud(np.arange(n, dtype=np.uint64), pos, q / np.linalg.norm(q, axis=1, keepdims=True),
+                      np.full((n, 3), -4.0), g.uniform(0, 1, (n, 3)), g.normal(size=n) - 3.0)
+    b = new_block(cloud)
+    rgb, T, cnt = b.render(dev_cam(cam))
+    want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
+    ek, er = expected_pairs(want, cam.width, cam.height)
+    assert len(ek) > 4096
+    tile, row = b.tile_pairs()
+    assert np.array_equal(row.astype(np.int64), er)
+    wrgb, wT, wn = orc.render(cloud.oracle(), cam, orc.RenderConfig())
+    assert np.abs(rgb - wrgb).max() <= 1e-3
 
 
 @pytest.mark.parametrize("name,cloud,cam", CASES, ids=[c[0] for c in CASES])
