@@ -210,14 +210,15 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
 // One CTA per tile: the tile's rows sorted by (FP64 depth bits, row) with a
 // bitonic network in shared memory (size: the next power of two of the
 // tile's count, at most kTileSortCap; dynamic shared memory sized for the
-// view's largest tile).
-__global__ __launch_bounds__(512) void tile_sort_kernel(const uint2* __restrict__ ranges,
+// view's largest tile). Tiles in the blend launch order (longest first).
+__global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict__ ranges,
+                                                        const uint32_t* __restrict__ order,
                                                         const uint32_t* __restrict__ rows_in,
                                                         const uint64_t* __restrict__ depth_key,
                                                         uint32_t* __restrict__ rows_out) {
     pdl_prologue();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const uint2 r = ranges[blockIdx.x];
+    const uint2 r = ranges[order[blockIdx.x]];  // longest tiles first
     const uint32_t n = r.y - r.x;
     if (n == 0) return;
     if (n == 1) {
@@ -241,6 +242,8 @@ __global__ __launch_bounds__(512) void tile_sort_kernel(const uint2* __restrict_
     __syncthreads();
     for (uint32_t k = 2; k <= N; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            // pairs with j <= 32 stay inside the 64 elements of one warp's
+            // 32 compare-exchanges: those stages only need a warp barrier
             for (uint32_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
                 // i-th compare-exchange pair of this stage: a has bit j clear
                 const uint32_t a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
@@ -254,9 +257,14 @@ __global__ __launch_bounds__(512) void tile_sort_kernel(const uint2* __restrict_
                     sv[a] = vb; sv[b] = va;
                 }
             }
-            __syncthreads();
+            const uint32_t jn = j > 1 ? j >> 1 : k;  // the next stage's distance
+            if (j >= 64 || jn >= 64)
+                __syncthreads();
+            else
+                __syncwarp();
         }
     }
+    __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rows_out[r.x + i] = sv[i];
 }
 
@@ -724,7 +732,10 @@ void launch_tile_sort(Ctx* c, const DevCam& cam, uint32_t max_tile) {
                                       static_cast<int>(kTileSortCap * (sizeof(uint64_t) + sizeof(uint32_t)))));
         attr_set[c->device] = true;
     }
-    launch_pdl(c->stream, ntiles, 512, smem, tile_sort_kernel, c->ranges, c->pval[1], c->depth_key, c->pval[0]);
+    // 128 threads: one compare-exchange per thread per stage for tiles up to
+    // 256 pairs (the common case), a few for the long ones, launched first
+    launch_pdl(c->stream, ntiles, 128, smem, tile_sort_kernel, c->ranges, c->tile_order, c->pval[1], c->depth_key,
+               c->pval[0]);
     BSG_LAUNCHED(c);
 }
 
