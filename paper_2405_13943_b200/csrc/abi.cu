@@ -339,11 +339,15 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     pv.extra_dst = &c->mbox->visible_pre;
     compact_visible(c, static_cast<uint32_t>(c->n), true, pv);
     stage_end(c, kStCompact);
-    if (c->global_order) {
+    // the previous view's largest tile picks the path up front, so a dense
+    // sequence of views does not pay the speculative per-tile emission
+    if (c->global_order || c->last_max_tile > kTileSortCap) {
+        launch_tile_scan(c, cam, ++c->mbox_seq);  // only for the largest-tile count (cheap)
         wait_mailbox(c, &c->mbox->seq_v, pv.seq);
         V = c->mbox->V;
         kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
-        P = bin_global(c, cam, V, kbits);
+        P = bin_global(c, cam, V, kbits);  // its P wait orders the tile scan's mailbox write before this read
+        c->last_max_tile = c->mbox->max_tile;
     } else {
         stage_begin(c, kStDepthSort);
         uint32_t seq = ++c->mbox_seq;
@@ -357,6 +361,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
         wait_mailbox(c, &c->mbox->seq_p, seq);
         P = c->mbox->P;
         const uint32_t max_tile = c->mbox->max_tile;
+        c->last_max_tile = max_tile;
         stage_end(c, kStPairs);
         if (max_tile > kTileSortCap) {
             P = bin_global(c, cam, V, kbits);  // a tile too long for the shared-memory sort
