@@ -175,10 +175,10 @@ def algorithmic_bytes(stage, n, V, P, HW, shared):
         # zeroed gradient record for visible rows
         "preprocess": 28 * n + (32 + 48 + 8 + 48) * V,
         "compact": 4 * n + 16 * V,
-        # per-tile binning (the default path; stage names kept from the global path):
-        "depth_sort": 0,                            # tile scan: a few KB of per-tile counts / ranges
-        "pairs": 4 * V + 16 * V + 4 * P,            # visible row + its rect read, one row written per pair
-        "tile_sort": 4 * P + 8 * P + 4 * P,         # rows read, their FP64 depth gathered, sorted rows written
+        # per-tile binning (the path taken at this config):
+        "bin_scan": 0,                              # tile scan: a few KB of per-tile counts / ranges
+        "bin_emit": 4 * V + 16 * V + 4 * P,         # visible row + its rect read, one row written per pair
+        "bin_sort": 4 * P + 8 * P + 4 * P,          # rows read, their FP64 depth gathered, sorted rows written
         "blend_fwd": 52 * P + 24 * HW,              # pair row + 48 B record per pair; rgb, T, n, last per pixel
         "loss_ssim": 36 * HW,                       # rendered + GT read, dL/dC written (fused minimum)
         "blend_bwd": 52 * P + 20 * HW + 48 * V,     # records; T, last, dL/dC per pixel; one gradient record per splat

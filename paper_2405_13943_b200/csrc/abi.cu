@@ -1563,7 +1563,9 @@ int bsg_enable_stage_timing(bsg_ctx* h, int enable) {
 int bsg_stage_count(void) { return kStCount; }
 
 const char* bsg_stage_name(int i) {
-    static const char* names[kStCount] = {"preprocess", "compact", "depth_sort", "pairs", "tile_sort",
+    // bin_scan / bin_emit / bin_sort: tile scan, pair emission, per-tile sort
+    // (per-tile binning) or depth sort, pair emission, tile-key sort (global)
+    static const char* names[kStCount] = {"preprocess", "compact", "bin_scan", "bin_emit", "bin_sort",
                                           "ranges", "blend_fwd", "loss_ssim", "blend_bwd", "fold", "adam"};
     return (i >= 0 && i < kStCount) ? names[i] : "";
 }
