@@ -165,6 +165,11 @@ int bsg_train_step_host(bsg_ctx* ctx, const bsg_camera* cam, const float* gt_rgb
  * n at the end of the call). */
 int bsg_train_steps_host(bsg_ctx* ctx, size_t n, const bsg_camera* cams, const float* const* gts_host,
                          double* losses);
+/* As bsg_train_steps_host with 8-bit RGB images (HxWx3 bytes: the PPM data
+ * the reference loads, image.cpp:60-79), widened on the device as
+ * dequantize does (byte / 255, image.cpp:21-27): a quarter of the upload. */
+int bsg_train_steps_host_u8(bsg_ctx* ctx, size_t n, const bsg_camera* cams, const uint8_t* const* gts_host,
+                            double* losses);
 uint64_t bsg_iteration(const bsg_ctx* ctx);
 /* Optimizer moments, [D][n] component-major FP64 (D = 11 + fd), for parity. */
 int bsg_download_moments(bsg_ctx* ctx, double* m, double* v);

@@ -131,6 +131,7 @@ SYMBOLS = [
     ("bsg_train_steps", ctypes.c_int, [_P, _SZ, _U32P, _DP]),
     ("bsg_train_step_host", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _FP, _DP]),
     ("bsg_train_steps_host", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_FP), _DP]),
+    ("bsg_train_steps_host_u8", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_U8P), _DP]),
     ("bsg_iteration", ctypes.c_uint64, [_P]),
     ("bsg_download_moments", ctypes.c_int, [_P, _DP, _DP]),
     ("bsg_take_removed_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
@@ -412,6 +413,16 @@ class Block:
         ptrs = (_FP * n)(*[_ptr(g, ctypes.c_float) for g in keep])
         out = np.zeros(n)
         _check(_lib.bsg_train_steps_host(self.h, n, cam_arr, ptrs, _ptr(out, ctypes.c_double)))
+        return out
+
+    def train_steps_host_u8(self, cams, gts_u8):
+        """n steps on 8-bit host images (uint8 HxWx3, pinned for overlap); returns the n losses."""
+        n = len(cams)
+        cam_arr = (bsg_camera * n)(*cams)
+        keep = [np.ascontiguousarray(g, dtype=np.uint8) for g in gts_u8]
+        ptrs = (_U8P * n)(*[_ptr(g, ctypes.c_uint8) for g in keep])
+        out = np.zeros(n)
+        _check(_lib.bsg_train_steps_host_u8(self.h, n, cam_arr, ptrs, _ptr(out, ctypes.c_double)))
         return out
 
     def iteration(self):

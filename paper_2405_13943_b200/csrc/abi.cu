@@ -81,7 +81,7 @@ void free_all(Ctx* c) {
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->tile_cnt, c->tile_cur, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
-                    c->ssim_f, c->gt_stage, c->gt_stage_b, c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
+                    c->ssim_f, c->gt_stage, c->gt_stage_b, c->gt_u8[0], c->gt_u8[1], c->sh_rows, c->sh_slots, c->sh_first, c->z, c->u, c->zprev, c->zslot,
                     c->in_zprev, c->slot_owners, c->pack, c->qref, c->slot_reset, c->round_scalars};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -585,6 +585,45 @@ void round_pack_duals(Ctx* c);
 void round_dual_linf(Ctx* c);
 void round_pack_minmax(Ctx* c);
 void round_spread(Ctx* c);
+
+// image.cpp:21-27 (dequantize): byte / 255 in FP64, then the device's FP32.
+__global__ __launch_bounds__(256) void dequantize_kernel(const uint8_t* __restrict__ in, float* __restrict__ out,
+                                                         size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<float>(static_cast<double>(in[i]) / 255.0);
+}
+
+// n steps on host images, each uploaded on the copy stream into one of two
+// device buffers while the previous step computes. `upload(k, buf)` enqueues
+// step k's image into buf on the copy stream.
+template <typename Upload>
+void train_steps_from_host(Ctx* c, size_t n, const bsg_camera* cams, double* losses, Upload&& upload) {
+    ensure_views_buffers(c, std::max<size_t>(n, 1));
+    for (size_t k = 0; k < n; ++k) {
+        const bsg_camera& cam = cams[k];
+        ensure_image_buffers(c, static_cast<int>(cam.width), static_cast<int>(cam.height));
+        const int b = static_cast<int>(k & 1);
+        float* buf = b ? c->gt_stage_b : c->gt_stage;
+        cudaEvent_t ready = b ? c->gt_ready_b : c->gt_ready;
+        // step k-2 read this buffer: its loss must be done before the overwrite
+        if (k >= 2) BSG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->gt_free[b], 0));
+        upload(k, b, buf);
+        BSG_CUDA(cudaEventRecord(ready, c->copy_stream));
+        train_one(c, cam, buf, c->losses_dev + 3 * k, ready);
+        BSG_CUDA(cudaEventRecord(c->gt_free[b], c->stream));
+        maybe_densify(c);
+    }
+    if (n) {
+        std::vector<double> l(3 * n);
+        BSG_CUDA(cudaMemcpyAsync(l.data(), c->losses_dev, l.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        if (losses)
+            for (size_t k = 0; k < n; ++k) losses[k] = l[3 * k];
+    }
+    collect_stage_times(c);
+}
 
 }  // namespace bsg
 
@@ -1094,31 +1133,40 @@ int bsg_train_steps_host(bsg_ctx* h, size_t n, const bsg_camera* cams, const flo
             if (!gts_host[k]) invalid("null ground truth");
         }
         use_device(c);
-        ensure_views_buffers(c, std::max<size_t>(n, 1));
+        train_steps_from_host(c, n, cams, losses, [&](size_t k, int, float* buf) {
+            const size_t px = static_cast<size_t>(cams[k].width) * cams[k].height;
+            BSG_CUDA(cudaMemcpyAsync(buf, gts_host[k], 3 * px * sizeof(float), cudaMemcpyHostToDevice,
+                                     c->copy_stream));
+        });
+    });
+}
+
+int bsg_train_steps_host_u8(bsg_ctx* h, size_t n, const bsg_camera* cams, const uint8_t* const* gts_host,
+                            double* losses) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!c->trainer_ready) throw Error{BSG_ERR_STATE, "train step before bsg_trainer_init"};
+        if (n && (!cams || !gts_host)) invalid("null views");
+        size_t need = 0;
         for (size_t k = 0; k < n; ++k) {
-            const bsg_camera& cam = cams[k];
-            ensure_image_buffers(c, static_cast<int>(cam.width), static_cast<int>(cam.height));
-            const int b = static_cast<int>(k & 1);
-            float* buf = b ? c->gt_stage_b : c->gt_stage;
-            cudaEvent_t ready = b ? c->gt_ready_b : c->gt_ready;
-            // step k-2 read this buffer: its loss must be done before the overwrite
-            if (k >= 2) BSG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->gt_free[b], 0));
-            const size_t px = static_cast<size_t>(cam.width) * cam.height;
-            BSG_CUDA(cudaMemcpyAsync(buf, gts_host[k], 3 * px * sizeof(float), cudaMemcpyHostToDevice, c->copy_stream));
-            BSG_CUDA(cudaEventRecord(ready, c->copy_stream));
-            train_one(c, cam, buf, c->losses_dev + 3 * k, ready);
-            BSG_CUDA(cudaEventRecord(c->gt_free[b], c->stream));
-            maybe_densify(c);
+            check_camera(&cams[k]);
+            if (!gts_host[k]) invalid("null ground truth");
+            need = std::max(need, 3 * static_cast<size_t>(cams[k].width) * cams[k].height);
         }
-        if (n) {
-            std::vector<double> l(3 * n);
-            BSG_CUDA(cudaMemcpyAsync(l.data(), c->losses_dev, l.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                                     c->stream));
-            BSG_CUDA(cudaStreamSynchronize(c->stream));
-            if (losses)
-                for (size_t k = 0; k < n; ++k) losses[k] = l[3 * k];
+        use_device(c);
+        if (need > c->gt_u8_cap) {
+            for (auto& p : c->gt_u8) dev_alloc(&p, need);
+            c->gt_u8_cap = need;
         }
-        collect_stage_times(c);
+        train_steps_from_host(c, n, cams, losses, [&](size_t k, int b, float* buf) {
+            const size_t bytes = 3 * static_cast<size_t>(cams[k].width) * cams[k].height;
+            BSG_CUDA(cudaMemcpyAsync(c->gt_u8[b], gts_host[k], bytes, cudaMemcpyHostToDevice, c->copy_stream));
+            // widened on the copy stream too, overlapping the compute stream
+            const unsigned grid = static_cast<unsigned>(std::min<size_t>((bytes + 255) / 256, 148 * 4));
+            dequantize_kernel<<<grid, 256, 0, c->copy_stream>>>(c->gt_u8[b], buf, bytes);
+            BSG_LAUNCHED(c);
+        });
     });
 }
 

@@ -198,6 +198,8 @@ struct Ctx {
     float* ssim_f = nullptr;   // 9 planes of the valid window grid
     float* gt_stage = nullptr; // host ground truth staging (e2e path)
     float* gt_stage_b = nullptr;  // second staging buffer (bsg_train_steps_host)
+    uint8_t* gt_u8[2] = {nullptr, nullptr};  // 8-bit host images in flight (bsg_train_steps_host_u8)
+    size_t gt_u8_cap = 0;
 
     // resident training views
     std::vector<bsg_camera> view_cams;

@@ -423,3 +423,23 @@ def test_train_steps_host_matches_resident_views():
     err = np.abs(gb - ga)
     assert np.mean(err <= 1e-6 + 1e-5 * np.abs(ga)) >= 0.97
     assert err.max() <= 2 * 5e-2 * len(seq)
+
+
+def test_train_steps_host_u8_matches_dequantized_float_images():
+    """8-bit host images (the PPM bytes the reference loads, image.cpp:60-79)
+    train exactly like their FP32 dequantization (byte / 255, image.cpp:21-27)."""
+    s, init = toy_scene(seed=6)
+    seq = orc.view_sequence(1, 0, len(s.views), 7)
+    ims = s.images()
+    q = [np.round(np.clip(ims[v], 0.0, 1.0) * 255.0).astype(np.uint8) for v in seq]  # quantize, image.cpp:12-19
+    cams = [dev_cam(s.views[v]) for v in seq]
+    a = device_trainer(init, s)
+    la = a.train_steps_host(cams, [(b.astype(np.float64) / 255.0).astype(np.float32) for b in q])
+    b8 = device_trainer(init, s)
+    lb = b8.train_steps_host_u8(cams, q)
+    np.testing.assert_allclose(lb, la, rtol=1e-6)
+    ca, cb = a.download_cloud(), b8.download_cloud()
+    ga = np.concatenate([ca["pos"], ca["rot"], ca["ls"], ca["feat"], ca["op"][:, None]], 1)
+    gb = np.concatenate([cb["pos"], cb["rot"], cb["ls"], cb["feat"], cb["op"][:, None]], 1)
+    err = np.abs(gb - ga)
+    assert np.mean(err <= 1e-6 + 1e-5 * np.abs(ga)) >= 0.97
