@@ -367,7 +367,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   unsigned long long* __restrict__ evals,
                                                                   const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
-    __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
+    __shared__ float4 s_rec[3 * kBatch];  // entry j's splat record at 3j .. 3j+2 (one base address per entry)
     __shared__ uint16_t s_hm[kBlendThreads / 32][kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
     const int tile = static_cast<int>(tile_order[blockIdx.x]);
@@ -396,9 +396,9 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                 int x0, x1, y0, y1;
                 unpack_rect(c, x0, x1, y0, y1);
                 const int t = threadIdx.x + h * kBlendThreads;
-                s_a[t] = rec[r];
-                s_b[t] = rec[r + 1];
-                s_c[t] = c;
+                s_rec[3 * t] = rec[r];
+                s_rec[3 * t + 1] = rec[r + 1];
+                s_rec[3 * t + 2] = c;
 #pragma unroll
                 for (int w = 0; w < kBlendThreads / 32; ++w)
                     s_hm[w][t] = region_hits(x0, x1, y0, y1, tx0 + (w & 1) * 8, ty0 + (w >> 1) * 8);
@@ -423,7 +423,7 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
             const bool hit0 = !done0 && (cb & (hm >> hr) & 1u);
             const bool hit1 = !done1 && (cb & (hm >> (hr + 4)) & 1u);
             if (!(hit0 || hit1)) continue;
-            const float4 a = s_a[j], b = s_b[j], c = s_c[j];
+            const float4 a = s_rec[3 * j], b = s_rec[3 * j + 1], c = s_rec[3 * j + 2];
             const float dx = fx - a.x;
             const uint32_t pos = start - range.x + static_cast<uint32_t>(j) + 1;
             if (hit0) {
@@ -572,7 +572,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   double* __restrict__ g2d_wide,
                                                                   const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
-    __shared__ float4 s_a[kBatch], s_b[kBatch], s_c[kBatch];
+    __shared__ float4 s_rec[3 * kBatch];  // entry j's splat record at 3j .. 3j+2 (one base address per entry)
     __shared__ uint32_t s_row[kBatch];
     __shared__ uint8_t s_m[kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
@@ -624,9 +624,9 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                 const float4 c = rec[r + 2];
                 int x0, x1, y0, y1;
                 unpack_rect(c, x0, x1, y0, y1);
-                s_a[t] = rec[r];
-                s_b[t] = rec[r + 1];
-                s_c[t] = c;
+                s_rec[3 * t] = rec[r];
+                s_rec[3 * t + 1] = rec[r + 1];
+                s_rec[3 * t + 2] = c;
                 s_row[t] = row;
                 s_m[t] = static_cast<uint8_t>(subtile_mask(x0, x1, y0, y1, tx0, ty0));
             }
@@ -646,7 +646,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
         for (int k = nl - 1; k >= 0; --k) {
             const int sj = s_list[warp][k];
             const int j = start + sj;
-            const float4 c = s_c[sj];
+            const float4 c = s_rec[3 * sj + 2];
             int x0, x1, y0, y1;
             unpack_rect(c, x0, x1, y0, y1);
             const bool inx = px >= x0 && px <= x1;
@@ -655,7 +655,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             const unsigned mask = __ballot_sync(0xffffffffu, hit0 || hit1);
             if (mask == 0) continue;
             float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            const float4 a = s_a[sj], b = s_b[sj];
+            const float4 a = s_rec[3 * sj], b = s_rec[3 * sj + 1];
             const float dx = fx - a.x;
             if (hit0) bwd_step(P0, dx, fy0 - a.y, a, b, c, aclamp, acc);
             if (hit1) bwd_step(P1, dx, fy1 - a.y, a, b, c, aclamp, acc);
