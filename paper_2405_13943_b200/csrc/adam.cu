@@ -37,8 +37,9 @@ struct Grad2D {
 __device__ __forceinline__ Grad2D load_g2d(uint32_t i, const float4* __restrict__ rec,
                                            const float4* __restrict__ g2d, const double* __restrict__ g2d_wide) {
     Grad2D g;
-    const uint32_t wslot = __float_as_uint(rec[3 * static_cast<size_t>(i) + 2].w);
-    if (wslot != kNoWide) {
+    const uint32_t target = __float_as_uint(rec[3 * static_cast<size_t>(i) + 2].w);
+    if (target & kWideBit) {
+        const uint32_t wslot = target & ~kWideBit;
 #pragma unroll
         for (int k = 0; k < 9; ++k) g.v[k] = g2d_wide[9 * static_cast<size_t>(wslot) + k];
     } else {

@@ -23,6 +23,9 @@ constexpr int kTile = 16;             // 16x16 pixel tiles, one thread per pixel
 constexpr uint32_t kWideArea = 4096;
 constexpr uint32_t kWideCap = 65536;  // wide splats per step with an FP64 slot (others stay FP32)
 constexpr uint32_t kNoWide = 0xffffffffu;
+// rec[3i+2].w: the splat's gradient target -- its row i, or kWideBit | slot
+// for a wide footprint's FP64 slot (the backward blend adds to it directly).
+constexpr uint32_t kWideBit = 0x80000000u;
 constexpr int kTileThreads = kTile * kTile;
 constexpr int kMaxFd = 12;            // SH degree 1 (cloud.hpp:16-17)
 constexpr int kMaxD = 11 + kMaxFd;    // pos3 rot4 ls3 feat fd op1
@@ -139,7 +142,7 @@ struct Ctx {
     uint64_t* depth_key = nullptr; // FP64 depth bits
     uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
     float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
-    double* g2d_wide = nullptr;    // [kWideCap][9] FP64 gradients of wide splats (slot in rec[3i+2].w)
+    double* g2d_wide = nullptr;    // [kWideCap][9] FP64 gradients of wide splats (kWideBit | slot in rec[3i+2].w)
     float4* pcache = nullptr;      // kParamVec float4 per row: the parameters of the rows the preprocess
                                    // found visible, row-contiguous for the fold's gather
     float* gbuf = nullptr;         // parameter gradient of the visible rows, [D][cap] by visible position

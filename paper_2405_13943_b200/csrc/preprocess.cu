@@ -221,12 +221,12 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                     make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(m00), static_cast<float>(m01));
                 rec[3 * static_cast<size_t>(i) + 1] =
                     make_float4(static_cast<float>(m11), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
-                // wide footprint: FP64 gradient slot (see kWideArea)
-                uint32_t wslot = kNoWide;
+                // gradient target: the row, or a wide footprint's FP64 slot (see kWideArea)
+                uint32_t wslot = i;
                 if (static_cast<uint32_t>(x1 - x0 + 1) * static_cast<uint32_t>(y1 - y0 + 1) >= kWideArea) {
                     const uint32_t w = atomicAdd(&counters->wide, 1u);
                     if (w < kWideCap) {
-                        wslot = w;
+                        wslot = kWideBit | w;
 #pragma unroll
                         for (int k = 0; k < 9; ++k) g2d_wide[9 * static_cast<size_t>(w) + k] = 0.0;
                     }

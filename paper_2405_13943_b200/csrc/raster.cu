@@ -573,7 +573,6 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
     __shared__ float4 s_rec[3 * kBatch];  // entry j's splat record at 3j .. 3j+2 (one base address per entry)
-    __shared__ uint32_t s_row[kBatch];
     __shared__ uint8_t s_m[kBatch];
     __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
     __shared__ uint32_t s_max;
@@ -627,7 +626,6 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                 s_rec[3 * t] = rec[r];
                 s_rec[3 * t + 1] = rec[r + 1];
                 s_rec[3 * t + 2] = c;
-                s_row[t] = row;
                 s_m[t] = static_cast<uint8_t>(subtile_mask(x0, x1, y0, y1, tx0, ty0));
             }
         }
@@ -659,9 +657,10 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             const float dx = fx - a.x;
             if (hit0) bwd_step(P0, dx, fy0 - a.y, a, b, c, aclamp, acc);
             if (hit1) bwd_step(P1, dx, fy1 - a.y, a, b, c, aclamp, acc);
-            const uint32_t wslot = __float_as_uint(c.w);  // FP64 slot of a wide splat (kWideArea)
-            float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(s_row[sj]));
-            if (__popc(mask) <= 2 && wslot == kNoWide) {
+            const uint32_t target = __float_as_uint(c.w);  // row, or kWideBit | FP64 slot (kWideArea)
+            const bool wide = target & kWideBit;
+            float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(target & ~kWideBit));
+            if (__popc(mask) <= 2 && !wide) {
                 if (hit0 || hit1) {
                     atomicAdd(reinterpret_cast<float4*>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
                     atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
@@ -671,10 +670,10 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                 const float r = warp_reduce9(acc, lane);
                 const int idx = reduced9_index(lane);
                 if ((lane & 1) == 0 && idx < 9) {
-                    if (wslot == kNoWide)
+                    if (!wide)
                         atomicAdd(dst + idx, r);
                     else
-                        atomicAdd(g2d_wide + 9 * static_cast<size_t>(wslot) + idx, static_cast<double>(r));
+                        atomicAdd(g2d_wide + 9 * static_cast<size_t>(target & ~kWideBit) + idx, static_cast<double>(r));
                 }
             }
         }
