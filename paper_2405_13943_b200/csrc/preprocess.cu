@@ -49,6 +49,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  uint32_t* __restrict__ tile_cnt) {
     pdl_prologue();
     __shared__ uint32_t s_rows[kPreChunk];
+    __shared__ float s_pl[6][kPreChunk];  // a candidate's position + log-scale from phase 1 (not re-gathered)
     __shared__ uint32_t s_count;
     __shared__ unsigned long long s_zmin_inv, s_zmax;
     __shared__ uint32_t s_visible;
@@ -107,7 +108,13 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                 cand = false;
         }
         if (cand) {
-            s_rows[atomicAdd(&s_count, 1u)] = i;
+            const uint32_t q = atomicAdd(&s_count, 1u);
+            s_rows[q] = i;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                s_pl[a][q] = pp[k][a];
+                s_pl[3 + a][q] = ll[k][a];
+            }
         } else {
             tiles[i] = 0;
         }
@@ -121,7 +128,14 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
         // every parameter of the row up front: one dependent DRAM round trip
         float prm[kMaxD];
 #pragma unroll
-        for (int k = 0; k < 11 + 3; ++k) prm[k] = x[k * cap + i];
+        for (int k = 0; k < 11 + 3; ++k) {
+            if (k >= kPos && k < kPos + 3)
+                prm[k] = s_pl[k - kPos][q];
+            else if (k >= kLs && k < kLs + 3)
+                prm[k] = s_pl[3 + k - kLs][q];
+            else
+                prm[k] = x[k * cap + i];
+        }
         if (fd >= 12)
 #pragma unroll
             for (int k = 14; k < 11 + kMaxFd; ++k) prm[k] = x[k * cap + i];
