@@ -227,16 +227,17 @@ __global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict_
     }
     uint32_t N = 2;
     while (N < n) N <<= 1;
+    // one 64-bit word per pair: the upper 32 bits of the FP64 depth (its sign,
+    // exponent and 20 mantissa bits: order-preserving for positive depths) and
+    // the row, so a compare-exchange moves one word; pairs whose upper depth
+    // bits tie are put in (full depth, row) order afterwards
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-    uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint64_t) * N);
     for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
         if (i < n) {
             const uint32_t row = rows_in[r.x + i];
-            sk[i] = depth_key[row];
-            sv[i] = row;
+            sk[i] = (depth_key[row] & 0xffffffff00000000ull) | row;
         } else {
             sk[i] = ~0ull;  // padding sorts last
-            sv[i] = 0xffffffffu;
         }
     }
     __syncthreads();
@@ -250,11 +251,9 @@ __global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict_
                 const uint32_t b = a | j;
                 const bool up = (a & k) == 0;
                 const uint64_t ka = sk[a], kb = sk[b];
-                const uint32_t va = sv[a], vb = sv[b];
-                const bool gt = ka > kb || (ka == kb && va > vb);
-                if (gt == up) {
-                    sk[a] = kb; sk[b] = ka;
-                    sv[a] = vb; sv[b] = va;
+                if ((ka > kb) == up) {
+                    sk[a] = kb;
+                    sk[b] = ka;
                 }
             }
             const uint32_t jn = j > 1 ? j >> 1 : k;  // the next stage's distance
@@ -265,7 +264,27 @@ __global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict_
         }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rows_out[r.x + i] = sv[i];
+    // runs of equal upper depth bits (depths within ~1e-6 relative): odd-even
+    // transposition by (full FP64 depth, row) until a round swaps nothing
+    for (;;) {
+        bool swapped = false;
+        for (uint32_t parity = 0; parity < 2; ++parity) {
+            for (uint32_t i = 2 * threadIdx.x + parity; i + 1 < n; i += 2 * blockDim.x) {
+                const uint64_t ka = sk[i], kb = sk[i + 1];
+                if ((ka >> 32) != (kb >> 32)) continue;
+                const uint32_t ra = static_cast<uint32_t>(ka), rb = static_cast<uint32_t>(kb);
+                const uint64_t da = depth_key[ra], db = depth_key[rb];
+                if (da > db || (da == db && ra > rb)) {
+                    sk[i] = kb;
+                    sk[i + 1] = ka;
+                    swapped = true;
+                }
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(swapped)) break;
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rows_out[r.x + i] = static_cast<uint32_t>(sk[i]);
 }
 
 // Blend launch order: tiles sorted by descending pair count (longest
@@ -724,7 +743,7 @@ void launch_tile_sort(Ctx* c, const DevCam& cam, uint32_t max_tile) {
     const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
     uint32_t N = 2;
     while (N < max_tile) N <<= 1;
-    const size_t smem = N * (sizeof(uint64_t) + sizeof(uint32_t));
+    const size_t smem = N * sizeof(uint64_t);
     static bool attr_set[64] = {};
     if (!attr_set[c->device]) {
         BSG_CUDA(cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
