@@ -64,7 +64,7 @@ def test_tile_keys_and_order_bit_exact(name, cloud, cam):
 
 def test_per_tile_binning_falls_back_for_a_crowded_tile():
     """More pairs in one tile than the shared-memory sort takes (kTileSortCap
-    = 1024): the first render switches to the global sort path after the tile
+    = 2048): the first render switches to the global sort path after the tile
     scan, the next one takes it up front; order and image match both times."""
     g = np.random.default_rng(11)
     n = 6000
