@@ -131,14 +131,18 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
         sum += x;
     }
     if (MODE != 0) {
-        // 1 bit per row: this thread's 8 rows form one byte, 4 lanes one word
-        uint32_t byte = 0;
+        // 1 bit per row: this thread's kScanItems rows are kScanItems bits of a
+        // 32-row word, kLanesPerWord consecutive lanes fill one word
+        static_assert(32 % kScanItems == 0, "rows per thread must divide a mask word");
+        constexpr int kLanesPerWord = 32 / kScanItems;
+        uint32_t bits = 0;
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k) byte |= v[k] << k;
-        const uint32_t b1 = __shfl_down_sync(0xffffffffu, byte, 1), b2 = __shfl_down_sync(0xffffffffu, byte, 2),
-                       b3 = __shfl_down_sync(0xffffffffu, byte, 3);
+        for (int k = 0; k < kScanItems; ++k) bits |= v[k] << k;
+        uint32_t wbits = bits;
+#pragma unroll
+        for (int l = 1; l < kLanesPerWord; ++l) wbits |= __shfl_down_sync(0xffffffffu, bits, l) << (kScanItems * l);
         const uint64_t word = base / 32;
-        if ((threadIdx.x & 3) == 0 && word < mask_words) mask_out[word] = byte | (b1 << 8) | (b2 << 16) | (b3 << 24);
+        if ((threadIdx.x % kLanesPerWord) == 0 && word < mask_words) mask_out[word] = wbits;
     }
     const uint32_t tprefix = block_exclusive(sum, s_warp, &s_total);
     if (threadIdx.x < 32) {
@@ -170,7 +174,7 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
     }
     uint32_t run = s_prefix + tprefix;
     const int lane = threadIdx.x & 31;
-    if (MODE != 0 && (threadIdx.x & 3) == 0 && base / 32 < mask_words)
+    if (MODE != 0 && (threadIdx.x % (32 / kScanItems)) == 0 && base / 32 < mask_words)
         prefix_out[base / 32] = run;  // visible rows before this 32-row word
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
