@@ -499,12 +499,12 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     const uint32_t n = static_cast<uint32_t>(c->n);
     const int scalar_groups = c->D - 4;  // every component but the quaternion
     const dim3 g1(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(scalar_groups));
-    launch_pdl(c->stream, g1, 256, 0, adam_kernel<1>, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf,
+    launch_pdl(PdlAlways{}, c->stream, g1, 256, 0, adam_kernel<1>, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf,
                                               c->sh_mask,
                                               c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
                                               &c->scalars->penalty);
     BSG_LAUNCHED(c);
-    launch_pdl(c->stream, static_cast<uint32_t>((c->n + 255) / 256), 256, 0, adam_rot_kernel, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u,
+    launch_pdl(PdlAlways{}, c->stream, static_cast<uint32_t>((c->n + 255) / 256), 256, 0, adam_rot_kernel, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u,
         c->n_shared,
         c->rho_dev, st, &c->scalars->penalty);
     BSG_LAUNCHED(c);
