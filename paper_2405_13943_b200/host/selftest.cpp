@@ -2,6 +2,7 @@
 // mirroring a few of the reference's own unit tests (test_renderer.cpp,
 // test_trainer.cpp) so that a reference call site is shown to compile and run
 // unchanged against the device implementation. Exit code = failures.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -210,6 +211,51 @@ int main() {
         CHECK(t.shared_ids() == std::vector<uint64_t>{1});
         CHECK(t.anchor().ids == std::vector<uint64_t>{1});
         CHECK(t.duals().ids == std::vector<uint64_t>{1});
+    }
+    {  // scene container (test_image_scene.cpp:127-250): round trip, narrowing, error codes
+        SceneDataset d;
+        CameraView v = look_at({0, 2, -5}, {0, 0, 0}, {0, 1, 0}, 40, 40, 16, 12, 32, 24);
+        v.view_id = 7;
+        v.image_path = "gt/view_00007.ppm";
+        d.views.push_back(v);
+        d.points.push_back(ScenePoint{{0.5f, -1.0f, 2.0f}, {1, 2, 3}});
+        d.has_checkpoint = true;
+        d.checkpoint = spread_cloud(3, -1.5);
+        d.checkpoint.positions[0] = 0.1;  // not representable in f32
+        const std::vector<uint8_t> bytes = encode_scene(d);
+        const SceneDataset back = decode_scene(bytes.data(), bytes.size());
+        CHECK(back.views.size() == 1 && back.views[0].view_id == 7 && back.views[0].image_path == v.image_path);
+        CHECK(back.views[0].fx == v.fx && back.views[0].translation == v.translation);
+        CHECK(back.points.size() == 1 && back.points[0].rgb[2] == 3);
+        CHECK(back.has_checkpoint && back.checkpoint.ids == d.checkpoint.ids);
+        CHECK(back.checkpoint.positions == narrow_to_f32(d.checkpoint).positions);
+        CHECK(encode_scene(back) == bytes);  // narrowing is idempotent
+        auto code_of = [](std::vector<uint8_t> b) {
+            try {
+                decode_scene(b.data(), b.size());
+            } catch (const FormatError& e) {
+                return static_cast<int>(e.code());
+            }
+            return -1;
+        };
+        std::vector<uint8_t> bad = bytes;
+        bad[0] = 'X';
+        CHECK(code_of(bad) == static_cast<int>(FormatErrorCode::BadMagic));
+        bad = bytes;
+        bad.resize(bad.size() - 3);
+        CHECK(code_of(bad) == static_cast<int>(FormatErrorCode::TruncatedSection));
+        bad = bytes;
+        bad.push_back(0);
+        CHECK(code_of(bad) == static_cast<int>(FormatErrorCode::TruncatedBuffer));
+        // the device encoder writes the same GSPL section as the host codec
+        bsg_ctx* ctx = nullptr;
+        CHECK(bsg_create(0, 3, &ctx) == BSG_OK);
+        const GaussianCloud& c = d.checkpoint;
+        CHECK(bsg_upload_cloud(ctx, c.size(), c.ids.data(), c.positions.data(), c.rotations.data(),
+                               c.log_scales.data(), c.features.data(), c.opacity_logits.data()) == BSG_OK);
+        const std::vector<uint8_t> dev = encode_gspl_device(ctx);
+        CHECK(dev.size() > 12 && std::equal(dev.begin(), dev.end(), bytes.end() - static_cast<long>(dev.size())));
+        bsg_destroy(ctx);
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures;
