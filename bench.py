@@ -419,6 +419,8 @@ def run_ours(args, rank, world, local_rank):
                    "shared_ids": info["shared_ids"], "l2": "inputs > L2 (Adam state 2M x 168 B)",
                    "parallelism": f"blocks{world}"},
         "e2e": {"value": 1000.0 / e2e_ms_step, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 24},
+        "e2e_path": "bsg_train_steps_host_u8: every step's 8-bit RGB ground truth (the reference's PPM data, quantized "
+                    "once) copied from pinned host memory and widened on the device; every step's loss read back",
         # one global iteration = one local step of every block (Alg. 2); each GPU renders one full view per
         # iteration whatever K is, so the job's view throughput is K x value
         "block_steps_per_s": world * 1000.0 / ms_step,
