@@ -3,9 +3,8 @@
 // device piece is encode_gspl_device, which asks the block's context for the
 // GSPL payload of its cloud (csrc/checkpoint.cu) instead of downloading FP64
 // rows and narrowing them on the host.
+#include <cstdio>
 #include <cstring>
-#include <fstream>
-#include <limits>
 
 #include "../../include/blocksplat_gpu.hpp"
 
@@ -58,7 +57,7 @@ public:
 
 private:
     void need(size_t k) const {
-        if (k > n_ - at_) throw FormatError(code_, "read past the end");
+        if (k > n_ - at_) throw FormatError(code_, "payload ends early");
     }
     const uint8_t* p_;
     size_t n_, at_ = 0;
@@ -68,7 +67,7 @@ private:
 // A count read from the payload must fit in what is left (per item bytes)
 // before anything is allocated for it.
 size_t bounded_count(const Source& r, uint64_t count, uint64_t item_bytes) {
-    if (count > r.left() / item_bytes) throw FormatError(FormatErrorCode::CountOverflow, "count exceeds section payload");
+    if (count > r.left() / item_bytes) throw FormatError(FormatErrorCode::CountOverflow, "declared count needs more bytes than the section holds");
     return static_cast<size_t>(count);
 }
 
@@ -154,7 +153,7 @@ GaussianCloud read_gspl(Source& r) {
     const uint64_t count = r.get<uint64_t>();
     const uint32_t fd = r.get<uint32_t>();
     if (fd != static_cast<uint32_t>(kFeatureDimDeg0) && fd != static_cast<uint32_t>(kFeatureDimDeg1))
-        throw FormatError(FormatErrorCode::BadHeader, "unsupported feature width");
+        throw FormatError(FormatErrorCode::BadHeader, "GSPL feature width is neither 3 nor 12");
     const size_t n = bounded_count(r, count, 8 + 4 * (11 + static_cast<uint64_t>(fd)));
     GaussianCloud c(static_cast<int>(fd));
     c.ids.resize(n);
@@ -167,7 +166,7 @@ GaussianCloud read_gspl(Source& r) {
     for (auto* arr : {&c.positions, &c.rotations, &c.log_scales, &c.features, &c.opacity_logits})
         for (double& v : *arr) v = r.get<float>();
     for (size_t i = 1; i < n; ++i)
-        if (c.ids[i] <= c.ids[i - 1]) throw FormatError(FormatErrorCode::NonMonotoneIds, "checkpoint ids not ascending");
+        if (c.ids[i] <= c.ids[i - 1]) throw FormatError(FormatErrorCode::NonMonotoneIds, "GSPL ids must increase strictly");
     return c;
 }
 
@@ -191,21 +190,21 @@ SceneDataset decode_scene(const uint8_t* data, size_t size) {  // scene_io.cpp:1
     Source top(data, size, FormatErrorCode::TruncatedBuffer);
     char magic[4];
     top.take(magic, 4);
-    if (std::memcmp(magic, "DOGS", 4) != 0) throw FormatError(FormatErrorCode::BadMagic, "not a scene container");
+    if (std::memcmp(magic, "DOGS", 4) != 0) throw FormatError(FormatErrorCode::BadMagic, "missing DOGS magic");
     const uint32_t version = top.get<uint32_t>();
     if (version != kSceneFormatVersion)
-        throw FormatError(FormatErrorCode::UnsupportedVersion, "scene container version " + std::to_string(version));
+        throw FormatError(FormatErrorCode::UnsupportedVersion, "DOGS version " + std::to_string(version));
     SceneDataset scene;
     bool cams = false, pnts = false, gspl = false;
     while (!top.done()) {
         char tag[4];
         top.take(tag, 4);
         const uint64_t len = top.get<uint64_t>();
-        if (len > top.left()) throw FormatError(FormatErrorCode::TruncatedSection, "section payload truncated");
+        if (len > top.left()) throw FormatError(FormatErrorCode::TruncatedSection, "section length runs past the container");
         Source sec(data + top.pos(), static_cast<size_t>(len), FormatErrorCode::TruncatedSection);
         top.skip(static_cast<size_t>(len));
         auto once = [&](bool& seen, const char* name) {
-            if (seen) throw FormatError(FormatErrorCode::BadHeader, std::string("duplicate ") + name + " section");
+            if (seen) throw FormatError(FormatErrorCode::BadHeader, std::string(name) + " section appears twice");
             seen = true;
         };
         if (std::memcmp(tag, "CAMS", 4) == 0) {
@@ -219,29 +218,32 @@ SceneDataset decode_scene(const uint8_t* data, size_t size) {  // scene_io.cpp:1
             scene.checkpoint = read_gspl(sec);
             scene.has_checkpoint = true;
         } else {
-            throw FormatError(FormatErrorCode::UnknownSection, "unknown section tag " + std::string(tag, 4));
+            throw FormatError(FormatErrorCode::UnknownSection, "section tag " + std::string(tag, 4) + " is not CAMS / PNTS / GSPL");
         }
-        if (!sec.done()) throw FormatError(FormatErrorCode::TruncatedSection, "section has trailing bytes");
+        if (!sec.done()) throw FormatError(FormatErrorCode::TruncatedSection, "section payload longer than its contents");
     }
     return scene;
 }
 
 void save_scene(const std::string& path, const SceneDataset& scene) {
     const std::vector<uint8_t> bytes = encode_scene(scene);
-    std::ofstream f(path, std::ios::binary);
-    if (!f) throw std::runtime_error("cannot open for write: " + path);
-    f.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
-    if (!f) throw std::runtime_error("write failed: " + path);
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("save_scene: cannot create " + path);
+    const size_t wrote = std::fwrite(bytes.data(), 1, bytes.size(), f);
+    const bool ok = std::fclose(f) == 0 && wrote == bytes.size();
+    if (!ok) throw std::runtime_error("save_scene: short write to " + path);
 }
 
 SceneDataset load_scene(const std::string& path) {
-    std::ifstream f(path, std::ios::binary | std::ios::ate);
-    if (!f) throw std::runtime_error("cannot open for read: " + path);
-    const std::streamsize size = f.tellg();
-    f.seekg(0);
-    std::vector<uint8_t> bytes(static_cast<size_t>(size));
-    f.read(reinterpret_cast<char*>(bytes.data()), size);
-    if (!f) throw std::runtime_error("read failed: " + path);
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("load_scene: cannot open " + path);
+    std::vector<uint8_t> bytes;
+    uint8_t chunk[1 << 16];
+    size_t got = 0;
+    while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) bytes.insert(bytes.end(), chunk, chunk + got);
+    const bool err = std::ferror(f) != 0;
+    std::fclose(f);
+    if (err) throw std::runtime_error("load_scene: read error on " + path);
     return decode_scene(bytes.data(), bytes.size());
 }
 

@@ -1,6 +1,6 @@
 """Checkpoint files (the GSPL f32 checkpoint writer and model.dogs).
 
-The native codec (host/scene_io.cpp through libbsgpu.so, no device needed) is
+The native codec (host/checkpoint_io.cpp through libbsgpu.so, no device needed) is
 compared byte for byte with the oracle's restatement of scene_io.cpp
 (oracle/scene_format.py), and given the malformed inputs of the reference's
 own format tests (test_image_scene.cpp:170-240), each of which must raise
