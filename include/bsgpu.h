@@ -355,6 +355,11 @@ int bsg_step_counters(bsg_ctx* ctx, uint64_t* visible, uint64_t* pairs, uint64_t
  * (read only while stage timing is enabled; the FP32 work measure of the
  * blend rooflines). */
 uint64_t bsg_step_blend_evals(const bsg_ctx* ctx);
+/* Binning path of the most recent projection: 0 = per-tile shared-memory
+ * sort (every tile <= 2048 pairs), 1 = global depth sort + stable tile-key
+ * sort (bsg_project, or a view with a longer tile). Both give the order of
+ * renderer.cpp:86-117; the parity tests assert which one they exercised. */
+int bsg_last_binning(const bsg_ctx* ctx);
 /* Kernel launches since context creation (all entry points). */
 uint64_t bsg_launch_count(const bsg_ctx* ctx);
 /* Opaque cudaStream_t of the context (for event timing by the caller). */

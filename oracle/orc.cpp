@@ -8,6 +8,9 @@
 //   matrix products: left-to-right over k.
 #include "orc.hpp"
 
+#include <atomic>
+#include <thread>
+
 #include <algorithm>
 #include <numeric>
 
@@ -1574,7 +1577,21 @@ Scene generate_scene(const SynthConfig& cfg) {  // synth.cpp:13-77
                              cfg.image_size, cfg.image_size);
         cam.view_id = i;
         out.views.push_back(cam);
-        out.images.push_back(render(gt, cam, cfg.render).color);
+    }
+    // The views' renders are independent pure functions of (gt, cam): drawn
+    // on worker threads (test-fixture setup time only; each image is the
+    // same sequential per-pixel loop, so the bytes do not change).
+    out.images.resize(out.views.size());
+    {
+        const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+        std::atomic<size_t> next{0};
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < nt; ++w)
+            pool.emplace_back([&] {
+                for (size_t i; (i = next.fetch_add(1)) < out.views.size();)
+                    out.images[i] = render(gt, out.views[i], cfg.render).color;
+            });
+        for (auto& t : pool) t.join();
     }
     std::vector<size_t> order(cfg.gaussians);
     std::iota(order.begin(), order.end(), size_t{0});

@@ -175,6 +175,7 @@ SYMBOLS = [
     ("bsg_stage_times", ctypes.c_int, [_P, _DP]),
     ("bsg_step_counters", ctypes.c_int, [_P, _U64P, _U64P, _U64P]),
     ("bsg_step_blend_evals", ctypes.c_uint64, [_P]),
+    ("bsg_last_binning", ctypes.c_int, [_P]),
     ("bsg_launch_count", ctypes.c_uint64, [_P]),
     ("bsg_stream", _P, [_P]),
     ("bsg_synchronize", ctypes.c_int, [_P]),
@@ -535,6 +536,10 @@ class Block:
         v, p, l = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         _check(_lib.bsg_step_counters(self.h, ctypes.byref(v), ctypes.byref(p), ctypes.byref(l)))
         return dict(visible=v.value, pairs=p.value, launches=l.value, blend_evals=_lib.bsg_step_blend_evals(self.h))
+
+    def last_binning(self):
+        """'tile' (per-tile shared-memory sort) or 'global' for the last projection."""
+        return {0: "tile", 1: "global"}[int(_lib.bsg_last_binning(self.h))]
 
     def launch_count(self):
         return _lib.bsg_launch_count(self.h)

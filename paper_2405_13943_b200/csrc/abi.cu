@@ -1638,6 +1638,8 @@ int bsg_step_counters(bsg_ctx* h, uint64_t* visible, uint64_t* pairs, uint64_t* 
 
 uint64_t bsg_step_blend_evals(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->last_evals : 0; }
 
+int bsg_last_binning(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->last_binning : -1; }
+
 uint64_t bsg_launch_count(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->launches : 0; }
 
 void* bsg_stream(bsg_ctx* h) { return h ? reinterpret_cast<Ctx*>(h)->stream : nullptr; }

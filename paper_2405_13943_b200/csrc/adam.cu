@@ -30,10 +30,21 @@ __device__ __forceinline__ void load_row(const float4* __restrict__ pcache, uint
 }
 
 // The 9 image-space gradients of row i: FP32 record, or the FP64 slot of a
-// wide splat (slot index in rec[3i+2].w, see kWideArea).
+// wide splat (slot index in rec[3i+2].w, see kWideArea). The blend backward
+// accumulates the mean path as sum k L'^T L' d and the covariance path as
+// sum k (L'^T L' d)(L'^T L' d)^T with the scaled factor L' = kQScale L and
+// without the 1/2 (renderer.cpp:298-306); both are rescaled here.
 struct Grad2D {
     double v[9];
 };
+__device__ __forceinline__ void unscale_g2d(Grad2D& g) {
+    constexpr double kMean = 1.0 / kQScale2, kCov = 0.5 / (kQScale2 * kQScale2);
+    g.v[0] *= kMean;
+    g.v[1] *= kMean;
+    g.v[2] *= kCov;
+    g.v[3] *= kCov;
+    g.v[4] *= kCov;
+}
 __device__ __forceinline__ Grad2D load_g2d(uint32_t i, const float4* __restrict__ rec,
                                            const float4* __restrict__ g2d, const double* __restrict__ g2d_wide) {
     Grad2D g;
@@ -48,6 +59,7 @@ __device__ __forceinline__ Grad2D load_g2d(uint32_t i, const float4* __restrict_
         g.v[0] = ga.x; g.v[1] = ga.y; g.v[2] = ga.z; g.v[3] = ga.w;
         g.v[4] = gb.x; g.v[5] = gb.y; g.v[6] = gb.z; g.v[7] = gb.w; g.v[8] = gc.x;
     }
+    unscale_g2d(g);
     return g;
 }
 

@@ -27,6 +27,12 @@ constexpr uint32_t kNoWide = 0xffffffffu;
 // for a wide footprint's FP64 slot (the backward blend adds to it directly).
 constexpr uint32_t kWideBit = 0x80000000u;
 constexpr int kTileThreads = kTile * kTile;
+// Splat record scale: the factor L of minv (= L^T L) and the affine offsets k
+// are stored times sqrt(log2(e) / 2), so |L d|^2 is the exponent of ex2. The
+// backward's accumulators then carry kQScale^2 (mean path) and kQScale^4
+// (covariance path), removed when the fold reads them.
+constexpr double kQScale = 0.84932180028801904272;  // sqrt(0.5 * log2(e))
+constexpr double kQScale2 = kQScale * kQScale;
 constexpr int kMaxFd = 12;            // SH degree 1 (cloud.hpp:16-17)
 constexpr int kMaxD = 11 + kMaxFd;    // pos3 rot4 ls3 feat fd op1
 constexpr int kParamVec = (kMaxD + 3) / 4;  // float4 per row in the parameter cache

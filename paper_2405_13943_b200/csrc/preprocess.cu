@@ -231,10 +231,22 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                 const double o = 1.0 / (1.0 + exp(-static_cast<double>(fd >= 12 ? prm[kFeat + kMaxFd] : prm[kFeat + 3])));  // op_comp(fd)
                 const uint32_t r01 = (static_cast<uint32_t>(x0) & 0xffffu) | (static_cast<uint32_t>(x1) << 16);
                 const uint32_t r23 = (static_cast<uint32_t>(y0) & 0xffffu) | (static_cast<uint32_t>(y1) << 16);
+                // The blend evaluates q = d^T minv d (d = pixel - mean) as |L d|^2 with
+                // minv = L^T L, L = [[l11, l12], [0, l22]], in the affine form
+                // L d = L (p - o) + k around o = the rect centre, so no FP32 term is
+                // ever large: near-plane splats (depth ~0.01, |mean2d| ~1e6 px,
+                // minv ~1e-7) cancel terms of ~1e3 into q ~ 0.1 in the conic form,
+                // which FP32 cannot hold; here that cancellation happens once, in
+                // FP64 (k). L and k carry sqrt(log2(e) / 2), so the blend's
+                // exponent is ex2(-|L d|^2) = exp(-q / 2).
+                const double l11 = sqrt(m00), l12 = m01 / l11, l22 = sqrt(fmax(0.0, m11 - l12 * l12));
+                const double ox = 0.5 * static_cast<double>(x0 + x1), oy = 0.5 * static_cast<double>(y0 + y1);
+                const double k1 = -(l11 * (mx - ox) + l12 * (my - oy)), k2 = -(l22 * (my - oy));
                 rec[3 * static_cast<size_t>(i) + 0] =
-                    make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(m00), static_cast<float>(m01));
+                    make_float4(static_cast<float>(kQScale * l11), static_cast<float>(kQScale * l12),
+                                static_cast<float>(kQScale * l22), static_cast<float>(kQScale * k1));
                 rec[3 * static_cast<size_t>(i) + 1] =
-                    make_float4(static_cast<float>(m11), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
+                    make_float4(static_cast<float>(kQScale * k2), static_cast<float>(o), static_cast<float>(col[0]), static_cast<float>(col[1]));
                 // gradient target: the row, or a wide footprint's FP64 slot (see kWideArea)
                 uint32_t wslot = i;
                 if (static_cast<uint32_t>(x1 - x0 + 1) * static_cast<uint32_t>(y1 - y0 + 1) >= kWideArea) {

@@ -15,16 +15,6 @@
 namespace bsg {
 namespace {
 
-// exp(-q/2) as one MUFU.EX2 (ex2.approx.ftz: ~2 ulp; results below 2^-126
-// flush to 0, i.e. alpha < 1e-38), shared by the forward and backward blends
-// so both see bit-identical alphas.
-constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 * log2(e)
-__device__ __forceinline__ float gauss_weight(float q) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(q * kNegHalfLog2e));
-    return y;
-}
-
 __device__ __forceinline__ float fast_rcp(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -338,43 +328,126 @@ __global__ __launch_bounds__(1024) void tile_order_kernel(const uint2* __restric
 
 // K7 blend forward: one CTA of 128 threads per 16x16 tile. Warp w owns the
 // 8x8 sub-tile (w & 1, w >> 1); each lane owns two pixels of it (rows ly and
-// ly + 4), so every shared-memory record load and rect unpack serves two
-// pixels. Splat records are staged 256 at a time with a 4-bit mask of the
-// sub-tiles their rect overlaps; a warp skips entries outside its sub-tile
-// with one uniform test. Semantics (renderer.cpp:160-181): per pixel, the
-// contributors are the splats whose rect contains it, in (depth, index)
-// order; break before compositing once T < stop; alpha = min(o g, clamp); no
-// 1/255 skip. The stop decision uses T in FP64 (stacked clamped splats give
-// T = (1 - 0.99)^k exactly at the 1e-4 threshold, test_renderer.cpp:272-282).
+// ly + 4), so every shared-memory record load serves two pixels. Splat
+// records are staged 256 at a time; staging turns each record into the
+// tile-local affine form of its conic (see stage_entry) and builds, per warp,
+// a 16-bit hit mask over the warp's sub-tile; each warp then walks only the
+// entries that touch its sub-tile, with the mask packed into the list word.
+// Semantics (renderer.cpp:160-181): per pixel, the contributors are the
+// splats whose rect contains it, in (depth, index) order; break before
+// compositing once T < stop; alpha = min(o g, clamp); no 1/255 skip. The stop
+// decision uses T in FP64 (stacked clamped splats give T = (1 - 0.99)^k
+// exactly at the 1e-4 threshold, test_renderer.cpp:272-282).
 constexpr int kBlendThreads = 128;
 constexpr int kBatch = 256;
+constexpr int kBlendWarps = kBlendThreads / 32;
 
-__device__ __forceinline__ uint32_t subtile_mask(int x0, int x1, int y0, int y1, int tx0, int ty0) {
-    // rect (tile-local) vs the four 8x8 sub-tiles
-    const int lx0 = x0 - tx0, lx1 = x1 - tx0, ly0 = y0 - ty0, ly1 = y1 - ty0;
-    const bool left = lx0 <= 7 && lx1 >= 0, right = lx1 >= 8 && lx0 <= 15;
-    const bool top = ly0 <= 7 && ly1 >= 0, bottom = ly1 >= 8 && ly0 <= 15;
-    return (left && top ? 1u : 0u) | (right && top ? 2u : 0u) | (left && bottom ? 4u : 0u) |
-           (right && bottom ? 8u : 0u);
+// exp2(-q): the record's factor carries sqrt(log2(e) / 2), so this is
+// exp(-q_ref / 2) of renderer.cpp:53-59 (ex2.approx.ftz: ~2 ulp).
+__device__ __forceinline__ float ex2_neg(float q) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-q));
+    return y;
 }
 
-// Forward blend: hit mask of a splat rect over warp w's 8x8 sub-tile: low
-// byte = the sub-tile columns inside [x0, x1], high byte = the rows inside
-// [y0, y1]; 0 when they do not overlap. Built once per staged entry, so the
-// per-entry hit test of a lane is two shifts and an AND (measured: -3% fwd;
-// in the backward the extra staging work outweighed it, +2%).
+// Hit mask of a splat rect over the 8x8 sub-tile at (sx, sy): low byte = the
+// sub-tile columns inside [x0, x1], high byte = the rows inside [y0, y1]; 0
+// when they do not overlap. A lane's hit test is then two shifts and an AND.
 __device__ __forceinline__ uint32_t span_bits(int lo, int hi) {  // bits [lo, hi] of 0..7, clamped
     lo = max(lo, 0);
     hi = min(hi, 7);
     return lo <= hi ? ((0xffu >> (7 - hi)) & (0xffu << lo)) : 0u;
 }
 
-__device__ __forceinline__ uint16_t region_hits(int x0, int x1, int y0, int y1, int sx, int sy) {
+__device__ __forceinline__ uint32_t region_hits(int x0, int x1, int y0, int y1, int sx, int sy) {
     const uint32_t cm = span_bits(x0 - sx, x1 - sx), rm = span_bits(y0 - sy, y1 - sy);
-    return static_cast<uint16_t>(cm && rm ? (cm | (rm << 8)) : 0u);
+    return cm && rm ? (cm | (rm << 8)) : 0u;
 }
 
-__global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* __restrict__ ranges,
+// Entry t of a batch into shared memory. The record holds L' = kQScale L
+// (minv = L^T L, L upper triangular) and the offsets k' of L'(p - m) written
+// around the rect centre o (preprocess.cu); here o moves to the tile origin,
+// so t = L'(p - m) at tile-local pixel (lx, ly) is
+//   t1 = l11 lx + l12 ly + k1,  t2 = l22 ly + k2
+// with every FP32 term of the size of the footprint in pixels (the rect
+// centre is within the image, the tile origin within 16 px of the pixel).
+// Layout: {l11, l12, l22, k1}, {k2, o, r, g}, {b, target, -, -}.
+__device__ __forceinline__ void stage_entry(int t, uint32_t row, const float4* __restrict__ rec, int tx0, int ty0,
+                                            float4* s_rec, uint16_t (*s_hm)[kBatch]) {
+    const size_t r = 3 * static_cast<size_t>(row);
+    const float4 a = rec[r], b = rec[r + 1], c = rec[r + 2];
+    int x0, x1, y0, y1;
+    unpack_rect(c, x0, x1, y0, y1);
+    const float ox = 0.5f * static_cast<float>(x0 + x1) - static_cast<float>(tx0);  // exact
+    const float oy = 0.5f * static_cast<float>(y0 + y1) - static_cast<float>(ty0);
+    s_rec[3 * t] = make_float4(a.x, a.y, a.z, fmaf(-a.x, ox, fmaf(-a.y, oy, a.w)));
+    s_rec[3 * t + 1] = make_float4(fmaf(-a.z, oy, b.x), b.y, b.z, b.w);
+    s_rec[3 * t + 2] = make_float4(c.x, c.w, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < kBlendWarps; ++w)
+        s_hm[w][t] = static_cast<uint16_t>(region_hits(x0, x1, y0, y1, tx0 + (w & 1) * 8, ty0 + (w >> 1) * 8));
+}
+
+// This warp's entries of the batch (hit mask != 0), ascending, as
+// (entry | hit mask << 16).
+__device__ __forceinline__ int build_list(int warp, int lane, int cnt, const uint16_t (*s_hm)[kBatch],
+                                          uint32_t (*s_list)[kBatch]) {
+    int nl = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+        const int e = c0 + lane;
+        const uint32_t hm = e < cnt ? s_hm[warp][e] : 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, hm != 0);
+        if (hm) s_list[warp][nl + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint32_t>(e) | (hm << 16);
+        nl += __popc(bal);
+    }
+    __syncwarp();
+    return nl;
+}
+
+// One pixel's front-to-back loop over the entries of a 32-entry chunk it
+// hits (bit e of m = entry e of the chunk, ascending = compositing order).
+struct FwdPix {
+    float T, r, g, b;
+    double Td;
+    uint32_t n, last;
+    bool done;
+};
+
+__device__ __forceinline__ void fwd_pixel(FwdPix& P, uint32_t m, const uint32_t* __restrict__ list,
+                                          const float4* s_rec, float lx, float ly, uint32_t base, double tstop,
+                                          float aclamp, double oma_clamp) {
+    while (m) {
+        const int e = __ffs(m) - 1;
+        m &= m - 1;
+        if (P.Td < tstop) {
+            P.done = true;
+            return;
+        }
+        const uint32_t j = list[e] & 0xffffu;
+        const float4 A = s_rec[3 * j], B = s_rec[3 * j + 1];
+        const float cbl = s_rec[3 * j + 2].x;
+        const float t1 = fmaf(A.y, ly, fmaf(A.x, lx, A.w)), t2 = fmaf(A.z, ly, B.x);
+        const float og = B.y * ex2_neg(fmaf(t1, t1, t2 * t2));
+        const bool clamped = og >= aclamp;  // no float lies in [0.99, float(0.99))
+        const float alpha = clamped ? aclamp : og;
+        const float w = alpha * P.T;
+        P.r = fmaf(B.z, w, P.r);
+        P.g = fmaf(B.w, w, P.g);
+        P.b = fmaf(cbl, w, P.b);
+        P.T *= 1.f - alpha;
+        P.Td *= clamped ? oma_clamp : static_cast<double>(1.f - og);  // 1 - og exact for og >= 0.5
+        ++P.n;
+        P.last = base + j;
+    }
+}
+
+// The forward walks each pixel's own contributors: per 32-entry chunk of the
+// warp's list, 16 ballots give every lane the chunk's column and row masks
+// over its sub-tile, their AND is the set of entries whose rect contains the
+// lane's pixel, and the lane loops over those set bits. Lanes of a warp are
+// busy whenever their pixel has a contributor left in the chunk (a per-entry
+// warp loop idles every lane outside the entry's rect).
+__global__ __launch_bounds__(kBlendThreads, 8) void blend_fwd_kernel(const uint2* __restrict__ ranges,
                                                                   const uint32_t* __restrict__ pval,
                                                                   const float4* __restrict__ rec, int W, int H,
                                                                   int tiles_x, double tstop, float aclamp,
@@ -386,123 +459,73 @@ __global__ __launch_bounds__(kBlendThreads) void blend_fwd_kernel(const uint2* _
                                                                   unsigned long long* __restrict__ evals,
                                                                   const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
-    __shared__ float4 s_rec[3 * kBatch];  // entry j's splat record at 3j .. 3j+2 (one base address per entry)
-    __shared__ uint16_t s_hm[kBlendThreads / 32][kBatch];
-    __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
+    __shared__ float4 s_rec[3 * kBatch];
+    __shared__ uint16_t s_hm[kBlendWarps][kBatch];
+    __shared__ uint32_t s_list[kBlendWarps][kBatch];
     const int tile = static_cast<int>(tile_order[blockIdx.x]);
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int px = tx0 + (warp & 1) * 8 + (lane & 7);
-    const int py0 = ty0 + (warp >> 1) * 8 + (lane >> 3);
-    const int py1 = py0 + 4;
+    const int lxi = (warp & 1) * 8 + (lane & 7), ly0i = (warp >> 1) * 8 + (lane >> 3);
+    const int px = tx0 + lxi, py0 = ty0 + ly0i, py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
-    const int hb = lane & 7, hr = 8 + (lane >> 3);  // this lane's column bit, first row bit
+    const float lx = static_cast<float>(lxi), ly0 = static_cast<float>(ly0i), ly1 = ly0 + 4.f;
+    const int hc = lane & 7, hr = lane >> 3;  // this lane's sub-tile column, first row
     const uint2 range = ranges[tile];
     const double oma_clamp = 1.0 - aclamp_d;
-    float T0 = 1.f, T1 = 1.f, r0 = 0.f, g0 = 0.f, b0 = 0.f, r1 = 0.f, g1 = 0.f, b1 = 0.f;
-    double Td0 = 1.0, Td1 = 1.0;
-    uint32_t n0 = 0, n1 = 0, last0 = 0, last1 = 0;
-    bool done0 = !in0, done1 = !in1;
-    const float fx = static_cast<float>(px), fy0 = static_cast<float>(py0), fy1 = static_cast<float>(py1);
+    FwdPix P0{1.f, 0.f, 0.f, 0.f, 1.0, 0u, 0u, !in0}, P1{1.f, 0.f, 0.f, 0.f, 1.0, 0u, 0u, !in1};
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
-        if (__syncthreads_count(done0 && done1) == kBlendThreads) break;
+        if (__syncthreads_count(P0.done && P1.done) == kBlendThreads) break;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t idx = start + threadIdx.x + h * kBlendThreads;
-            if (idx < range.y) {
-                const size_t r = 3 * static_cast<size_t>(pval[idx]);
-                const float4 c = rec[r + 2];
-                int x0, x1, y0, y1;
-                unpack_rect(c, x0, x1, y0, y1);
-                const int t = threadIdx.x + h * kBlendThreads;
-                s_rec[3 * t] = rec[r];
-                s_rec[3 * t + 1] = rec[r + 1];
-                s_rec[3 * t + 2] = c;
-#pragma unroll
-                for (int w = 0; w < kBlendThreads / 32; ++w)
-                    s_hm[w][t] = region_hits(x0, x1, y0, y1, tx0 + (w & 1) * 8, ty0 + (w >> 1) * 8);
-            }
+            if (idx < range.y) stage_entry(threadIdx.x + h * kBlendThreads, pval[idx], rec, tx0, ty0, s_rec, s_hm);
         }
         __syncthreads();
         const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBatch), range.y - start));
-        // this warp's entries (rect overlaps its sub-tile), in list order
-        int nl = 0;
-        for (int c0 = 0; c0 < cnt; c0 += 32) {
-            const int e = c0 + lane;
-            const bool mine = e < cnt && s_hm[warp][e] != 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, mine);
-            if (mine) s_list[warp][nl + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
-            nl += __popc(bal);
+        const int nl = build_list(warp, lane, cnt, s_hm, s_list);
+        const uint32_t base = start - range.x + 1;  // 1-based list position of entry 0 of the batch
+        for (int c0 = 0; c0 < nl; c0 += 32) {
+            const uint32_t hm = c0 + lane < nl ? s_list[warp][c0 + lane] >> 16 : 0u;
+            uint32_t mc = 0, mr0 = 0, mr1 = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (hm >> c) & 1u);
+                mc = c == hc ? b : mc;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (hm >> (8 + r)) & 1u);
+                mr0 = r == hr ? b : mr0;
+                mr1 = r == hr + 4 ? b : mr1;
+            }
+            const uint32_t* list = &s_list[warp][c0];
+            if (!P0.done) fwd_pixel(P0, mc & mr0, list, s_rec, lx, ly0, base, tstop, aclamp, oma_clamp);
+            if (!P1.done) fwd_pixel(P1, mc & mr1, list, s_rec, lx, ly1, base, tstop, aclamp, oma_clamp);
         }
         __syncwarp();
-        for (int k = 0; k < nl && !(done0 && done1); ++k) {
-            const int j = s_list[warp][k];
-            const uint32_t hm = s_hm[warp][j];
-            const uint32_t cb = hm >> hb;
-            const bool hit0 = !done0 && (cb & (hm >> hr) & 1u);
-            const bool hit1 = !done1 && (cb & (hm >> (hr + 4)) & 1u);
-            if (!(hit0 || hit1)) continue;
-            const float4 a = s_rec[3 * j], b = s_rec[3 * j + 1], c = s_rec[3 * j + 2];
-            const float dx = fx - a.x;
-            const uint32_t pos = start - range.x + static_cast<uint32_t>(j) + 1;
-            if (hit0) {
-                if (Td0 < tstop) {
-                    done0 = true;
-                } else {
-                    const float dy = fy0 - a.y;
-                    const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
-                    const float og = b.y * gauss_weight(q);
-                    const bool clamped = og >= aclamp;  // no float lies in [0.99, float(0.99))
-                    const float alpha = clamped ? aclamp : og;
-                    const float w = alpha * T0;
-                    r0 += b.z * w; g0 += b.w * w; b0 += c.x * w;
-                    T0 *= 1.f - alpha;
-                    Td0 *= clamped ? oma_clamp : static_cast<double>(1.f - og);  // 1 - og exact for og >= 0.5
-                    ++n0;
-                    last0 = pos;
-                }
-            }
-            if (hit1) {
-                if (Td1 < tstop) {
-                    done1 = true;
-                } else {
-                    const float dy = fy1 - a.y;
-                    const float q = dx * (a.z * dx + a.w * dy) + dy * (a.w * dx + b.x * dy);
-                    const float og = b.y * gauss_weight(q);
-                    const bool clamped = og >= aclamp;
-                    const float alpha = clamped ? aclamp : og;
-                    const float w = alpha * T1;
-                    r1 += b.z * w; g1 += b.w * w; b1 += c.x * w;
-                    T1 *= 1.f - alpha;
-                    Td1 *= clamped ? oma_clamp : static_cast<double>(1.f - og);
-                    ++n1;
-                    last1 = pos;
-                }
-            }
-        }
     }
     // work counter for the FP32 roofline: composited (pixel, contributor) pairs
-    uint32_t ev = n0 + n1;
+    uint32_t ev = P0.n + P1.n;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
     if (lane == 0 && ev) atomicAdd(evals, static_cast<unsigned long long>(ev));
     if (in0) {
         const size_t p = static_cast<size_t>(py0) * W + px;
-        out_rgb[3 * p + 0] = r0 + T0 * bg0;
-        out_rgb[3 * p + 1] = g0 + T0 * bg1;
-        out_rgb[3 * p + 2] = b0 + T0 * bg2;
-        out_T[p] = static_cast<float>(Td0);
-        out_n[p] = n0;
-        out_last[p] = last0;
+        out_rgb[3 * p + 0] = P0.r + P0.T * bg0;
+        out_rgb[3 * p + 1] = P0.g + P0.T * bg1;
+        out_rgb[3 * p + 2] = P0.b + P0.T * bg2;
+        out_T[p] = static_cast<float>(P0.Td);
+        out_n[p] = P0.n;
+        out_last[p] = P0.last;
     }
     if (in1) {
         const size_t p = static_cast<size_t>(py1) * W + px;
-        out_rgb[3 * p + 0] = r1 + T1 * bg0;
-        out_rgb[3 * p + 1] = g1 + T1 * bg1;
-        out_rgb[3 * p + 2] = b1 + T1 * bg2;
-        out_T[p] = static_cast<float>(Td1);
-        out_n[p] = n1;
-        out_last[p] = last1;
+        out_rgb[3 * p + 0] = P1.r + P1.T * bg0;
+        out_rgb[3 * p + 1] = P1.g + P1.T * bg1;
+        out_rgb[3 * p + 2] = P1.b + P1.T * bg2;
+        out_T[p] = static_cast<float>(P1.Td);
+        out_n[p] = P1.n;
+        out_last[p] = P1.last;
     }
 }
 
@@ -538,48 +561,54 @@ __device__ __forceinline__ int reduced9_index(int lane) {
     return ((lane & 2) ? 8 : 0) + ((lane & 4) ? 4 : 0) + ((lane & 8) ? 2 : 0) + ((lane & 16) ? 1 : 0);
 }
 
-// Per-pixel reverse recurrence (renderer.cpp:288-308) for one contributor;
-// accumulates this pixel's share of the splat's 9 image-space gradients.
+// Per-pixel reverse recurrence (renderer.cpp:288-308) for one contributor.
+// The colour suffix enters dL/dalpha only through its dot product with the
+// pixel's dL/dC, so that dot product (ds) is carried instead of the 3-vector:
+//   dL/dalpha = dL/dC . (c T_before - s / (1 - alpha))
+//             = T_before (dL/dC . c) - ds / (1 - alpha),   ds += (dL/dC . c) alpha T_before.
 struct BwdPix {
-    float T, d0, d1, d2, s0, s1, s2;
+    float T, d0, d1, d2, ds;
 };
 
-__device__ __forceinline__ void bwd_step(BwdPix& P, float dx, float dy, const float4& a, const float4& b,
-                                         const float4& c, float aclamp, float (&acc)[9]) {
-    const float mdx = a.z * dx + a.w * dy, mdy = a.w * dx + b.x * dy;
-    const float q = dx * mdx + dy * mdy;
-    const float g = gauss_weight(q);
-    const float og = b.y * g;
+// Accumulators: 0,1 k L'^T L'd (mean); 2,3,4 k (L'^T L'd)(L'^T L'd)^T (cov, no
+// 1/2); 5,6,7 colour; 8 opacity -- rescaled by the fold (unscale_g2d).
+__device__ __forceinline__ void bwd_step(BwdPix& P, float u, float ly, const float4& A, const float4& B, float cbl,
+                                         float aclamp, float (&acc)[9]) {
+    const float t1 = fmaf(A.y, ly, u), t2 = fmaf(A.z, ly, B.x);
+    const float g = ex2_neg(fmaf(t1, t1, t2 * t2));
+    const float og = B.y * g;
     const float alpha = fminf(og, aclamp);
     const float inv = fast_rcp(1.f - alpha);  // 1 - alpha >= 0.01
     const float Tb = P.T * inv;
     const float at = alpha * Tb;
-    acc[5] += P.d0 * at;
-    acc[6] += P.d1 * at;
-    acc[7] += P.d2 * at;
-    const float dlda = (P.d0 * (b.z * Tb - P.s0 * inv) + P.d1 * (b.w * Tb - P.s1 * inv)) + P.d2 * (c.x * Tb - P.s2 * inv);
+    acc[5] = fmaf(P.d0, at, acc[5]);
+    acc[6] = fmaf(P.d1, at, acc[6]);
+    acc[7] = fmaf(P.d2, at, acc[7]);
+    const float dc = fmaf(P.d0, B.z, fmaf(P.d1, B.w, P.d2 * cbl));
+    const float dlda = fmaf(Tb, dc, -(inv * P.ds));
     if (og < aclamp) {
-        const float k = dlda * b.y * g;
-        acc[0] += k * mdx;
-        acc[1] += k * mdy;
-        const float h = 0.5f * k;
-        acc[2] += h * (mdx * mdx);
-        acc[3] += h * (mdx * mdy);
-        acc[4] += h * (mdy * mdy);
-        acc[8] += dlda * g;
+        const float kk = dlda * og;
+        const float mdx = A.x * t1, mdy = fmaf(A.y, t1, A.z * t2);  // L'^T t
+        const float u0 = kk * mdx, u1 = kk * mdy;
+        acc[0] += u0;
+        acc[1] += u1;
+        acc[2] = fmaf(u0, mdx, acc[2]);
+        acc[3] = fmaf(u0, mdy, acc[3]);
+        acc[4] = fmaf(u1, mdy, acc[4]);
+        acc[8] = fmaf(dlda, g, acc[8]);
     }
-    P.s0 += b.z * at;
-    P.s1 += b.w * at;
-    P.s2 += c.x * at;
+    P.ds = fmaf(dc, at, P.ds);
     P.T = Tb;
 }
 
 // K9 blend backward: reverse traversal of each pixel's composited list
-// (T recovered by division, 1 - alpha >= 0.01), same CTA layout as K7 (two
-// pixels per lane, per-warp sub-tile skip). The 9 per-splat gradients of the
-// warp's 64 pixels are summed in registers, transpose-reduced across the warp
-// in 12 shuffles and added with 9 scalar atomics; one or two contributing
-// lanes add directly.
+// (T recovered by division, 1 - alpha >= 0.01), same CTA layout, staging and
+// per-warp lists as K7. The 9 per-splat gradients of the warp's 64 pixels are
+// summed in registers, transpose-reduced across the warp in 12 shuffles and
+// added with 9 scalar atomics; up to kDirectLanes contributing lanes add
+// their own values directly (the same number of L2 atomics, no shuffles).
+constexpr int kDirectLanes = 4;
+
 __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2* __restrict__ ranges,
                                                                   const uint32_t* __restrict__ pval,
                                                                   const float4* __restrict__ rec, int W, int H,
@@ -591,19 +620,22 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   double* __restrict__ g2d_wide,
                                                                   const uint32_t* __restrict__ tile_order) {
     pdl_prologue();
-    __shared__ float4 s_rec[3 * kBatch];  // entry j's splat record at 3j .. 3j+2 (one base address per entry)
-    __shared__ uint8_t s_m[kBatch];
-    __shared__ uint16_t s_list[kBlendThreads / 32][kBatch];
+    __shared__ float4 s_rec[3 * kBatch];
+    __shared__ uint16_t s_hm[kBlendWarps][kBatch];
+    __shared__ uint32_t s_list[kBlendWarps][kBatch];
     __shared__ uint32_t s_max;
     const int tile = static_cast<int>(tile_order[blockIdx.x]);
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int px = tx0 + (warp & 1) * 8 + (lane & 7);
-    const int py0 = ty0 + (warp >> 1) * 8 + (lane >> 3);
-    const int py1 = py0 + 4;
+    const int lxi = (warp & 1) * 8 + (lane & 7), ly0i = (warp >> 1) * 8 + (lane >> 3);
+    const int px = tx0 + lxi, py0 = ty0 + ly0i, py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+    const float lx = static_cast<float>(lxi), ly0 = static_cast<float>(ly0i), ly1 = ly0 + 4.f;
+    // this lane's two pixels in a hit mask: column bit | row bit
+    const uint32_t hit_bits0 = (1u << (lane & 7)) | (1u << (8 + (lane >> 3)));
+    const uint32_t hit_bits1 = (1u << (lane & 7)) | (1u << (12 + (lane >> 3)));
     const uint2 range = ranges[tile];
-    BwdPix P0{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, P1{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    BwdPix P0{1.f, 0.f, 0.f, 0.f, 0.f}, P1{1.f, 0.f, 0.f, 0.f, 0.f};
     uint32_t last0 = 0, last1 = 0;
     if (in0) {
         const size_t p = static_cast<size_t>(py0) * W + px;
@@ -617,8 +649,9 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
         P1.T = in_T[p];
         P1.d0 = dl_dc[3 * p]; P1.d1 = dl_dc[3 * p + 1]; P1.d2 = dl_dc[3 * p + 2];
     }
-    P0.s0 = P0.T * bg0; P0.s1 = P0.T * bg1; P0.s2 = P0.T * bg2;  // suffix: contributions behind
-    P1.s0 = P1.T * bg0; P1.s1 = P1.T * bg1; P1.s2 = P1.T * bg2;
+    // suffix behind the last contributor: T_final bg (renderer.cpp:282-286)
+    P0.ds = P0.T * fmaf(P0.d0, bg0, fmaf(P0.d1, bg1, P0.d2 * bg2));
+    P1.ds = P1.T * fmaf(P1.d0, bg0, fmaf(P1.d1, bg1, P1.d2 * bg2));
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
     uint32_t wm = max(last0, last1);
@@ -627,59 +660,34 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
     if (lane == 0) atomicMax(&s_max, wm);
     __syncthreads();
     const uint32_t max_last = s_max;
-    const uint32_t wbit = 1u << warp;
-    const float fx = static_cast<float>(px), fy0 = static_cast<float>(py0), fy1 = static_cast<float>(py1);
     for (int end = static_cast<int>(max_last); end > 0; end -= kBatch) {
         const int start = end - kBatch > 0 ? end - kBatch : 0;
         __syncthreads();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int t = threadIdx.x + h * kBlendThreads;
-            const int li = start + t;
-            if (li < end) {
-                const uint32_t row = pval[range.x + li];
-                const size_t r = 3 * static_cast<size_t>(row);
-                const float4 c = rec[r + 2];
-                int x0, x1, y0, y1;
-                unpack_rect(c, x0, x1, y0, y1);
-                s_rec[3 * t] = rec[r];
-                s_rec[3 * t + 1] = rec[r + 1];
-                s_rec[3 * t + 2] = c;
-                s_m[t] = static_cast<uint8_t>(subtile_mask(x0, x1, y0, y1, tx0, ty0));
-            }
+            if (start + t < end) stage_entry(t, pval[range.x + start + t], rec, tx0, ty0, s_rec, s_hm);
         }
         __syncthreads();
-        // this warp's entries (rect overlaps its sub-tile), ascending
-        const int cnt = end - start;
-        int nl = 0;
-        for (int c0 = 0; c0 < cnt; c0 += 32) {
-            const int e = c0 + lane;
-            const bool mine = e < cnt && (s_m[e] & wbit);
-            const unsigned bal = __ballot_sync(0xffffffffu, mine);
-            if (mine) s_list[warp][nl + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
-            nl += __popc(bal);
-        }
-        __syncwarp();
+        const int nl = build_list(warp, lane, end - start, s_hm, s_list);
         for (int k = nl - 1; k >= 0; --k) {
-            const int sj = s_list[warp][k];
-            const int j = start + sj;
-            const float4 c = s_rec[3 * sj + 2];
-            int x0, x1, y0, y1;
-            unpack_rect(c, x0, x1, y0, y1);
-            const bool inx = px >= x0 && px <= x1;
-            const bool hit0 = static_cast<uint32_t>(j) < last0 && inx && py0 >= y0 && py0 <= y1;
-            const bool hit1 = static_cast<uint32_t>(j) < last1 && inx && py1 >= y0 && py1 <= y1;
+            const uint32_t wd = s_list[warp][k];
+            const uint32_t sj = wd & 0xffffu, hm = wd >> 16;
+            const uint32_t j = static_cast<uint32_t>(start) + sj;  // 0-based list position
+            const bool hit0 = j < last0 && (hm & hit_bits0) == hit_bits0;
+            const bool hit1 = j < last1 && (hm & hit_bits1) == hit_bits1;
             const unsigned mask = __ballot_sync(0xffffffffu, hit0 || hit1);
             if (mask == 0) continue;
+            const float4 A = s_rec[3 * sj], B = s_rec[3 * sj + 1];
+            const float2 C = *reinterpret_cast<const float2*>(&s_rec[3 * sj + 2]);
+            const float u = fmaf(A.x, lx, A.w);
             float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            const float4 a = s_rec[3 * sj], b = s_rec[3 * sj + 1];
-            const float dx = fx - a.x;
-            if (hit0) bwd_step(P0, dx, fy0 - a.y, a, b, c, aclamp, acc);
-            if (hit1) bwd_step(P1, dx, fy1 - a.y, a, b, c, aclamp, acc);
-            const uint32_t target = __float_as_uint(c.w);  // row, or kWideBit | FP64 slot (kWideArea)
+            if (hit0) bwd_step(P0, u, ly0, A, B, C.x, aclamp, acc);
+            if (hit1) bwd_step(P1, u, ly1, A, B, C.x, aclamp, acc);
+            const uint32_t target = __float_as_uint(C.y);  // row, or kWideBit | FP64 slot (kWideArea)
             const bool wide = target & kWideBit;
             float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(target & ~kWideBit));
-            if (__popc(mask) <= 2 && !wide) {
+            if (__popc(mask) <= kDirectLanes && !wide) {
                 if (hit0 || hit1) {
                     atomicAdd(reinterpret_cast<float4*>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
                     atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
