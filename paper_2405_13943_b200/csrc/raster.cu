@@ -11,6 +11,7 @@
 #include "bsg_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace bsg {
 namespace {
@@ -606,8 +607,12 @@ __device__ __forceinline__ void bwd_step(BwdPix& P, float u, float ly, const flo
 // per-warp lists as K7. The 9 per-splat gradients of the warp's 64 pixels are
 // summed in registers, transpose-reduced across the warp in 12 shuffles and
 // added with 9 scalar atomics; up to kDirectLanes contributing lanes add
-// their own values directly (the same number of L2 atomics, no shuffles).
-constexpr int kDirectLanes = 4;
+// their own values directly with vector atomics instead (no shuffles). The
+// threshold trades issue slots against L2 atomic traffic: measured at cfg 2,
+// blend bwd 0.178 / 0.173 / 0.165 / 0.156 / 0.158 / 0.186 / 0.295 ms for
+// 2 / 4 / 8 / 16 / 20 / 24 / 32 lanes; one butterfly stage with the lower 16
+// lanes adding directly (fewer shuffles, more atomics) was slower still.
+constexpr int kDirectLanes = 16;
 
 __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2* __restrict__ ranges,
                                                                   const uint32_t* __restrict__ pval,
@@ -618,7 +623,8 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                                                                   const float* __restrict__ dl_dc,
                                                                   float4* __restrict__ g2d,
                                                                   double* __restrict__ g2d_wide,
-                                                                  const uint32_t* __restrict__ tile_order) {
+                                                                  const uint32_t* __restrict__ tile_order,
+                                                                  int direct_lanes) {
     pdl_prologue();
     __shared__ float4 s_rec[3 * kBatch];
     __shared__ uint16_t s_hm[kBlendWarps][kBatch];
@@ -687,7 +693,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             const uint32_t target = __float_as_uint(C.y);  // row, or kWideBit | FP64 slot (kWideArea)
             const bool wide = target & kWideBit;
             float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(target & ~kWideBit));
-            if (__popc(mask) <= kDirectLanes && !wide) {
+            if (__popc(mask) <= direct_lanes && !wide) {
                 if (hit0 || hit1) {
                     atomicAdd(reinterpret_cast<float4*>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
                     atomicAdd(reinterpret_cast<float4*>(dst) + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
@@ -695,11 +701,18 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
                 }
             } else {
                 const float r = warp_reduce9(acc, lane);
-                const int idx = reduced9_index(lane);
-                if ((lane & 1) == 0 && idx < 9) {
-                    if (!wide)
-                        atomicAdd(dst + idx, r);
-                    else
+                if (!wide) {
+                    // values 0-3 / 4-7 sit in lanes {0,16,8,24} / {4,20,12,28}, value 8
+                    // in lane 2: three shuffles gather the quads into lanes 0 and 4,
+                    // so the sum reaches L2 as 3 vector atomics instead of 9 scalar
+                    const float q1 = __shfl_down_sync(0xffffffffu, r, 16);
+                    const float q2 = __shfl_down_sync(0xffffffffu, r, 8);
+                    const float q3 = __shfl_down_sync(0xffffffffu, r, 24);
+                    if ((lane & ~4) == 0) atomicAdd(reinterpret_cast<float4*>(dst + lane), make_float4(r, q1, q2, q3));
+                    if (lane == 2) atomicAdd(dst + 8, r);
+                } else {
+                    const int idx = reduced9_index(lane);
+                    if ((lane & 1) == 0 && idx < 9)
                         atomicAdd(g2d_wide + 9 * static_cast<size_t>(target & ~kWideBit) + idx, static_cast<double>(r));
                 }
             }
@@ -773,10 +786,20 @@ void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     BSG_LAUNCHED(c);
 }
 
+// BSG_DIRECT_LANES overrides kDirectLanes (measurement only)
+static int direct_lanes() {
+    static const int v = [] {
+        const char* e = std::getenv("BSG_DIRECT_LANES");
+        return e ? std::atoi(e) : kDirectLanes;
+    }();
+    return v;
+}
+
 void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const int ntiles = cam.tiles_x * cam.tiles_y;
     launch_pdl(c->stream, ntiles, kBlendThreads, 0, blend_bwd_kernel, c->ranges, c->pval[c->pairs_sorted], c->rec, cam.W, cam.H, cam.tiles_x, static_cast<float>(rc.alpha_clamp),
-        rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d, c->g2d_wide, c->tile_order);
+        rc.bg[0], rc.bg[1], rc.bg[2], c->out_T, c->out_last, c->dl_dc, c->g2d, c->g2d_wide, c->tile_order,
+        direct_lanes());
     BSG_LAUNCHED(c);
 }
 
