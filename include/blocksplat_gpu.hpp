@@ -297,6 +297,11 @@ struct SessionOptions {  // runtime.hpp:109-115
 // run_simulated (runtime.cpp:623-671): K blocks in one process, one host
 // thread per block, consensus by an in-order device reduction across the
 // group (no master hop). devices[b % devices.size()] hosts block b.
+// The view order BlockTrainer::train_step draws (trainer.cpp:116-118,250-252:
+// derive_seed, then a Fisher-Yates shuffle with rejection-sampled indices on
+// mt19937_64 at the start of every pass) -- the same code path.
+std::vector<uint32_t> view_sequence(uint64_t seed, uint32_t block_id, size_t n_views, size_t n_steps);
+
 RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, const SessionOptions& opt,
                         const std::function<void(const RoundDiagnostics&)>& observer = {},
                         const std::vector<int>& devices = {0});

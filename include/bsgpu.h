@@ -136,6 +136,14 @@ int bsg_render_backward(bsg_ctx* ctx, const bsg_camera* cam, const double* gt_rg
                         double* out_loss3, double* g_pos, double* g_rot, double* g_log_scale, double* g_features,
                         double* g_opacity_logit, double* screen_grad_norm, uint8_t* visible, double* out_rendered);
 
+/* The loss and its image gradient of the training step on given images:
+ * loss_value (renderer.cpp:185-192) and dL/dC = sign(C - GT) / (3HW) -
+ * lambda dSSIM/dC (renderer.cpp:259-272, ssim_with_gradient ssim.cpp:138-185),
+ * through the step's own SSIM kernels. rendered, gt: HxWx3; out_loss3 =
+ * {loss, l1, ssim}; out_dl_dc HxWx3 (both nullable). */
+int bsg_image_loss(bsg_ctx* ctx, uint32_t width, uint32_t height, const double* rendered, const double* gt,
+                   const bsg_render_config* cfg, double* out_loss3, double* out_dl_dc);
+
 /* ---- projection / sort introspection (parity of the integer paths) --- */
 /* Per row: visible flag, FP64 depth, footprint rect {x0,x1,y0,y1}; and the
  * compositing order (rows of visible splats sorted by (depth, index),
@@ -260,7 +268,10 @@ typedef struct bsg_adapt_args {
  * rank decides on identical reduced values). Collective: all ranks call it in
  * the same order. bsg_consensus_wait blocks for the pending round and returns
  * its result and the rho now in force (rho_out nullable). The pending round
- * must be waited for before the next one is started. */
+ * must be waited for before the next one is started. A bsg_train_steps that
+ * crosses a densification iteration while a round is pending blocks for the
+ * round before densifying (densification rewrites the anchor and dual rows
+ * the round writes); the round's result stays pending for bsg_consensus_wait. */
 int bsg_consensus_round_async(bsg_ctx* ctx, const bsg_round_args* args, const bsg_adapt_args* adapt);
 int bsg_consensus_wait(bsg_ctx* ctx, bsg_round_result* out, bsg_penalties* rho_out);
 
@@ -313,6 +324,10 @@ typedef struct bsg_round_diag {  /* RoundDiagnostics (runtime.hpp:61-71) */
 } bsg_round_diag;
 
 const char* bsg_driver_last_error(void);
+/* The view sequence of BlockTrainer::train_step (trainer.cpp:116-118,250-252)
+ * for seed / block id: the host trainer's own Fisher-Yates code path
+ * (errors via bsg_driver_last_error). */
+int bsg_view_sequence(uint64_t seed, uint32_t block_id, size_t n_views, size_t n_steps, uint32_t* out);
 int bsg_run_simulated(int feature_dim, size_t n, const uint64_t* ids, const double* pos, const double* rot,
                       const double* log_scale, const double* features, const double* opacity_logit, size_t n_views,
                       const bsg_camera* cams, const double* const* gt_rgb, const bsg_trainer_config* trainer,
@@ -341,6 +356,31 @@ int bsg_load_checkpoint(const char* path, size_t capacity, uint64_t* ids, double
 int bsg_decode_checkpoint(const uint8_t* data, size_t size, size_t capacity, uint64_t* ids, double* pos,
                           double* rot, double* log_scale, double* features, double* opacity_logit, size_t* out_n,
                           int* out_fd, int* format_code);
+
+/* ---- master-round ownership bookkeeping (device) ------------------------ */
+/* The owner table of the consensus slot table on one device (
+ * replaces the master's std::map of owners, runtime.cpp:490-518): n_slots
+ * shared ids (ascending) with a bitmask of their owning blocks (K <= 32,
+ * >= 2 bits set). Non-shared ids never enter it: they have one owner, so a
+ * removal kills them, and new rows are born single-owner. */
+typedef struct bsg_owner_table bsg_owner_table;
+int bsg_owners_create(int device, size_t n_slots, const uint64_t* slot_ids, const uint32_t* owner_masks,
+                      uint32_t blocks, bsg_owner_table** out);
+int bsg_owners_destroy(bsg_owner_table* t);
+size_t bsg_owners_size(const bsg_owner_table* t);
+/* Current table (n = bsg_owners_size): ids ascending, owner masks. */
+int bsg_owners_download(const bsg_owner_table* t, uint64_t* slot_ids, uint32_t* owner_masks);
+/* One round's removals: removed[b] (n_removed[b] ids) taken from block b.
+ * Clears the owners, classifies every touched slot (1 reset: >= 2 owners
+ * remain; 2 unshared: one remains; 3 dead: none) and drops the slots left
+ * with fewer than 2 owners from the table. Writes the touched slots in
+ * ascending order -- their index in the table before this call, class and
+ * new owner mask -- (capacity cap; BSG_ERR_CAPACITY with *out_touched set
+ * when too small, the table unchanged) and, per removed id in block order,
+ * whether it was in the table (found; nullable). */
+int bsg_owners_remove(bsg_owner_table* t, const uint64_t* const* removed, const size_t* n_removed,
+                      uint32_t* out_slot, uint8_t* out_class, uint32_t* out_mask, size_t cap, size_t* out_touched,
+                      uint8_t* out_found);
 
 /* ---- measurement ------------------------------------------------------ */
 /* Per-stage device times of the most recent step (CUDA events on the

@@ -432,4 +432,16 @@ PYBIND11_MODULE(_oracle, m) {
         return run_simulated(plan, tc, opt);
     });
     m.def("consensus_schedule", &consensus_schedule);
+    m.def("master_ownership_round", [](std::map<uint64_t, std::vector<uint32_t>> owners,
+                                       std::vector<std::vector<uint64_t>> removed,
+                                       std::vector<std::vector<uint64_t>> added) {
+        OwnershipRound r = master_ownership_round(owners, removed, added);
+        py::dict d;
+        d["reset"] = r.reset;
+        d["unshared"] = r.unshared;
+        d["dead"] = r.dead;
+        d["shared_now"] = r.shared_now;
+        d["owners"] = owners;
+        return d;
+    });
 }

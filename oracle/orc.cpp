@@ -1658,6 +1658,33 @@ ClusterPlan plan_cluster(const Scene& scene, uint32_t blocks, double expand_scal
     return plan;
 }
 
+OwnershipRound master_ownership_round(std::map<uint64_t, std::vector<uint32_t>>& owners,
+                                      const std::vector<std::vector<uint64_t>>& removed,
+                                      const std::vector<std::vector<uint64_t>>& added) {  // runtime.cpp:490-518
+    std::map<uint64_t, size_t> prev_owner_count;
+    for (uint32_t b = 0; b < removed.size(); ++b)
+        for (uint64_t id : removed[b]) {
+            auto it = owners.find(id);
+            if (it == owners.end()) continue;
+            prev_owner_count.emplace(id, it->second.size());
+            auto& list = it->second;
+            list.erase(std::remove(list.begin(), list.end(), b), list.end());
+        }
+    OwnershipRound r;
+    for (const auto& [id, prev] : prev_owner_count) {
+        const auto& list = owners.at(id);
+        if (list.empty()) r.dead.push_back(id);
+        else if (prev >= 2 && list.size() == 1) r.unshared.push_back(id);
+        else if (prev >= 2) r.reset.push_back(id);
+    }
+    for (uint64_t id : r.dead) owners.erase(id);
+    for (uint32_t b = 0; b < added.size(); ++b)
+        for (uint64_t id : added[b]) owners[id] = {b};
+    for (const auto& [id, list] : owners)  // current_shared (runtime.cpp:520)
+        if (list.size() >= 2) r.shared_now.push_back(id);
+    return r;
+}
+
 RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& tc, const SessionOptions& opt) {
     if (opt.total_iterations != tc.iterations) throw InvalidArgument("session and trainer iteration counts differ");
     const auto blocks = static_cast<uint32_t>(plan.shards.size());
@@ -1702,30 +1729,17 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& tc, const 
             if (ups[b].has_nonshared) ups[b].nonshared = trainers[b].nonshared_slice();
         }
         done = t;
-        std::map<uint64_t, size_t> prev_owner_count;
-        for (uint32_t b = 0; b < blocks; ++b)
-            for (uint64_t id : ups[b].removed) {
-                auto it = owners.find(id);
-                if (it == owners.end()) continue;
-                prev_owner_count.emplace(id, it->second.size());
-                auto& list = it->second;
-                list.erase(std::remove(list.begin(), list.end(), b), list.end());
-            }
-        std::vector<uint64_t> reset_ids, unshared_ids, dead_ids;
-        for (const auto& [id, prev] : prev_owner_count) {
-            const auto& list = owners.at(id);
-            if (list.empty()) dead_ids.push_back(id);
-            else if (prev >= 2 && list.size() == 1) unshared_ids.push_back(id);
-            else if (prev >= 2) reset_ids.push_back(id);
-        }
-        erase_by_ids(global, dead_ids);
-        for (uint64_t id : dead_ids) owners.erase(id);
+        std::vector<std::vector<uint64_t>> removed(blocks), added(blocks);
         for (uint32_t b = 0; b < blocks; ++b) {
-            if (ups[b].new_rows.size() == 0) continue;
-            insert_rows(global, ups[b].new_rows);
-            for (uint64_t id : ups[b].new_rows.ids) owners[id] = {b};
+            removed[b] = ups[b].removed;
+            added[b] = ups[b].new_rows.ids;
         }
-        shared_now = current_shared();
+        OwnershipRound own = master_ownership_round(owners, removed, added);
+        std::vector<uint64_t> reset_ids = own.reset, unshared_ids = own.unshared;
+        erase_by_ids(global, own.dead);
+        for (uint32_t b = 0; b < blocks; ++b)
+            if (ups[b].new_rows.size() != 0) insert_rows(global, ups[b].new_rows);
+        shared_now = own.shared_now;
         std::vector<Cloud> slices(blocks);
         std::vector<Contribution> contribs;
         for (uint32_t b = 0; b < blocks; ++b) {

@@ -354,7 +354,14 @@ struct Scene {
     Cloud checkpoint;
     Cloud ground_truth;
 };
-Scene generate_scene(const SynthConfig& cfg);                                  // synth.cpp:13-77
+Scene generate_scene(const SynthConfig& cfg);
+// Master-round ownership changes (runtime.cpp:490-518 + current_shared):
+// owners updated in place; reset (before the flipped ids join), unshared,
+// dead ids and the shared set after the round, all ascending.
+struct OwnershipRound { std::vector<uint64_t> reset, unshared, dead, shared_now; };
+OwnershipRound master_ownership_round(std::map<uint64_t, std::vector<uint32_t>>& owners,
+                                      const std::vector<std::vector<uint64_t>>& removed,
+                                      const std::vector<std::vector<uint64_t>>& added);                                  // synth.cpp:13-77
 
 struct ShardSpec { uint32_t block_id = 0; Cloud initial; std::vector<TrainView> views;
                    std::vector<size_t> view_indices; std::vector<uint64_t> shared_ids;

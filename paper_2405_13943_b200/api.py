@@ -123,6 +123,8 @@ SYMBOLS = [
                                     ctypes.POINTER(bsg_render_config), _DP, _DP, _SZP, _DP, _DP]),
     ("bsg_render_backward", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), _DP, ctypes.POINTER(bsg_render_config), _DP,
                                             _DP, _DP, _DP, _DP, _DP, _DP, _U8P, _DP]),
+    ("bsg_image_loss", ctypes.c_int, [_P, ctypes.c_uint32, ctypes.c_uint32, _DP, _DP, ctypes.POINTER(bsg_render_config),
+                                       _DP, _DP]),
     ("bsg_project", ctypes.c_int, [_P, ctypes.POINTER(bsg_camera), ctypes.POINTER(bsg_render_config), _U8P, _DP,
                                     ctypes.POINTER(ctypes.c_int32), _U32P, _SZP]),
     ("bsg_tile_pairs", ctypes.c_int, [_P, _U32P, _U32P, _SZ, _SZP]),
@@ -164,11 +166,17 @@ SYMBOLS = [
     ("bsg_plan_shared", ctypes.c_int, [_P, _U64P, _U32P, _U32P]),
     ("bsg_plan_block_shared", ctypes.c_int, [_P, ctypes.c_uint32, _SZP, _U32P, _U32P, _U8P]),
     ("bsg_driver_last_error", ctypes.c_char_p, []),
+    ("bsg_view_sequence", ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint32, _SZ, _SZ, _U32P]),
     ("bsg_run_simulated", ctypes.c_int, [ctypes.c_int, _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZ,
                                           ctypes.POINTER(bsg_camera), ctypes.POINTER(_DP),
                                           ctypes.POINTER(bsg_trainer_config), ctypes.POINTER(bsg_session_options), _SZ,
                                           ctypes.POINTER(ctypes.c_int), _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZP,
                                           ctypes.POINTER(bsg_round_diag), _SZ, _SZP, _DP]),
+    ("bsg_owners_create", ctypes.c_int, [ctypes.c_int, _SZ, _U64P, _U32P, ctypes.c_uint32, ctypes.POINTER(_P)]),
+    ("bsg_owners_destroy", ctypes.c_int, [_P]),
+    ("bsg_owners_size", _SZ, [_P]),
+    ("bsg_owners_download", ctypes.c_int, [_P, _U64P, _U32P]),
+    ("bsg_owners_remove", ctypes.c_int, [_P, ctypes.POINTER(_U64P), _SZP, _U32P, _U8P, _U32P, _SZ, _SZP, _U8P]),
     ("bsg_enable_stage_timing", ctypes.c_int, [_P, ctypes.c_int]),
     ("bsg_stage_count", ctypes.c_int, []),
     ("bsg_stage_name", ctypes.c_char_p, [ctypes.c_int]),
@@ -364,6 +372,18 @@ class Block:
                                         _ptr(rend, ctypes.c_double)))
         g.update(loss=loss3[0], l1=loss3[1], ssim=loss3[2], screen_grad_norm=sgn, visible=vis, rendered=rend)
         return g
+
+    def image_loss(self, rendered, gt, cfg=None):
+        """(loss, l1, ssim), dL/dC of the step's loss on given HxWx3 images."""
+        rendered, gt = _f64(rendered), _f64(gt)
+        H, W = rendered.shape[:2]
+        if gt.shape != rendered.shape or rendered.shape != (H, W, 3):
+            raise InvalidArgument("image dimension mismatch")
+        l3, g = np.zeros(3), np.zeros((H, W, 3))
+        _check(_lib.bsg_image_loss(self.h, W, H, _ptr(rendered, ctypes.c_double), _ptr(gt, ctypes.c_double),
+                                   ctypes.byref(cfg) if cfg else None, _ptr(l3, ctypes.c_double),
+                                   _ptr(g, ctypes.c_double)))
+        return l3, g
 
     def project(self, cam, cfg=None):
         n = self.n
@@ -578,6 +598,55 @@ def group_consensus_round(blocks, alpha, relax, reset_slots=(), diagnostics=Fals
     return _round_dict(r)
 
 
+class OwnerTable:
+    """The master round's device owner table (bsg_owners_*):
+    shared ids (ascending) with owner bitmasks over K <= 32 blocks."""
+
+    def __init__(self, slot_ids, owner_masks, blocks, device=0):
+        load_library()
+        ids = np.ascontiguousarray(slot_ids, np.uint64)
+        masks = np.ascontiguousarray(owner_masks, np.uint32)
+        self.blocks = blocks
+        h = ctypes.c_void_p()
+        _check(_lib.bsg_owners_create(device, len(ids), _ptr(ids, ctypes.c_uint64), _ptr(masks, ctypes.c_uint32),
+                                      blocks, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            _lib.bsg_owners_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def table(self):
+        n = _lib.bsg_owners_size(self.h)
+        ids, masks = np.zeros(max(n, 1), np.uint64), np.zeros(max(n, 1), np.uint32)
+        _check(_lib.bsg_owners_download(self.h, _ptr(ids, ctypes.c_uint64), _ptr(masks, ctypes.c_uint32)))
+        return ids[:n], masks[:n]
+
+    def remove(self, removed):
+        """removed: per block, the ids it dropped this round. Returns (slots,
+        classes, masks) of the touched slots and the per-id found flags."""
+        lists = [np.ascontiguousarray(r, np.uint64) for r in removed]
+        assert len(lists) == self.blocks
+        ptrs = (_U64P * self.blocks)(*[_ptr(r, ctypes.c_uint64) for r in lists])
+        ns = np.array([len(r) for r in lists], dtype=np.uintp)
+        cap = int(_lib.bsg_owners_size(self.h)) + 1
+        slot, cls, mask = np.zeros(cap, np.uint32), np.zeros(cap, np.uint8), np.zeros(cap, np.uint32)
+        found = np.zeros(max(int(ns.sum()), 1), np.uint8)
+        touched = ctypes.c_size_t()
+        _check(_lib.bsg_owners_remove(self.h, ptrs, ns.ctypes.data_as(_SZP), _ptr(slot, ctypes.c_uint32),
+                                      _ptr(cls, ctypes.c_uint8), _ptr(mask, ctypes.c_uint32), cap,
+                                      ctypes.byref(touched), _ptr(found, ctypes.c_uint8)))
+        k = touched.value
+        return slot[:k], cls[:k], mask[:k], found[:int(ns.sum())]
+
+
 def nccl_unique_id():
     load_library()
     buf = (ctypes.c_uint8 * 128)()
@@ -636,6 +705,17 @@ class Plan:
         _lib.bsg_plan_block_shared(self.h, b, ctypes.byref(n), _ptr(rows, ctypes.c_uint32), _ptr(slots, ctypes.c_uint32),
                                    _ptr(first, ctypes.c_uint8))
         return rows[:n.value], slots[:n.value], first[:n.value]
+
+
+def view_sequence(seed, block_id, n_views, n_steps):
+    """The C++ host BlockTrainer's view order (bsg_view_sequence)."""
+    load_library()
+    out = np.zeros(max(n_steps, 1), np.uint32)
+    st = _lib.bsg_view_sequence(seed, block_id, n_views, n_steps, _ptr(out, ctypes.c_uint32))
+    if st != BSG_OK:
+        msg = _lib.bsg_driver_last_error().decode()
+        raise InvalidArgument(msg) if st == BSG_ERR_INVALID_ARGUMENT else BsgError(msg)
+    return out[:n_steps]
 
 
 def session_options(total_iterations, interval=100, alpha=1.6, blocks=1, expand_scale=1.4, holdout=8, seed=0,

@@ -347,6 +347,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
         V = c->mbox->V;
         kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
         P = bin_global(c, cam, V, kbits);  // its P wait orders the tile scan's mailbox write before this read
+        if (c->mbox->pairs_big) throw Error{BSG_ERR_CAPACITY, "view with 2^30 or more tile pairs"};
         c->last_max_tile = c->mbox->max_tile;
     } else {
         stage_begin(c, kStDepthSort);
@@ -360,6 +361,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
         kbits = static_cast<uint32_t>(depth_key_bits(c->mbox->visible_pre));
         wait_mailbox(c, &c->mbox->seq_p, seq);
         P = c->mbox->P;
+        if (c->mbox->pairs_big) throw Error{BSG_ERR_CAPACITY, "view with 2^30 or more tile pairs"};
         const uint32_t max_tile = c->mbox->max_tile;
         c->last_max_tile = max_tile;
         stage_end(c, kStPairs);
@@ -702,7 +704,7 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             BSG_CUDA(cudaEventCreateWithFlags(&c->round_done, cudaEventDisableTiming));
             BSG_CUDA(cudaEventCreate(&c->round_t0));
             BSG_CUDA(cudaEventCreate(&c->round_t1));
-            BSG_CUDA(cudaMallocHost(&c->round_host, 8 * sizeof(double)));
+            BSG_CUDA(cudaMallocHost(&c->round_host, 16 * sizeof(double)));  // 8 round scalars + 5 rho
             dev_alloc(&c->rho_dev, kMaxD);
             dev_alloc(&c->rho_state, 5);
             dev_alloc(&c->g2d_wide, 9 * static_cast<size_t>(kWideCap));
@@ -965,6 +967,44 @@ int bsg_render_backward(bsg_ctx* h, const bsg_camera* cam, const double* gt, con
             if (g_op) g_op[i] = g[op_comp(c->fd) * n + i];
         }
         if (out_rendered) for (size_t i = 0; i < 3 * px; ++i) out_rendered[i] = rgb[i];
+    });
+}
+
+int bsg_image_loss(bsg_ctx* h, uint32_t width, uint32_t height, const double* rendered, const double* gt,
+                   const bsg_render_config* cfg, double* out_loss3, double* out_dl_dc) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!rendered || !gt || width == 0 || height == 0) invalid("image dimension mismatch");
+        bsg_render_config rcfg;
+        if (cfg) rcfg = *cfg; else bsg_default_render_config(&rcfg);
+        use_device(c);
+        bsg_camera cam{};
+        cam.fx = cam.fy = 1.0;
+        cam.R[0] = cam.R[4] = cam.R[8] = 1.0;
+        cam.width = width;
+        cam.height = height;
+        const DevCam dc = make_cam(cam);
+        const DevRender rc = make_render(rcfg);
+        const size_t px = static_cast<size_t>(width) * height;
+        ensure_image_buffers(c, dc.W, dc.H);
+        const float* gtd = upload_gt_f64(c, gt, px);
+        {
+            std::vector<float> r(3 * px);
+            for (size_t i = 0; i < 3 * px; ++i) r[i] = static_cast<float>(rendered[i]);
+            BSG_CUDA(cudaMemcpyAsync(c->out_rgb, r.data(), r.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+            BSG_CUDA(cudaMemsetAsync(c->scalars, 0, sizeof(StepScalars), c->stream));
+            launch_loss(c, dc, rc, gtd);
+            ensure_views_buffers(c, 1);
+            launch_finalize_loss(c, dc, rc, c->losses_dev, false);
+            std::vector<float> g(3 * px);
+            double l3[3];
+            BSG_CUDA(cudaMemcpyAsync(g.data(), c->dl_dc, g.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+            BSG_CUDA(cudaMemcpyAsync(l3, c->losses_dev, sizeof(l3), cudaMemcpyDeviceToHost, c->stream));
+            BSG_CUDA(cudaStreamSynchronize(c->stream));
+            if (out_loss3) for (int k = 0; k < 3; ++k) out_loss3[k] = l3[k];
+            if (out_dl_dc) for (size_t i = 0; i < 3 * px; ++i) out_dl_dc[i] = g[i];
+        }
     });
 }
 
@@ -1494,6 +1534,10 @@ int bsg_consensus_round_async(bsg_ctx* h, const bsg_round_args* a, const bsg_ada
         BSG_CUDA(cudaEventRecord(c->round_t1, c->stream));
         BSG_CUDA(cudaMemcpyAsync(c->round_host, c->round_scalars, 8 * sizeof(double), cudaMemcpyDeviceToHost,
                                  c->stream));
+        // rho (adapted on the device or not) rides in the same pinned block, so
+        // the wait never touches the compute stream
+        BSG_CUDA(cudaMemcpyAsync(c->round_host + 8, c->rho_state, 5 * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c->stream));
         BSG_CUDA(cudaEventRecord(c->round_done, c->stream));
         c->round_pending = true;
         c->round_diag = a->diagnostics != 0;
@@ -1508,8 +1552,7 @@ int bsg_consensus_wait(bsg_ctx* h, bsg_round_result* out, bsg_penalties* rho_out
         use_device(c);
         BSG_CUDA(cudaEventSynchronize(c->round_done));
         c->round_pending = false;
-        double rs[5];
-        BSG_CUDA(cudaMemcpyAsync(rs, c->rho_state, sizeof(rs), cudaMemcpyDeviceToHost, c->stream));
+        const double* rs = c->round_host + 8;
         c->rho = bsg_penalties{rs[0], rs[1], rs[2], rs[3], rs[4]};
         if (rho_out) *rho_out = c->rho;
         float ms = 0;
@@ -1637,6 +1680,123 @@ int bsg_step_counters(bsg_ctx* h, uint64_t* visible, uint64_t* pairs, uint64_t* 
 }
 
 uint64_t bsg_step_blend_evals(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->last_evals : 0; }
+
+// ---- master-round ownership bookkeeping (owners.cu) ----------------------
+
+int bsg_owners_create(int device, size_t n, const uint64_t* ids, const uint32_t* masks, uint32_t blocks,
+                      bsg_owner_table** out) {
+    return guarded([&] {
+        if (!out || (n && (!ids || !masks))) invalid("null argument");
+        if (blocks == 0 || blocks > 32) invalid("owner table: 1..32 blocks");
+        for (size_t i = 0; i < n; ++i) {
+            if (i && ids[i] <= ids[i - 1]) invalid("owner table ids must be strictly ascending");
+            if (__builtin_popcount(masks[i]) < 2 || (blocks < 32 && (masks[i] >> blocks)))
+                invalid("owner table rows need >= 2 owners among the blocks");
+        }
+        auto* t = new OwnerTable;
+        t->device = device;
+        t->blocks = blocks;
+        try {
+            BSG_CUDA(cudaSetDevice(device));
+            BSG_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+            BSG_CUDA(cudaMalloc(&t->totals_dev, 2 * sizeof(uint32_t)));
+            BSG_CUDA(cudaMallocHost(&t->totals_host, 2 * sizeof(uint32_t)));
+            owners_alloc(t, n);
+            if (n) {
+                BSG_CUDA(cudaMemcpyAsync(t->ids[0], ids, n * sizeof(uint64_t), cudaMemcpyHostToDevice, t->stream));
+                BSG_CUDA(cudaMemcpyAsync(t->mask[0], masks, n * sizeof(uint32_t), cudaMemcpyHostToDevice, t->stream));
+            }
+            BSG_CUDA(cudaStreamSynchronize(t->stream));
+            t->n = static_cast<uint32_t>(n);
+        } catch (...) {
+            bsg_owners_destroy(reinterpret_cast<bsg_owner_table*>(t));
+            throw;
+        }
+        *out = reinterpret_cast<bsg_owner_table*>(t);
+    });
+}
+
+int bsg_owners_destroy(bsg_owner_table* h) {
+    auto* t = reinterpret_cast<OwnerTable*>(h);
+    if (!t) return BSG_OK;
+    cudaSetDevice(t->device);
+    void* dev[] = {t->ids[0], t->ids[1], t->mask[0], t->mask[1], t->rm, t->chunk, t->totals_dev, t->t_slot,
+                   t->t_class, t->t_mask, t->in_ids, t->in_blk, t->in_found};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    if (t->totals_host) cudaFreeHost(t->totals_host);
+    if (t->stream) cudaStreamDestroy(t->stream);
+    delete t;
+    return BSG_OK;
+}
+
+size_t bsg_owners_size(const bsg_owner_table* h) { return h ? reinterpret_cast<const OwnerTable*>(h)->n : 0; }
+
+int bsg_owners_download(const bsg_owner_table* h, uint64_t* ids, uint32_t* masks) {
+    return guarded([&] {
+        const auto* t = reinterpret_cast<const OwnerTable*>(h);
+        if (!t) invalid("null owner table");
+        BSG_CUDA(cudaSetDevice(t->device));
+        if (t->n && ids)
+            BSG_CUDA(cudaMemcpyAsync(ids, t->ids[t->cur], t->n * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->stream));
+        if (t->n && masks)
+            BSG_CUDA(cudaMemcpyAsync(masks, t->mask[t->cur], t->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, t->stream));
+        BSG_CUDA(cudaStreamSynchronize(t->stream));
+    });
+}
+
+int bsg_owners_remove(bsg_owner_table* h, const uint64_t* const* removed, const size_t* n_removed, uint32_t* out_slot,
+                      uint8_t* out_class, uint32_t* out_mask, size_t cap, size_t* out_touched, uint8_t* out_found) {
+    return guarded([&] {
+        auto* t = reinterpret_cast<OwnerTable*>(h);
+        if (!t || !n_removed || !out_touched) invalid("null argument");
+        BSG_CUDA(cudaSetDevice(t->device));
+        std::vector<uint64_t> ids;
+        std::vector<uint32_t> blk;
+        for (uint32_t b = 0; b < t->blocks; ++b) {
+            if (n_removed[b] && (!removed || !removed[b])) invalid("null removed list");
+            for (size_t i = 0; i < n_removed[b]; ++i) {
+                ids.push_back(removed[b][i]);
+                blk.push_back(b);
+            }
+        }
+        const size_t m = ids.size();
+        if (m > t->in_cap) {
+            for (void* p : {static_cast<void*>(t->in_ids), static_cast<void*>(t->in_blk), static_cast<void*>(t->in_found)})
+                if (p) cudaFree(p);
+            t->in_cap = std::max<size_t>(m, 1024);
+            BSG_CUDA(cudaMalloc(&t->in_ids, t->in_cap * sizeof(uint64_t)));
+            BSG_CUDA(cudaMalloc(&t->in_blk, t->in_cap * sizeof(uint32_t)));
+            BSG_CUDA(cudaMalloc(&t->in_found, t->in_cap));
+        }
+        if (m) {
+            BSG_CUDA(cudaMemcpyAsync(t->in_ids, ids.data(), m * sizeof(uint64_t), cudaMemcpyHostToDevice, t->stream));
+            BSG_CUDA(cudaMemcpyAsync(t->in_blk, blk.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice, t->stream));
+        }
+        // the removals are marked first; the capacity check happens before the
+        // compaction commits, so a too-small output leaves the table unchanged
+        const uint32_t n_before = t->n;
+        const int cur_before = t->cur;
+        const uint32_t touched = owners_round(t, t->in_ids, t->in_blk, static_cast<uint32_t>(m), t->in_found);
+        *out_touched = touched;
+        if (touched > cap) {
+            // undo: the compaction swapped buffers; restore the pre-round table
+            // (the removal bits were cleared by the compaction, the masks of the
+            // old buffer are untouched)
+            t->cur = cur_before;
+            t->n = n_before;
+            throw Error{BSG_ERR_CAPACITY, "owner round: more touched slots than the output capacity"};
+        }
+        if (touched) {
+            if (!out_slot || !out_class || !out_mask) invalid("null output");
+            BSG_CUDA(cudaMemcpyAsync(out_slot, t->t_slot, touched * sizeof(uint32_t), cudaMemcpyDeviceToHost, t->stream));
+            BSG_CUDA(cudaMemcpyAsync(out_class, t->t_class, touched, cudaMemcpyDeviceToHost, t->stream));
+            BSG_CUDA(cudaMemcpyAsync(out_mask, t->t_mask, touched * sizeof(uint32_t), cudaMemcpyDeviceToHost, t->stream));
+        }
+        if (out_found && m) BSG_CUDA(cudaMemcpyAsync(out_found, t->in_found, m, cudaMemcpyDeviceToHost, t->stream));
+        BSG_CUDA(cudaStreamSynchronize(t->stream));
+    });
+}
 
 int bsg_last_binning(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->last_binning : -1; }
 

@@ -83,7 +83,9 @@ struct StepCounters {
 struct Mailbox {
     uint32_t seq_v, V, visible_pre, pad0;
     uint32_t seq_p, P, overflow, max_tile;  // max_tile: largest per-tile pair count (per-tile binning)
+    uint32_t pairs_big, pad1, pad2, pad3;   // the view's tile pairs reach kMaxPairs (32-bit offsets, 30-bit look-back counts)
 };
+constexpr unsigned long long kMaxPairs = 1ull << 30;
 
 // Per-tile binning sorts a tile's pairs by (FP64 depth bits, row) in shared
 // memory with a bitonic network; a view with a tile holding more pairs uses
@@ -120,6 +122,33 @@ enum Stage {
     kStPreprocess = 0, kStCompact, kStDepthSort, kStPairs, kStTileSort, kStRanges, kStBlendFwd, kStLoss,
     kStBlendBwd, kStFold, kStAdam, kStCount
 };
+
+// Device owner table of the master round (owners.cu): the
+// consensus slot table's ids (ascending) and owner bitmasks, ping-pong for
+// the compaction, plus the touched-slot outputs of the last round.
+struct OwnerTable {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t n = 0, blocks = 0;
+    size_t cap = 0;
+    int cur = 0;
+    uint64_t* ids[2] = {nullptr, nullptr};
+    uint32_t* mask[2] = {nullptr, nullptr};
+    uint32_t* rm = nullptr;      // this round's removal bits per slot (kept zero between rounds)
+    uint2* chunk = nullptr;      // per-chunk (kept, touched) counts -> offsets
+    uint32_t* totals_dev = nullptr;
+    uint32_t* totals_host = nullptr;  // pinned
+    size_t t_cap = 0;
+    uint32_t* t_slot = nullptr;  // touched slots (pre-compaction numbering), ascending
+    uint8_t* t_class = nullptr;  // 1 reset, 2 unshared, 3 dead
+    uint32_t* t_mask = nullptr;  // owner mask after the round
+    size_t in_cap = 0;
+    uint64_t* in_ids = nullptr;  // removed ids of the round (all blocks)
+    uint32_t* in_blk = nullptr;
+    uint8_t* in_found = nullptr;
+};
+void owners_alloc(OwnerTable* t, size_t n);
+uint32_t owners_round(OwnerTable* t, const uint64_t* d_in_ids, const uint32_t* d_in_blk, uint32_t m, uint8_t* d_found);
 
 struct Ctx {
     int device = 0;

@@ -151,7 +151,11 @@ void maybe_densify(Ctx* c) {
     if (it % d.interval != 0 || it > d.stop_iteration) return;  // trainer.cpp:303-304
     const uint32_t n = static_cast<uint32_t>(c->n);
     if (n == 0) return;
-    if (c->round_pending) throw Error{BSG_ERR_STATE, "densification while a consensus round is pending"};
+    // an asynchronous round still in flight (bsg_consensus_round_async, then
+    // bsg_train_steps across a densification iteration): densification
+    // rewrites the anchor / dual rows the round writes, so it waits for the
+    // round here; the round's result stays pending for bsg_consensus_wait
+    if (c->round_pending) BSG_CUDA(cudaEventSynchronize(c->round_done));
     DensifyParams p;
     p.grad_threshold = d.grad_threshold;
     p.prune_opacity = d.prune_opacity;

@@ -97,6 +97,7 @@ __global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restr
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_bucket[1024];
     __shared__ uint32_t s_max;
+    __shared__ unsigned long long s_total;  // P without 32-bit wrap-around (the capacity guard)
     const uint32_t t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     const uint32_t per = (ntiles + 1023) / 1024;  // consecutive tiles per thread
@@ -108,7 +109,10 @@ __global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restr
         mx = max(mx, v);
     }
     s_bucket[t] = 0;
-    if (t == 0) s_max = 0;
+    if (t == 0) {
+        s_max = 0;
+        s_total = 0;
+    }
     // block exclusive scan of the per-thread sums
     uint32_t inc = sum;
 #pragma unroll
@@ -121,6 +125,11 @@ __global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restr
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
     if (lane == 0) atomicMax(&s_max, mx);
+    {
+        unsigned long long wide = 0;
+        for (uint32_t i = b0; i < b1; ++i) wide += cnt[i];
+        if (wide) atomicAdd(&s_total, wide);
+    }
     if (warp == 0) {
         const uint32_t w = s_warp[lane];
         uint32_t wi = w;
@@ -172,6 +181,7 @@ __global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restr
         *pairs_dev = run;
         *reinterpret_cast<volatile uint32_t*>(&mb->P) = run;
         *reinterpret_cast<volatile uint32_t*>(&mb->max_tile) = s_max;
+        *reinterpret_cast<volatile uint32_t*>(&mb->pairs_big) = s_total >= kMaxPairs ? 1u : 0u;
         __threadfence_system();
         *reinterpret_cast<volatile uint32_t*>(&mb->seq_p) = seq;
     }
@@ -197,6 +207,8 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
             }
     }
 }
+
+constexpr int kTieRounds = 32;  // odd-even rounds before the full-key re-sort (runs can be ~2048 long)
 
 // One CTA per tile: the tile's rows sorted by (FP64 depth bits, row) with a
 // bitonic network in shared memory (size: the next power of two of the
@@ -256,8 +268,11 @@ __global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict_
     }
     __syncthreads();
     // runs of equal upper depth bits (depths within ~1e-6 relative): odd-even
-    // transposition by (full FP64 depth, row) until a round swaps nothing
-    for (;;) {
+    // transposition by (full FP64 depth, row) until a round swaps nothing --
+    // at most kTieRounds rounds (short runs, the common case); a tile whose
+    // runs are longer is re-sorted by the full key below
+    bool sorted = false;
+    for (int round = 0; round < kTieRounds; ++round) {
         bool swapped = false;
         for (uint32_t parity = 0; parity < 2; ++parity) {
             for (uint32_t i = 2 * threadIdx.x + parity; i + 1 < n; i += 2 * blockDim.x) {
@@ -273,7 +288,43 @@ __global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict_
             }
             __syncthreads();
         }
-        if (!__syncthreads_or(swapped)) break;
+        if (!__syncthreads_or(swapped)) {
+            sorted = true;
+            break;
+        }
+    }
+    if (!sorted) {
+        // long runs of near-equal depths: one bitonic network over the full
+        // (FP64 depth bits, row) key, rows alongside (the shared memory holds
+        // kTileSortCap x 12 B)
+        uint32_t* srow = reinterpret_cast<uint32_t*>(sk + N);
+        for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+            const uint32_t row = i < n ? static_cast<uint32_t>(sk[i]) : 0xffffffffu;
+            srow[i] = row;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) sk[i] = i < n ? depth_key[srow[i]] : ~0ull;
+        __syncthreads();
+        for (uint32_t k = 2; k <= N; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                    const uint32_t a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+                    const uint32_t b = a | j;
+                    const bool up = (a & k) == 0;
+                    const uint64_t ka = sk[a], kb = sk[b];
+                    const uint32_t ra = srow[a], rb = srow[b];
+                    if ((ka > kb || (ka == kb && ra > rb)) == up) {
+                        sk[a] = kb;
+                        sk[b] = ka;
+                        srow[a] = rb;
+                        srow[b] = ra;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rows_out[r.x + i] = srow[i];
+        return;
     }
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rows_out[r.x + i] = static_cast<uint32_t>(sk[i]);
 }
@@ -764,7 +815,7 @@ void launch_tile_sort(Ctx* c, const DevCam& cam, uint32_t max_tile) {
     const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
     uint32_t N = 2;
     while (N < max_tile) N <<= 1;
-    const size_t smem = N * sizeof(uint64_t);
+    const size_t smem = N * (sizeof(uint64_t) + sizeof(uint32_t));  // packed keys (+ rows for the full-key re-sort)
     static bool attr_set[64] = {};
     if (!attr_set[c->device]) {
         BSG_CUDA(cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

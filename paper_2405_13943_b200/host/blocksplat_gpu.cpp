@@ -140,6 +140,22 @@ uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {
     return v % n;
 }
 
+// trainer.cpp:250-252: a fresh Fisher-Yates shuffle of the view order at the
+// start of every pass, then the views in that order.
+void draw_views(std::mt19937_64& g, std::vector<size_t>& order, size_t& cursor, uint32_t* seq, uint64_t n) {
+    for (uint64_t s = 0; s < n; ++s) {
+        if (cursor == 0)
+            for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[uniform_index(g, i)]);
+        seq[s] = static_cast<uint32_t>(order[cursor]);
+        cursor = (cursor + 1) % order.size();
+    }
+}
+
+// derive_seed (trainer.cpp:116-118)
+uint64_t derive_seed(uint64_t seed, uint32_t block_id) {
+    return seed ^ (0x9e3779b97f4a7c15ull * (static_cast<uint64_t>(block_id) + 1));
+}
+
 Mat3 quat_to_rotation(const Vec4& q) {  // math.hpp:37-44
     const double w = q[0], x = q[1], y = q[2], z = q[3];
     return {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
@@ -372,7 +388,7 @@ BlockTrainer::BlockTrainer(uint32_t block_id, GaussianCloud initial, std::vector
     tc.densify.global_initial_count = global_initial_count;
     check(bsg_trainer_init(ctx_, &tc));
     // trainer.cpp:116-118,135-159
-    rng_ = new std::mt19937_64(cfg_.seed ^ (0x9e3779b97f4a7c15ull * (static_cast<uint64_t>(block_id) + 1)));
+    rng_ = new std::mt19937_64(derive_seed(cfg_.seed, block_id));
     view_order_.resize(views_.size());
     for (size_t i = 0; i < view_order_.size(); ++i) view_order_[i] = i;
     for (uint64_t id : shared_ids_)
@@ -406,12 +422,7 @@ void BlockTrainer::run_iterations(uint64_t n) {
     if (n == 0) return;
     auto& g = *static_cast<std::mt19937_64*>(rng_);
     std::vector<uint32_t> seq(n);
-    for (uint64_t s = 0; s < n; ++s) {  // trainer.cpp:250-252
-        if (view_cursor_ == 0)
-            for (size_t i = view_order_.size(); i > 1; --i) std::swap(view_order_[i - 1], view_order_[uniform_index(g, i)]);
-        seq[s] = static_cast<uint32_t>(view_order_[view_cursor_]);
-        view_cursor_ = (view_cursor_ + 1) % view_order_.size();
-    }
+    draw_views(g, view_order_, view_cursor_, seq.data(), n);
     const uint64_t it0 = bsg_iteration(ctx_);
     std::vector<double> losses(n);
     check(bsg_train_steps(ctx_, n, seq.data(), losses.data()));
@@ -614,6 +625,17 @@ ClusterPlan plan_cluster(const GaussianCloud& init, const std::vector<CameraView
         if (s.views.empty()) throw std::runtime_error("block " + std::to_string(b) + " has no training views");
     }
     return plan;
+}
+
+std::vector<uint32_t> view_sequence(uint64_t seed, uint32_t block_id, size_t n_views, size_t n_steps) {
+    if (n_views == 0) throw InvalidArgument("block has no training views");  // trainer.cpp:147
+    std::mt19937_64 g(derive_seed(seed, block_id));
+    std::vector<size_t> order(n_views);
+    for (size_t i = 0; i < n_views; ++i) order[i] = i;
+    size_t cursor = 0;
+    std::vector<uint32_t> seq(n_steps);
+    draw_views(g, order, cursor, seq.data(), n_steps);
+    return seq;
 }
 
 RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, const SessionOptions& opt,

@@ -54,6 +54,21 @@ extern "C" {
 
 const char* bsg_driver_last_error(void) { return g_drv_err.c_str(); }
 
+int bsg_view_sequence(uint64_t seed, uint32_t block_id, size_t n_views, size_t n_steps, uint32_t* out) {
+    try {
+        if (!out && n_steps) throw blocksplat::InvalidArgument("null output");
+        const std::vector<uint32_t> seq = blocksplat::view_sequence(seed, block_id, n_views, n_steps);
+        std::copy(seq.begin(), seq.end(), out);
+        return BSG_OK;
+    } catch (const blocksplat::InvalidArgument& e) {
+        g_drv_err = e.what();
+        return BSG_ERR_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_drv_err = e.what();
+        return BSG_ERR_STATE;
+    }
+}
+
 int bsg_run_simulated(int fd, size_t n, const uint64_t* ids, const double* pos, const double* rot, const double* ls,
                       const double* feat, const double* op, size_t n_views, const bsg_camera* cams,
                       const double* const* gts, const bsg_trainer_config* tc, const bsg_session_options* so,

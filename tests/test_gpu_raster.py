@@ -224,37 +224,44 @@ def test_zero_gradients_at_ground_truth():
 
 
 def test_fd_gradients_through_device():
-    """acceptance_main.cpp:67-129 subset: device analytic gradients vs central
-    differences of the oracle's FP64 loss (the device is FP32, so the bar is
-    the reference's 1e-3 relative with a 1e-4 absolute floor)."""
+    """Acceptance criterion 1 (acceptance_main.cpp:67-129) through the device,
+    at the reference's own bar: all 50 seeds (1000-1049), every parameter of
+    every Gaussian, the device's FP32 analytic gradient against FP64 central
+    differences of the oracle's loss, passing when err <= 1e-6 or rel <= 1e-3
+    at h = 1e-5, re-probed at 1e-6 and 1e-7 (acceptance_main.cpp:101) --
+    zero failures. The cloud is FP32-rounded so both sides see the same point.
+    The camera position is Vec3(rng, rng, 5.5) drawn right to left (GCC's
+    argument order, see refcases)."""
     from refcases import grad_check_cloud
-    failed = 0
-    checked = 0
-    for s in range(3):
+    failed, checked = [], 0
+    for s in range(50):
         rng = orc.Rng(1000 + s)
         c = grad_check_cloud(rng).narrowed()
-        ey = rng.uniform_range(-0.5, 0.5)
-        ex = rng.uniform_range(-0.5, 0.5)
-        cam = orc.look_at([ey, ex, 5.5], [0, 0, 0], [0, 1, 0], 14, 14, 8, 8, 16, 16)
+        cy = rng.uniform_range(-0.5, 0.5)
+        cx = rng.uniform_range(-0.5, 0.5)
+        cam = orc.look_at([cx, cy, 5.5], [0, 0, 0], [0, 1, 0], 14, 14, 8, 8, 16, 16)
         gt = np.array([rng.uniform() for _ in range(16 * 16 * 3)]).reshape(16, 16, 3)
         got = new_block(c).render_backward(dev_cam(cam), gt)
         for name, gname in (("pos", "g_pos"), ("rot", "g_rot"), ("ls", "g_ls"), ("feat", "g_feat"), ("op", "g_op")):
             arr = getattr(c, name)
             for idx in np.ndindex(arr.shape):
+                g = got[gname][idx]
                 ok = False
-                for h in (1e-5, 1e-6):
+                for h in (1e-5, 1e-6, 1e-7):
                     up, dn = c.copy(), c.copy()
                     getattr(up, name)[idx] += h
                     getattr(dn, name)[idx] -= h
                     fd = (orc.loss_value(orc.render(up.oracle(), cam, orc.RenderConfig())[0], gt, 0.2) -
                           orc.loss_value(orc.render(dn.oracle(), cam, orc.RenderConfig())[0], gt, 0.2)) / (2 * h)
-                    g = got[gname][idx]
-                    if abs(g - fd) <= 1e-4 or abs(g - fd) / max(abs(g), abs(fd)) <= 1e-2:
+                    err = abs(g - fd)
+                    if err <= 1e-6 or err / max(abs(g), abs(fd), 1e-300) <= 1e-3:
                         ok = True
                         break
                 checked += 1
-                failed += not ok
-    assert failed <= 0.01 * checked, (failed, checked)
+                if not ok:
+                    failed.append((s, name, idx, g, fd))
+    assert checked == 50 * 8 * 14
+    assert not failed, failed[:10]
 
 
 def test_equal_depth_runs_keep_index_order():
@@ -271,9 +278,24 @@ def test_equal_depth_runs_keep_index_order():
                      (0.1, 0.2, 0.5), 0.5, -3.0)
         c = cloud_from_rows(rows).narrowed()
         cam = axis_camera(100, 32, 64)
-        got = new_block(c).project(dev_cam(cam))
+        b = new_block(c)
+        got = b.project(dev_cam(cam))
         want = orc.project(c.oracle(), cam, orc.RenderConfig())
         assert np.array_equal(got["order"], want["order"])
+        _per_tile_pairs_match(b, want, cam)
+
+
+def _per_tile_pairs_match(b, want, cam):
+    """The render's per-tile path (upper-32-bit bitonic sort + bounded tie
+    fix-up + full-key re-sort of long runs) on the same cloud: tile keys and
+    rows bit-exact against the reference bins re-expressed as tiles."""
+    ek, er = expected_pairs(want, cam.width, cam.height)
+    assert np.bincount(ek).max() <= 2048  # every tile fits the per-tile sort
+    b.render(dev_cam(cam))
+    assert b.last_binning() == "tile"
+    tile, row = b.tile_pairs()
+    assert np.array_equal(tile.astype(np.int64), ek)
+    assert np.array_equal(row.astype(np.int64), er)
 
 
 def plane_cluster_cloud(n, half_width, depth_spread, seed):
@@ -301,12 +323,14 @@ def test_depth_key_collisions_match_reference_order(n, spread):
     through the tie fix-up, longer out-of-order runs through the full 64-bit
     fall-back; both must reproduce renderer.cpp:86-89 bit-exactly."""
     cloud, cam = plane_cluster_cloud(n, 1.5, spread, 3)
-    got = new_block(cloud).project(dev_cam(cam))
+    b = new_block(cloud)
+    got = b.project(dev_cam(cam))
     want = orc.project(cloud.oracle(), cam, orc.RenderConfig())
     vis = want["visible"].astype(bool)
     assert vis.sum() > 0.9 * n
     assert np.array_equal(got["visible"], want["visible"])
     assert np.array_equal(got["order"], want["order"])
+    _per_tile_pairs_match(b, want, cam)
 
 
 def with_sh1(hc, seed, amp=0.5):
@@ -364,3 +388,25 @@ def test_sh1_render_and_gradients(name, cloud, cam):
     for k, e in errs.items():
         assert e <= 2e-3, (k, e)
     assert g["g_feat"].shape[1] == 12 and np.abs(w["g_feat"][:, 3:]).max() > 0
+
+
+@pytest.mark.parametrize("w,h,seed", [(16, 16, 1), (64, 48, 2), (256, 192, 3), (1024, 768, 4), (8, 12, 5)])
+def test_image_loss_gradient_matches_ssim_with_gradient(w, h, seed):
+    """dL/dC of the step (renderer.cpp:259-272) from the device's SSIM kernels
+    against the FP64 oracle's ssim_with_gradient (ssim.cpp:138-185) on the
+    same FP32-representable images: SSIM within 1e-6 absolute (the
+    test_ssim.cpp gate), the loss within 1e-6 relative, and every dL/dC
+    element within 1e-6 of the largest element (FP32 window sums; the L1 term
+    is exact). Below 11x11 pixels SSIM = 1 with zero gradient (ssim.cpp:12-14)."""
+    g = np.random.default_rng(seed)
+    x = g.uniform(0, 1, (h, w, 3)).astype(np.float32).astype(np.float64)
+    y = np.clip(x + 0.2 * g.standard_normal(x.shape), 0, 1).astype(np.float32).astype(np.float64)
+    b = new_block(empty_cloud())
+    l3, got = b.image_loss(x, y)
+    s, ds = orc.ssim_with_gradient(x, y)
+    want = np.sign(x - y) / (3.0 * w * h) - 0.2 * ds
+    assert abs(l3[2] - s) <= 1e-6
+    assert l3[0] == pytest.approx(orc.loss_value(x, y, 0.2), rel=1e-6)
+    assert np.abs(got - want).max() <= 1e-6 * np.abs(want).max()
+    if w < 11 or h < 11:
+        assert s == 1.0 and not np.any(ds)

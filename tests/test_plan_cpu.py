@@ -92,3 +92,35 @@ def test_planner_matches_oracle_plan():
         rows, slots, first = p.block_shared(b)
         sids, _, _ = p.shared()
         assert list(sids[slots]) == plan.shard_shared(b)
+
+
+@pytest.mark.parametrize("seed,block,n_views,steps", [(1, 0, 6, 20), (7, 3, 28, 100), (42, 1, 1, 5),
+                                                      (123456789, 7, 64, 300), (0, 31, 96, 200)])
+def test_host_trainer_view_order_matches_reference(seed, block, n_views, steps):
+    """S20 (trainer.cpp:116-118,250-252): the C++ host BlockTrainer's view
+    order (bsg_view_sequence runs the trainer's own draw_views) against the
+    oracle's Rng::shuffle restatement, and that against the oracle
+    BlockTrainer's actual train_step draws."""
+    got = list(api.view_sequence(seed, block, n_views, steps))
+    assert got == list(orc.view_sequence(seed, block, n_views, steps))
+
+
+def test_oracle_trainer_draws_the_restated_sequence():
+    sc = orc.SynthConfig()
+    sc.seed, sc.gaussians, sc.cameras, sc.image_size, sc.extent = 3, 30, 5, 16, 4.0
+    s = orc.generate_scene(sc)
+    p, c = s.points()
+    init = orc.init_cloud_from_points(p, c, 0, 0.1)
+    tc = orc.TrainerConfig()
+    tc.iterations, tc.seed = 20, 11
+    tc.densify_enabled = False
+    t = orc.BlockTrainer(2, init, s.views, s.images(), [], init.size(), tc)
+    seq = list(api.view_sequence(11, 2, len(s.views), 12))
+    for k in range(12):
+        t.train_step()
+        assert t.last_view() == seq[k]
+
+
+def test_view_sequence_rejects_empty_views():
+    with pytest.raises(api.InvalidArgument):
+        api.view_sequence(1, 0, 0, 3)
