@@ -258,6 +258,25 @@ typedef struct bsg_adapt_args {
     uint64_t iteration;
 } bsg_adapt_args;
 
+/* One process driving k contexts on k distinct devices (run_simulated with
+ * one GPU per block): one NCCL communicator per context, initialised as a
+ * group (ncclGroupStart / CommInitRank x k / GroupEnd); rank = position. */
+int bsg_comm_init_local(bsg_ctx* const* ctxs, size_t k);
+/* Host communicator: the round's all-reduces go through pinned host memory
+ * and fn (in place on buf: count elements, dtype 0 = f32 / 1 = f64, op 0 =
+ * sum / 1 = max; nonzero return = failure -> BSG_ERR_NCCL). For ranks that
+ * cannot share an NCCL communicator (several blocks on one GPU, the
+ * in-process threaded driver; processes joined by another transport, e.g. a
+ * gloo group in tests). A round on a host communicator blocks its caller
+ * until the reductions are done; the unpack still runs on the comm stream. */
+typedef int (*bsg_host_allreduce)(void* user, void* buf, size_t count, int dtype, int op);
+int bsg_comm_init_host(bsg_ctx* ctx, bsg_host_allreduce fn, void* user, int nranks, int rank);
+/* Round watchdog: bsg_consensus_wait gives up after `seconds` (0 = never,
+ * the default) and checks the NCCL communicator for asynchronous errors while
+ * it waits; either aborts the communicator and returns BSG_ERR_NCCL (the
+ * reference's per-message timeouts, runtime.cpp:44-53,98-119). */
+int bsg_set_round_timeout(bsg_ctx* ctx, double seconds);
+
 /* Asynchronous round (the overlap of SURVEY §8(e)): enqueued on the block's
  * communication stream behind the last parameter update, returns at once.
  * The next bsg_train_steps runs projection, sorting, both blends and the fold

@@ -150,6 +150,9 @@ SYMBOLS = [
     ("bsg_apply_broadcast", ctypes.c_int, [_P, _DP, _SZ, _U32P, ctypes.c_double, ctypes.c_int]),
     ("bsg_nccl_unique_id", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
     ("bsg_comm_init", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int]),
+    ("bsg_comm_init_local", ctypes.c_int, [ctypes.POINTER(_P), _SZ]),
+    ("bsg_comm_init_host", ctypes.c_int, [_P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    ("bsg_set_round_timeout", ctypes.c_int, [_P, ctypes.c_double]),
     ("bsg_consensus_round", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_round_result)]),
     ("bsg_consensus_round_async", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_args), ctypes.POINTER(bsg_adapt_args)]),
     ("bsg_consensus_wait", ctypes.c_int, [_P, ctypes.POINTER(bsg_round_result), ctypes.POINTER(bsg_penalties)]),
@@ -190,6 +193,8 @@ SYMBOLS = [
 ]
 
 _lib = None
+HOST_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                  ctypes.c_int)
 
 
 def load_library(path=LIB_PATH):
@@ -517,6 +522,23 @@ class Block:
     def comm_init(self, uid, nranks, rank):
         buf = (ctypes.c_uint8 * 128)(*uid)
         _check(_lib.bsg_comm_init(self.h, buf, nranks, rank))
+
+    def comm_init_host(self, allreduce, nranks, rank):
+        """Host communicator (bsg_comm_init_host): allreduce(array, op) reduces
+        the numpy view of the staging buffer in place (op "sum" / "max")."""
+        def tramp(user, buf, count, dtype, op):
+            try:
+                ct = ctypes.c_double if dtype == 1 else ctypes.c_float
+                arr = np.ctypeslib.as_array((ct * count).from_address(buf))
+                allreduce(arr, "max" if op == 1 else "sum")
+                return 0
+            except Exception:
+                return 1
+        self._host_reduce = HOST_ALLREDUCE(tramp)  # kept alive with the block
+        _check(_lib.bsg_comm_init_host(self.h, ctypes.cast(self._host_reduce, ctypes.c_void_p), None, nranks, rank))
+
+    def set_round_timeout(self, seconds):
+        _check(_lib.bsg_set_round_timeout(self.h, float(seconds)))
 
     def consensus_round(self, alpha, relax, reset_slots=(), diagnostics=False):
         a = _round_args(alpha, relax, reset_slots, diagnostics)

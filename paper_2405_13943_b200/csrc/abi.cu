@@ -12,6 +12,9 @@
 
 #include "bsg_internal.cuh"
 
+#include <chrono>
+#include <thread>
+
 namespace bsg {
 
 namespace {
@@ -28,6 +31,10 @@ struct NcclApi {
                                cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    ncclResult_t (*comm_get_async_error)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*comm_abort)(ncclComm_t) = nullptr;
 };
 
 NcclApi& nccl_api() {
@@ -41,7 +48,12 @@ NcclApi& nccl_api() {
     api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy || !api.error_string)
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.comm_get_async_error = reinterpret_cast<decltype(api.comm_get_async_error)>(dlsym(h, "ncclCommGetAsyncError"));
+    api.comm_abort = reinterpret_cast<decltype(api.comm_abort)>(dlsym(h, "ncclCommAbort"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy || !api.error_string ||
+        !api.group_start || !api.group_end || !api.comm_get_async_error || !api.comm_abort)
         throw std::runtime_error("libnccl.so.2 lacks a required symbol");
     api.ready = true;
     return api;
@@ -93,6 +105,7 @@ void free_all(Ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->nccl) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl));
+    if (c->host_buf) cudaFreeHost(c->host_buf);
     for (cudaEvent_t e : {c->gt_ready, c->gt_ready_b, c->gt_free[0], c->gt_free[1]})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->x_ready, c->round_done, c->round_t0, c->round_t1})
@@ -521,6 +534,25 @@ void ensure_views_buffers(Ctx* c, size_t n) {
 
 // ---- consensus plumbing --------------------------------------------------
 void reduce_nccl(Ctx* c, void* buf, size_t count, ncclDataType_t type, ncclRedOp_t op) {
+    if (c->host_reduce) {
+        // host communicator (bsg_comm_init_host): the buffer goes through pinned
+        // host memory and the caller's all-reduce; the round blocks here
+        const size_t bytes = count * (type == ncclFloat64 ? 8 : 4);
+        if (bytes == 0) return;
+        if (bytes > c->host_buf_cap) {
+            if (c->host_buf) cudaFreeHost(c->host_buf);
+            c->host_buf = nullptr;
+            BSG_CUDA(cudaMallocHost(&c->host_buf, bytes));
+            c->host_buf_cap = bytes;
+        }
+        BSG_CUDA(cudaMemcpyAsync(c->host_buf, buf, bytes, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+        const int rc = c->host_reduce(c->host_user, c->host_buf, count, type == ncclFloat64 ? 1 : 0,
+                                      op == ncclMax ? 1 : 0);
+        if (rc != 0) throw Error{BSG_ERR_NCCL, "host all-reduce failed (" + std::to_string(rc) + ")"};
+        BSG_CUDA(cudaMemcpyAsync(buf, c->host_buf, bytes, cudaMemcpyHostToDevice, c->stream));
+        return;
+    }
     if (!c->nccl) return;
     NcclApi& n = nccl_api();
     const ncclResult_t r = n.all_reduce(buf, buf, count, type, op, static_cast<ncclComm_t>(c->nccl), c->stream);
@@ -1473,6 +1505,41 @@ int bsg_nccl_unique_id(uint8_t out_id[128]) {
     });
 }
 
+// Round watchdog (the reference's per-message timeouts,
+// runtime.cpp:44-53,98-119): poll the round's event; between polls check the
+// NCCL communicator for an asynchronous error, and give up after the round
+// timeout (0 = wait forever). Either failure aborts the communicator, so the
+// collective cannot hang the process, and surfaces as BSG_ERR_NCCL.
+void wait_round(Ctx* c) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t q = cudaEventQuery(c->round_done);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) BSG_CUDA(q);
+        if (c->nccl) {
+            NcclApi& napi = nccl_api();
+            ncclResult_t ae = ncclSuccess;
+            napi.comm_get_async_error(static_cast<ncclComm_t>(c->nccl), &ae);
+            if (ae != ncclSuccess && ae != ncclInProgress) {
+                napi.comm_abort(static_cast<ncclComm_t>(c->nccl));
+                c->nccl = nullptr;
+                c->round_pending = false;
+                throw Error{BSG_ERR_NCCL, std::string("consensus round: NCCL async error: ") + napi.error_string(ae)};
+            }
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (c->round_timeout > 0 && el > c->round_timeout) {
+            if (c->nccl) {
+                nccl_api().comm_abort(static_cast<ncclComm_t>(c->nccl));
+                c->nccl = nullptr;
+            }
+            c->round_pending = false;
+            throw Error{BSG_ERR_NCCL, "consensus round timed out after " + std::to_string(c->round_timeout) + " s"};
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
 int bsg_comm_init(bsg_ctx* h, const uint8_t id[128], int nranks, int rank) {
     return guarded([&] {
         auto* c = reinterpret_cast<Ctx*>(h);
@@ -1490,6 +1557,62 @@ int bsg_comm_init(bsg_ctx* h, const uint8_t id[128], int nranks, int rank) {
         const ncclResult_t r = napi.comm_init_rank(&comm, nranks, uid, rank);
         if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, std::string("ncclCommInitRank: ") + napi.error_string(r)};
         c->nccl = comm;
+    });
+}
+
+int bsg_comm_init_local(bsg_ctx* const* hs, size_t k) {
+    return guarded([&] {
+        if (!hs || k == 0) invalid("no contexts");
+        std::vector<Ctx*> cs(k);
+        for (size_t b = 0; b < k; ++b) {
+            cs[b] = reinterpret_cast<Ctx*>(hs[b]);
+            if (!cs[b]) invalid("null context");
+            for (size_t a = 0; a < b; ++a)
+                if (cs[a]->device == cs[b]->device) invalid("local NCCL group needs one device per context");
+        }
+        NcclApi& napi = nccl_api();
+        ncclUniqueId uid;
+        ncclResult_t r = napi.get_unique_id(&uid);
+        if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, std::string("ncclGetUniqueId: ") + napi.error_string(r)};
+        std::vector<ncclComm_t> comms(k);
+        // one process, k ranks: the inits must be grouped (each blocks until all ranks joined)
+        napi.group_start();
+        for (size_t b = 0; b < k; ++b) {
+            use_device(cs[b]);
+            r = napi.comm_init_rank(&comms[b], static_cast<int>(k), uid, static_cast<int>(b));
+            if (r != ncclSuccess) {
+                napi.group_end();
+                throw Error{BSG_ERR_NCCL, std::string("ncclCommInitRank: ") + napi.error_string(r)};
+            }
+        }
+        r = napi.group_end();
+        if (r != ncclSuccess) throw Error{BSG_ERR_NCCL, std::string("ncclGroupEnd: ") + napi.error_string(r)};
+        for (size_t b = 0; b < k; ++b) {
+            cs[b]->nccl = comms[b];
+            cs[b]->nranks = static_cast<int>(k);
+            cs[b]->rank = static_cast<int>(b);
+        }
+    });
+}
+
+int bsg_comm_init_host(bsg_ctx* h, bsg_host_allreduce fn, void* user, int nranks, int rank) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c || !fn) invalid("null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) invalid("bad rank layout");
+        c->host_reduce = fn;
+        c->host_user = user;
+        c->nranks = nranks;
+        c->rank = rank;
+    });
+}
+
+int bsg_set_round_timeout(bsg_ctx* h, double seconds) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (!(seconds >= 0)) invalid("negative timeout");
+        c->round_timeout = seconds;
     });
 }
 
@@ -1550,7 +1673,7 @@ int bsg_consensus_wait(bsg_ctx* h, bsg_round_result* out, bsg_penalties* rho_out
         if (!c) invalid("null context");
         if (!c->round_pending) throw Error{BSG_ERR_STATE, "no consensus round pending"};
         use_device(c);
-        BSG_CUDA(cudaEventSynchronize(c->round_done));
+        wait_round(c);
         c->round_pending = false;
         const double* rs = c->round_host + 8;
         c->rho = bsg_penalties{rs[0], rs[1], rs[2], rs[3], rs[4]};

@@ -276,6 +276,11 @@ struct Ctx {
     float* rho_dev = nullptr;      // per-component rho [kMaxD] read by the penalty + Adam
     double* rho_state = nullptr;   // rho_p, rho_q, rho_s, rho_f, rho_o (adapted on the device)
     void* nccl = nullptr;       // ncclComm_t
+    bsg_host_allreduce host_reduce = nullptr;  // host communicator (bsg_comm_init_host)
+    void* host_user = nullptr;
+    void* host_buf = nullptr;   // pinned staging of the host communicator
+    size_t host_buf_cap = 0;
+    double round_timeout = 0;   // seconds, 0 = none (bsg_set_round_timeout)
     int nranks = 1, rank = 0;
 
     // measurement

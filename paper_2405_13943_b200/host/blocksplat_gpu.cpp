@@ -5,6 +5,9 @@
 #include "../../include/blocksplat_gpu.hpp"
 
 #include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <condition_variable>
 #include <chrono>
 #include <cmath>
 #include <exception>
@@ -638,6 +641,98 @@ std::vector<uint32_t> view_sequence(uint64_t seed, uint32_t block_id, size_t n_v
     return seq;
 }
 
+namespace {
+
+// Generation barrier of the driver's threads; abort() releases every waiter
+// with an exception (a failing block must not leave the others blocked).
+class Barrier {
+public:
+    explicit Barrier(size_t n) : n_(n) {}
+    void wait() {
+        std::unique_lock<std::mutex> lk(m_);
+        if (aborted_) throw std::runtime_error("run aborted by another block");
+        const uint64_t gen = gen_;
+        if (++count_ == n_) {
+            count_ = 0;
+            ++gen_;
+            cv_.notify_all();
+            return;
+        }
+        cv_.wait(lk, [&] { return gen_ != gen || aborted_; });
+        if (gen_ == gen) throw std::runtime_error("run aborted by another block");
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(m_);
+        aborted_ = true;
+        cv_.notify_all();
+    }
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_;
+    size_t n_, count_ = 0;
+    uint64_t gen_ = 0;
+    bool aborted_ = false;
+};
+
+// In-process all-reduce among the K block threads (bsg_comm_init_host), for
+// blocks that share a GPU (an NCCL communicator needs one device per rank):
+// rank 0 reduces in ascending block order, every rank copies the result.
+class HostGroup {
+public:
+    explicit HostGroup(size_t k) : k_(k), bar_(k), bufs_(k, nullptr) {}
+    struct Member {
+        HostGroup* g;
+        size_t rank;
+    };
+    static int allreduce(void* user, void* buf, size_t count, int dtype, int op) {
+        auto* m = static_cast<Member*>(user);
+        try {
+            m->g->run(m->rank, buf, count, dtype, op);
+            return 0;
+        } catch (...) {
+            return 1;
+        }
+    }
+    void abort() { bar_.abort(); }
+
+private:
+    template <typename T>
+    void reduce(size_t count, int op) {
+        T* acc = static_cast<T*>(bufs_[0]);
+        for (size_t r = 1; r < k_; ++r) {
+            const T* src = static_cast<const T*>(bufs_[r]);
+            if (op == 1)
+                for (size_t i = 0; i < count; ++i) acc[i] = std::max(acc[i], src[i]);
+            else
+                for (size_t i = 0; i < count; ++i) acc[i] += src[i];
+        }
+    }
+    void run(size_t rank, void* buf, size_t count, int dtype, int op) {
+        bufs_[rank] = buf;
+        bar_.wait();
+        if (rank == 0) {
+            if (dtype == 1)
+                reduce<double>(count, op);
+            else
+                reduce<float>(count, op);
+        }
+        bar_.wait();
+        if (rank != 0) std::memcpy(buf, bufs_[0], count * (dtype == 1 ? 8 : 4));
+        bar_.wait();
+    }
+    size_t k_;
+    Barrier bar_;
+    std::vector<void*> bufs_;
+};
+
+struct OwnerTableHandle {
+    bsg_owner_table* t = nullptr;
+    ~OwnerTableHandle() { bsg_owners_destroy(t); }
+};
+
+}  // namespace
+
 RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, const SessionOptions& opt,
                         const std::function<void(const RoundDiagnostics&)>& observer,
                         const std::vector<int>& devices) {  // runtime.cpp:427-671
@@ -645,6 +740,7 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
     if (opt.total_iterations != trainer.iterations) throw InvalidArgument("session and trainer iteration counts differ");
     const auto K = static_cast<uint32_t>(plan.shards.size());
     if (K == 0) throw InvalidArgument("plan has no shards");
+    if (K > 32) throw InvalidArgument("at most 32 blocks (owner bitmasks)");
     if (devices.empty()) throw InvalidArgument("no devices");
     const int fd = plan.init_cloud.feature_dim(), D = 11 + fd;
     std::vector<BlockTrainer> tr;
@@ -654,10 +750,17 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
         tr.emplace_back(s.block_id, s.initial, s.views, s.shared_ids, s.global_initial_count, trainer,
                         devices[b % devices.size()]);
     }
-    // Global slots and the round-0 anchor (runtime.cpp:465-477, trainer.cpp:161-166).
+    // Global slots, their owners (the device owner table on block 0's GPU) and
+    // the round-0 anchor (runtime.cpp:465-477, trainer.cpp:161-166).
     std::vector<uint64_t> S = plan.shared_ids;  // the current consensus slot table (ascending ids)
-    std::map<uint64_t, std::vector<uint32_t>> owners = plan.owners;
-    std::set<uint64_t> global_ids(plan.init_cloud.ids.begin(), plan.init_cloud.ids.end());
+    std::vector<uint32_t> slot_cnt = plan.shared_owner_count, slot_first = plan.shared_first_owner;
+    OwnerTableHandle owners;
+    {
+        std::vector<uint32_t> masks(S.size(), 0);
+        for (size_t k = 0; k < S.size(); ++k)
+            for (uint32_t b : plan.owners.at(S[k])) masks[k] |= 1u << b;
+        check(bsg_owners_create(devices[0], S.size(), S.data(), masks.data(), K, &owners.t));
+    }
     const GaussianCloud z0 = slice_by_ids(plan.init_cloud, S);
     const std::vector<double> z0_rows = rows_of(z0, find_all(z0, S, "initial cloud ill-formed"));
     PropertyPenalties rho = opt.rho;
@@ -669,157 +772,271 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
         std::vector<double> zr(s.shared_ids.size() * D);
         for (size_t j = 0; j < s.shared_ids.size(); ++j) {
             slots[j] = static_cast<uint32_t>(std::lower_bound(S.begin(), S.end(), s.shared_ids[j]) - S.begin());
-            first[j] = plan.shared_first_owner[slots[j]] == b ? 1 : 0;
+            first[j] = slot_first[slots[j]] == b ? 1 : 0;
             std::copy(&z0_rows[slots[j] * D], &z0_rows[slots[j] * D] + D, &zr[j * D]);
         }
-        tr[b].bind_slots(slots, first, plan.shared_owner_count);
+        tr[b].bind_slots(slots, first, slot_cnt);
         // consensus disabled: blocks train independently (zero penalty), z is still reported
         const bsg_penalties p = to_dev(opt.consensus.enabled ? rho : zero_rho);
         check(bsg_set_anchor(tr[b].context(), zr.data(), z0_rows.data(), &p));
     }
     std::vector<bsg_ctx*> ctxs(K);
     for (uint32_t b = 0; b < K; ++b) ctxs[b] = tr[b].context();
+    // Communicators: one NCCL rank per GPU when every block has its own
+    // device (the 8xB200 layout), else the in-process host all-reduce.
+    bool distinct = K > 1;
+    for (uint32_t a = 0; a < K && distinct; ++a)
+        for (uint32_t b = 0; b < a; ++b)
+            if (devices[a % devices.size()] == devices[b % devices.size()]) distinct = false;
+    HostGroup hg(K);
+    std::vector<HostGroup::Member> members(K);
+    if (K > 1) {
+        if (distinct) {
+            check(bsg_comm_init_local(ctxs.data(), K));
+        } else {
+            for (uint32_t b = 0; b < K; ++b) {
+                members[b] = HostGroup::Member{&hg, b};
+                check(bsg_comm_init_host(ctxs[b], &HostGroup::allreduce, &members[b], static_cast<int>(K),
+                                         static_cast<int>(b)));
+            }
+        }
+    }
+    uint64_t global_count = plan.init_cloud.size();
+    std::vector<uint64_t> alloc_start(K), newest(K, UINT64_MAX);  // IdAllocator ranges (trainer.cpp:55-61)
+    for (uint32_t b = 0; b < K; ++b)
+        alloc_start[b] = (static_cast<uint64_t>(plan.shards[b].block_id) << 48) +
+                         (plan.shards[b].block_id == 0 ? plan.shards[b].global_initial_count : 0);
+    bool have_z = false;  // a round has produced z (else the slot rebind starts from z0)
+
+    // One host thread per block runs its iterations, reports its densify
+    // changes, and -- after the master's bookkeeping -- starts its consensus
+    // round asynchronously: the round's reductions and unpack run on the
+    // block's communication stream while the block's next iterations
+    // project, sort, blend and fold; only their first Adam waits for it
+    // (SURVEY §8(e)). The master (this thread) collects the rounds' results
+    // when the blocks wait for them at the next consensus point.
+    struct Report {
+        double loss = 0;
+        std::vector<uint64_t> removed, added;
+        bsg_round_result res{};
+        bsg_penalties rho{};
+    };
+    std::vector<Report> rep(K);
+    std::vector<std::vector<uint32_t>> resets(K);
+    std::vector<bsg_round_args> args(K);
+    bsg_adapt_args adapt{};
+    adapt.mu = opt.consensus.mu;
+    adapt.tau_inc = opt.consensus.tau_inc;
+    adapt.tau_dec = opt.consensus.tau_dec;
+    adapt.freeze_iteration = opt.consensus.freeze_iteration;
+    adapt.adaptive = opt.consensus.adaptive ? 1 : 0;
+    Barrier ready(K + 1), go(K + 1);
+    std::vector<std::exception_ptr> errs(K + 1);
+    auto fail_all = [&] {
+        ready.abort();
+        go.abort();
+        hg.abort();
+    };
+    const std::vector<uint64_t> schedule = consensus_schedule(opt.total_iterations, opt.consensus.interval);
+    std::vector<std::thread> workers;
+    for (uint32_t b = 0; b < K; ++b)
+        workers.emplace_back([&, b] {
+            try {
+                uint64_t done = 0;
+                bool pending = false;
+                for (size_t j = 0; j < schedule.size(); ++j) {
+                    tr[b].run_iterations(schedule[j] - done);
+                    done = schedule[j];
+                    Report& r = rep[b];
+                    if (pending) {
+                        check(bsg_consensus_wait(tr[b].context(), &r.res, &r.rho));
+                        pending = false;
+                    }
+                    r.loss = tr[b].last_loss();
+                    r.removed = tr[b].take_removed_ids();
+                    r.added = tr[b].take_new_rows().ids;
+                    ready.wait();  // master: ownership bookkeeping, slot rebinds
+                    go.wait();
+                    check(bsg_consensus_round_async(tr[b].context(), &args[b],
+                                                    opt.consensus.enabled ? &adapt : nullptr));
+                    pending = true;
+                }
+                if (pending) check(bsg_consensus_wait(tr[b].context(), &rep[b].res, &rep[b].rho));
+                ready.wait();
+            } catch (...) {
+                errs[b] = std::current_exception();
+                fail_all();
+            }
+        });
 
     RunResult result;
-    const std::vector<uint64_t> schedule = consensus_schedule(opt.total_iterations, opt.consensus.interval);
-    uint64_t done = 0;
-    for (uint64_t t : schedule) {
-        const bool final_round = t == opt.total_iterations;
-        // worker halves in parallel, one host thread per block (runtime.cpp:641-656)
-        std::vector<std::exception_ptr> errs(K);
-        std::vector<std::thread> th;
-        for (uint32_t b = 0; b < K; ++b)
-            th.emplace_back([&, b] {
-                try {
-                    tr[b].run_iterations(t - done);
-                } catch (...) {
-                    errs[b] = std::current_exception();
-                }
-            });
-        for (auto& x : th) x.join();
-        for (auto& e : errs)
-            if (e) std::rethrow_exception(e);
-        done = t;
-        // ownership changes from densification (runtime.cpp:490-518)
-        std::map<uint64_t, size_t> prev_owner_count;
-        for (uint32_t b = 0; b < K; ++b)
-            for (uint64_t id : tr[b].take_removed_ids()) {
-                auto it = owners.find(id);
-                if (it == owners.end()) continue;
-                prev_owner_count.emplace(id, it->second.size());
-                auto& list = it->second;
-                list.erase(std::remove(list.begin(), list.end(), b), list.end());
-            }
-        std::vector<uint64_t> reset_ids, dead_ids;
-        for (const auto& [id, prev] : prev_owner_count) {
-            const auto& list = owners.at(id);
-            if (list.empty())
-                dead_ids.push_back(id);
-            else if (prev >= 2 && list.size() >= 2)
-                reset_ids.push_back(id);  // (prev >= 2, now 1 owner: unshared, leaves the slot table)
-        }
-        for (uint64_t id : dead_ids) {
-            owners.erase(id);
-            global_ids.erase(id);
-        }
-        for (uint32_t b = 0; b < K; ++b)
-            for (uint64_t id : tr[b].take_new_rows().ids) {
-                owners[id] = {b};
-                global_ids.insert(id);
-            }
-        // The shared set only shrinks (new rows have one owner; removals drop
-        // owners), so it is S minus the ids that fell below two owners: a
-        // merge over S and the (sorted) changed ids instead of a scan of the
-        // whole owner map every round.
-        std::vector<uint64_t> lost;
-        for (const auto& [id, prev] : prev_owner_count) {
-            (void)prev;
-            auto it = owners.find(id);
-            if (it == owners.end() || it->second.size() < 2) lost.push_back(id);
-        }
-        std::vector<uint64_t> shared_now;
-        if (!lost.empty()) {
-            shared_now.reserve(S.size());
-            std::set_difference(S.begin(), S.end(), lost.begin(), lost.end(), std::back_inserter(shared_now));
-        }
-        if (!lost.empty() && shared_now.size() != S.size()) {
-            // new slot table; every block keeps its anchor / duals for the ids
-            // that stay shared, z_prev comes from the last consensus (all of
-            // shared_now was shared before: new rows start single-owner)
-            std::vector<double> zp_old(S.size() * D), zp_new(shared_now.size() * D);
-            if (!S.empty()) check(bsg_download_consensus(ctxs[0], zp_old.data()));
-            if (done == schedule.front()) std::copy(z0_rows.begin(), z0_rows.end(), zp_old.begin());
-            std::vector<uint32_t> cnt(shared_now.size()), first_owner(shared_now.size());
-            for (size_t k = 0; k < shared_now.size(); ++k) {
-                const size_t old = std::lower_bound(S.begin(), S.end(), shared_now[k]) - S.begin();
-                std::copy(&zp_old[old * D], &zp_old[old * D] + D, &zp_new[k * D]);
-                const auto& list = owners.at(shared_now[k]);
-                cnt[k] = static_cast<uint32_t>(list.size());
-                first_owner[k] = *std::min_element(list.begin(), list.end());
-            }
-            for (uint32_t b = 0; b < K; ++b) {
-                std::vector<uint64_t> keep;
-                std::vector<uint32_t> slots;
-                std::vector<uint8_t> first;
-                for (uint64_t id : tr[b].shared_ids()) {
-                    auto it = std::lower_bound(shared_now.begin(), shared_now.end(), id);
-                    if (it == shared_now.end() || *it != id) continue;
-                    keep.push_back(id);
-                    slots.push_back(static_cast<uint32_t>(it - shared_now.begin()));
-                    first.push_back(first_owner[slots.back()] == b ? 1 : 0);
-                }
-                tr[b].rebind_slots(keep, slots, first, cnt, zp_new, opt.consensus.enabled ? rho : zero_rho);
-                ctxs[b] = tr[b].context();
-            }
-            S = shared_now;
-        }
-        std::vector<uint32_t> reset_slots;
-        for (uint64_t id : reset_ids) {
-            auto it = std::lower_bound(S.begin(), S.end(), id);
-            if (it != S.end() && *it == id) reset_slots.push_back(static_cast<uint32_t>(it - S.begin()));
-        }
-        // consensus round on the device (runtime.cpp:529-548, trainer.cpp:168-223)
-        bsg_round_args args{};
-        args.alpha = opt.consensus.alpha;
-        args.relax = opt.consensus.enabled && opt.consensus.alpha != 1.0 && !final_round;
-        args.diagnostics = 1;
-        args.n_reset = reset_slots.size();
-        args.reset_slots = reset_slots.empty() ? nullptr : reset_slots.data();
-        bsg_round_result r{};
-        const auto r0 = std::chrono::steady_clock::now();
-        check(bsg_group_consensus_round(ctxs.data(), K, &args, &r));
-        const double round_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
-        if (opt.consensus.enabled) {
-            rho = adapt_penalties(rho, r.primal, r.dual, opt.consensus, t);
-            const bsg_penalties p = to_dev(rho);
-            for (auto* c : ctxs) check(bsg_set_penalties(c, &p));
-        }
-        RoundDiagnostics d;
-        d.iteration = t;
+    RoundDiagnostics pending_diag;
+    auto emit = [&](RoundDiagnostics d) {  // the round's device results, collected by the blocks' waits
+        const bsg_round_result& r = rep[0].res;
         d.primal_residual = r.primal;
         d.dual_residual = r.dual;
-        d.rho = rho;
         d.max_disagreement = r.max_disagreement;
         d.dual_mean_linf = r.dual_mean_linf;
-        for (auto& x : tr) d.mean_loss += x.last_loss();
-        d.mean_loss /= K;
-        d.shared_count = S.size();
-        d.global_count = global_ids.size();
-        d.consensus_ms = round_ms;
+        d.consensus_ms = r.ms;
+        if (opt.consensus.enabled) {
+            const bsg_penalties& p = rep[0].rho;
+            rho = PropertyPenalties{p.rho_p, p.rho_q, p.rho_s, p.rho_f, p.rho_o};
+        }
+        d.rho = rho;
         result.rounds.push_back(d);
         if (observer) observer(d);
+    };
+    try {
+        for (size_t j = 0; j < schedule.size(); ++j) {
+            const uint64_t t = schedule[j];
+            const bool final_round = t == opt.total_iterations;
+            ready.wait();
+            if (j > 0) emit(pending_diag);
+            // ownership changes from densification (runtime.cpp:490-518), on the device
+            std::vector<const uint64_t*> rl(K);
+            std::vector<size_t> rn(K);
+            size_t n_removed = 0, n_added = 0;
+            for (uint32_t b = 0; b < K; ++b) {
+                rl[b] = rep[b].removed.data();
+                rn[b] = rep[b].removed.size();
+                n_removed += rn[b];
+                n_added += rep[b].added.size();
+            }
+            std::vector<uint32_t> t_slot(S.size() + 1), t_mask(S.size() + 1);
+            std::vector<uint8_t> t_class(S.size() + 1), found(std::max<size_t>(n_removed, 1));
+            size_t touched = 0;
+            check(bsg_owners_remove(owners.t, rl.data(), rn.data(), t_slot.data(), t_class.data(), t_mask.data(),
+                                    t_slot.size(), &touched, found.data()));
+            // a removed id outside the table had one owner and dies -- unless it
+            // was born and pruned within this interval (never reported as new,
+            // so never in the global model; runtime.cpp:498-499 skips it):
+            // ids are allocated in increasing order per block (IdAllocator,
+            // trainer.cpp:55-66), so such an id lies past the block's newest
+            // reported one
+            size_t dead = 0;
+            for (uint32_t b = 0, i = 0; b < K; ++b)
+                for (size_t q = 0; q < rn[b]; ++q, ++i) {
+                    if (found[i]) continue;
+                    const uint64_t id = rl[b][q];
+                    const bool fresh = id >= alloc_start[b] && (newest[b] == UINT64_MAX || id > newest[b]);
+                    dead += fresh ? 0 : 1;
+                }
+            for (uint32_t b = 0; b < K; ++b)
+                for (uint64_t id : rep[b].added) newest[b] = newest[b] == UINT64_MAX ? id : std::max(newest[b], id);
+            std::vector<uint64_t> reset_ids;
+            std::vector<uint32_t> lost;  // slots that leave the table (now < 2 owners)
+            for (size_t k = 0; k < touched; ++k) {
+                if (t_class[k] == 3) ++dead;
+                if (t_class[k] == 1) {
+                    reset_ids.push_back(S[t_slot[k]]);
+                    slot_cnt[t_slot[k]] = static_cast<uint32_t>(__builtin_popcount(t_mask[k]));
+                    slot_first[t_slot[k]] = static_cast<uint32_t>(__builtin_ctz(t_mask[k]));
+                } else {
+                    lost.push_back(t_slot[k]);
+                }
+            }
+            global_count = global_count + n_added - dead;
+            if (!lost.empty()) {
+                // new slot table: the kept slots in order; every block keeps its
+                // anchor / duals for the ids that stay shared, z_prev from the
+                // last consensus (all of it was shared before)
+                std::vector<double> zp_old(S.size() * D);
+                if (have_z && !S.empty())
+                    check(bsg_download_consensus(ctxs[0], zp_old.data()));
+                else
+                    std::copy(z0_rows.begin(), z0_rows.end(), zp_old.begin());
+                std::vector<uint64_t> S_new;
+                std::vector<uint32_t> cnt_new, first_new;
+                std::vector<double> zp_new;
+                std::vector<uint32_t> new_of(S.size(), UINT32_MAX);
+                size_t li = 0;
+                for (size_t k = 0; k < S.size(); ++k) {
+                    if (li < lost.size() && lost[li] == k) {
+                        ++li;
+                        continue;
+                    }
+                    new_of[k] = static_cast<uint32_t>(S_new.size());
+                    S_new.push_back(S[k]);
+                    cnt_new.push_back(slot_cnt[k]);
+                    first_new.push_back(slot_first[k]);
+                    zp_new.insert(zp_new.end(), &zp_old[k * D], &zp_old[k * D] + D);
+                }
+                for (uint32_t b = 0; b < K; ++b) {
+                    std::vector<uint64_t> keep;
+                    std::vector<uint32_t> slots;
+                    std::vector<uint8_t> first;
+                    for (uint64_t id : tr[b].shared_ids()) {
+                        auto it = std::lower_bound(S.begin(), S.end(), id);
+                        if (it == S.end() || *it != id) continue;
+                        const uint32_t ns = new_of[it - S.begin()];
+                        if (ns == UINT32_MAX) continue;
+                        keep.push_back(id);
+                        slots.push_back(ns);
+                        first.push_back(first_new[ns] == b ? 1 : 0);
+                    }
+                    tr[b].rebind_slots(keep, slots, first, cnt_new, zp_new, opt.consensus.enabled ? rho : zero_rho);
+                }
+                S = std::move(S_new);
+                slot_cnt = std::move(cnt_new);
+                slot_first = std::move(first_new);
+            }
+            std::vector<uint32_t> reset_slots;
+            for (uint64_t id : reset_ids) {
+                auto it = std::lower_bound(S.begin(), S.end(), id);
+                if (it != S.end() && *it == id) reset_slots.push_back(static_cast<uint32_t>(it - S.begin()));
+            }
+            // this round's arguments (runtime.cpp:529-548, trainer.cpp:168-223)
+            adapt.iteration = t;
+            for (uint32_t b = 0; b < K; ++b) {
+                resets[b] = reset_slots;
+                args[b] = bsg_round_args{};
+                args[b].alpha = opt.consensus.alpha;
+                args[b].relax = opt.consensus.enabled && opt.consensus.alpha != 1.0 && !final_round;
+                args[b].diagnostics = 1;
+                args[b].n_reset = resets[b].size();
+                args[b].reset_slots = resets[b].empty() ? nullptr : resets[b].data();
+            }
+            pending_diag = RoundDiagnostics{};
+            pending_diag.iteration = t;
+            for (uint32_t b = 0; b < K; ++b) pending_diag.mean_loss += rep[b].loss;
+            pending_diag.mean_loss /= K;
+            pending_diag.shared_count = S.size();
+            pending_diag.global_count = global_count;
+            have_z = true;
+            go.wait();
+        }
+        ready.wait();
+        emit(pending_diag);
+    } catch (...) {
+        errs[K] = std::current_exception();
+        fail_all();
     }
-    // Global model (runtime.cpp:550-565): shared rows = normalised z, the rest
-    // from their single owner's final cloud.
+    for (auto& w : workers) w.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+
+    // Global model (runtime.cpp:550-565): shared rows = normalised z, every
+    // other row from the one block that holds it (a non-shared id has a single
+    // owner: the others removed it).
+    std::vector<double> zs(S.size() * D);
+    if (!S.empty()) check(bsg_download_consensus(ctxs[0], zs.data()));
+    std::vector<GaussianCloud> finals;
+    finals.reserve(K);
+    std::vector<uint64_t> all_ids(S.begin(), S.end());
+    for (uint32_t b = 0; b < K; ++b) {
+        finals.push_back(tr[b].cloud());
+        for (uint64_t id : finals.back().ids)
+            if (!std::binary_search(S.begin(), S.end(), id)) all_ids.push_back(id);
+    }
+    std::sort(all_ids.begin(), all_ids.end());
+    all_ids.erase(std::unique(all_ids.begin(), all_ids.end()), all_ids.end());
     GaussianCloud model(fd);
-    model.ids.assign(global_ids.begin(), global_ids.end());
+    model.ids = all_ids;
     model.positions.resize(3 * model.size());
     model.rotations.resize(4 * model.size());
     model.log_scales.resize(3 * model.size());
     model.features.resize(static_cast<size_t>(fd) * model.size());
     model.opacity_logits.resize(model.size());
-    std::vector<double> zs(S.size() * D);
-    if (!S.empty()) check(bsg_download_consensus(ctxs[0], zs.data()));
     auto row_of = [&](uint64_t id) {
         return static_cast<size_t>(std::lower_bound(model.ids.begin(), model.ids.end(), id) - model.ids.begin());
     };
@@ -842,14 +1059,11 @@ RunResult run_simulated(const ClusterPlan& plan, const TrainerConfig& trainer, c
         }
         put(row_of(S[k]), row);
     }
-    // every other row from its single owner's final cloud, one pass per block
     for (uint32_t b = 0; b < K; ++b) {
-        const GaussianCloud c = tr[b].cloud();
+        const GaussianCloud& c = finals[b];
         for (size_t j = 0; j < c.size(); ++j) {
             const uint64_t id = c.ids[j];
             if (std::binary_search(S.begin(), S.end(), id)) continue;
-            auto it = owners.find(id);
-            if (it == owners.end() || it->second.front() != b) continue;
             double row[11 + kFeatureDimDeg1];
             for (int k = 0; k < 3; ++k) row[k] = c.positions[3 * j + k];
             for (int k = 0; k < 4; ++k) row[3 + k] = c.rotations[4 * j + k];

@@ -67,9 +67,12 @@ def test_run_simulated_matches_oracle(blocks, alpha):
     for g, w in zip(rounds, want.rounds):
         assert g["iteration"] == w.iteration
         assert g["shared_count"] == w.shared_count and g["global_count"] == w.global_count
-        assert g["mean_loss"] == pytest.approx(w.mean_loss, rel=2e-2)
-        assert g["primal"] == pytest.approx(w.primal_residual, rel=0.1, abs=1e-4)
-        assert g["max_disagreement"] == pytest.approx(w.max_disagreement, rel=0.1, abs=1e-4)
+        # 20-60 FP32 Adam steps per block between rounds (measured: loss 2e-3,
+        # primal 4e-3 relative at the last round)
+        assert g["mean_loss"] == pytest.approx(w.mean_loss, rel=5e-3)
+        assert g["primal"] == pytest.approx(w.primal_residual, rel=1e-2)
+        assert g["dual"] == pytest.approx(w.dual_residual, rel=1e-2, abs=1e-9)
+        assert g["max_disagreement"] == pytest.approx(w.max_disagreement, rel=1e-2, abs=1e-6)
         assert g["rho"][0] == w.rho.rho_p  # same adaptation decisions
     mc = HostCloud(model["ids"], model["pos"], model["rot"], model["ls"], model["feat"], model["op"])
     p_gpu = holdout_psnr(mc.oracle(), s)
@@ -114,6 +117,9 @@ def test_run_simulated_with_densification():
         assert abs(g["global_count"] - w.global_count) <= 0.02 * w.global_count
         assert abs(g["shared_count"] - w.shared_count) <= 0.02 * max(w.shared_count, 1) + 1
     assert want.rounds[-1].global_count != init.n  # the run really densified
+    # the driver's device owner table / id accounting agrees with the model it assembles
+    assert rounds[-1]["global_count"] == len(model["ids"])
+    assert np.all(np.diff(model["ids"].astype(np.int64)) > 0)
     mc = HostCloud(model["ids"], model["pos"], model["rot"], model["ls"], model["feat"], model["op"])
     p_gpu = holdout_psnr(mc.oracle(), s)
     p_ref = holdout_psnr(want.model, s)

@@ -206,6 +206,59 @@ def test_async_round_overlaps_next_step_exactly():
         np.testing.assert_allclose(gb[k], ga[k], rtol=1e-4, atol=1e-5)
 
 
+def test_async_round_then_densify_waits_for_the_round():
+    """An asynchronous round still pending when the next bsg_train_steps crosses
+    a densification iteration (bsg_consensus_round_async, then train steps):
+    densification waits for the round (it rewrites the anchor / dual rows the
+    round writes) and the round's result stays pending for consensus_wait.
+    Same densify decisions, round result and trajectory as the synchronous
+    order (round, wait, then the steps)."""
+    s, init = toy_scene(gaussians=120, cameras=6, size=40)
+    shared_rows = list(range(0, init.n, 4))
+    x0 = rows_of(init)[shared_rows]
+    zprev = (x0 + 0.02 * np.random.default_rng(6).standard_normal(x0.shape)).astype(np.float32).astype(np.float64)
+    rho = api.penalties()
+    seq = orc.view_sequence(1, 0, len(s.views), 10)
+    # densify at iteration 6 with thresholds that act on this scene: a probe run places them
+    probe = _anchored_trainer(init, s, shared_rows, zprev, rho)
+    probe.train_steps(seq[:6])
+    ga, gs = probe.densify_stats()
+    pc = probe.download_cloud()
+    grad_thr = _midpoint_threshold(ga[gs > 0] / gs[gs > 0], 0.5)
+    prune = _midpoint_threshold(1 / (1 + np.exp(-pc["op"])), 0.2)
+    dens = dict(enabled=1, interval=6, stop_iteration=6, grad_threshold=grad_thr, prune_opacity=prune,
+                split_scale_fraction=0.01, split_shrink=1.6)
+
+    def trainer():
+        b = new_block(init)
+        b.set_views([dev_cam(v) for v in s.views], s.images())
+        b.trainer_init(api.trainer_config(iterations=20, densify=dens))
+        n = len(shared_rows)
+        b.set_shared(shared_rows, list(range(n)), [1] * n, [1] * n)
+        b.set_anchor(zprev, zprev, rho)
+        return b
+
+    a = trainer()
+    a.train_steps(seq[:4])
+    ra = a.consensus_round(1.6, True)
+    la = a.train_steps(seq[4:10])
+    b = trainer()
+    b.train_steps(seq[:4])
+    b.consensus_round_async(1.6, True)
+    lb = b.train_steps(seq[4:10])  # iteration 6 densifies while the round may be in flight
+    rb = b.consensus_wait()
+    assert rb["primal"] == pytest.approx(ra["primal"], rel=1e-6)
+    assert rb["dual"] == pytest.approx(ra["dual"], rel=1e-6)
+    removed_a, removed_b = list(a.take_removed_ids()), list(b.take_removed_ids())
+    assert len(removed_a) > 0 and removed_a == removed_b
+    assert np.array_equal(a.take_new_ids(), b.take_new_ids())
+    assert list(a.shared_ids()) == list(b.shared_ids())
+    np.testing.assert_allclose(lb, la, rtol=1e-4)
+    ga_, gb_ = a.download_cloud(), b.download_cloud()
+    assert np.array_equal(ga_["ids"], gb_["ids"])
+    np.testing.assert_allclose(gb_["pos"], ga_["pos"], rtol=1e-4, atol=1e-5)
+
+
 def test_evaluate_matches_reference_metrics():
     """evaluate (metrics.cpp:28-51) on the device: holdout rule, PSNR
     (metrics.cpp:14-26) and SSIM (ssim.cpp) vs the FP64 oracle rendering."""
