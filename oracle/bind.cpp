@@ -160,7 +160,11 @@ PYBIND11_MODULE(_oracle, m) {
     });
 
     m.def("render", [](const Cloud& c, const Camera& cam, const RenderConfig& cfg) {
-        RenderOut o = render(c, cam, cfg);
+        RenderOut o;
+        {
+            py::gil_scoped_release rel;  // pure function: fixture renders may run on threads
+            o = render(c, cam, cfg);
+        }
         const ssize_t h = cam.height, w = cam.width;
         return py::make_tuple(image_np(o.color), to_np(o.transmittance, {h, w}), to_np(o.contributors, {h, w}));
     });
