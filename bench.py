@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="cfg3", choices=sorted(CFGS))
     p.add_argument("--interval", type=int, default=25, help="consensus interval (iterations)")
-    p.add_argument("--n", type=int, default=None, help="override the Gaussian count (profiling only)")
+    p.add_argument("--gaussians", type=int, default=None, help="override the Gaussian count (profiling, tests)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-also", action="store_true", help="skip the secondary configurations")
     p.add_argument("--views", type=int, default=None, help="fewer views for profiling runs only")
@@ -299,11 +299,20 @@ def barrier(world):
 
 def max_over_ranks(v, world):
     import torch
-    t = torch.tensor([float(v)], device="cuda")
     if world > 1:
         import torch.distributed as dist
+        t = torch.tensor([float(v)], device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+        return float(t.item())
+    return float(v)
+
+
+def host_allreduce(arr, op):
+    """The host communicator's reduction over the process group (ranks that
+    share a GPU cannot share an NCCL communicator)."""
+    import torch
+    import torch.distributed as dist
+    dist.all_reduce(torch.from_numpy(arr), op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
 
 
 def stage_pass(run, steps):
@@ -407,21 +416,30 @@ def run_ours(args, rank, world, local_rank):
     from paper_2405_13943_b200 import api
 
     cfg = CFGS[args.config]
-    torch.cuda.set_device(local_rank)
+    ndev = torch.cuda.device_count()
+    device = local_rank % ndev
+    shared_gpu = world > ndev  # more ranks than GPUs (a test of the N > 1 flow on one GPU)
+    torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    blk, view_cams, gts, info = build_block(cfg, rank, world, local_rank, args.n, args.views, args.profile)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+    blk, view_cams, gts, info = build_block(cfg, rank, world, device, args.gaussians, args.views, args.profile)
     if world > 1:
         import torch.distributed as dist
-        uid = [api.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        blk.comm_init(uid[0], world, rank)
+        if shared_gpu:
+            blk.comm_init_host(host_allreduce, world, rank)
+        else:
+            uid = [api.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            blk.comm_init(uid[0], world, rank)
         blk.set_round_timeout(120.0)
     nv = len(view_cams)
     run = Runner(blk, nv, rank, world, args.interval)
     stream = torch.cuda.ExternalStream(blk.stream())
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(device)
     clocks.start()
     clocks.wait_first()
     run.steps(args.warmup)
@@ -551,13 +569,15 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "f32 (FP64 projection)",
         "data": "synthetic (aerial scene, GT rendered on device from the generating cloud; training from a "
                 "perturbed copy)",
-        "config": {"workload": WORKLOAD[args.config] + (f" ({args.n} Gaussians)" if args.n else ""),
-                   "gaussians": args.n or cfg["n"], "width": cfg["width"], "height": cfg["height"],
+        "config": {"workload": WORKLOAD[args.config] + (f" ({args.gaussians} Gaussians)" if args.gaussians else ""),
+                   "gaussians": args.gaussians or cfg["n"], "width": cfg["width"], "height": cfg["height"],
                    "views": cfg["views"], "tilt_deg": cfg["tilt"], "blocks": world, "expand_scale": cfg["scale"],
                    "consensus_interval": args.interval, "block0_gaussians": nb, "block0_views": info["block_views"],
                    "shared_ids": info["shared_ids"], "view_order": "BlockTrainer (trainer.cpp:250-252), seed 1",
                    "l2": "inputs > L2 (Adam state %.1fM rows x 168 B)" % (nb / 1e6),
-                   "parallelism": f"blocks{world}"},
+                   "parallelism": f"blocks{world}",
+                   "transport": ("nccl" if not shared_gpu else "host all-reduce over gloo (ranks share a GPU)")
+                   if world > 1 else None},
         "e2e": {"value": 1000.0 / e2e_ms_step, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 24},
         "e2e_path": "bsg_train_steps_host_u8: every step's 8-bit RGB ground truth (the reference's PPM data, quantized "
                     "once) copied from pinned host memory and widened on the device; every step's loss read back",
@@ -591,11 +611,11 @@ def run_ours(args, rank, world, local_rank):
         also = {}
         for name in ("cfg2", "cfg2_tilt30"):
             if name != args.config:
-                also[name] = secondary(name, local_rank, max(args.steps, 100), max(args.warmup, 5))
-        also["consensus_k8"] = consensus_k8(local_rank)
+                also[name] = secondary(name, device, max(args.steps, 100), max(args.warmup, 5))
+        also["consensus_k8"] = consensus_k8(device)
         out["also"] = also
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg, args.n)
+        out["cpu_baseline"] = cpu_baseline(cfg, args.gaussians)
     print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -663,7 +683,7 @@ def run_reference(args, rank, world):
     budget = 150.0  # seconds of timed FP64 steps (one step of cfg 3 takes ~10-15 s)
     warm = min(args.warmup, 2)
     est_steps = min(args.steps, 16)
-    tr = oracle_block(cfg, args.n, warm + est_steps)
+    tr = oracle_block(cfg, args.gaussians, warm + est_steps)
     for _ in range(warm):
         tr.train_step()
     t0 = time.perf_counter()
@@ -680,8 +700,8 @@ def run_reference(args, rank, world):
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
            "data": "synthetic (the same scene, block, view order; GT rendered from the generating cloud by the "
                    "reference's FP64 renderer)",
-           "config": {"workload": WORKLOAD[args.config] + " -- block 0 (K=1)" + (f" ({args.n} Gaussians)" if args.n else ""),
-                      "gaussians": args.n or cfg["n"], "width": cfg["width"], "height": cfg["height"],
+           "config": {"workload": WORKLOAD[args.config] + " -- block 0 (K=1)" + (f" ({args.gaussians} Gaussians)" if args.gaussians else ""),
+                      "gaussians": args.gaussians or cfg["n"], "width": cfg["width"], "height": cfg["height"],
                       "views": cfg["views"], "tilt_deg": cfg["tilt"], "blocks": 1,
                       "view_order": "BlockTrainer (trainer.cpp:250-252), seed 1"},
            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "port",
