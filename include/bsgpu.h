@@ -376,6 +376,14 @@ int bsg_decode_checkpoint(const uint8_t* data, size_t size, size_t capacity, uin
                           double* rot, double* log_scale, double* features, double* opacity_logit, size_t* out_n,
                           int* out_fd, int* format_code);
 
+/* ---- checked build ------------------------------------------------------ */
+/* 1 in lib/libbsgpu_checked.so (device invariant checks compiled in), else 0. */
+int bsg_checked_build(void);
+/* Launches one kernel whose check fails on purpose: BSG_ERR_CUDA (and a
+ * corrupted CUDA context -- run it in a throwaway process) in the checked
+ * build, BSG_OK otherwise. Proves the checks are live. */
+int bsg_checked_probe(int device);
+
 /* ---- master-round ownership bookkeeping (device) ------------------------ */
 /* The owner table of the consensus slot table on one device (
  * replaces the master's std::map of owners, runtime.cpp:490-518): n_slots

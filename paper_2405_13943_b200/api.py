@@ -18,6 +18,9 @@ LIB_PATH = os.environ.get("BSG_LIB") or os.path.join(_HERE, "lib", "libbsgpu.so"
 
 BSG_OK = 0
 BSG_ERR_INVALID_ARGUMENT = 1
+BSG_ERR_CUDA = 2
+BSG_ERR_NCCL = 3
+BSG_ERR_STATE = 4
 BSG_ERR_CAPACITY = 5
 BSG_ERR_FORMAT = 6
 
@@ -175,6 +178,8 @@ SYMBOLS = [
                                           ctypes.POINTER(bsg_trainer_config), ctypes.POINTER(bsg_session_options), _SZ,
                                           ctypes.POINTER(ctypes.c_int), _SZ, _U64P, _DP, _DP, _DP, _DP, _DP, _SZP,
                                           ctypes.POINTER(bsg_round_diag), _SZ, _SZP, _DP]),
+    ("bsg_checked_build", ctypes.c_int, []),
+    ("bsg_checked_probe", ctypes.c_int, [ctypes.c_int]),
     ("bsg_owners_create", ctypes.c_int, [ctypes.c_int, _SZ, _U64P, _U32P, ctypes.c_uint32, ctypes.POINTER(_P)]),
     ("bsg_owners_destroy", ctypes.c_int, [_P]),
     ("bsg_owners_size", _SZ, [_P]),

@@ -1804,6 +1804,27 @@ int bsg_step_counters(bsg_ctx* h, uint64_t* visible, uint64_t* pairs, uint64_t* 
 
 uint64_t bsg_step_blend_evals(const bsg_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->last_evals : 0; }
 
+// ---- checked build probe ---------------------------------------------------
+
+__global__ void checked_probe_kernel(int v) { BSG_DASSERT(v != 1); }
+
+int bsg_checked_build(void) {
+#ifdef BSG_CHECKED
+    return 1;
+#else
+    return 0;
+#endif
+}
+
+int bsg_checked_probe(int device) {
+    return guarded([&] {
+        BSG_CUDA(cudaSetDevice(device));
+        checked_probe_kernel<<<1, 1>>>(1);
+        BSG_CUDA(cudaGetLastError());
+        BSG_CUDA(cudaDeviceSynchronize());
+    });
+}
+
 // ---- master-round ownership bookkeeping (owners.cu) ----------------------
 
 int bsg_owners_create(int device, size_t n, const uint64_t* ids, const uint32_t* masks, uint32_t blocks,

@@ -326,6 +326,7 @@ __global__ __launch_bounds__(256, 5) void adam_kernel(float* __restrict__ x, flo
         const uint32_t vis = (vword >> bit0) & 0xfu;
         // visible position of the quad's first row (gbuf is by visible position)
         const uint32_t vpos = vis ? vis_prefix[word] + __popc(vword & ((1u << bit0) - 1u)) : 0u;
+        BSG_DASSERT(vpos <= cap);
         int aj[4] = {-1, -1, -1, -1};
         if (st.has_anchor) {
             const uint32_t sm = sh_mask[word];
@@ -335,6 +336,7 @@ __global__ __launch_bounds__(256, 5) void adam_kernel(float* __restrict__ x, flo
                 for (int r = 0; r < 4; ++r) {
                     const uint32_t b = bit0 + r;
                     if ((sm >> b) & 1u) aj[r] = static_cast<int>(pre + __popc(sm & ((1u << b) - 1u)));
+                    BSG_DASSERT(aj[r] < static_cast<int>(ns));
                 }
             }
         }

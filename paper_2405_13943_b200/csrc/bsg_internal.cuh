@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include <string>
@@ -92,6 +93,24 @@ constexpr unsigned long long kMaxPairs = 1ull << 30;
 // the global depth sort + stable tile sort. cfg 5 (1080p): a 2048 cap beats
 // 1024 at 4M rows (3.60 -> 3.48 ms/iter) and ties 4096 at 8M-16M.
 constexpr uint32_t kTileSortCap = 2048;
+
+// Device-side invariant checks of the checked build (lib/libbsgpu_checked.so,
+// -DBSG_CHECKED; tests/test_gpu_checked.py): a failed check prints its site
+// and traps, so the entry point returns BSG_ERR_CUDA. Compiled out otherwise.
+#ifdef BSG_CHECKED
+#define BSG_DASSERT(cond)                                                                       \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("BSG_DASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));              \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define BSG_DASSERT(cond) \
+    do {                  \
+    } while (0)
+#endif
 
 // Where a scan's final CTA publishes its total (all null: nowhere).
 struct Publish {

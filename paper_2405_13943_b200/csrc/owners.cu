@@ -29,6 +29,7 @@ __global__ __launch_bounds__(kOwnThreads) void own_mark_kernel(const uint64_t* _
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     const uint64_t id = in_ids[i];
+    BSG_DASSERT(in_blk[i] < 32);
     uint32_t lo = 0, hi = n;  // first slot with ids[slot] >= id
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;

@@ -192,7 +192,7 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
                                                          const StepCounters* __restrict__ counters,
                                                          const float4* __restrict__ rec, int tiles_x,
                                                          uint32_t* __restrict__ cur, uint32_t* __restrict__ out_rows,
-                                                         uint32_t pcap) {
+                                                         uint32_t pcap, const uint2* __restrict__ ranges_end) {
     pdl_prologue();
     const uint32_t V = counters->visible;
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < V; p += gridDim.x * blockDim.x) {
@@ -202,6 +202,7 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
         for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
             for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
                 const uint32_t slot = atomicAdd(&cur[ty * tiles_x + tx], 1u);
+                BSG_DASSERT(slot < ranges_end[ty * tiles_x + tx].y);  // the tile's cursor stays in its range
                 if (slot < pcap) out_rows[slot] = row;
             }
     }
@@ -229,6 +230,7 @@ __global__ __launch_bounds__(128) void tile_sort_kernel(const uint2* __restrict_
     }
     uint32_t N = 2;
     while (N < n) N <<= 1;
+    BSG_DASSERT(N <= kTileSortCap);
     // one 64-bit word per pair: the upper 32 bits of the FP64 depth (its sign,
     // exponent and 20 mantissa bits: order-preserving for positive depths) and
     // the row, so a compare-exchange moves one word; pairs whose upper depth
@@ -475,6 +477,7 @@ __device__ __forceinline__ void fwd_pixel(FwdPix& P, uint32_t m, const uint32_t*
             return;
         }
         const uint32_t j = list[e] & 0xffffu;
+        BSG_DASSERT(j < kBatch);
         const float4 A = s_rec[3 * j], B = s_rec[3 * j + 1];
         const float cbl = s_rec[3 * j + 2].x;
         const float t1 = fmaf(A.y, ly, fmaf(A.x, lx, A.w)), t2 = fmaf(A.z, ly, B.x);
@@ -522,6 +525,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_fwd_kernel(const uint2
     const float lx = static_cast<float>(lxi), ly0 = static_cast<float>(ly0i), ly1 = ly0 + 4.f;
     const int hc = lane & 7, hr = lane >> 3;  // this lane's sub-tile column, first row
     const uint2 range = ranges[tile];
+    BSG_DASSERT(range.x <= range.y);
     const double oma_clamp = 1.0 - aclamp_d;
     FwdPix P0{1.f, 0.f, 0.f, 0.f, 1.0, 0u, 0u, !in0}, P1{1.f, 0.f, 0.f, 0.f, 1.0, 0u, 0u, !in1};
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
@@ -742,6 +746,7 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             if (hit1) bwd_step(P1, u, ly1, A, B, C.x, aclamp, acc);
             const uint32_t target = __float_as_uint(C.y);  // row, or kWideBit | FP64 slot (kWideArea)
             const bool wide = target & kWideBit;
+            BSG_DASSERT(sj < kBatch && (wide ? (target & ~kWideBit) < kWideCap : true));
             float* dst = reinterpret_cast<float*>(g2d + 3 * static_cast<size_t>(target & ~kWideBit));
             if (__popc(mask) <= direct_lanes && !wide) {
                 if (hit0 || hit1) {
@@ -806,7 +811,7 @@ void launch_tile_scan(Ctx* c, const DevCam& cam, uint32_t seq) {
 void launch_emit_tiles(Ctx* c, const DevCam& cam) {
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(static_cast<uint32_t>((c->n + 255) / 256), 148 * 8));
     launch_pdl(c->stream, grid, 256, 0, emit_tiles_kernel, c->vis_rows, c->counters, c->rec, cam.tiles_x, c->tile_cur,
-               c->pval[1], static_cast<uint32_t>(c->pcap));
+               c->pval[1], static_cast<uint32_t>(c->pcap), c->ranges);
     BSG_LAUNCHED(c);
 }
 
