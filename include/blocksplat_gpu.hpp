@@ -158,7 +158,7 @@ struct AdamParams {
     double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
 };
 struct DensifyConfig {
-    bool enabled = true;  // on the device (csrc/densify.cu); run_simulated with K > 1 rejects a run that densifies
+    bool enabled = true;  // on the device (csrc/densify.cu); run_simulated tracks ownership on the device (csrc/owners.cu)
     uint32_t interval = 200;
     uint64_t stop_iteration = 0;
     double grad_threshold = 2e-4, prune_opacity = 0.005, split_scale_fraction = 0.01, split_shrink = 1.6;
@@ -295,8 +295,12 @@ struct SessionOptions {  // runtime.hpp:109-115
     uint32_t nonshared_refresh = 10;
 };
 // run_simulated (runtime.cpp:623-671): K blocks in one process, one host
-// thread per block, consensus by an in-order device reduction across the
-// group (no master hop). devices[b % devices.size()] hosts block b.
+// thread per block, each starting its consensus round asynchronously so the
+// round overlaps its next iterations; the all-reduces go over NCCL (one rank
+// per GPU) when every block has its own device, else through an in-process
+// host all-reduce (blocks sharing a GPU). The master's ownership bookkeeping
+// (runtime.cpp:490-518) runs on the device owner table (bsg_owners_*).
+// devices[b % devices.size()] hosts block b.
 // The view order BlockTrainer::train_step draws (trainer.cpp:116-118,250-252:
 // derive_seed, then a Fisher-Yates shuffle with rejection-sampled indices on
 // mt19937_64 at the start of every pass) -- the same code path.
