@@ -210,8 +210,8 @@ void ensure_image_buffers(Ctx* c, int W, int H) {
     if (ntiles > c->ranges_cap) {
         dev_alloc(&c->ranges, ntiles);
         dev_alloc(&c->tile_order, ntiles);
-        dev_alloc(&c->tile_cnt, ntiles);
-        dev_alloc(&c->tile_cur, ntiles);
+        dev_alloc(&c->tile_cnt, kTileSub * ntiles);
+        dev_alloc(&c->tile_cur, kTileSub * ntiles);
         c->ranges_cap = ntiles;
     }
 }
@@ -244,7 +244,7 @@ __global__ __launch_bounds__(512) void zero_counters_kernel(StepCounters* __rest
     pdl_prologue();
     uint32_t* w = reinterpret_cast<uint32_t*>(cnt);
     for (uint32_t i = threadIdx.x; i < sizeof(StepCounters) / 4; i += blockDim.x) w[i] = 0;
-    for (uint32_t i = threadIdx.x; i < ntiles; i += blockDim.x) tile_cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < kTileSub * ntiles; i += blockDim.x) tile_cnt[i] = 0;
 }
 
 // K1-K5: projection, compaction, depth sort, pair emission, tile sort, ranges.

@@ -93,6 +93,11 @@ constexpr unsigned long long kMaxPairs = 1ull << 30;
 // the global depth sort + stable tile sort. cfg 5 (1080p): a 2048 cap beats
 // 1024 at 4M rows (3.60 -> 3.48 ms/iter) and ties 4096 at 8M-16M.
 constexpr uint32_t kTileSortCap = 2048;
+// Each tile's pair count and emission cursor are split kTileSub ways (by row
+// mod kTileSub): the preprocess's counting reductions and the emission's slot
+// claims on a busy tile spread over kTileSub addresses instead of
+// serialising on one (the tile scan lays the sub-ranges end to end).
+constexpr uint32_t kTileSub = 4;
 
 // Device-side invariant checks of the checked build (lib/libbsgpu_checked.so,
 // -DBSG_CHECKED; tests/test_gpu_checked.py): a failed check prints its site

@@ -263,7 +263,8 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                 ntiles = static_cast<uint32_t>((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
                 // pairs per tile for the per-tile binning
                 for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) atomicAdd(&tile_cnt[ty * cam.tiles_x + tx], 1u);
+                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx)
+                        atomicAdd(&tile_cnt[kTileSub * (ty * cam.tiles_x + tx) + (i & (kTileSub - 1))], 1u);
                 const unsigned long long zb = static_cast<unsigned long long>(__double_as_longlong(z));
                 depth_key[i] = zb;
                 zmin_inv = max(zmin_inv, ~zb);

@@ -139,14 +139,19 @@ __global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restr
     // ranges, cursors and the launch-order histogram (bucket 1023 - min(count, 1023))
     uint32_t carry = 0, mx = 0;
     unsigned long long wide = 0;
+    static_assert(kTileSub == 4, "one uint4 of sub-counts per tile");
+    const uint4* cnt4 = reinterpret_cast<const uint4*>(cnt);
+    uint4* cur4 = reinterpret_cast<uint4*>(cur);
     for (uint32_t c0 = 0; c0 < ntiles; c0 += 1024) {
         const uint32_t i = c0 + t;
-        const uint32_t v = i < ntiles ? cnt[i] : 0u;
+        const uint4 sc = i < ntiles ? cnt4[i] : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t v = sc.x + sc.y + sc.z + sc.w;
         uint32_t total;
         const uint32_t ex = block_exclusive_scan(v, s_warp, total);
         if (i < ntiles) {
-            ranges[i] = make_uint2(carry + ex, carry + ex + v);
-            cur[i] = carry + ex;
+            const uint32_t b = carry + ex;
+            ranges[i] = make_uint2(b, b + v);
+            cur4[i] = make_uint4(b, b + sc.x, b + sc.x + sc.y, b + sc.x + sc.y + sc.z);  // sub-ranges end to end
             atomicAdd(&s_bucket[1023u - min(v, 1023u)], 1u);
         }
         carry += total;
@@ -174,7 +179,10 @@ __global__ __launch_bounds__(1024) void tile_scan_kernel(const uint32_t* __restr
     // launch order: tiles by descending count (order inside a bucket is free)
     for (uint32_t c0 = 0; c0 < ntiles; c0 += 1024) {
         const uint32_t i = c0 + t;
-        if (i < ntiles) order[atomicAdd(&s_bucket[1023u - min(cnt[i], 1023u)], 1u)] = i;
+        if (i < ntiles) {
+            const uint4 sc = cnt4[i];
+            order[atomicAdd(&s_bucket[1023u - min(sc.x + sc.y + sc.z + sc.w, 1023u)], 1u)] = i;
+        }
     }
     if (t == 0) {
         *pairs_dev = carry;
@@ -201,7 +209,7 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
         unpack_rect(rec[3 * static_cast<size_t>(row) + 2], x0, x1, y0, y1);
         for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
             for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
-                const uint32_t slot = atomicAdd(&cur[ty * tiles_x + tx], 1u);
+                const uint32_t slot = atomicAdd(&cur[kTileSub * (ty * tiles_x + tx) + (row & (kTileSub - 1))], 1u);
                 BSG_DASSERT(slot < ranges_end[ty * tiles_x + tx].y);  // the tile's cursor stays in its range
                 if (slot < pcap) out_rows[slot] = row;
             }
