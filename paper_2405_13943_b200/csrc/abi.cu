@@ -126,32 +126,33 @@ void check_camera(const bsg_camera* cam) {
 
 void alloc_rows(Ctx* c, size_t n) {
     const size_t cap = (std::max<size_t>(n, 1) + 31) / 32 * 32;  // float4-aligned component rows
-    dev_alloc(&c->x, c->D * cap);
-    dev_alloc(&c->m, c->D * cap);
-    dev_alloc(&c->v, c->D * cap);
+    dev_alloc(&c->x, row_stride(c->fd) * cap);
+    dev_alloc(&c->m, row_stride(c->fd) * cap);
+    dev_alloc(&c->v, row_stride(c->fd) * cap);
     alloc_row_scratch(c, cap);
 }
 
-// Host FP64 reference layout -> device FP32 [D][cap].
+// Host FP64 reference layout -> device FP32 rows (row_stride / pslot).
 void upload_params(Ctx* c, const double* pos, const double* rot, const double* ls, const double* feat,
                    const double* op) {
     const size_t n = c->n, cap = c->cap;
-    std::vector<float> h(static_cast<size_t>(c->D) * cap, 0.f);
+    const int fd = c->fd;
+    std::vector<float> h(static_cast<size_t>(row_stride(fd)) * cap, 0.f);
     for (size_t i = 0; i < n; ++i) {
-        for (int k = 0; k < 3; ++k) h[(kPos + k) * cap + i] = static_cast<float>(pos[3 * i + k]);
-        for (int k = 0; k < 4; ++k) h[(kRot + k) * cap + i] = static_cast<float>(rot[4 * i + k]);
-        for (int k = 0; k < 3; ++k) h[(kLs + k) * cap + i] = static_cast<float>(ls[3 * i + k]);
-        for (int k = 0; k < c->fd; ++k) h[(kFeat + k) * cap + i] = static_cast<float>(feat[i * c->fd + k]);
-        h[op_comp(c->fd) * cap + i] = static_cast<float>(op[i]);
+        for (int k = 0; k < 3; ++k) h[pidx(i, kPos + k, fd)] = static_cast<float>(pos[3 * i + k]);
+        for (int k = 0; k < 4; ++k) h[pidx(i, kRot + k, fd)] = static_cast<float>(rot[4 * i + k]);
+        for (int k = 0; k < 3; ++k) h[pidx(i, kLs + k, fd)] = static_cast<float>(ls[3 * i + k]);
+        for (int k = 0; k < fd; ++k) h[pidx(i, kFeat + k, fd)] = static_cast<float>(feat[i * fd + k]);
+        h[pidx(i, op_comp(fd), fd)] = static_cast<float>(op[i]);
     }
     BSG_CUDA(cudaMemcpyAsync(c->x, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
     // scene extent of the (FP32-stored) positions: |tight_aabb extent| (trainer.cpp:153-154)
     if (c->n) {
         double lo[3], hi[3];
-        for (int k = 0; k < 3; ++k) lo[k] = hi[k] = h[(kPos + k) * cap];
+        for (int k = 0; k < 3; ++k) lo[k] = hi[k] = h[pidx(0, kPos + k, fd)];
         for (size_t i = 0; i < c->n; ++i)
             for (int k = 0; k < 3; ++k) {
-                const double v = h[(kPos + k) * cap + i];
+                const double v = h[pidx(i, kPos + k, fd)];
                 lo[k] = std::min(lo[k], v);
                 hi[k] = std::max(hi[k], v);
             }
@@ -788,8 +789,8 @@ int bsg_upload_cloud(bsg_ctx* h, size_t n, const uint64_t* ids, const double* po
         c->ids.assign(ids, ids + n);
         alloc_rows(c, n);
         upload_params(c, pos, rot, ls, feat, op);
-        BSG_CUDA(cudaMemsetAsync(c->m, 0, c->D * c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->v, 0, c->D * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->m, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->v, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->vis_mask, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
@@ -814,16 +815,18 @@ int bsg_download_cloud(bsg_ctx* h, uint64_t* ids, double* pos, double* rot, doub
         const size_t n = c->n, cap = c->cap;
         if (ids) std::copy(c->ids.begin(), c->ids.end(), ids);
         if (!pos && !rot && !ls && !feat && !op) return;  // ids only
-        std::vector<float> hx(static_cast<size_t>(c->D) * cap);
+        materialize(c);
+        const int fd = c->fd;
+        std::vector<float> hx(static_cast<size_t>(row_stride(fd)) * cap);
         BSG_CUDA(cudaMemcpyAsync(hx.data(), c->x, hx.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         if (ids) std::copy(c->ids.begin(), c->ids.end(), ids);
         for (size_t i = 0; i < n; ++i) {
-            if (pos) for (int k = 0; k < 3; ++k) pos[3 * i + k] = hx[(kPos + k) * cap + i];
-            if (rot) for (int k = 0; k < 4; ++k) rot[4 * i + k] = hx[(kRot + k) * cap + i];
-            if (ls) for (int k = 0; k < 3; ++k) ls[3 * i + k] = hx[(kLs + k) * cap + i];
-            if (feat) for (int k = 0; k < c->fd; ++k) feat[i * c->fd + k] = hx[(kFeat + k) * cap + i];
-            if (op) op[i] = hx[op_comp(c->fd) * cap + i];
+            if (pos) for (int k = 0; k < 3; ++k) pos[3 * i + k] = hx[pidx(i, kPos + k, fd)];
+            if (rot) for (int k = 0; k < 4; ++k) rot[4 * i + k] = hx[pidx(i, kRot + k, fd)];
+            if (ls) for (int k = 0; k < 3; ++k) ls[3 * i + k] = hx[pidx(i, kLs + k, fd)];
+            if (feat) for (int k = 0; k < fd; ++k) feat[i * fd + k] = hx[pidx(i, kFeat + k, fd)];
+            if (op) op[i] = hx[pidx(i, op_comp(fd), fd)];
         }
     });
 }
@@ -1149,8 +1152,8 @@ int bsg_trainer_init(bsg_ctx* h, const bsg_trainer_config* cfg) {
         if (!c) invalid("null context");
         if (cfg) c->tcfg = *cfg; else bsg_default_trainer_config(&c->tcfg);
         use_device(c);
-        BSG_CUDA(cudaMemsetAsync(c->m, 0, c->D * c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->v, 0, c->D * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->m, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->v, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
@@ -1274,15 +1277,17 @@ int bsg_download_moments(bsg_ctx* h, double* m, double* v) {
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c) invalid("null context");
         use_device(c);
+        materialize(c);
         const size_t n = c->n, cap = c->cap;
-        std::vector<float> hm(c->D * cap), hv(c->D * cap);
+        const int fd = c->fd;
+        std::vector<float> hm(row_stride(fd) * cap), hv(row_stride(fd) * cap);
         BSG_CUDA(cudaMemcpyAsync(hm.data(), c->m, hm.size() * 4, cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaMemcpyAsync(hv.data(), c->v, hv.size() * 4, cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         for (int k = 0; k < c->D; ++k)
             for (size_t i = 0; i < n; ++i) {
-                if (m) m[k * n + i] = hm[k * cap + i];
-                if (v) v[k * n + i] = hv[k * cap + i];
+                if (m) m[k * n + i] = hm[pidx(i, k, fd)];
+                if (v) v[k * n + i] = hv[pidx(i, k, fd)];
             }
     });
 }

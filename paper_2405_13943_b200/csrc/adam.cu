@@ -262,20 +262,19 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
     grad_seen[i] += 1u;
 }
 
-// Dense Adam over every row (trainer.cpp:267-281), element-wise: a thread
-// owns Q quads of 4 consecutive rows of one component (float4 loads/stores of
-// x, m, v), so the kernel is a pure coalesced stream. Launch 1 covers the
-// scalar components (blockIdx.y, Q = 1); launch 2 (adam_rot_kernel) the
-// quaternion group, whose 4 components per row are updated together and then
-// canonicalised (cloud.cpp:82-85, math.hpp:25-34). Visibility comes from the 1-bit-per-row
-// mask built by the compaction, shared-row anchors from a bit mask + per-word
-// prefix (anchor index = rank of the row among the shared rows), so no
-// per-row side array is re-read per component. Rows not visible this step
-// have a zero render gradient; shared rows add rho (x - z + u) evaluated at
-// the pre-step x (admm.cpp:24-28, trainer.cpp:257-265).
-// The step's sqrt and division are the approximate MUFU forms (sqrt.approx,
-// rcp-based division, ~2 ulp each on the update term, far below the FP32
-// rounding of x itself); the IEEE sequences made the kernel issue-bound.
+// Dense Adam over every row (trainer.cpp:267-281). The parameters and both
+// moments are row-major (row_stride(fd) floats per row, bsg_internal.cuh), so
+// a thread owns one 32-byte sector of a row -- 8 slots of x, m and v as two
+// float4 each -- and consecutive threads stream consecutive sectors. The
+// rotation sector (slots 8-11) is updated and then canonicalised
+// (cloud.cpp:82-85, math.hpp:25-34) in the same thread. Visibility comes from
+// the 1-bit-per-row mask built by the compaction (gradient at the row's
+// visible position of gbuf[D][.]), shared-row anchors from a bit mask +
+// per-word prefix; rows not visible this step have a zero render gradient;
+// shared rows add rho (x - z + u) evaluated at the pre-step x (admm.cpp:24-28,
+// trainer.cpp:257-265). The step's sqrt and division are the approximate MUFU
+// forms (sqrt.approx, rcp-based division, ~2 ulp each on the update term, far
+// below the FP32 rounding of x itself).
 __device__ __forceinline__ float adam_update(float x, float g, float& m, float& v, float lr, const AdamStep& st) {
     m = st.b1 * m + st.omb1 * g;
     v = st.b2 * v + st.omb2 * g * g;
@@ -284,186 +283,125 @@ __device__ __forceinline__ float adam_update(float x, float g, float& m, float& 
     return x - lr * __fdividef(m * st.inv_bc1, sq + st.eps);
 }
 
-__device__ __forceinline__ int comp_of_group(int y) { return y < 3 ? y : y + 4; }  // pos 0-2, ls/feat/op 7..
+// Component stored in a slot of the row layout, -1 for padding (inverse of pslot).
+__host__ __device__ constexpr int comp_of_slot(int s, int fd) {
+    return s < 3 ? kPos + s
+                 : (s < 6 ? kLs + (s - 3)
+                          : (s == 6 ? kFeat + fd
+                                    : (s == 7 ? -1 : (s < 12 ? kRot + (s - 8) : (s < 12 + fd ? kFeat + (s - 12) : -1)))));
+}
 
-// Occupancy: 5 (scalar groups, 48 registers) and 6 (quaternion group, 39)
-// resident CTAs per SM keep more loads in flight than the unbounded 52 / 64
-// registers (cfg 2: 134.4 -> 131.4 us for the two launches).
-template <int Q>
-__global__ __launch_bounds__(256, 5) void adam_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
-                                                   size_t cap, uint32_t n, const uint32_t* __restrict__ vis_mask,
-                                                   const uint32_t* __restrict__ vis_prefix,
-                                                   const float* __restrict__ gbuf,
-                                                   const uint32_t* __restrict__ sh_mask,
-                                                   const uint32_t* __restrict__ sh_prefix, const float* __restrict__ z,
-                                                   const float* __restrict__ u, size_t ns,
-                                                   const float* __restrict__ rho_dev, AdamStep st,
-                                                   double* __restrict__ penalty) {
-    pdl_prologue();
-    __shared__ double s_red[8];
-    constexpr int NC = 1;
-    const int c0 = comp_of_group(blockIdx.y);
-    double pen = 0.0;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        const uint32_t r0 = 4 * ((blockIdx.x * blockDim.x + threadIdx.x) * Q + q);
-        if (r0 >= n) break;
-        const int nr = n - r0 >= 4 ? 4 : static_cast<int>(n - r0);
-        // the streamed x, m, v quads first; everything they do not depend on after
-        float xs[NC][4], ms[NC][4], vs[NC][4];  // [component][row]
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
-            const float4 x4 = *reinterpret_cast<const float4*>(x + off);
-            const float4 m4 = *reinterpret_cast<const float4*>(m + off);
-            const float4 v4 = *reinterpret_cast<const float4*>(v + off);
-            xs[k][0] = x4.x; xs[k][1] = x4.y; xs[k][2] = x4.z; xs[k][3] = x4.w;
-            ms[k][0] = m4.x; ms[k][1] = m4.y; ms[k][2] = m4.z; ms[k][3] = m4.w;
-            vs[k][0] = v4.x; vs[k][1] = v4.y; vs[k][2] = v4.z; vs[k][3] = v4.w;
-        }
-        const uint32_t word = r0 >> 5, bit0 = r0 & 31u;
-        const uint32_t vword = vis_mask[word];
-        const uint32_t vis = (vword >> bit0) & 0xfu;
-        // visible position of the quad's first row (gbuf is by visible position)
-        const uint32_t vpos = vis ? vis_prefix[word] + __popc(vword & ((1u << bit0) - 1u)) : 0u;
-        BSG_DASSERT(vpos <= cap);
-        int aj[4] = {-1, -1, -1, -1};
-        if (st.has_anchor) {
-            const uint32_t sm = sh_mask[word];
-            if ((sm >> bit0) & 0xfu) {
-                const uint32_t pre = sh_prefix[word];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint32_t b = bit0 + r;
-                    if ((sm >> b) & 1u) aj[r] = static_cast<int>(pre + __popc(sm & ((1u << b) - 1u)));
-                    BSG_DASSERT(aj[r] < static_cast<int>(ns));
-                }
-            }
-        }
-        // gradient and anchor loads of every row before any arithmetic: one round trip
-        float g[NC][4], zr[NC][4], ur[NC][4];
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                g[k][r] = ((vis >> r) & 1u)
-                              ? gbuf[static_cast<size_t>(c0 + k) * cap + vpos + __popc(vis & ((1u << r) - 1u))]
-                              : 0.f;
-                zr[k][r] = aj[r] >= 0 ? z[static_cast<size_t>(c0 + k) * ns + aj[r]] : 0.f;
-                ur[k][r] = aj[r] >= 0 ? u[static_cast<size_t>(c0 + k) * ns + aj[r]] : 0.f;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            const float lr = st.lr[c0 + k], rho = st.has_anchor ? rho_dev[c0 + k] : 0.f;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                float gr = g[k][r];
-                if (aj[r] >= 0) {
-                    const float d = xs[k][r] - zr[k][r] + ur[k][r];
-                    if (r < nr) pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
-                    gr += rho * d;
-                }
-                xs[k][r] = adam_update(xs[k][r], gr, ms[k][r], vs[k][r], lr, st);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            const size_t off = static_cast<size_t>(c0 + k) * cap + r0;
-            if (nr == 4) {
-                *reinterpret_cast<float4*>(x + off) = make_float4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
-                *reinterpret_cast<float4*>(m + off) = make_float4(ms[k][0], ms[k][1], ms[k][2], ms[k][3]);
-                *reinterpret_cast<float4*>(v + off) = make_float4(vs[k][0], vs[k][1], vs[k][2], vs[k][3]);
-            } else {
-                for (int r = 0; r < nr; ++r) {
-                    x[off + r] = xs[k][r];
-                    m[off + r] = ms[k][r];
-                    v[off + r] = vs[k][r];
-                }
-            }
-        }
-    }
-    if (st.has_anchor) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) pen += __shfl_xor_sync(0xffffffffu, pen, o);
-        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pen;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0;
-            for (int w = 0; w < 8; ++w) t += s_red[w];
-            if (t != 0.0) atomicAdd(penalty, t);
-        }
+// canonicalise (cloud.cpp:82-85): normalise, (0,0,0,0) -> (1,0,0,0), w >= 0;
+// one reciprocal per row, the sign flip folded into the scale
+__device__ __forceinline__ void canonicalize(float& qw, float& qx, float& qy, float& qz) {
+    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    if (qn == 0.f) {
+        qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
+    } else {
+        const float inv = (qw < 0.f ? -1.f : 1.f) / qn;
+        qw *= inv; qx *= inv; qy *= inv; qz *= inv;
     }
 }
 
-// Quaternion group, one row per thread: the 4 components are read as 4
-// coalesced scalar streams (x, m, v each), updated, canonicalised and written
-// back. One row per thread keeps the register count low enough for the
-// occupancy a 12-stream kernel needs.
-__global__ __launch_bounds__(256, 6) void adam_rot_kernel(float* __restrict__ x, float* __restrict__ m,
-                                                       float* __restrict__ v, size_t cap, uint32_t n,
-                                                       const uint32_t* __restrict__ vis_mask,
-                                                       const uint32_t* __restrict__ vis_prefix,
-                                                       const float* __restrict__ gbuf,
-                                                       const uint32_t* __restrict__ sh_mask,
-                                                       const uint32_t* __restrict__ sh_prefix,
-                                                       const float* __restrict__ z, const float* __restrict__ u,
-                                                       size_t ns, const float* __restrict__ rho_dev, AdamStep st,
-                                                       double* __restrict__ penalty) {
+// One 8-slot sector of row i (slots 8h .. 8h+7), with its slot -> component
+// mapping known at compile time.
+template <int fd, int h>
+__device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
+                                              size_t cap, uint32_t i, bool visible, uint32_t vpos, int aj,
+                                              const float* __restrict__ gbuf, const float* __restrict__ z,
+                                              const float* __restrict__ u, size_t ns,
+                                              const float* __restrict__ rho_dev, const AdamStep& st) {
+    constexpr int RS = row_stride(fd);
+    const size_t off = static_cast<size_t>(i) * RS + 8 * h;
+    float xs[8], ms[8], vs[8];
+    {
+        const float4* x4 = reinterpret_cast<const float4*>(x + off);
+        const float4* m4 = reinterpret_cast<const float4*>(m + off);
+        const float4* v4 = reinterpret_cast<const float4*>(v + off);
+        const float4 xa = x4[0], xb = x4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+        xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w; xs[4] = xb.x; xs[5] = xb.y; xs[6] = xb.z; xs[7] = xb.w;
+        ms[0] = ma.x; ms[1] = ma.y; ms[2] = ma.z; ms[3] = ma.w; ms[4] = mb.x; ms[5] = mb.y; ms[6] = mb.z; ms[7] = mb.w;
+        vs[0] = va.x; vs[1] = va.y; vs[2] = va.z; vs[3] = va.w; vs[4] = vb.x; vs[5] = vb.y; vs[6] = vb.z; vs[7] = vb.w;
+    }
+    float g[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int c = comp_of_slot(8 * h + j, fd);
+        g[j] = (visible && c >= 0) ? gbuf[static_cast<size_t>(c) * cap + vpos] : 0.f;
+    }
+    double pen = 0.0;
+    if (aj >= 0) {
+        float zr[8], ur[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = comp_of_slot(8 * h + j, fd);
+            zr[j] = c >= 0 ? z[static_cast<size_t>(c) * ns + aj] : 0.f;
+            ur[j] = c >= 0 ? u[static_cast<size_t>(c) * ns + aj] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = comp_of_slot(8 * h + j, fd);
+            if (c < 0) continue;
+            const float rho = rho_dev[c];
+            const float d = xs[j] - zr[j] + ur[j];
+            pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
+            g[j] += rho * d;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int c = comp_of_slot(8 * h + j, fd);
+        if (c >= 0) xs[j] = adam_update(xs[j], g[j], ms[j], vs[j], st.lr[c], st);
+    }
+    if (h == 1) canonicalize(xs[0], xs[1], xs[2], xs[3]);  // slots 8-11: the rotation
+    float4* x4 = reinterpret_cast<float4*>(x + off);
+    float4* m4 = reinterpret_cast<float4*>(m + off);
+    float4* v4 = reinterpret_cast<float4*>(v + off);
+    x4[0] = make_float4(xs[0], xs[1], xs[2], xs[3]);
+    x4[1] = make_float4(xs[4], xs[5], xs[6], xs[7]);
+    m4[0] = make_float4(ms[0], ms[1], ms[2], ms[3]);
+    m4[1] = make_float4(ms[4], ms[5], ms[6], ms[7]);
+    v4[0] = make_float4(vs[0], vs[1], vs[2], vs[3]);
+    v4[1] = make_float4(vs[4], vs[5], vs[6], vs[7]);
+    return pen;
+}
+
+template <int fd>
+__global__ __launch_bounds__(256, 4) void adam_rows_kernel(float* __restrict__ x, float* __restrict__ m,
+                                                        float* __restrict__ v, size_t cap, uint32_t n,
+                                                        const uint32_t* __restrict__ vis_mask,
+                                                        const uint32_t* __restrict__ vis_prefix,
+                                                        const float* __restrict__ gbuf,
+                                                        const uint32_t* __restrict__ sh_mask,
+                                                        const uint32_t* __restrict__ sh_prefix,
+                                                        const float* __restrict__ z, const float* __restrict__ u,
+                                                        size_t ns, const float* __restrict__ rho_dev, AdamStep st,
+                                                        double* __restrict__ penalty) {
     pdl_prologue();
     __shared__ double s_red[8];
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int H = fd <= 4 ? 2 : 3;  // sectors holding components (fd 12: slots 24-31 are padding)
+    const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t i = static_cast<uint32_t>(t / H);
+    const int h = static_cast<int>(t % H);
     double pen = 0.0;
     if (i < n) {
-        float xs[4], ms[4], vs[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const size_t off = static_cast<size_t>(kRot + k) * cap + i;
-            xs[k] = x[off];
-            ms[k] = m[off];
-            vs[k] = v[off];
-        }
         const uint32_t word = i >> 5, bit = i & 31u;
         const uint32_t vword = vis_mask[word];
         const bool visible = (vword >> bit) & 1u;
         const uint32_t vpos = visible ? vis_prefix[word] + __popc(vword & ((1u << bit) - 1u)) : 0u;
+        BSG_DASSERT(vpos <= cap);
         int aj = -1;
         if (st.has_anchor) {
             const uint32_t sm = sh_mask[word];
             if ((sm >> bit) & 1u) aj = static_cast<int>(sh_prefix[word] + __popc(sm & ((1u << bit) - 1u)));
+            BSG_DASSERT(aj < static_cast<int>(ns));
         }
-        float g[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) g[k] = visible ? gbuf[static_cast<size_t>(kRot + k) * cap + vpos] : 0.f;
-        if (aj >= 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float rho = rho_dev[kRot + k];
-                const float d = xs[k] - z[static_cast<size_t>(kRot + k) * ns + aj] + u[static_cast<size_t>(kRot + k) * ns + aj];
-                pen += 0.5 * static_cast<double>(rho) * static_cast<double>(d) * static_cast<double>(d);
-                g[k] += rho * d;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) xs[k] = adam_update(xs[k], g[k], ms[k], vs[k], st.lr[kRot + k], st);
-        // canonicalise (cloud.cpp:82-85): one reciprocal per row, sign flip folded into the scale
-        float qw = xs[0], qx = xs[1], qy = xs[2], qz = xs[3];
-        const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-        if (qn == 0.f) {
-            qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
-        } else {
-            const float inv = (qw < 0.f ? -1.f : 1.f) / qn;
-            qw *= inv; qx *= inv; qy *= inv; qz *= inv;
-        }
-        xs[0] = qw; xs[1] = qx; xs[2] = qy; xs[3] = qz;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const size_t off = static_cast<size_t>(kRot + k) * cap + i;
-            x[off] = xs[k];
-            m[off] = ms[k];
-            v[off] = vs[k];
-        }
+        if (h == 0)
+            pen = adam_sector<fd, 0>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
+        else if (h == 1)
+            pen = adam_sector<fd, 1>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
+        else if constexpr (H > 2)
+            pen = adam_sector<fd, 2>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
     }
     if (st.has_anchor) {
 #pragma unroll
@@ -471,9 +409,9 @@ __global__ __launch_bounds__(256, 6) void adam_rot_kernel(float* __restrict__ x,
         if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pen;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double t = 0;
-            for (int w = 0; w < 8; ++w) t += s_red[w];
-            if (t != 0.0) atomicAdd(penalty, t);
+            double tt = 0;
+            for (int w = 0; w < 8; ++w) tt += s_red[w];
+            if (tt != 0.0) atomicAdd(penalty, tt);
         }
     }
 }
@@ -511,17 +449,21 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     (void)step_index;
     if (c->n == 0) return;
     const uint32_t n = static_cast<uint32_t>(c->n);
-    const int scalar_groups = c->D - 4;  // every component but the quaternion
-    const dim3 g1(static_cast<uint32_t>((c->n + 1023) / 1024), static_cast<uint32_t>(scalar_groups));
-    launch_pdl(PdlAlways{}, c->stream, g1, 256, 0, adam_kernel<1>, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf,
-                                              c->sh_mask,
-                                              c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
-                                              &c->scalars->penalty);
-    BSG_LAUNCHED(c);
-    launch_pdl(PdlAlways{}, c->stream, static_cast<uint32_t>((c->n + 255) / 256), 256, 0, adam_rot_kernel, c->x, c->m, c->v, c->cap, n, c->vis_mask, c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u,
-        c->n_shared,
-        c->rho_dev, st, &c->scalars->penalty);
+    const size_t threads = static_cast<size_t>(n) * (c->fd <= 4 ? 2 : 3);
+    const uint32_t grid = static_cast<uint32_t>((threads + 255) / 256);
+    if (c->fd == 3)
+        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_rows_kernel<3>, c->x, c->m, c->v, c->cap, n, c->vis_mask,
+                   c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
+                   &c->scalars->penalty);
+    else
+        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_rows_kernel<12>, c->x, c->m, c->v, c->cap, n, c->vis_mask,
+                   c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
+                   &c->scalars->penalty);
     BSG_LAUNCHED(c);
 }
+
+// Every row's parameters current (the lazy Adam's catch-up): a no-op while
+// the update is dense.
+void materialize(Ctx* c) { (void)c; }
 
 }  // namespace bsg

@@ -44,6 +44,23 @@ constexpr double kSh1 = 0.4886025119029199;   // cloud.hpp:15
 constexpr int kPos = 0, kRot = 3, kLs = 7, kFeat = 10;
 __host__ __device__ inline int op_comp(int fd) { return kFeat + fd; }
 
+// Parameter and Adam-moment storage (x, m, v): row-major, row_stride(fd)
+// FP32 per row (64 B at SH degree 0, 128 B at degree 1), slots
+//   [pos0 pos1 pos2 ls0 ls1 ls2 op -][rot0 rot1 rot2 rot3 feat0 .. feat(fd-1) -..]
+// so the per-step culling read of every row (position + log-scale) is one
+// 32-byte sector and a whole row is 2 (4) sectors: the kernels that touch a
+// subset of rows (the preprocess's candidates, densification, consensus
+// packs) gather whole rows instead of one sector per component.
+__host__ __device__ constexpr int row_stride(int fd) { return fd <= 4 ? 16 : 32; }
+__host__ __device__ constexpr int pslot(int comp, int fd) {
+    return comp < kRot ? comp
+                       : (comp < kLs ? 8 + (comp - kRot)
+                                     : (comp < kFeat ? 3 + (comp - kLs) : (comp < kFeat + fd ? 12 + (comp - kFeat) : 6)));
+}
+__host__ __device__ inline size_t pidx(size_t row, int comp, int fd) {
+    return row * static_cast<size_t>(row_stride(fd)) + static_cast<size_t>(pslot(comp, fd));
+}
+
 // Camera as consumed by kernels (by value).
 struct DevCam {
     double fx, fy, cx, cy;
@@ -458,6 +475,7 @@ struct AdamStep {
 };
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
+void materialize(Ctx* c);
 void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty);
 bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt);
 // K1-K5 for one view (abi.cu), and the evaluation of one holdout view (eval.cu).

@@ -1,7 +1,7 @@
 // GSPL checkpoint payload on the device (scene_io.cpp:48-59). The float part
 // of the section is five row-interleaved arrays -- positions [n][3],
 // rotations [n][4], log-scales [n][3], features [n][F], opacity logits [n] --
-// i.e. the component-major device store [D][cap] transposed group by group.
+// gathered from the row-major device store (row_stride / pslot) group by group.
 // One streaming kernel writes it in section order (coalesced stores, reads of
 // w consecutive components of consecutive rows); the host prepends the count,
 // width and ids. HBM-bound: 4 D n bytes read, 4 D n written.
@@ -28,7 +28,7 @@ __global__ __launch_bounds__(256) void gspl_floats_kernel(const float* __restric
         else { local = e - s4; w = 1; c0 = op_comp(fd); }
         const uint64_t row = local / static_cast<uint64_t>(w);
         const int k = static_cast<int>(local - row * static_cast<uint64_t>(w));
-        out[e] = x[static_cast<size_t>(c0 + k) * cap + row];
+        out[e] = x[pidx(row, c0 + k, fd)];
     }
 }
 
@@ -38,6 +38,7 @@ void launch_gspl_floats(Ctx* c, float* out) {
     if (c->n == 0) return;
     const uint64_t total = static_cast<uint64_t>(11 + c->fd) * c->n;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+    materialize(c);
     gspl_floats_kernel<<<grid, 256, 0, c->stream>>>(c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, out);
     BSG_LAUNCHED(c);
 }

@@ -21,14 +21,14 @@ __device__ __forceinline__ float relaxed(float x, float zp, float alpha, bool bl
     return alpha * x + (1.0f - alpha) * zp;
 }
 
-__global__ void pack_q_kernel(const float* __restrict__ x, size_t cap, const uint32_t* __restrict__ rows,
+__global__ void pack_q_kernel(const float* __restrict__ x, int fd, const uint32_t* __restrict__ rows,
                               const uint32_t* __restrict__ slots, const uint8_t* __restrict__ first, size_t ns,
                               size_t S, float* __restrict__ qref) {
     const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (j >= ns || !first[j]) return;
     const uint32_t r = rows[j], s = slots[j];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) qref[c * S + s] = x[(kRot + c) * cap + r];
+    for (int c = 0; c < 4; ++c) qref[c * S + s] = x[pidx(r, kRot + c, fd)];
 }
 
 template <int D>
@@ -47,7 +47,7 @@ __global__ __launch_bounds__(256) void pack_main_kernel(const float* __restrict_
     float v[D], zp[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-        v[c] = x[c * cap + r];
+        v[c] = x[pidx(r, c, D - 11)];
         zp[c] = blend ? zprev[c * S + s] : 0.f;
     }
     float flip = 0.f;
@@ -95,7 +95,7 @@ __global__ __launch_bounds__(256) void dual_update_kernel(const float* __restric
         const uint32_t r = rows[j], s = slots[j];
         const bool reset = pack[static_cast<size_t>(D) * S + s] > 0.f || (slot_reset && slot_reset[s]);
         for (int c = 0; c < D; ++c) {
-            const float xv = x[c * cap + r];
+            const float xv = x[pidx(r, c, D - 11)];
             const float zn = zslot[c * S + s];
             const float xh = relaxed(xv, z[c * ns + j], alpha, relax != 0);
             const double dr = static_cast<double>(xv) - zn;
@@ -139,7 +139,7 @@ __global__ __launch_bounds__(256, 2) void unpack_own_kernel(const float* __restr
         for (int c = 0; c < D; ++c) {
             pk[c] = pack[c * S + s];
             zp[c] = zprev[c * S + s];
-            xv[c] = x[c * cap + r];
+            xv[c] = x[pidx(r, c, D - 11)];
             za[c] = z[c * ns + j];
             uv[c] = u[c * ns + j];
         }
@@ -202,7 +202,7 @@ __global__ void pack_minmax_kernel(const float* __restrict__ x, size_t cap, int 
     if (j >= ns) return;
     const uint32_t r = rows[j], s = slots[j];
     for (int c = 0; c < D; ++c) {
-        const float v = x[c * cap + r];
+        const float v = x[pidx(r, c, D - 11)];
         pack[c * S + s] = v;
         pack[(D + c) * S + s] = -v;
     }
@@ -281,7 +281,7 @@ __global__ void rho_components_kernel(const double* __restrict__ rs, int fd, flo
 void round_pack_q(Ctx* c) {
     BSG_CUDA(cudaMemsetAsync(c->qref, 0, 4 * c->n_slots * sizeof(float), c->stream));
     if (c->n_shared == 0) return;
-    pack_q_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(c->x, c->cap, c->sh_rows, c->sh_slots, c->sh_first,
+    pack_q_kernel<<<grid_for(c->n_shared), 256, 0, c->stream>>>(c->x, c->fd, c->sh_rows, c->sh_slots, c->sh_first,
                                                                  c->n_shared, c->n_slots, c->qref);
     BSG_LAUNCHED(c);
 }

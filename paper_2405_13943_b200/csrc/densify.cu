@@ -8,7 +8,7 @@
 // or bud one child (shared: the id must stay alive across blocks). Two scans
 // give every survivor its new row and every parent its first child slot; one
 // scatter pass writes the compacted parameters and Adam moments (survivors in
-// order, then the children in parent order, moments zero) into fresh [D][cap]
+// order, then the children in parent order, moments zero) into fresh row-major
 // buffers. Ids, the removed / new id lists and the shared-row bookkeeping are
 // updated on the host from the 1-byte action per row (one download per
 // densification, every `interval` iterations).
@@ -27,14 +27,14 @@ struct DensifyParams {
 
 // Offset of the children along the longest axis (trainer.cpp:327-331) and that
 // axis' scale; quat_normalized / quat_to_rotation as math.hpp:25-44.
-__device__ __forceinline__ double split_offset(const float* __restrict__ x, size_t cap, uint32_t i, double off[3]) {
-    const double s[3] = {exp(static_cast<double>(x[(kLs + 0) * cap + i])), exp(static_cast<double>(x[(kLs + 1) * cap + i])),
-                         exp(static_cast<double>(x[(kLs + 2) * cap + i]))};
+__device__ __forceinline__ double split_offset(const float* __restrict__ x, int fd, uint32_t i, double off[3]) {
+    const double s[3] = {exp(static_cast<double>(x[pidx(i, kLs + 0, fd)])), exp(static_cast<double>(x[pidx(i, kLs + 1, fd)])),
+                         exp(static_cast<double>(x[pidx(i, kLs + 2, fd)]))};
     int axis = 0;
     for (int a = 1; a < 3; ++a)
         if (s[a] > s[axis]) axis = a;  // Eigen maxCoeff: first maximum
-    double w = x[(kRot + 0) * cap + i], qx = x[(kRot + 1) * cap + i], qy = x[(kRot + 2) * cap + i],
-           qz = x[(kRot + 3) * cap + i];
+    double w = x[pidx(i, kRot + 0, fd)], qx = x[pidx(i, kRot + 1, fd)], qy = x[pidx(i, kRot + 2, fd)],
+           qz = x[pidx(i, kRot + 3, fd)];
     const double n = sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
     if (n == 0.0) {
         w = 1.0; qx = 0.0; qy = 0.0; qz = 0.0;
@@ -64,14 +64,14 @@ __global__ __launch_bounds__(256) void densify_classify_kernel(const float* __re
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint8_t act = kActKeep;
-    const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[(kFeat + fd) * cap + i])));  // cloud.hpp:55
+    const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[pidx(i, kFeat + fd, fd)])));  // cloud.hpp:55
     if (o < p.prune_opacity) {
         act = kActPrune;
     } else if (grad_seen[i] != 0) {
         const double mean_grad = static_cast<double>(grad_accum[i]) / grad_seen[i];
         if (!(mean_grad < p.grad_threshold)) {
             double off[3];
-            const double smax = split_offset(x, cap, i, off);
+            const double smax = split_offset(x, fd, i, off);
             const bool shared = (sh_mask[i >> 5] >> (i & 31)) & 1u;
             act = smax >= p.split_scale ? (shared ? kActBud : kActSplit) : kActClone;
         }
@@ -95,22 +95,24 @@ __global__ __launch_bounds__(256) void densify_scatter_kernel(const float* __res
     const uint8_t act = action[i];
     if (act != kActPrune && act != kActSplit) {
         const size_t r = keep_pos[i];
+        constexpr int RS = row_stride(D - 11);
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            nx[c * ncap + r] = x[c * cap + i];
-            nm[c * ncap + r] = m[c * cap + i];
-            nv[c * ncap + r] = v[c * cap + i];
+        for (int k = 0; k < RS; ++k) {  // whole rows (padding included)
+            nx[r * RS + k] = x[static_cast<size_t>(i) * RS + k];
+            nm[r * RS + k] = m[static_cast<size_t>(i) * RS + k];
+            nv[r * RS + k] = v[static_cast<size_t>(i) * RS + k];
         }
     }
     if (act == kActKeep || act == kActPrune) return;
     double off[3] = {0.0, 0.0, 0.0};
-    if (act != kActClone) split_offset(x, cap, i, off);
+    if (act != kActClone) split_offset(x, D - 11, i, off);
     const int count = act == kActSplit ? 2 : 1;
     for (int s = 0; s < count; ++s) {
         const size_t r = static_cast<size_t>(n_keep) + child_pos[i] + s;
+        constexpr int fd = D - 11;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            float val = x[c * cap + i];
+            float val = x[pidx(i, c, fd)];
             if (act != kActClone) {
                 if (c >= kPos && c < kPos + 3) {
                     const double o = s == 0 ? off[c - kPos] : -off[c - kPos];
@@ -119,9 +121,9 @@ __global__ __launch_bounds__(256) void densify_scatter_kernel(const float* __res
                     val = static_cast<float>(static_cast<double>(val) - log_shrink);
                 }
             }
-            nx[c * ncap + r] = val;
-            nm[c * ncap + r] = 0.f;  // remove_and_append appends zero moments
-            nv[c * ncap + r] = 0.f;
+            nx[pidx(r, c, fd)] = val;
+            nm[pidx(r, c, fd)] = 0.f;  // remove_and_append appends zero moments
+            nv[pidx(r, c, fd)] = 0.f;
         }
     }
 }
@@ -168,6 +170,7 @@ void maybe_densify(Ctx* c) {
     uint32_t* nchild = c->vrow[1];
     uint32_t* keep_pos = c->poff;
     uint32_t* child_pos = c->vis_rows;
+    materialize(c);
     densify_classify_kernel<<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->cap, n, c->fd, c->grad_accum,
                                                                     c->grad_seen, c->sh_mask, p, action, keep, nchild);
     BSG_LAUNCHED(c);
@@ -206,9 +209,13 @@ void maybe_densify(Ctx* c) {
     const size_t n_new = static_cast<size_t>(n_keep) + n_child;
     const size_t ncap = n_new <= c->cap ? c->cap : ((n_new + n_new / 4) + 31) / 32 * 32;
     float *nx = nullptr, *nm = nullptr, *nv = nullptr;
-    BSG_CUDA(cudaMalloc(&nx, c->D * ncap * sizeof(float)));
-    BSG_CUDA(cudaMalloc(&nm, c->D * ncap * sizeof(float)));
-    BSG_CUDA(cudaMalloc(&nv, c->D * ncap * sizeof(float)));
+    BSG_CUDA(cudaMalloc(&nx, row_stride(c->fd) * ncap * sizeof(float)));
+    BSG_CUDA(cudaMalloc(&nm, row_stride(c->fd) * ncap * sizeof(float)));
+    BSG_CUDA(cudaMalloc(&nv, row_stride(c->fd) * ncap * sizeof(float)));
+    // children rows are written slot by slot: their padding starts zeroed
+    BSG_CUDA(cudaMemsetAsync(nx, 0, row_stride(c->fd) * ncap * sizeof(float), c->stream));
+    BSG_CUDA(cudaMemsetAsync(nm, 0, row_stride(c->fd) * ncap * sizeof(float), c->stream));
+    BSG_CUDA(cudaMemsetAsync(nv, 0, row_stride(c->fd) * ncap * sizeof(float), c->stream));
     if (c->fd == 3)
         densify_scatter_kernel<14><<<(n + 255) / 256, 256, 0, c->stream>>>(
             c->x, c->m, c->v, c->cap, n, action, keep_pos, child_pos, n_keep, p.log_shrink, nx, nm, nv, ncap);

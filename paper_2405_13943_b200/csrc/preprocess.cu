@@ -73,16 +73,17 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
     for (int k = 0; k < 3; ++k) tf[k] = static_cast<float>(cam.t[k]);
     const float nearf = static_cast<float>(rc.near_plane);
     // all loads of the thread's rows first (one DRAM round trip), then the tests
+    // position + log-scale: the first 32-byte sector of the row (two float4)
+    const int rs = row_stride(fd);
     float pp[kPreRowsPerThread][3], ll[kPreRowsPerThread][3];
 #pragma unroll
     for (int k = 0; k < kPreRowsPerThread; ++k) {
         const uint32_t i = chunk0 + k * kPreThreads + threadIdx.x;
         const uint32_t j = i < n ? i : 0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            pp[k][a] = x[(kPos + a) * cap + j];
-            ll[k][a] = x[(kLs + a) * cap + j];
-        }
+        const float4* r4 = reinterpret_cast<const float4*>(x + static_cast<size_t>(j) * rs);
+        const float4 a = r4[0], b = r4[1];
+        pp[k][0] = a.x; pp[k][1] = a.y; pp[k][2] = a.z;
+        ll[k][0] = a.w; ll[k][1] = b.x; ll[k][2] = b.y;
     }
 #pragma unroll
     for (int k = 0; k < kPreRowsPerThread; ++k) {
@@ -125,20 +126,29 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
     uint32_t nvis = 0;
     for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
         const uint32_t i = s_rows[q];
-        // every parameter of the row up front: one dependent DRAM round trip
+        // the rest of the row up front (op, then rot + features: contiguous
+        // float4s of the row): one dependent DRAM round trip
         float prm[kMaxD];
+        const float4* r4 = reinterpret_cast<const float4*>(x + static_cast<size_t>(i) * rs);
 #pragma unroll
-        for (int k = 0; k < 11 + 3; ++k) {
-            if (k >= kPos && k < kPos + 3)
-                prm[k] = s_pl[k - kPos][q];
-            else if (k >= kLs && k < kLs + 3)
-                prm[k] = s_pl[3 + k - kLs][q];
-            else
-                prm[k] = x[k * cap + i];
+        for (int a = 0; a < 3; ++a) {
+            prm[kPos + a] = s_pl[a][q];
+            prm[kLs + a] = s_pl[3 + a][q];
         }
-        if (fd >= 12)
-#pragma unroll
-            for (int k = 14; k < 11 + kMaxFd; ++k) prm[k] = x[k * cap + i];
+        {
+            const float4 b = r4[1], c2 = r4[2], d = r4[3];
+            prm[kRot + 0] = c2.x; prm[kRot + 1] = c2.y; prm[kRot + 2] = c2.z; prm[kRot + 3] = c2.w;
+            prm[kFeat + 0] = d.x; prm[kFeat + 1] = d.y; prm[kFeat + 2] = d.z;
+            if (fd >= 12) {
+                prm[kFeat + 3] = d.w;
+                const float4 e = r4[4], f = r4[5];
+                prm[kFeat + 4] = e.x; prm[kFeat + 5] = e.y; prm[kFeat + 6] = e.z; prm[kFeat + 7] = e.w;
+                prm[kFeat + 8] = f.x; prm[kFeat + 9] = f.y; prm[kFeat + 10] = f.z; prm[kFeat + 11] = f.w;
+                prm[kFeat + 12] = b.z;  // op
+            } else {
+                prm[kFeat + 3] = b.z;  // op
+            }
+        }
         // the row's parameters, row-contiguous, for the fold's gather (64 / 96 B;
         // written for every FP32-test survivor, read only for visible rows)
 #pragma unroll
