@@ -89,7 +89,7 @@ void dev_alloc(T** p, size_t count) {
 void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
-    void* ptrs[] = {c->x, c->m, c->v, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
+    void* ptrs[] = {c->x, c->m, c->v, c->t_last, c->adam_ring, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->tile_cnt, c->tile_cur, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
@@ -406,6 +406,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
 void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc) { project_and_bin(c, cam, rc); }
 
 void alloc_row_scratch(Ctx* c, size_t cap) {
+    dev_alloc(&c->t_last, cap);
     dev_alloc(&c->grad_accum, cap);
     dev_alloc(&c->grad_seen, cap);
     dev_alloc(&c->rec, 3 * cap);
@@ -471,6 +472,7 @@ AdamStep make_adam_step(Ctx* c) {
     AdamStep st{};
     const bsg_trainer_config& t = c->tcfg;
     const uint64_t step = ++c->adam_t;  // trainer.cpp:267
+    st.t = static_cast<uint32_t>(step);
     const double progress = t.iterations > 0 ? static_cast<double>(c->iteration) / static_cast<double>(t.iterations) : 0.0;
     const double lr_pos = t.lr_position * std::pow(t.lr_position_decay, progress);  // trainer.cpp:268-271
     const double bc1 = 1.0 - std::pow(t.beta1, static_cast<double>(step));
@@ -740,6 +742,7 @@ int bsg_create(int device, int feature_dim, bsg_ctx** out) {
             BSG_CUDA(cudaMallocHost(&c->round_host, 16 * sizeof(double)));  // 8 round scalars + 5 rho
             dev_alloc(&c->rho_dev, kMaxD);
             dev_alloc(&c->rho_state, 5);
+            dev_alloc(&c->adam_ring, kAdamRing);
             dev_alloc(&c->g2d_wide, 9 * static_cast<size_t>(kWideCap));
             BSG_CUDA(cudaMallocHost(&c->counters_host, sizeof(StepCounters)));
             BSG_CUDA(cudaHostAlloc(&c->mbox, sizeof(Mailbox), cudaHostAllocMapped | cudaHostAllocPortable));
@@ -798,6 +801,7 @@ int bsg_upload_cloud(bsg_ctx* h, size_t n, const uint64_t* ids, const double* po
         BSG_CUDA(cudaMemsetAsync(c->sh_prefix, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->adam_t = 0;
+        fill_t_last(c, 0);
         c->iteration = 0;
         c->anchored = false;
         c->n_shared = 0;
@@ -1158,6 +1162,7 @@ int bsg_trainer_init(bsg_ctx* h, const bsg_trainer_config* cfg) {
         BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->adam_t = 0;
+        fill_t_last(c, 0);
         c->iteration = 0;
         bsg_densify_config& d = c->tcfg.densify;
         if (d.stop_iteration == 0) d.stop_iteration = (c->tcfg.iterations * 6) / 10;  // trainer.cpp:148-149
@@ -1352,6 +1357,7 @@ int bsg_set_shared(bsg_ctx* h, size_t ns, const uint32_t* rows, const uint32_t* 
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c) invalid("null context");
         use_device(c);
+        materialize(c);  // anchored rows are updated every step: none may be stale
         for (size_t j = 0; j < ns; ++j) {
             if (rows[j] >= c->n) invalid("shared rows missing from cloud");
             if (slots[j] >= n_slots) invalid("slot out of range");

@@ -9,6 +9,9 @@
 // x, m, v back; visible rows add a 4D-byte gradient read, shared rows z and u.
 #include "bsg_internal.cuh"
 
+#include <algorithm>
+#include <cmath>
+
 namespace bsg {
 namespace {
 
@@ -276,31 +279,7 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
 // forms (sqrt.approx, rcp-based division, ~2 ulp each on the update term, far
 // below the FP32 rounding of x itself).
 __device__ __forceinline__ float adam_update(float x, float g, float& m, float& v, float lr, const AdamStep& st) {
-    m = st.b1 * m + st.omb1 * g;
-    v = st.b2 * v + st.omb2 * g * g;
-    float sq;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * st.inv_bc2));
-    return x - lr * __fdividef(m * st.inv_bc1, sq + st.eps);
-}
-
-// Component stored in a slot of the row layout, -1 for padding (inverse of pslot).
-__host__ __device__ constexpr int comp_of_slot(int s, int fd) {
-    return s < 3 ? kPos + s
-                 : (s < 6 ? kLs + (s - 3)
-                          : (s == 6 ? kFeat + fd
-                                    : (s == 7 ? -1 : (s < 12 ? kRot + (s - 8) : (s < 12 + fd ? kFeat + (s - 12) : -1)))));
-}
-
-// canonicalise (cloud.cpp:82-85): normalise, (0,0,0,0) -> (1,0,0,0), w >= 0;
-// one reciprocal per row, the sign flip folded into the scale
-__device__ __forceinline__ void canonicalize(float& qw, float& qx, float& qy, float& qz) {
-    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-    if (qn == 0.f) {
-        qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
-    } else {
-        const float inv = (qw < 0.f ? -1.f : 1.f) / qn;
-        qw *= inv; qx *= inv; qy *= inv; qz *= inv;
-    }
+    return adam_update_step(x, g, m, v, lr, st.b1, st.omb1, st.b2, st.omb2, st.inv_bc1, st.inv_bc2, st.eps);
 }
 
 // One 8-slot sector of row i (slots 8h .. 8h+7), with its slot -> component
@@ -366,30 +345,47 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
     return pen;
 }
 
+// Sparse Adam (lazy Adam, bsg_internal.cuh): the rows with a gradient this
+// step -- the visible rows (their gradient at their visible position) and
+// the anchored rows (penalty rho (x - z + u)) -- all current (the preprocess
+// caught the visible ones up; anchored rows are updated every step). Thread
+// = one sector of one such row; the row's t_last becomes the step's count.
+// The first thread also files the step's constants in the ring.
 template <int fd>
-__global__ __launch_bounds__(256, 4) void adam_rows_kernel(float* __restrict__ x, float* __restrict__ m,
-                                                        float* __restrict__ v, size_t cap, uint32_t n,
-                                                        const uint32_t* __restrict__ vis_mask,
-                                                        const uint32_t* __restrict__ vis_prefix,
-                                                        const float* __restrict__ gbuf,
-                                                        const uint32_t* __restrict__ sh_mask,
-                                                        const uint32_t* __restrict__ sh_prefix,
-                                                        const float* __restrict__ z, const float* __restrict__ u,
-                                                        size_t ns, const float* __restrict__ rho_dev, AdamStep st,
-                                                        double* __restrict__ penalty) {
+__global__ __launch_bounds__(256, 4) void adam_sparse_kernel(float* __restrict__ x, float* __restrict__ m,
+                                                          float* __restrict__ v, size_t cap,
+                                                          const uint32_t* __restrict__ vis_rows, uint32_t V,
+                                                          const uint32_t* __restrict__ sh_rows, uint32_t n_sh,
+                                                          const uint32_t* __restrict__ vis_mask,
+                                                          const float* __restrict__ gbuf,
+                                                          const uint32_t* __restrict__ sh_mask,
+                                                          const uint32_t* __restrict__ sh_prefix,
+                                                          const float* __restrict__ z, const float* __restrict__ u,
+                                                          size_t ns, const float* __restrict__ rho_dev, AdamStep st,
+                                                          uint32_t* __restrict__ t_last, float4* __restrict__ ring,
+                                                          double* __restrict__ penalty) {
     pdl_prologue();
     __shared__ double s_red[8];
-    constexpr int H = fd <= 4 ? 2 : 3;  // sectors holding components (fd 12: slots 24-31 are padding)
+    constexpr int H = fd <= 4 ? 2 : 3;
     const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint32_t i = static_cast<uint32_t>(t / H);
+    if (t == 0) ring[st.t % kAdamRing] = make_float4(st.inv_bc1, st.inv_bc2, st.lr[kPos], 0.f);
+    const size_t idx = t / H;
     const int h = static_cast<int>(t % H);
     double pen = 0.0;
-    if (i < n) {
+    bool live = false;
+    uint32_t i = 0, vpos = 0;
+    bool visible = false;
+    if (idx < V) {
+        i = vis_rows[idx];
+        vpos = static_cast<uint32_t>(idx);
+        visible = true;
+        live = true;
+    } else if (idx < static_cast<size_t>(V) + n_sh && st.has_anchor) {
+        i = sh_rows[idx - V];
+        live = !((vis_mask[i >> 5] >> (i & 31u)) & 1u);  // visible anchored rows: done above
+    }
+    if (live) {
         const uint32_t word = i >> 5, bit = i & 31u;
-        const uint32_t vword = vis_mask[word];
-        const bool visible = (vword >> bit) & 1u;
-        const uint32_t vpos = visible ? vis_prefix[word] + __popc(vword & ((1u << bit) - 1u)) : 0u;
-        BSG_DASSERT(vpos <= cap);
         int aj = -1;
         if (st.has_anchor) {
             const uint32_t sm = sh_mask[word];
@@ -402,6 +398,7 @@ __global__ __launch_bounds__(256, 4) void adam_rows_kernel(float* __restrict__ x
             pen = adam_sector<fd, 1>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
         else if constexpr (H > 2)
             pen = adam_sector<fd, 2>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
+        if (h == 0) t_last[i] = st.t;
     }
     if (st.has_anchor) {
 #pragma unroll
@@ -414,6 +411,26 @@ __global__ __launch_bounds__(256, 4) void adam_rows_kernel(float* __restrict__ x
             if (tt != 0.0) atomicAdd(penalty, tt);
         }
     }
+}
+
+// Every stale row caught up to la.t (one thread per row, sector by sector).
+template <int fd>
+__global__ __launch_bounds__(256) void materialize_kernel(float* __restrict__ x, float* __restrict__ m,
+                                                          float* __restrict__ v, uint32_t n,
+                                                          uint32_t* __restrict__ t_last, LazyAdam la) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t0 = t_last[i];
+    if (t0 >= la.t) return;
+    BSG_DASSERT(la.t - t0 <= kAdamRing);
+    catch_up_row<fd>(x, m, v, i, t0, la);
+    t_last[i] = la.t;
+}
+
+__global__ void fill_u32_kernel(uint32_t* __restrict__ p, size_t n, uint32_t value) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = value;
 }
 
 }  // namespace
@@ -448,22 +465,70 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     (void)loss_out;
     (void)step_index;
     if (c->n == 0) return;
-    const uint32_t n = static_cast<uint32_t>(c->n);
-    const size_t threads = static_cast<size_t>(n) * (c->fd <= 4 ? 2 : 3);
-    const uint32_t grid = static_cast<uint32_t>((threads + 255) / 256);
+    const uint32_t V = c->last_counters.visible;
+    const uint32_t n_sh = st.has_anchor ? static_cast<uint32_t>(c->n_shared) : 0u;
+    const size_t threads = (static_cast<size_t>(V) + n_sh) * (c->fd <= 4 ? 2 : 3);
+    const uint32_t grid = static_cast<uint32_t>(std::max<size_t>(1, (threads + 255) / 256));
     if (c->fd == 3)
-        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_rows_kernel<3>, c->x, c->m, c->v, c->cap, n, c->vis_mask,
-                   c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
-                   &c->scalars->penalty);
+        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<3>, c->x, c->m, c->v, c->cap, c->vis_rows, V,
+                   c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
+                   c->rho_dev, st, c->t_last, c->adam_ring, &c->scalars->penalty);
     else
-        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_rows_kernel<12>, c->x, c->m, c->v, c->cap, n, c->vis_mask,
-                   c->vis_prefix, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st,
-                   &c->scalars->penalty);
+        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<12>, c->x, c->m, c->v, c->cap, c->vis_rows,
+                   V, c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
+                   c->rho_dev, st, c->t_last, c->adam_ring, &c->scalars->penalty);
+    BSG_LAUNCHED(c);
+    // every kAdamRing / 2 steps all rows catch up: a stale row never needs a
+    // step the ring no longer holds
+    if (st.t % (kAdamRing / 2) == 0) materialize(c);
+}
+
+LazyAdam make_lazy_adam(const Ctx* c) {
+    LazyAdam la{};
+    const bsg_trainer_config& t = c->tcfg;
+    la.b1 = static_cast<float>(t.beta1);
+    la.b2 = static_cast<float>(t.beta2);
+    la.omb1 = static_cast<float>(1.0 - t.beta1);
+    la.omb2 = static_cast<float>(1.0 - t.beta2);
+    la.eps = static_cast<float>(t.eps);
+    for (int k = 0; k < c->D; ++k) {
+        double lr = t.lr_features;
+        if (k < kRot) lr = t.lr_position;  // (the ring carries the decayed rate per step)
+        else if (k < kLs) lr = t.lr_rotation;
+        else if (k < kFeat) lr = t.lr_log_scale;
+        else if (k == op_comp(c->fd)) lr = t.lr_opacity;
+        la.lr[k] = static_cast<float>(lr);
+    }
+    la.ring = c->adam_ring;
+    la.t = static_cast<uint32_t>(c->adam_t);
+    // |m_hat / (sqrt(v_hat) + eps)| <= (1 - b1) sqrt(1 / (1 - b1^2 / b2)) / sqrt(1 - b2) (Cauchy-Schwarz on
+    // the moment sums; the bias corrections only shrink it), and a zero-gradient step scales it by
+    // rho = b1 / sqrt(b2): after k such steps a component has moved by at most
+    // bound * lr * rho (1 - rho^k) / (1 - rho). drift_* = bound * lr (with 1% slack);
+    // the preprocess multiplies by the geometric factor of the row's staleness.
+    const double b1 = t.beta1, b2 = t.beta2;
+    const double bound = (1.0 - b1) * std::sqrt(1.0 / (1.0 - b1 * b1 / b2)) / std::sqrt(1.0 - b2);
+    la.rho = static_cast<float>(b1 / std::sqrt(b2) * (1.0 + 1e-6));
+    la.drift_pos = static_cast<float>(1.01 * bound * std::max(t.lr_position, t.lr_position * t.lr_position_decay));
+    la.drift_ls = static_cast<float>(1.01 * bound * t.lr_log_scale);
+    return la;
+}
+
+void materialize(Ctx* c) {
+    if (c->n == 0 || c->adam_t == 0 || !c->t_last) return;
+    const LazyAdam la = make_lazy_adam(c);
+    const uint32_t n = static_cast<uint32_t>(c->n);
+    if (c->fd == 3)
+        materialize_kernel<3><<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->m, c->v, n, c->t_last, la);
+    else
+        materialize_kernel<12><<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->m, c->v, n, c->t_last, la);
     BSG_LAUNCHED(c);
 }
 
-// Every row's parameters current (the lazy Adam's catch-up): a no-op while
-// the update is dense.
-void materialize(Ctx* c) { (void)c; }
+void fill_t_last(Ctx* c, uint32_t value) {
+    if (c->cap == 0) return;
+    fill_u32_kernel<<<148 * 4, 256, 0, c->stream>>>(c->t_last, c->cap, value);
+    BSG_LAUNCHED(c);
+}
 
 }  // namespace bsg

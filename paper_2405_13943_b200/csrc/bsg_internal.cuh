@@ -222,6 +222,8 @@ struct Ctx {
     float4* pcache = nullptr;      // kParamVec float4 per row: the parameters of the rows the preprocess
                                    // found visible, row-contiguous for the fold's gather
     float* gbuf = nullptr;         // parameter gradient of the visible rows, [D][cap] by visible position
+    uint32_t* t_last = nullptr;    // Adam steps applied to each row (lazy Adam: stale while < adam_t)
+    float4* adam_ring = nullptr;   // per Adam step t, at t % kAdamRing: {1/bc1, 1/bc2, lr_pos, -}
     uint32_t* vis_prefix = nullptr;// visible rows before each 32-row word (visible position = prefix + rank in word)
     uint32_t* vis_mask = nullptr;  // 1 bit per row: visible this step (written by the compaction)
     uint32_t* sh_mask = nullptr;   // 1 bit per row: shared (has an anchor)
@@ -472,10 +474,109 @@ struct AdamStep {
     float b1, b2, eps, omb1, omb2;
     float inv_bc1, inv_bc2;
     int has_anchor;
+    uint32_t t;  // the step's Adam count (after the increment, trainer.cpp:267)
 };
+
+// ---- lazy Adam ------------------------------------------------------------
+// The reference's Adam is dense (every row, every step, trainer.cpp:267-281).
+// A row whose gradient is zero at a step (not visible, not anchored) evolves
+// there as m <- b1 m, v <- b2 v, x <- x - lr m_hat / (sqrt(v_hat) + eps) (then
+// the quaternion canonicalisation): a pure function of the row and the step's
+// constants. Such rows are left untouched and replayed -- the same FP32
+// operations, so bit-identical -- when they are next needed: by the
+// preprocess for a culling candidate, by materialize() before any host read
+// or densification, and every kAdamRing / 2 steps for all rows (the ring of
+// per-step constants covers kAdamRing steps). The sparse Adam updates only
+// the visible and anchored rows.
+constexpr uint32_t kAdamRing = 64;
+struct LazyAdam {
+    float b1, b2, eps, omb1, omb2;
+    float lr[kMaxD];        // lr of the components whose rate does not change (not used for positions)
+    const float4* ring;
+    uint32_t t;             // Adam steps applied so far (rows with t_last < t are stale)
+    float drift_pos, drift_ls;  // per-component drift bounds per unit of the geometric staleness factor
+    float rho;              // b1 / sqrt(b2): decay of |m_hat / sqrt(v_hat)| over a zero-gradient step
+};
+
+__device__ __forceinline__ float adam_update_step(float x, float g, float& m, float& v, float lr, float b1, float omb1,
+                                                  float b2, float omb2, float inv_bc1, float inv_bc2, float eps) {
+    m = b1 * m + omb1 * g;
+    v = b2 * v + omb2 * g * g;
+    float sq;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * inv_bc2));
+    return x - lr * __fdividef(m * inv_bc1, sq + eps);
+}
+
+// canonicalise (cloud.cpp:82-85): normalise, (0,0,0,0) -> (1,0,0,0), w >= 0;
+// one reciprocal per row, the sign flip folded into the scale
+__device__ __forceinline__ void canonicalize(float& qw, float& qx, float& qy, float& qz) {
+    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    if (qn == 0.f) {
+        qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
+    } else {
+        const float inv = (qw < 0.f ? -1.f : 1.f) / qn;
+        qw *= inv; qx *= inv; qy *= inv; qz *= inv;
+    }
+}
+
+// Component stored in a slot of the row layout, -1 for padding (inverse of pslot).
+__host__ __device__ constexpr int comp_of_slot(int s, int fd) {
+    return s < 3 ? kPos + s
+                 : (s < 6 ? kLs + (s - 3)
+                          : (s == 6 ? kFeat + fd
+                                    : (s == 7 ? -1 : (s < 12 ? kRot + (s - 8) : (s < 12 + fd ? kFeat + (s - 12) : -1)))));
+}
+
+// Replays Adam steps t0+1 .. la.t with zero gradient on sector h (slots
+// 8h .. 8h+7) of a row, in registers.
+template <int fd, int h>
+__device__ __forceinline__ void catch_up_sector(float (&xs)[8], float (&ms)[8], float (&vs)[8], uint32_t t0,
+                                                const LazyAdam& la) {
+    for (uint32_t t = t0 + 1; t <= la.t; ++t) {
+        const float4 k = la.ring[t % kAdamRing];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+                const int c = comp_of_slot(8 * h + j, fd);
+            if (c < 0) continue;
+            const float lr = c < kRot ? k.z : la.lr[c];
+            xs[j] = adam_update_step(xs[j], 0.f, ms[j], vs[j], lr, la.b1, la.omb1, la.b2, la.omb2, k.x, k.y, la.eps);
+        }
+        if (h == 1) canonicalize(xs[0], xs[1], xs[2], xs[3]);
+    }
+}
+
+// Brings row i (stale since t0) up to la.t in memory: x, m, v sector by sector.
+template <int fd>
+__device__ __forceinline__ void catch_up_row(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
+                                             uint32_t i, uint32_t t0, const LazyAdam& la) {
+    constexpr int RS = row_stride(fd), H = fd <= 4 ? 2 : 3;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        const size_t off = static_cast<size_t>(i) * RS + 8 * h;
+        float xs[8], ms[8], vs[8];
+        float4* x4 = reinterpret_cast<float4*>(x + off);
+        float4* m4 = reinterpret_cast<float4*>(m + off);
+        float4* v4 = reinterpret_cast<float4*>(v + off);
+        const float4 xa = x4[0], xb = x4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+        xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w; xs[4] = xb.x; xs[5] = xb.y; xs[6] = xb.z; xs[7] = xb.w;
+        ms[0] = ma.x; ms[1] = ma.y; ms[2] = ma.z; ms[3] = ma.w; ms[4] = mb.x; ms[5] = mb.y; ms[6] = mb.z; ms[7] = mb.w;
+        vs[0] = va.x; vs[1] = va.y; vs[2] = va.z; vs[3] = va.w; vs[4] = vb.x; vs[5] = vb.y; vs[6] = vb.z; vs[7] = vb.w;
+        if (h == 0) catch_up_sector<fd, 0>(xs, ms, vs, t0, la);
+        else if (h == 1) catch_up_sector<fd, 1>(xs, ms, vs, t0, la);
+        else catch_up_sector<fd, 2>(xs, ms, vs, t0, la);
+        x4[0] = make_float4(xs[0], xs[1], xs[2], xs[3]);
+        x4[1] = make_float4(xs[4], xs[5], xs[6], xs[7]);
+        m4[0] = make_float4(ms[0], ms[1], ms[2], ms[3]);
+        m4[1] = make_float4(ms[4], ms[5], ms[6], ms[7]);
+        v4[0] = make_float4(vs[0], vs[1], vs[2], vs[3]);
+        v4[1] = make_float4(vs[4], vs[5], vs[6], vs[7]);
+    }
+}
+LazyAdam make_lazy_adam(const Ctx* c);
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
 void materialize(Ctx* c);
+void fill_t_last(Ctx* c, uint32_t value);
 void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty);
 bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt);
 // K1-K5 for one view (abi.cu), and the evaluation of one holdout view (eval.cu).

@@ -235,6 +235,7 @@ void maybe_densify(Ctx* c) {
     c->ids = std::move(ids);
     BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
     BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
+    fill_t_last(c, static_cast<uint32_t>(c->adam_t));  // every row current (materialized above; children new)
     // shared rows (trainer.cpp:360-371): pruned shared ids leave the consensus;
     // survivors move to their new rows (split never applies to shared rows)
     if (c->n_shared) {

@@ -36,7 +36,9 @@ constexpr int kPreChunk = kPreThreads * kPreRowsPerThread;
 // the queue with every lane busy (rows are in id order, i.e. spatially random,
 // so doing this per thread would leave most lanes of a warp idle). The
 // visible set and every rect are exactly those of the exact path.
-__global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
+__global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __restrict__ x, float* __restrict__ m,
+                                                                 float* __restrict__ v, uint32_t* __restrict__ t_last,
+                                                                 LazyAdam la, uint32_t n,
                                                                  int fd, DevCam cam, DevRender rc,
                                                                  float4* __restrict__ rec,
                                                                  uint64_t* __restrict__ depth_key,
@@ -49,7 +51,6 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
                                                                  uint32_t* __restrict__ tile_cnt) {
     pdl_prologue();
     __shared__ uint32_t s_rows[kPreChunk];
-    __shared__ float s_pl[6][kPreChunk];  // a candidate's position + log-scale from phase 1 (not re-gathered)
     __shared__ uint32_t s_count;
     __shared__ unsigned long long s_zmin_inv, s_zmax;
     __shared__ uint32_t s_visible;
@@ -76,6 +77,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
     // position + log-scale: the first 32-byte sector of the row (two float4)
     const int rs = row_stride(fd);
     float pp[kPreRowsPerThread][3], ll[kPreRowsPerThread][3];
+    uint32_t stale[kPreRowsPerThread];  // Adam steps the row is behind (lazy Adam)
 #pragma unroll
     for (int k = 0; k < kPreRowsPerThread; ++k) {
         const uint32_t i = chunk0 + k * kPreThreads + threadIdx.x;
@@ -84,6 +86,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
         const float4 a = r4[0], b = r4[1];
         pp[k][0] = a.x; pp[k][1] = a.y; pp[k][2] = a.z;
         ll[k][0] = a.w; ll[k][1] = b.x; ll[k][2] = b.y;
+        stale[k] = la.t - t_last[j];
     }
 #pragma unroll
     for (int k = 0; k < kPreRowsPerThread; ++k) {
@@ -93,29 +96,39 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
         const float z = (Rf[6] * p0 + Rf[7] * p1) + Rf[8] * p2 + tf[2];
         const float px = (Rf[0] * p0 + Rf[1] * p1) + Rf[2] * p2 + tf[0];
         const float py = (Rf[3] * p0 + Rf[4] * p1) + Rf[5] * p2 + tf[1];
+        // A stale row's current position / log-scale lie within the lazy-Adam
+        // drift bound of the stored ones (bsg_internal.cuh, make_lazy_adam):
+        // per component dpos / dls, so the camera-space centre within
+        // delta = sqrt(3) dpos (R orthonormal).
+        float dpos = 0.f, dls = 0.f;
+        if (stale[k]) {
+            const float geo = la.rho * (1.f - __powf(la.rho, static_cast<float>(stale[k]))) / (1.f - la.rho);
+            dpos = la.drift_pos * geo * 1.01f;
+            dls = la.drift_ls * geo * 1.01f;
+        }
+        const float delta = 1.7321f * dpos;
         // FP32 z may differ from FP64 z by ~1e-6 |p|: keep anything that could be past the near plane
-        bool cand = z > nearf - 1e-3f * (1.0f + fabsf(p0) + fabsf(p1) + fabsf(p2));
-        if (cand && z > 0.5f * nearf) {
-            const float iz = 1.0f / z;
+        bool cand = z + delta > nearf - 1e-3f * (1.0f + fabsf(p0) + fabsf(p1) + fabsf(p2));
+        if (cand && z - delta > 0.5f * nearf) {
+            const float zl = z - delta, iz = 1.0f / zl, iz0 = 1.0f / z;
             const float fxz = fxf * iz, fyz = fyf * iz;
-            const float jx = fxz * px * iz, jy = fyz * py * iz;
+            const float ax = fabsf(px) + delta, ay = fabsf(py) + delta;
+            const float jx = fxz * ax * iz, jy = fyz * ay * iz;
             const float jf2 = fxz * fxz + fyz * fyz + jx * jx + jy * jy;
-            const float lmax = fmaxf(fmaxf(ll[k][0], ll[k][1]), ll[k][2]);
+            const float lmax = fmaxf(fmaxf(ll[k][0], ll[k][1]), ll[k][2]) + dls;
             const float smax = expf(lmax) * 1.01f;
             const float rb = static_cast<float>(rc.sigma_extent) * sqrtf(jf2 * smax * smax + static_cast<float>(rc.dilation)) * 1.01f + 2.0f;
-            const float mxf = fxz * px + cxf, myf = fyz * py + cyf;
-            if (mxf + rb < 0.f || mxf - rb > static_cast<float>(cam.W - 1) || myf + rb < 0.f ||
-                myf - rb > static_cast<float>(cam.H - 1))
+            // |d(f X / Z)| <= f delta (Z + |X|) / (Z (Z - delta)) for a centre moved by <= delta
+            const float sx = fxf * delta * (z + fabsf(px)) * iz0 * iz, sy = fyf * delta * (z + fabsf(py)) * iz0 * iz;
+            const float mxf = fxf * iz0 * px + cxf, myf = fyf * iz0 * py + cyf;
+            const float rx = rb + sx * 1.01f, ry = rb + sy * 1.01f;
+            if (mxf + rx < 0.f || mxf - rx > static_cast<float>(cam.W - 1) || myf + ry < 0.f ||
+                myf - ry > static_cast<float>(cam.H - 1))
                 cand = false;
         }
         if (cand) {
             const uint32_t q = atomicAdd(&s_count, 1u);
             s_rows[q] = i;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                s_pl[a][q] = pp[k][a];
-                s_pl[3 + a][q] = ll[k][a];
-            }
         } else {
             tiles[i] = 0;
         }
@@ -126,17 +139,25 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(const float*
     uint32_t nvis = 0;
     for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
         const uint32_t i = s_rows[q];
-        // the rest of the row up front (op, then rot + features: contiguous
-        // float4s of the row): one dependent DRAM round trip
+        // a stale candidate first catches up (lazy Adam: the same FP32 steps
+        // the dense update would have taken), then the whole row up front
+        // (contiguous float4s): one dependent DRAM round trip
+        {
+            const uint32_t t0 = t_last[i];
+            if (t0 < la.t) {
+                if (fd >= 12)
+                    catch_up_row<12>(x, m, v, i, t0, la);
+                else
+                    catch_up_row<3>(x, m, v, i, t0, la);
+                t_last[i] = la.t;
+            }
+        }
         float prm[kMaxD];
         const float4* r4 = reinterpret_cast<const float4*>(x + static_cast<size_t>(i) * rs);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            prm[kPos + a] = s_pl[a][q];
-            prm[kLs + a] = s_pl[3 + a][q];
-        }
         {
-            const float4 b = r4[1], c2 = r4[2], d = r4[3];
+            const float4 a = r4[0], b = r4[1], c2 = r4[2], d = r4[3];
+            prm[kPos + 0] = a.x; prm[kPos + 1] = a.y; prm[kPos + 2] = a.z;
+            prm[kLs + 0] = a.w; prm[kLs + 1] = b.x; prm[kLs + 2] = b.y;
             prm[kRot + 0] = c2.x; prm[kRot + 1] = c2.y; prm[kRot + 2] = c2.z; prm[kRot + 3] = c2.w;
             prm[kFeat + 0] = d.x; prm[kFeat + 1] = d.y; prm[kFeat + 2] = d.z;
             if (fd >= 12) {
@@ -343,7 +364,8 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
         return;
     }
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
-    launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->cap, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
+    const LazyAdam la = make_lazy_adam(c);
+    launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->m, c->v, c->t_last, la, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
                                                       c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters,
                                                       c->scalars, c->tile_cnt);
     BSG_LAUNCHED(c);
