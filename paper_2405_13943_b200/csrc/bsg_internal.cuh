@@ -498,6 +498,10 @@ struct LazyAdam {
     float rho;              // b1 / sqrt(b2): decay of |m_hat / sqrt(v_hat)| over a zero-gradient step
 };
 
+// One Adam step of one component (trainer.cpp:120-131); the sqrt and the
+// division are the approximate MUFU forms (~2 ulp each on the update term,
+// far below the FP32 rounding of x). Every Adam update and every lazy replay
+// runs this same function.
 __device__ __forceinline__ float adam_update_step(float x, float g, float& m, float& v, float lr, float b1, float omb1,
                                                   float b2, float omb2, float inv_bc1, float inv_bc2, float eps) {
     m = b1 * m + omb1 * g;
@@ -508,13 +512,15 @@ __device__ __forceinline__ float adam_update_step(float x, float g, float& m, fl
 }
 
 // canonicalise (cloud.cpp:82-85): normalise, (0,0,0,0) -> (1,0,0,0), w >= 0;
-// one reciprocal per row, the sign flip folded into the scale
+// one reciprocal square root per row, the sign flip folded into the scale
 __device__ __forceinline__ void canonicalize(float& qw, float& qx, float& qy, float& qz) {
-    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-    if (qn == 0.f) {
+    const float n2 = qw * qw + qx * qx + qy * qy + qz * qz;
+    if (n2 == 0.f) {
         qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
     } else {
-        const float inv = (qw < 0.f ? -1.f : 1.f) / qn;
+        float r;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(n2));
+        const float inv = qw < 0.f ? -r : r;
         qw *= inv; qx *= inv; qy *= inv; qz *= inv;
     }
 }
@@ -543,6 +549,28 @@ __device__ __forceinline__ void catch_up_sector(float (&xs)[8], float (&ms)[8], 
         }
         if (h == 1) canonicalize(xs[0], xs[1], xs[2], xs[3]);
     }
+}
+
+// Sector h of row i (stale since t0) brought up to la.t in memory.
+template <int fd, int h>
+__device__ __forceinline__ void catch_up_sector_mem(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
+                                                    uint32_t i, uint32_t t0, const LazyAdam& la) {
+    const size_t off = static_cast<size_t>(i) * row_stride(fd) + 8 * h;
+    float xs[8], ms[8], vs[8];
+    float4* x4 = reinterpret_cast<float4*>(x + off);
+    float4* m4 = reinterpret_cast<float4*>(m + off);
+    float4* v4 = reinterpret_cast<float4*>(v + off);
+    const float4 xa = x4[0], xb = x4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+    xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w; xs[4] = xb.x; xs[5] = xb.y; xs[6] = xb.z; xs[7] = xb.w;
+    ms[0] = ma.x; ms[1] = ma.y; ms[2] = ma.z; ms[3] = ma.w; ms[4] = mb.x; ms[5] = mb.y; ms[6] = mb.z; ms[7] = mb.w;
+    vs[0] = va.x; vs[1] = va.y; vs[2] = va.z; vs[3] = va.w; vs[4] = vb.x; vs[5] = vb.y; vs[6] = vb.z; vs[7] = vb.w;
+    catch_up_sector<fd, h>(xs, ms, vs, t0, la);
+    x4[0] = make_float4(xs[0], xs[1], xs[2], xs[3]);
+    x4[1] = make_float4(xs[4], xs[5], xs[6], xs[7]);
+    m4[0] = make_float4(ms[0], ms[1], ms[2], ms[3]);
+    m4[1] = make_float4(ms[4], ms[5], ms[6], ms[7]);
+    v4[0] = make_float4(vs[0], vs[1], vs[2], vs[3]);
+    v4[1] = make_float4(vs[4], vs[5], vs[6], vs[7]);
 }
 
 // Brings row i (stale since t0) up to la.t in memory: x, m, v sector by sector.
