@@ -204,13 +204,15 @@ def test_async_round_overlaps_next_step_exactly():
     # The two runs differ only by the order of the blend backward's FP32
     # atomics (the gradients agree to ~1e-7 relative); Adam turns that into
     # differences of up to 2 lr per step on coordinates whose gradient is
-    # near zero, so: every coordinate within that bound, 99% within 1e-5.
+    # near zero, so: every coordinate within that bound, all but 1% (at
+    # least 2) within 1e-5.
     ga, gb = a.download_cloud(), b.download_cloud()
     lr = {"pos": 1.6e-4, "rot": 1e-3, "ls": 5e-3, "feat": 2.5e-3, "op": 5e-2}
     for k in ("pos", "rot", "ls", "feat", "op"):
         err = np.abs(gb[k] - ga[k])
         assert np.all(err <= 2 * lr[k] * 8 + 1e-6), (k, err.max())
-        assert np.mean(err <= 1e-5 + 1e-4 * np.abs(ga[k])) >= 0.99, k
+        far = int(np.sum(err > 1e-5 + 1e-4 * np.abs(ga[k])))
+        assert far <= max(2, err.size // 100), (k, far)
 
 
 def test_async_round_then_densify_waits_for_the_round():
