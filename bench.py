@@ -40,11 +40,13 @@ CFGS = {
     "cfg2": dict(n=2_000_000, width=1024, height=768, views=64, extent=100.0, scale=1.4, seed=42, tilt=5.0),
     "cfg2_tilt30": dict(n=2_000_000, width=1024, height=768, views=64, extent=100.0, scale=1.4, seed=42, tilt=30.0),
     "cfg3": dict(n=6_000_000, width=1600, height=1066, views=96, extent=100.0, scale=1.4, seed=42, tilt=5.0),
+    "cfg4": dict(n=20_000_000, width=1600, height=1066, views=96, extent=100.0, scale=2.0, seed=42, tilt=5.0),
 }
 WORKLOAD = {
     "cfg2": "cfg2 (configs[1]): 2M Gaussians, 64 views 1024x768, 5 deg off nadir",
     "cfg2_tilt30": "cfg2 geometry at 30 deg off nadir (near-plane splats cover whole views)",
     "cfg3": "cfg3 (configs[2]): 6M Gaussians, 96 views 1600x1066, 5 deg off nadir",
+    "cfg4": "cfg4 (configs[3]): 20M Gaussians, K=8 at s=2.0 (high shared overlap), 1600x1066 views",
 }
 TRAIN_SEED = 1  # TrainerConfig::seed of both arms (view order)
 
@@ -349,17 +351,18 @@ def secondary(name, device, steps, warmup):
             "stage_ms": {k: round(v, 4) for k, v in stage.items()}, "wall_s": round(time.time() - t0, 1)}
 
 
-def consensus_k8(device, steps=100, interval=25):
-    """ADMM consensus ms/iter (BASELINE metric) of the K = 8 plan of cfg 3 on
-    one GPU: block 0 with its real shared set and slot table; the round's
-    device work (sign pre-pass, relaxed pack, unpack / duals / residuals,
-    device penalty adaptation) measured, asynchronous and synchronous, against
-    the same steps without rounds. One rank, so the all-reduce itself is not
-    on the wire; its payload is reported with a nominal NVLink 5 time."""
+def consensus_k8(device, name="cfg3", steps=100, interval=25):
+    """ADMM consensus ms/iter (BASELINE metric) of the K = 8 plan of cfg 3
+    (or cfg 4: s = 2.0, the consensus stress) on one GPU: block 0 with its
+    real shared set and slot table; the round's device work (sign pre-pass,
+    relaxed pack, unpack / duals / residuals, device penalty adaptation)
+    measured, asynchronous, against the same steps without rounds. One rank,
+    so the all-reduce itself is not on the wire; its payload is reported with
+    a nominal NVLink 5 time."""
     import torch
 
     from paper_2405_13943_b200 import api
-    cfg = CFGS["cfg3"]
+    cfg = CFGS[name]
     cloud, cams, init = scene(cfg)
     centers = np.array([c.center() for c in cams])
     plan = api.Plan(cloud["ids"], cloud["pos"], centers, 8, cfg["scale"])
@@ -397,7 +400,8 @@ def consensus_k8(device, steps=100, interval=25):
     payload = 4 * 4 * S + 4 * (D + 1) * S + 8 * 3
     est = 2 * (K - 1) / K * payload / 900e9 * 1e3
     rms = float(np.mean(rounds)) if rounds else None
-    return {"workload": "cfg3 K=8 plan, block 0 on this GPU (its real shared set), interval %d" % interval,
+    return {"workload": "%s K=8 plan (s=%.1f), block 0 on this GPU (its real shared set), interval %d" %
+                        (name, cfg["scale"], interval),
             "block0_gaussians": int(len(ids)), "block0_shared_rows": int(len(rows)), "global_shared_slots": int(S),
             "round_ms_device": rms, "consensus_ms_per_iter": (rms / interval) if rms else None,
             "ms_per_step_no_rounds": plain, "ms_per_step_async_rounds": with_async,
@@ -612,7 +616,8 @@ def run_ours(args, rank, world, local_rank):
         for name in ("cfg2", "cfg2_tilt30"):
             if name != args.config:
                 also[name] = secondary(name, device, max(args.steps, 100), max(args.warmup, 5))
-        also["consensus_k8"] = consensus_k8(device)
+        also["consensus_k8"] = consensus_k8(device, "cfg3")
+        also["consensus_cfg4_k8"] = consensus_k8(device, "cfg4")
         out["also"] = also
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args.gaussians)
