@@ -223,10 +223,15 @@ void ensure_image_buffers(Ctx* c, int W, int H) {
 // must not trigger one each time.
 void ensure_pair_capacity(Ctx* c, size_t P) {
     if (P <= c->pcap) return;
-    const size_t cap = std::max({2 * P, 2 * c->pcap, c->cap, static_cast<size_t>(1) << 20});
-    for (int k = 0; k < 2; ++k) {
-        dev_alloc(&c->pkey[k], cap);
-        dev_alloc(&c->pval[k], cap);
+    // Headroom of 2x the rows: a view sequence rarely needs a second growth.
+    // Stream-ordered: cudaFree would wait for the whole device (a growth in
+    // the middle of a run cost ~0.1 s that way) and stall the other streams.
+    const size_t cap = std::max({2 * P, 2 * c->pcap, 2 * c->cap, static_cast<size_t>(1) << 20});
+    uint32_t** bufs[4] = {&c->pkey[0], &c->pkey[1], &c->pval[0], &c->pval[1]};
+    for (uint32_t** p : bufs) {
+        if (*p) BSG_CUDA(cudaFreeAsync(*p, c->stream));
+        *p = nullptr;
+        BSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), cap * sizeof(uint32_t), c->stream));
     }
     c->pcap = cap;
 }
