@@ -181,6 +181,18 @@ int bsg_train_steps_host_u8(bsg_ctx* ctx, size_t n, const bsg_camera* cams, cons
 uint64_t bsg_iteration(const bsg_ctx* ctx);
 /* Optimizer moments, [D][n] component-major FP64 (D = 11 + fd), for parity. */
 int bsg_download_moments(bsg_ctx* ctx, double* m, double* v);
+/* Restores optimizer state (resume; the inverse of bsg_download_moments):
+ * moments [D][n] (v >= 0, finite) and the Adam step count t of
+ * OptimizerState (trainer.cpp:267) the bias corrections continue from. Call
+ * after bsg_trainer_init (which resets them). */
+int bsg_upload_moments(bsg_ctx* ctx, const double* m, const double* v, uint64_t adam_step);
+/* Lazy Adam: a row with no gradient and no penalty this step is not touched;
+ * the zero-gradient steps it skipped are replayed (the same FP32 operations,
+ * bit for bit) when it next becomes a projection candidate, before any host
+ * read, and for every row every `every` steps (1..32; default 32). 1 = the
+ * reference's dense update (trainer.cpp:120-131) applied to every row every
+ * step. The results do not depend on it; only the cost does. */
+int bsg_set_adam_sync_interval(bsg_ctx* ctx, uint32_t every);
 /* Densify statistics (trainer.cpp:284-289): grad_accum n, grad_seen n. */
 int bsg_download_densify_stats(bsg_ctx* ctx, double* grad_accum, uint32_t* grad_seen);
 /* take_removed_ids / take_new_rows (trainer.hpp:137-140): ids removed by

@@ -139,6 +139,8 @@ SYMBOLS = [
     ("bsg_train_steps_host_u8", ctypes.c_int, [_P, _SZ, ctypes.POINTER(bsg_camera), ctypes.POINTER(_U8P), _DP]),
     ("bsg_iteration", ctypes.c_uint64, [_P]),
     ("bsg_download_moments", ctypes.c_int, [_P, _DP, _DP]),
+    ("bsg_upload_moments", ctypes.c_int, [_P, _DP, _DP, ctypes.c_uint64]),
+    ("bsg_set_adam_sync_interval", ctypes.c_int, [_P, ctypes.c_uint32]),
     ("bsg_take_removed_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
     ("bsg_take_new_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
     ("bsg_shared_ids", ctypes.c_int, [_P, _U64P, _SZ, _SZP]),
@@ -463,6 +465,16 @@ class Block:
         m, v = np.zeros((self.D, self.n)), np.zeros((self.D, self.n))
         _check(_lib.bsg_download_moments(self.h, _ptr(m, ctypes.c_double), _ptr(v, ctypes.c_double)))
         return m, v
+
+    def upload_moments(self, m, v, adam_step):
+        """Optimizer state for a resume: m, v [D][n], the Adam step count."""
+        m = np.ascontiguousarray(m, np.float64).reshape(self.D, self.n)
+        v = np.ascontiguousarray(v, np.float64).reshape(self.D, self.n)
+        _check(_lib.bsg_upload_moments(self.h, _ptr(m, ctypes.c_double), _ptr(v, ctypes.c_double), int(adam_step)))
+
+    def set_adam_sync_interval(self, every):
+        """Lazy Adam: every row caught up every `every` steps (1 = dense)."""
+        _check(_lib.bsg_set_adam_sync_interval(self.h, int(every)))
 
     def _id_list(self, fn):
         n = ctypes.c_size_t()

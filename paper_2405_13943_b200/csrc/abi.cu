@@ -1302,6 +1302,41 @@ int bsg_download_moments(bsg_ctx* h, double* m, double* v) {
     });
 }
 
+int bsg_upload_moments(bsg_ctx* h, const double* m, const double* v, uint64_t adam_step) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (c->n > 0 && (!m || !v)) invalid("null moment array");
+        if (adam_step >= (1ull << 31)) invalid("adam step out of range");
+        use_device(c);
+        const size_t n = c->n, cap = c->cap;
+        const int fd = c->fd;
+        for (size_t i = 0; i < static_cast<size_t>(c->D) * n; ++i)
+            if (!(v[i] >= 0.0) || !std::isfinite(v[i]) || !std::isfinite(m[i])) invalid("moments not finite or v < 0");
+        std::vector<float> hm(row_stride(fd) * cap, 0.f), hv(row_stride(fd) * cap, 0.f);
+        for (int k = 0; k < c->D; ++k)
+            for (size_t i = 0; i < n; ++i) {
+                hm[pidx(i, k, fd)] = static_cast<float>(m[k * n + i]);
+                hv[pidx(i, k, fd)] = static_cast<float>(v[k * n + i]);
+            }
+        if (c->round_pending) throw Error{BSG_ERR_STATE, "upload_moments while a consensus round is pending"};
+        BSG_CUDA(cudaMemcpyAsync(c->m, hm.data(), hm.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(c->v, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        c->adam_t = adam_step;
+        fill_t_last(c, static_cast<uint32_t>(adam_step));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int bsg_set_adam_sync_interval(bsg_ctx* h, uint32_t every) {
+    return guarded([&] {
+        auto* c = reinterpret_cast<Ctx*>(h);
+        if (!c) invalid("null context");
+        if (every < 1 || every > kAdamRing / 2) invalid("adam sync interval outside 1..32");
+        c->adam_sync = every;
+    });
+}
+
 int bsg_download_densify_stats(bsg_ctx* h, double* ga, uint32_t* gs) {
     return guarded([&] {
         auto* c = reinterpret_cast<Ctx*>(h);

@@ -478,9 +478,9 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
                    V, c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
                    c->rho_dev, st, c->t_last, c->adam_ring, &c->scalars->penalty);
     BSG_LAUNCHED(c);
-    // every kAdamRing / 2 steps all rows catch up: a stale row never needs a
-    // step the ring no longer holds
-    if (st.t % (kAdamRing / 2) == 0) materialize(c);
+    // every adam_sync (<= kAdamRing / 2) steps all rows catch up: a stale row
+    // never needs a step the ring no longer holds
+    if (st.t % c->adam_sync == 0) materialize(c);
 }
 
 LazyAdam make_lazy_adam(const Ctx* c) {

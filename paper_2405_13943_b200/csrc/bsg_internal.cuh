@@ -291,6 +291,7 @@ struct Ctx {
     bsg_trainer_config tcfg{};
     uint64_t iteration = 0;
     uint64_t adam_t = 0;
+    uint32_t adam_sync = 32;       // every row caught up every adam_sync steps (1 = dense Adam; <= kAdamRing / 2)
     // densification (trainer.cpp:301-385)
     double scene_extent = 1e-9;
     uint64_t alloc_next = 0, alloc_end = 0;  // IdAllocator
@@ -501,20 +502,23 @@ struct LazyAdam {
 // One Adam step of one component (trainer.cpp:120-131); the sqrt and the
 // division are the approximate MUFU forms (~2 ulp each on the update term,
 // far below the FP32 rounding of x). Every Adam update and every lazy replay
-// runs this same function.
+// runs this same function, and every rounding is spelled out (explicit
+// _rn intrinsics), so its bits do not depend on the file's --fmad setting:
+// the replay in the preprocess (--fmad=false) and in the Adam kernels give
+// the dense update's bits exactly (tests/test_gpu_lazy_adam.py).
 __device__ __forceinline__ float adam_update_step(float x, float g, float& m, float& v, float lr, float b1, float omb1,
                                                   float b2, float omb2, float inv_bc1, float inv_bc2, float eps) {
-    m = b1 * m + omb1 * g;
-    v = b2 * v + omb2 * g * g;
+    m = __fmaf_rn(b1, m, __fmul_rn(omb1, g));
+    v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(omb2, g), g));
     float sq;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * inv_bc2));
-    return x - lr * __fdividef(m * inv_bc1, sq + eps);
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(__fmul_rn(v, inv_bc2)));
+    return __fmaf_rn(-lr, __fdividef(__fmul_rn(m, inv_bc1), __fadd_rn(sq, eps)), x);
 }
 
 // canonicalise (cloud.cpp:82-85): normalise, (0,0,0,0) -> (1,0,0,0), w >= 0;
 // one reciprocal square root per row, the sign flip folded into the scale
 __device__ __forceinline__ void canonicalize(float& qw, float& qx, float& qy, float& qz) {
-    const float n2 = qw * qw + qx * qx + qy * qy + qz * qz;
+    const float n2 = __fmaf_rn(qz, qz, __fmaf_rn(qy, qy, __fmaf_rn(qx, qx, __fmul_rn(qw, qw))));
     if (n2 == 0.f) {
         qw = 1.f; qx = 0.f; qy = 0.f; qz = 0.f;
     } else {
