@@ -23,6 +23,22 @@ __device__ __forceinline__ int to_int_clamped(double v) {
     return static_cast<int>(v);
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float exp2f_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 constexpr int kPreThreads = 256;
 constexpr int kPreRowsPerThread = 4;
 constexpr int kPreChunk = kPreThreads * kPreRowsPerThread;
@@ -88,40 +104,48 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
         ll[k][0] = a.w; ll[k][1] = b.x; ll[k][2] = b.y;
         stale[k] = la.t - t_last[j];
     }
+    // The test is FP32 with explicit FMAs (this file is compiled --fmad=false
+    // for the exact FP64 path below) and approximate MUFU reciprocals /
+    // exponentials / roots: every bound carries 1% + 2 px of slack, far above
+    // their few-ulp errors.
+    const float lg_rho = __log2f(la.rho), geo_scale = la.rho / (1.f - la.rho);
+    const float sig = static_cast<float>(rc.sigma_extent), dil = static_cast<float>(rc.dilation);
 #pragma unroll
     for (int k = 0; k < kPreRowsPerThread; ++k) {
         const uint32_t i = chunk0 + k * kPreThreads + threadIdx.x;
         if (i >= n) break;
         const float p0 = pp[k][0], p1 = pp[k][1], p2 = pp[k][2];
-        const float z = (Rf[6] * p0 + Rf[7] * p1) + Rf[8] * p2 + tf[2];
-        const float px = (Rf[0] * p0 + Rf[1] * p1) + Rf[2] * p2 + tf[0];
-        const float py = (Rf[3] * p0 + Rf[4] * p1) + Rf[5] * p2 + tf[1];
+        const float z = fmaf(Rf[8], p2, fmaf(Rf[7], p1, fmaf(Rf[6], p0, tf[2])));
+        const float px = fmaf(Rf[2], p2, fmaf(Rf[1], p1, fmaf(Rf[0], p0, tf[0])));
+        const float py = fmaf(Rf[5], p2, fmaf(Rf[4], p1, fmaf(Rf[3], p0, tf[1])));
         // A stale row's current position / log-scale lie within the lazy-Adam
         // drift bound of the stored ones (bsg_internal.cuh, make_lazy_adam):
         // per component dpos / dls, so the camera-space centre within
         // delta = sqrt(3) dpos (R orthonormal).
         float dpos = 0.f, dls = 0.f;
         if (stale[k]) {
-            const float geo = la.rho * (1.f - __powf(la.rho, static_cast<float>(stale[k]))) / (1.f - la.rho);
-            dpos = la.drift_pos * geo * 1.01f;
-            dls = la.drift_ls * geo * 1.01f;
+            const float geo = geo_scale * (1.f - exp2f_approx(static_cast<float>(stale[k]) * lg_rho)) * 1.01f;
+            dpos = la.drift_pos * geo;
+            dls = la.drift_ls * geo;
         }
         const float delta = 1.7321f * dpos;
         // FP32 z may differ from FP64 z by ~1e-6 |p|: keep anything that could be past the near plane
         bool cand = z + delta > nearf - 1e-3f * (1.0f + fabsf(p0) + fabsf(p1) + fabsf(p2));
         if (cand && z - delta > 0.5f * nearf) {
-            const float zl = z - delta, iz = 1.0f / zl, iz0 = 1.0f / z;
+            const float iz = rcp_approx(z - delta), iz0 = rcp_approx(z);
             const float fxz = fxf * iz, fyz = fyf * iz;
             const float ax = fabsf(px) + delta, ay = fabsf(py) + delta;
             const float jx = fxz * ax * iz, jy = fyz * ay * iz;
-            const float jf2 = fxz * fxz + fyz * fyz + jx * jx + jy * jy;
+            const float jf2 = fmaf(jy, jy, fmaf(jx, jx, fmaf(fyz, fyz, fxz * fxz)));
             const float lmax = fmaxf(fmaxf(ll[k][0], ll[k][1]), ll[k][2]) + dls;
-            const float smax = expf(lmax) * 1.01f;
-            const float rb = static_cast<float>(rc.sigma_extent) * sqrtf(jf2 * smax * smax + static_cast<float>(rc.dilation)) * 1.01f + 2.0f;
+            const float smax = exp2f_approx(lmax * 1.44269504f) * 1.01f;
+            const float rb = fmaf(sig * 1.01f, sqrt_approx(fmaf(jf2 * smax, smax, dil)), 2.0f);
             // |d(f X / Z)| <= f delta (Z + |X|) / (Z (Z - delta)) for a centre moved by <= delta
-            const float sx = fxf * delta * (z + fabsf(px)) * iz0 * iz, sy = fyf * delta * (z + fabsf(py)) * iz0 * iz;
-            const float mxf = fxf * iz0 * px + cxf, myf = fyf * iz0 * py + cyf;
-            const float rx = rb + sx * 1.01f, ry = rb + sy * 1.01f;
+            const float dz = delta * iz0 * iz * 1.01f;
+            const float rx = fmaf(fxf * dz, z + fabsf(px), rb), ry = fmaf(fyf * dz, z + fabsf(py), rb);
+            const float mxf = fmaf(fxf * iz0, px, cxf), myf = fmaf(fyf * iz0, py, cyf);
+            // (the image bounds converted here, not hoisted out of the loop:
+            // nvcc 12.9 dropped this whole test when they were)
             if (mxf + rx < 0.f || mxf - rx > static_cast<float>(cam.W - 1) || myf + ry < 0.f ||
                 myf - ry > static_cast<float>(cam.H - 1))
                 cand = false;
