@@ -67,7 +67,10 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
                                                                  uint32_t* __restrict__ tile_cnt) {
     pdl_prologue();
     __shared__ uint32_t s_rows[kPreChunk];
-    __shared__ uint32_t s_count;
+    __shared__ uint8_t s_stale[kPreChunk];     // Adam steps each queued row is behind (lazy Adam)
+    __shared__ uint16_t s_by_stale[kPreChunk];  // queue positions of the stale rows, most stale first
+    __shared__ uint32_t s_bin[kAdamRing];
+    __shared__ uint32_t s_count, s_nstale;
     __shared__ unsigned long long s_zmin_inv, s_zmax;
     __shared__ uint32_t s_visible;
     if (threadIdx.x == 0) {
@@ -153,29 +156,61 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
         if (cand) {
             const uint32_t q = atomicAdd(&s_count, 1u);
             s_rows[q] = i;
+            s_stale[q] = static_cast<uint8_t>(stale[k]);
         } else {
             tiles[i] = 0;
         }
     }
+    if (threadIdx.x < kAdamRing) s_bin[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t count = s_count;
+    // Lazy-Adam catch-up of the stale queued rows, before the projection
+    // reads them: one (row, 32-byte sector) per thread, the rows ordered by
+    // staleness so that the lanes of a warp replay the same number of steps
+    // (in queue order the warp ran as long as its stalest row, most lanes
+    // idle), and every warp of the CTA takes part.
+    for (uint32_t q = threadIdx.x; q < count; q += kPreThreads)
+        if (s_stale[q]) atomicAdd(&s_bin[kAdamRing - 1 - s_stale[q]], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 64 bins (most stale first), in place
+        const uint32_t a = s_bin[2 * threadIdx.x], b = s_bin[2 * threadIdx.x + 1];
+        uint32_t inc = a + b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (threadIdx.x >= o) inc += y;
+        }
+        s_bin[2 * threadIdx.x] = inc - a - b;
+        s_bin[2 * threadIdx.x + 1] = inc - b;
+        if (threadIdx.x == 31) s_nstale = inc;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < count; q += kPreThreads)
+        if (s_stale[q]) s_by_stale[atomicAdd(&s_bin[kAdamRing - 1 - s_stale[q]], 1u)] = static_cast<uint16_t>(q);
+    __syncthreads();
+    {
+        const int H = fd >= 12 ? 3 : 2;
+        const uint32_t items = s_nstale * H;
+        for (uint32_t it = threadIdx.x; it < items; it += kPreThreads) {
+            const uint32_t q = s_by_stale[it / H], h = it % H;
+            const uint32_t i = s_rows[q], t0 = la.t - s_stale[q];
+            if (fd >= 12) {
+                if (h == 0) catch_up_sector_mem<12, 0>(x, m, v, i, t0, la);
+                else if (h == 1) catch_up_sector_mem<12, 1>(x, m, v, i, t0, la);
+                else catch_up_sector_mem<12, 2>(x, m, v, i, t0, la);
+            } else {
+                if (h == 0) catch_up_sector_mem<3, 0>(x, m, v, i, t0, la);
+                else catch_up_sector_mem<3, 1>(x, m, v, i, t0, la);
+            }
+        }
+    }
+    __syncthreads();  // (the caught-up rows are read back below by other threads of the CTA)
     unsigned long long zmin_inv = 0, zmax = 0;  // depth range of this thread's visible splats
     uint32_t nvis = 0;
     for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
         const uint32_t i = s_rows[q];
-        // a stale candidate first catches up (lazy Adam: the same FP32 steps
-        // the dense update would have taken), then the whole row up front
-        // (contiguous float4s): one dependent DRAM round trip
-        {
-            const uint32_t t0 = t_last[i];
-            if (t0 < la.t) {
-                if (fd >= 12)
-                    catch_up_row<12>(x, m, v, i, t0, la);
-                else
-                    catch_up_row<3>(x, m, v, i, t0, la);
-                t_last[i] = la.t;
-            }
-        }
+        if (s_stale[q]) t_last[i] = la.t;
+        // the whole row up front (contiguous float4s): one dependent DRAM round trip
         float prm[kMaxD];
         const float4* r4 = reinterpret_cast<const float4*>(x + static_cast<size_t>(i) * rs);
         {
