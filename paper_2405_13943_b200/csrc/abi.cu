@@ -89,7 +89,7 @@ void dev_alloc(T** p, size_t count) {
 void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
-    void* ptrs[] = {c->x, c->m, c->v, c->t_last, c->adam_ring, c->grad_accum, c->grad_seen, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
+    void* ptrs[] = {c->x, c->m, c->v, c->vis_sgn, c->adam_ring, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->tile_cnt, c->tile_cur, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
@@ -411,9 +411,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
 void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc) { project_and_bin(c, cam, rc); }
 
 void alloc_row_scratch(Ctx* c, size_t cap) {
-    dev_alloc(&c->t_last, cap);
-    dev_alloc(&c->grad_accum, cap);
-    dev_alloc(&c->grad_seen, cap);
+    dev_alloc(&c->vis_sgn, cap);
     dev_alloc(&c->rec, 3 * cap);
     dev_alloc(&c->depth_key, cap);
     dev_alloc(&c->tiles, cap);
@@ -797,16 +795,14 @@ int bsg_upload_cloud(bsg_ctx* h, size_t n, const uint64_t* ids, const double* po
         c->ids.assign(ids, ids + n);
         alloc_rows(c, n);
         upload_params(c, pos, rot, ls, feat, op);
-        BSG_CUDA(cudaMemsetAsync(c->m, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
+        BSG_CUDA(cudaMemsetAsync(c->m, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));  // (densify stats too)
         BSG_CUDA(cudaMemsetAsync(c->v, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->vis_mask, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->sh_mask, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
         BSG_CUDA(cudaMemsetAsync(c->sh_prefix, 0, c->cap / 32 * sizeof(uint32_t), c->stream));
-        BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->adam_t = 0;
-        fill_t_last(c, 0);
+        reset_row_meta(c, 0, false);
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->iteration = 0;
         c->anchored = false;
         c->n_shared = 0;
@@ -1159,15 +1155,14 @@ int bsg_trainer_init(bsg_ctx* h, const bsg_trainer_config* cfg) {
     return guarded([&] {
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c) invalid("null context");
-        if (cfg) c->tcfg = *cfg; else bsg_default_trainer_config(&c->tcfg);
         use_device(c);
-        BSG_CUDA(cudaMemsetAsync(c->m, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
+        materialize(c);  // the parameters current under the previous optimizer state (and its config)
+        if (cfg) c->tcfg = *cfg; else bsg_default_trainer_config(&c->tcfg);
+        BSG_CUDA(cudaMemsetAsync(c->m, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));  // (densify stats too)
         BSG_CUDA(cudaMemsetAsync(c->v, 0, row_stride(c->fd) * c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
-        BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->adam_t = 0;
-        fill_t_last(c, 0);
+        reset_row_meta(c, 0, false);
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         c->iteration = 0;
         bsg_densify_config& d = c->tcfg.densify;
         if (d.stop_iteration == 0) d.stop_iteration = (c->tcfg.iterations * 6) / 10;  // trainer.cpp:148-149
@@ -1313,17 +1308,23 @@ int bsg_upload_moments(bsg_ctx* h, const double* m, const double* v, uint64_t ad
         const int fd = c->fd;
         for (size_t i = 0; i < static_cast<size_t>(c->D) * n; ++i)
             if (!(v[i] >= 0.0) || !std::isfinite(v[i]) || !std::isfinite(m[i])) invalid("moments not finite or v < 0");
-        std::vector<float> hm(row_stride(fd) * cap, 0.f), hv(row_stride(fd) * cap, 0.f);
+        if (c->round_pending) throw Error{BSG_ERR_STATE, "upload_moments while a consensus round is pending"};
+        // the parameters current under the old state first; the rows' metadata
+        // slots (densify statistics) kept
+        materialize(c);
+        std::vector<float> hm(row_stride(fd) * cap), hv(row_stride(fd) * cap);
+        BSG_CUDA(cudaMemcpyAsync(hm.data(), c->m, hm.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaMemcpyAsync(hv.data(), c->v, hv.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaStreamSynchronize(c->stream));
         for (int k = 0; k < c->D; ++k)
             for (size_t i = 0; i < n; ++i) {
                 hm[pidx(i, k, fd)] = static_cast<float>(m[k * n + i]);
                 hv[pidx(i, k, fd)] = static_cast<float>(v[k * n + i]);
             }
-        if (c->round_pending) throw Error{BSG_ERR_STATE, "upload_moments while a consensus round is pending"};
         BSG_CUDA(cudaMemcpyAsync(c->m, hm.data(), hm.size() * 4, cudaMemcpyHostToDevice, c->stream));
         BSG_CUDA(cudaMemcpyAsync(c->v, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, c->stream));
         c->adam_t = adam_step;
-        fill_t_last(c, static_cast<uint32_t>(adam_step));
+        reset_row_meta(c, static_cast<uint32_t>(adam_step), false);
         BSG_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
@@ -1342,9 +1343,13 @@ int bsg_download_densify_stats(bsg_ctx* h, double* ga, uint32_t* gs) {
         auto* c = reinterpret_cast<Ctx*>(h);
         if (!c) invalid("null context");
         use_device(c);
+        // (the rows' metadata slot of m and v, bsg_internal.cuh)
         std::vector<float> a(c->n);
-        if (c->n) BSG_CUDA(cudaMemcpyAsync(a.data(), c->grad_accum, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
-        if (gs && c->n) BSG_CUDA(cudaMemcpyAsync(gs, c->grad_seen, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+        const size_t pitch = row_stride(c->fd) * sizeof(float);
+        if (c->n)
+            BSG_CUDA(cudaMemcpy2DAsync(a.data(), 4, c->m + kMetaSlot, pitch, 4, c->n, cudaMemcpyDeviceToHost, c->stream));
+        if (gs && c->n)
+            BSG_CUDA(cudaMemcpy2DAsync(gs, 4, c->v + kMetaSlot, pitch, 4, c->n, cudaMemcpyDeviceToHost, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
         if (ga) for (size_t i = 0; i < c->n; ++i) ga[i] = a[i];
     });

@@ -237,8 +237,9 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
 }
 
 // Fold over the compacted visible list (V threads): parameter gradient of
-// each visible row into gbuf[D][.] at its visible position (coalesced; Adam
-// finds it through the visibility mask + per-word prefix), densify statistics.
+// each visible row into gbuf[D][.] at its visible position, and its
+// screen-space gradient norm into vis_sgn (both coalesced; the Adam adds the
+// norm to the row's densify statistics in the sector it rewrites anyway).
 template <int fd>
 __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, DevCam cam,
                                                            const uint32_t* __restrict__ vis_rows, uint32_t V,
@@ -246,8 +247,7 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
                                                            const float4* __restrict__ pcache,
                                                            const float4* __restrict__ g2d,
                                                            const double* __restrict__ g2d_wide, float* __restrict__ gbuf,
-                                                           float* __restrict__ grad_accum,
-                                                           uint32_t* __restrict__ grad_seen) {
+                                                           float* __restrict__ vis_sgn) {
     pdl_prologue();
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= V) return;
@@ -261,8 +261,7 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
     const double s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
 #pragma unroll
     for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + p] = static_cast<float>(g[c]);  // coalesced
-    grad_accum[i] += static_cast<float>(s);
-    grad_seen[i] += 1u;
+    vis_sgn[p] = static_cast<float>(s);
 }
 
 // Dense Adam over every row (trainer.cpp:267-281). The parameters and both
@@ -289,7 +288,8 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
                                               size_t cap, uint32_t i, bool visible, uint32_t vpos, int aj,
                                               const float* __restrict__ gbuf, const float* __restrict__ z,
                                               const float* __restrict__ u, size_t ns,
-                                              const float* __restrict__ rho_dev, const AdamStep& st) {
+                                              const float* __restrict__ rho_dev, const float* __restrict__ vis_sgn,
+                                              const AdamStep& st) {
     constexpr int RS = row_stride(fd);
     const size_t off = static_cast<size_t>(i) * RS + 8 * h;
     float xs[8], ms[8], vs[8];
@@ -333,6 +333,13 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
         if (c >= 0) xs[j] = adam_update(xs[j], g[j], ms[j], vs[j], st.lr[c], st);
     }
     if (h == 1) canonicalize(xs[0], xs[1], xs[2], xs[3]);  // slots 8-11: the rotation
+    if (h == 0) {  // row metadata (bsg_internal.cuh): step stamp; densify statistics (trainer.cpp:284-289)
+        xs[kMetaSlot] = __uint_as_float(st.t);
+        if (visible) {
+            ms[kMetaSlot] += vis_sgn[vpos];
+            vs[kMetaSlot] = __uint_as_float(__float_as_uint(vs[kMetaSlot]) + 1u);
+        }
+    }
     float4* x4 = reinterpret_cast<float4*>(x + off);
     float4* m4 = reinterpret_cast<float4*>(m + off);
     float4* v4 = reinterpret_cast<float4*>(v + off);
@@ -349,7 +356,7 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
 // step -- the visible rows (their gradient at their visible position) and
 // the anchored rows (penalty rho (x - z + u)) -- all current (the preprocess
 // caught the visible ones up; anchored rows are updated every step). Thread
-// = one sector of one such row; the row's t_last becomes the step's count.
+// = one sector of one such row; the row's step stamp becomes the step's count.
 // The first thread also files the step's constants in the ring.
 template <int fd>
 __global__ __launch_bounds__(256, 4) void adam_sparse_kernel(float* __restrict__ x, float* __restrict__ m,
@@ -362,7 +369,7 @@ __global__ __launch_bounds__(256, 4) void adam_sparse_kernel(float* __restrict__
                                                           const uint32_t* __restrict__ sh_prefix,
                                                           const float* __restrict__ z, const float* __restrict__ u,
                                                           size_t ns, const float* __restrict__ rho_dev, AdamStep st,
-                                                          uint32_t* __restrict__ t_last, float4* __restrict__ ring,
+                                                          const float* __restrict__ vis_sgn, float4* __restrict__ ring,
                                                           double* __restrict__ penalty) {
     pdl_prologue();
     __shared__ double s_red[8];
@@ -393,12 +400,11 @@ __global__ __launch_bounds__(256, 4) void adam_sparse_kernel(float* __restrict__
             BSG_DASSERT(aj < static_cast<int>(ns));
         }
         if (h == 0)
-            pen = adam_sector<fd, 0>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
+            pen = adam_sector<fd, 0>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, vis_sgn, st);
         else if (h == 1)
-            pen = adam_sector<fd, 1>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
+            pen = adam_sector<fd, 1>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, vis_sgn, st);
         else if constexpr (H > 2)
-            pen = adam_sector<fd, 2>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, st);
-        if (h == 0) t_last[i] = st.t;
+            pen = adam_sector<fd, 2>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, vis_sgn, st);
     }
     if (st.has_anchor) {
 #pragma unroll
@@ -416,21 +422,25 @@ __global__ __launch_bounds__(256, 4) void adam_sparse_kernel(float* __restrict__
 // Every stale row caught up to la.t (one thread per row, sector by sector).
 template <int fd>
 __global__ __launch_bounds__(256) void materialize_kernel(float* __restrict__ x, float* __restrict__ m,
-                                                          float* __restrict__ v, uint32_t n,
-                                                          uint32_t* __restrict__ t_last, LazyAdam la) {
+                                                          float* __restrict__ v, uint32_t n, LazyAdam la) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t t0 = t_last[i];
+    const uint32_t t0 = __float_as_uint(x[static_cast<size_t>(i) * row_stride(fd) + kMetaSlot]);
     if (t0 >= la.t) return;
     BSG_DASSERT(la.t - t0 <= kAdamRing);
-    catch_up_row<fd>(x, m, v, i, t0, la);
-    t_last[i] = la.t;
+    catch_up_row<fd>(x, m, v, i, t0, la);  // (writes the new stamp)
 }
 
-__global__ void fill_u32_kernel(uint32_t* __restrict__ p, size_t n, uint32_t value) {
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x)
-        p[i] = value;
+__global__ void reset_row_meta_kernel(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v, size_t cap,
+                                      int rs, uint32_t stamp, int reset_stats) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cap;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        x[i * rs + kMetaSlot] = __uint_as_float(stamp);
+        if (reset_stats) {
+            m[i * rs + kMetaSlot] = 0.f;
+            v[i * rs + kMetaSlot] = 0.f;
+        }
+    }
 }
 
 }  // namespace
@@ -452,11 +462,11 @@ void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (c->fd == 3)
         launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<3>, c->x, c->cap, cam, c->vis_rows, V,
                                                                         c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
-                                                                        c->grad_accum, c->grad_seen);
+                                                                        c->vis_sgn);
     else
         launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<12>, c->x, c->cap, cam, c->vis_rows, V,
                                                                          c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
-                                                                        c->grad_accum, c->grad_seen);
+                                                                        c->vis_sgn);
     BSG_LAUNCHED(c);
 }
 
@@ -472,11 +482,11 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
     if (c->fd == 3)
         launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<3>, c->x, c->m, c->v, c->cap, c->vis_rows, V,
                    c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
-                   c->rho_dev, st, c->t_last, c->adam_ring, &c->scalars->penalty);
+                   c->rho_dev, st, c->vis_sgn, c->adam_ring, &c->scalars->penalty);
     else
         launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<12>, c->x, c->m, c->v, c->cap, c->vis_rows,
                    V, c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
-                   c->rho_dev, st, c->t_last, c->adam_ring, &c->scalars->penalty);
+                   c->rho_dev, st, c->vis_sgn, c->adam_ring, &c->scalars->penalty);
     BSG_LAUNCHED(c);
     // every adam_sync (<= kAdamRing / 2) steps all rows catch up: a stale row
     // never needs a step the ring no longer holds
@@ -515,19 +525,20 @@ LazyAdam make_lazy_adam(const Ctx* c) {
 }
 
 void materialize(Ctx* c) {
-    if (c->n == 0 || c->adam_t == 0 || !c->t_last) return;
+    if (c->n == 0 || c->adam_t == 0) return;
     const LazyAdam la = make_lazy_adam(c);
     const uint32_t n = static_cast<uint32_t>(c->n);
     if (c->fd == 3)
-        materialize_kernel<3><<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->m, c->v, n, c->t_last, la);
+        materialize_kernel<3><<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->m, c->v, n, la);
     else
-        materialize_kernel<12><<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->m, c->v, n, c->t_last, la);
+        materialize_kernel<12><<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->m, c->v, n, la);
     BSG_LAUNCHED(c);
 }
 
-void fill_t_last(Ctx* c, uint32_t value) {
+void reset_row_meta(Ctx* c, uint32_t stamp, bool reset_stats) {
     if (c->cap == 0) return;
-    fill_u32_kernel<<<148 * 4, 256, 0, c->stream>>>(c->t_last, c->cap, value);
+    reset_row_meta_kernel<<<148 * 4, 256, 0, c->stream>>>(c->x, c->m, c->v, c->cap, row_stride(c->fd), stamp,
+                                                                   reset_stats ? 1 : 0);
     BSG_LAUNCHED(c);
 }
 

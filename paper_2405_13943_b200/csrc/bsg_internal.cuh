@@ -51,7 +51,14 @@ __host__ __device__ inline int op_comp(int fd) { return kFeat + fd; }
 // 32-byte sector and a whole row is 2 (4) sectors: the kernels that touch a
 // subset of rows (the preprocess's candidates, densification, consensus
 // packs) gather whole rows instead of one sector per component.
+// Slot 7 (padding of the first sector) carries per-row metadata, so it rides
+// along with sectors the kernels read or write whole anyway (a separate 4-byte
+// array costs a DRAM read-modify-write per scattered update): in x the Adam
+// step the row is current at (lazy Adam, u32 bits), in m the densify gradient
+// accumulator and in v the densify visibility count (u32 bits)
+// (trainer.cpp:284-289).
 __host__ __device__ constexpr int row_stride(int fd) { return fd <= 4 ? 16 : 32; }
+constexpr int kMetaSlot = 7;
 __host__ __device__ constexpr int pslot(int comp, int fd) {
     return comp < kRot ? comp
                        : (comp < kLs ? 8 + (comp - kRot)
@@ -210,8 +217,7 @@ struct Ctx {
     float* x = nullptr;
     float* m = nullptr;
     float* v = nullptr;
-    float* grad_accum = nullptr;   // densify statistics
-    uint32_t* grad_seen = nullptr;
+    float* vis_sgn = nullptr;      // screen-space gradient norm per visible position (fold -> the Adam's densify stats)
 
     // per-row scratch
     float4* rec = nullptr;         // 3 x float4 per row: {mx,my,m00,m01},{m11,o,r,g},{b,rect01,rect23,-}
@@ -222,7 +228,6 @@ struct Ctx {
     float4* pcache = nullptr;      // kParamVec float4 per row: the parameters of the rows the preprocess
                                    // found visible, row-contiguous for the fold's gather
     float* gbuf = nullptr;         // parameter gradient of the visible rows, [D][cap] by visible position
-    uint32_t* t_last = nullptr;    // Adam steps applied to each row (lazy Adam: stale while < adam_t)
     float4* adam_ring = nullptr;   // per Adam step t, at t % kAdamRing: {1/bc1, 1/bc2, lr_pos, -}
     uint32_t* vis_prefix = nullptr;// visible rows before each 32-row word (visible position = prefix + rank in word)
     uint32_t* vis_mask = nullptr;  // 1 bit per row: visible this step (written by the compaction)
@@ -494,7 +499,7 @@ struct LazyAdam {
     float b1, b2, eps, omb1, omb2;
     float lr[kMaxD];        // lr of the components whose rate does not change (not used for positions)
     const float4* ring;
-    uint32_t t;             // Adam steps applied so far (rows with t_last < t are stale)
+    uint32_t t;             // Adam steps applied so far (rows whose step stamp is below are stale)
     float drift_pos, drift_ls;  // per-component drift bounds per unit of the geometric staleness factor
     float rho;              // b1 / sqrt(b2): decay of |m_hat / sqrt(v_hat)| over a zero-gradient step
 };
@@ -546,13 +551,14 @@ __device__ __forceinline__ void catch_up_sector(float (&xs)[8], float (&ms)[8], 
         const float4 k = la.ring[t % kAdamRing];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-                const int c = comp_of_slot(8 * h + j, fd);
+            const int c = comp_of_slot(8 * h + j, fd);
             if (c < 0) continue;
             const float lr = c < kRot ? k.z : la.lr[c];
             xs[j] = adam_update_step(xs[j], 0.f, ms[j], vs[j], lr, la.b1, la.omb1, la.b2, la.omb2, k.x, k.y, la.eps);
         }
         if (h == 1) canonicalize(xs[0], xs[1], xs[2], xs[3]);
     }
+    if (h == 0) xs[kMetaSlot] = __uint_as_float(la.t);  // the row is current at la.t
 }
 
 // Sector h of row i (stale since t0) brought up to la.t in memory.
@@ -608,7 +614,9 @@ LazyAdam make_lazy_adam(const Ctx* c);
 void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
 void materialize(Ctx* c);
-void fill_t_last(Ctx* c, uint32_t value);
+// Every row's step stamp (x slot kMetaSlot) set to `stamp`; with reset_stats
+// the densify statistics (m, v slot kMetaSlot) zeroed.
+void reset_row_meta(Ctx* c, uint32_t stamp, bool reset_stats);
 void launch_finalize_loss(Ctx* c, const DevCam& cam, const DevRender& rc, double* out, bool add_penalty);
 bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt);
 // K1-K5 for one view (abi.cu), and the evaluation of one holdout view (eval.cu).

@@ -55,8 +55,8 @@ __device__ __forceinline__ double split_offset(const float* __restrict__ x, int 
 }
 
 __global__ __launch_bounds__(256) void densify_classify_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
-                                                               int fd, const float* __restrict__ grad_accum,
-                                                               const uint32_t* __restrict__ grad_seen,
+                                                               int fd, const float* __restrict__ m,
+                                                               const float* __restrict__ v,
                                                                const uint32_t* __restrict__ sh_mask, DensifyParams p,
                                                                uint8_t* __restrict__ action,
                                                                uint32_t* __restrict__ keep,
@@ -67,8 +67,9 @@ __global__ __launch_bounds__(256) void densify_classify_kernel(const float* __re
     const double o = 1.0 / (1.0 + exp(-static_cast<double>(x[pidx(i, kFeat + fd, fd)])));  // cloud.hpp:55
     if (o < p.prune_opacity) {
         act = kActPrune;
-    } else if (grad_seen[i] != 0) {
-        const double mean_grad = static_cast<double>(grad_accum[i]) / grad_seen[i];
+    } else if (const uint32_t seen = __float_as_uint(v[static_cast<size_t>(i) * row_stride(fd) + kMetaSlot])) {
+        // densify statistics in the rows' metadata slot (bsg_internal.cuh)
+        const double mean_grad = static_cast<double>(m[static_cast<size_t>(i) * row_stride(fd) + kMetaSlot]) / seen;
         if (!(mean_grad < p.grad_threshold)) {
             double off[3];
             const double smax = split_offset(x, fd, i, off);
@@ -171,8 +172,8 @@ void maybe_densify(Ctx* c) {
     uint32_t* keep_pos = c->poff;
     uint32_t* child_pos = c->vis_rows;
     materialize(c);
-    densify_classify_kernel<<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->cap, n, c->fd, c->grad_accum,
-                                                                    c->grad_seen, c->sh_mask, p, action, keep, nchild);
+    densify_classify_kernel<<<(n + 255) / 256, 256, 0, c->stream>>>(c->x, c->cap, n, c->fd, c->m, c->v,
+                                                                    c->sh_mask, p, action, keep, nchild);
     BSG_LAUNCHED(c);
     scan_exclusive_u32(c, keep, nullptr, keep_pos, n, &c->counters->dens_keep);
     scan_exclusive_u32(c, nchild, nullptr, child_pos, n, &c->counters->dens_children);
@@ -182,8 +183,7 @@ void maybe_densify(Ctx* c) {
     BSG_CUDA(cudaStreamSynchronize(c->stream));
     const uint32_t n_keep = c->counters_host->dens_keep, n_child = c->counters_host->dens_children;
     if (n_keep == n && n_child == 0) {
-        BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
-        BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
+        reset_row_meta(c, static_cast<uint32_t>(c->adam_t), true);  // (every row is current: materialized above)
         return;
     }
     // ids (trainer.cpp:315-355): removal order is row order; children take
@@ -233,9 +233,7 @@ void maybe_densify(Ctx* c) {
     if (ncap != c->cap) alloc_row_scratch(c, ncap);
     c->n = n_new;
     c->ids = std::move(ids);
-    BSG_CUDA(cudaMemsetAsync(c->grad_accum, 0, c->cap * sizeof(float), c->stream));
-    BSG_CUDA(cudaMemsetAsync(c->grad_seen, 0, c->cap * sizeof(uint32_t), c->stream));
-    fill_t_last(c, static_cast<uint32_t>(c->adam_t));  // every row current (materialized above; children new)
+    reset_row_meta(c, static_cast<uint32_t>(c->adam_t), true);  // every row current (materialized above; children new)
     // shared rows (trainer.cpp:360-371): pruned shared ids leave the consensus;
     // survivors move to their new rows (split never applies to shared rows)
     if (c->n_shared) {

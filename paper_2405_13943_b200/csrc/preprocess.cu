@@ -53,8 +53,7 @@ constexpr int kPreChunk = kPreThreads * kPreRowsPerThread;
 // so doing this per thread would leave most lanes of a warp idle). The
 // visible set and every rect are exactly those of the exact path.
 __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __restrict__ x, float* __restrict__ m,
-                                                                 float* __restrict__ v, uint32_t* __restrict__ t_last,
-                                                                 LazyAdam la, uint32_t n,
+                                                                 float* __restrict__ v, LazyAdam la, uint32_t n,
                                                                  int fd, DevCam cam, DevRender rc,
                                                                  float4* __restrict__ rec,
                                                                  uint64_t* __restrict__ depth_key,
@@ -105,7 +104,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
         const float4 a = r4[0], b = r4[1];
         pp[k][0] = a.x; pp[k][1] = a.y; pp[k][2] = a.z;
         ll[k][0] = a.w; ll[k][1] = b.x; ll[k][2] = b.y;
-        stale[k] = la.t - t_last[j];
+        stale[k] = la.t - __float_as_uint(b.w);  // the row's step stamp (slot kMetaSlot)
     }
     // The test is FP32 with explicit FMAs (this file is compiled --fmad=false
     // for the exact FP64 path below) and approximate MUFU reciprocals /
@@ -209,7 +208,6 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
     uint32_t nvis = 0;
     for (uint32_t q = threadIdx.x; q < count; q += kPreThreads) {
         const uint32_t i = s_rows[q];
-        if (s_stale[q]) t_last[i] = la.t;
         // the whole row up front (contiguous float4s): one dependent DRAM round trip
         float prm[kMaxD];
         const float4* r4 = reinterpret_cast<const float4*>(x + static_cast<size_t>(i) * rs);
@@ -424,7 +422,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     }
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     const LazyAdam la = make_lazy_adam(c);
-    launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->m, c->v, c->t_last, la, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
+    launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->m, c->v, la, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
                                                       c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters,
                                                       c->scalars, c->tile_cnt);
     BSG_LAUNCHED(c);
