@@ -207,12 +207,23 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
         const uint32_t row = vis_rows[p];
         int x0, x1, y0, y1;
         unpack_rect(rec[3 * static_cast<size_t>(row) + 2], x0, x1, y0, y1);
-        for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-            for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) {
-                const uint32_t slot = atomicAdd(&cur[kTileSub * (ty * tiles_x + tx) + (row & (kTileSub - 1))], 1u);
-                BSG_DASSERT(slot < ranges_end[ty * tiles_x + tx].y);  // the tile's cursor stays in its range
-                if (slot < pcap) out_rows[slot] = row;
-            }
+        // the row's slot claims are independent: up to 4 in flight at once
+        // (the kernel is bound by the claims' L2 round trips)
+        const int tx0 = x0 / kTile, ty0 = y0 / kTile, w = x1 / kTile - tx0 + 1;
+        const int nt = w * (y1 / kTile - ty0 + 1);
+        for (int b = 0; b < nt; b += 4) {
+            uint32_t slot[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (b + k < nt) {
+                    const int ty = ty0 + (b + k) / w, tx = tx0 + (b + k) % w;
+                    slot[k] = atomicAdd(&cur[kTileSub * (ty * tiles_x + tx) + (row & (kTileSub - 1))], 1u);
+                    BSG_DASSERT(slot[k] < ranges_end[ty * tiles_x + tx].y);  // the tile's cursor stays in its range
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (b + k < nt && slot[k] < pcap) out_rows[slot[k]] = row;
+        }
     }
 }
 

@@ -10,13 +10,15 @@ FILES=(); while [ $# -gt 0 ] && [ "$1" != "--" ]; do FILES+=("$1"); shift; done
 D=/root/repo/paper_2405_13943_b200
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 mkdir -p $D/lib_var $D/build_var/$NAME
-OBJS=$(ls $D/build/*.o)
 for f in "${FILES[@]}"; do
   FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I$D/../include"
   case $f in preprocess.cu|densify.cu) FL="$FL --fmad=false";; esac
   nvcc $FL "$@" -Xptxas -v -c $VDIR/$f -o $D/build_var/$NAME/${f%.cu}.o 2> $D/build_var/$NAME/${f%.cu}.ptxas.log || { cat $D/build_var/$NAME/${f%.cu}.ptxas.log; exit 1; }
-  OBJS=$(echo "$OBJS" | grep -v "/${f%.cu}.o$")
-  OBJS="$OBJS $D/build_var/$NAME/${f%.cu}.o"
+done
+OBJS=""
+for o in $D/build/*.o; do
+  b=$(basename $o .o)
+  if [ -f $D/build_var/$NAME/$b.o ] && printf '%s\n' "${FILES[@]}" | grep -qx "$b.cu"; then OBJS="$OBJS $D/build_var/$NAME/$b.o"; else OBJS="$OBJS $o"; fi
 done
 nvcc $ARCH -shared -o $D/lib_var/libbsgpu_${NAME}.so $OBJS -ldl -lpthread
 echo built $D/lib_var/libbsgpu_${NAME}.so
