@@ -5,7 +5,8 @@ gpu__time_duration.sum launch list of `bench.py --profile`) and
 full_<kernel>_<tag>.ncu-rep (ncu --set full captures), and writes
   profiles/launches_<tag>.md   per-kernel share of the step (cold-cache, serialised)
   profiles/ncu_<tag>.md        per-kernel SOL, DRAM bytes, pipes, top stalls
-  profiles/dram_traffic.json   bench stage -> measured DRAM bytes per launch
+  profiles/dram_traffic.json   bench stage -> measured DRAM bytes per step (kernels that run less
+                               often than every step scaled by their launches per step)
 
 usage: python tools/profile_summary.py <tag> [gpurun_out]
 """
@@ -112,6 +113,14 @@ def main():
             lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.2f} | {sum(v) / tot:.3f} |")
         lines.append(f"\nTotal kernel time in the capture: {tot / 1e6:.3f} ms")
         open(os.path.join(prof, f"launches_{tag}.md"), "w").write("\n".join(lines) + "\n")
+    # launches per step of each kernel (materialize runs every 32 steps): the
+    # per-launch DRAM bytes of a capture are scaled to bytes per step
+    per_step = {}
+    if os.path.exists(lp):
+        steps = max((len(v) for k, v in d.items() if base(k) == "preprocess_kernel"), default=0)
+        for k, v in d.items():
+            if steps:
+                per_step[base(k)] = len(v) / steps
     traffic = {}
     tp = os.path.join(prof, "dram_traffic.json")
     if os.path.exists(tp):
@@ -134,7 +143,7 @@ def main():
         st = STAGE_OF.get(base(name))
         rd, wr = num(m.get("dram__bytes_read.sum", "")), num(m.get("dram__bytes_write.sum", ""))
         if st and rd is not None and wr is not None:
-            traffic.setdefault(st, {})[base(name)] = rd + wr
+            traffic.setdefault(st, {})[base(name)] = (rd + wr) * min(1.0, per_step.get(base(name), 1.0))
         kmet[base(name)] = {k: (num(m.get(key, "")) or 0.0) * sc for k, key, sc in METRICS}
         kmet[base(name)]["capture"] = f"profiles/ncu_{tag}.md"
     open(os.path.join(prof, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
