@@ -499,10 +499,12 @@ AdamStep make_adam_step(Ctx* c) {
     return st;
 }
 
-// One train_step (trainer.cpp:249-295) on a device-resident ground truth.
+// One train_step (trainer.cpp:249-295) on a device-resident ground truth:
+// FP32, or (gt8 non-null) the 8-bit image the loss kernels read directly.
 // gt_ready (nullable): event the loss waits on (ground truth still in flight
 // on the copy stream while projection, sorting and the forward blend run).
-void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev, cudaEvent_t gt_ready = nullptr) {
+void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev, cudaEvent_t gt_ready = nullptr,
+               const uint8_t* gt8 = nullptr) {
     c->step_launches = 0;
     const DevCam cam = make_cam(view);
     const DevRender rc = make_render(c->tcfg.render);
@@ -512,7 +514,10 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     stage_end(c, kStBlendFwd);
     stage_begin(c, kStLoss);
     if (gt_ready) BSG_CUDA(cudaStreamWaitEvent(c->stream, gt_ready, 0));
-    launch_loss(c, cam, rc, gt);
+    if (gt8)
+        launch_loss(c, cam, rc, gt8);
+    else
+        launch_loss(c, cam, rc, gt);
     stage_end(c, kStLoss);
     stage_begin(c, kStBlendBwd);
     launch_blend_bwd(c, cam, rc);
@@ -626,31 +631,35 @@ void round_dual_linf(Ctx* c);
 void round_pack_minmax(Ctx* c);
 void round_spread(Ctx* c);
 
-// image.cpp:21-27 (dequantize): byte / 255 in FP64, then the device's FP32.
-__global__ __launch_bounds__(256) void dequantize_kernel(const uint8_t* __restrict__ in, float* __restrict__ out,
-                                                         size_t n) {
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x)
-        out[i] = static_cast<float>(static_cast<double>(in[i]) / 255.0);
-}
-
 // n steps on host images, each uploaded on the copy stream into one of two
-// device buffers while the previous step computes. `upload(k, buf)` enqueues
-// step k's image into buf on the copy stream.
+// device buffers while the previous step computes. `upload(k, b, buf)`
+// enqueues step k's image on the copy stream: into the FP32 buffer buf
+// (returns null), or into an 8-bit buffer it returns.
 template <typename Upload>
 void train_steps_from_host(Ctx* c, size_t n, const bsg_camera* cams, double* losses, Upload&& upload) {
     ensure_views_buffers(c, std::max<size_t>(n, 1));
-    for (size_t k = 0; k < n; ++k) {
-        const bsg_camera& cam = cams[k];
-        ensure_image_buffers(c, static_cast<int>(cam.width), static_cast<int>(cam.height));
+    // every buffer sized for the largest view first: an image-buffer growth
+    // must not free a staging buffer with an upload in flight
+    for (size_t k = 0; k < n; ++k)
+        ensure_image_buffers(c, static_cast<int>(cams[k].width), static_cast<int>(cams[k].height));
+    // Step k's image is uploaded while step k-1 computes (issued before step
+    // k-1's kernels), so step k waits for it at its start -- a step boundary --
+    // and the step's own kernels stay one programmatic-launch chain.
+    const uint8_t* gt8[2] = {nullptr, nullptr};
+    auto issue = [&](size_t k) {
         const int b = static_cast<int>(k & 1);
         float* buf = b ? c->gt_stage_b : c->gt_stage;
-        cudaEvent_t ready = b ? c->gt_ready_b : c->gt_ready;
         // step k-2 read this buffer: its loss must be done before the overwrite
         if (k >= 2) BSG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->gt_free[b], 0));
-        upload(k, b, buf);
-        BSG_CUDA(cudaEventRecord(ready, c->copy_stream));
-        train_one(c, cam, buf, c->losses_dev + 3 * k, ready);
+        gt8[b] = upload(k, b, buf);
+        BSG_CUDA(cudaEventRecord(b ? c->gt_ready_b : c->gt_ready, c->copy_stream));
+    };
+    if (n) issue(0);
+    for (size_t k = 0; k < n; ++k) {
+        const int b = static_cast<int>(k & 1);
+        if (k + 1 < n) issue(k + 1);
+        BSG_CUDA(cudaStreamWaitEvent(c->stream, b ? c->gt_ready_b : c->gt_ready, 0));
+        train_one(c, cams[k], b ? c->gt_stage_b : c->gt_stage, c->losses_dev + 3 * k, nullptr, gt8[b]);
         BSG_CUDA(cudaEventRecord(c->gt_free[b], c->stream));
         maybe_densify(c);
     }
@@ -1217,6 +1226,7 @@ int bsg_train_steps_host(bsg_ctx* h, size_t n, const bsg_camera* cams, const flo
             const size_t px = static_cast<size_t>(cams[k].width) * cams[k].height;
             BSG_CUDA(cudaMemcpyAsync(buf, gts_host[k], 3 * px * sizeof(float), cudaMemcpyHostToDevice,
                                      c->copy_stream));
+            return static_cast<const uint8_t*>(nullptr);
         });
     });
 }
@@ -1241,11 +1251,11 @@ int bsg_train_steps_host_u8(bsg_ctx* h, size_t n, const bsg_camera* cams, const 
         }
         train_steps_from_host(c, n, cams, losses, [&](size_t k, int b, float* buf) {
             const size_t bytes = 3 * static_cast<size_t>(cams[k].width) * cams[k].height;
+            (void)buf;
             BSG_CUDA(cudaMemcpyAsync(c->gt_u8[b], gts_host[k], bytes, cudaMemcpyHostToDevice, c->copy_stream));
-            // widened on the copy stream too, overlapping the compute stream
-            const unsigned grid = static_cast<unsigned>(std::min<size_t>((bytes + 255) / 256, 148 * 4));
-            dequantize_kernel<<<grid, 256, 0, c->copy_stream>>>(c->gt_u8[b], buf, bytes);
-            BSG_LAUNCHED(c);
+            // the loss kernels read the bytes (v / 255 as the dequantisation of
+            // image.cpp): no widening pass competing with the step's kernels
+            return static_cast<const uint8_t*>(c->gt_u8[b]);
         });
     });
 }

@@ -473,6 +473,7 @@ void launch_gspl_floats(Ctx* c, float* out);
 void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P);
 void launch_blend_fwd(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt);
+void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const uint8_t* gt);  // 8-bit ground truth
 void launch_blend_bwd(Ctx* c, const DevCam& cam, const DevRender& rc);
 void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out /*[D][n] f64*/, double* sgn, uint8_t* vis);
 struct AdamStep {

@@ -69,14 +69,29 @@ __device__ __forceinline__ void corr4(const float (&v)[16], float (&o)[4]) {
     }
 }
 
+// Ground truth as FP32, or as the 8-bit values of the reference's PPM images
+// (bsg_train_steps_host_u8): the reference's dequantisation v / 255 in FP64
+// rounded to FP32 (image.cpp:21-27), here as q = v r (r = 1/255 rounded)
+// refined by one FMA residual step -- the correctly rounded FP32 quotient,
+// equal to the FP64 one rounded, for every v in 0..255 (checked exhaustively;
+// three FMA-pipe ops instead of an IEEE division).
+__device__ __forceinline__ float gt_val(const float* __restrict__ y, size_t p) { return y[p]; }
+__device__ __forceinline__ float gt_val(const uint8_t* __restrict__ y, size_t p) {
+    constexpr float r = 1.0f / 255.0f;
+    const float v = static_cast<float>(y[p]);
+    const float q = __fmul_rn(v, r);
+    return __fmaf_rn(__fmaf_rn(-q, 255.f, v), r, q);
+}
+
 struct WinSmem {
     float x[kPY][kPS], y[kPY][kPS];
     float h[5][kPY][kTX];
 };
 
-// x, y: HxWx3 FP32. f: [3 channels][3 maps][Hv][Wv].
+// x, y: HxWx3 FP32 (y: FP32 or 8-bit). f: [3 channels][3 maps][Hv][Wv].
+template <typename G>
 __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __restrict__ x,
-                                                                const float* __restrict__ y, int W, int H,
+                                                                const G* __restrict__ y, int W, int H,
                                                                 float* __restrict__ f, double* __restrict__ ssim_sum) {
     pdl_prologue();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -96,7 +111,7 @@ __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __r
             if (gx < W && gy < H) {
                 const size_t p = 3 * (static_cast<size_t>(gy) * W + gx) + ch;
                 a = x[p];
-                b = y[p];
+                b = gt_val(y, p);
             }
             S.x[ly][lx] = a;
             S.y[ly][lx] = b;
@@ -175,7 +190,8 @@ struct PixSmem {
 };
 
 // Per pixel: spread f1..f3 (adjoint of the valid blur) and form dL/dC.
-__global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* __restrict__ x, const float* __restrict__ y,
+template <typename G>
+__global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* __restrict__ x, const G* __restrict__ y,
                                                                int W, int H, const float* __restrict__ f, int has_ssim,
                                                                float lam_over_count, float inv_count3,
                                                                float* __restrict__ dl_dc, double* __restrict__ l1_sum) {
@@ -225,7 +241,7 @@ __global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* _
             const int py = py0 + r0 + j;
             if (px < W && py < H) {
                 const size_t p = 3 * (static_cast<size_t>(py) * W + px) + ch;
-                const float a = x[p], b = y[p];
+                const float a = x[p], b = gt_val(y, p);
                 const float diff = a - b;
                 const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
                 local += fabs(static_cast<double>(diff));
@@ -266,15 +282,22 @@ void ensure_ssim_ready(Ctx* c) {
         for (int i = 0; i < kW; ++i)
             if (static_cast<float>(k[i] / sum) != kWinHost[i])
                 throw Error{BSG_ERR_CUDA, "SSIM window taps differ from ssim_window_1d"};
-        BSG_CUDA(cudaFuncSetAttribute(ssim_windows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BSG_CUDA(cudaFuncSetAttribute(ssim_windows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sizeof(WinSmem))));
-        BSG_CUDA(cudaFuncSetAttribute(ssim_pixels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BSG_CUDA(cudaFuncSetAttribute(ssim_windows_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sizeof(WinSmem))));
+        BSG_CUDA(cudaFuncSetAttribute(ssim_pixels_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sizeof(PixSmem))));
+        BSG_CUDA(cudaFuncSetAttribute(ssim_pixels_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sizeof(PixSmem))));
         g_ready[c->device] = true;
     }
 }
 
-void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt) {
+namespace {
+
+template <typename G>
+void launch_loss_t(Ctx* c, const DevCam& cam, const DevRender& rc, const G* gt) {
     ensure_ssim_ready(c);
     const int W = cam.W, H = cam.H;
     const bool has_ssim = W >= kW && H >= kW;
@@ -282,15 +305,21 @@ void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt
     const double count = has_ssim ? 3.0 * Wv * Hv : 1.0;
     if (has_ssim) {
         dim3 grid((Wv + kTX - 1) / kTX, (Hv + kTY - 1) / kTY);
-        launch_pdl(c->stream, grid, kThreads, sizeof(WinSmem), ssim_windows_kernel, c->out_rgb, gt, W, H, c->ssim_f,
-                                                                           &c->scalars->ssim_sum);
+        launch_pdl(c->stream, grid, kThreads, sizeof(WinSmem), ssim_windows_kernel<G>, c->out_rgb, gt, W, H, c->ssim_f,
+                   &c->scalars->ssim_sum);
         BSG_LAUNCHED(c);
     }
     dim3 grid2((W + kTX - 1) / kTX, (H + kTY - 1) / kTY);
-    launch_pdl(c->stream, grid2, kThreads, sizeof(PixSmem), ssim_pixels_kernel, c->out_rgb, gt, W, H, c->ssim_f, has_ssim ? 1 : 0, static_cast<float>(rc.lambda / count),
-        static_cast<float>(1.0 / (3.0 * W * H)), c->dl_dc, &c->scalars->l1_sum);
+    launch_pdl(c->stream, grid2, kThreads, sizeof(PixSmem), ssim_pixels_kernel<G>, c->out_rgb, gt, W, H, c->ssim_f,
+               has_ssim ? 1 : 0, static_cast<float>(rc.lambda / count), static_cast<float>(1.0 / (3.0 * W * H)),
+               c->dl_dc, &c->scalars->l1_sum);
     BSG_LAUNCHED(c);
 }
+
+}  // namespace
+
+void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const float* gt) { launch_loss_t(c, cam, rc, gt); }
+void launch_loss(Ctx* c, const DevCam& cam, const DevRender& rc, const uint8_t* gt) { launch_loss_t(c, cam, rc, gt); }
 
 // Windows pass only (mean SSIM into scalars->ssim_sum); false when the image
 // is smaller than the window (ssim.cpp:12-14: SSIM = 1).
@@ -300,8 +329,8 @@ bool launch_ssim_windows(Ctx* c, const DevCam& cam, const float* gt) {
     ensure_ssim_ready(c);
     const int Wv = W - 2 * kHalf, Hv = H - 2 * kHalf;
     dim3 grid((Wv + kTX - 1) / kTX, (Hv + kTY - 1) / kTY);
-    launch_pdl(c->stream, grid, kThreads, sizeof(WinSmem), ssim_windows_kernel, c->out_rgb, gt, W, H, c->ssim_f,
-                                                                       &c->scalars->ssim_sum);
+    launch_pdl(c->stream, grid, kThreads, sizeof(WinSmem), ssim_windows_kernel<float>, c->out_rgb, gt, W, H, c->ssim_f,
+               &c->scalars->ssim_sum);
     BSG_LAUNCHED(c);
     return true;
 }
