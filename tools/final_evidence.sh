@@ -2,8 +2,8 @@
 # list and full captures (tools/gpu_round.sh), the other BASELINE configs'
 # drivers and the kernel timeline. usage: bash tools/final_evidence.sh [tag]
 set -u
-TAG=${1:-r01f}
-KERNELS="blend_bwd_kernel blend_fwd_kernel adam_kernel adam_rot_kernel fold_visible_kernel preprocess_kernel ssim_windows_kernel ssim_pixels_kernel tile_sort_kernel emit_tiles_kernel" bash tools/gpu_round.sh $TAG
+TAG=${1:-r02e}
+bash tools/gpu_round.sh $TAG
 timeout 900 python tools/timeline.py --out gpurun_out/timeline_$TAG.json > gpurun_out/timeline_$TAG.log 2>&1
 timeout 900 python tools/timeline.py --e2e --out gpurun_out/timeline_e2e_$TAG.json > gpurun_out/timeline_e2e_$TAG.log 2>&1
 timeout 1200 python tools/cfg5_sweep.py --out gpurun_out/cfg5_sweep_$TAG.json > gpurun_out/cfg5_$TAG.log 2>&1
