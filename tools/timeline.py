@@ -1,4 +1,4 @@
-"""Kernel timeline of the bench workload (cfg 2, one block) from CUPTI via
+"""Kernel timeline of the bench workload (cfg 3 headline, one block) from CUPTI via
 torch.profiler: per-kernel warm durations, GPU idle gaps between consecutive
 kernels of one step, and the busy fraction of the step. Answers "how much of
 the step is launch / host-sync gap rather than kernel time".
@@ -20,7 +20,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--e2e", action="store_true", help="steps through bsg_train_step_host (pinned host GT)")
+    ap.add_argument("--e2e", action="store_true", help="steps through bsg_train_steps_host_u8 (pinned 8-bit host GT)")
+    ap.add_argument("--config", default="cfg3")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -28,18 +29,19 @@ def main():
 
     import bench
     torch.cuda.set_device(0)
-    blk, cams, _, _ = bench.build_block(0, 1, bench.CFG["n"], 0, constant_gt=False)
+    cfg = bench.CFGS[args.config]
+    blk, cams, gts, _ = bench.build_block(cfg, 0, 1, 0)
     g = np.random.default_rng(3)
     seq = [int(v) for v in g.integers(0, len(cams), args.warmup + args.steps)]
     if args.e2e:
-        _, _, gts, _ = bench.build_block(0, 1, 1000, 0, constant_gt=True)  # shapes only
-        pinned = [torch.full((bench.CFG["height"], bench.CFG["width"], 3), 0.5).pin_memory() for _ in range(4)]
+        pinned = [torch.from_numpy(np.clip(np.rint(np.clip(x, 0.0, 1.0) * 255.0), 0, 255).astype(np.uint8)).pin_memory()
+                  for x in gts]
 
         def step(v):
-            blk.train_step_host(cams[v], pinned[v % 4].numpy())
+            blk.train_steps_host_u8([cams[v]], [pinned[v].numpy()])
 
         def chunk(vs):  # the bench's e2e path: one host-image call per consensus interval
-            blk.train_steps_host([cams[v] for v in vs], [pinned[v % 4].numpy() for v in vs])
+            blk.train_steps_host_u8([cams[v] for v in vs], [pinned[v].numpy() for v in vs])
     else:
         def step(v):
             blk.train_steps([v], want_losses=False)
