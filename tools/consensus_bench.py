@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--interval", type=int, default=25)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--profile", action="store_true",
+                    help="also: per-kernel GPU time per step with and without asynchronous rounds (CUPTI)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     import torch
@@ -151,6 +153,42 @@ def main():
         "setup_s": round(t_plan, 1),
         "gpu": torch.cuda.get_device_name(0),
     }
+    if args.profile:
+        from collections import defaultdict
+
+        from torch.profiler import ProfilerActivity, profile
+
+        def kernel_times(fn, n):
+            pos[0] = 40
+            torch.cuda.synchronize()
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                fn(n)
+                torch.cuda.synchronize()
+            tot = defaultdict(float)
+            iv = []
+            for e in prof.events():
+                if e.device_type.name == "CUDA":
+                    name = e.name.replace("bsg::(anonymous namespace)::", "").replace("void ", "").split("(")[0]
+                    tot[name] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+                    iv.append((e.time_range.start, e.time_range.end))
+            iv.sort()
+            busy, cur_s, cur_e = 0.0, None, None
+            for a, b in iv:  # union of the kernels' intervals: the GPU's busy time
+                if cur_e is None or a > cur_e:
+                    if cur_e is not None:
+                        busy += cur_e - cur_s
+                    cur_s, cur_e = a, b
+                else:
+                    cur_e = max(cur_e, b)
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            span = (iv[-1][1] - iv[0][0]) if iv else 0.0
+            res = {k: round(v / n, 2) for k, v in sorted(tot.items(), key=lambda x: -x[1])}
+            res["_busy_us_per_step"] = round(busy / n, 1)
+            res["_span_us_per_step"] = round(span / n, 1)
+            return res
+        out["us_per_step_by_kernel_plain"] = kernel_times(lambda n: [step() for _ in range(n)], 50)
+        out["us_per_step_by_kernel_async"] = kernel_times(with_async, 50)
     print(json.dumps(out), flush=True)
     if args.out:
         with open(args.out, "w") as f:
