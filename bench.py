@@ -392,11 +392,36 @@ def consensus_k8(device, name="cfg3", steps=100, interval=25):
         blk.consensus_round_async(1.6, True, iteration=0)
         run.steps(1, consensus=False)
         blk.consensus_wait()
-    run.round_ms = []
-    plain, _, _ = timed_region(run, stream, steps, 1, consensus=False)
-    run.it = 0
-    with_async, _, _ = timed_region(run, stream, steps, 1, consensus=True)
-    rounds = list(run.round_ms)
+    # Windows of `interval` steps, alternately without and with a round at
+    # their start (waited after the window's first step, as in training): the
+    # model keeps training, so interleaving keeps both sides on the same state
+    # (timing all plain steps first and all rounds after measured the drift of
+    # the step cost as consensus overhead).
+    rounds, t_plain, t_round = [], 0.0, 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    windows = max(1, steps // interval)
+    vs = []
+    for w in range(2 * windows):
+        with_round = w % 2 == 1
+        if not with_round:  # both windows of a pair render the same views (the step cost is view-dependent)
+            vs = [run.next_view() for _ in range(interval)]
+        torch.cuda.synchronize()
+        e0.record(stream)
+        if with_round:
+            blk.consensus_round_async(1.6, True, iteration=run.it)
+        for j in range(interval):
+            blk.train_steps([vs[j]], want_losses=False)
+            run.it += 1
+            if with_round and j == 0:
+                rounds.append(blk.consensus_wait()["ms"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if with_round:
+            t_round += e0.elapsed_time(e1)
+        else:
+            t_plain += e0.elapsed_time(e1)
+    plain = t_plain / (windows * interval)
+    with_async = t_round / (windows * interval)
     blk.close()
     D, S, K = 14, len(sids), 8
     payload = 4 * 4 * S + 4 * (D + 1) * S + 8 * 3

@@ -74,7 +74,7 @@ def main():
     nv = len(vcams)
     stream = torch.cuda.ExternalStream(blk.stream())
     g = np.random.default_rng(1)
-    seq = [int(v) for v in g.integers(0, nv, 40 + 2 * args.steps)]
+    seq = [int(v) for v in g.integers(0, nv, 40 + 4 * args.steps)]
     pos = [0]
 
     def step():
@@ -100,35 +100,50 @@ def main():
         blk.consensus_wait()
         blk.consensus_round(1.6, True)
         step()
-    # (a) no consensus
-    ms_plain = timed(lambda n: [step() for _ in range(n)], args.steps) / args.steps
-    # (b) asynchronous rounds every `interval` steps (overlapped with the next step)
-    rounds_async = []
+    # Windows of `interval` steps in rotation: no round / an asynchronous
+    # round at the start (waited after the window's first step) / a
+    # synchronous round at the start. The model keeps training, so the
+    # rotation keeps every variant on the same state (timing the variants one
+    # after the other measured the drift of the step cost as consensus cost).
+    rounds_async, rounds_sync = [], []
+    tot = {"plain": 0.0, "async": 0.0, "sync": 0.0}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    windows = max(1, args.steps // args.interval)
+    pos[0] = 40
+    for w in range(3 * windows):
+        kind = ("plain", "async", "sync")[w % 3]
+        if kind == "plain":
+            start = pos[0] if pos[0] + args.interval <= len(seq) else 40
+        pos[0] = start  # the three windows of a rotation render the same views
+        torch.cuda.synchronize()
+        e0.record(stream)
+        if kind == "async":
+            blk.consensus_round_async(1.6, True, iteration=w)
+        elif kind == "sync":
+            rounds_sync.append(blk.consensus_round(1.6, True))
+        for j in range(args.interval):
+            step()
+            if kind == "async" and j == 0:
+                rounds_async.append(blk.consensus_wait())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tot[kind] += e0.elapsed_time(e1)
+    n_w = windows * args.interval
+    ms_plain, ms_async, ms_sync = tot["plain"] / n_w, tot["async"] / n_w, tot["sync"] / n_w
 
-    def with_async(n):
+    def with_async(n):  # (for --profile)
         pending = False
         for i in range(1, n + 1):
             step()
             if pending:
-                rounds_async.append(blk.consensus_wait())
+                blk.consensus_wait()
                 pending = False
             if i % args.interval == 0:
                 blk.consensus_round_async(1.6, True, iteration=i)
                 pending = True
         if pending:
-            rounds_async.append(blk.consensus_wait())
+            blk.consensus_wait()
 
-    ms_async = timed(with_async, args.steps) / args.steps
-    # (c) synchronous rounds (round, host wait, then the next step)
-    rounds_sync = []
-
-    def with_sync(n):
-        for i in range(1, n + 1):
-            step()
-            if i % args.interval == 0:
-                rounds_sync.append(blk.consensus_round(1.6, True))
-
-    ms_sync = timed(with_sync, args.steps) / args.steps
     D = 14
     S = len(sids)
     payload = 4 * 4 * S + 4 * (D + 1) * S + 8 * 3  # q pre-pass + relaxed contributions/flags + residual scalars
