@@ -300,15 +300,19 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
             const int y0 = max(0, to_int_clamped(ceil(my - radius)));
             const int y1 = min(cam.H - 1, to_int_clamped(floor(my + radius)));
             if (x0 <= x1 && y0 <= y1) {
-                // minv (renderer.cpp:76-78), colour (cloud.cpp:180-193), opacity (cloud.hpp:55)
-                const double m00 = C[1][1] / det, m01 = -C[0][1] / det, m11 = C[0][0] / det;
+                // minv (renderer.cpp:76-78), colour (cloud.cpp:180-193), opacity (cloud.hpp:55).
+                // These only reach the FP32 record (no integer depends on them): one
+                // reciprocal instead of three FP64 divisions (~1 FP64 ulp apart).
+                const double idet = 1.0 / det;
+                const double m00 = C[1][1] * idet, m01 = -C[0][1] * idet, m11 = C[0][0] * idet;
                 double col[3];
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) col[ch] = kSh0 * static_cast<double>(prm[kFeat + ch]);
                 if (fd >= 12) {
                     const double u0 = p0 - cam.center[0], u1 = p1 - cam.center[1], u2 = p2 - cam.center[2];
                     const double un = sqrt((u0 * u0 + u1 * u1) + u2 * u2);
-                    const double d0 = u0 / un, d1 = u1 / un, d2 = u2 / un;
+                    const double iun = 1.0 / un;  // (record only, as above)
+                    const double d0 = u0 * iun, d1 = u1 * iun, d2 = u2 * iun;
                     const double b0 = -kSh1 * d1, b1 = kSh1 * d2, b2 = -kSh1 * d0;
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch)
