@@ -89,7 +89,7 @@ void dev_alloc(T** p, size_t count) {
 void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
-    void* ptrs[] = {c->x, c->m, c->v, c->vis_sgn, c->adam_ring, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->gbuf,
+    void* ptrs[] = {c->x, c->m, c->v, c->vis_sgn, c->adam_ring, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->gbuf,
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->tile_cnt, c->tile_cur, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
@@ -416,7 +416,6 @@ void alloc_row_scratch(Ctx* c, size_t cap) {
     dev_alloc(&c->depth_key, cap);
     dev_alloc(&c->tiles, cap);
     dev_alloc(&c->g2d, 3 * cap);
-    dev_alloc(&c->pcache, static_cast<size_t>(kParamVec) * cap);
     dev_alloc(&c->gbuf, c->D * cap);
     dev_alloc(&c->vis_mask, cap / 32);
     dev_alloc(&c->vis_prefix, cap / 32);

@@ -17,19 +17,21 @@ namespace {
 
 // Fold of one visible row; FP64 arithmetic over FP32 inputs. g receives the
 // D parameter gradients; returns the screen-space gradient norm.
-// The row's parameters from the preprocess's row-contiguous cache (visible
-// rows only; same values as x[.][i] this step).
+// The row's parameters in component order, from its row-major x (current:
+// the preprocess caught every visible row up and nothing writes x before the
+// Adam): whole aligned sectors, 64 bytes at SH degree 0.
 template <int fd>
-__device__ __forceinline__ void load_row(const float4* __restrict__ pcache, uint32_t i, float (&prm)[11 + fd]) {
-    constexpr int D = 11 + fd, NV = (D + 3) / 4;
-    float v[4 * NV];
+__device__ __forceinline__ void load_row(const float* __restrict__ x, uint32_t i, float (&prm)[11 + fd]) {
+    constexpr int D = 11 + fd, NS = fd <= 4 ? 16 : 24;  // slots in use
+    const float4* r4 = reinterpret_cast<const float4*>(x + static_cast<size_t>(i) * row_stride(fd));
+    float v[NS];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const float4 q = pcache[static_cast<size_t>(kParamVec) * i + k];
+    for (int k = 0; k < NS / 4; ++k) {
+        const float4 q = r4[k];
         v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
     }
 #pragma unroll
-    for (int k = 0; k < D; ++k) prm[k] = v[k];
+    for (int c = 0; c < D; ++c) prm[c] = v[pslot(c, fd)];
 }
 
 // The 9 image-space gradients of row i: FP32 record, or the FP64 slot of a
@@ -212,7 +214,6 @@ template <int fd>
 __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict__ x, size_t cap, uint32_t n,
                                                          DevCam cam, const uint32_t* __restrict__ tiles,
                                                          const float4* __restrict__ rec,
-                                                         const float4* __restrict__ pcache,
                                                          const float4* __restrict__ g2d,
                                                          const double* __restrict__ g2d_wide, double* __restrict__ gout,
                                                          double* __restrict__ sgn_out, uint8_t* __restrict__ vis) {
@@ -227,7 +228,7 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
     const bool visible = tiles[i] > 0;
     if (visible) {
         float prm[11 + fd];
-        load_row<fd>(pcache, i, prm);
+        load_row<fd>(x, i, prm);
         s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
     }
 #pragma unroll
@@ -244,7 +245,6 @@ template <int fd>
 __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, DevCam cam,
                                                            const uint32_t* __restrict__ vis_rows, uint32_t V,
                                                            const float4* __restrict__ rec,
-                                                           const float4* __restrict__ pcache,
                                                            const float4* __restrict__ g2d,
                                                            const double* __restrict__ g2d_wide, float* __restrict__ gbuf,
                                                            float* __restrict__ vis_sgn) {
@@ -257,7 +257,7 @@ __global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restri
 #pragma unroll
     for (int c = 0; c < D; ++c) g[c] = 0.0;
     float prm[11 + fd];
-    load_row<fd>(pcache, i, prm);
+    load_row<fd>(x, i, prm);
     const double s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
 #pragma unroll
     for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + p] = static_cast<float>(g[c]);  // coalesced
@@ -450,10 +450,10 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
     const uint32_t blocks = static_cast<uint32_t>((c->n + 255) / 256);
     if (c->fd == 3)
         launch_pdl(c->stream, blocks, 256, 0, fold_grads_kernel<3>, c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
-                                                            c->rec, c->pcache, c->g2d, c->g2d_wide, g_out, sgn, vis);
+                                                            c->rec, c->g2d, c->g2d_wide, g_out, sgn, vis);
     else
         launch_pdl(c->stream, blocks, 256, 0, fold_grads_kernel<12>, c->x, c->cap, static_cast<uint32_t>(c->n), cam, c->tiles,
-                                                             c->rec, c->pcache, c->g2d, c->g2d_wide, g_out, sgn, vis);
+                                                             c->rec, c->g2d, c->g2d_wide, g_out, sgn, vis);
     BSG_LAUNCHED(c);
 }
 
@@ -461,11 +461,11 @@ void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
     if (V == 0) return;
     if (c->fd == 3)
         launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<3>, c->x, c->cap, cam, c->vis_rows, V,
-                                                                        c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
+                                                                        c->rec, c->g2d, c->g2d_wide, c->gbuf,
                                                                         c->vis_sgn);
     else
         launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<12>, c->x, c->cap, cam, c->vis_rows, V,
-                                                                         c->rec, c->pcache, c->g2d, c->g2d_wide, c->gbuf,
+                                                                         c->rec, c->g2d, c->g2d_wide, c->gbuf,
                                                                         c->vis_sgn);
     BSG_LAUNCHED(c);
 }

@@ -36,7 +36,6 @@ constexpr double kQScale = 0.84932180028801904272;  // sqrt(0.5 * log2(e))
 constexpr double kQScale2 = kQScale * kQScale;
 constexpr int kMaxFd = 12;            // SH degree 1 (cloud.hpp:16-17)
 constexpr int kMaxD = 11 + kMaxFd;    // pos3 rot4 ls3 feat fd op1
-constexpr int kParamVec = (kMaxD + 3) / 4;  // float4 per row in the parameter cache
 constexpr double kSh0 = 0.28209479177387814;  // cloud.hpp:14
 constexpr double kSh1 = 0.4886025119029199;   // cloud.hpp:15
 
@@ -225,8 +224,6 @@ struct Ctx {
     uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
     float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
     double* g2d_wide = nullptr;    // [kWideCap][9] FP64 gradients of wide splats (kWideBit | slot in rec[3i+2].w)
-    float4* pcache = nullptr;      // kParamVec float4 per row: the parameters of the rows the preprocess
-                                   // found visible, row-contiguous for the fold's gather
     float* gbuf = nullptr;         // parameter gradient of the visible rows, [D][cap] by visible position
     float4* adam_ring = nullptr;   // per Adam step t, at t % kAdamRing: {1/bc1, 1/bc2, lr_pos, -}
     uint32_t* vis_prefix = nullptr;// visible rows before each 32-row word (visible position = prefix + rank in word)

@@ -60,7 +60,6 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
                                                                  uint32_t* __restrict__ tiles,
                                                                  float4* __restrict__ g2d,
                                                                  double* __restrict__ g2d_wide,
-                                                                 float4* __restrict__ pcache,
                                                                  StepCounters* __restrict__ counters,
                                                                  StepScalars* __restrict__ scalars,
                                                                  uint32_t* __restrict__ tile_cnt) {
@@ -227,14 +226,6 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
                 prm[kFeat + 3] = b.z;  // op
             }
         }
-        // the row's parameters, row-contiguous, for the fold's gather (64 / 96 B;
-        // written for every FP32-test survivor, read only for visible rows)
-#pragma unroll
-        for (int v = 0; v < kParamVec; ++v)
-            if (4 * v < 11 + (fd >= 12 ? kMaxFd : 3))
-                pcache[static_cast<size_t>(kParamVec) * i + v] =
-                    make_float4(prm[4 * v], 4 * v + 1 < kMaxD ? prm[4 * v + 1] : 0.f,
-                                4 * v + 2 < kMaxD ? prm[4 * v + 2] : 0.f, 4 * v + 3 < kMaxD ? prm[4 * v + 3] : 0.f);
         const double p0 = prm[kPos + 0], p1 = prm[kPos + 1], p2 = prm[kPos + 2];
         // p_cam = R p + t (camera.hpp:28)
         double pc[3];
@@ -427,7 +418,7 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const uint32_t blocks = static_cast<uint32_t>((c->n + kPreChunk - 1) / kPreChunk);
     const LazyAdam la = make_lazy_adam(c);
     launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->m, c->v, la, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
-                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->pcache, c->counters,
+                                                      c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->counters,
                                                       c->scalars, c->tile_cnt);
     BSG_LAUNCHED(c);
 }
