@@ -356,11 +356,16 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     pv.seq = ++c->mbox_seq;
     pv.extra_src = &c->counters->visible_pre;
     pv.extra_dst = &c->mbox->visible_pre;
-    compact_visible(c, static_cast<uint32_t>(c->n), true, pv);
-    stage_end(c, kStCompact);
     // the previous view's largest tile picks the path up front, so a dense
-    // sequence of views does not pay the speculative per-tile emission
-    if (c->global_order || c->last_max_tile > kTileSortCap) {
+    // sequence of views does not pay the speculative per-tile emission; the
+    // per-tile path compacts from the preprocess's visibility mask (no depth keys)
+    const bool global_path = c->global_order || c->last_max_tile > kTileSortCap;
+    if (global_path)
+        compact_visible(c, static_cast<uint32_t>(c->n), true, pv);
+    else
+        compact_visible_mask(c, static_cast<uint32_t>(c->n), pv);
+    stage_end(c, kStCompact);
+    if (global_path) {
         launch_tile_scan(c, cam, ++c->mbox_seq);  // only for the largest-tile count (cheap)
         wait_mailbox(c, &c->mbox->seq_v, pv.seq);
         V = c->mbox->V;
@@ -385,7 +390,10 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
         c->last_max_tile = max_tile;
         stage_end(c, kStPairs);
         if (max_tile > kTileSortCap) {
-            P = bin_global(c, cam, V, kbits);  // a tile too long for the shared-memory sort
+            // a tile too long for the shared-memory sort: the global path, whose
+            // depth sort needs the keyed compaction
+            compact_visible(c, static_cast<uint32_t>(c->n), true);
+            P = bin_global(c, cam, V, kbits);
         } else {
             if (P > c->pcap) {  // the emission ran out of capacity: grow, reset the cursors, emit again
                 ensure_pair_capacity(c, P);

@@ -422,6 +422,9 @@ __host__ __device__ inline int depth_key_bits(uint32_t V) {
 }
 
 // ---- building blocks (scan.cu, radix.cu) -------------------------------
+// Visible rows (ascending) from the preprocess's visibility mask: the
+// per-tile binning path's compaction (no depth keys).
+void compact_visible_mask(Ctx* c, uint32_t n, const Publish& pub);
 // Exclusive scan of n u32 values read through a gather (in[idx ? idx[i] : i]),
 // optional predicate compaction. Result in out; total in *total_dev.
 void scan_exclusive_u32(Ctx* c, const uint32_t* in, const uint32_t* gather_idx, uint32_t* out, uint32_t n,

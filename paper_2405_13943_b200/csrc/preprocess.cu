@@ -62,7 +62,8 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
                                                                  double* __restrict__ g2d_wide,
                                                                  StepCounters* __restrict__ counters,
                                                                  StepScalars* __restrict__ scalars,
-                                                                 uint32_t* __restrict__ tile_cnt) {
+                                                                 uint32_t* __restrict__ tile_cnt,
+                                                                 uint32_t* __restrict__ vis_mask, uint32_t mask_words) {
     pdl_prologue();
     __shared__ uint32_t s_rows[kPreChunk];
     __shared__ uint8_t s_stale[kPreChunk];     // Adam steps each queued row is behind (lazy Adam)
@@ -71,6 +72,8 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
     __shared__ uint32_t s_count, s_nstale;
     __shared__ unsigned long long s_zmin_inv, s_zmax;
     __shared__ uint32_t s_visible;
+    __shared__ uint32_t s_vis[kPreChunk / 32];  // this chunk's visibility mask words
+    if (threadIdx.x < kPreChunk / 32) s_vis[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
         s_count = 0;
         s_visible = 0;
@@ -353,6 +356,7 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
                 zmin_inv = max(zmin_inv, ~zb);
                 zmax = max(zmax, zb);
                 ++nvis;
+                atomicOr(&s_vis[(i - chunk0) >> 5], 1u << (i & 31u));
                 const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
                 g2d[3 * static_cast<size_t>(i) + 0] = zero;
                 g2d[3 * static_cast<size_t>(i) + 1] = zero;
@@ -375,6 +379,10 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
         atomicAdd(&s_visible, nvis);
     }
     __syncthreads();
+    // the visibility mask (1 bit per row, the compaction's input on the
+    // per-tile path and the Adam's visible-row test): whole words per chunk
+    if (threadIdx.x < kPreChunk / 32 && (chunk0 >> 5) + threadIdx.x < mask_words)
+        vis_mask[(chunk0 >> 5) + threadIdx.x] = s_vis[threadIdx.x];
     if (threadIdx.x == 0 && s_zmax) {
         atomicMax(&counters->zmin_inv, s_zmin_inv);
         atomicMax(&counters->zmax, s_zmax);
@@ -419,7 +427,8 @@ void launch_preprocess(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const LazyAdam la = make_lazy_adam(c);
     launch_pdl(c->stream, blocks, kPreThreads, 0, preprocess_kernel, c->x, c->m, c->v, la, static_cast<uint32_t>(c->n), c->fd, cam, rc, c->rec,
                                                       c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->counters,
-                                                      c->scalars, c->tile_cnt);
+                                                      c->scalars, c->tile_cnt, c->vis_mask,
+                                                      static_cast<uint32_t>(c->cap / 32));
     BSG_LAUNCHED(c);
 }
 

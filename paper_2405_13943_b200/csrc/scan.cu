@@ -224,6 +224,71 @@ __global__ __launch_bounds__(kScanThreads) void scan_kernel(const uint32_t* __re
     }
 }
 
+// Compaction of the visible rows from the 1-bit-per-row visibility mask the
+// preprocess writes (per-tile binning path: no depth keys needed): 8 mask
+// words (256 rows) per thread, decoupled look-back across CTAs, each
+// thread's visible rows written in ascending order. Reads n / 8 bytes instead
+// of the 4-byte tile count of every row.
+constexpr int kMaskItems = 8;
+constexpr int kMaskTile = kScanThreads * kMaskItems;  // words per CTA
+__global__ __launch_bounds__(kScanThreads) void compact_mask_kernel(const uint32_t* __restrict__ mask, uint32_t nwords,
+                                                                    unsigned long long* status, Lookback lb,
+                                                                    Publish pub, uint32_t* total_out,
+                                                                    uint32_t* __restrict__ out_rows) {
+    pdl_prologue();
+    __shared__ uint32_t s_tile, s_prefix, s_total;
+    __shared__ uint32_t s_warp[kScanThreads / 32];
+    if (threadIdx.x == 0) s_tile = static_cast<uint32_t>(atomicAdd(lb.ticket, 1ull) - lb.base);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t w0 = static_cast<uint64_t>(tile) * kMaskTile + static_cast<uint64_t>(threadIdx.x) * kMaskItems;
+    uint32_t wv[kMaskItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kMaskItems; ++k) {
+        wv[k] = w0 + k < nwords ? mask[w0 + k] : 0u;
+        sum += __popc(wv[k]);
+    }
+    const uint32_t tprefix = block_exclusive(sum, s_warp, &s_total);
+    if (threadIdx.x < 32) {
+        const uint32_t total = s_total;
+        if (tile == 0) {
+            if (threadIdx.x == 0) {
+                publish(&status[0], lb.epoch, kFlagInc, total);
+                s_prefix = 0;
+            }
+        } else {
+            if (threadIdx.x == 0) publish(&status[tile], lb.epoch, kFlagAgg, total);
+            const uint32_t prefix = look_back(status, tile, lb.epoch);
+            if (threadIdx.x == 0) {
+                publish(&status[tile], lb.epoch, kFlagInc, prefix + total);
+                s_prefix = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (static_cast<uint64_t>(tile) + 1) * kMaskTile >= nwords) {
+        const uint32_t grand = s_prefix + s_total;
+        if (total_out) *total_out = grand;
+        if (pub.seq_word) {  // host-mapped mailbox: value(s), system fence, sequence word
+            *reinterpret_cast<volatile uint32_t*>(pub.val) = grand;
+            if (pub.extra_dst) *reinterpret_cast<volatile uint32_t*>(pub.extra_dst) = *pub.extra_src;
+            __threadfence_system();
+            *reinterpret_cast<volatile uint32_t*>(pub.seq_word) = pub.seq;
+        }
+    }
+    uint32_t run = s_prefix + tprefix;
+#pragma unroll
+    for (int k = 0; k < kMaskItems; ++k) {
+        uint32_t b = wv[k];
+        const uint32_t row0 = static_cast<uint32_t>((w0 + k) * 32);
+        while (b) {
+            out_rows[run++] = row0 + (__ffs(b) - 1);
+            b &= b - 1;
+        }
+    }
+}
+
 void prepare_status(Ctx* c, uint32_t tiles) {
     const size_t need = static_cast<size_t>(tiles) + 1;
     if (c->scan_status_cap < need) {
@@ -311,6 +376,16 @@ void compact_visible(Ctx* c, uint32_t n, bool key32, const Publish& pub) {
                                                               c->counters, c->vrow[0], &c->counters->depth_hist[0][0], 0,
                                                               c->vis_mask, static_cast<uint32_t>(c->cap / 32),
                                                               c->vis_prefix);
+    BSG_LAUNCHED(c);
+}
+
+void compact_visible_mask(Ctx* c, uint32_t n, const Publish& pub) {
+    const uint32_t nwords = (n + 31) / 32;
+    const uint32_t tiles = std::max<uint32_t>(1, (nwords + kMaskTile - 1) / kMaskTile);
+    prepare_status(c, tiles);
+    const Lookback lb = next_lookback(c, 0, tiles);
+    launch_pdl(c->stream, tiles, kScanThreads, 0, compact_mask_kernel, c->vis_mask, nwords, c->scan_status, lb, pub,
+               &c->counters->visible, c->vis_rows);
     BSG_LAUNCHED(c);
 }
 
