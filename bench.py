@@ -228,10 +228,11 @@ def algorithmic_bytes(stage, n, V, P, HW, shared):
         "adam": (6 * D4 + D4 + 4) * V + (6 * D4 + 4) * n // 32 + 8 * D4 * shared,
         # visible row's parameters + 2D gradient record read; parameter gradient + densify stats written
         "fold": (D4 + 48 + 4) * V + (D4 + 8) * V,
-        # pos + log-scale + step stamp of every row, tiles-touched written; rest of the row, splat record,
-        # depth key, zeroed gradient record for visible rows
-        "preprocess": 32 * n + (32 + 48 + 8 + 48) * V,
-        "compact": 4 * n + 16 * V,
+        # pos + log-scale + step stamp of every row, tiles-touched and the visibility bit written; rest of the
+        # row, splat record, depth key, zeroed gradient record for visible rows
+        "preprocess": 32 * n + n // 8 + (32 + 48 + 8 + 48) * V,
+        # per-tile path: the visibility mask read, the visible rows written
+        "compact": n // 8 + 4 * V,
         # per-tile binning (the path taken at this config):
         "bin_scan": 0,                              # tile scan: a few KB of per-tile counts / ranges
         "bin_emit": 4 * V + 16 * V + 4 * P,         # visible row + its rect read, one row written per pair
