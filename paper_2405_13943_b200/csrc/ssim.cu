@@ -104,17 +104,30 @@ __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __r
     double local = 0.0;
     for (int ch = 0; ch < 3; ++ch) {
         // window (wx, wy) covers pixels [wx, wx+10] x [wy, wy+10]
-        for (int k = threadIdx.x; k < kPX * kPY; k += kThreads) {
-            const int lx = k % kPX, ly = k / kPX;
-            const int gx = wx0 + lx, gy = wy0 + ly;
-            float a = 0.f, b = 0.f;
-            if (gx < W && gy < H) {
-                const size_t p = 3 * (static_cast<size_t>(gy) * W + gx) + ch;
-                a = x[p];
-                b = gt_val(y, p);
+        // patch rows per warp, columns per lane: a row's 74 loads in flight
+        // together, consecutive lanes on consecutive pixels
+        for (int ly = threadIdx.x >> 5; ly < kPY; ly += kThreads / 32) {
+            const int gy = wy0 + ly, lane = threadIdx.x & 31;
+            float a[3], b[3];
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const int lx = lane + 32 * cc, gx = wx0 + lx;
+                a[cc] = 0.f;
+                b[cc] = 0.f;
+                if (lx < kPX && gx < W && gy < H) {
+                    const size_t p = 3 * (static_cast<size_t>(gy) * W + gx) + ch;
+                    a[cc] = x[p];
+                    b[cc] = gt_val(y, p);
+                }
             }
-            S.x[ly][lx] = a;
-            S.y[ly][lx] = b;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const int lx = lane + 32 * cc;
+                if (lx < kPX) {
+                    S.x[ly][lx] = a[cc];
+                    S.y[ly][lx] = b[cc];
+                }
+            }
         }
         __syncthreads();
         // horizontal: 26 rows x 16 groups of 4 outputs, five moments
@@ -213,13 +226,27 @@ __global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* _
         float g[3][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         if (has_ssim) {
             // windows [px0-10, px0+63] x [py0-10, py0+15], zero outside the valid grid
-            for (int k = threadIdx.x; k < kPX * kPY; k += kThreads) {
-                const int lx = k % kPX, ly = k / kPX;
-                const int wx = px0 - 2 * kHalf + lx, wy = py0 - 2 * kHalf + ly;
-                const bool ok = wx >= 0 && wy >= 0 && wx < Wv && wy < Hv;
-                const size_t o = ok ? static_cast<size_t>(wy) * Wv + wx : 0;
+            // patch rows per warp, columns per lane: a row's 3 x 74 loads in
+            // flight together (coalesced), then the stores
+            for (int ly = threadIdx.x >> 5; ly < kPY; ly += kThreads / 32) {
+                const int wy = py0 - 2 * kHalf + ly, lane = threadIdx.x & 31;
+                float v[3][3];
 #pragma unroll
-                for (int m = 0; m < 3; ++m) S.f[m][ly][lx] = ok ? f[(3 * ch + m) * plane + o] : 0.f;
+                for (int cc = 0; cc < 3; ++cc) {
+                    const int lx = lane + 32 * cc, wx = px0 - 2 * kHalf + lx;
+                    const bool ok = lx < kPX && wx >= 0 && wy >= 0 && wx < Wv && wy < Hv;
+                    const size_t o = ok ? static_cast<size_t>(wy) * Wv + wx : 0;
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) v[cc][m] = ok ? f[(3 * ch + m) * plane + o] : 0.f;
+                }
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    const int lx = lane + 32 * cc;
+                    if (lx < kPX) {
+#pragma unroll
+                        for (int m = 0; m < 3; ++m) S.f[m][ly][lx] = v[cc][m];
+                    }
+                }
             }
             __syncthreads();
 #pragma unroll
