@@ -336,6 +336,7 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
     const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
     launch_pdl(c->stream, 1, 512, 0, zero_counters_kernel, c->counters, c->tile_cnt, ntiles);
     BSG_LAUNCHED(c);
+    c->tile_scan_used = false;
     stage_begin(c, kStPreprocess);
     launch_preprocess(c, cam, rc);  // + pairs per tile
     stage_end(c, kStPreprocess);

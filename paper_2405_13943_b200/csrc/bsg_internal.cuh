@@ -98,6 +98,11 @@ struct StepCounters {
     unsigned long long zmax;      // bits of the largest visible FP64 depth
     uint32_t depth_hist[8][256];  // digit histograms of the visible depth keys (filled by the compaction)
     uint32_t tile_hist[2][256];   // digit histograms of the tile keys (filled by the pair emission)
+    uint32_t order_hist[1024];    // tiles per launch-order bucket (1023 - min(pairs, 1023)), tile scan
+    uint32_t order_cur[1024];     // per-bucket placement cursors of the launch order
+    uint32_t tile_max;            // largest per-tile pair count
+    uint32_t pad4;
+    unsigned long long pairs_wide;  // P without 32-bit wrap-around (the 2^30 capacity guard)
 };
 
 // Host-mapped pinned mailbox: the compaction and the pair-offset scan write
@@ -206,6 +211,7 @@ struct Ctx {
     cudaStream_t comm_stream = nullptr;  // consensus rounds (overlap with the next step)
     cudaEvent_t x_ready = nullptr, round_done = nullptr, round_t0 = nullptr, round_t1 = nullptr;
     bool round_pending = false;
+    bool tile_scan_used = false;  // the multi-CTA tile scan ran since this step's counters were zeroed
     bool round_diag = false;
     double* round_host = nullptr;        // pinned copy of round_scalars
     int fd = 3, D = 14;
@@ -466,6 +472,7 @@ void launch_pairs(Ctx* c, const DevCam& cam, uint32_t V);
 // tile counts (P and the largest count to the mailbox under `seq`), the rows
 // placed into their tiles (pval[1]), each tile sorted by (depth, row) into pval[0].
 void launch_tile_scan(Ctx* c, const DevCam& cam, uint32_t seq);
+void launch_tile_scan_multi(Ctx* c, uint32_t ntiles, uint32_t seq);  // (scan.cu; views over 1024 tiles)
 void launch_emit_tiles(Ctx* c, const DevCam& cam);
 void launch_tile_sort(Ctx* c, const DevCam& cam, uint32_t max_tile);
 // The f32 arrays of the GSPL checkpoint section ((11 + fd) n floats, section order) into out.

@@ -822,6 +822,10 @@ void launch_ranges(Ctx* c, const DevCam& cam, uint32_t V, uint32_t P) {
 
 void launch_tile_scan(Ctx* c, const DevCam& cam, uint32_t seq) {
     const uint32_t ntiles = static_cast<uint32_t>(cam.tiles_x * cam.tiles_y);
+    if (ntiles > 1024u) {  // several CTAs (scan.cu)
+        launch_tile_scan_multi(c, ntiles, seq);
+        return;
+    }
     launch_pdl(c->stream, 1, 1024, 0, tile_scan_kernel, c->tile_cnt, ntiles, c->ranges, c->tile_cur, c->tile_order,
                c->mbox, seq, &c->counters->pairs);
     BSG_LAUNCHED(c);

@@ -1,6 +1,8 @@
 // Single-pass exclusive scan with decoupled look-back, and the stable
 // compaction of visible splats built on it. Both are HBM-bound streaming
 // passes: one read of the input, one write of the output.
+#include <cstddef>
+
 #include "bsg_internal.cuh"
 
 #include <atomic>
@@ -45,6 +47,32 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_warp
         }
         if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
         if (lane == kScanThreads / 32 - 1) *total = wi;
+    }
+    __syncthreads();
+    return s_warp[warp] + inc - v;
+}
+
+// block_exclusive for a 1024-thread block (32 warps).
+__device__ __forceinline__ uint32_t block_exclusive_1024(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi - w;
+        if (lane == 31) *total = wi;
     }
     __syncthreads();
     return s_warp[warp] + inc - v;
@@ -289,6 +317,122 @@ __global__ __launch_bounds__(kScanThreads) void compact_mask_kernel(const uint32
     }
 }
 
+// Per-tile binning, multi-CTA: 1024 tiles per CTA. Pass A: each tile's pair
+// range and its kTileSub sub-cursors from an exclusive scan of the tile
+// counts (decoupled look-back across CTAs); the launch-order histogram, the
+// largest tile and the total; the last CTA publishes P, the largest tile and
+// the capacity flag to the mailbox (every predecessor's contributions are in
+// by then: each adds them before publishing its aggregate). Pass B: the
+// launch order (tiles by descending count, order inside a bucket free), each
+// CTA placing its tiles through per-bucket ranges reserved with one atomic
+// per bucket.
+constexpr int kTileScanThreads = 1024;
+__global__ __launch_bounds__(kTileScanThreads) void tile_scan_a_kernel(const uint32_t* __restrict__ cnt, uint32_t ntiles,
+                                                                      uint2* __restrict__ ranges,
+                                                                      uint32_t* __restrict__ cur,
+                                                                      unsigned long long* status, Lookback lb,
+                                                                      StepCounters* __restrict__ counters, Mailbox* mb,
+                                                                      uint32_t seq) {
+    pdl_prologue();
+    __shared__ uint32_t s_tile, s_prefix, s_total, s_max;
+    __shared__ uint32_t s_warp[kTileScanThreads / 32];
+    __shared__ uint32_t s_hist[1024];
+    __shared__ unsigned long long s_wide;
+    const uint32_t t = threadIdx.x;
+    s_hist[t] = 0;
+    if (t == 0) {
+        s_tile = static_cast<uint32_t>(atomicAdd(lb.ticket, 1ull) - lb.base);
+        s_max = 0;
+        s_wide = 0;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile, i = tile * kTileScanThreads + t;
+    static_assert(kTileSub == 4, "one uint4 of sub-counts per tile");
+    const uint4 sc = i < ntiles ? reinterpret_cast<const uint4*>(cnt)[i] : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t v = sc.x + sc.y + sc.z + sc.w;
+    if (i < ntiles) atomicAdd(&s_hist[1023u - min(v, 1023u)], 1u);
+    uint32_t mx = v;
+    unsigned long long wide = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        wide += __shfl_xor_sync(0xffffffffu, wide, o);
+    }
+    if ((t & 31) == 0) {
+        atomicMax(&s_max, mx);
+        atomicAdd(&s_wide, wide);
+    }
+    const uint32_t ex = block_exclusive_1024(v, s_warp, &s_total);  // (its barriers order the shared atomics above)
+    // this CTA's contributions to the bucket counts, the largest tile and the
+    // wide total, before its aggregate is published
+    if (s_hist[t]) atomicAdd(&counters->order_hist[t], s_hist[t]);
+    if (t == 0) {
+        atomicMax(&counters->tile_max, s_max);
+        atomicAdd(&counters->pairs_wide, s_wide);
+    }
+    __threadfence();
+    __syncthreads();
+    if (t < 32) {
+        const uint32_t total = s_total;
+        if (tile == 0) {
+            if (t == 0) {
+                publish(&status[0], lb.epoch, kFlagInc, total);
+                s_prefix = 0;
+            }
+        } else {
+            if (t == 0) publish(&status[tile], lb.epoch, kFlagAgg, total);
+            const uint32_t prefix = look_back(status, tile, lb.epoch);
+            if (t == 0) {
+                publish(&status[tile], lb.epoch, kFlagInc, prefix + total);
+                s_prefix = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    if (i < ntiles) {
+        const uint32_t b = s_prefix + ex;
+        ranges[i] = make_uint2(b, b + v);
+        reinterpret_cast<uint4*>(cur)[i] = make_uint4(b, b + sc.x, b + sc.x + sc.y, b + sc.x + sc.y + sc.z);
+    }
+    if (t == 0 && (static_cast<uint64_t>(tile) + 1) * kTileScanThreads >= ntiles) {
+        // the last CTA: all predecessors' aggregates (and so their atomics) are in
+        __threadfence();
+        const uint32_t P = s_prefix + s_total;
+        counters->pairs = P;
+        const uint32_t tmax = *reinterpret_cast<volatile uint32_t*>(&counters->tile_max);
+        const unsigned long long pw = *reinterpret_cast<volatile unsigned long long*>(&counters->pairs_wide);
+        *reinterpret_cast<volatile uint32_t*>(&mb->P) = P;
+        *reinterpret_cast<volatile uint32_t*>(&mb->max_tile) = tmax;
+        *reinterpret_cast<volatile uint32_t*>(&mb->pairs_big) = pw >= kMaxPairs ? 1u : 0u;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&mb->seq_p) = seq;
+    }
+}
+
+__global__ __launch_bounds__(kTileScanThreads) void tile_scan_b_kernel(const uint32_t* __restrict__ cnt, uint32_t ntiles,
+                                                                      StepCounters* __restrict__ counters,
+                                                                      uint32_t* __restrict__ order) {
+    pdl_prologue();
+    __shared__ uint32_t s_warp[kTileScanThreads / 32];
+    __shared__ uint32_t s_total;
+    __shared__ uint32_t s_off[1024], s_loc[1024];
+    const uint32_t t = threadIdx.x;
+    s_loc[t] = 0;
+    s_off[t] = block_exclusive_1024(counters->order_hist[t], s_warp, &s_total);  // bucket offsets
+    const uint32_t i = blockIdx.x * kTileScanThreads + t;
+    uint32_t bucket = 0, rank = 0;
+    if (i < ntiles) {
+        const uint4 sc = reinterpret_cast<const uint4*>(cnt)[i];
+        bucket = 1023u - min(sc.x + sc.y + sc.z + sc.w, 1023u);
+        rank = atomicAdd(&s_loc[bucket], 1u);
+    }
+    __syncthreads();
+    // one range per non-empty bucket of this CTA
+    if (s_loc[t]) s_loc[t] = s_off[t] + atomicAdd(&counters->order_cur[t], s_loc[t]);
+    __syncthreads();
+    if (i < ntiles) order[s_loc[bucket] + rank] = i;
+}
+
 void prepare_status(Ctx* c, uint32_t tiles) {
     const size_t need = static_cast<size_t>(tiles) + 1;
     if (c->scan_status_cap < need) {
@@ -386,6 +530,24 @@ void compact_visible_mask(Ctx* c, uint32_t n, const Publish& pub) {
     const Lookback lb = next_lookback(c, 0, tiles);
     launch_pdl(c->stream, tiles, kScanThreads, 0, compact_mask_kernel, c->vis_mask, nwords, c->scan_status, lb, pub,
                &c->counters->visible, c->vis_rows);
+    BSG_LAUNCHED(c);
+}
+
+void launch_tile_scan_multi(Ctx* c, uint32_t ntiles, uint32_t seq) {
+    const uint32_t grid = std::max<uint32_t>(1, (ntiles + kTileScanThreads - 1) / kTileScanThreads);
+    if (c->tile_scan_used) {  // a second scan this step (the emission re-run): its accumulators afresh
+        BSG_CUDA(cudaMemsetAsync(&c->counters->order_hist[0], 0,
+                                 offsetof(StepCounters, pad4) - offsetof(StepCounters, order_hist), c->stream));
+        BSG_CUDA(cudaMemsetAsync(&c->counters->pairs_wide, 0, sizeof(unsigned long long), c->stream));
+    }
+    c->tile_scan_used = true;
+    prepare_status(c, grid);
+    const Lookback lb = next_lookback(c, 0, grid);
+    launch_pdl(c->stream, grid, kTileScanThreads, 0, tile_scan_a_kernel, c->tile_cnt, ntiles, c->ranges, c->tile_cur,
+               c->scan_status, lb, c->counters, c->mbox, seq);
+    BSG_LAUNCHED(c);
+    launch_pdl(c->stream, grid, kTileScanThreads, 0, tile_scan_b_kernel, c->tile_cnt, ntiles, c->counters,
+               c->tile_order);
     BSG_LAUNCHED(c);
 }
 
