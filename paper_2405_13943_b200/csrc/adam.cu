@@ -35,7 +35,8 @@ __device__ __forceinline__ void load_row(const float* __restrict__ x, uint32_t i
 }
 
 // The 9 image-space gradients of row i: FP32 record, or the FP64 slot of a
-// wide splat (slot index in rec[3i+2].w, see kWideArea). The blend backward
+// wide splat (the gradient target -- rec[3i+2].w -- is also in float 9 of the
+// record, see kWideArea). The blend backward
 // accumulates the mean path as sum k L'^T L' d and the covariance path as
 // sum k (L'^T L' d)(L'^T L' d)^T with the scaled factor L' = kQScale L and
 // without the 1/2 (renderer.cpp:298-306); both are rescaled here.
@@ -52,15 +53,16 @@ __device__ __forceinline__ void unscale_g2d(Grad2D& g) {
 }
 __device__ __forceinline__ Grad2D load_g2d(uint32_t i, const float4* __restrict__ rec,
                                            const float4* __restrict__ g2d, const double* __restrict__ g2d_wide) {
+    (void)rec;
     Grad2D g;
-    const uint32_t target = __float_as_uint(rec[3 * static_cast<size_t>(i) + 2].w);
+    const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
+                 gc = g2d[3 * static_cast<size_t>(i) + 2];
+    const uint32_t target = __float_as_uint(gc.y);  // (written there by the preprocess, preprocess.cu)
     if (target & kWideBit) {
         const uint32_t wslot = target & ~kWideBit;
 #pragma unroll
         for (int k = 0; k < 9; ++k) g.v[k] = g2d_wide[9 * static_cast<size_t>(wslot) + k];
     } else {
-        const float4 ga = g2d[3 * static_cast<size_t>(i)], gb = g2d[3 * static_cast<size_t>(i) + 1],
-                     gc = g2d[3 * static_cast<size_t>(i) + 2];
         g.v[0] = ga.x; g.v[1] = ga.y; g.v[2] = ga.z; g.v[3] = ga.w;
         g.v[4] = gb.x; g.v[5] = gb.y; g.v[6] = gb.z; g.v[7] = gb.w; g.v[8] = gc.x;
     }

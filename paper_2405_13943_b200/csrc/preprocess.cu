@@ -360,7 +360,9 @@ __global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __res
                 const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
                 g2d[3 * static_cast<size_t>(i) + 0] = zero;
                 g2d[3 * static_cast<size_t>(i) + 1] = zero;
-                g2d[3 * static_cast<size_t>(i) + 2] = zero;
+                // (float 9, unused by the accumulators: the gradient target, so the
+                // fold reads it with the gradients instead of from the splat record)
+                g2d[3 * static_cast<size_t>(i) + 2] = make_float4(0.f, __uint_as_float(wslot), 0.f, 0.f);
             }
         }
         tiles[i] = ntiles;
