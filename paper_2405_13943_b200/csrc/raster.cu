@@ -556,7 +556,9 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_fwd_kernel(const uint2
         }
         __syncthreads();
         const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBatch), range.y - start));
-        const int nl = build_list(warp, lane, cnt, s_hm, s_list);
+        // a warp whose pixels have all stopped skips the batch (the CTA leaves
+        // once every warp has)
+        const int nl = __all_sync(0xffffffffu, P0.done && P1.done) ? 0 : build_list(warp, lane, cnt, s_hm, s_list);
         const uint32_t base = start - range.x + 1;  // 1-based list position of entry 0 of the batch
         for (int c0 = 0; c0 < nl; c0 += 32) {
             const uint32_t hm = c0 + lane < nl ? s_list[warp][c0 + lane] >> 16 : 0u;
@@ -748,7 +750,8 @@ __global__ __launch_bounds__(kBlendThreads, 8) void blend_bwd_kernel(const uint2
             if (start + t < end) stage_entry(t, pval[range.x + start + t], rec, tx0, ty0, s_rec, s_hm);
         }
         __syncthreads();
-        const int nl = build_list(warp, lane, end - start, s_hm, s_list);
+        // entries at or past this warp's largest `last` touch none of its pixels
+        const int nl = build_list(warp, lane, max(0, min(end, static_cast<int>(wm)) - start), s_hm, s_list);
         for (int k = nl - 1; k >= 0; --k) {
             const uint32_t wd = s_list[warp][k];
             const uint32_t sj = wd & 0xffffu, hm = wd >> 16;
