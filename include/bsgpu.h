@@ -12,7 +12,8 @@
  *  - Plain pointers and sizes; no C++ or torch types. Host arrays use the
  *    reference's own layouts (GaussianCloud SoA, cloud.hpp:41-46; Image
  *    row-major interleaved RGB, image.hpp:11-25) and FP64, converted at the
- *    boundary. Device-resident state is FP32 component-major ([D][N]).
+ *    boundary. Device-resident parameters and Adam moments are FP32 row-major
+ *    (16 floats a row at SH degree 0, 32 at degree 1).
  *  - Every call returns a status (BSG_OK = 0). On failure bsg_last_error()
  *    returns a thread-local message; BSG_ERR_INVALID_ARGUMENT maps to the
  *    reference's blocksplat::InvalidArgument, everything else to
@@ -189,7 +190,7 @@ int bsg_upload_moments(bsg_ctx* ctx, const double* m, const double* v, uint64_t 
 /* Lazy Adam: a row with no gradient and no penalty this step is not touched;
  * the zero-gradient steps it skipped are replayed (the same FP32 operations,
  * bit for bit) when it next becomes a projection candidate, before any host
- * read, and for every row every `every` steps (1..32; default 32). 1 = the
+ * read, and for every row every `every` steps (1..32; default 16). 1 = the
  * reference's dense update (trainer.cpp:120-131) applied to every row every
  * step. The results do not depend on it; only the cost does. */
 int bsg_set_adam_sync_interval(bsg_ctx* ctx, uint32_t every);

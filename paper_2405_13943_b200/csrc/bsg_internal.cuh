@@ -299,7 +299,10 @@ struct Ctx {
     bsg_trainer_config tcfg{};
     uint64_t iteration = 0;
     uint64_t adam_t = 0;
-    uint32_t adam_sync = 32;       // every row caught up every adam_sync steps (1 = dense Adam; <= kAdamRing / 2)
+    // every row caught up every adam_sync steps (1 = dense Adam; <= kAdamRing / 2). 16: the
+    // full replays run as one MUFU-bound kernel, cheaper than the same steps replayed piecemeal
+    // for the culling candidates (cfg 3 preprocess + Adam: 355 / 347 / 346 / 349 us at 32 / 16 / 12 / 8)
+    uint32_t adam_sync = 16;
     // densification (trainer.cpp:301-385)
     double scene_extent = 1e-9;
     uint64_t alloc_next = 0, alloc_end = 0;  // IdAllocator
@@ -499,7 +502,7 @@ struct AdamStep {
 // constants. Such rows are left untouched and replayed -- the same FP32
 // operations, so bit-identical -- when they are next needed: by the
 // preprocess for a culling candidate, by materialize() before any host read
-// or densification, and every kAdamRing / 2 steps for all rows (the ring of
+// or densification, and every adam_sync (<= kAdamRing / 2) steps for all rows (the ring of
 // per-step constants covers kAdamRing steps). The sparse Adam updates only
 // the visible and anchored rows.
 constexpr uint32_t kAdamRing = 64;
