@@ -531,7 +531,7 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     launch_blend_bwd(c, cam, rc);
     stage_end(c, kStBlendBwd);
     stage_begin(c, kStFold);
-    launch_fold_visible(c, cam, c->last_counters.visible);
+    // (the fold runs fused with the Adam: fold_adam_kernel)
     stage_end(c, kStFold);
     stage_begin(c, kStAdam);
     // penalty + Adam need the round's anchor, duals and rho

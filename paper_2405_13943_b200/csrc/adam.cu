@@ -283,6 +283,13 @@ __device__ __forceinline__ float adam_update(float x, float g, float& m, float& 
     return adam_update_step(x, g, m, v, lr, st.b1, st.omb1, st.b2, st.omb2, st.inv_bc1, st.inv_bc2, st.eps);
 }
 
+template <int fd, int h>
+__device__ __forceinline__ double adam_sector_core(float* __restrict__ x, float* __restrict__ m,
+                                                   float* __restrict__ v, uint32_t i, float (&xs)[8], float (&ms)[8],
+                                                   float (&vs)[8], float (&g)[8], bool visible, float sgn, int aj,
+                                                   const float* __restrict__ z, const float* __restrict__ u, size_t ns,
+                                                   const float* __restrict__ rho_dev, const AdamStep& st);
+
 // One 8-slot sector of row i (slots 8h .. 8h+7), with its slot -> component
 // mapping known at compile time.
 template <int fd, int h>
@@ -310,6 +317,20 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
         const int c = comp_of_slot(8 * h + j, fd);
         g[j] = (visible && c >= 0) ? gbuf[static_cast<size_t>(c) * cap + vpos] : 0.f;
     }
+    return adam_sector_core<fd, h>(x, m, v, i, xs, ms, vs, g, visible, visible ? vis_sgn[vpos] : 0.f, aj, z, u, ns,
+                                   rho_dev, st);
+}
+
+// The rest of a sector's step, its render gradient g given: penalty, Adam,
+// canonicalisation, step stamp and densify statistics, stores.
+template <int fd, int h>
+__device__ __forceinline__ double adam_sector_core(float* __restrict__ x, float* __restrict__ m,
+                                                   float* __restrict__ v, uint32_t i, float (&xs)[8], float (&ms)[8],
+                                                   float (&vs)[8], float (&g)[8], bool visible, float sgn, int aj,
+                                                   const float* __restrict__ z, const float* __restrict__ u, size_t ns,
+                                                   const float* __restrict__ rho_dev, const AdamStep& st) {
+    constexpr int RS = row_stride(fd);
+    const size_t off = static_cast<size_t>(i) * RS + 8 * h;
     double pen = 0.0;
     if (aj >= 0) {
         float zr[8], ur[8];
@@ -338,7 +359,7 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
     if (h == 0) {  // row metadata (bsg_internal.cuh): step stamp; densify statistics (trainer.cpp:284-289)
         xs[kMetaSlot] = __uint_as_float(st.t);
         if (visible) {
-            ms[kMetaSlot] += vis_sgn[vpos];
+            ms[kMetaSlot] += sgn;
             vs[kMetaSlot] = __uint_as_float(__float_as_uint(vs[kMetaSlot]) + 1u);
         }
     }
@@ -352,6 +373,84 @@ __device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __re
     v4[0] = make_float4(vs[0], vs[1], vs[2], vs[3]);
     v4[1] = make_float4(vs[4], vs[5], vs[6], vs[7]);
     return pen;
+}
+
+// Fold + Adam of the visible rows in one pass (thread = visible row): the
+// FP64 fold of fold_visible_kernel, then each sector's step with the
+// gradient still in registers (no [D][V] gradient buffer round trip, the
+// row's parameters read once). Anchored rows that are not visible: the
+// sparse kernel. The first thread files the step's constants in the ring.
+template <int fd>
+__global__ __launch_bounds__(128) void fold_adam_kernel(float* __restrict__ x, float* __restrict__ m,
+                                                        float* __restrict__ v, DevCam cam,
+                                                        const uint32_t* __restrict__ vis_rows, uint32_t V,
+                                                        const float4* __restrict__ rec,
+                                                        const float4* __restrict__ g2d,
+                                                        const double* __restrict__ g2d_wide,
+                                                        const uint32_t* __restrict__ sh_mask,
+                                                        const uint32_t* __restrict__ sh_prefix,
+                                                        const float* __restrict__ z, const float* __restrict__ u,
+                                                        size_t ns, const float* __restrict__ rho_dev, AdamStep st,
+                                                        float4* __restrict__ ring, double* __restrict__ penalty) {
+    pdl_prologue();
+    __shared__ double s_red[4];
+    constexpr int D = 11 + fd, H = fd <= 4 ? 2 : 3, RS = row_stride(fd);
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p == 0) ring[st.t % kAdamRing] = make_float4(st.inv_bc1, st.inv_bc2, st.lr[kPos], 0.f);
+    double pen = 0.0;
+    if (p < V) {
+        const uint32_t i = vis_rows[p];
+        float gf[D], sgn;
+        {
+            double g[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) g[c] = 0.0;
+            float prm[D];
+            load_row<fd>(x, i, prm);
+            sgn = static_cast<float>(fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g));
+#pragma unroll
+            for (int c = 0; c < D; ++c) gf[c] = static_cast<float>(g[c]);
+        }
+        int aj = -1;
+        if (st.has_anchor) {
+            const uint32_t word = i >> 5, bit = i & 31u, sm = sh_mask[word];
+            if ((sm >> bit) & 1u) aj = static_cast<int>(sh_prefix[word] + __popc(sm & ((1u << bit) - 1u)));
+            BSG_DASSERT(aj < static_cast<int>(ns));
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const size_t off = static_cast<size_t>(i) * RS + 8 * h;
+            float xs[8], ms[8], vs[8], gs[8];
+            const float4* x4 = reinterpret_cast<const float4*>(x + off);
+            const float4* m4 = reinterpret_cast<const float4*>(m + off);
+            const float4* v4 = reinterpret_cast<const float4*>(v + off);
+            const float4 xa = x4[0], xb = x4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+            xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w; xs[4] = xb.x; xs[5] = xb.y; xs[6] = xb.z; xs[7] = xb.w;
+            ms[0] = ma.x; ms[1] = ma.y; ms[2] = ma.z; ms[3] = ma.w; ms[4] = mb.x; ms[5] = mb.y; ms[6] = mb.z; ms[7] = mb.w;
+            vs[0] = va.x; vs[1] = va.y; vs[2] = va.z; vs[3] = va.w; vs[4] = vb.x; vs[5] = vb.y; vs[6] = vb.z; vs[7] = vb.w;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = comp_of_slot(8 * h + j, fd);
+                gs[j] = c >= 0 ? gf[c < 0 ? 0 : c] : 0.f;
+            }
+            if (h == 0)
+                pen += adam_sector_core<fd, 0>(x, m, v, i, xs, ms, vs, gs, true, sgn, aj, z, u, ns, rho_dev, st);
+            else if (h == 1)
+                pen += adam_sector_core<fd, 1>(x, m, v, i, xs, ms, vs, gs, true, sgn, aj, z, u, ns, rho_dev, st);
+            else if constexpr (H > 2)
+                pen += adam_sector_core<fd, 2>(x, m, v, i, xs, ms, vs, gs, true, sgn, aj, z, u, ns, rho_dev, st);
+        }
+    }
+    if (st.has_anchor) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pen += __shfl_xor_sync(0xffffffffu, pen, o);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = pen;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const double tt = (s_red[0] + s_red[1]) + (s_red[2] + s_red[3]);
+            if (tt != 0.0) atomicAdd(penalty, tt);
+        }
+    }
 }
 
 // Sparse Adam (lazy Adam, bsg_internal.cuh): the rows with a gradient this
@@ -473,11 +572,22 @@ void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
 }
 
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index) {
-    (void)cam;
     (void)loss_out;
     (void)step_index;
     if (c->n == 0) return;
-    const uint32_t V = c->last_counters.visible;
+    const uint32_t Vf = c->last_counters.visible;
+    if (Vf) {
+        if (c->fd == 3)
+            launch_pdl(PdlAlways{}, c->stream, (Vf + 127) / 128, 128, 0, fold_adam_kernel<3>, c->x, c->m, c->v, cam,
+                       c->vis_rows, Vf, c->rec, c->g2d, c->g2d_wide, c->sh_mask, c->sh_prefix, c->z, c->u,
+                       c->n_shared, c->rho_dev, st, c->adam_ring, &c->scalars->penalty);
+        else
+            launch_pdl(PdlAlways{}, c->stream, (Vf + 127) / 128, 128, 0, fold_adam_kernel<12>, c->x, c->m, c->v, cam,
+                       c->vis_rows, Vf, c->rec, c->g2d, c->g2d_wide, c->sh_mask, c->sh_prefix, c->z, c->u,
+                       c->n_shared, c->rho_dev, st, c->adam_ring, &c->scalars->penalty);
+        BSG_LAUNCHED(c);
+    }
+    const uint32_t V = 0;  // (the visible rows: fold_adam_kernel above)
     const uint32_t n_sh = st.has_anchor ? static_cast<uint32_t>(c->n_shared) : 0u;
     const size_t threads = (static_cast<size_t>(V) + n_sh) * (c->fd <= 4 ? 2 : 3);
     const uint32_t grid = static_cast<uint32_t>(std::max<size_t>(1, (threads + 255) / 256));
