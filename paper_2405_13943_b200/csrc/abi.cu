@@ -89,7 +89,7 @@ void dev_alloc(T** p, size_t count) {
 void use_device(Ctx* c) { BSG_CUDA(cudaSetDevice(c->device)); }
 
 void free_all(Ctx* c) {
-    void* ptrs[] = {c->x, c->m, c->v, c->vis_sgn, c->adam_ring, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide, c->gbuf,
+    void* ptrs[] = {c->x, c->m, c->v, c->adam_ring, c->rec, c->depth_key, c->tiles, c->g2d, c->g2d_wide,
                     c->vis_mask, c->vis_prefix, c->sh_mask, c->sh_prefix, c->vkey[0], c->vkey[1], c->vrow[0], c->vrow[1], c->poff, c->vis_rows, c->pkey[0],
                     c->pkey[1], c->pval[0], c->pval[1], c->ranges, c->tile_order, c->tile_cnt, c->tile_cur, c->scan_status, c->radix_status, c->radix_hist,
                     c->counters, c->scalars, c->losses_dev, c->out_rgb, c->out_T, c->out_n, c->out_last, c->dl_dc,
@@ -420,12 +420,10 @@ void project_and_bin(Ctx* c, const DevCam& cam, const DevRender& rc) {
 void project_and_bin_public(Ctx* c, const DevCam& cam, const DevRender& rc) { project_and_bin(c, cam, rc); }
 
 void alloc_row_scratch(Ctx* c, size_t cap) {
-    dev_alloc(&c->vis_sgn, cap);
     dev_alloc(&c->rec, 3 * cap);
     dev_alloc(&c->depth_key, cap);
     dev_alloc(&c->tiles, cap);
     dev_alloc(&c->g2d, 3 * cap);
-    dev_alloc(&c->gbuf, c->D * cap);
     dev_alloc(&c->vis_mask, cap / 32);
     dev_alloc(&c->vis_prefix, cap / 32);
     dev_alloc(&c->sh_mask, cap / 32);
@@ -871,9 +869,12 @@ int bsg_encode_gspl(bsg_ctx* h, uint8_t* out, size_t out_cap, size_t* out_len) {
         std::memcpy(out + 8, &fd, 4);
         if (n) std::memcpy(out + 12, c->ids.data(), 8 * n);
         if (!floats) return;
-        // gbuf ([D][cap] f32 step scratch) holds the transposed arrays
-        launch_gspl_floats(c, c->gbuf);
-        BSG_CUDA(cudaMemcpyAsync(out + 12 + 8 * n, c->gbuf, 4 * floats, cudaMemcpyDeviceToHost, c->stream));
+        // the transposed arrays in a scratch buffer of the call
+        float* scratch = nullptr;
+        BSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), 4 * static_cast<size_t>(c->D) * c->cap, c->stream));
+        launch_gspl_floats(c, scratch);
+        BSG_CUDA(cudaMemcpyAsync(out + 12 + 8 * n, scratch, 4 * floats, cudaMemcpyDeviceToHost, c->stream));
+        BSG_CUDA(cudaFreeAsync(scratch, c->stream));
         BSG_CUDA(cudaStreamSynchronize(c->stream));
     });
 }

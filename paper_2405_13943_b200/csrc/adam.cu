@@ -239,46 +239,14 @@ __global__ __launch_bounds__(256) void fold_grads_kernel(const float* __restrict
     vis[i] = visible ? 1 : 0;
 }
 
-// Fold over the compacted visible list (V threads): parameter gradient of
-// each visible row into gbuf[D][.] at its visible position, and its
-// screen-space gradient norm into vis_sgn (both coalesced; the Adam adds the
-// norm to the row's densify statistics in the sector it rewrites anyway).
-template <int fd>
-__global__ __launch_bounds__(128) void fold_visible_kernel(const float* __restrict__ x, size_t cap, DevCam cam,
-                                                           const uint32_t* __restrict__ vis_rows, uint32_t V,
-                                                           const float4* __restrict__ rec,
-                                                           const float4* __restrict__ g2d,
-                                                           const double* __restrict__ g2d_wide, float* __restrict__ gbuf,
-                                                           float* __restrict__ vis_sgn) {
-    pdl_prologue();
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= V) return;
-    const uint32_t i = vis_rows[p];
-    constexpr int D = 11 + fd;
-    double g[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) g[c] = 0.0;
-    float prm[11 + fd];
-    load_row<fd>(x, i, prm);
-    const double s = fold_row<fd>(prm, load_g2d(i, rec, g2d, g2d_wide), cam, g);
-#pragma unroll
-    for (int c = 0; c < D; ++c) gbuf[static_cast<size_t>(c) * cap + p] = static_cast<float>(g[c]);  // coalesced
-    vis_sgn[p] = static_cast<float>(s);
-}
-
-// Dense Adam over every row (trainer.cpp:267-281). The parameters and both
-// moments are row-major (row_stride(fd) floats per row, bsg_internal.cuh), so
-// a thread owns one 32-byte sector of a row -- 8 slots of x, m and v as two
-// float4 each -- and consecutive threads stream consecutive sectors. The
-// rotation sector (slots 8-11) is updated and then canonicalised
-// (cloud.cpp:82-85, math.hpp:25-34) in the same thread. Visibility comes from
-// the 1-bit-per-row mask built by the compaction (gradient at the row's
-// visible position of gbuf[D][.]), shared-row anchors from a bit mask +
-// per-word prefix; rows not visible this step have a zero render gradient;
-// shared rows add rho (x - z + u) evaluated at the pre-step x (admm.cpp:24-28,
-// trainer.cpp:257-265). The step's sqrt and division are the approximate MUFU
-// forms (sqrt.approx, rcp-based division, ~2 ulp each on the update term, far
-// below the FP32 rounding of x itself).
+// The Adam step (trainer.cpp:267-281) of one row, a sector at a time. The
+// parameters and both moments are row-major (row_stride(fd) floats per row,
+// bsg_internal.cuh): a sector is 8 slots of x, m and v, two float4 each. The
+// rotation sector (slots 8-11) is canonicalised (cloud.cpp:82-85,
+// math.hpp:25-34) after its step; shared rows add rho (x - z + u) evaluated at
+// the pre-step x (admm.cpp:24-28, trainer.cpp:257-265), their anchor found
+// through the shared-row bit mask + per-word prefix. The step itself is
+// adam_update_step (bsg_internal.cuh), shared with the lazy replays.
 __device__ __forceinline__ float adam_update(float x, float g, float& m, float& v, float lr, const AdamStep& st) {
     return adam_update_step(x, g, m, v, lr, st.b1, st.omb1, st.b2, st.omb2, st.inv_bc1, st.inv_bc2, st.eps);
 }
@@ -289,37 +257,6 @@ __device__ __forceinline__ double adam_sector_core(float* __restrict__ x, float*
                                                    float (&vs)[8], float (&g)[8], bool visible, float sgn, int aj,
                                                    const float* __restrict__ z, const float* __restrict__ u, size_t ns,
                                                    const float* __restrict__ rho_dev, const AdamStep& st);
-
-// One 8-slot sector of row i (slots 8h .. 8h+7), with its slot -> component
-// mapping known at compile time.
-template <int fd, int h>
-__device__ __forceinline__ double adam_sector(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
-                                              size_t cap, uint32_t i, bool visible, uint32_t vpos, int aj,
-                                              const float* __restrict__ gbuf, const float* __restrict__ z,
-                                              const float* __restrict__ u, size_t ns,
-                                              const float* __restrict__ rho_dev, const float* __restrict__ vis_sgn,
-                                              const AdamStep& st) {
-    constexpr int RS = row_stride(fd);
-    const size_t off = static_cast<size_t>(i) * RS + 8 * h;
-    float xs[8], ms[8], vs[8];
-    {
-        const float4* x4 = reinterpret_cast<const float4*>(x + off);
-        const float4* m4 = reinterpret_cast<const float4*>(m + off);
-        const float4* v4 = reinterpret_cast<const float4*>(v + off);
-        const float4 xa = x4[0], xb = x4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
-        xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w; xs[4] = xb.x; xs[5] = xb.y; xs[6] = xb.z; xs[7] = xb.w;
-        ms[0] = ma.x; ms[1] = ma.y; ms[2] = ma.z; ms[3] = ma.w; ms[4] = mb.x; ms[5] = mb.y; ms[6] = mb.z; ms[7] = mb.w;
-        vs[0] = va.x; vs[1] = va.y; vs[2] = va.z; vs[3] = va.w; vs[4] = vb.x; vs[5] = vb.y; vs[6] = vb.z; vs[7] = vb.w;
-    }
-    float g[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int c = comp_of_slot(8 * h + j, fd);
-        g[j] = (visible && c >= 0) ? gbuf[static_cast<size_t>(c) * cap + vpos] : 0.f;
-    }
-    return adam_sector_core<fd, h>(x, m, v, i, xs, ms, vs, g, visible, visible ? vis_sgn[vpos] : 0.f, aj, z, u, ns,
-                                   rho_dev, st);
-}
 
 // The rest of a sector's step, its render gradient g given: penalty, Adam,
 // canonicalisation, step stamp and densify statistics, stores.
@@ -453,59 +390,54 @@ __global__ __launch_bounds__(128) void fold_adam_kernel(float* __restrict__ x, f
     }
 }
 
-// Sparse Adam (lazy Adam, bsg_internal.cuh): the rows with a gradient this
-// step -- the visible rows (their gradient at their visible position) and
-// the anchored rows (penalty rho (x - z + u)) -- all current (the preprocess
-// caught the visible ones up; anchored rows are updated every step). Thread
-// = one sector of one such row; the row's step stamp becomes the step's count.
-// The first thread also files the step's constants in the ring.
+// Sparse Adam of the anchored rows that are not visible (penalty gradient
+// rho (x - z + u) only; the visible rows' steps run in fold_adam_kernel).
+// Thread = one sector of one such row; the row's step stamp becomes the
+// step's count. The first thread also files the step's constants in the ring
+// (the kernel always runs, at least one CTA).
 template <int fd>
 __global__ __launch_bounds__(256, 4) void adam_sparse_kernel(float* __restrict__ x, float* __restrict__ m,
-                                                          float* __restrict__ v, size_t cap,
-                                                          const uint32_t* __restrict__ vis_rows, uint32_t V,
+                                                          float* __restrict__ v,
                                                           const uint32_t* __restrict__ sh_rows, uint32_t n_sh,
                                                           const uint32_t* __restrict__ vis_mask,
-                                                          const float* __restrict__ gbuf,
                                                           const uint32_t* __restrict__ sh_mask,
                                                           const uint32_t* __restrict__ sh_prefix,
                                                           const float* __restrict__ z, const float* __restrict__ u,
                                                           size_t ns, const float* __restrict__ rho_dev, AdamStep st,
-                                                          const float* __restrict__ vis_sgn, float4* __restrict__ ring,
-                                                          double* __restrict__ penalty) {
+                                                          float4* __restrict__ ring, double* __restrict__ penalty) {
     pdl_prologue();
     __shared__ double s_red[8];
-    constexpr int H = fd <= 4 ? 2 : 3;
+    constexpr int H = fd <= 4 ? 2 : 3, RS = row_stride(fd);
     const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t == 0) ring[st.t % kAdamRing] = make_float4(st.inv_bc1, st.inv_bc2, st.lr[kPos], 0.f);
     const size_t idx = t / H;
     const int h = static_cast<int>(t % H);
     double pen = 0.0;
+    uint32_t i = 0;
     bool live = false;
-    uint32_t i = 0, vpos = 0;
-    bool visible = false;
-    if (idx < V) {
-        i = vis_rows[idx];
-        vpos = static_cast<uint32_t>(idx);
-        visible = true;
-        live = true;
-    } else if (idx < static_cast<size_t>(V) + n_sh && st.has_anchor) {
-        i = sh_rows[idx - V];
-        live = !((vis_mask[i >> 5] >> (i & 31u)) & 1u);  // visible anchored rows: done above
+    if (idx < n_sh && st.has_anchor) {
+        i = sh_rows[idx];
+        live = !((vis_mask[i >> 5] >> (i & 31u)) & 1u);  // visible anchored rows: fold_adam_kernel
     }
     if (live) {
-        const uint32_t word = i >> 5, bit = i & 31u;
-        int aj = -1;
-        if (st.has_anchor) {
-            const uint32_t sm = sh_mask[word];
-            if ((sm >> bit) & 1u) aj = static_cast<int>(sh_prefix[word] + __popc(sm & ((1u << bit) - 1u)));
-            BSG_DASSERT(aj < static_cast<int>(ns));
-        }
+        const uint32_t word = i >> 5, bit = i & 31u, sm = sh_mask[word];
+        const int aj = ((sm >> bit) & 1u) ? static_cast<int>(sh_prefix[word] + __popc(sm & ((1u << bit) - 1u))) : -1;
+        BSG_DASSERT(aj < static_cast<int>(ns));
+        const size_t off = static_cast<size_t>(i) * RS + 8 * h;
+        float xs[8], ms[8], vs[8], g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float4* x4 = reinterpret_cast<const float4*>(x + off);
+        const float4* m4 = reinterpret_cast<const float4*>(m + off);
+        const float4* v4 = reinterpret_cast<const float4*>(v + off);
+        const float4 xa = x4[0], xb = x4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+        xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w; xs[4] = xb.x; xs[5] = xb.y; xs[6] = xb.z; xs[7] = xb.w;
+        ms[0] = ma.x; ms[1] = ma.y; ms[2] = ma.z; ms[3] = ma.w; ms[4] = mb.x; ms[5] = mb.y; ms[6] = mb.z; ms[7] = mb.w;
+        vs[0] = va.x; vs[1] = va.y; vs[2] = va.z; vs[3] = va.w; vs[4] = vb.x; vs[5] = vb.y; vs[6] = vb.z; vs[7] = vb.w;
         if (h == 0)
-            pen = adam_sector<fd, 0>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, vis_sgn, st);
+            pen = adam_sector_core<fd, 0>(x, m, v, i, xs, ms, vs, g, false, 0.f, aj, z, u, ns, rho_dev, st);
         else if (h == 1)
-            pen = adam_sector<fd, 1>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, vis_sgn, st);
+            pen = adam_sector_core<fd, 1>(x, m, v, i, xs, ms, vs, g, false, 0.f, aj, z, u, ns, rho_dev, st);
         else if constexpr (H > 2)
-            pen = adam_sector<fd, 2>(x, m, v, cap, i, visible, vpos, aj, gbuf, z, u, ns, rho_dev, vis_sgn, st);
+            pen = adam_sector_core<fd, 2>(x, m, v, i, xs, ms, vs, g, false, 0.f, aj, z, u, ns, rho_dev, st);
     }
     if (st.has_anchor) {
 #pragma unroll
@@ -558,19 +490,6 @@ void launch_fold_grads(Ctx* c, const DevCam& cam, double* g_out, double* sgn, ui
     BSG_LAUNCHED(c);
 }
 
-void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V) {
-    if (V == 0) return;
-    if (c->fd == 3)
-        launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<3>, c->x, c->cap, cam, c->vis_rows, V,
-                                                                        c->rec, c->g2d, c->g2d_wide, c->gbuf,
-                                                                        c->vis_sgn);
-    else
-        launch_pdl(c->stream, (V + 127) / 128, 128, 0, fold_visible_kernel<12>, c->x, c->cap, cam, c->vis_rows, V,
-                                                                         c->rec, c->g2d, c->g2d_wide, c->gbuf,
-                                                                        c->vis_sgn);
-    BSG_LAUNCHED(c);
-}
-
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index) {
     (void)loss_out;
     (void)step_index;
@@ -587,18 +506,21 @@ void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out
                        c->n_shared, c->rho_dev, st, c->adam_ring, &c->scalars->penalty);
         BSG_LAUNCHED(c);
     }
-    const uint32_t V = 0;  // (the visible rows: fold_adam_kernel above)
     const uint32_t n_sh = st.has_anchor ? static_cast<uint32_t>(c->n_shared) : 0u;
-    const size_t threads = (static_cast<size_t>(V) + n_sh) * (c->fd <= 4 ? 2 : 3);
+    const size_t threads = static_cast<size_t>(n_sh) * (c->fd <= 4 ? 2 : 3);
     const uint32_t grid = static_cast<uint32_t>(std::max<size_t>(1, (threads + 255) / 256));
+    if (n_sh == 0 && Vf > 0) {  // (the fused kernel filed the ring entry)
+        if (st.t % c->adam_sync == 0) materialize(c);
+        return;
+    }
     if (c->fd == 3)
-        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<3>, c->x, c->m, c->v, c->cap, c->vis_rows, V,
-                   c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
-                   c->rho_dev, st, c->vis_sgn, c->adam_ring, &c->scalars->penalty);
+        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<3>, c->x, c->m, c->v, c->sh_rows, n_sh,
+                   c->vis_mask, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st, c->adam_ring,
+                   &c->scalars->penalty);
     else
-        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<12>, c->x, c->m, c->v, c->cap, c->vis_rows,
-                   V, c->sh_rows, n_sh, c->vis_mask, c->gbuf, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared,
-                   c->rho_dev, st, c->vis_sgn, c->adam_ring, &c->scalars->penalty);
+        launch_pdl(PdlAlways{}, c->stream, grid, 256, 0, adam_sparse_kernel<12>, c->x, c->m, c->v, c->sh_rows, n_sh,
+                   c->vis_mask, c->sh_mask, c->sh_prefix, c->z, c->u, c->n_shared, c->rho_dev, st, c->adam_ring,
+                   &c->scalars->penalty);
     BSG_LAUNCHED(c);
     // every adam_sync (<= kAdamRing / 2) steps all rows catch up: a stale row
     // never needs a step the ring no longer holds

@@ -222,15 +222,13 @@ struct Ctx {
     float* x = nullptr;
     float* m = nullptr;
     float* v = nullptr;
-    float* vis_sgn = nullptr;      // screen-space gradient norm per visible position (fold -> the Adam's densify stats)
 
     // per-row scratch
-    float4* rec = nullptr;         // 3 x float4 per row: {mx,my,m00,m01},{m11,o,r,g},{b,rect01,rect23,-}
+    float4* rec = nullptr;         // 3 x float4 per row: {l11,l12,l22,k1},{k2,o,r,g},{b,rect01,rect23,target}
     uint64_t* depth_key = nullptr; // FP64 depth bits
     uint32_t* tiles = nullptr;     // tiles touched, 0 = culled
     float4* g2d = nullptr;         // 3 x float4 per row: {gmx,gmy,gc00,gc01},{gc11,gr,gg,gb},{go,-,-,-}
     double* g2d_wide = nullptr;    // [kWideCap][9] FP64 gradients of wide splats (kWideBit | slot in rec[3i+2].w)
-    float* gbuf = nullptr;         // parameter gradient of the visible rows, [D][cap] by visible position
     float4* adam_ring = nullptr;   // per Adam step t, at t % kAdamRing: {1/bc1, 1/bc2, lr_pos, -}
     uint32_t* vis_prefix = nullptr;// visible rows before each 32-row word (visible position = prefix + rank in word)
     uint32_t* vis_mask = nullptr;  // 1 bit per row: visible this step (written by the compaction)
@@ -622,7 +620,6 @@ __device__ __forceinline__ void catch_up_row(float* __restrict__ x, float* __res
     }
 }
 LazyAdam make_lazy_adam(const Ctx* c);
-void launch_fold_visible(Ctx* c, const DevCam& cam, uint32_t V);
 void launch_adam(Ctx* c, const DevCam& cam, const AdamStep& st, double* loss_out, int step_index);
 void materialize(Ctx* c);
 // Every row's step stamp (x slot kMetaSlot) set to `stamp`; with reset_stats
