@@ -212,8 +212,8 @@ def build_block(cfg, rank, world, device, n=None, n_views=None, constant_gt=Fals
     return blk, view_cams, gts, info
 
 
-STAGE_KERNEL = {"blend_bwd": "blend_bwd_kernel", "blend_fwd": "blend_fwd_kernel", "adam": "adam_sparse_kernel",
-                "preprocess": "preprocess_kernel", "fold": "fold_visible_kernel", "loss_ssim": "ssim_windows_kernel"}
+STAGE_KERNEL = {"blend_bwd": "blend_bwd_kernel", "blend_fwd": "blend_fwd_kernel", "adam": "fold_adam_kernel",
+                "preprocess": "preprocess_kernel", "loss_ssim": "ssim_windows_kernel"}
 
 
 def algorithmic_bytes(stage, n, V, P, HW, shared):
@@ -222,12 +222,10 @@ def algorithmic_bytes(stage, n, V, P, HW, shared):
     per row at SH degree 0). DESIGN.md §3 lists the same figures."""
     D4 = 56
     model = {
-        # lazy Adam (DESIGN.md §3.2): x, m, v of the visible rows read + written once, their gradient read,
-        # their step stamp written; every row caught up once per 32 steps (x, m, v read + written, stamp);
-        # shared rows: x, m, v, z, u (the penalty keeps them current every step)
-        "adam": (6 * D4 + D4 + 4) * V + (6 * D4 + 4) * n // 32 + 8 * D4 * shared,
-        # visible row's parameters + 2D gradient record read; parameter gradient + densify stats written
-        "fold": (D4 + 48 + 4) * V + (D4 + 8) * V,
+        # fold + lazy Adam (DESIGN.md §3.2), one kernel: the visible row's 2D gradient record read, its x, m, v
+        # read + written once; every row caught up once per 16 steps (x, m, v read + written, stamp); shared
+        # rows: x, m, v, z, u (the penalty keeps them current every step)
+        "adam": (48 + 6 * D4 + 8) * V + (6 * D4 + 4) * n // 16 + 8 * D4 * shared,
         # pos + log-scale + step stamp of every row, tiles-touched and the visibility bit written; rest of the
         # row, splat record, depth key, zeroed gradient record for visible rows
         "preprocess": 32 * n + n // 8 + (32 + 48 + 8 + 48) * V,

@@ -528,9 +528,7 @@ void train_one(Ctx* c, const bsg_camera& view, const float* gt, double* loss_dev
     stage_begin(c, kStBlendBwd);
     launch_blend_bwd(c, cam, rc);
     stage_end(c, kStBlendBwd);
-    stage_begin(c, kStFold);
-    // (the fold runs fused with the Adam: fold_adam_kernel)
-    stage_end(c, kStFold);
+    // the fold runs fused with the Adam (fold_adam_kernel), stage "adam"
     stage_begin(c, kStAdam);
     // penalty + Adam need the round's anchor, duals and rho
     if (c->round_pending) BSG_CUDA(cudaStreamWaitEvent(c->stream, c->round_done, 0));

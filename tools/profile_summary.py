@@ -22,10 +22,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # kernel -> bench stage whose CUDA-event time it dominates
 STAGE_OF = {"preprocess_kernel": "preprocess", "blend_fwd_kernel": "blend_fwd", "blend_bwd_kernel": "blend_bwd",
-            "adam_kernel": "adam", "adam_rot_kernel": "adam", "adam_sparse_kernel": "adam", "materialize_kernel": "adam", "fold_visible_kernel": "fold", "ssim_windows_kernel": "loss_ssim",
+            "adam_kernel": "adam", "adam_rot_kernel": "adam", "adam_sparse_kernel": "adam", "materialize_kernel": "adam", "fold_visible_kernel": "fold", "fold_adam_kernel": "adam", "ssim_windows_kernel": "loss_ssim",
             "ssim_pixels_kernel": "loss_ssim", "onesweep_kernel": "bin_sort", "scan_kernel": "compact",
             "emit_pairs_kernel": "bin_emit", "emit_tiles_kernel": "bin_emit", "tile_sort_kernel": "bin_sort",
-            "tile_scan_kernel": "bin_scan"}
+            "tile_scan_kernel": "bin_scan", "tile_scan_a_kernel": "bin_scan", "tile_scan_b_kernel": "bin_scan",
+            "compact_mask_kernel": "compact"}
 
 METRICS = [
     ("time_us", "gpu__time_duration.sum", 1e-3),
