@@ -41,11 +41,12 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 
 constexpr int kPreThreads = 256;
 constexpr int kPreRowsPerThread = 4;
-// Phase 1 in batches of kPreRowsPerThread rows per thread, 4096 rows per CTA:
+// Phase 1 in batches of kPreRowsPerThread rows per thread, 3072 rows per CTA:
 // larger chunks give phase 2 (replays, exact projection) more candidates per
 // CTA to spread over its warps (measured at cfg 3: 1024 / 2048 / 4096 / 6144
-// rows per CTA -> 248 / 240 / 229 / 246 us).
-constexpr int kPreSubBatches = 4;
+// rows per CTA -> 248 / 240 / 229 / 246 us; later 3072 / 4096 / 5120 -> 214 /
+// 220 / 224 us).
+constexpr int kPreSubBatches = 3;
 constexpr int kPreChunk = kPreThreads * kPreRowsPerThread * kPreSubBatches;
 
 // Two phases per CTA over a chunk of kPreChunk rows. Phase 1 (FP32, every row):
