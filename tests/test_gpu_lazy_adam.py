@@ -8,7 +8,7 @@ from the same parameters and optimizer state (bsg_upload_moments, t = 5) and
 train 40 steps on camera B only, so cluster A never receives a gradient:
 - block D syncs every step (`bsg_set_adam_sync_interval(1)`: every row's
   zero-gradient step applied in the Adam kernels' file, the dense update);
-- block L keeps the default interval 32: cluster A is replayed 27 steps at
+- block L uses interval 32 (default 16): cluster A is replayed 27 steps at
   once at t = 32 (materialize), then 13 steps inside the projection kernel
   (a file compiled with --fmad=false) when camera A is rendered at t = 45,
   and the rows outside camera A's view by the read's materialize.
