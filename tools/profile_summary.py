@@ -128,6 +128,10 @@ def main():
         traffic = json.load(open(tp))
     kp = os.path.join(prof, "kernel_metrics.json")
     kmet = json.load(open(kp)) if os.path.exists(kp) else {}
+    if per_step:  # kernels the current build no longer launches drop out of both files
+        traffic = {st: {k: v for k, v in ks.items() if k in per_step} for st, ks in traffic.items()}
+        traffic = {st: ks for st, ks in traffic.items() if ks}
+        kmet = {k: v for k, v in kmet.items() if k in per_step}
     lines = [f"# ncu --set full captures `{tag}` (one launch each, inside `bench.py --profile`)", "",
              "| kernel | " + " | ".join(k for k, _, _ in METRICS) + " | top stalls (warps per issue) |",
              "|---" * (len(METRICS) + 2) + "|"]
