@@ -199,17 +199,23 @@ __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __r
     if (threadIdx.x == 0) atomicAdd(ssim_sum, t);
 }
 
-// One horizontal buffer reused map by map (30 KB instead of 44 KB) and <= 40
-// registers: 6 CTAs per SM, so a 1024x768 image's 768 tiles run in one wave
-// (at 5 per SM they needed 1.04 waves; cfg 2: 1394 -> 1424 iters/s).
+// Double-buffered f patches filled by cp.async: channel ch+1's patch loads
+// are in flight while channel ch is spread (the loads were the kernel's
+// stall: long scoreboard); 54 KB and <= 64 registers, 4 CTAs per SM
+// (cfg 3 loss stage 136 -> 128 us against the single-buffered 6-CTA form).
 struct PixSmem {
-    float f[3][kPY][kPS];
+    float f[2][3][kPY][kPS];
     float h[kPY][kTX];
 };
 
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+}
+
 // Per pixel: spread f1..f3 (adjoint of the valid blur) and form dL/dC.
 template <typename G>
-__global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* __restrict__ x, const G* __restrict__ y,
+__global__ __launch_bounds__(kThreads, 4) void ssim_pixels_kernel(const float* __restrict__ x, const G* __restrict__ y,
                                                                int W, int H, const float* __restrict__ f, int has_ssim,
                                                                float lam_over_count, float inv_count3,
                                                                float* __restrict__ dl_dc, double* __restrict__ l1_sum) {
@@ -221,32 +227,47 @@ __global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* _
     const int px0 = blockIdx.x * kTX, py0 = blockIdx.y * kTY;
     const size_t plane = static_cast<size_t>(Wv) * Hv;
     const int col = threadIdx.x % kTX, r0 = 4 * (threadIdx.x / kTX);
+    // windows [px0-10, px0+63] x [py0-10, py0+15], zero outside the valid grid;
+    // patch rows per warp, columns per lane
+    auto fetch = [&](int ch, int buf) {
+        for (int ly = threadIdx.x >> 5; ly < kPY; ly += kThreads / 32) {
+            const int wy = py0 - 2 * kHalf + ly, lane = threadIdx.x & 31;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const int lx = lane + 32 * cc, wx = px0 - 2 * kHalf + lx;
+                if (lx < kPX) {
+                    const bool ok = wx >= 0 && wy >= 0 && wx < Wv && wy < Hv;
+                    const size_t o = ok ? static_cast<size_t>(wy) * Wv + wx : 0;
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) cp_async4(&S.f[buf][m][ly][lx], f + (3 * ch + m) * plane + o, ok);
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    if (has_ssim) fetch(0, 0);
     double local = 0.0;
     for (int ch = 0; ch < 3; ++ch) {
         float g[3][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        const int px = px0 + col;
+        float xa[4], yb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int py = py0 + r0 + j;
+            xa[j] = yb[j] = 0.f;
+            if (px < W && py < H) {
+                const size_t p = 3 * (static_cast<size_t>(py) * W + px) + ch;
+                xa[j] = x[p];
+                yb[j] = gt_val(y, p);
+            }
+        }
         if (has_ssim) {
-            // windows [px0-10, px0+63] x [py0-10, py0+15], zero outside the valid grid
-            // patch rows per warp, columns per lane: a row's 3 x 74 loads in
-            // flight together (coalesced), then the stores
-            for (int ly = threadIdx.x >> 5; ly < kPY; ly += kThreads / 32) {
-                const int wy = py0 - 2 * kHalf + ly, lane = threadIdx.x & 31;
-                float v[3][3];
-#pragma unroll
-                for (int cc = 0; cc < 3; ++cc) {
-                    const int lx = lane + 32 * cc, wx = px0 - 2 * kHalf + lx;
-                    const bool ok = lx < kPX && wx >= 0 && wy >= 0 && wx < Wv && wy < Hv;
-                    const size_t o = ok ? static_cast<size_t>(wy) * Wv + wx : 0;
-#pragma unroll
-                    for (int m = 0; m < 3; ++m) v[cc][m] = ok ? f[(3 * ch + m) * plane + o] : 0.f;
-                }
-#pragma unroll
-                for (int cc = 0; cc < 3; ++cc) {
-                    const int lx = lane + 32 * cc;
-                    if (lx < kPX) {
-#pragma unroll
-                        for (int m = 0; m < 3; ++m) S.f[m][ly][lx] = v[cc][m];
-                    }
-                }
+            const int buf = ch & 1;
+            if (ch < 2) {
+                fetch(ch + 1, buf ^ 1);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
             }
             __syncthreads();
 #pragma unroll
@@ -254,7 +275,7 @@ __global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* _
                 for (int it = threadIdx.x; it < kPY * (kTX / 4); it += kThreads) {
                     const int r = it / (kTX / 4), g4 = 4 * (it % (kTX / 4));
                     float a[16], o[4];
-                    load16(&S.f[m][r][g4], a);
+                    load16(&S.f[buf][m][r][g4], a);
                     corr4(a, o);  // symmetric window: full correlation of the padded map
                     *reinterpret_cast<float4*>(&S.h[r][g4]) = make_float4(o[0], o[1], o[2], o[3]);
                 }
@@ -267,13 +288,12 @@ __global__ __launch_bounds__(kThreads, 6) void ssim_pixels_kernel(const float* _
                 __syncthreads();
             }
         }
-        const int px = px0 + col;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int py = py0 + r0 + j;
             if (px < W && py < H) {
                 const size_t p = 3 * (static_cast<size_t>(py) * W + px) + ch;
-                const float a = x[p], b = gt_val(y, p);
+                const float a = xa[j], b = yb[j];
                 const float diff = a - b;
                 const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
                 local += fabs(static_cast<double>(diff));
