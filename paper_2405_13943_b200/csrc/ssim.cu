@@ -13,6 +13,8 @@
 // Each thread produces 4 adjacent outputs per pass so a row of inputs is read
 // with 128-bit shared loads and reused across 4 outputs (register blocking).
 // Loss partials are reduced to FP64.
+#include <type_traits>
+
 #include "bsg_internal.cuh"
 
 namespace bsg {
@@ -84,11 +86,19 @@ __device__ __forceinline__ float gt_val(const uint8_t* __restrict__ y, size_t p)
 }
 
 struct WinSmem {
-    float x[kPY][kPS], y[kPY][kPS];
+    float x[2][kPY][kPS], y[2][kPY][kPS];
     float h[5][kPY][kTX];
 };
 
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+}
+
 // x, y: HxWx3 FP32 (y: FP32 or 8-bit). f: [3 channels][3 maps][Hv][Wv].
+// Double-buffered patches: channel ch+1's loads are in flight (cp.async; for
+// 8-bit ground truth the y patch is converted through registers) while
+// channel ch is blurred.
 template <typename G>
 __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __restrict__ x,
                                                                 const G* __restrict__ y, int W, int H,
@@ -101,41 +111,45 @@ __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __r
     const int wx0 = blockIdx.x * kTX, wy0 = blockIdx.y * kTY;
     const float C1 = 1e-4f, C2 = 9e-4f;
     const size_t plane = static_cast<size_t>(Wv) * Hv;
-    double local = 0.0;
-    for (int ch = 0; ch < 3; ++ch) {
-        // window (wx, wy) covers pixels [wx, wx+10] x [wy, wy+10]
-        // patch rows per warp, columns per lane: a row's 74 loads in flight
-        // together, consecutive lanes on consecutive pixels
+    // window (wx, wy) covers pixels [wx, wx+10] x [wy, wy+10]; patch rows per
+    // warp, columns per lane, consecutive lanes on consecutive pixels
+    auto fetch = [&](int ch, int buf) {
         for (int ly = threadIdx.x >> 5; ly < kPY; ly += kThreads / 32) {
             const int gy = wy0 + ly, lane = threadIdx.x & 31;
-            float a[3], b[3];
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {
                 const int lx = lane + 32 * cc, gx = wx0 + lx;
-                a[cc] = 0.f;
-                b[cc] = 0.f;
-                if (lx < kPX && gx < W && gy < H) {
-                    const size_t p = 3 * (static_cast<size_t>(gy) * W + gx) + ch;
-                    a[cc] = x[p];
-                    b[cc] = gt_val(y, p);
-                }
-            }
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                const int lx = lane + 32 * cc;
                 if (lx < kPX) {
-                    S.x[ly][lx] = a[cc];
-                    S.y[ly][lx] = b[cc];
+                    const bool ok = gx < W && gy < H;
+                    const size_t p = ok ? 3 * (static_cast<size_t>(gy) * W + gx) + ch : 0;
+                    cp_async4(&S.x[buf][ly][lx], x + p, ok);
+                    if constexpr (std::is_same<G, float>::value) {
+                        cp_async4(&S.y[buf][ly][lx], y + p, ok);
+                    } else {
+                        S.y[buf][ly][lx] = ok ? gt_val(y, p) : 0.f;
+                    }
                 }
             }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    fetch(0, 0);
+    double local = 0.0;
+    for (int ch = 0; ch < 3; ++ch) {
+        const int buf = ch & 1;
+        if (ch < 2) {
+            fetch(ch + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();
         // horizontal: 26 rows x 16 groups of 4 outputs, five moments
         for (int it = threadIdx.x; it < kPY * (kTX / 4); it += kThreads) {
             const int r = it / (kTX / 4), g4 = 4 * (it % (kTX / 4));
             float a[16], b[16], t[16], o[4];
-            load16(&S.x[r][g4], a);
-            load16(&S.y[r][g4], b);
+            load16(&S.x[buf][r][g4], a);
+            load16(&S.y[buf][r][g4], b);
             corr4(a, o);
             *reinterpret_cast<float4*>(&S.h[0][r][g4]) = make_float4(o[0], o[1], o[2], o[3]);
             corr4(b, o);
@@ -193,7 +207,8 @@ __global__ __launch_bounds__(kThreads) void ssim_windows_kernel(const float* __r
                 }
             }
         }
-        __syncthreads();
+        // (no barrier: the next channel's barrier after its fetch orders the
+        // S.h reads above before its horizontal pass overwrites them)
     }
     const double t = block_sum_d(local, s_red);
     if (threadIdx.x == 0) atomicAdd(ssim_sum, t);
@@ -207,11 +222,6 @@ struct PixSmem {
     float f[2][3][kPY][kPS];
     float h[kPY][kTX];
 };
-
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
-}
 
 // Per pixel: spread f1..f3 (adjoint of the valid blur) and form dL/dC.
 template <typename G>
