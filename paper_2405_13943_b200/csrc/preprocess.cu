@@ -39,13 +39,17 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
-constexpr int kPreThreads = 256;
+// 128-thread CTAs, 6 per SM: a CTA's barriers (between the cull, the replays
+// and the projection) stall 4 warps instead of 8 (cfg 3: 256 x 3 rows per
+// thread-batch 214 us, 128: 208 us, 64 x 12 CTAs: 208 us).
+constexpr int kPreThreads = 128;
 constexpr int kPreRowsPerThread = 4;
-// Phase 1 in batches of kPreRowsPerThread rows per thread, 3072 rows per CTA:
+// Phase 1 in batches of kPreRowsPerThread rows per thread, 1536 rows per CTA:
 // larger chunks give phase 2 (replays, exact projection) more candidates per
-// CTA to spread over its warps (measured at cfg 3: 1024 / 2048 / 4096 / 6144
-// rows per CTA -> 248 / 240 / 229 / 246 us; later 3072 / 4096 / 5120 -> 214 /
-// 220 / 224 us).
+// CTA to spread over its warps (measured at cfg 3 with 256 threads: 1024 /
+// 2048 / 4096 / 6144 rows per CTA -> 248 / 240 / 229 / 246 us; later 3072 /
+// 4096 / 5120 -> 214 / 220 / 224 us; with 128 threads 1024 / 1536 / 2048 ->
+// 218 / 208 / 215 us).
 constexpr int kPreSubBatches = 3;
 constexpr int kPreChunk = kPreThreads * kPreRowsPerThread * kPreSubBatches;
 
@@ -58,7 +62,7 @@ constexpr int kPreChunk = kPreThreads * kPreRowsPerThread * kPreSubBatches;
 // the queue with every lane busy (rows are in id order, i.e. spatially random,
 // so doing this per thread would leave most lanes of a warp idle). The
 // visible set and every rect are exactly those of the exact path.
-__global__ __launch_bounds__(kPreThreads, 3) void preprocess_kernel(float* __restrict__ x, float* __restrict__ m,
+__global__ __launch_bounds__(kPreThreads, 6) void preprocess_kernel(float* __restrict__ x, float* __restrict__ m,
                                                                  float* __restrict__ v, LazyAdam la, uint32_t n,
                                                                  int fd, DevCam cam, DevRender rc,
                                                                  float4* __restrict__ rec,
