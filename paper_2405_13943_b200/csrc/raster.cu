@@ -230,6 +230,70 @@ __global__ __launch_bounds__(256) void emit_tiles_kernel(const uint32_t* __restr
 constexpr int kTieRounds = 32;  // odd-even rounds before the full-key re-sort (runs can be ~2048 long)
 constexpr uint32_t kTileSortThreads = 128;
 
+// Bitonic sort of a tile's N <= EPT x kTileSortThreads packed keys in
+// registers, EPT consecutive positions per thread: a stage's partner is in the
+// same thread (distance < EPT), a lane of the same warp (distance < 32 EPT:
+// shuffles) or another warp (through shared memory). The sorted keys end in sk.
+// (cfg 3 sort stage: shared-memory network 58.7 us, registers up to 256 pairs
+// 51.0, up to 1024 pairs 49.5.)
+template <int EPT>
+__device__ __forceinline__ void tile_sort_regs(uint64_t* __restrict__ sk, const uint32_t* __restrict__ rows,
+                                               uint32_t n, uint32_t N, const uint64_t* __restrict__ depth_key) {
+    const uint32_t p0 = EPT * threadIdx.x;
+    uint64_t v[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        v[e] = ~0ull;  // padding sorts last
+        if (p0 + e < n) {
+            const uint32_t row = rows[p0 + e];
+            v[e] = (depth_key[row] & 0xffffffff00000000ull) | row;
+        }
+    }
+    for (uint32_t k = 2; k <= N; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j < EPT) {
+#pragma unroll
+                for (int jj = EPT / 2; jj >= 1; jj >>= 1)
+                    if (jj == static_cast<int>(j)) {
+#pragma unroll
+                        for (int e = 0; e < EPT; ++e)
+                            if ((e & jj) == 0) {
+                                const bool up = ((p0 + e) & k) == 0;
+                                if ((v[e] > v[e | jj]) == up) {
+                                    const uint64_t tmp = v[e];
+                                    v[e] = v[e | jj];
+                                    v[e | jj] = tmp;
+                                }
+                            }
+                    }
+                continue;
+            }
+            // j >= EPT: all of the thread's positions share bits j and k
+            const bool keep_min = ((p0 & j) == 0) == ((p0 & k) == 0);
+            uint64_t o[EPT];
+            if (j < 32u * EPT) {
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) o[e] = __shfl_xor_sync(0xffffffffu, v[e], j / EPT);
+            } else {
+                if (p0 < N) {
+#pragma unroll
+                    for (int e = 0; e < EPT; ++e) sk[p0 + e] = v[e];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) o[e] = p0 < N ? sk[(p0 + e) ^ j] : v[e];
+                __syncthreads();
+            }
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) v[e] = keep_min ? (o[e] < v[e] ? o[e] : v[e]) : (o[e] > v[e] ? o[e] : v[e]);
+        }
+    }
+    if (p0 < N) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) sk[p0 + e] = v[e];
+    }
+}
+
 // One CTA per tile: the tile's rows sorted by (FP64 depth bits, row) with a
 // bitonic network in shared memory (size: the next power of two of the
 // tile's count, at most kTileSortCap; dynamic shared memory sized for the
@@ -257,60 +321,11 @@ __global__ __launch_bounds__(kTileSortThreads) void tile_sort_kernel(const uint2
     // bits tie are put in (full depth, row) order afterwards
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
     if (N <= 2 * kTileSortThreads) {
-        // up to 256 pairs (the common case): two keys per thread in registers
-        // (positions 2t, 2t + 1); a stage's partner is in the same thread
-        // (distance 1), a lane of the same warp (distance 2..32: shuffles) or
-        // another warp (distance >= 64: through shared memory). cfg 3 sort
-        // stage 58.7 -> 51.3 us against the shared-memory network.
-        const uint32_t t = threadIdx.x, p0 = 2 * t, p1 = p0 + 1;
-        uint64_t e0 = ~0ull, e1 = ~0ull;  // padding sorts last
-        if (p0 < n) {
-            const uint32_t row = rows_in[r.x + p0];
-            e0 = (depth_key[row] & 0xffffffff00000000ull) | row;
-        }
-        if (p1 < n) {
-            const uint32_t row = rows_in[r.x + p1];
-            e1 = (depth_key[row] & 0xffffffff00000000ull) | row;
-        }
-        for (uint32_t k = 2; k <= N; k <<= 1) {
-            const bool up = (p0 & k) == 0;  // (p0, p1 and their partners share bit k)
-            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-                if (j == 1) {
-                    if ((e0 > e1) == up) {
-                        const uint64_t tmp = e0;
-                        e0 = e1;
-                        e1 = tmp;
-                    }
-                    continue;
-                }
-                uint64_t o0, o1;
-                if (j <= 32) {
-                    o0 = __shfl_xor_sync(0xffffffffu, e0, j >> 1);
-                    o1 = __shfl_xor_sync(0xffffffffu, e1, j >> 1);
-                } else {
-                    if (p0 < N) {
-                        sk[p0] = e0;
-                        sk[p1] = e1;
-                    }
-                    __syncthreads();
-                    if (p0 < N) {
-                        o0 = sk[p0 ^ j];
-                        o1 = sk[p1 ^ j];
-                    } else {
-                        o0 = e0;
-                        o1 = e1;
-                    }
-                    __syncthreads();
-                }
-                const bool keep_min = ((p0 & j) == 0) == up;
-                e0 = keep_min ? (o0 < e0 ? o0 : e0) : (o0 > e0 ? o0 : e0);
-                e1 = keep_min ? (o1 < e1 ? o1 : e1) : (o1 > e1 ? o1 : e1);
-            }
-        }
-        if (p0 < N) {
-            sk[p0] = e0;
-            sk[p1] = e1;
-        }
+        tile_sort_regs<2>(sk, rows_in + r.x, n, N, depth_key);
+    } else if (N <= 4 * kTileSortThreads) {
+        tile_sort_regs<4>(sk, rows_in + r.x, n, N, depth_key);
+    } else if (N <= 8 * kTileSortThreads) {
+        tile_sort_regs<8>(sk, rows_in + r.x, n, N, depth_key);
     } else {
     for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
         if (i < n) {
